@@ -1,0 +1,15 @@
+"""B200-native Big-means hot path (arXiv 2204.07485).
+
+Drop-in for the reference's `bigmeans::big_means` path: hand-written sm_100a
+CUDA kernels behind a C-ABI (include/bigmeans_b200.h), driven from C++ host
+code that owns the reference's RNG stream.  This Python package mirrors the
+reference C++ API (see api.py) for tests, benchmarks and multi-GPU plumbing.
+"""
+from .api import (  # noqa: F401
+    K_DEFAULT_SEED, K_REDUCTION_BLOCK, BigMeansConfig, BigMeansTrace, Centroids, ChunkRecord,
+    ClusteringOutcome, ConfigError, Dataset, DeviceError, EvalCounter, InitConfig, Rng,
+    SearchConfig, StateError, assign_nearest, assign_rows, big_means, block_sum, device_count,
+    kmeans, kmeanspp_fill, last_profile, lloyd, objective, sample_chunk, set_profiling,
+    update_centroids)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,1167 @@
+// engine.cu — host side of the B200-native Big-means hot path and its C-ABI.
+//
+// One host thread drives one chain on one device stream.  The host owns the
+// reference RNG stream (std::mt19937_64 + the libstdc++ distributions, exactly
+// the reference's Rng, common.hpp:13) and the few sequential decisions that
+// depend on it (K-means++ CDF picks, init.cpp:171-198).  Everything else —
+// Fisher-Yates resolution and sort of the sample, gather, assignment, update,
+// Lloyd control, accept, final pass — runs on the device.
+//
+// Citations are relative to /root/reference/proj.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <random>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "bigmeans_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+struct bm_rng {
+    std::mt19937_64 eng;  // Rng (common.hpp:13)
+};
+
+namespace bm {
+
+thread_local std::string g_last_error;
+thread_local bm_profile g_profile{};
+thread_local bool g_profiling = false;
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------------------
+// Device memory helpers
+// ---------------------------------------------------------------------------
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) BM_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+template <class T>
+struct HostBuf {  // pinned
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) BM_CUDA(cudaMallocHost(&p, count * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~HostBuf() { release(); }
+};
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        BM_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) BM_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Points view: rows x n, row stride ld elements, storage type dtype.
+struct Points {
+    const void* X;
+    bm_dtype dtype;
+    uint64_t rows;
+    int n;
+    uint64_t ld;
+};
+
+template <class F>
+void dispatch(bm_dtype t, F&& f) {
+    if (t == BM_F64) f(double{});
+    else f(float{});
+}
+
+size_t dtype_size(bm_dtype t) { return t == BM_F64 ? 8 : 4; }
+
+// Row stride: rows padded to 16-byte multiples for vector gathers.
+uint64_t padded_ld(uint64_t n, bm_dtype t) {
+    const uint64_t per16 = 16 / dtype_size(t);
+    return ceil_div(n, per16) * per16;
+}
+
+// ---------------------------------------------------------------------------
+// Workspace: every device buffer one chain needs, sized for (rows, k, n).
+// ---------------------------------------------------------------------------
+struct Workspace {
+    uint64_t R = 0;  // max rows processed (chunk size s, or m)
+    int k = 0, n = 0, ncand = 0;
+    uint64_t hist_cap = 0;
+    uint64_t tiles = 0;
+
+    DevBuf<int32_t> labels;  // 2 * R (ping-pong)
+    DevBuf<double> dists;    // R
+    DevBuf<double> tile_buf; // max(ncand,1) * tiles
+    DevBuf<double> psum;     // tiles * k * n
+    DevBuf<uint32_t> pcnt;   // tiles * k
+    DevBuf<double> C, Cact;  // k * n
+    DevBuf<uint8_t> mask;    // k
+    DevBuf<int> act;         // k
+    DevBuf<dev::LloydStatus> status;
+    DevBuf<double> history;
+    // K-means++ (init.cpp:123-201)
+    DevBuf<double> d2pool;   // (ncand + 1) * R
+    DevBuf<uint32_t> cand;   // ncand
+    // incumbent (big_means.cpp:63-64, 89-93)
+    DevBuf<double> Cinc, fopt;
+    DevBuf<uint8_t> maskinc;
+    // pinned host mirrors
+    HostBuf<dev::LloydStatus> h_status;
+    HostBuf<double> h_tiles;
+    HostBuf<double> h_d2;
+    HostBuf<uint8_t> h_mask;
+    HostBuf<uint32_t> h_cand;
+
+    void init(uint64_t rows, int k_, int n_, int ncand_, uint64_t hist) {
+        R = rows;
+        k = k_;
+        n = n_;
+        ncand = std::max(ncand_, 1);
+        tiles = tiles_of(rows);
+        hist_cap = hist;
+        labels.alloc(2 * R);
+        dists.alloc(R);
+        tile_buf.alloc(tiles * ncand);
+        psum.alloc(tiles * (uint64_t)k * n);
+        pcnt.alloc(tiles * (uint64_t)k);
+        C.alloc((uint64_t)k * n);
+        Cact.alloc((uint64_t)k * n);
+        mask.alloc(k);
+        act.alloc(k);
+        status.alloc(1);
+        BM_CUDA(cudaMemset(status.p, 0, sizeof(dev::LloydStatus)));
+        history.alloc(hist_cap);
+        d2pool.alloc((uint64_t)(ncand + 1) * R);
+        cand.alloc(ncand);
+        Cinc.alloc((uint64_t)k * n);
+        fopt.alloc(1);
+        maskinc.alloc(k);
+        h_status.alloc(1);
+        h_tiles.alloc(tiles * ncand);
+        h_d2.alloc(R);
+        h_mask.alloc(k);
+        h_cand.alloc(ncand);
+    }
+};
+
+// Sampler workspace (sample_chunk big_means.cpp:39-56) for one dataset size m.
+struct SamplerWs {
+    uint64_t m = 0, s = 0;
+    uint32_t hmask = 0;
+    uint32_t nwords = 0, nblocks = 0;
+    DevBuf<uint32_t> js, hkeys, bitmap, blockcnt, idx;
+    DevBuf<int> LT, hvals;
+    DevBuf<uint8_t> kept;
+    HostBuf<uint32_t> h_js[2];
+    cudaEvent_t js_done[2] = {nullptr, nullptr};
+    int cur = 0;
+
+    void init(uint64_t m_, uint64_t s_) {
+        m = m_;
+        s = s_;
+        uint32_t h = 1;
+        while (h < 2 * s) h <<= 1;
+        hmask = h - 1;
+        nwords = (uint32_t)ceil_div(m, 32);
+        nblocks = (uint32_t)ceil_div(nwords, dev::kWordsPerBlock);
+        js.alloc(s);
+        hkeys.alloc(h);
+        hvals.alloc(h);
+        bitmap.alloc(nwords);
+        blockcnt.alloc(std::max<uint32_t>(nblocks, 1));
+        idx.alloc(s);
+        LT.alloc(s);
+        kept.alloc(s);
+        for (int b = 0; b < 2; ++b) {
+            h_js[b].alloc(s);
+            if (!js_done[b]) BM_CUDA(cudaEventCreateWithFlags(&js_done[b], cudaEventDisableTiming));
+        }
+    }
+    ~SamplerWs() {
+        for (auto& e : js_done)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace bm
+
+// Device-resident immutable dataset (Dataset core.hpp:13-37).
+struct bm_dataset {
+    int device = 0;
+    uint64_t m = 0, n = 0, ld = 0;
+    bm_dtype dtype = BM_F64;
+    void* X = nullptr;
+    cudaStream_t stream = nullptr;
+    std::map<std::tuple<uint64_t, int, int, uint64_t>, std::unique_ptr<bm::Workspace>> ws;
+    std::map<uint64_t, std::unique_ptr<bm::SamplerWs>> sws;
+    bm::DevBuf<uint8_t> chunk;  // gathered chunk, s * ld * elem
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ~bm_dataset() {
+        ws.clear();
+        sws.clear();
+        chunk.release();
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (X) cudaFree(X);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace bm {
+namespace {
+
+Points dataset_points(const bm_dataset* d) { return Points{d->X, d->dtype, d->m, (int)d->n, d->ld}; }
+
+Workspace& get_ws(bm_dataset* d, uint64_t rows, int k, int ncand, uint64_t hist) {
+    auto key = std::make_tuple(rows, k, std::max(ncand, 1), hist);
+    auto it = d->ws.find(key);
+    if (it != d->ws.end()) return *it->second;
+    auto w = std::make_unique<Workspace>();
+    w->init(rows, k, (int)d->n, ncand, hist);
+    auto& ref = *w;
+    d->ws.emplace(key, std::move(w));
+    return ref;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel launch wrappers
+// ---------------------------------------------------------------------------
+struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    std::vector<uint64_t> rows;
+    std::vector<int> final_flag;
+    cudaStream_t stream = nullptr;
+    void begin(cudaStream_t s) { stream = s; }
+    std::pair<cudaEvent_t, cudaEvent_t> record_start() {
+        cudaEvent_t a, b;
+        BM_CUDA(cudaEventCreate(&a));
+        BM_CUDA(cudaEventCreate(&b));
+        BM_CUDA(cudaEventRecord(a, stream));
+        return {a, b};
+    }
+    void record_end(std::pair<cudaEvent_t, cudaEvent_t> p, uint64_t r, bool fin) {
+        BM_CUDA(cudaEventRecord(p.second, stream));
+        evs.push_back(p);
+        rows.push_back(r);
+        final_flag.push_back(fin);
+    }
+    void flush(bm_profile& out) {
+        for (size_t i = 0; i < evs.size(); ++i) {
+            float ms = 0;
+            BM_CUDA(cudaEventSynchronize(evs[i].second));
+            BM_CUDA(cudaEventElapsedTime(&ms, evs[i].first, evs[i].second));
+            if (final_flag[i]) {
+                out.final_ms += ms;
+                out.final_rows += rows[i];
+            } else {
+                out.assign_ms_total += ms;
+                out.assign_launches += 1;
+                out.assign_rows_total += rows[i];
+            }
+            cudaEventDestroy(evs[i].first);
+            cudaEventDestroy(evs[i].second);
+        }
+        evs.clear();
+        rows.clear();
+        final_flag.clear();
+    }
+};
+thread_local Profiler g_prof;
+
+void count_launch(uint64_t n = 1) { g_profile.kernel_launches += n; }
+
+int assign_threads(int k) {
+    const int kg = std::min<int>(dev::kAMaxCG, (int)ceil_div(std::max(k, 1), dev::kAK));
+    return dev::kAPG * kg;
+}
+
+// assign_nearest over P with the compacted centroids of ws (Cact/act/n_active).
+void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_t* labels_pair,
+                   uint64_t pair_stride, const int* parity, double* dists, int* changed,
+                   const int* stop, bool final_pass = false) {
+    const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
+    if (grid == 0) return;
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (g_profiling) ev = g_prof.record_start();
+    dispatch(P.dtype, [&](auto tag) {
+        using T = decltype(tag);
+        dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
+            static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
+            labels_pair, pair_stride, parity, dists, changed, stop);
+    });
+    BM_LAUNCH();
+    count_launch();
+    if (g_profiling) g_prof.record_end(ev, P.rows, final_pass);
+}
+
+void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t stride, int narrays,
+                      double* tiles, const int* stop) {
+    const uint64_t warps = tiles_of(count) * narrays;
+    const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
+    if (grid == 0) return;
+    dev::k_tile_sums<<<grid, 256, 0, st>>>(v, count, stride, narrays, tiles, stop);
+    BM_LAUNCH();
+    count_launch();
+}
+
+void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_t* mask) {
+    dev::k_compact<<<1, 256, w.k * sizeof(int), st>>>(C, mask, w.k, w.n, w.Cact.p, w.act.p,
+                                                       &w.status.p->n_active);
+    BM_LAUNCH();
+    count_launch();
+}
+
+void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* parity, const int* stop) {
+    const int k = w.k, n = w.n;
+    const uint64_t tiles = tiles_of(P.rows);
+    // d-slab so that the grid covers the GPU even when there are few tiles.
+    int slabs = 1;
+    while (tiles * slabs < 296 && n / (slabs * 2) >= 16) slabs *= 2;
+    const int dslab = (int)ceil_div(n, slabs);
+    dim3 grid((unsigned)tiles, (unsigned)ceil_div(n, dslab));
+    const size_t shm = (2 * kTile + 3 * k) * sizeof(int);
+    dispatch(P.dtype, [&](auto tag) {
+        using T = decltype(tag);
+        dev::k_update_partials<T><<<grid, dev::kUThreads, shm, st>>>(
+            static_cast<const T*>(P.X), P.rows, n, P.ld, w.labels.p, w.R, parity, k, dslab, w.psum.p,
+            w.pcnt.p, &w.status.p->bad_label, stop);
+    });
+    BM_LAUNCH();
+    const uint64_t pairs = (uint64_t)k * n;
+    const unsigned mgrid = (unsigned)std::min<uint64_t>(ceil_div(pairs, dev::kUThreads), 1024);
+    const size_t mshm = k * (sizeof(unsigned long long) + sizeof(int));
+    dev::k_update_merge<<<mgrid, dev::kUThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p,
+                                                            w.mask.p, w.Cact.p, w.act.p,
+                                                            &w.status.p->n_active, stop);
+    BM_LAUNCH();
+    count_launch(2);
+}
+
+// ---------------------------------------------------------------------------
+// lloyd (local_search.cpp:16-60) with the loop state on the device.
+// Start centroids in w.C / w.mask.  Kernels of a finished loop early-exit, so
+// the host launches rounds in batches and checks the status once per batch.
+// ---------------------------------------------------------------------------
+struct LloydResult {
+    double objective;
+    uint64_t evals;
+    uint64_t iterations;
+    int parity;
+};
+
+void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w) {
+    launch_compact(st, w, w.C.p, w.mask.p);
+    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr);  // :26
+    launch_tile_sums(st, w.dists.p, P.rows, 0, 1, w.tile_buf.p, nullptr);              // :27
+    dev::k_lloyd_begin<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows,
+                                         w.hist_cap ? w.history.p : nullptr);
+    BM_LAUNCH();
+    count_launch();
+}
+
+void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol) {
+    const int* parity = &w.status.p->parity;
+    const int* stop = &w.status.p->stop;
+    launch_update(st, P, w, parity, stop);                                                 // :33
+    launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop);  // :34
+    launch_tile_sums(st, w.dists.p, P.rows, 0, 1, w.tile_buf.p, stop);                    // :35
+    dev::k_lloyd_step<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows, max_it,
+                                        tol, w.hist_cap ? w.history.p : nullptr);
+    BM_LAUNCH();
+    count_launch();
+}
+
+// Runs the loop to completion; `between` is called once after the first
+// batch is enqueued (used to overlap host RNG work with device work).
+template <class Between>
+LloydResult lloyd_run(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol,
+                      Between&& between) {
+    lloyd_enqueue_begin(st, P, w);
+    uint64_t launched = 0;
+    int batch = 2;
+    bool first = true;
+    while (true) {
+        const uint64_t todo = std::min<uint64_t>(batch, max_it - launched);
+        for (uint64_t i = 0; i < todo; ++i) lloyd_enqueue_round(st, P, w, max_it, tol);
+        launched += todo;
+        BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus),
+                                cudaMemcpyDeviceToHost, st));
+        if (first) {
+            between();
+            first = false;
+        }
+        BM_CUDA(cudaStreamSynchronize(st));
+        const dev::LloydStatus& s = *w.h_status.p;
+        if (s.state_error) throw StateError("assign_nearest: every centroid is degenerate");
+        if (s.stop || launched >= max_it) break;
+        batch = std::min(batch * 2, 8);
+    }
+    const dev::LloydStatus& s = *w.h_status.p;
+    if (s.bad_label) throw ConfigError("update_centroids: label out of range");
+    return LloydResult{s.objective, s.evals, s.iterations, s.parity};
+}
+
+LloydResult lloyd_run(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol) {
+    return lloyd_run(st, P, w, max_it, tol, [] {});
+}
+
+// ---------------------------------------------------------------------------
+// kmeanspp_fill (init.cpp:123-201).  Centroids in w.C / w.mask (device) with
+// the host mask mirror `mask`.  D^2 arrays live on the device; the sequential
+// prefix sum, the draws and upper_bound run on the host (the reference RNG).
+// ---------------------------------------------------------------------------
+template <class T>
+void set_row(cudaStream_t st, const Points& P, Workspace& w, uint64_t row, int j) {
+    dev::k_set_row<T><<<1, 256, 0, st>>>(static_cast<const T*>(P.X), P.ld, P.n, row, w.C.p, w.mask.p, j);
+    BM_LAUNCH();
+    count_launch();
+}
+
+void set_row_any(cudaStream_t st, const Points& P, Workspace& w, uint64_t row, int j) {
+    dispatch(P.dtype, [&](auto tag) { set_row<decltype(tag)>(st, P, w, row, j); });
+}
+
+void launch_dist_rows(cudaStream_t st, const Points& P, const uint32_t* cand, int ncand, const double* d2,
+                      double* out) {
+    const unsigned grid = (unsigned)ceil_div(P.rows, 128);
+    dispatch(P.dtype, [&](auto tag) {
+        using T = decltype(tag);
+        dev::k_dist_rows<T><<<grid, 128, 0, st>>>(static_cast<const T*>(P.X), P.rows, P.n, P.ld, cand,
+                                                  ncand, d2, out);
+    });
+    BM_LAUNCH();
+    count_launch();
+}
+
+// pick_by_mass (init.cpp:73-79): upper_bound clamped to the last index.
+uint64_t pick_by_mass(const std::vector<double>& cum, double u) {
+    auto it = std::upper_bound(cum.begin(), cum.end(), u);
+    if (it == cum.end()) --it;
+    return (uint64_t)(it - cum.begin());
+}
+
+void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::vector<uint8_t>& mask,
+                          int candidates, std::mt19937_64& rng, uint64_t& evals) {
+    if (candidates < 1) throw ConfigError("kmeanspp_fill: candidates_per_step must be at least 1");
+    const uint64_t m = P.rows;
+    std::vector<int> degenerate;
+    int active = 0;
+    for (int j = 0; j < w.k; ++j) {
+        if (mask[j]) degenerate.push_back(j);
+        else ++active;
+    }
+    if (degenerate.empty()) return;
+    if ((int)w.ncand < candidates) throw ConfigError("kmeanspp_fill: workspace candidate capacity");
+    // D^2 pool: trial arrays in slots [0, candidates), D^2 in slot `candidates`.
+    auto buf = [&](int i) { return w.d2pool.p + (uint64_t)i * w.R; };
+    const int d2i = candidates;
+    size_t first_slot = 0;
+    if (active == 0) {  // :144-150
+        std::uniform_int_distribution<std::size_t> pick(0, m - 1);
+        const uint64_t first = pick(rng);
+        const int slot = degenerate.front();
+        set_row_any(st, P, w, first, slot);
+        mask[slot] = 0;
+        first_slot = 1;
+        w.h_cand.p[0] = (uint32_t)first;
+        BM_CUDA(cudaMemcpyAsync(w.cand.p, w.h_cand.p, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        launch_dist_rows(st, P, w.cand.p, 1, nullptr, buf(d2i));  // distances_to_row :149
+        evals += m;
+    } else {  // :151-164 — min over active rows == assignment distance
+        launch_compact(st, w, w.C.p, w.mask.p);
+        launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, buf(d2i), nullptr, nullptr);
+        evals += m * (uint64_t)active;
+    }
+    std::vector<double> cum(m);
+    std::vector<double> pot(candidates);
+    std::vector<uint64_t> picks(candidates);
+    const uint64_t ntiles = tiles_of(m);
+    for (size_t q = first_slot; q < degenerate.size(); ++q) {  // :171-199
+        const int slot = degenerate[q];
+        BM_CUDA(cudaMemcpyAsync(w.h_d2.p, buf(d2i), m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        double running = 0.0;  // prefix_sums :81-88 (sequential)
+        for (uint64_t i = 0; i < m; ++i) {
+            running += w.h_d2.p[i];
+            cum[i] = running;
+        }
+        const double total = cum.back();
+        if (total <= 0.0) {  // :174-180
+            std::uniform_int_distribution<std::size_t> pick(0, m - 1);
+            set_row_any(st, P, w, pick(rng), slot);
+            mask[slot] = 0;
+            continue;
+        }
+        for (int c = 0; c < candidates; ++c) {  // :183-185
+            std::uniform_real_distribution<double> draw(0.0, total);
+            picks[c] = pick_by_mass(cum, draw(rng));
+            w.h_cand.p[c] = (uint32_t)picks[c];
+        }
+        BM_CUDA(cudaMemcpyAsync(w.cand.p, w.h_cand.p, candidates * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, st));
+        const int base = 0;
+        launch_dist_rows(st, P, w.cand.p, candidates, buf(d2i), buf(base));  // :186-189
+        evals += m * (uint64_t)candidates;
+        launch_tile_sums(st, buf(base), m, w.R, candidates, w.tile_buf.p, nullptr);  // :190
+        BM_CUDA(cudaMemcpyAsync(w.h_tiles.p, w.tile_buf.p, candidates * ntiles * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        double best_potential = std::numeric_limits<double>::infinity();
+        int best = -1;
+        uint64_t best_index = 0;
+        for (int c = 0; c < candidates; ++c) {
+            double potential = 0.0;  // block_sum outer fold
+            for (uint64_t t = 0; t < ntiles; ++t) potential += w.h_tiles.p[c * ntiles + t];
+            if (potential < best_potential) {  // :191-195
+                best_potential = potential;
+                best_index = picks[c];
+                best = c;
+            }
+        }
+        set_row_any(st, P, w, best_index, slot);  // :197
+        mask[slot] = 0;
+        if (best >= 0)  // dist2 := best_trial (:198)
+            BM_CUDA(cudaMemcpyAsync(buf(d2i), buf(best), m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Sampling (sample_chunk big_means.cpp:39-56): host draws, device resolution.
+// ---------------------------------------------------------------------------
+SamplerWs& get_sws(bm_dataset* d, uint64_t s) {
+    auto it = d->sws.find(s);
+    if (it != d->sws.end()) return *it->second;
+    auto w = std::make_unique<SamplerWs>();
+    w->init(d->m, s);
+    auto& ref = *w;
+    d->sws.emplace(s, std::move(w));
+    return ref;
+}
+
+// Draw the s raw Fisher-Yates targets j_i = uniform_int(i, m-1) into the
+// next pinned buffer (waits until the buffer's previous upload finished).
+uint32_t* draw_targets(SamplerWs& sw, std::mt19937_64& rng) {
+    const int b = sw.cur;
+    BM_CUDA(cudaEventSynchronize(sw.js_done[b]));
+    uint32_t* out = sw.h_js[b].p;
+    const uint64_t m = sw.m;
+    for (uint64_t i = 0; i < sw.s; ++i) {
+        std::uniform_int_distribution<std::size_t> pick(i, m - 1);  // :50
+        out[i] = (uint32_t)pick(rng);
+    }
+    return out;
+}
+
+// Enqueue resolution of the drawn targets in buffer sw.cur; result in sw.idx.
+void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
+    const int b = sw.cur;
+    const uint32_t s = (uint32_t)sw.s;
+    BM_CUDA(cudaMemcpyAsync(sw.js.p, sw.h_js[b].p, s * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaEventRecord(sw.js_done[b], st));
+    sw.cur ^= 1;
+    BM_CUDA(cudaMemsetAsync(sw.LT.p, 0xFF, s * sizeof(int), st));
+    BM_CUDA(cudaMemsetAsync(sw.hkeys.p, 0xFF, (sw.hmask + 1) * sizeof(uint32_t), st));
+    BM_CUDA(cudaMemsetAsync(sw.hvals.p, 0xFF, (sw.hmask + 1) * sizeof(int), st));
+    BM_CUDA(cudaMemsetAsync(sw.kept.p, 1, s, st));
+    BM_CUDA(cudaMemsetAsync(sw.bitmap.p, 0, sw.nwords * sizeof(uint32_t), st));
+    const unsigned g = (unsigned)ceil_div(s, 256);
+    dev::k_fy_pass1<<<g, 256, 0, st>>>(sw.js.p, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
+    dev::k_fy_pass2<<<g, 256, 0, st>>>(sw.js.p, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.kept.p,
+                                       sw.bitmap.p);
+    dev::k_fy_pass3<<<g, 256, 0, st>>>(sw.kept.p, s, sw.bitmap.p);
+    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.nwords,
+                                                                         sw.blockcnt.p);
+    dev::k_scan_block_counts<<<1, dev::kScanThreads, 0, st>>>(sw.blockcnt.p, sw.nblocks);
+    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.nwords, sw.blockcnt.p,
+                                                                 sw.idx.p);
+    BM_LAUNCH();
+    count_launch(6);
+}
+
+void enqueue_gather(cudaStream_t st, bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
+    const uint64_t row_vecs = d->ld * dtype_size(d->dtype) / 16;
+    const unsigned grid = (unsigned)ceil_div((uint64_t)s * 32, 256);
+    dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X), row_vecs, idx, s,
+                                        static_cast<uint4*>(out));
+    BM_LAUNCH();
+    count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// validate (big_means.cpp:16-35)
+// ---------------------------------------------------------------------------
+void validate(const bm_dataset* d, const bm_config& c) {
+    if (c.k < 1) throw ConfigError("big_means: k must be at least 1");
+    if (c.chunk_size < c.k) throw ConfigError("big_means: chunk_size must be at least k");
+    if (c.chunk_size > d->m) throw ConfigError("big_means: chunk_size exceeds the dataset size");
+    if (!c.has_max_cpu_seconds && !c.has_max_chunks)
+        throw ConfigError("big_means: no stop condition; set max_cpu_seconds or max_chunks");
+    if (c.has_max_cpu_seconds && c.max_cpu_seconds < 0.0)
+        throw ConfigError("big_means: max_cpu_seconds must be nonnegative");
+    if (c.has_max_chunks && c.max_chunks < 1) throw ConfigError("big_means: max_chunks must be at least 1");
+    if (c.max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
+    if (c.rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
+    if (c.candidates_per_step < 1)
+        throw ConfigError("kmeanspp_fill: candidates_per_step must be at least 1");
+}
+
+// ---------------------------------------------------------------------------
+// Final pass: assign all rows [r0, r1) + per-tile partials (big_means.cpp:102-107)
+// ---------------------------------------------------------------------------
+void final_pass(cudaStream_t st, bm_dataset* d, Workspace& w, uint64_t r0, uint64_t r1, int32_t* labels_host,
+                double* tiles_host, uint64_t* evals, DevBuf<int32_t>& dlabels, DevBuf<double>& ddists,
+                DevBuf<double>& dtiles) {
+    Points P = dataset_points(d);
+    P.X = static_cast<const uint8_t*>(d->X) + r0 * d->ld * dtype_size(d->dtype);
+    P.rows = r1 - r0;
+    launch_assign(st, P, w, w.k, dlabels.p, 0, nullptr, ddists.p, nullptr, nullptr, true);
+    launch_tile_sums(st, ddists.p, P.rows, 0, 1, dtiles.p, nullptr);
+    BM_CUDA(cudaMemcpyAsync(tiles_host, dtiles.p, tiles_of(P.rows) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (labels_host)
+        BM_CUDA(cudaMemcpyAsync(labels_host, dlabels.p, P.rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    if (w.h_status.p->n_active == 0) throw StateError("assign_nearest: every centroid is degenerate");
+    if (evals) *evals += P.rows * (uint64_t)w.h_status.p->n_active;
+}
+
+// ---------------------------------------------------------------------------
+// big_means (big_means.cpp:58-112)
+// ---------------------------------------------------------------------------
+void big_means(bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_record* trace,
+               uint64_t trace_cap) {
+    validate(d, cfg);
+    DeviceGuard g(d->device);
+    cudaStream_t st = d->stream;
+    const uint64_t m = d->m, s = cfg.chunk_size;
+    const int k = (int)cfg.k, n = (int)d->n;
+    if (g_profiling) {
+        g_profile = bm_profile{};
+        g_prof.begin(st);
+    }
+    std::mt19937_64 rng(cfg.seed);  // :62
+    Workspace& w = get_ws(d, s, k, cfg.candidates_per_step, 0);
+    const bool identity = s == m;  // sample_chunk(s == m): whole range, no draws (:46-48)
+    SamplerWs* sw = identity ? nullptr : &get_sws(d, s);
+    Points chunkP{nullptr, d->dtype, s, n, d->ld};
+    if (identity) {
+        chunkP = dataset_points(d);
+    } else {
+        const size_t bytes = s * d->ld * dtype_size(d->dtype);
+        if (d->chunk.n < bytes) d->chunk.alloc(bytes);
+        chunkP.X = d->chunk.p;
+    }
+    // incumbent: all degenerate, f_opt = +inf (:63-64)
+    BM_CUDA(cudaMemsetAsync(w.Cinc.p, 0, (size_t)k * n * sizeof(double), st));
+    BM_CUDA(cudaMemsetAsync(w.maskinc.p, 1, k, st));
+    const double inf = std::numeric_limits<double>::infinity();
+    BM_CUDA(cudaMemcpyAsync(w.fopt.p, &inf, sizeof(double), cudaMemcpyHostToDevice, st));
+    const uint64_t cap_chunks = cfg.has_max_chunks ? cfg.max_chunks : 0;
+    DevBuf<dev::Record> drec(std::max<uint64_t>(cap_chunks ? cap_chunks : 1024, 1));
+    std::vector<dev::Record> records;
+    uint64_t evals = 0, iterations = 0;
+    int inc_degenerate = k;
+    std::vector<uint8_t> hmask(k);
+
+    const auto t_loop = std::chrono::steady_clock::now();
+    bool have_next = false;  // targets for the next chunk already drawn
+    for (uint64_t chunk = 0;; ++chunk) {
+        if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
+        if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
+            break;  // :74-77
+        if (!identity) {
+            if (!have_next) draw_targets(*sw, rng);
+            have_next = false;
+            enqueue_resolve(st, *sw);
+            enqueue_gather(st, d, sw->idx.p, (uint32_t)s, d->chunk.p);  // :80
+        }
+        // start = incumbent (:82), repaired = degenerate_count (:83)
+        BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        BM_CUDA(cudaMemcpyAsync(w.mask.p, w.maskinc.p, k, cudaMemcpyDeviceToDevice, st));
+        const uint64_t repaired = (uint64_t)inc_degenerate;
+        if (repaired > 0) {  // kmeanspp_fill (:84) consumes draws before the next sample
+            BM_CUDA(cudaMemcpyAsync(w.h_mask.p, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
+            BM_CUDA(cudaStreamSynchronize(st));
+            std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
+            kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
+        }
+        // Next chunk's draws come after this chunk's repair draws in the
+        // stream (big_means.hpp:21-23), so they can be drawn while Lloyd runs.
+        const bool next_exists = !identity && (!cfg.has_max_chunks || chunk + 1 < cfg.max_chunks);
+        LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance, [&] {
+            if (next_exists) {
+                draw_targets(*sw, rng);
+                have_next = true;
+            }
+        });
+        evals += lr.evals;  // lloyd accumulate (local_search.cpp:55-58)
+        iterations += lr.iterations;
+        if (chunk >= drec.n) {  // time-budget runs: grow the record buffer
+            records.resize(drec.n);
+            BM_CUDA(cudaMemcpyAsync(records.data(), drec.p, drec.n * sizeof(dev::Record), cudaMemcpyDeviceToHost, st));
+            BM_CUDA(cudaStreamSynchronize(st));
+            DevBuf<dev::Record> bigger(drec.n * 2);
+            BM_CUDA(cudaMemcpyAsync(bigger.p, records.data(), records.size() * sizeof(dev::Record),
+                                    cudaMemcpyHostToDevice, st));
+            BM_CUDA(cudaStreamSynchronize(st));
+            std::swap(drec.p, bigger.p);
+            std::swap(drec.n, bigger.n);
+        }
+        dev::k_accept<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p, w.maskinc.p, k, n,
+                                         drec.p + chunk, chunk, repaired, &w.status.p->inc_degenerate);
+        BM_LAUNCH();
+        count_launch();
+        BM_CUDA(cudaMemcpyAsync(&w.h_status.p->inc_degenerate, &w.status.p->inc_degenerate, sizeof(int),
+                                cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        inc_degenerate = w.h_status.p->inc_degenerate;
+        out->chunks = chunk + 1;
+    }
+    const double cpu_init = seconds_since(t_loop);  // :96
+    records.resize(out->chunks);
+    if (out->chunks)
+        BM_CUDA(cudaMemcpyAsync(records.data(), drec.p, out->chunks * sizeof(dev::Record), cudaMemcpyDeviceToHost, st));
+    double fopt = 0.0;
+    BM_CUDA(cudaMemcpyAsync(&fopt, w.fopt.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(out->centroids, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(out->mask, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    out->cpu_init = cpu_init;
+    out->cpu_full = 0.0;
+    if (cfg.final_assignment) {  // :102-107
+        const auto t_full = std::chrono::steady_clock::now();
+        Workspace& fw = get_ws(d, 0, k, 1, 0);  // centroid state only
+        launch_compact(st, fw, w.Cinc.p, w.maskinc.p);
+        DevBuf<int32_t> dl(m);
+        DevBuf<double> dd(m), dt(tiles_of(m));
+        std::vector<double> tiles(tiles_of(m));
+        final_pass(st, d, fw, 0, m, out->labels, tiles.data(), &evals, dl, dd, dt);
+        double total = 0.0;  // block_sum outer fold (core.cpp:172)
+        for (double t : tiles) total += t;
+        out->objective = total;
+        out->cpu_full = seconds_since(t_full);
+    } else {
+        out->objective = fopt;  // :108-110
+    }
+    out->distance_evals = evals;
+    out->iterations = iterations;  // :97
+    for (uint64_t i = 0; i < out->chunks && trace && i < trace_cap; ++i) {
+        trace[i].chunk_index = records[i].chunk_index;
+        trace[i].candidate_objective = records[i].candidate_objective;
+        trace[i].incumbent_objective = records[i].incumbent_objective;
+        trace[i].accepted = records[i].accepted;
+        trace[i].degenerate_repaired = records[i].degenerate_repaired;
+    }
+    if (g_profiling) g_prof.flush(g_profile);
+}
+
+template <class F>
+bm_status guarded(F&& f) {
+    try {
+        f();
+        return BM_OK;
+    } catch (const ConfigError& e) {
+        g_last_error = e.what();
+        return BM_CONFIG_ERROR;
+    } catch (const StateError& e) {
+        g_last_error = e.what();
+        return BM_STATE_ERROR;
+    } catch (const CudaError& e) {
+        g_last_error = e.what();
+        return BM_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BM_INTERNAL_ERROR;
+    }
+}
+
+// Upload host centroids (k*n f64 + mask) into w.C / w.mask and compact.
+void upload_centroids(cudaStream_t st, Workspace& w, const double* C, const uint8_t* mask) {
+    const size_t kn = (size_t)w.k * w.n;
+    std::vector<double> tmp(C, C + kn);
+    for (int j = 0; j < w.k; ++j)  // degenerate rows hold 0.0 (core.cpp:50-53)
+        if (mask[j]) std::fill(tmp.begin() + (size_t)j * w.n, tmp.begin() + (size_t)(j + 1) * w.n, 0.0);
+    BM_CUDA(cudaMemcpyAsync(w.C.p, tmp.data(), kn * sizeof(double), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaMemcpyAsync(w.mask.p, mask, w.k, cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+}  // namespace bm
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace bm;
+
+extern "C" {
+
+const char* bm_last_error(void) { return g_last_error.c_str(); }
+int bm_abi_version(void) { return BM_ABI_VERSION; }
+
+void bm_config_init(bm_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->max_iterations = 300;   // local_search.hpp:11
+    c->rel_tolerance = 1e-4;   // local_search.hpp:14
+    c->candidates_per_step = 3;  // init.hpp:18
+    c->seed = 123456789ULL;    // kDefaultSeed common.hpp:17
+    c->final_assignment = 1;   // big_means.hpp:25
+}
+
+bm_status bm_device_count(int* count) {
+    return guarded([&] {
+        BM_CUDA(cudaGetDeviceCount(count));
+        if (*count < 1) throw CudaError("no CUDA device");
+    });
+}
+
+bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype dtype, int device,
+                            bm_dataset** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (m < 1 || n < 1) throw ConfigError("dataset must have at least one row and one column");
+        if (dtype != BM_F64 && dtype != BM_F32) throw ConfigError("dataset dtype must be f64 or f32");
+        if (m >= 0xFFFFFFFFull) throw ConfigError("dataset too large for 32-bit row indices");
+        DeviceGuard g(device);
+        auto d = std::make_unique<bm_dataset>();
+        d->device = device;
+        d->m = m;
+        d->n = n;
+        d->dtype = dtype;
+        d->ld = padded_ld(n, dtype);
+        const size_t es = dtype_size(dtype);
+        BM_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+        BM_CUDA(cudaMalloc(&d->X, m * d->ld * es));
+        if (d->ld == n) {
+            BM_CUDA(cudaMemcpyAsync(d->X, values, m * n * es, cudaMemcpyHostToDevice, d->stream));
+        } else {
+            BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * es, values, n * es, n * es, m, cudaMemcpyHostToDevice,
+                                      d->stream));
+        }
+        // Dataset ctor finiteness scan (core.cpp:27-31)
+        DevBuf<int> bad(1);
+        BM_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), d->stream));
+        dispatch(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            dev::k_check_finite<T><<<1184, 256, 0, d->stream>>>(static_cast<const T*>(d->X), m, (int)n, d->ld, bad.p);
+        });
+        BM_LAUNCH();
+        int hbad = 0;
+        BM_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaStreamSynchronize(d->stream));
+        if (hbad) throw ConfigError("dataset contains a non-finite value");
+        *out = d.release();
+    });
+}
+
+bm_status bm_dataset_destroy(bm_dataset* d) {
+    return guarded([&] {
+        if (!d) return;
+        DeviceGuard g(d->device);
+        delete d;
+    });
+}
+
+bm_status bm_dataset_shape(const bm_dataset* d, uint64_t* m, uint64_t* n) {
+    return guarded([&] {
+        *m = d->m;
+        *n = d->n;
+    });
+}
+
+bm_status bm_dataset_gather(const bm_dataset* d, const uint64_t* rows, uint64_t count, bm_dataset** out) {
+    return guarded([&] {
+        *out = nullptr;
+        for (uint64_t i = 0; i < count; ++i)
+            if (rows[i] >= d->m) throw ConfigError("gather index out of range");
+        if (count < 1) throw ConfigError("dataset must have at least one row and one column");
+        DeviceGuard g(d->device);
+        auto o = std::make_unique<bm_dataset>();
+        o->device = d->device;
+        o->m = count;
+        o->n = d->n;
+        o->dtype = d->dtype;
+        o->ld = d->ld;
+        BM_CUDA(cudaStreamCreateWithFlags(&o->stream, cudaStreamNonBlocking));
+        BM_CUDA(cudaMalloc(&o->X, count * o->ld * dtype_size(o->dtype)));
+        DevBuf<uint64_t> idx(count);
+        BM_CUDA(cudaMemcpyAsync(idx.p, rows, count * sizeof(uint64_t), cudaMemcpyHostToDevice, o->stream));
+        dispatch(d->dtype, [&](auto tag) {
+            using T = decltype(tag);
+            dev::k_gather_checked<T><<<592, 256, 0, o->stream>>>(static_cast<const T*>(d->X), d->ld, (int)d->n,
+                                                                 idx.p, count, static_cast<T*>(o->X), o->ld);
+        });
+        BM_LAUNCH();
+        BM_CUDA(cudaStreamSynchronize(o->stream));
+        *out = o.release();
+    });
+}
+
+bm_status bm_dataset_download(const bm_dataset* d, double* out) {
+    return guarded([&] {
+        DeviceGuard g(d->device);
+        DevBuf<double> tmp(d->m * d->n);
+        dispatch(d->dtype, [&](auto tag) {
+            using T = decltype(tag);
+            dev::k_promote<T><<<592, 256, 0, d->stream>>>(static_cast<const T*>(d->X), d->m, (int)d->n, d->ld, tmp.p);
+        });
+        BM_LAUNCH();
+        BM_CUDA(cudaMemcpyAsync(out, tmp.p, d->m * d->n * sizeof(double), cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaStreamSynchronize(d->stream));
+    });
+}
+
+bm_status bm_rng_create(uint64_t seed, bm_rng** out) {
+    return guarded([&] { *out = new bm_rng{std::mt19937_64(seed)}; });
+}
+bm_status bm_rng_destroy(bm_rng* r) {
+    return guarded([&] { delete r; });
+}
+uint64_t bm_rng_next(bm_rng* r) { return r->eng(); }
+
+bm_status bm_sample_chunk(const bm_dataset* dc, uint64_t s, bm_rng* rng, uint64_t* out) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        const uint64_t m = d->m;
+        if (s < 1 || s > m) throw ConfigError("sample_chunk: chunk size must be in [1, m]");
+        if (s == m) {  // :46-48
+            for (uint64_t i = 0; i < m; ++i) out[i] = i;
+            return;
+        }
+        DeviceGuard g(d->device);
+        SamplerWs& sw = get_sws(d, s);
+        draw_targets(sw, rng->eng);
+        enqueue_resolve(d->stream, sw);
+        std::vector<uint32_t> tmp(s);
+        BM_CUDA(cudaMemcpyAsync(tmp.data(), sw.idx.p, s * sizeof(uint32_t), cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaStreamSynchronize(d->stream));
+        for (uint64_t i = 0; i < s; ++i) out[i] = tmp[i];
+    });
+}
+
+bm_status bm_assign_nearest(const bm_dataset* dc, const double* C, const uint8_t* mask, uint64_t k,
+                            int32_t* labels, double* dists, uint64_t* evals) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        if (k < 1) throw ConfigError("centroids must have at least one row and one column");
+        DeviceGuard g(d->device);
+        Workspace& w = get_ws(d, 0, (int)k, 1, 0);
+        upload_centroids(d->stream, w, C, mask);
+        launch_compact(d->stream, w, w.C.p, w.mask.p);
+        DevBuf<int32_t> dl(d->m);
+        DevBuf<double> dd(d->m);
+        Points P = dataset_points(d);
+        launch_assign(d->stream, P, w, (int)k, dl.p, 0, nullptr, dd.p, nullptr, nullptr);
+        BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaStreamSynchronize(d->stream));
+        if (w.h_status.p->n_active == 0) throw StateError("assign_nearest: every centroid is degenerate");
+        BM_CUDA(cudaMemcpyAsync(labels, dl.p, d->m * sizeof(int32_t), cudaMemcpyDeviceToHost, d->stream));
+        if (dists) BM_CUDA(cudaMemcpyAsync(dists, dd.p, d->m * sizeof(double), cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaStreamSynchronize(d->stream));
+        if (evals) *evals += d->m * (uint64_t)w.h_status.p->n_active;
+    });
+}
+
+bm_status bm_assign_rows(const bm_dataset* dc, const double* C, const uint8_t* mask, uint64_t k,
+                         uint64_t row_begin, uint64_t row_end, int32_t* labels, double* tile_partials,
+                         uint64_t* evals) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        if (k < 1) throw ConfigError("centroids must have at least one row and one column");
+        if (row_begin % kTile != 0 || row_begin > row_end || row_end > d->m)
+            throw ConfigError("assign_rows: row range must start on a 1024-row tile and lie in [0, m]");
+        if (row_begin == row_end) return;
+        DeviceGuard g(d->device);
+        Workspace& w = get_ws(d, 0, (int)k, 1, 0);
+        upload_centroids(d->stream, w, C, mask);
+        launch_compact(d->stream, w, w.C.p, w.mask.p);
+        const uint64_t r = row_end - row_begin;
+        DevBuf<int32_t> dl(r);
+        DevBuf<double> dd(r), dt(tiles_of(r));
+        final_pass(d->stream, d, w, row_begin, row_end, labels, tile_partials, evals, dl, dd, dt);
+    });
+}
+
+bm_status bm_objective(const bm_dataset* d, const double* C, const uint8_t* mask, uint64_t k, double* objective,
+                       uint64_t* evals) {
+    return guarded([&] {
+        std::vector<double> tiles(tiles_of(d->m));
+        bm_status rc = bm_assign_rows(d, C, mask, k, 0, d->m, nullptr, tiles.data(), evals);
+        if (rc != BM_OK) {
+            if (rc == BM_CONFIG_ERROR) throw ConfigError(g_last_error);
+            if (rc == BM_STATE_ERROR) throw StateError(g_last_error);
+            throw std::runtime_error(g_last_error);
+        }
+        double total = 0.0;
+        for (double t : tiles) total += t;
+        *objective = total;
+    });
+}
+
+bm_status bm_block_sum(const double* values, uint64_t count, int device, double* out) {
+    return guarded([&] {
+        if (count == 0) {
+            *out = 0.0;
+            return;
+        }
+        DeviceGuard g(device);
+        DevBuf<double> dv(count), dt(tiles_of(count));
+        BM_CUDA(cudaMemcpy(dv.p, values, count * sizeof(double), cudaMemcpyHostToDevice));
+        launch_tile_sums(0, dv.p, count, 0, 1, dt.p, nullptr);
+        std::vector<double> tiles(tiles_of(count));
+        BM_CUDA(cudaMemcpy(tiles.data(), dt.p, tiles.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        double total = 0.0;
+        for (double t : tiles) total += t;
+        *out = total;
+    });
+}
+
+bm_status bm_update_centroids(const bm_dataset* dc, const int32_t* labels, uint64_t k, double* C, uint8_t* mask) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        for (uint64_t i = 0; i < d->m; ++i)
+            if (labels[i] < 0 || (uint64_t)labels[i] >= k) throw ConfigError("update_centroids: label out of range");
+        DeviceGuard g(d->device);
+        Workspace& w = get_ws(d, d->m, (int)k, 1, 0);
+        cudaStream_t st = d->stream;
+        BM_CUDA(cudaMemcpyAsync(w.labels.p, labels, d->m * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        launch_update(st, dataset_points(d), w, nullptr, nullptr);
+        BM_CUDA(cudaMemcpyAsync(C, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(mask, w.mask.p, k, cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+bm_status bm_kmeanspp_fill(const bm_dataset* dc, double* C, uint8_t* mask, uint64_t k, int32_t candidates,
+                           bm_rng* rng, uint64_t* evals) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        if (candidates < 1) throw ConfigError("kmeanspp_fill: candidates_per_step must be at least 1");
+        DeviceGuard g(d->device);
+        Workspace& w = get_ws(d, d->m, (int)k, candidates, 0);
+        upload_centroids(d->stream, w, C, mask);
+        std::vector<uint8_t> hmask(mask, mask + k);
+        uint64_t ev = 0;
+        kmeanspp_fill_device(d->stream, dataset_points(d), w, hmask, candidates, rng->eng, ev);
+        BM_CUDA(cudaMemcpyAsync(C, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaMemcpyAsync(mask, w.mask.p, k, cudaMemcpyDeviceToHost, d->stream));
+        BM_CUDA(cudaStreamSynchronize(d->stream));
+        if (evals) *evals += ev;
+    });
+}
+
+bm_status bm_lloyd(const bm_dataset* dc, double* C, uint8_t* mask, uint64_t k, uint64_t max_iterations,
+                   double rel_tolerance, int32_t* labels, double* history, uint64_t history_capacity,
+                   uint64_t* history_len, double* objective, uint64_t* evals, uint64_t* iterations) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        if (max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
+        if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
+        DeviceGuard g(d->device);
+        Workspace& w = get_ws(d, d->m, (int)k, 1, max_iterations + 1);
+        cudaStream_t st = d->stream;
+        upload_centroids(st, w, C, mask);
+        LloydResult r = lloyd_run(st, dataset_points(d), w, max_iterations, rel_tolerance);
+        const uint64_t hl = r.iterations + 1;
+        std::vector<double> h(hl);
+        BM_CUDA(cudaMemcpyAsync(h.data(), w.history.p, hl * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(C, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(mask, w.mask.p, k, cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(labels, w.labels.p + (uint64_t)r.parity * w.R, d->m * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        for (uint64_t i = 0; i < hl && i < history_capacity; ++i) history[i] = h[i];
+        if (history_len) *history_len = hl;
+        *objective = r.objective;
+        *evals = r.evals;
+        *iterations = r.iterations;
+    });
+}
+
+bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uint64_t seed,
+                       uint64_t max_iterations, double rel_tolerance, bm_outcome* out) {
+    return guarded([&] {
+        bm_dataset* d = const_cast<bm_dataset*>(dc);
+        if (k < 1) throw ConfigError("kmeans: k must be at least 1");
+        if (d->m < k) throw ConfigError("kmeans: dataset has fewer points than clusters");
+        if (max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
+        if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
+        DeviceGuard g(d->device);
+        cudaStream_t st = d->stream;
+        Workspace& w = get_ws(d, d->m, (int)k, candidates, 0);
+        std::mt19937_64 rng(seed);  // local_search.cpp:69
+        const auto t_init = std::chrono::steady_clock::now();
+        BM_CUDA(cudaMemsetAsync(w.C.p, 0, k * d->n * sizeof(double), st));
+        BM_CUDA(cudaMemsetAsync(w.mask.p, 1, k, st));
+        std::vector<uint8_t> hmask(k, 1);
+        uint64_t init_evals = 0;
+        Points P = dataset_points(d);
+        kmeanspp_fill_device(st, P, w, hmask, candidates, rng, init_evals);
+        BM_CUDA(cudaStreamSynchronize(st));
+        out->cpu_init = seconds_since(t_init);
+        const auto t_search = std::chrono::steady_clock::now();
+        LloydResult r = lloyd_run(st, P, w, max_iterations, rel_tolerance);
+        BM_CUDA(cudaMemcpyAsync(out->centroids, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(out->mask, w.mask.p, k, cudaMemcpyDeviceToHost, st));
+        if (out->labels)
+            BM_CUDA(cudaMemcpyAsync(out->labels, w.labels.p + (uint64_t)r.parity * w.R, d->m * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        out->cpu_full = seconds_since(t_search);
+        out->objective = r.objective;
+        out->distance_evals = r.evals + init_evals;
+        out->iterations = r.iterations;
+        out->chunks = 1;
+    });
+}
+
+bm_status bm_big_means(bm_dataset* d, const bm_config* cfg, bm_outcome* out, bm_chunk_record* trace,
+                       uint64_t trace_capacity) {
+    return guarded([&] { big_means(d, *cfg, out, trace, trace_capacity); });
+}
+
+bm_status bm_set_profiling(int enabled) {
+    g_profiling = enabled != 0;
+    return BM_OK;
+}
+
+bm_status bm_last_profile(bm_profile* out) {
+    *out = g_profile;
+    return BM_OK;
+}
+
+}  // extern "C"

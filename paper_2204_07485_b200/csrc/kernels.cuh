@@ -1,0 +1,680 @@
+// kernels.cuh — sm_100a kernels of the Big-means hot path.
+//
+// Bit-exactness contract.  Every fp64 operation that the
+// reference performs is performed here with the same operands in the same
+// order, with explicit round-to-nearest intrinsics (__dsub_rn/__dmul_rn/
+// __dadd_rn) so that nvcc can never contract a*b+c into an FMA (the
+// reference's default x86-64 build emits none).  fp32-stored datasets are
+// promoted to fp64 exactly ((double)x) before any arithmetic.
+//
+// Citations are relative to /root/reference/proj.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace bm {
+namespace dev {
+
+// ---------------------------------------------------------------------------
+// Device-side Lloyd status (one per workspace).  Mirrors the loop state of
+// lloyd() local_search.cpp:16-60 so that the loop can run without host trips.
+// ---------------------------------------------------------------------------
+struct LloydStatus {
+    double f;            // f of the previous round (local_search.cpp:27,51)
+    double objective;    // history.back() (:54)
+    unsigned long long evals;       // this run's distance evals (core.cpp:157-159)
+    unsigned long long iterations;  // ++iterations (:36)
+    int parity;          // labels[parity] holds the current assignment
+    int stop;            // loop finished
+    int changed;         // set by the assignment when a label differs (:39)
+    int n_active;        // active rows of the centroid buffer last assigned with
+    int state_error;     // assign against all-degenerate centroids (core.cpp:115-118)
+    int inc_degenerate;  // degenerate rows of the incumbent after the accept step
+    int bad_label;       // update saw a label outside [0,k) (core.cpp:189-193)
+    int pad;
+};
+
+// Per-chunk accept record (ChunkRecord big_means.hpp:28-34).
+struct Record {
+    unsigned long long chunk_index;
+    double candidate_objective;
+    double incumbent_objective;
+    unsigned long long accepted;
+    unsigned long long degenerate_repaired;
+};
+
+// Exact promotion of the storage type (P11).
+__device__ __forceinline__ double to_f64(double v) { return v; }
+__device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v); }
+
+// One step of the reference distance loop core.cpp:144-145 / init.cpp:34-35:
+// diff = x - c; sum += diff * diff  (three separately rounded operations).
+__device__ __forceinline__ double dist_step(double sum, double x, double c) {
+    const double diff = __dsub_rn(x, c);
+    return __dadd_rn(sum, __dmul_rn(diff, diff));
+}
+
+// ===========================================================================
+// 1. Chunk sampling: Fisher-Yates resolution of the host's raw draws.
+//
+// sample_chunk big_means.cpp:49-54 swaps idx[i] <-> idx[j_i] (j_i >= i) for
+// i < s and returns sort(idx[0:s]).  Only the SET of the first s positions
+// matters (it is sorted).  With W(t) = value at position t just before step t
+// (W(t) = W(LT[t]) if LT[t] = max{t' < t : j_t' = t} exists, else t):
+//   set ∩ [s,m) = { distinct j_t >= s }
+//   set ∩ [0,s) = [0,s) \ { W(t_last(p)) : p >= s targeted, t_last = last step hitting p }
+// (a value < s that ends at a position >= s is exactly the one left there by
+// the last swap into that position).  All steps are data-parallel.
+// ===========================================================================
+__device__ __forceinline__ uint32_t hash_slot(uint32_t key, uint32_t hmask) {
+    return (key * 2654435761u) & hmask;
+}
+
+__global__ void k_fy_pass1(const uint32_t* __restrict__ js, uint32_t s, int* __restrict__ LT,
+                           uint32_t* __restrict__ hkeys, int* __restrict__ hvals, uint32_t hmask) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s) return;
+    const uint32_t j = js[t];
+    if (j < s) {
+        if (j > t) atomicMax(&LT[j], static_cast<int>(t));
+        return;
+    }
+    uint32_t h = hash_slot(j, hmask);
+    while (true) {
+        const uint32_t prev = atomicCAS(&hkeys[h], 0xFFFFFFFFu, j);
+        if (prev == 0xFFFFFFFFu || prev == j) {
+            atomicMax(&hvals[h], static_cast<int>(t));
+            return;
+        }
+        h = (h + 1) & hmask;
+    }
+}
+
+__global__ void k_fy_pass2(const uint32_t* __restrict__ js, uint32_t s, const int* __restrict__ LT,
+                           const uint32_t* __restrict__ hkeys, const int* __restrict__ hvals,
+                           uint32_t hmask, uint8_t* __restrict__ kept, uint32_t* __restrict__ bitmap) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s) return;
+    const uint32_t j = js[t];
+    if (j < s) return;
+    uint32_t h = hash_slot(j, hmask);
+    while (hkeys[h] != j) h = (h + 1) & hmask;
+    if (hvals[h] != static_cast<int>(t)) return;  // not the last swap into j
+    atomicOr(&bitmap[j >> 5], 1u << (j & 31));
+    int w = static_cast<int>(t);
+    while (LT[w] >= 0) w = LT[w];
+    kept[w] = 0;
+}
+
+__global__ void k_fy_pass3(const uint8_t* __restrict__ kept, uint32_t s, uint32_t* __restrict__ bitmap) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= s) return;
+    if (kept[v]) atomicOr(&bitmap[v >> 5], 1u << (v & 31));
+}
+
+// Bitmap -> ascending index list (the std::sort of big_means.cpp:54).
+constexpr int kScanThreads = 256;
+constexpr int kWordsPerThread = 8;
+constexpr int kWordsPerBlock = kScanThreads * kWordsPerThread;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot,
+                                                         uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const uint32_t x = warp_tot[w];
+            warp_tot[w] = run;
+            run += x;
+        }
+        *total = run;
+    }
+    __syncthreads();
+    return warp_tot[warp] + incl - v;
+}
+
+__global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, uint32_t nwords,
+                                      uint32_t* __restrict__ block_counts) {
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    __shared__ uint32_t total;
+    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q)
+        if (base + q < nwords) c += __popc(bitmap[base + q]);
+    block_exclusive_scan(c, warp_tot, &total);
+    if (threadIdx.x == 0) block_counts[blockIdx.x] = total;
+}
+
+__global__ void k_scan_block_counts(uint32_t* __restrict__ counts, uint32_t nblocks) {
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    __shared__ uint32_t total;
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < nblocks; b0 += blockDim.x) {
+        const uint32_t b = b0 + threadIdx.x;
+        const uint32_t v = b < nblocks ? counts[b] : 0;
+        const uint32_t ex = block_exclusive_scan(v, warp_tot, &total);
+        if (b < nblocks) counts[b] = carry + ex;
+        carry += total;
+        __syncthreads();
+    }
+}
+
+__global__ void k_bitmap_emit(const uint32_t* __restrict__ bitmap, uint32_t nwords,
+                              const uint32_t* __restrict__ block_offsets, uint32_t* __restrict__ out) {
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    __shared__ uint32_t total;
+    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
+    uint32_t words[kWordsPerThread];
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        words[q] = base + q < nwords ? bitmap[base + q] : 0u;
+        c += __popc(words[q]);
+    }
+    uint32_t pos = block_offsets[blockIdx.x] + block_exclusive_scan(c, warp_tot, &total);
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        uint32_t w = words[q];
+        while (w) {
+            const int b = __ffs(w) - 1;
+            out[pos++] = (base + q) * 32u + static_cast<uint32_t>(b);
+            w &= w - 1;
+        }
+    }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ out, uint32_t s) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s) out[i] = i;
+}
+
+// ===========================================================================
+// 2. Row gather (Dataset::gather core.cpp:34-44): one warp per output row,
+//    16-byte vectors (rows are padded to 16-byte multiples).
+// ===========================================================================
+__global__ void k_gather(const uint4* __restrict__ X, uint64_t row_vecs, const uint32_t* __restrict__ idx,
+                         uint32_t s, uint4* __restrict__ out) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= s) return;
+    const uint4* src = X + static_cast<uint64_t>(idx[warp]) * row_vecs;
+    uint4* dst = out + static_cast<uint64_t>(warp) * row_vecs;
+    for (uint64_t v = lane; v < row_vecs; v += 32) dst[v] = __ldg(src + v);
+}
+
+// ===========================================================================
+// 3. Exact nearest-centroid assignment (assign_nearest core.cpp:106-161).
+//
+// CTA = 128 points x all active centroids.  Thread (pg, cg) owns points
+// {pg + 32 t : t < 4} and compacted centroids {4 cg + u : u < 4}: 16
+// independent fp64 chains, each a strict left fold over d (P1).  Points and
+// centroids are staged through shared memory in 16-dim slabs, transposed so
+// that the point loads are conflict-free and the centroid loads broadcast.
+// Centroids are the COMPACTED active rows in ascending original index, so an
+// ascending strict-< scan over them is the reference's masked j-loop (P2).
+// ===========================================================================
+constexpr int kAP = 4;            // points per thread
+constexpr int kAK = 4;            // centroids per thread
+constexpr int kAPG = 32;          // point groups (= lanes) per CTA
+constexpr int kABP = kAP * kAPG;  // 128 points per CTA
+constexpr int kADC = 16;          // dims per shared-memory slab
+constexpr int kAMaxCG = 8;        // centroid groups per CTA (<= 32 centroids per pass)
+constexpr int kAXS = kABP + 1;    // padded slab stride
+
+template <typename T>
+__global__ void __launch_bounds__(kAPG * kAMaxCG)
+k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+         const double* __restrict__ Cact, const int* __restrict__ act_idx,
+         const int* __restrict__ n_active_ptr,
+         int32_t* __restrict__ labels_pair, uint64_t pair_stride, const int* __restrict__ parity_ptr,
+         double* __restrict__ dists_out, int* __restrict__ changed_flag,
+         const int* __restrict__ stop_ptr) {
+    __shared__ double xs[kADC * kAXS];
+    __shared__ double cs[kADC * kAMaxCG * kAK];
+    __shared__ double red_d[kAMaxCG][kABP];
+    __shared__ int red_j[kAMaxCG][kABP];
+    __shared__ double best_d[kABP];
+    __shared__ int best_j[kABP];
+
+    if (stop_ptr && *stop_ptr) return;  // Lloyd loop already finished
+    const int KA = *n_active_ptr;
+    // Lloyd mode: write labels[1-parity], compare with labels[parity] (:34,:39).
+    int32_t* labels_out = labels_pair;
+    const int32_t* labels_old = nullptr;
+    if (parity_ptr) {
+        const int par = *parity_ptr;
+        labels_out = labels_pair + (1 - par) * pair_stride;
+        labels_old = labels_pair + par * pair_stride;
+    }
+    const int KG = blockDim.x / kAPG;
+    const int KB = KG * kAK;  // centroids per pass
+    const int tid = threadIdx.x, pg = tid % kAPG, cg = tid / kAPG;
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
+
+    if (tid < kABP) {
+        best_d[tid] = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+        best_j[tid] = -1;
+    }
+    for (int kb = 0; kb < KA; kb += KB) {
+        double acc[kAP][kAK];
+#pragma unroll
+        for (int t = 0; t < kAP; ++t)
+#pragma unroll
+            for (int u = 0; u < kAK; ++u) acc[t][u] = 0.0;
+
+        for (int d0 = 0; d0 < n; d0 += kADC) {
+            const int dl = min(kADC, n - d0);
+            __syncthreads();
+            for (int e = tid; e < kABP * kADC; e += blockDim.x) {
+                const int p = e / kADC, d = e % kADC;
+                const uint64_t gp = p0 + p;
+                double v = 0.0;
+                if (gp < rows && d < dl) v = to_f64(X[gp * ld + d0 + d]);
+                xs[d * kAXS + p] = v;
+            }
+            for (int e = tid; e < KB * kADC; e += blockDim.x) {
+                const int j = e / kADC, d = e % kADC;
+                double v = 0.0;
+                if (kb + j < KA && d < dl) v = Cact[static_cast<uint64_t>(kb + j) * n + d0 + d];
+                cs[d * KB + j] = v;
+            }
+            __syncthreads();
+            for (int d = 0; d < dl; ++d) {
+                double xv[kAP], cv[kAK];
+#pragma unroll
+                for (int t = 0; t < kAP; ++t) xv[t] = xs[d * kAXS + pg + kAPG * t];
+#pragma unroll
+                for (int u = 0; u < kAK; ++u) cv[u] = cs[d * KB + cg * kAK + u];
+#pragma unroll
+                for (int t = 0; t < kAP; ++t)
+#pragma unroll
+                    for (int u = 0; u < kAK; ++u) acc[t][u] = dist_step(acc[t][u], xv[t], cv[u]);
+            }
+        }
+        // Ascending strict-< within the thread's 4 centroids ...
+#pragma unroll
+        for (int t = 0; t < kAP; ++t) {
+            double b = __longlong_as_double(0x7FF0000000000000LL);
+            int bj = -1;
+#pragma unroll
+            for (int u = 0; u < kAK; ++u) {
+                const int j = kb + cg * kAK + u;
+                if (j < KA && acc[t][u] < b) {
+                    b = acc[t][u];
+                    bj = j;
+                }
+            }
+            red_d[cg][pg + kAPG * t] = b;
+            red_j[cg][pg + kAPG * t] = bj;
+        }
+        __syncthreads();
+        // ... then across centroid groups in ascending order (first minimum wins).
+        if (tid < kABP) {
+            double b = best_d[tid];
+            int bj = best_j[tid];
+            for (int g = 0; g < KG; ++g) {
+                if (red_j[g][tid] >= 0 && red_d[g][tid] < b) {
+                    b = red_d[g][tid];
+                    bj = red_j[g][tid];
+                }
+            }
+            best_d[tid] = b;
+            best_j[tid] = bj;
+        }
+        __syncthreads();
+    }
+    if (tid < kABP) {
+        const uint64_t gp = p0 + tid;
+        if (gp < rows) {
+            const int bj = best_j[tid];
+            const int label = bj >= 0 ? act_idx[bj] : -1;
+            labels_out[gp] = label;
+            if (dists_out) dists_out[gp] = best_d[tid];
+            if (labels_old && labels_old[gp] != label) *changed_flag = 1;
+        }
+    }
+}
+
+// ===========================================================================
+// 4. Per-tile sequential sums (block_sum inner loop core.cpp:167-173).
+//    One warp per (array, tile); lanes stage 32 values, all lanes fold them in
+//    index order (redundantly), lane 0 writes.
+// ===========================================================================
+__global__ void k_tile_sums(const double* __restrict__ v, uint64_t count, uint64_t stride,
+                            int narrays, double* __restrict__ tiles, const int* __restrict__ stop_ptr) {
+    if (stop_ptr && *stop_ptr) return;
+    const uint64_t ntiles = (count + kTile - 1) / kTile;
+    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= ntiles * narrays) return;
+    const uint64_t a = w / ntiles, t = w % ntiles;
+    const double* src = v + a * stride;
+    const uint64_t b = t * kTile, e = min(b + kTile, count);
+    double acc = 0.0;
+    for (uint64_t i0 = b; i0 < e; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const double x = i < e ? src[i] : 0.0;
+        const int cnt = static_cast<int>(min((uint64_t)32, e - i0));
+        for (int l = 0; l < cnt; ++l) acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, x, l));
+    }
+    if (lane == 0) tiles[a * ntiles + t] = acc;
+}
+
+// Ordered fold of tile partials (block_sum outer loop core.cpp:172).
+__device__ __forceinline__ double fold_tiles(const double* tiles, uint64_t ntiles) {
+    double total = 0.0;
+    for (uint64_t t = 0; t < ntiles; ++t) total = __dadd_rn(total, tiles[t]);
+    return total;
+}
+
+// ===========================================================================
+// 5. Centroid update (update_centroids core.cpp:183-244), bit-exact order.
+//
+// Phase A, grid (tile, d-slab): stable per-tile bucketing of points by label
+// (warp-synchronous, index order preserved), then one thread per
+// (label, dim) folds its members' coordinates in index order from 0.0 — the
+// reference's per-block partial row[d] += x[d] (:206-214).
+// Phase B: one thread per (label, dim) folds the non-empty tile partials in
+// tile order (:217-229; empty partials are +0.0 and adding +0.0 to a sum that
+// is never -0.0 is the identity, so they are skipped), then sum * (1.0/count)
+// (:237-239); count 0 -> degenerate row of 0.0 (:231 all_degenerate).
+// ===========================================================================
+constexpr int kUThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kUThreads)
+k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+                  const int32_t* __restrict__ labels_pair, uint64_t pair_stride,
+                  const int* __restrict__ parity_ptr, int k, int dslab,
+                  double* __restrict__ psum, uint32_t* __restrict__ pcnt, int* __restrict__ bad_label,
+                  const int* __restrict__ stop_ptr) {
+    if (stop_ptr && *stop_ptr) return;
+    extern __shared__ int ush[];
+    int* lab = ush;                 // [kTile]
+    int* order = lab + kTile;       // [kTile]
+    int* cnt = order + kTile;       // [k]
+    int* off = cnt + k;             // [k]
+    int* run = off + k;             // [k]
+
+    const int32_t* labels = labels_pair + (parity_ptr ? (*parity_ptr) * pair_stride : 0);
+    const uint64_t tile = blockIdx.x;
+    const uint64_t b = tile * kTile;
+    const int len = static_cast<int>(min((uint64_t)kTile, rows - b));
+    const int d0 = blockIdx.y * dslab;
+    const int d1 = min(n, d0 + dslab);
+
+    for (int j = threadIdx.x; j < k; j += blockDim.x) cnt[j] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        int l = labels[b + i];
+        if (l < 0 || l >= k) {  // update_centroids label range check (core.cpp:189-193)
+            *bad_label = 1;
+            l = 0;
+        }
+        lab[i] = l;
+        atomicAdd(&cnt[l], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int j = 0; j < k; ++j) {
+            off[j] = r;
+            run[j] = r;
+            r += cnt[j];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // stable placement, one warp, index order
+        const int lane = threadIdx.x;
+        for (int c0 = 0; c0 < len; c0 += 32) {
+            const int i = c0 + lane;
+            const bool valid = i < len;
+            const int l = valid ? lab[i] : -1 - lane;
+            const unsigned peers = __match_any_sync(0xFFFFFFFFu, l);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            const int leader = __ffs(peers) - 1;
+            int basev = 0;
+            if (valid && lane == leader) basev = run[l];
+            basev = __shfl_sync(0xFFFFFFFFu, basev, leader);
+            if (valid) order[basev + rank] = i;
+            __syncwarp();
+            if (valid && lane == leader) run[l] = basev + __popc(peers);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    const int dl = d1 - d0;
+    if (dl <= 0) return;
+    for (int e = threadIdx.x; e < k * dl; e += blockDim.x) {
+        const int j = e / dl, d = d0 + e % dl;
+        const int c = cnt[j];
+        if (c == 0) continue;
+        const int o = off[j];
+        double acc = 0.0;
+#pragma unroll 4
+        for (int q = 0; q < c; ++q)
+            acc = __dadd_rn(acc, to_f64(X[(b + order[o + q]) * ld + d]));
+        psum[(tile * k + j) * n + d] = acc;
+    }
+    if (blockIdx.y == 0)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) pcnt[tile * k + j] = cnt[j];
+}
+
+__global__ void __launch_bounds__(kUThreads)
+k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcnt, uint64_t ntiles,
+               int k, int n, double* __restrict__ C, uint8_t* __restrict__ mask,
+               double* __restrict__ Cact, int* __restrict__ act_idx, int* __restrict__ n_active,
+               const int* __restrict__ stop_ptr) {
+    if (stop_ptr && *stop_ptr) return;
+    extern __shared__ unsigned long long msh[];
+    unsigned long long* total = msh;                          // [k]
+    int* rank = reinterpret_cast<int*>(total + k);             // [k]
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        unsigned long long c = 0;
+        for (uint64_t t = 0; t < ntiles; ++t) c += pcnt[t * k + j];
+        total[j] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int j = 0; j < k; ++j) {
+            rank[j] = total[j] ? r : -1;
+            if (total[j]) {
+                if (blockIdx.x == 0) act_idx[r] = j;
+                ++r;
+            }
+            if (blockIdx.x == 0) mask[j] = total[j] ? 0 : 1;
+        }
+        if (blockIdx.x == 0) *n_active = r;
+    }
+    __syncthreads();
+    const uint64_t pairs = static_cast<uint64_t>(k) * n;
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < pairs;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(e / n), d = static_cast<int>(e % n);
+        if (total[j] == 0) {
+            C[e] = 0.0;
+            continue;
+        }
+        double acc = 0.0;
+        for (uint64_t t = 0; t < ntiles; ++t)
+            if (pcnt[t * k + j]) acc = __dadd_rn(acc, psum[(t * k + j) * n + d]);
+        const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
+        const double v = __dmul_rn(acc, inv);
+        C[e] = v;
+        Cact[static_cast<uint64_t>(rank[j]) * n + d] = v;
+    }
+}
+
+// Compact the active rows of (C, mask) for the assignment (single CTA).
+__global__ void k_compact(const double* __restrict__ C, const uint8_t* __restrict__ mask, int k, int n,
+                          double* __restrict__ Cact, int* __restrict__ act_idx, int* __restrict__ n_active) {
+    extern __shared__ int csh[];
+    if (threadIdx.x == 0) {
+        int r = 0;
+        for (int j = 0; j < k; ++j) {
+            csh[j] = mask[j] ? -1 : r;
+            if (!mask[j]) act_idx[r++] = j;
+        }
+        *n_active = r;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+        const int j = e / n;
+        if (csh[j] >= 0) Cact[static_cast<uint64_t>(csh[j]) * n + (e % n)] = C[e];
+    }
+}
+
+// ===========================================================================
+// 6. Lloyd control (local_search.cpp:26-54), single thread.
+// ===========================================================================
+__global__ void k_lloyd_begin(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+                              double* history) {
+    if (threadIdx.x != 0) return;
+    const double f = fold_tiles(tiles, ntiles);  // :27
+    if (history) history[0] = f;                 // :28
+    st->f = f;
+    st->objective = f;
+    st->evals = static_cast<unsigned long long>(rows) * st->n_active;  // :26 counter
+    st->iterations = 0;
+    st->parity = 0;
+    st->stop = 0;
+    st->changed = 0;
+    st->state_error = st->n_active == 0;
+    st->bad_label = 0;
+}
+
+__global__ void k_lloyd_step(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+                             unsigned long long max_iterations, double rel_tolerance, double* history) {
+    if (threadIdx.x != 0) return;
+    if (st->stop) return;
+    const double f_new = fold_tiles(tiles, ntiles);  // :35
+    st->evals += static_cast<unsigned long long>(rows) * st->n_active;
+    if (st->n_active == 0) st->state_error = 1;
+    st->iterations += 1;            // :36
+    st->objective = f_new;          // history.push_back (:37)
+    if (history) history[st->iterations] = f_new;
+    const bool unchanged = st->changed == 0;  // :39
+    st->changed = 0;
+    st->parity ^= 1;                // :40-41 advance
+    const double f = st->f;
+    bool stop = unchanged;                                                      // :42-44
+    if (!stop && f <= 0.0) stop = true;                                         // :45-47
+    if (!stop && rel_tolerance > 0.0 && __ddiv_rn(__dsub_rn(f, f_new), f) < rel_tolerance)
+        stop = true;                                                            // :48-50
+    if (!stop) st->f = f_new;                                                   // :51
+    if (st->iterations >= max_iterations) stop = true;                          // :32
+    st->stop = stop ? 1 : 0;
+}
+
+// ===========================================================================
+// 7. Accept (big_means.cpp:89-94) on the device.
+// ===========================================================================
+__global__ void k_accept(const LloydStatus* st, double* f_opt, const double* __restrict__ C,
+                         const uint8_t* __restrict__ mask, double* __restrict__ Cinc,
+                         uint8_t* __restrict__ maskinc, int k, int n, Record* rec,
+                         unsigned long long chunk, unsigned long long repaired, int* inc_degenerate) {
+    // st is const here; the count is written through inc_degenerate (&st->inc_degenerate).
+    __shared__ int accepted;
+    if (threadIdx.x == 0) {
+        accepted = st->objective < *f_opt;  // strict (:89)
+        if (accepted) *f_opt = st->objective;
+        rec->chunk_index = chunk;
+        rec->candidate_objective = st->objective;
+        rec->incumbent_objective = *f_opt;
+        rec->accepted = accepted;
+        rec->degenerate_repaired = repaired;
+    }
+    __syncthreads();
+    if (accepted) {
+        for (int e = threadIdx.x; e < k * n; e += blockDim.x) Cinc[e] = C[e];
+        for (int j = threadIdx.x; j < k; j += blockDim.x) maskinc[j] = mask[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int dcount = 0;
+        for (int j = 0; j < k; ++j) dcount += maskinc[j] ? 1 : 0;
+        *inc_degenerate = dcount;
+    }
+}
+
+// ===========================================================================
+// 8. K-means++ helpers (init.cpp:19-43, 183-198).
+// out[c*rows + i] = dist(x_i, x_{cand[c]}), lowered by d2 when given
+// (trial = std::min(trial, dist2) -> dist2 < trial ? dist2 : trial).
+// ===========================================================================
+template <typename T>
+__global__ void k_dist_rows(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+                            const uint32_t* __restrict__ cand, int ncand,
+                            const double* __restrict__ d2, double* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const T* x = X + i * ld;
+    for (int c = 0; c < ncand; ++c) {
+        const T* r = X + static_cast<uint64_t>(cand[c]) * ld;
+        double sum = 0.0;
+        for (int d = 0; d < n; ++d) sum = dist_step(sum, to_f64(x[d]), to_f64(r[d]));
+        if (d2) {
+            const double o = d2[i];
+            if (o < sum) sum = o;
+        }
+        out[static_cast<uint64_t>(c) * rows + i] = sum;
+    }
+}
+
+// set_row (core.cpp:78-83 / init.cpp:146,197): centroid j := pool row.
+template <typename T>
+__global__ void k_set_row(const T* __restrict__ X, uint64_t ld, int n, uint64_t r,
+                          double* __restrict__ C, uint8_t* __restrict__ mask, int j) {
+    for (int d = threadIdx.x; d < n; d += blockDim.x)
+        C[static_cast<uint64_t>(j) * n + d] = to_f64(X[r * ld + d]);
+    if (threadIdx.x == 0) mask[j] = 0;
+}
+
+// ===========================================================================
+// 9. Dataset helpers.
+// ===========================================================================
+template <typename T>
+__global__ void k_check_finite(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld, int* bad) {
+    const uint64_t total = rows * static_cast<uint64_t>(n);
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double v = to_f64(X[(e / n) * ld + (e % n)]);
+        if (!isfinite(v)) *bad = 1;
+    }
+}
+
+template <typename T>
+__global__ void k_promote(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld, double* __restrict__ out) {
+    const uint64_t total = rows * static_cast<uint64_t>(n);
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[e] = to_f64(X[(e / n) * ld + (e % n)]);
+}
+
+template <typename T>
+__global__ void k_gather_checked(const T* __restrict__ X, uint64_t ld, int n, const uint64_t* __restrict__ idx,
+                                 uint64_t count, T* __restrict__ out, uint64_t out_ld) {
+    const uint64_t total = count * static_cast<uint64_t>(n);
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = e / n;
+        out[r * out_ld + (e % n)] = X[idx[r] * ld + (e % n)];
+    }
+}
+
+}  // namespace dev
+}  // namespace bm

@@ -1,0 +1,144 @@
+"""GPU parity: the big_means driver (big_means.cpp:58-112) — reference
+test_big_means.cpp / acceptance criteria 2, 3, 9 and bitwise agreement with the
+golden vectors and the oracle on every BASELINE config (reduced m and s)."""
+import numpy as np
+import pytest
+
+import paper_2204_07485_b200 as bm
+from paper_2204_07485_b200 import synthetic
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg(k, s, chunks, seed=bm.K_DEFAULT_SEED, **kw):
+    return bm.BigMeansConfig(k=k, chunk_size=s, max_chunks=chunks, seed=seed, **kw)
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_big_means_golden(golden, i):
+    X = golden[f"bm{i}_X"]
+    k, s, ch, seed = golden[f"bm{i}_cfg"].tolist()
+    out, trace = bm.big_means(bm.Dataset(X), cfg(k, s, ch, seed))
+    assert (bits(out.centroids.values) == bits(golden[f"bm{i}_C"])).all()
+    assert (out.centroids.mask == golden[f"bm{i}_mask"]).all()
+    assert (out.assignment == golden[f"bm{i}_labels"]).all()
+    assert out.objective == golden[f"bm{i}_obj"][0]
+    assert [out.counter.distance_evals, out.counter.iterations, trace.chunks()] == \
+        golden[f"bm{i}_stats"].tolist()
+    tr = np.array([[r.candidate_objective, r.incumbent_objective] for r in trace.records])
+    assert (bits(tr) == bits(golden[f"bm{i}_trace"])).all()
+    ti = np.array([[r.chunk_index, r.accepted, r.degenerate_repaired] for r in trace.records],
+                  np.uint64)
+    assert ti.tolist() == golden[f"bm{i}_trace_int"].tolist()
+
+
+def test_validation():  # test_big_means.cpp:56-73
+    d = bm.Dataset(np.random.default_rng(3).uniform(0, 50, (50, 2)))
+    with pytest.raises(bm.ConfigError):
+        bm.big_means(d, bm.BigMeansConfig(k=3, chunk_size=10))
+    for bad in (cfg(0, 10, 1), cfg(5, 4, 1), cfg(5, 51, 1), cfg(5, 10, 0)):
+        with pytest.raises(bm.ConfigError):
+            bm.big_means(d, bad)
+    with pytest.raises(bm.ConfigError):
+        bm.big_means(d, bm.BigMeansConfig(k=5, chunk_size=10, max_cpu_seconds=-1.0))
+
+
+def test_trace_monotone_and_first_chunk_repairs_k():  # test_big_means.cpp:75-92
+    d = bm.Dataset(np.random.default_rng(4).uniform(0, 50, (600, 2)))
+    out, trace = bm.big_means(d, cfg(5, 100, 40))
+    assert trace.chunks() == 40
+    prev = trace.records[0].incumbent_objective
+    for i, r in enumerate(trace.records):
+        assert r.chunk_index == i and r.incumbent_objective <= prev
+        prev = r.incumbent_objective
+        if r.accepted:
+            assert r.incumbent_objective == r.candidate_objective
+        else:
+            assert r.candidate_objective >= r.incumbent_objective
+    assert trace.records[0].accepted and trace.records[0].degenerate_repaired == 5
+
+
+def test_final_pass_and_skip():  # test_big_means.cpp:103-128
+    X = np.random.default_rng(6).uniform(0, 50, (500, 2))
+    d = bm.Dataset(X)
+    out, _ = bm.big_means(d, cfg(4, 80, 15))
+    assert out.assignment.size == 500
+    assert bm.objective(d, out.centroids) == out.objective
+    labels, _ = bm.assign_nearest(d, out.centroids)
+    assert (labels == out.assignment).all() and out.counter.cpu_full > 0.0
+    out2, tr2 = bm.big_means(d, cfg(4, 80, 15, final_assignment=False))
+    assert out2.assignment.size == 0
+    assert out2.objective == tr2.records[-1].incumbent_objective
+    assert out.counter.distance_evals - out2.counter.distance_evals == 500 * 4
+
+
+def test_budgets_and_determinism():  # test_big_means.cpp:130-158
+    d = bm.Dataset(np.random.default_rng(7).uniform(0, 50, (400, 2)))
+    _, tr = bm.big_means(d, cfg(3, 50, 6))
+    assert tr.chunks() == 6
+    out, tr = bm.big_means(d, bm.BigMeansConfig(k=3, chunk_size=50, max_cpu_seconds=0.05))
+    assert tr.chunks() >= 1 and out.counter.cpu_init >= 0.0
+    d = bm.Dataset(np.random.default_rng(8).uniform(0, 50, (800, 2)))
+    a, ta = bm.big_means(d, cfg(5, 120, 30, seed=31337))
+    b, tb = bm.big_means(d, cfg(5, 120, 30, seed=31337))
+    assert a.centroids == b.centroids and (a.assignment == b.assignment).all()
+    assert bits([a.objective]) == bits([b.objective])
+    assert [r.candidate_objective for r in ta.records] == [r.candidate_objective for r in tb.records]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_single_chunk_equals_kmeans(seed, port):  # test_big_means.cpp:177-195, criterion 3
+    X = np.random.default_rng(40 + seed).uniform(0, 50, (200 + 30 * seed, 2))
+    d = bm.Dataset(X)
+    b, _ = bm.big_means(d, cfg(4, X.shape[0], 1, seed=900 + seed))
+    km = bm.kmeans(d, 4, bm.InitConfig(seed=900 + seed), bm.SearchConfig())
+    assert b.centroids == km.centroids and (b.assignment == km.assignment).all()
+    assert bits([b.objective]) == bits([km.objective])
+    assert b.counter.iterations == km.counter.iterations
+    p = port.kmeans_pp(X, 4, 900 + seed)
+    assert km.objective == p.objective and km.counter.distance_evals == p.evals
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_big_means_vs_oracle_random(port, seed):
+    rng = np.random.default_rng(500 + seed)
+    m = int(rng.integers(300, 20000))
+    n = int(rng.integers(1, 40))
+    k = int(rng.integers(1, 30))
+    s = int(rng.integers(k, min(m, 5000) + 1))
+    X = rng.normal(size=(m, n)) * rng.uniform(0.1, 30)
+    if seed % 3 == 1:
+        X = np.rint(X)
+    if seed % 3 == 2:
+        X = X.astype(np.float32)
+    out, trace = bm.big_means(bm.Dataset(X), cfg(k, s, 8, seed=seed))
+    p = port.big_means(X.astype(np.float64), k, s, 8, seed=seed)
+    got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+            r.degenerate_repaired) for r in trace.records]
+    assert got == p.trace
+    assert out.objective == p.objective
+    assert (bits(out.centroids.values) == bits(p.centroids)).all()
+    assert (out.assignment == p.labels).all()
+    assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+CONFIG_SCALE = {"c1": (1.0, 6), "c2": (0.02, 4), "c3": (0.005, 4), "c4": (0.05, 3),
+                "c5": (0.25, 3)}
+
+
+@pytest.mark.parametrize("key", sorted(CONFIG_SCALE))
+def test_configs_bitwise_vs_oracle(port, key):
+    """Every BASELINE config's generator, reduced m/s, bitwise vs the oracle."""
+    scale, chunks = CONFIG_SCALE[key]
+    w = synthetic.scaled(synthetic.CONFIGS[key], scale, chunks)
+    X = synthetic.generate(key, w.m)
+    out, trace = bm.big_means(bm.Dataset(X), cfg(w.k, w.s, w.chunks, seed=w.seed))
+    p = port.big_means(X.astype(np.float64), w.k, w.s, w.chunks, seed=w.seed)
+    got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+            r.degenerate_repaired) for r in trace.records]
+    assert got == p.trace
+    assert out.objective == p.objective
+    assert (bits(out.centroids.values) == bits(p.centroids)).all()
+    assert (out.assignment == p.labels).all()
+    assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)

@@ -1,0 +1,125 @@
+"""GPU parity: core kernels (core.cpp) — known answers from the reference's
+test_core.cpp plus bitwise agreement with the golden vectors / oracle."""
+import numpy as np
+import pytest
+
+import paper_2204_07485_b200 as bm
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+
+def test_dataset_validates_shape_and_finiteness():  # test_core.cpp:27-37
+    with pytest.raises(bm.ConfigError):
+        bm.Dataset([1.0, 2.0, 3.0], 2, 2)
+    with pytest.raises(bm.ConfigError):
+        bm.Dataset([1.0, np.nan], 1, 2)
+    with pytest.raises(bm.ConfigError):
+        bm.Dataset([np.inf], 1, 1)
+    with pytest.raises(bm.ConfigError):
+        bm.Dataset(np.array([[1.0, np.inf]], np.float32))
+    d = bm.Dataset([1.0, 2.0, 3.0, 4.0], 2, 2)
+    assert (d.m, d.n) == (2, 2)
+    v = d.values()
+    assert v[1, 0] == 3.0 and v[1, 1] == 4.0
+
+
+def test_gather_copies_rows_in_listed_order():  # test_core.cpp:39-45
+    d = bm.Dataset([0.0, 1.0, 2.0, 3.0, 4.0, 5.0], 3, 2)
+    g = d.gather([2, 0])
+    assert g.m == 2
+    v = g.values()
+    assert v[0, 0] == 4.0 and v[1, 1] == 1.0
+    with pytest.raises(bm.ConfigError):
+        d.gather([3])
+
+
+def test_assign_nearest_ties_low():  # test_core.cpp:72-82
+    d = bm.Dataset([0.0, 0.0, 10.0, 0.0, 5.0, 0.0], 3, 2)
+    c = bm.Centroids.from_rows([0.0, 0.0, 10.0, 0.0], 2, 2)
+    counter = bm.EvalCounter()
+    labels, dists = bm.assign_nearest(d, c, counter)
+    assert labels.tolist() == [0, 1, 0]
+    assert dists[0] == 0.0 and dists[2] == 25.0
+    assert counter.distance_evals == 6
+
+
+def test_assign_nearest_skips_degenerate():  # test_core.cpp:84-95
+    d = bm.Dataset([0.0, 0.0, 10.0, 0.0], 2, 2)
+    c = bm.Centroids.all_degenerate(2, 2)
+    with pytest.raises(bm.StateError):
+        bm.assign_nearest(d, c)
+    c.set_row(1, [10.0, 0.0])
+    counter = bm.EvalCounter()
+    labels, _ = bm.assign_nearest(d, c, counter)
+    assert labels.tolist() == [1, 1]
+    assert counter.distance_evals == 2
+
+
+def test_update_centroids_means_and_empty():  # test_core.cpp:97-108
+    d = bm.Dataset([0.0, 0.0, 2.0, 0.0, 0.0, 4.0], 3, 2)
+    c = bm.update_centroids(d, [0, 0, 2], 3)
+    assert c.row(0)[0] == 1.0 and c.row(0)[1] == 0.0
+    assert c.degenerate(1)
+    assert c.row(2)[1] == 4.0
+    with pytest.raises(bm.ConfigError):
+        bm.update_centroids(d, [0, 0, 3], 3)
+
+
+def test_objective_equals_summed_distances():  # test_core.cpp:110-119
+    X = np.random.default_rng(7).uniform(-10, 10, (257, 3))
+    d = bm.Dataset(X)
+    c = bm.Centroids.from_rows(np.stack([X[0], X[9]]))
+    _, dists = bm.assign_nearest(d, c)
+    assert bm.objective(d, c) == pytest.approx(dists.sum(), rel=1e-12)
+
+
+def test_core_golden_bitwise(golden):
+    d = bm.Dataset(golden["core_X"])
+    c = bm.Centroids(golden["core_C"], golden["core_mask"])
+    counter = bm.EvalCounter()
+    labels, dists = bm.assign_nearest(d, c, counter)
+    assert (labels == golden["core_labels"]).all()
+    assert (bits(dists) == bits(golden["core_dists"])).all()
+    assert counter.distance_evals == int(golden["core_evals"][0])
+    assert bm.objective(d, c) == golden["core_block_sum"][0]
+    u = bm.update_centroids(d, labels, 4)
+    assert (bits(u.values) == bits(golden["core_update_C"])).all()
+    assert (u.mask == golden["core_update_mask"]).all()
+
+
+def test_block_sum_golden(golden):  # test_core.cpp:121-136
+    assert bm.block_sum(golden["blocksum_values"]) == golden["blocksum_total"][0]
+    assert bm.block_sum(np.zeros(0)) == 0.0
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("n,k", [(1, 1), (2, 3), (16, 10), (28, 20), (68, 25), (70, 33), (300, 7)])
+def test_assign_update_bitwise_vs_oracle(port, n, k, dtype):
+    rng = np.random.default_rng(n * 100 + k)
+    m = 3 * 1024 + 77
+    X = (rng.normal(size=(m, n)) * 3).astype(dtype)
+    Xd = X.astype(np.float64)
+    C = Xd[rng.choice(m, k, replace=False)] + 0.25
+    mask = (rng.random(k) < 0.2).astype(np.uint8)
+    mask[0] = 0
+    d = bm.Dataset(X)
+    cent = bm.Centroids(C, mask)
+    labels, dists = bm.assign_nearest(d, cent)
+    l2, d2, _ = port.assign_nearest(Xd, cent.values, mask)
+    assert (labels == l2).all()
+    assert (bits(dists) == bits(d2)).all()
+    u = bm.update_centroids(d, l2, k)
+    uc, um = port.update_centroids(Xd, l2, k)
+    assert (bits(u.values) == bits(uc)).all() and (u.mask == um).all()
+
+
+def test_integer_data_exact_ties(port):
+    """Integer-valued data (config 2 style) produces many exact distance ties."""
+    rng = np.random.default_rng(3)
+    X = rng.integers(0, 4, (5000, 3)).astype(np.float64)
+    C = np.array([[1, 1, 1], [2, 2, 2], [1, 1, 1], [0, 2, 1], [2, 0, 1]], np.float64)
+    mask = np.zeros(5, np.uint8)
+    labels, dists = bm.assign_nearest(bm.Dataset(X), bm.Centroids(C, mask))
+    l2, d2, _ = port.assign_nearest(X, C, mask)
+    assert (labels == l2).all() and (bits(dists) == bits(d2)).all()
