@@ -264,9 +264,9 @@ k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     const int tid = threadIdx.x, pg = tid % kAPG, cg = tid / kAPG;
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
 
-    if (tid < kABP) {
-        best_d[tid] = __longlong_as_double(0x7FF0000000000000LL);  // +inf
-        best_j[tid] = -1;
+    for (int p = tid; p < kABP; p += blockDim.x) {
+        best_d[p] = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+        best_j[p] = -1;
     }
     for (int kb = 0; kb < KA; kb += KB) {
         double acc[kAP][kAK];
@@ -322,27 +322,27 @@ k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         }
         __syncthreads();
         // ... then across centroid groups in ascending order (first minimum wins).
-        if (tid < kABP) {
-            double b = best_d[tid];
-            int bj = best_j[tid];
+        for (int p = tid; p < kABP; p += blockDim.x) {
+            double b = best_d[p];
+            int bj = best_j[p];
             for (int g = 0; g < KG; ++g) {
-                if (red_j[g][tid] >= 0 && red_d[g][tid] < b) {
-                    b = red_d[g][tid];
-                    bj = red_j[g][tid];
+                if (red_j[g][p] >= 0 && red_d[g][p] < b) {
+                    b = red_d[g][p];
+                    bj = red_j[g][p];
                 }
             }
-            best_d[tid] = b;
-            best_j[tid] = bj;
+            best_d[p] = b;
+            best_j[p] = bj;
         }
         __syncthreads();
     }
-    if (tid < kABP) {
-        const uint64_t gp = p0 + tid;
+    for (int p = tid; p < kABP; p += blockDim.x) {
+        const uint64_t gp = p0 + p;
         if (gp < rows) {
-            const int bj = best_j[tid];
+            const int bj = best_j[p];
             const int label = bj >= 0 ? act_idx[bj] : -1;
             labels_out[gp] = label;
-            if (dists_out) dists_out[gp] = best_d[tid];
+            if (dists_out) dists_out[gp] = best_d[p];
             if (labels_old && labels_old[gp] != label) *changed_flag = 1;
         }
     }
