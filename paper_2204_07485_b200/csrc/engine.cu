@@ -261,29 +261,40 @@ Workspace& get_ws(bm_dataset* d, uint64_t rows, int k, int ncand, uint64_t hist)
 // Kernel launch wrappers
 // ---------------------------------------------------------------------------
 struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    std::vector<cudaEvent_t> pool;  // reused across calls: no per-launch creation
+    size_t used = 0;
     std::vector<uint64_t> rows;
     std::vector<int> final_flag;
     cudaStream_t stream = nullptr;
-    void begin(cudaStream_t s) { stream = s; }
+    void begin(cudaStream_t s) {
+        stream = s;
+        used = 0;
+        rows.clear();
+        final_flag.clear();
+    }
+    cudaEvent_t next() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            BM_CUDA(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
     std::pair<cudaEvent_t, cudaEvent_t> record_start() {
-        cudaEvent_t a, b;
-        BM_CUDA(cudaEventCreate(&a));
-        BM_CUDA(cudaEventCreate(&b));
+        cudaEvent_t a = next(), b = next();
         BM_CUDA(cudaEventRecord(a, stream));
         return {a, b};
     }
     void record_end(std::pair<cudaEvent_t, cudaEvent_t> p, uint64_t r, bool fin) {
         BM_CUDA(cudaEventRecord(p.second, stream));
-        evs.push_back(p);
         rows.push_back(r);
         final_flag.push_back(fin);
     }
     void flush(bm_profile& out) {
-        for (size_t i = 0; i < evs.size(); ++i) {
+        for (size_t i = 0; i < rows.size(); ++i) {
             float ms = 0;
-            BM_CUDA(cudaEventSynchronize(evs[i].second));
-            BM_CUDA(cudaEventElapsedTime(&ms, evs[i].first, evs[i].second));
+            BM_CUDA(cudaEventSynchronize(pool[2 * i + 1]));
+            BM_CUDA(cudaEventElapsedTime(&ms, pool[2 * i], pool[2 * i + 1]));
             if (final_flag[i]) {
                 out.final_ms += ms;
                 out.final_rows += rows[i];
@@ -292,10 +303,8 @@ struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
                 out.assign_launches += 1;
                 out.assign_rows_total += rows[i];
             }
-            cudaEventDestroy(evs[i].first);
-            cudaEventDestroy(evs[i].second);
         }
-        evs.clear();
+        used = 0;
         rows.clear();
         final_flag.clear();
     }
