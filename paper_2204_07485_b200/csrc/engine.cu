@@ -126,6 +126,7 @@ struct Workspace {
     DevBuf<int32_t> labels;  // 2 * R (ping-pong)
     DevBuf<double> dists;    // R
     DevBuf<double> tile_buf; // max(ncand,1) * tiles
+    DevBuf<unsigned> tile_ctr;  // tiles (fused tile-fold arrival counters)
     DevBuf<double> psum;     // tiles * k * n
     DevBuf<uint32_t> pcnt;   // tiles * k
     DevBuf<double> C, Cact;  // k * n
@@ -156,6 +157,8 @@ struct Workspace {
         labels.alloc(2 * R);
         dists.alloc(R);
         tile_buf.alloc(tiles * ncand);
+        tile_ctr.alloc(tiles);
+        if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
         psum.alloc(tiles * (uint64_t)k * n);
         pcnt.alloc(tiles * (uint64_t)k);
         C.alloc((uint64_t)k * n);
@@ -219,41 +222,81 @@ struct SamplerWs {
 
 }  // namespace bm
 
-// Device-resident immutable dataset (Dataset core.hpp:13-37).
+// Device-resident immutable dataset (Dataset core.hpp:13-37).  Immutable and
+// shareable: all per-run state lives in the calling thread's DeviceCache.
 struct bm_dataset {
     int device = 0;
     uint64_t m = 0, n = 0, ld = 0;
     bm_dtype dtype = BM_F64;
     void* X = nullptr;
-    cudaStream_t stream = nullptr;
-    std::map<std::tuple<uint64_t, int, int, uint64_t>, std::unique_ptr<bm::Workspace>> ws;
-    std::map<uint64_t, std::unique_ptr<bm::SamplerWs>> sws;
-    bm::DevBuf<uint8_t> chunk;  // gathered chunk, s * ld * elem
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t stream = nullptr;  // upload / download only
     ~bm_dataset() {
-        ws.clear();
-        sws.clear();
-        chunk.release();
-        if (ev0) cudaEventDestroy(ev0);
-        if (ev1) cudaEventDestroy(ev1);
         if (X) cudaFree(X);
         if (stream) cudaStreamDestroy(stream);
     }
 };
 
 namespace bm {
+
+// Per (host thread, device) workspaces and stream: one host thread drives one
+// chain per device, several threads may share one dataset.
+struct DeviceCache {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::map<std::tuple<uint64_t, int, int, int, uint64_t>, std::unique_ptr<Workspace>> ws;
+    std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SamplerWs>> sws;
+    DevBuf<uint8_t> chunk;        // gathered chunk, s * ld * elem
+    DevBuf<int32_t> flabels;      // final pass
+    DevBuf<double> fdists, ftiles;
+    DevBuf<unsigned> fctr;
+    ~DeviceCache() {
+        ws.clear();
+        sws.clear();
+        if (stream) cudaStreamDestroy(stream);
+    }
+    void ensure_final(uint64_t rows) {
+        if (flabels.n < rows) flabels.alloc(rows);
+        if (fdists.n < rows) fdists.alloc(rows);
+        const uint64_t t = tiles_of(rows);
+        if (ftiles.n < t) ftiles.alloc(t);
+        if (fctr.n < t) {
+            fctr.alloc(t);
+            BM_CUDA(cudaMemset(fctr.p, 0, t * sizeof(unsigned)));
+        }
+    }
+};
+
+thread_local std::map<int, std::unique_ptr<DeviceCache>> t_cache;
+
+DeviceCache& cache_of(int device) {
+    auto it = t_cache.find(device);
+    if (it != t_cache.end()) return *it->second;
+    auto c = std::make_unique<DeviceCache>();
+    c->device = device;
+    BM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    auto& ref = *c;
+    t_cache.emplace(device, std::move(c));
+    return ref;
+}
+
+cudaStream_t stream_of(const bm_dataset* d) { return cache_of(d->device).stream; }
+
+}  // namespace bm
+
+namespace bm {
 namespace {
 
 Points dataset_points(const bm_dataset* d) { return Points{d->X, d->dtype, d->m, (int)d->n, d->ld}; }
 
-Workspace& get_ws(bm_dataset* d, uint64_t rows, int k, int ncand, uint64_t hist) {
-    auto key = std::make_tuple(rows, k, std::max(ncand, 1), hist);
-    auto it = d->ws.find(key);
-    if (it != d->ws.end()) return *it->second;
+Workspace& get_ws(const bm_dataset* d, uint64_t rows, int k, int ncand, uint64_t hist) {
+    DeviceCache& c = cache_of(d->device);
+    auto key = std::make_tuple(rows, k, (int)d->n, std::max(ncand, 1), hist);
+    auto it = c.ws.find(key);
+    if (it != c.ws.end()) return *it->second;
     auto w = std::make_unique<Workspace>();
     w->init(rows, k, (int)d->n, ncand, hist);
     auto& ref = *w;
-    d->ws.emplace(key, std::move(w));
+    c.ws.emplace(key, std::move(w));
     return ref;
 }
 
@@ -318,31 +361,83 @@ int assign_threads(int k) {
     return dev::kAPG * kg;
 }
 
+// fp32 value of x rounded toward -inf / +inf (host-side constant setup)
+float f_rd(double x) {
+    float f = (float)x;
+    if ((double)f > x) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+float f_ru(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+dev::ScreenConsts screen_consts(int n) {
+    const double u = std::ldexp(1.0, -24);
+    const double gn = n * u / (1.0 - n * u);
+    const double u64 = std::ldexp(1.0, -53);
+    const double g64 = (n + 3) * u64 / (1.0 - (n + 3) * u64);
+    dev::ScreenConsts c;
+    c.inv_1p_gn_rd = f_rd(1.0 / (1.0 + gn) * (1.0 - 4 * u64));
+    c.inv_1m_gn_ru = f_ru(1.0 / (1.0 - gn) * (1.0 + 4 * u64));
+    c.inv_1pu_rd = f_rd(1.0 / (1.0 + u) * (1.0 - 4 * u64));
+    c.inv_1mu_ru = f_ru(1.0 / (1.0 - u) * (1.0 + 4 * u64));
+    c.w_scale = f_ru(u * (1.0 + 4 * u) / (1.0 - u) * (1.0 + 4 * u64));
+    c.w_abs = std::ldexp(1.0f, -60);
+    c.lo64 = f_rd((1.0 - g64) * (1.0 - 4 * u64));
+    c.hi64 = f_ru((1.0 + g64) * (1.0 + 4 * u64));
+    return c;
+}
+
+// BM_ASSIGN_MODE=exact forces the unscreened kernel (A/B parity checks).
+bool screen_enabled(int k) {
+    static const bool exact_forced = [] {
+        const char* e = std::getenv("BM_ASSIGN_MODE");
+        return e && std::string(e) == "exact";
+    }();
+    return !exact_forced && k <= dev::kSMaxK;
+}
+
+void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t stride, int narrays,
+                      double* tiles, const int* stop);
+
 // assign_nearest over P with the compacted centroids of ws (Cact/act/n_active).
+// With tile_out the per-1024-row tile partials of the distances are produced
+// too (fused into the screened kernel; a separate fold after the exact one).
 void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_t* labels_pair,
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
-                   const int* stop, bool final_pass = false) {
+                   const int* stop, bool final_pass = false, double* tile_out = nullptr,
+                   unsigned* tile_ctr = nullptr) {
     const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
     if (grid == 0) return;
     std::pair<cudaEvent_t, cudaEvent_t> ev{};
     if (g_profiling) ev = g_prof.record_start();
+    const bool screen = screen_enabled(k);
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
-        dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
-            static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
-            labels_pair, pair_stride, parity, dists, changed, stop);
+        if (screen) {
+            dev::k_assign_screen<T><<<grid, assign_threads(k), 0, st>>>(
+                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
+                labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
+                screen_consts(P.n));
+        } else {
+            dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
+                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
+                labels_pair, pair_stride, parity, dists, changed, stop);
+        }
     });
     BM_LAUNCH();
     count_launch();
     if (g_profiling) g_prof.record_end(ev, P.rows, final_pass);
+    if (tile_out && !screen) launch_tile_sums(st, dists, P.rows, 0, 1, tile_out, stop);
 }
 
 void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t stride, int narrays,
                       double* tiles, const int* stop) {
-    const uint64_t warps = tiles_of(count) * narrays;
-    const unsigned grid = (unsigned)ceil_div(warps * 32, 256);
-    if (grid == 0) return;
-    dev::k_tile_sums<<<grid, 256, 0, st>>>(v, count, stride, narrays, tiles, stop);
+    const uint64_t blocks = tiles_of(count) * narrays;
+    if (blocks == 0) return;
+    dev::k_tile_sums<<<(unsigned)blocks, 256, 0, st>>>(v, count, stride, narrays, tiles, stop);
     BM_LAUNCH();
     count_launch();
 }
@@ -394,8 +489,8 @@ struct LloydResult {
 
 void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w) {
     launch_compact(st, w, w.C.p, w.mask.p);
-    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr);  // :26
-    launch_tile_sums(st, w.dists.p, P.rows, 0, 1, w.tile_buf.p, nullptr);              // :27
+    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr, false,
+                  w.tile_buf.p, w.tile_ctr.p);  // :26-27
     dev::k_lloyd_begin<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows,
                                          w.hist_cap ? w.history.p : nullptr);
     BM_LAUNCH();
@@ -406,8 +501,8 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
     const int* parity = &w.status.p->parity;
     const int* stop = &w.status.p->stop;
     launch_update(st, P, w, parity, stop);                                                 // :33
-    launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop);  // :34
-    launch_tile_sums(st, w.dists.p, P.rows, 0, 1, w.tile_buf.p, stop);                    // :35
+    launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop, false,
+                  w.tile_buf.p, w.tile_ctr.p);  // :34-35
     dev::k_lloyd_step<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows, max_it,
                                         tol, w.hist_cap ? w.history.p : nullptr);
     BM_LAUNCH();
@@ -571,13 +666,15 @@ void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::v
 // ---------------------------------------------------------------------------
 // Sampling (sample_chunk big_means.cpp:39-56): host draws, device resolution.
 // ---------------------------------------------------------------------------
-SamplerWs& get_sws(bm_dataset* d, uint64_t s) {
-    auto it = d->sws.find(s);
-    if (it != d->sws.end()) return *it->second;
+SamplerWs& get_sws(const bm_dataset* d, uint64_t s) {
+    DeviceCache& c = cache_of(d->device);
+    auto key = std::make_pair(d->m, s);
+    auto it = c.sws.find(key);
+    if (it != c.sws.end()) return *it->second;
     auto w = std::make_unique<SamplerWs>();
     w->init(d->m, s);
     auto& ref = *w;
-    d->sws.emplace(s, std::move(w));
+    c.sws.emplace(key, std::move(w));
     return ref;
 }
 
@@ -621,7 +718,7 @@ void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
     count_launch(6);
 }
 
-void enqueue_gather(cudaStream_t st, bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
+void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
     const uint64_t row_vecs = d->ld * dtype_size(d->dtype) / 16;
     const unsigned grid = (unsigned)ceil_div((uint64_t)s * 32, 256);
     dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X), row_vecs, idx, s,
@@ -651,17 +748,18 @@ void validate(const bm_dataset* d, const bm_config& c) {
 // ---------------------------------------------------------------------------
 // Final pass: assign all rows [r0, r1) + per-tile partials (big_means.cpp:102-107)
 // ---------------------------------------------------------------------------
-void final_pass(cudaStream_t st, bm_dataset* d, Workspace& w, uint64_t r0, uint64_t r1, int32_t* labels_host,
-                double* tiles_host, uint64_t* evals, DevBuf<int32_t>& dlabels, DevBuf<double>& ddists,
-                DevBuf<double>& dtiles) {
+void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0, uint64_t r1,
+                int32_t* labels_host, double* tiles_host, uint64_t* evals) {
+    DeviceCache& c = cache_of(d->device);
     Points P = dataset_points(d);
     P.X = static_cast<const uint8_t*>(d->X) + r0 * d->ld * dtype_size(d->dtype);
     P.rows = r1 - r0;
-    launch_assign(st, P, w, w.k, dlabels.p, 0, nullptr, ddists.p, nullptr, nullptr, true);
-    launch_tile_sums(st, ddists.p, P.rows, 0, 1, dtiles.p, nullptr);
-    BM_CUDA(cudaMemcpyAsync(tiles_host, dtiles.p, tiles_of(P.rows) * sizeof(double), cudaMemcpyDeviceToHost, st));
+    c.ensure_final(P.rows);
+    launch_assign(st, P, w, w.k, c.flabels.p, 0, nullptr, c.fdists.p, nullptr, nullptr, true, c.ftiles.p,
+                  c.fctr.p);
+    BM_CUDA(cudaMemcpyAsync(tiles_host, c.ftiles.p, tiles_of(P.rows) * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (labels_host)
-        BM_CUDA(cudaMemcpyAsync(labels_host, dlabels.p, P.rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(labels_host, c.flabels.p, P.rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaStreamSynchronize(st));
     if (w.h_status.p->n_active == 0) throw StateError("assign_nearest: every centroid is degenerate");
@@ -671,11 +769,12 @@ void final_pass(cudaStream_t st, bm_dataset* d, Workspace& w, uint64_t r0, uint6
 // ---------------------------------------------------------------------------
 // big_means (big_means.cpp:58-112)
 // ---------------------------------------------------------------------------
-void big_means(bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_record* trace,
+void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_record* trace,
                uint64_t trace_cap) {
     validate(d, cfg);
     DeviceGuard g(d->device);
-    cudaStream_t st = d->stream;
+    DeviceCache& dc = cache_of(d->device);
+    cudaStream_t st = dc.stream;
     const uint64_t m = d->m, s = cfg.chunk_size;
     const int k = (int)cfg.k, n = (int)d->n;
     g_profile = bm_profile{};  // launch counts always; event timing only when profiling
@@ -689,8 +788,8 @@ void big_means(bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_re
         chunkP = dataset_points(d);
     } else {
         const size_t bytes = s * d->ld * dtype_size(d->dtype);
-        if (d->chunk.n < bytes) d->chunk.alloc(bytes);
-        chunkP.X = d->chunk.p;
+        if (dc.chunk.n < bytes) dc.chunk.alloc(bytes);
+        chunkP.X = dc.chunk.p;
     }
     // incumbent: all degenerate, f_opt = +inf (:63-64)
     BM_CUDA(cudaMemsetAsync(w.Cinc.p, 0, (size_t)k * n * sizeof(double), st));
@@ -714,7 +813,7 @@ void big_means(bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_re
             if (!have_next) draw_targets(*sw, rng);
             have_next = false;
             enqueue_resolve(st, *sw);
-            enqueue_gather(st, d, sw->idx.p, (uint32_t)s, d->chunk.p);  // :80
+            enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);  // :80
         }
         // start = incumbent (:82), repaired = degenerate_count (:83)
         BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -773,10 +872,8 @@ void big_means(bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_re
         const auto t_full = std::chrono::steady_clock::now();
         Workspace& fw = get_ws(d, 0, k, 1, 0);  // centroid state only
         launch_compact(st, fw, w.Cinc.p, w.maskinc.p);
-        DevBuf<int32_t> dl(m);
-        DevBuf<double> dd(m), dt(tiles_of(m));
         std::vector<double> tiles(tiles_of(m));
-        final_pass(st, d, fw, 0, m, out->labels, tiles.data(), &evals, dl, dd, dt);
+        final_pass(st, d, fw, 0, m, out->labels, tiles.data(), &evals);
         double total = 0.0;  // block_sum outer fold (core.cpp:172)
         for (double t : tiles) total += t;
         out->objective = total;
@@ -972,10 +1069,10 @@ bm_status bm_sample_chunk(const bm_dataset* dc, uint64_t s, bm_rng* rng, uint64_
         DeviceGuard g(d->device);
         SamplerWs& sw = get_sws(d, s);
         draw_targets(sw, rng->eng);
-        enqueue_resolve(d->stream, sw);
+        enqueue_resolve(stream_of(d), sw);
         std::vector<uint32_t> tmp(s);
-        BM_CUDA(cudaMemcpyAsync(tmp.data(), sw.idx.p, s * sizeof(uint32_t), cudaMemcpyDeviceToHost, d->stream));
-        BM_CUDA(cudaStreamSynchronize(d->stream));
+        BM_CUDA(cudaMemcpyAsync(tmp.data(), sw.idx.p, s * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_of(d)));
+        BM_CUDA(cudaStreamSynchronize(stream_of(d)));
         for (uint64_t i = 0; i < s; ++i) out[i] = tmp[i];
     });
 }
@@ -987,18 +1084,18 @@ bm_status bm_assign_nearest(const bm_dataset* dc, const double* C, const uint8_t
         if (k < 1) throw ConfigError("centroids must have at least one row and one column");
         DeviceGuard g(d->device);
         Workspace& w = get_ws(d, 0, (int)k, 1, 0);
-        upload_centroids(d->stream, w, C, mask);
-        launch_compact(d->stream, w, w.C.p, w.mask.p);
+        upload_centroids(stream_of(d), w, C, mask);
+        launch_compact(stream_of(d), w, w.C.p, w.mask.p);
         DevBuf<int32_t> dl(d->m);
         DevBuf<double> dd(d->m);
         Points P = dataset_points(d);
-        launch_assign(d->stream, P, w, (int)k, dl.p, 0, nullptr, dd.p, nullptr, nullptr);
-        BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, d->stream));
-        BM_CUDA(cudaStreamSynchronize(d->stream));
+        launch_assign(stream_of(d), P, w, (int)k, dl.p, 0, nullptr, dd.p, nullptr, nullptr);
+        BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, stream_of(d)));
+        BM_CUDA(cudaStreamSynchronize(stream_of(d)));
         if (w.h_status.p->n_active == 0) throw StateError("assign_nearest: every centroid is degenerate");
-        BM_CUDA(cudaMemcpyAsync(labels, dl.p, d->m * sizeof(int32_t), cudaMemcpyDeviceToHost, d->stream));
-        if (dists) BM_CUDA(cudaMemcpyAsync(dists, dd.p, d->m * sizeof(double), cudaMemcpyDeviceToHost, d->stream));
-        BM_CUDA(cudaStreamSynchronize(d->stream));
+        BM_CUDA(cudaMemcpyAsync(labels, dl.p, d->m * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_of(d)));
+        if (dists) BM_CUDA(cudaMemcpyAsync(dists, dd.p, d->m * sizeof(double), cudaMemcpyDeviceToHost, stream_of(d)));
+        BM_CUDA(cudaStreamSynchronize(stream_of(d)));
         if (evals) *evals += d->m * (uint64_t)w.h_status.p->n_active;
     });
 }
@@ -1014,12 +1111,9 @@ bm_status bm_assign_rows(const bm_dataset* dc, const double* C, const uint8_t* m
         if (row_begin == row_end) return;
         DeviceGuard g(d->device);
         Workspace& w = get_ws(d, 0, (int)k, 1, 0);
-        upload_centroids(d->stream, w, C, mask);
-        launch_compact(d->stream, w, w.C.p, w.mask.p);
-        const uint64_t r = row_end - row_begin;
-        DevBuf<int32_t> dl(r);
-        DevBuf<double> dd(r), dt(tiles_of(r));
-        final_pass(d->stream, d, w, row_begin, row_end, labels, tile_partials, evals, dl, dd, dt);
+        upload_centroids(stream_of(d), w, C, mask);
+        launch_compact(stream_of(d), w, w.C.p, w.mask.p);
+        final_pass(stream_of(d), d, w, row_begin, row_end, labels, tile_partials, evals);
     });
 }
 
@@ -1064,7 +1158,7 @@ bm_status bm_update_centroids(const bm_dataset* dc, const int32_t* labels, uint6
             if (labels[i] < 0 || (uint64_t)labels[i] >= k) throw ConfigError("update_centroids: label out of range");
         DeviceGuard g(d->device);
         Workspace& w = get_ws(d, d->m, (int)k, 1, 0);
-        cudaStream_t st = d->stream;
+        cudaStream_t st = stream_of(d);
         BM_CUDA(cudaMemcpyAsync(w.labels.p, labels, d->m * sizeof(int32_t), cudaMemcpyHostToDevice, st));
         launch_update(st, dataset_points(d), w, nullptr, nullptr);
         BM_CUDA(cudaMemcpyAsync(C, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1080,13 +1174,13 @@ bm_status bm_kmeanspp_fill(const bm_dataset* dc, double* C, uint8_t* mask, uint6
         if (candidates < 1) throw ConfigError("kmeanspp_fill: candidates_per_step must be at least 1");
         DeviceGuard g(d->device);
         Workspace& w = get_ws(d, d->m, (int)k, candidates, 0);
-        upload_centroids(d->stream, w, C, mask);
+        upload_centroids(stream_of(d), w, C, mask);
         std::vector<uint8_t> hmask(mask, mask + k);
         uint64_t ev = 0;
-        kmeanspp_fill_device(d->stream, dataset_points(d), w, hmask, candidates, rng->eng, ev);
-        BM_CUDA(cudaMemcpyAsync(C, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, d->stream));
-        BM_CUDA(cudaMemcpyAsync(mask, w.mask.p, k, cudaMemcpyDeviceToHost, d->stream));
-        BM_CUDA(cudaStreamSynchronize(d->stream));
+        kmeanspp_fill_device(stream_of(d), dataset_points(d), w, hmask, candidates, rng->eng, ev);
+        BM_CUDA(cudaMemcpyAsync(C, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, stream_of(d)));
+        BM_CUDA(cudaMemcpyAsync(mask, w.mask.p, k, cudaMemcpyDeviceToHost, stream_of(d)));
+        BM_CUDA(cudaStreamSynchronize(stream_of(d)));
         if (evals) *evals += ev;
     });
 }
@@ -1100,7 +1194,7 @@ bm_status bm_lloyd(const bm_dataset* dc, double* C, uint8_t* mask, uint64_t k, u
         if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
         DeviceGuard g(d->device);
         Workspace& w = get_ws(d, d->m, (int)k, 1, max_iterations + 1);
-        cudaStream_t st = d->stream;
+        cudaStream_t st = stream_of(d);
         upload_centroids(st, w, C, mask);
         LloydResult r = lloyd_run(st, dataset_points(d), w, max_iterations, rel_tolerance);
         const uint64_t hl = r.iterations + 1;
@@ -1128,7 +1222,7 @@ bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uin
         if (max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
         if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
         DeviceGuard g(d->device);
-        cudaStream_t st = d->stream;
+        cudaStream_t st = stream_of(d);
         Workspace& w = get_ws(d, d->m, (int)k, candidates, 0);
         std::mt19937_64 rng(seed);  // local_search.cpp:69
         const auto t_init = std::chrono::steady_clock::now();

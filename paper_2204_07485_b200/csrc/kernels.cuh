@@ -349,28 +349,249 @@ k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
 }
 
 // ===========================================================================
+// 3b. Screened exact assignment (same results as k_assign, bit for bit).
+//
+// Screen: every (point, active centroid) distance is approximated in fp32 by
+// the direct form  d~ = sum_d fl(fl32(x_d) - fl32(c_d))^2  (FFMA chain), and
+// turned into CERTIFIED bounds L <= d_ref <= U on the reference's fp64 value
+// d_ref (core.cpp:142-146) with directed-rounding fp32 arithmetic:
+//   r = ||x - c|| lies in [ sqrt(d~/(1+g_n))/(1+u) - w , sqrt(d~/(1-g_n))/(1-u) + w ]
+//   w = u (||x|| + ||c||) + 2^-60   (fp32 rounding of the inputs, incl. subnormals)
+//   d_ref in [ r^2 (1-g64), r^2 (1+g64) ]   (reference's own rounding, g64 = gamma_{n+3})
+// with u = 2^-24, g_n = n u/(1-n u).  Any centroid whose L exceeds the point's
+// smallest U cannot be the reference's minimum (nor tie with it), so only the
+// candidates L_j <= min_i U_i are recomputed exactly in fp64 (direct form,
+// strict <, ascending j) — reproducing assign_nearest exactly.
+// Non-finite fp32 intermediates (inputs beyond fp32 range) force L=0, U=inf.
+//
+// Fused per-1024-point tile sums (block_sum inner loop core.cpp:167-173): the
+// last CTA to finish a tile folds the tile's distances in index order.
+// ===========================================================================
+struct ScreenConsts {
+    float inv_1p_gn_rd;  // 1/(1+g_n), rounded down
+    float inv_1m_gn_ru;  // 1/(1-g_n), rounded up
+    float inv_1pu_rd;    // 1/(1+u),   rounded down
+    float inv_1mu_ru;    // 1/(1-u),   rounded up
+    float w_scale;       // u(1+4u)/(1-u), rounded up
+    float w_abs;         // 2^-60
+    float lo64;          // 1-g64, rounded down
+    float hi64;          // 1+g64, rounded up
+};
+
+constexpr int kSMaxK = 32;  // centroids handled by the screened path
+
+template <typename T>
+__global__ void __launch_bounds__(kAPG * kAMaxCG)
+k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+                const double* __restrict__ Cact, const int* __restrict__ act_idx,
+                const int* __restrict__ n_active_ptr,
+                int32_t* __restrict__ labels_pair, uint64_t pair_stride,
+                const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
+                int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
+                double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
+                ScreenConsts cst) {
+    __shared__ float xs[kADC][kABP + 4];
+    __shared__ float cs[kADC][kSMaxK];
+    __shared__ __align__(16) float Ls[kSMaxK * kABP];  // [j][p]; reused for the tile fold
+    __shared__ float red_u[kAMaxCG][kABP];
+    __shared__ float umin[kABP];
+    __shared__ int is_last;
+
+    if (stop_ptr && *stop_ptr) return;
+    const int KA = *n_active_ptr;
+    int32_t* labels_out = labels_pair;
+    const int32_t* labels_old = nullptr;
+    if (parity_ptr) {
+        const int par = *parity_ptr;
+        labels_out = labels_pair + (1 - par) * pair_stride;
+        labels_old = labels_pair + par * pair_stride;
+    }
+    const int KG = blockDim.x / kAPG;
+    const int tid = threadIdx.x, pg = tid % kAPG, cg = tid / kAPG;
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
+    const float finf = __int_as_float(0x7F800000);
+
+    float acc[kAP][kAK], xn[kAP], cn[kAK];
+#pragma unroll
+    for (int t = 0; t < kAP; ++t) {
+        xn[t] = 0.f;
+#pragma unroll
+        for (int u = 0; u < kAK; ++u) acc[t][u] = 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kAK; ++u) cn[u] = 0.f;
+
+    for (int d0 = 0; d0 < n; d0 += kADC) {
+        const int dl = min(kADC, n - d0);
+        __syncthreads();
+        for (int e = tid; e < kABP * kADC; e += blockDim.x) {
+            const int p = e / kADC, d = e % kADC;
+            const uint64_t gp = p0 + p;
+            float v = 0.f;
+            if (gp < rows && d < dl) v = static_cast<float>(X[gp * ld + d0 + d]);  // rn
+            xs[d][p] = v;
+        }
+        for (int e = tid; e < kSMaxK * kADC; e += blockDim.x) {
+            const int j = e / kADC, d = e % kADC;
+            float v = 0.f;
+            if (j < KA && d < dl) v = __double2float_rn(Cact[static_cast<uint64_t>(j) * n + d0 + d]);
+            cs[d][j] = v;
+        }
+        __syncthreads();
+        if (cg * kAK < KA) {
+#pragma unroll 4
+            for (int d = 0; d < dl; ++d) {
+                float xv[kAP], cv[kAK];
+#pragma unroll
+                for (int t = 0; t < kAP; ++t) xv[t] = xs[d][pg + kAPG * t];
+#pragma unroll
+                for (int u = 0; u < kAK; ++u) cv[u] = cs[d][cg * kAK + u];
+#pragma unroll
+                for (int t = 0; t < kAP; ++t) {
+                    xn[t] = __fmaf_ru(xv[t], xv[t], xn[t]);
+#pragma unroll
+                    for (int u = 0; u < kAK; ++u) {
+                        const float df = __fsub_rn(xv[t], cv[u]);
+                        acc[t][u] = __fmaf_rn(df, df, acc[t][u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kAK; ++u) cn[u] = __fmaf_ru(cv[u], cv[u], cn[u]);
+            }
+        }
+    }
+    // certified bounds
+    float un[kAP];
+#pragma unroll
+    for (int t = 0; t < kAP; ++t) un[t] = finf;
+    if (cg * kAK < KA) {
+        float cnorm[kAK];
+#pragma unroll
+        for (int u = 0; u < kAK; ++u) cnorm[u] = __fsqrt_ru(cn[u]);
+#pragma unroll
+        for (int t = 0; t < kAP; ++t) {
+            const float xnorm = __fsqrt_ru(xn[t]);
+#pragma unroll
+            for (int u = 0; u < kAK; ++u) {
+                const int j = cg * kAK + u;
+                if (j >= KA) continue;
+                const float dt = acc[t][u];
+                float L = 0.f, U = finf;
+                float w = __fadd_ru(__fmul_ru(__fadd_ru(xnorm, cnorm[u]), cst.w_scale), cst.w_abs);
+                if (dt <= 3.0e38f && w <= 1.0e18f) {
+                    float rlo = __fmul_rd(__fsqrt_rd(__fmul_rd(dt, cst.inv_1p_gn_rd)), cst.inv_1pu_rd);
+                    rlo = fmaxf(__fsub_rd(rlo, w), 0.f);
+                    float rhi = __fmul_ru(__fsqrt_ru(__fmul_ru(dt, cst.inv_1m_gn_ru)), cst.inv_1mu_ru);
+                    rhi = __fadd_ru(rhi, w);
+                    L = __fmul_rd(__fmul_rd(rlo, rlo), cst.lo64);
+                    U = __fmul_ru(__fmul_ru(rhi, rhi), cst.hi64);
+                }
+                Ls[j * kABP + pg + kAPG * t] = L;
+                un[t] = fminf(un[t], U);
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kAP; ++t) red_u[cg][pg + kAPG * t] = un[t];
+    __syncthreads();
+    for (int p = tid; p < kABP; p += blockDim.x) {
+        float m = finf;
+        for (int g = 0; g < KG; ++g) m = fminf(m, red_u[g][p]);
+        umin[p] = m;
+    }
+    __syncthreads();
+    // exact fp64 recheck of the candidates, ascending j, strict < (core.cpp:137-151)
+    for (int p = tid; p < kABP; p += blockDim.x) {
+        const uint64_t gp = p0 + p;
+        if (gp >= rows) continue;
+        const float um = umin[p];
+        const T* x = X + gp * ld;
+        double best = __longlong_as_double(0x7FF0000000000000LL);
+        int bj = -1;
+        for (int j = 0; j < KA; ++j) {
+            if (!(Ls[j * kABP + p] <= um)) continue;
+            const double* c = Cact + static_cast<uint64_t>(j) * n;
+            double sum = 0.0;
+            for (int d = 0; d < n; ++d) sum = dist_step(sum, to_f64(x[d]), c[d]);
+            if (sum < best) {
+                best = sum;
+                bj = j;
+            }
+        }
+        const int label = bj >= 0 ? act_idx[bj] : -1;
+        labels_out[gp] = label;
+        if (dists_out) dists_out[gp] = best;
+        if (labels_old && labels_old[gp] != label) *changed_flag = 1;
+    }
+    if (!tile_out) return;
+    // ---- fused tile fold: the last CTA of each 1024-point tile ----
+    __syncthreads();
+    const uint64_t tile = p0 / kTile;
+    if (tid == 0) {
+        __threadfence();
+        const uint64_t tb = tile * kTile;
+        const unsigned ctas = static_cast<unsigned>((min(rows, tb + kTile) - tb + kABP - 1) / kABP);
+        const unsigned old = atomicAdd(&tile_counter[tile], 1u);
+        is_last = old == ctas - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const uint64_t tb = tile * kTile;
+    const int len = static_cast<int>(min(rows, tb + kTile) - tb);
+    double* fold = reinterpret_cast<double*>(Ls);
+    for (int i = tid; i < len; i += blockDim.x) fold[i] = __ldcg(dists_out + tb + i);
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0;
+        int i = 0;
+        for (; i + 8 <= len; i += 8) {
+            const double2 v0 = *reinterpret_cast<const double2*>(fold + i);
+            const double2 v1 = *reinterpret_cast<const double2*>(fold + i + 2);
+            const double2 v2 = *reinterpret_cast<const double2*>(fold + i + 4);
+            const double2 v3 = *reinterpret_cast<const double2*>(fold + i + 6);
+            a = __dadd_rn(a, v0.x); a = __dadd_rn(a, v0.y);
+            a = __dadd_rn(a, v1.x); a = __dadd_rn(a, v1.y);
+            a = __dadd_rn(a, v2.x); a = __dadd_rn(a, v2.y);
+            a = __dadd_rn(a, v3.x); a = __dadd_rn(a, v3.y);
+        }
+        for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
+        tile_out[tile] = a;
+        tile_counter[tile] = 0u;  // ready for the next launch
+    }
+}
+
+// ===========================================================================
 // 4. Per-tile sequential sums (block_sum inner loop core.cpp:167-173).
 //    One warp per (array, tile); lanes stage 32 values, all lanes fold them in
 //    index order (redundantly), lane 0 writes.
 // ===========================================================================
 __global__ void k_tile_sums(const double* __restrict__ v, uint64_t count, uint64_t stride,
                             int narrays, double* __restrict__ tiles, const int* __restrict__ stop_ptr) {
+    // one CTA per (array, tile): coalesced staging, then a single-thread fold
+    __shared__ __align__(16) double sm[kTile];
     if (stop_ptr && *stop_ptr) return;
     const uint64_t ntiles = (count + kTile - 1) / kTile;
-    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= ntiles * narrays) return;
-    const uint64_t a = w / ntiles, t = w % ntiles;
-    const double* src = v + a * stride;
-    const uint64_t b = t * kTile, e = min(b + kTile, count);
+    const uint64_t a = blockIdx.x / ntiles, t = blockIdx.x % ntiles;
+    const double* src = v + a * stride + t * kTile;
+    const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), count - t * kTile));
+    for (int i = threadIdx.x; i < len; i += blockDim.x) sm[i] = src[i];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     double acc = 0.0;
-    for (uint64_t i0 = b; i0 < e; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const double x = i < e ? src[i] : 0.0;
-        const int cnt = static_cast<int>(min((uint64_t)32, e - i0));
-        for (int l = 0; l < cnt; ++l) acc = __dadd_rn(acc, __shfl_sync(0xFFFFFFFFu, x, l));
+    int i = 0;
+    for (; i + 8 <= len; i += 8) {
+        const double2 v0 = *reinterpret_cast<const double2*>(sm + i);
+        const double2 v1 = *reinterpret_cast<const double2*>(sm + i + 2);
+        const double2 v2 = *reinterpret_cast<const double2*>(sm + i + 4);
+        const double2 v3 = *reinterpret_cast<const double2*>(sm + i + 6);
+        acc = __dadd_rn(acc, v0.x); acc = __dadd_rn(acc, v0.y);
+        acc = __dadd_rn(acc, v1.x); acc = __dadd_rn(acc, v1.y);
+        acc = __dadd_rn(acc, v2.x); acc = __dadd_rn(acc, v2.y);
+        acc = __dadd_rn(acc, v3.x); acc = __dadd_rn(acc, v3.y);
     }
-    if (lane == 0) tiles[a * ntiles + t] = acc;
+    for (; i < len; ++i) acc = __dadd_rn(acc, sm[i]);
+    tiles[a * ntiles + t] = acc;
 }
 
 // Ordered fold of tile partials (block_sum outer loop core.cpp:172).

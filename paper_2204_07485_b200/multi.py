@@ -15,7 +15,7 @@ the ranks exchange exactly three small messages:
 
 The exchange is written against torch.distributed (NCCL on GPUs, gloo on CPU
 for tests) with injectable `chain` / `rows` callables, so the same logic is
-exercised on CPU with the oracle standing in for the device engine.
+exercised on CPU with a host-side stand-in for the device engine.
 """
 from __future__ import annotations
 

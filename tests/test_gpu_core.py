@@ -123,3 +123,57 @@ def test_integer_data_exact_ties(port):
     labels, dists = bm.assign_nearest(bm.Dataset(X), bm.Centroids(C, mask))
     l2, d2, _ = port.assign_nearest(X, C, mask)
     assert (labels == l2).all() and (bits(dists) == bits(d2)).all()
+
+
+ADVERSARIAL = {
+    # exact ties: duplicated centroids and points on bisectors
+    "dup_centroids": lambda r: (r.integers(0, 5, (4000, 3)).astype(np.float64),
+                                np.array([[1, 1, 1], [1, 1, 1], [2, 2, 2], [0, 0, 0], [2, 2, 2.0]])),
+    # values far beyond fp32 range: the screen must defer to the exact path
+    "beyond_fp32": lambda r: (r.normal(size=(3000, 4)) * 1e40,
+                              r.normal(size=(6, 4)) * 1e40),
+    # fp32-subnormal magnitudes
+    "subnormal": lambda r: (r.normal(size=(3000, 5)) * 1e-41,
+                            r.normal(size=(7, 5)) * 1e-41),
+    # large offset, tiny spread (catastrophic for a norm-expansion screen)
+    "offset": lambda r: (1e6 + r.normal(size=(5000, 8)) * 1e-3,
+                         1e6 + r.normal(size=(12, 8)) * 1e-3),
+    # mixed scales per dimension
+    "mixed": lambda r: (r.normal(size=(5000, 30)) * np.logspace(-8, 8, 30),
+                        r.normal(size=(20, 30)) * np.logspace(-8, 8, 30)),
+    # near ties: centroids separated by one ulp
+    "ulp_pairs": lambda r: (r.normal(size=(4000, 2)),
+                            np.array([[0.5, 0.5], [np.nextafter(0.5, 1), 0.5], [-0.5, 0.1],
+                                      [-0.5, np.nextafter(0.1, 1)]])),
+}
+
+
+@pytest.mark.parametrize("case", sorted(ADVERSARIAL))
+def test_screen_adversarial_bitwise(port, case):
+    X, C = ADVERSARIAL[case](np.random.default_rng(11))
+    X = X.copy()
+    X[:C.shape[0]] = C  # points that coincide with centroids (distance 0)
+    mask = np.zeros(C.shape[0], np.uint8)
+    labels, dists = bm.assign_nearest(bm.Dataset(X), bm.Centroids(C, mask))
+    l2, d2, _ = port.assign_nearest(X, C, mask)
+    assert (labels == l2).all()
+    assert (bits(dists) == bits(d2)).all()
+    assert bm.objective(bm.Dataset(X), bm.Centroids(C, mask)) == port.block_sum(d2)
+
+
+def test_exact_mode_matches_screen_mode():
+    """BM_ASSIGN_MODE=exact (unscreened kernel) gives the same bits in a fresh process."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "import paper_2204_07485_b200 as bm;"
+        "X = np.random.default_rng(5).normal(size=(20000, 16)) * 4;"
+        "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=10, chunk_size=3000, max_chunks=6, seed=3));"
+        "print(repr(o.objective), o.counter.distance_evals, hash(o.centroids.values.tobytes()))")
+    env = dict(os.environ)
+    outs = []
+    for mode in ("screen", "exact"):
+        env["BM_ASSIGN_MODE"] = mode
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                                   text=True, check=True).stdout)
+    assert outs[0] == outs[1] and outs[0]
