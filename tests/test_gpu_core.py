@@ -169,7 +169,7 @@ def test_exact_mode_matches_screen_mode():
         "import paper_2204_07485_b200 as bm;"
         "X = np.random.default_rng(5).normal(size=(20000, 16)) * 4;"
         "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=10, chunk_size=3000, max_chunks=6, seed=3));"
-        "print(repr(o.objective), o.counter.distance_evals, hash(o.centroids.values.tobytes()))")
+        "import hashlib; print(repr(o.objective), o.counter.distance_evals, hashlib.sha1(o.centroids.values.tobytes()).hexdigest())")
     env = dict(os.environ)
     outs = []
     for mode in ("screen", "exact"):
