@@ -226,6 +226,8 @@ def main():
     a_rows = sum(r["prof"]["assign_rows_total"] for r in res)
     f_ms = sum(r["prof"]["final_ms"] for r in res)
     f_rows = sum(r["prof"]["final_rows"] for r in res)
+    s_cand = sum(r["prof"]["screen_candidates"] for r in res)
+    s_rows = sum(r["prof"]["screen_rows"] for r in res)
     objective = res[-1]["objective"]
     if world > 1:
         t = torch.tensor([ms, evals, chunks], dtype=torch.float64, device=dev)
@@ -284,6 +286,7 @@ def main():
                 "launches_timed": a_n, "avg_launch_ms": avg_ms,
                 "alg_bytes_per_launch": alg_bytes,
                 "fp64_flops_per_launch": 3.0 * rows_per_launch * w.k * w.n,
+                "screen_candidates_per_point": s_cand / s_rows if s_rows else None,
                 "final_pass": {"avg_ms": final_avg_ms, "alg_bytes": final_bytes,
                                "achieved_gbs": final_bytes / (final_avg_ms * 1e-3) / 1e9
                                if final_avg_ms > 0 else None}}

@@ -172,6 +172,8 @@ typedef struct bm_profile {
     uint64_t kernel_launches;
     double final_ms;
     uint64_t final_rows;
+    uint64_t screen_candidates; /* exact rechecks issued by the screened assignment */
+    uint64_t screen_rows;       /* rows that went through the screened assignment */
 } bm_profile;
 bm_status bm_set_profiling(int enabled);
 bm_status bm_last_profile(bm_profile* out);

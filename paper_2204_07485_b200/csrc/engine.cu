@@ -309,11 +309,16 @@ struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
     std::vector<uint64_t> rows;
     std::vector<int> final_flag;
     cudaStream_t stream = nullptr;
+    unsigned long long* d_cand = nullptr;  // device tally of screened candidates
+    uint64_t screen_rows = 0;
     void begin(cudaStream_t s) {
         stream = s;
         used = 0;
         rows.clear();
         final_flag.clear();
+        screen_rows = 0;
+        if (!d_cand) BM_CUDA(cudaMalloc(&d_cand, sizeof(unsigned long long)));
+        BM_CUDA(cudaMemsetAsync(d_cand, 0, sizeof(unsigned long long), s));
     }
     cudaEvent_t next() {
         if (used == pool.size()) {
@@ -347,12 +352,18 @@ struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
                 out.assign_rows_total += rows[i];
             }
         }
+        unsigned long long cand = 0;
+        BM_CUDA(cudaMemcpyAsync(&cand, d_cand, sizeof(cand), cudaMemcpyDeviceToHost, stream));
+        BM_CUDA(cudaStreamSynchronize(stream));
+        out.screen_candidates += cand;
+        out.screen_rows += screen_rows;
         used = 0;
         rows.clear();
         final_flag.clear();
     }
 };
 thread_local Profiler g_prof;
+
 
 void count_launch(uint64_t n = 1) { g_profile.kernel_launches += n; }
 
@@ -420,7 +431,8 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             dev::k_assign_screen<T><<<grid, assign_threads(k), 0, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
                 labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
-                screen_consts(P.n));
+                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
+            if (g_profiling) g_prof.screen_rows += P.rows;
         } else {
             dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
@@ -779,6 +791,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     const int k = (int)cfg.k, n = (int)d->n;
     g_profile = bm_profile{};  // launch counts always; event timing only when profiling
     if (g_profiling) g_prof.begin(st);
+    g_prof.stream = st;
     std::mt19937_64 rng(cfg.seed);  // :62
     Workspace& w = get_ws(d, s, k, cfg.candidates_per_step, 0);
     const bool identity = s == m;  // sample_chunk(s == m): whole range, no draws (:46-48)

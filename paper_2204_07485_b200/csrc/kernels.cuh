@@ -380,6 +380,8 @@ struct ScreenConsts {
 
 constexpr int kSMaxK = 32;  // centroids handled by the screened path
 
+constexpr int kSItems = 4;  // exact chains per thread per recheck round
+
 template <typename T>
 __global__ void __launch_bounds__(kAPG * kAMaxCG)
 k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
@@ -389,12 +391,19 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                 const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
                 int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
                 double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
-                ScreenConsts cst) {
+                unsigned long long* __restrict__ cand_counter, ScreenConsts cst) {
+    // pass-1 buffers; pass 2 reuses Ls (x slab, fp64) and red_u (c slab, fp64)
+    __shared__ __align__(16) float Ls[kSMaxK * kABP];  // [j][p] lower bounds
+    __shared__ __align__(16) float red_u[kAMaxCG * kABP];
     __shared__ float xs[kADC][kABP + 4];
     __shared__ float cs[kADC][kSMaxK];
-    __shared__ __align__(16) float Ls[kSMaxK * kABP];  // [j][p]; reused for the tile fold
-    __shared__ float red_u[kAMaxCG][kABP];
     __shared__ float umin[kABP];
+    __shared__ int icount[kABP];    // candidates per point -> item offsets
+    constexpr int kItemCap = 4 * kABP + 64;  // 576 items: ~4.5 candidates per point
+    __shared__ short item_p[kItemCap];
+    __shared__ signed char item_j[kItemCap];
+    __shared__ double item_d[kItemCap];
+    __shared__ uint32_t n_items;
     __shared__ int is_last;
 
     if (stop_ptr && *stop_ptr) return;
@@ -409,8 +418,10 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     const int KG = blockDim.x / kAPG;
     const int tid = threadIdx.x, pg = tid % kAPG, cg = tid / kAPG;
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
+    const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
     const float finf = __int_as_float(0x7F800000);
 
+    // ---------------- pass 1: fp32 screen ----------------
     float acc[kAP][kAK], xn[kAP], cn[kAK];
 #pragma unroll
     for (int t = 0; t < kAP; ++t) {
@@ -426,13 +437,12 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         __syncthreads();
         for (int e = tid; e < kABP * kADC; e += blockDim.x) {
             const int p = e / kADC, d = e % kADC;
-            const uint64_t gp = p0 + p;
             float v = 0.f;
-            if (gp < rows && d < dl) v = static_cast<float>(X[gp * ld + d0 + d]);  // rn
+            if (p < np && d < dl) v = static_cast<float>(X[(p0 + p) * ld + d0 + d]);  // rn
             xs[d][p] = v;
         }
         for (int e = tid; e < kSMaxK * kADC; e += blockDim.x) {
-            const int j = e / kADC, d = e % kADC;
+            const int d = e / kSMaxK, j = e % kSMaxK;
             float v = 0.f;
             if (j < KA && d < dl) v = __double2float_rn(Cact[static_cast<uint64_t>(j) * n + d0 + d]);
             cs[d][j] = v;
@@ -477,7 +487,7 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                 if (j >= KA) continue;
                 const float dt = acc[t][u];
                 float L = 0.f, U = finf;
-                float w = __fadd_ru(__fmul_ru(__fadd_ru(xnorm, cnorm[u]), cst.w_scale), cst.w_abs);
+                const float w = __fadd_ru(__fmul_ru(__fadd_ru(xnorm, cnorm[u]), cst.w_scale), cst.w_abs);
                 if (dt <= 3.0e38f && w <= 1.0e18f) {
                     float rlo = __fmul_rd(__fsqrt_rd(__fmul_rd(dt, cst.inv_1p_gn_rd)), cst.inv_1pu_rd);
                     rlo = fmaxf(__fsub_rd(rlo, w), 0.f);
@@ -492,30 +502,114 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         }
     }
 #pragma unroll
-    for (int t = 0; t < kAP; ++t) red_u[cg][pg + kAPG * t] = un[t];
+    for (int t = 0; t < kAP; ++t) red_u[cg * kABP + pg + kAPG * t] = un[t];
     __syncthreads();
     for (int p = tid; p < kABP; p += blockDim.x) {
         float m = finf;
-        for (int g = 0; g < KG; ++g) m = fminf(m, red_u[g][p]);
+        for (int g = 0; g < KG; ++g) m = fminf(m, red_u[g * kABP + p]);
         umin[p] = m;
+        int c = 0;
+        if (p < np)
+            for (int j = 0; j < KA; ++j) c += Ls[j * kABP + p] <= m;
+        icount[p] = c;
     }
     __syncthreads();
-    // exact fp64 recheck of the candidates, ascending j, strict < (core.cpp:137-151)
-    for (int p = tid; p < kABP; p += blockDim.x) {
+    if (tid == 0) {  // item offsets (points in order, candidates ascending j)
+        uint32_t r = 0;
+        for (int p = 0; p < kABP; ++p) {
+            const int c = icount[p];
+            icount[p] = r;
+            r += c;
+        }
+        n_items = r;
+        if (cand_counter) atomicAdd(cand_counter, static_cast<unsigned long long>(r));
+    }
+    __syncthreads();
+    const uint32_t NI = n_items;
+
+    // ---------------- pass 2: exact fp64 recheck of the candidates ----------------
+    // Items (point, candidate) in point order, candidates ascending j.  Each
+    // round gives every thread up to kSItems exact chains, streamed over the
+    // same 16-dim slabs (fp64 now) from shared memory.
+    const bool overflow = NI > static_cast<uint32_t>(kItemCap);
+    if (!overflow) {
+        for (int p = tid; p < np; p += blockDim.x) {
+            const float m = umin[p];
+            uint32_t it = icount[p];
+            for (int j = 0; j < KA; ++j)
+                if (Ls[j * kABP + p] <= m) {
+                    item_p[it] = static_cast<short>(p);
+                    item_j[it] = static_cast<signed char>(j);
+                    ++it;
+                }
+        }
+        double* xs64 = reinterpret_cast<double*>(Ls);     // [kADC][kABP]  (16 KB)
+        double* cs64 = reinterpret_cast<double*>(red_u);  // [kADC][kSMaxK] (4 KB)
+        const uint32_t per_round = kSItems * blockDim.x;
+        for (uint32_t base = 0; base < NI; base += per_round) {
+            __syncthreads();  // items complete / previous round's slabs consumed
+            double sum[kSItems];
+            int ip[kSItems], ij[kSItems];
+#pragma unroll
+            for (int r = 0; r < kSItems; ++r) {
+                const uint32_t i = base + tid + r * blockDim.x;
+                sum[r] = 0.0;
+                ip[r] = i < NI ? item_p[i] : -1;
+                ij[r] = i < NI ? item_j[i] : 0;
+            }
+            for (int d0 = 0; d0 < n; d0 += kADC) {
+                const int dl = min(kADC, n - d0);
+                __syncthreads();
+                for (int e = tid; e < kABP * kADC; e += blockDim.x) {
+                    const int pp = e / kADC, d = e % kADC;
+                    double v = 0.0;
+                    if (pp < np && d < dl) v = to_f64(X[(p0 + pp) * ld + d0 + d]);
+                    xs64[d * kABP + pp] = v;
+                }
+                for (int e = tid; e < kSMaxK * kADC; e += blockDim.x) {
+                    const int d = e / kSMaxK, j = e % kSMaxK;
+                    double v = 0.0;
+                    if (j < KA && d < dl) v = Cact[static_cast<uint64_t>(j) * n + d0 + d];
+                    cs64[d * kSMaxK + j] = v;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < kSItems; ++r) {
+                    if (ip[r] < 0) continue;
+                    double a = sum[r];
+                    for (int d = 0; d < dl; ++d)
+                        a = dist_step(a, xs64[d * kABP + ip[r]], cs64[d * kSMaxK + ij[r]]);
+                    sum[r] = a;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kSItems; ++r)
+                if (ip[r] >= 0) item_d[base + tid + r * blockDim.x] = sum[r];
+        }
+        __syncthreads();
+    }
+    for (int p = tid; p < np; p += blockDim.x) {
         const uint64_t gp = p0 + p;
-        if (gp >= rows) continue;
-        const float um = umin[p];
-        const T* x = X + gp * ld;
         double best = __longlong_as_double(0x7FF0000000000000LL);
         int bj = -1;
-        for (int j = 0; j < KA; ++j) {
-            if (!(Ls[j * kABP + p] <= um)) continue;
-            const double* c = Cact + static_cast<uint64_t>(j) * n;
-            double sum = 0.0;
-            for (int d = 0; d < n; ++d) sum = dist_step(sum, to_f64(x[d]), c[d]);
-            if (sum < best) {
-                best = sum;
-                bj = j;
+        if (!overflow) {  // ascending j, strict < (core.cpp:147)
+            const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(icount[p + 1]) : NI;
+            for (uint32_t i = icount[p]; i < b1; ++i) {
+                if (item_d[i] < best) {
+                    best = item_d[i];
+                    bj = item_j[i];
+                }
+            }
+        } else {  // candidate sets too large for the item buffer: full exact scan
+            const T* x = X + gp * ld;
+            for (int j = 0; j < KA; ++j) {
+                const double* c = Cact + static_cast<uint64_t>(j) * n;
+                double sm = 0.0;
+                for (int d = 0; d < n; ++d) sm = dist_step(sm, to_f64(x[d]), c[d]);
+                if (sm < best) {
+                    best = sm;
+                    bj = j;
+                }
             }
         }
         const int label = bj >= 0 ? act_idx[bj] : -1;
