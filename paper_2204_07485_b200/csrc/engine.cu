@@ -428,7 +428,14 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         if (screen) {
-            dev::k_assign_screen<T><<<grid, assign_threads(k), 0, st>>>(
+            constexpr size_t shm = dev::screen_smem_bytes<T>();
+            static bool attr_set = false;  // per template instance
+            if (!attr_set) {
+                BM_CUDA(cudaFuncSetAttribute(dev::k_assign_screen<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+                attr_set = true;
+            }
+            dev::k_assign_screen<T><<<grid, assign_threads(k), shm, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
                 labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                 g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));

@@ -380,7 +380,66 @@ struct ScreenConsts {
 
 constexpr int kSMaxK = 32;  // centroids handled by the screened path
 
-constexpr int kSItems = 4;  // exact chains per thread per recheck round
+constexpr int kSItems = 4;   // exact chains per thread per recheck round
+constexpr int kItemCap = 4 * kABP + 64;  // 576 (point, candidate) items per CTA
+
+// cp.async helpers (LDGSTS): global -> shared without staging through registers
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <typename T>
+struct ScreenSmem {
+    static constexpr int kVec = 16 / sizeof(T);            // elements per 16-byte chunk
+    static constexpr int kRS = kADC + kVec;                // raw row stride (elements), 16B aligned
+    T xraw[2][kABP * kRS];                                 // double-buffered raw point slabs
+    double craw[2][kADC * kSMaxK];                         // double-buffered centroid slabs [d][j]
+    float Ls[kSMaxK * kABP];                               // [j][p] certified lower bounds
+    float red_u[kAMaxCG * kABP];
+    float umin[kABP];
+    int icount[kABP];
+    union {
+        struct {
+            float xs[kADC][kABP + 4];                      // pass-1 fp32 slab (transposed)
+            float cs[kADC][kSMaxK];
+        } p1;
+        struct {
+            double item_d[kItemCap];
+            short item_p[kItemCap];
+            signed char item_j[kItemCap];
+        } p2;
+    } u;
+    uint32_t n_items;
+    int is_last;
+};
+
+// Issue the cp.async copies of slab [d0, d0+16) of the CTA's points and centroids.
+template <typename T>
+__device__ __forceinline__ void issue_slab(ScreenSmem<T>& S, int buf, const T* __restrict__ X, uint64_t p0,
+                                           int np, uint64_t ld, int d0, int n,
+                                           const double* __restrict__ Cact, int KA) {
+    constexpr int V = ScreenSmem<T>::kVec, RS = ScreenSmem<T>::kRS;
+    constexpr int CPR = kADC / V;  // chunks per row
+    const int dl = min(kADC, n - d0);
+    for (int e = threadIdx.x; e < kABP * CPR; e += blockDim.x) {
+        const int p = e / CPR, c = e % CPR;
+        if (p < np && c * V < dl)  // padded ld keeps the chunk inside the row
+            cp_async16(&S.xraw[buf][p * RS + c * V], X + (p0 + p) * ld + d0 + c * V);
+    }
+    for (int e = threadIdx.x; e < kADC * kSMaxK; e += blockDim.x) {
+        const int d = e / kSMaxK, j = e % kSMaxK;
+        if (j < KA && d < dl) cp_async8(&S.craw[buf][d * kSMaxK + j], Cact + static_cast<uint64_t>(j) * n + d0 + d);
+    }
+    cp_async_commit();
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kAPG * kAMaxCG)
@@ -392,19 +451,9 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                 int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
                 double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
                 unsigned long long* __restrict__ cand_counter, ScreenConsts cst) {
-    // pass-1 buffers; pass 2 reuses Ls (x slab, fp64) and red_u (c slab, fp64)
-    __shared__ __align__(16) float Ls[kSMaxK * kABP];  // [j][p] lower bounds
-    __shared__ __align__(16) float red_u[kAMaxCG * kABP];
-    __shared__ float xs[kADC][kABP + 4];
-    __shared__ float cs[kADC][kSMaxK];
-    __shared__ float umin[kABP];
-    __shared__ int icount[kABP];    // candidates per point -> item offsets
-    constexpr int kItemCap = 4 * kABP + 64;  // 576 items: ~4.5 candidates per point
-    __shared__ short item_p[kItemCap];
-    __shared__ signed char item_j[kItemCap];
-    __shared__ double item_d[kItemCap];
-    __shared__ uint32_t n_items;
-    __shared__ int is_last;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScreenSmem<T>& S = *reinterpret_cast<ScreenSmem<T>*>(smem_raw);
+    constexpr int RS = ScreenSmem<T>::kRS;
 
     if (stop_ptr && *stop_ptr) return;
     const int KA = *n_active_ptr;
@@ -420,8 +469,9 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
     const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
     const float finf = __int_as_float(0x7F800000);
+    const int nslab = (n + kADC - 1) / kADC;
 
-    // ---------------- pass 1: fp32 screen ----------------
+    // ---------------- pass 1: fp32 screen over cp.async-pipelined slabs ----------------
     float acc[kAP][kAK], xn[kAP], cn[kAK];
 #pragma unroll
     for (int t = 0; t < kAP; ++t) {
@@ -432,20 +482,26 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
 #pragma unroll
     for (int u = 0; u < kAK; ++u) cn[u] = 0.f;
 
-    for (int d0 = 0; d0 < n; d0 += kADC) {
-        const int dl = min(kADC, n - d0);
+    issue_slab(S, 0, X, p0, np, ld, 0, n, Cact, KA);
+    for (int sl = 0; sl < nslab; ++sl) {
+        const int d0 = sl * kADC, dl = min(kADC, n - d0), buf = sl & 1;
+        if (sl + 1 < nslab) {
+            issue_slab(S, buf ^ 1, X, p0, np, ld, d0 + kADC, n, Cact, KA);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
+        // raw -> fp32 transposed slab (round to nearest), once per element
         for (int e = tid; e < kABP * kADC; e += blockDim.x) {
             const int p = e / kADC, d = e % kADC;
             float v = 0.f;
-            if (p < np && d < dl) v = static_cast<float>(X[(p0 + p) * ld + d0 + d]);  // rn
-            xs[d][p] = v;
+            if (p < np && d < dl) v = static_cast<float>(S.xraw[buf][p * RS + d]);
+            S.u.p1.xs[d][p] = v;
         }
-        for (int e = tid; e < kSMaxK * kADC; e += blockDim.x) {
+        for (int e = tid; e < kADC * kSMaxK; e += blockDim.x) {
             const int d = e / kSMaxK, j = e % kSMaxK;
-            float v = 0.f;
-            if (j < KA && d < dl) v = __double2float_rn(Cact[static_cast<uint64_t>(j) * n + d0 + d]);
-            cs[d][j] = v;
+            S.u.p1.cs[d][j] = (j < KA && d < dl) ? __double2float_rn(S.craw[buf][e]) : 0.f;
         }
         __syncthreads();
         if (cg * kAK < KA) {
@@ -453,9 +509,9 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
             for (int d = 0; d < dl; ++d) {
                 float xv[kAP], cv[kAK];
 #pragma unroll
-                for (int t = 0; t < kAP; ++t) xv[t] = xs[d][pg + kAPG * t];
+                for (int t = 0; t < kAP; ++t) xv[t] = S.u.p1.xs[d][pg + kAPG * t];
 #pragma unroll
-                for (int u = 0; u < kAK; ++u) cv[u] = cs[d][cg * kAK + u];
+                for (int u = 0; u < kAK; ++u) cv[u] = S.u.p1.cs[d][cg * kAK + u];
 #pragma unroll
                 for (int t = 0; t < kAP; ++t) {
                     xn[t] = __fmaf_ru(xv[t], xv[t], xn[t]);
@@ -469,6 +525,7 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                 for (int u = 0; u < kAK; ++u) cn[u] = __fmaf_ru(cv[u], cv[u], cn[u]);
             }
         }
+        __syncthreads();  // buffers of this slab are free for the next issue
     }
     // certified bounds
     float un[kAP];
@@ -496,95 +553,86 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                     L = __fmul_rd(__fmul_rd(rlo, rlo), cst.lo64);
                     U = __fmul_ru(__fmul_ru(rhi, rhi), cst.hi64);
                 }
-                Ls[j * kABP + pg + kAPG * t] = L;
+                S.Ls[j * kABP + pg + kAPG * t] = L;
                 un[t] = fminf(un[t], U);
             }
         }
     }
 #pragma unroll
-    for (int t = 0; t < kAP; ++t) red_u[cg * kABP + pg + kAPG * t] = un[t];
+    for (int t = 0; t < kAP; ++t) S.red_u[cg * kABP + pg + kAPG * t] = un[t];
     __syncthreads();
     for (int p = tid; p < kABP; p += blockDim.x) {
         float m = finf;
-        for (int g = 0; g < KG; ++g) m = fminf(m, red_u[g * kABP + p]);
-        umin[p] = m;
+        for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g * kABP + p]);
+        S.umin[p] = m;
         int c = 0;
         if (p < np)
-            for (int j = 0; j < KA; ++j) c += Ls[j * kABP + p] <= m;
-        icount[p] = c;
+            for (int j = 0; j < KA; ++j) c += S.Ls[j * kABP + p] <= m;
+        S.icount[p] = c;
     }
     __syncthreads();
-    if (tid == 0) {  // item offsets (points in order, candidates ascending j)
+    if (tid == 0) {  // item offsets: points in order, candidates ascending j
         uint32_t r = 0;
         for (int p = 0; p < kABP; ++p) {
-            const int c = icount[p];
-            icount[p] = r;
+            const int c = S.icount[p];
+            S.icount[p] = r;
             r += c;
         }
-        n_items = r;
+        S.n_items = r;
         if (cand_counter) atomicAdd(cand_counter, static_cast<unsigned long long>(r));
     }
     __syncthreads();
-    const uint32_t NI = n_items;
-
-    // ---------------- pass 2: exact fp64 recheck of the candidates ----------------
-    // Items (point, candidate) in point order, candidates ascending j.  Each
-    // round gives every thread up to kSItems exact chains, streamed over the
-    // same 16-dim slabs (fp64 now) from shared memory.
+    const uint32_t NI = S.n_items;
     const bool overflow = NI > static_cast<uint32_t>(kItemCap);
+
+    // ---------------- pass 2: exact fp64 recheck of the candidate items ----------------
     if (!overflow) {
         for (int p = tid; p < np; p += blockDim.x) {
-            const float m = umin[p];
-            uint32_t it = icount[p];
+            const float m = S.umin[p];
+            uint32_t it = S.icount[p];
             for (int j = 0; j < KA; ++j)
-                if (Ls[j * kABP + p] <= m) {
-                    item_p[it] = static_cast<short>(p);
-                    item_j[it] = static_cast<signed char>(j);
+                if (S.Ls[j * kABP + p] <= m) {
+                    S.u.p2.item_p[it] = static_cast<short>(p);
+                    S.u.p2.item_j[it] = static_cast<signed char>(j);
                     ++it;
                 }
         }
-        double* xs64 = reinterpret_cast<double*>(Ls);     // [kADC][kABP]  (16 KB)
-        double* cs64 = reinterpret_cast<double*>(red_u);  // [kADC][kSMaxK] (4 KB)
         const uint32_t per_round = kSItems * blockDim.x;
         for (uint32_t base = 0; base < NI; base += per_round) {
-            __syncthreads();  // items complete / previous round's slabs consumed
+            __syncthreads();  // items complete / previous round done with the buffers
             double sum[kSItems];
             int ip[kSItems], ij[kSItems];
 #pragma unroll
             for (int r = 0; r < kSItems; ++r) {
                 const uint32_t i = base + tid + r * blockDim.x;
                 sum[r] = 0.0;
-                ip[r] = i < NI ? item_p[i] : -1;
-                ij[r] = i < NI ? item_j[i] : 0;
+                ip[r] = i < NI ? S.u.p2.item_p[i] : -1;
+                ij[r] = i < NI ? S.u.p2.item_j[i] : 0;
             }
-            for (int d0 = 0; d0 < n; d0 += kADC) {
-                const int dl = min(kADC, n - d0);
-                __syncthreads();
-                for (int e = tid; e < kABP * kADC; e += blockDim.x) {
-                    const int pp = e / kADC, d = e % kADC;
-                    double v = 0.0;
-                    if (pp < np && d < dl) v = to_f64(X[(p0 + pp) * ld + d0 + d]);
-                    xs64[d * kABP + pp] = v;
-                }
-                for (int e = tid; e < kSMaxK * kADC; e += blockDim.x) {
-                    const int d = e / kSMaxK, j = e % kSMaxK;
-                    double v = 0.0;
-                    if (j < KA && d < dl) v = Cact[static_cast<uint64_t>(j) * n + d0 + d];
-                    cs64[d * kSMaxK + j] = v;
+            issue_slab(S, 0, X, p0, np, ld, 0, n, Cact, KA);
+            for (int sl = 0; sl < nslab; ++sl) {
+                const int d0 = sl * kADC, dl = min(kADC, n - d0), buf = sl & 1;
+                if (sl + 1 < nslab) {
+                    issue_slab(S, buf ^ 1, X, p0, np, ld, d0 + kADC, n, Cact, KA);
+                    cp_async_wait<1>();
+                } else {
+                    cp_async_wait<0>();
                 }
                 __syncthreads();
 #pragma unroll
                 for (int r = 0; r < kSItems; ++r) {
                     if (ip[r] < 0) continue;
+                    const T* xr = &S.xraw[buf][ip[r] * RS];
+                    const double* cr = &S.craw[buf][ij[r]];
                     double a = sum[r];
-                    for (int d = 0; d < dl; ++d)
-                        a = dist_step(a, xs64[d * kABP + ip[r]], cs64[d * kSMaxK + ij[r]]);
+                    for (int d = 0; d < dl; ++d) a = dist_step(a, to_f64(xr[d]), cr[d * kSMaxK]);
                     sum[r] = a;
                 }
+                __syncthreads();
             }
 #pragma unroll
             for (int r = 0; r < kSItems; ++r)
-                if (ip[r] >= 0) item_d[base + tid + r * blockDim.x] = sum[r];
+                if (ip[r] >= 0) S.u.p2.item_d[base + tid + r * blockDim.x] = sum[r];
         }
         __syncthreads();
     }
@@ -593,11 +641,11 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         double best = __longlong_as_double(0x7FF0000000000000LL);
         int bj = -1;
         if (!overflow) {  // ascending j, strict < (core.cpp:147)
-            const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(icount[p + 1]) : NI;
-            for (uint32_t i = icount[p]; i < b1; ++i) {
-                if (item_d[i] < best) {
-                    best = item_d[i];
-                    bj = item_j[i];
+            const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(S.icount[p + 1]) : NI;
+            for (uint32_t i = S.icount[p]; i < b1; ++i) {
+                if (S.u.p2.item_d[i] < best) {
+                    best = S.u.p2.item_d[i];
+                    bj = S.u.p2.item_j[i];
                 }
             }
         } else {  // candidate sets too large for the item buffer: full exact scan
@@ -626,14 +674,14 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         const uint64_t tb = tile * kTile;
         const unsigned ctas = static_cast<unsigned>((min(rows, tb + kTile) - tb + kABP - 1) / kABP);
         const unsigned old = atomicAdd(&tile_counter[tile], 1u);
-        is_last = old == ctas - 1;
+        S.is_last = old == ctas - 1;
     }
     __syncthreads();
-    if (!is_last) return;
+    if (!S.is_last) return;
     __threadfence();
     const uint64_t tb = tile * kTile;
     const int len = static_cast<int>(min(rows, tb + kTile) - tb);
-    double* fold = reinterpret_cast<double*>(Ls);
+    double* fold = reinterpret_cast<double*>(S.xraw[0]);  // >= 8 KB
     for (int i = tid; i < len; i += blockDim.x) fold[i] = __ldcg(dists_out + tb + i);
     __syncthreads();
     if (tid == 0) {
@@ -654,6 +702,9 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         tile_counter[tile] = 0u;  // ready for the next launch
     }
 }
+
+template <typename T>
+constexpr size_t screen_smem_bytes() { return sizeof(ScreenSmem<T>); }
 
 // ===========================================================================
 // 4. Per-tile sequential sums (block_sum inner loop core.cpp:167-173).
