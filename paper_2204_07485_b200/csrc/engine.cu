@@ -120,6 +120,7 @@ uint64_t padded_ld(uint64_t n, bm_dtype t) {
 struct Workspace {
     uint64_t R = 0;  // max rows processed (chunk size s, or m)
     int k = 0, n = 0, ncand = 0;
+    int ldc = 0;  // compacted-centroid row stride (even: 16-byte rows)
     uint64_t hist_cap = 0;
     uint64_t tiles = 0;
 
@@ -152,6 +153,7 @@ struct Workspace {
         k = k_;
         n = n_;
         ncand = std::max(ncand_, 1);
+        ldc = n + (n & 1);
         tiles = tiles_of(rows);
         hist_cap = hist;
         labels.alloc(2 * R);
@@ -162,7 +164,7 @@ struct Workspace {
         psum.alloc(tiles * (uint64_t)k * n);
         pcnt.alloc(tiles * (uint64_t)k);
         C.alloc((uint64_t)k * n);
-        Cact.alloc((uint64_t)k * n);
+        Cact.alloc((uint64_t)k * (n + (n & 1)));
         mask.alloc(k);
         act.alloc(k);
         status.alloc(1);
@@ -386,16 +388,17 @@ float f_ru(double x) {
 
 dev::ScreenConsts screen_consts(int n) {
     const double u = std::ldexp(1.0, -24);
-    const double gn = n * u / (1.0 - n * u);
+    auto gam = [&](double m) { return m * u / (1.0 - m * u); };
+    const int nslab = (n + dev::kADC - 1) / dev::kADC;
+    const double g16 = gam(std::min(n, dev::kADC));
+    const double gb = g16 + gam(nslab) * (1.0 + g16);      // blocked dot-product error
+    const double up = u * (1.0 + 4 * u) / (1.0 - u);         // input rounding, incl. x^ vs x norms
+    const double K = gb / 2.0 + 2.0 * up + up * up;
     const double u64 = std::ldexp(1.0, -53);
     const double g64 = (n + 3) * u64 / (1.0 - (n + 3) * u64);
     dev::ScreenConsts c;
-    c.inv_1p_gn_rd = f_rd(1.0 / (1.0 + gn) * (1.0 - 4 * u64));
-    c.inv_1m_gn_ru = f_ru(1.0 / (1.0 - gn) * (1.0 + 4 * u64));
-    c.inv_1pu_rd = f_rd(1.0 / (1.0 + u) * (1.0 - 4 * u64));
-    c.inv_1mu_ru = f_ru(1.0 / (1.0 - u) * (1.0 + 4 * u64));
-    c.w_scale = f_ru(u * (1.0 + 4 * u) / (1.0 - u) * (1.0 + 4 * u64));
-    c.w_abs = std::ldexp(1.0f, -60);
+    c.K = f_ru(K * (1.0 + 1e-6));
+    c.dabs = std::ldexp(1.0f, -40);
     c.lo64 = f_rd((1.0 - g64) * (1.0 - 4 * u64));
     c.hi64 = f_ru((1.0 + g64) * (1.0 + 4 * u64));
     return c;
@@ -428,21 +431,21 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         if (screen) {
-            constexpr size_t shm = dev::screen_smem_bytes<T>();
+            constexpr size_t shm = dev::screen_smem_bytes();
             static bool attr_set = false;  // per template instance
             if (!attr_set) {
                 BM_CUDA(cudaFuncSetAttribute(dev::k_assign_screen<T>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
                 attr_set = true;
             }
-            dev::k_assign_screen<T><<<grid, assign_threads(k), shm, st>>>(
-                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
-                labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
-                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
+            dev::k_assign_screen<T><<<grid, dev::kSThreads, shm, st>>>(
+                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
+                &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out,
+                tile_ctr, g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
             if (g_profiling) g_prof.screen_rows += P.rows;
         } else {
             dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
-                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.act.p, &w.status.p->n_active,
+                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active,
                 labels_pair, pair_stride, parity, dists, changed, stop);
         }
     });
@@ -462,7 +465,7 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
 }
 
 void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_t* mask) {
-    dev::k_compact<<<1, 256, w.k * sizeof(int), st>>>(C, mask, w.k, w.n, w.Cact.p, w.act.p,
+    dev::k_compact<<<1, 256, w.k * sizeof(int), st>>>(C, mask, w.k, w.n, w.Cact.p, w.ldc, w.act.p,
                                                        &w.status.p->n_active);
     BM_LAUNCH();
     count_launch();
@@ -488,7 +491,7 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
     const unsigned mgrid = (unsigned)std::min<uint64_t>(ceil_div(pairs, dev::kUThreads), 1024);
     const size_t mshm = k * (sizeof(unsigned long long) + sizeof(int));
     dev::k_update_merge<<<mgrid, dev::kUThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p,
-                                                            w.mask.p, w.Cact.p, w.act.p,
+                                                            w.mask.p, w.Cact.p, w.ldc, w.act.p,
                                                             &w.status.p->n_active, stop);
     BM_LAUNCH();
     count_launch(2);

@@ -237,7 +237,7 @@ constexpr int kAXS = kABP + 1;    // padded slab stride
 template <typename T>
 __global__ void __launch_bounds__(kAPG * kAMaxCG)
 k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
-         const double* __restrict__ Cact, const int* __restrict__ act_idx,
+         const double* __restrict__ Cact, int ldc, const int* __restrict__ act_idx,
          const int* __restrict__ n_active_ptr,
          int32_t* __restrict__ labels_pair, uint64_t pair_stride, const int* __restrict__ parity_ptr,
          double* __restrict__ dists_out, int* __restrict__ changed_flag,
@@ -288,7 +288,7 @@ k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
             for (int e = tid; e < KB * kADC; e += blockDim.x) {
                 const int j = e / kADC, d = e % kADC;
                 double v = 0.0;
-                if (kb + j < KA && d < dl) v = Cact[static_cast<uint64_t>(kb + j) * n + d0 + d];
+                if (kb + j < KA && d < dl) v = Cact[static_cast<uint64_t>(kb + j) * ldc + d0 + d];
                 cs[d * KB + j] = v;
             }
             __syncthreads();
@@ -351,100 +351,83 @@ k_assign(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
 // ===========================================================================
 // 3b. Screened exact assignment (same results as k_assign, bit for bit).
 //
-// Screen: every (point, active centroid) distance is approximated in fp32 by
-// the direct form  d~ = sum_d fl(fl32(x_d) - fl32(c_d))^2  (FFMA chain), and
-// turned into CERTIFIED bounds L <= d_ref <= U on the reference's fp64 value
-// d_ref (core.cpp:142-146) with directed-rounding fp32 arithmetic:
-//   r = ||x - c|| lies in [ sqrt(d~/(1+g_n))/(1+u) - w , sqrt(d~/(1-g_n))/(1-u) + w ]
-//   w = u (||x|| + ||c||) + 2^-60   (fp32 rounding of the inputs, incl. subnormals)
-//   d_ref in [ r^2 (1-g64), r^2 (1+g64) ]   (reference's own rounding, g64 = gamma_{n+3})
-// with u = 2^-24, g_n = n u/(1-n u).  Any centroid whose L exceeds the point's
-// smallest U cannot be the reference's minimum (nor tie with it), so only the
-// candidates L_j <= min_i U_i are recomputed exactly in fp64 (direct form,
-// strict <, ascending j) — reproducing assign_nearest exactly.
-// Non-finite fp32 intermediates (inputs beyond fp32 range) force L=0, U=inf.
+// Screen (fp32, norm form).  With x^ = fl32(x), c^ = fl32(c), the dot product
+// s = sum_d x^_d c^_d is accumulated with packed FFMA2 in 16-dim blocks that
+// are then added up (error <= g_b ||x^|| ||c^||, g_b = g_16 + g_S(1+g_16)),
+// and ||x^||^2, ||c^||^2 are accumulated with rounding down and up.  Writing
+// S = ||x^||+||c^|| (upper bound), the reference's fp64 value d_ref
+// (core.cpp:142-146) is certified to lie in [L, U]:
+//   r^2 in [ nx_lo + nc_lo - 2s - K S^2 , nx_hi + nc_hi - 2s + K S^2 ]
+//   K = g_b/2 + 2u' + u'^2,  u' = u(1+4u)/(1-u)   (input rounding to fp32,
+//       via (r^ +- w)^2 with w <= u' S and r^ <= S)
+//   d_ref in [ r^2 (1-g64), r^2 (1+g64) ],  g64 = gamma_{n+3} (fp64 rounding)
+// evaluated with directed-rounding fp32 ops.  Every centroid whose L exceeds
+// the point's smallest U can be neither the reference's minimum nor tie it;
+// the remaining candidates are recomputed exactly in fp64 (direct form,
+// ascending j, strict <), which reproduces assign_nearest exactly.  Inputs or
+// intermediates beyond fp32 range force L = 0, U = inf (exact fallback).
 //
 // Fused per-1024-point tile sums (block_sum inner loop core.cpp:167-173): the
 // last CTA to finish a tile folds the tile's distances in index order.
 // ===========================================================================
 struct ScreenConsts {
-    float inv_1p_gn_rd;  // 1/(1+g_n), rounded down
-    float inv_1m_gn_ru;  // 1/(1-g_n), rounded up
-    float inv_1pu_rd;    // 1/(1+u),   rounded down
-    float inv_1mu_ru;    // 1/(1-u),   rounded up
-    float w_scale;       // u(1+4u)/(1-u), rounded up
-    float w_abs;         // 2^-60
-    float lo64;          // 1-g64, rounded down
-    float hi64;          // 1+g64, rounded up
+    float K;      // g_b/2 + 2u' + u'^2, rounded up
+    float dabs;   // absolute slack for fp32 underflow
+    float lo64;   // 1-g64, rounded down
+    float hi64;   // 1+g64, rounded up
 };
 
-constexpr int kSMaxK = 32;  // centroids handled by the screened path
+constexpr int kSMaxK = 32;        // centroids handled by the screened path
+constexpr int kSThreads = 256;    // 8 warps: warp w < KG owns centroids 4w..4w+3
+constexpr int kSXS = kABP + 4;    // fp32 slab stride (16-byte aligned rows)
+constexpr int kItemCap = 4 * kABP + 64;  // (point, candidate) items per CTA
 
-constexpr int kSItems = 4;   // exact chains per thread per recheck round
-constexpr int kItemCap = 4 * kABP + 64;  // 576 (point, candidate) items per CTA
-
-// cp.async helpers (LDGSTS): global -> shared without staging through registers
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-template <typename T>
 struct ScreenSmem {
-    static constexpr int kVec = 16 / sizeof(T);            // elements per 16-byte chunk
-    static constexpr int kRS = kADC + kVec;                // raw row stride (elements), 16B aligned
-    T xraw[2][kABP * kRS];                                 // double-buffered raw point slabs
-    double craw[2][kADC * kSMaxK];                         // double-buffered centroid slabs [d][j]
-    float Ls[kSMaxK * kABP];                               // [j][p] certified lower bounds
-    float red_u[kAMaxCG * kABP];
-    float umin[kABP];
-    int icount[kABP];
     union {
         struct {
-            float xs[kADC][kABP + 4];                      // pass-1 fp32 slab (transposed)
-            float cs[kADC][kSMaxK];
+            float xs[2][kADC][kSXS];    // double-buffered fp32 point slabs [d][p]
+            float cs[2][kADC][kSMaxK];  // double-buffered fp32 centroid slabs [d][j]
         } p1;
         struct {
             double item_d[kItemCap];
             short item_p[kItemCap];
             signed char item_j[kItemCap];
         } p2;
+        double fold[kTile];
     } u;
+    float Ls[kSMaxK][kABP];   // certified lower bounds [j][p]
+    float red_u[8][kABP];
+    float nx_lo[kABP], nx_hi[kABP], nxr[kABP];
+    float nc_lo[kSMaxK], nc_hi[kSMaxK], ncr[kSMaxK];
+    float umin[kABP];
+    int icount[kABP];
     uint32_t n_items;
     int is_last;
 };
 
-// Issue the cp.async copies of slab [d0, d0+16) of the CTA's points and centroids.
-template <typename T>
-__device__ __forceinline__ void issue_slab(ScreenSmem<T>& S, int buf, const T* __restrict__ X, uint64_t p0,
-                                           int np, uint64_t ld, int d0, int n,
-                                           const double* __restrict__ Cact, int KA) {
-    constexpr int V = ScreenSmem<T>::kVec, RS = ScreenSmem<T>::kRS;
-    constexpr int CPR = kADC / V;  // chunks per row
-    const int dl = min(kADC, n - d0);
-    for (int e = threadIdx.x; e < kABP * CPR; e += blockDim.x) {
-        const int p = e / CPR, c = e % CPR;
-        if (p < np && c * V < dl)  // padded ld keeps the chunk inside the row
-            cp_async16(&S.xraw[buf][p * RS + c * V], X + (p0 + p) * ld + d0 + c * V);
-    }
-    for (int e = threadIdx.x; e < kADC * kSMaxK; e += blockDim.x) {
-        const int d = e / kSMaxK, j = e % kSMaxK;
-        if (j < KA && d < dl) cp_async8(&S.craw[buf][d * kSMaxK + j], Cact + static_cast<uint64_t>(j) * n + d0 + d);
-    }
-    cp_async_commit();
+__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
+    unsigned long long d;
+    const float2 bb = make_float2(b, b);
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&bb)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+    return *reinterpret_cast<float2*>(&d);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kAPG * kAMaxCG)
+__global__ void __launch_bounds__(kSThreads, 3)
 k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
-                const double* __restrict__ Cact, const int* __restrict__ act_idx,
+                const double* __restrict__ Cact, int ldc, const int* __restrict__ act_idx,
                 const int* __restrict__ n_active_ptr,
                 int32_t* __restrict__ labels_pair, uint64_t pair_stride,
                 const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
@@ -452,8 +435,7 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                 double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
                 unsigned long long* __restrict__ cand_counter, ScreenConsts cst) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    ScreenSmem<T>& S = *reinterpret_cast<ScreenSmem<T>*>(smem_raw);
-    constexpr int RS = ScreenSmem<T>::kRS;
+    ScreenSmem& S = *reinterpret_cast<ScreenSmem*>(smem_raw);
 
     if (stop_ptr && *stop_ptr) return;
     const int KA = *n_active_ptr;
@@ -464,179 +446,237 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         labels_out = labels_pair + (1 - par) * pair_stride;
         labels_old = labels_pair + par * pair_stride;
     }
-    const int KG = blockDim.x / kAPG;
-    const int tid = threadIdx.x, pg = tid % kAPG, cg = tid / kAPG;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int KG = (KA + kAK - 1) / kAK;
+    const bool comp = warp < KG;
+    const bool normw = warp == 7;
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
     const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
     const float finf = __int_as_float(0x7F800000);
     const int nslab = (n + kADC - 1) / kADC;
 
-    // ---------------- pass 1: fp32 screen over cp.async-pipelined slabs ----------------
-    float acc[kAP][kAK], xn[kAP], cn[kAK];
+    // ---------------- pass 1: fp32 screen, register-prefetched slabs ----------------
+    T xr[8];
+    double cr[2];
+    auto load_slab = [&](int d0) {
+        const int dl = min(kADC, n - d0);
 #pragma unroll
-    for (int t = 0; t < kAP; ++t) {
-        xn[t] = 0.f;
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + kSThreads * i, p = e >> 4, d = e & 15;
+            xr[i] = (p < np && d < dl) ? X[(p0 + p) * ld + d0 + d] : T(0);
+        }
 #pragma unroll
-        for (int u = 0; u < kAK; ++u) acc[t][u] = 0.f;
-    }
+        for (int i = 0; i < 2; ++i) {
+            const int e = tid + kSThreads * i, d = e >> 5, j = e & 31;
+            cr[i] = (j < KA && d < dl) ? Cact[static_cast<uint64_t>(j) * ldc + d0 + d] : 0.0;
+        }
+    };
+    auto store_slab = [&](int buf) {
 #pragma unroll
-    for (int u = 0; u < kAK; ++u) cn[u] = 0.f;
+        for (int i = 0; i < 8; ++i) {
+            const int e = tid + kSThreads * i;
+            S.u.p1.xs[buf][e & 15][e >> 4] = static_cast<float>(xr[i]);  // round to nearest
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int e = tid + kSThreads * i;
+            S.u.p1.cs[buf][e >> 5][e & 31] = __double2float_rn(cr[i]);
+        }
+    };
+    load_slab(0);
+    store_slab(0);
+    if (nslab > 1) load_slab(kADC);
+    __syncthreads();
 
-    issue_slab(S, 0, X, p0, np, ld, 0, n, Cact, KA);
+    float2 tot[2][kAK];  // points (4l, 4l+1) and (4l+2, 4l+3) x centroids 4w+u
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < kAK; ++u) tot[h][u] = make_float2(0.f, 0.f);
+    float nxl[4] = {0.f, 0.f, 0.f, 0.f}, nxh[4] = {0.f, 0.f, 0.f, 0.f};
+    float ncl = 0.f, nch = 0.f;
+
     for (int sl = 0; sl < nslab; ++sl) {
-        const int d0 = sl * kADC, dl = min(kADC, n - d0), buf = sl & 1;
-        if (sl + 1 < nslab) {
-            issue_slab(S, buf ^ 1, X, p0, np, ld, d0 + kADC, n, Cact, KA);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        // raw -> fp32 transposed slab (round to nearest), once per element
-        for (int e = tid; e < kABP * kADC; e += blockDim.x) {
-            const int p = e / kADC, d = e % kADC;
-            float v = 0.f;
-            if (p < np && d < dl) v = static_cast<float>(S.xraw[buf][p * RS + d]);
-            S.u.p1.xs[d][p] = v;
-        }
-        for (int e = tid; e < kADC * kSMaxK; e += blockDim.x) {
-            const int d = e / kSMaxK, j = e % kSMaxK;
-            S.u.p1.cs[d][j] = (j < KA && d < dl) ? __double2float_rn(S.craw[buf][e]) : 0.f;
-        }
-        __syncthreads();
-        if (cg * kAK < KA) {
+        const int buf = sl & 1, dl = min(kADC, n - sl * kADC);
+        if (comp) {
+            float2 part[2][kAK];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < kAK; ++u) part[h][u] = make_float2(0.f, 0.f);
 #pragma unroll 4
             for (int d = 0; d < dl; ++d) {
-                float xv[kAP], cv[kAK];
+                const float4 xv = *reinterpret_cast<const float4*>(&S.u.p1.xs[buf][d][4 * lane]);
+                const float4 cv = *reinterpret_cast<const float4*>(&S.u.p1.cs[buf][d][4 * warp]);
+                const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
+                part[0][0] = ffma2(xa, cv.x, part[0][0]);
+                part[0][1] = ffma2(xa, cv.y, part[0][1]);
+                part[0][2] = ffma2(xa, cv.z, part[0][2]);
+                part[0][3] = ffma2(xa, cv.w, part[0][3]);
+                part[1][0] = ffma2(xb, cv.x, part[1][0]);
+                part[1][1] = ffma2(xb, cv.y, part[1][1]);
+                part[1][2] = ffma2(xb, cv.z, part[1][2]);
+                part[1][3] = ffma2(xb, cv.w, part[1][3]);
+            }
 #pragma unroll
-                for (int t = 0; t < kAP; ++t) xv[t] = S.u.p1.xs[d][pg + kAPG * t];
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int u = 0; u < kAK; ++u) cv[u] = S.u.p1.cs[d][cg * kAK + u];
-#pragma unroll
-                for (int t = 0; t < kAP; ++t) {
-                    xn[t] = __fmaf_ru(xv[t], xv[t], xn[t]);
-#pragma unroll
-                    for (int u = 0; u < kAK; ++u) {
-                        const float df = __fsub_rn(xv[t], cv[u]);
-                        acc[t][u] = __fmaf_rn(df, df, acc[t][u]);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < kAK; ++u) cn[u] = __fmaf_ru(cv[u], cv[u], cn[u]);
+                for (int u = 0; u < kAK; ++u) tot[h][u] = fadd2(tot[h][u], part[h][u]);
+        }
+        if (normw) {
+            for (int d = 0; d < dl; ++d) {
+                const float4 xv = *reinterpret_cast<const float4*>(&S.u.p1.xs[buf][d][4 * lane]);
+                nxl[0] = __fmaf_rd(xv.x, xv.x, nxl[0]); nxh[0] = __fmaf_ru(xv.x, xv.x, nxh[0]);
+                nxl[1] = __fmaf_rd(xv.y, xv.y, nxl[1]); nxh[1] = __fmaf_ru(xv.y, xv.y, nxh[1]);
+                nxl[2] = __fmaf_rd(xv.z, xv.z, nxl[2]); nxh[2] = __fmaf_ru(xv.z, xv.z, nxh[2]);
+                nxl[3] = __fmaf_rd(xv.w, xv.w, nxl[3]); nxh[3] = __fmaf_ru(xv.w, xv.w, nxh[3]);
+                const float c = S.u.p1.cs[buf][d][lane];
+                ncl = __fmaf_rd(c, c, ncl);
+                nch = __fmaf_ru(c, c, nch);
             }
         }
-        __syncthreads();  // buffers of this slab are free for the next issue
-    }
-    // certified bounds
-    float un[kAP];
-#pragma unroll
-    for (int t = 0; t < kAP; ++t) un[t] = finf;
-    if (cg * kAK < KA) {
-        float cnorm[kAK];
-#pragma unroll
-        for (int u = 0; u < kAK; ++u) cnorm[u] = __fsqrt_ru(cn[u]);
-#pragma unroll
-        for (int t = 0; t < kAP; ++t) {
-            const float xnorm = __fsqrt_ru(xn[t]);
-#pragma unroll
-            for (int u = 0; u < kAK; ++u) {
-                const int j = cg * kAK + u;
-                if (j >= KA) continue;
-                const float dt = acc[t][u];
-                float L = 0.f, U = finf;
-                const float w = __fadd_ru(__fmul_ru(__fadd_ru(xnorm, cnorm[u]), cst.w_scale), cst.w_abs);
-                if (dt <= 3.0e38f && w <= 1.0e18f) {
-                    float rlo = __fmul_rd(__fsqrt_rd(__fmul_rd(dt, cst.inv_1p_gn_rd)), cst.inv_1pu_rd);
-                    rlo = fmaxf(__fsub_rd(rlo, w), 0.f);
-                    float rhi = __fmul_ru(__fsqrt_ru(__fmul_ru(dt, cst.inv_1m_gn_ru)), cst.inv_1mu_ru);
-                    rhi = __fadd_ru(rhi, w);
-                    L = __fmul_rd(__fmul_rd(rlo, rlo), cst.lo64);
-                    U = __fmul_ru(__fmul_ru(rhi, rhi), cst.hi64);
-                }
-                S.Ls[j * kABP + pg + kAPG * t] = L;
-                un[t] = fminf(un[t], U);
-            }
+        if (sl + 1 < nslab) {
+            store_slab(buf ^ 1);  // buf^1 was released by the previous iteration's barrier
+            if (sl + 2 < nslab) load_slab((sl + 2) * kADC);
         }
+        __syncthreads();
     }
+    if (normw) {
 #pragma unroll
-    for (int t = 0; t < kAP; ++t) S.red_u[cg * kABP + pg + kAPG * t] = un[t];
+        for (int q = 0; q < 4; ++q) {
+            S.nx_lo[4 * lane + q] = nxl[q];
+            S.nx_hi[4 * lane + q] = nxh[q];
+            S.nxr[4 * lane + q] = __fsqrt_ru(nxh[q]);
+        }
+        S.nc_lo[lane] = ncl;
+        S.nc_hi[lane] = nch;
+        S.ncr[lane] = __fsqrt_ru(nch);
+    }
     __syncthreads();
-    for (int p = tid; p < kABP; p += blockDim.x) {
+    // certified bounds
+    if (comp) {
+        float un[4] = {finf, finf, finf, finf};
+#pragma unroll
+        for (int u = 0; u < kAK; ++u) {
+            const int j = kAK * warp + u;
+            if (j >= KA) continue;
+            const float cl = S.nc_lo[j], ch = S.nc_hi[j], crr = S.ncr[j];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int p = 4 * lane + q;
+                const float sdot = q & 1 ? tot[q >> 1][u].y : tot[q >> 1][u].x;
+                const float t2 = 2.f * sdot;  // exact
+                const float Sn = __fadd_ru(S.nxr[p], crr);
+                const float Al = __fadd_rd(S.nx_lo[p], cl), Ah = __fadd_ru(S.nx_hi[p], ch);
+                float L = 0.f, U = finf;
+                if (fabsf(t2) <= 1.0e37f && Sn <= 1.0e18f && Ah <= 1.0e37f) {
+                    const float D = __fadd_ru(__fmul_ru(__fmul_ru(cst.K, Sn), Sn), cst.dabs);
+                    L = fmaxf(__fsub_rd(__fsub_rd(Al, t2), D), 0.f);
+                    L = __fmul_rd(L, cst.lo64);
+                    U = __fmul_ru(__fadd_ru(__fsub_ru(Ah, t2), D), cst.hi64);
+                }
+                S.Ls[j][p] = L;
+                un[q] = fminf(un[q], U);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S.red_u[warp][4 * lane + q] = un[q];
+    }
+    __syncthreads();
+    if (tid < kABP) {
+        const int p = tid;
         float m = finf;
-        for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g * kABP + p]);
+        for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][p]);
         S.umin[p] = m;
         int c = 0;
         if (p < np)
-            for (int j = 0; j < KA; ++j) c += S.Ls[j * kABP + p] <= m;
+            for (int j = 0; j < KA; ++j) c += S.Ls[j][p] <= m;
         S.icount[p] = c;
     }
     __syncthreads();
-    if (tid == 0) {  // item offsets: points in order, candidates ascending j
-        uint32_t r = 0;
-        for (int p = 0; p < kABP; ++p) {
-            const int c = S.icount[p];
-            S.icount[p] = r;
-            r += c;
+    if (tid < 32) {  // exclusive scan of the 128 counts -> item offsets
+        int v[4], run = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = S.icount[4 * tid + q];
+            run += v[q];
         }
-        S.n_items = r;
-        if (cand_counter) atomicAdd(cand_counter, static_cast<unsigned long long>(r));
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        int ex = incl - run;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            S.icount[4 * tid + q] = ex;
+            ex += v[q];
+        }
+        if (tid == 31) {
+            S.n_items = static_cast<uint32_t>(incl);
+            if (cand_counter) atomicAdd(cand_counter, static_cast<unsigned long long>(incl));
+        }
     }
     __syncthreads();
     const uint32_t NI = S.n_items;
     const bool overflow = NI > static_cast<uint32_t>(kItemCap);
 
-    // ---------------- pass 2: exact fp64 recheck of the candidate items ----------------
+    // ---------------- pass 2: exact fp64 recheck of the candidates ----------------
     if (!overflow) {
-        for (int p = tid; p < np; p += blockDim.x) {
+        if (tid < np) {
+            const int p = tid;
             const float m = S.umin[p];
             uint32_t it = S.icount[p];
             for (int j = 0; j < KA; ++j)
-                if (S.Ls[j * kABP + p] <= m) {
+                if (S.Ls[j][p] <= m) {
                     S.u.p2.item_p[it] = static_cast<short>(p);
                     S.u.p2.item_j[it] = static_cast<signed char>(j);
                     ++it;
                 }
         }
-        const uint32_t per_round = kSItems * blockDim.x;
-        for (uint32_t base = 0; base < NI; base += per_round) {
-            __syncthreads();  // items complete / previous round done with the buffers
-            double sum[kSItems];
-            int ip[kSItems], ij[kSItems];
+        __syncthreads();
+        for (uint32_t i = tid; i < NI; i += kSThreads) {
+            const int p = S.u.p2.item_p[i], j = S.u.p2.item_j[i];
+            const T* xrow = X + (p0 + p) * ld;
+            const double* crow = Cact + static_cast<uint64_t>(j) * ldc;
+            double a = 0.0;
+            int d = 0;
+            for (; d + 8 <= n; d += 8) {
+                double xv[8], cv[8];
+                if constexpr (sizeof(T) == 8) {
 #pragma unroll
-            for (int r = 0; r < kSItems; ++r) {
-                const uint32_t i = base + tid + r * blockDim.x;
-                sum[r] = 0.0;
-                ip[r] = i < NI ? S.u.p2.item_p[i] : -1;
-                ij[r] = i < NI ? S.u.p2.item_j[i] : 0;
-            }
-            issue_slab(S, 0, X, p0, np, ld, 0, n, Cact, KA);
-            for (int sl = 0; sl < nslab; ++sl) {
-                const int d0 = sl * kADC, dl = min(kADC, n - d0), buf = sl & 1;
-                if (sl + 1 < nslab) {
-                    issue_slab(S, buf ^ 1, X, p0, np, ld, d0 + kADC, n, Cact, KA);
-                    cp_async_wait<1>();
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 t = *reinterpret_cast<const double2*>(xrow + d + 2 * q);
+                        xv[2 * q] = t.x;
+                        xv[2 * q + 1] = t.y;
+                    }
                 } else {
-                    cp_async_wait<0>();
-                }
-                __syncthreads();
 #pragma unroll
-                for (int r = 0; r < kSItems; ++r) {
-                    if (ip[r] < 0) continue;
-                    const T* xr = &S.xraw[buf][ip[r] * RS];
-                    const double* cr = &S.craw[buf][ij[r]];
-                    double a = sum[r];
-                    for (int d = 0; d < dl; ++d) a = dist_step(a, to_f64(xr[d]), cr[d * kSMaxK]);
-                    sum[r] = a;
+                    for (int q = 0; q < 2; ++q) {
+                        const float4 t = *reinterpret_cast<const float4*>(xrow + d + 4 * q);
+                        xv[4 * q] = t.x;
+                        xv[4 * q + 1] = t.y;
+                        xv[4 * q + 2] = t.z;
+                        xv[4 * q + 3] = t.w;
+                    }
                 }
-                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(crow + d + 2 * q));
+                    cv[2 * q] = t.x;
+                    cv[2 * q + 1] = t.y;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) a = dist_step(a, xv[q], cv[q]);
             }
-#pragma unroll
-            for (int r = 0; r < kSItems; ++r)
-                if (ip[r] >= 0) S.u.p2.item_d[base + tid + r * blockDim.x] = sum[r];
+            for (; d < n; ++d) a = dist_step(a, to_f64(xrow[d]), crow[d]);
+            S.u.p2.item_d[i] = a;
         }
         __syncthreads();
     }
-    for (int p = tid; p < np; p += blockDim.x) {
+    if (tid < np) {
+        const int p = tid;
         const uint64_t gp = p0 + p;
         double best = __longlong_as_double(0x7FF0000000000000LL);
         int bj = -1;
@@ -651,7 +691,7 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         } else {  // candidate sets too large for the item buffer: full exact scan
             const T* x = X + gp * ld;
             for (int j = 0; j < KA; ++j) {
-                const double* c = Cact + static_cast<uint64_t>(j) * n;
+                const double* c = Cact + static_cast<uint64_t>(j) * ldc;
                 double sm = 0.0;
                 for (int d = 0; d < n; ++d) sm = dist_step(sm, to_f64(x[d]), c[d]);
                 if (sm < best) {
@@ -681,8 +721,8 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     __threadfence();
     const uint64_t tb = tile * kTile;
     const int len = static_cast<int>(min(rows, tb + kTile) - tb);
-    double* fold = reinterpret_cast<double*>(S.xraw[0]);  // >= 8 KB
-    for (int i = tid; i < len; i += blockDim.x) fold[i] = __ldcg(dists_out + tb + i);
+    double* fold = S.u.fold;
+    for (int i = tid; i < len; i += kSThreads) fold[i] = __ldcg(dists_out + tb + i);
     __syncthreads();
     if (tid == 0) {
         double a = 0.0;
@@ -703,8 +743,7 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     }
 }
 
-template <typename T>
-constexpr size_t screen_smem_bytes() { return sizeof(ScreenSmem<T>); }
+constexpr size_t screen_smem_bytes() { return sizeof(ScreenSmem); }
 
 // ===========================================================================
 // 4. Per-tile sequential sums (block_sum inner loop core.cpp:167-173).
@@ -842,7 +881,7 @@ k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
 __global__ void __launch_bounds__(kUThreads)
 k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcnt, uint64_t ntiles,
                int k, int n, double* __restrict__ C, uint8_t* __restrict__ mask,
-               double* __restrict__ Cact, int* __restrict__ act_idx, int* __restrict__ n_active,
+               double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
                const int* __restrict__ stop_ptr) {
     if (stop_ptr && *stop_ptr) return;
     extern __shared__ unsigned long long msh[];
@@ -881,13 +920,13 @@ k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcn
         const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
         const double v = __dmul_rn(acc, inv);
         C[e] = v;
-        Cact[static_cast<uint64_t>(rank[j]) * n + d] = v;
+        Cact[static_cast<uint64_t>(rank[j]) * ldc + d] = v;
     }
 }
 
 // Compact the active rows of (C, mask) for the assignment (single CTA).
 __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restrict__ mask, int k, int n,
-                          double* __restrict__ Cact, int* __restrict__ act_idx, int* __restrict__ n_active) {
+                          double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active) {
     extern __shared__ int csh[];
     if (threadIdx.x == 0) {
         int r = 0;
@@ -900,7 +939,7 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
     __syncthreads();
     for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
         const int j = e / n;
-        if (csh[j] >= 0) Cact[static_cast<uint64_t>(csh[j]) * n + (e % n)] = C[e];
+        if (csh[j] >= 0) Cact[static_cast<uint64_t>(csh[j]) * ldc + (e % n)] = C[e];
     }
 }
 
