@@ -174,6 +174,10 @@ typedef struct bm_profile {
     uint64_t final_rows;
     uint64_t screen_candidates; /* exact rechecks issued by the screened assignment */
     uint64_t screen_rows;       /* rows that went through the screened assignment */
+    /* per launch group: 0 assign (chunk loop), 1 final pass, 2 update, 3 sample,
+     * 4 gather, 5 k-means++ distances, 6 Lloyd control */
+    double phase_ms[8];
+    uint64_t phase_count[8];
 } bm_profile;
 bm_status bm_set_profiling(int enabled);
 bm_status bm_last_profile(bm_profile* out);

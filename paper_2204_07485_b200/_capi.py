@@ -45,7 +45,8 @@ class bm_chunk_record(C.Structure):
 class bm_profile(C.Structure):
     _fields_ = [("assign_ms_total", dbl), ("assign_launches", u64),
                 ("assign_rows_total", u64), ("kernel_launches", u64), ("final_ms", dbl),
-                ("final_rows", u64), ("screen_candidates", u64), ("screen_rows", u64)]
+                ("final_rows", u64), ("screen_candidates", u64), ("screen_rows", u64),
+                ("phase_ms", dbl * 8), ("phase_count", u64 * 8)]
 
 
 # name -> (restype, argtypes)

@@ -496,4 +496,8 @@ def set_profiling(enabled: bool) -> None:
 def last_profile() -> dict:
     p = _capi.bm_profile()
     _check(_capi.load().bm_last_profile(C.byref(p)))
-    return {f: getattr(p, f) for f, _ in p._fields_}
+    out = {f: getattr(p, f) for f, _ in p._fields_}
+    names = ["assign", "final", "update", "sample", "gather", "kmeanspp", "control"]
+    out["phase_ms"] = {nm: out["phase_ms"][i] for i, nm in enumerate(names)}
+    out["phase_count"] = {nm: int(out["phase_count"][i]) for i, nm in enumerate(names)}
+    return out

@@ -305,22 +305,25 @@ Workspace& get_ws(const bm_dataset* d, uint64_t rows, int k, int ncand, uint64_t
 // ---------------------------------------------------------------------------
 // Kernel launch wrappers
 // ---------------------------------------------------------------------------
-struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
+// CUDA-event timing of the launch groups of one big_means call (roofline and
+// step-share reporting): events are recorded on the engine stream around
+// every launch group while profiling is enabled.
+enum Phase { PH_ASSIGN = 0, PH_FINAL, PH_UPDATE, PH_SAMPLE, PH_GATHER, PH_KMEANSPP, PH_CONTROL, PH_COUNT };
+
+struct Profiler {
     std::vector<cudaEvent_t> pool;  // reused across calls: no per-launch creation
     size_t used = 0;
     std::vector<uint64_t> rows;
-    std::vector<int> final_flag;
+    std::vector<int> kind;
     cudaStream_t stream = nullptr;
-    unsigned long long* d_cand = nullptr;  // device tally of screened candidates
-    uint64_t screen_rows = 0;
+    unsigned long long* d_cand = nullptr;  // [0] screened candidates, [1] screened rows
     void begin(cudaStream_t s) {
         stream = s;
         used = 0;
         rows.clear();
-        final_flag.clear();
-        screen_rows = 0;
-        if (!d_cand) BM_CUDA(cudaMalloc(&d_cand, sizeof(unsigned long long)));
-        BM_CUDA(cudaMemsetAsync(d_cand, 0, sizeof(unsigned long long), s));
+        kind.clear();
+        if (!d_cand) BM_CUDA(cudaMalloc(&d_cand, 2 * sizeof(unsigned long long)));
+        BM_CUDA(cudaMemsetAsync(d_cand, 0, 2 * sizeof(unsigned long long), s));
     }
     cudaEvent_t next() {
         if (used == pool.size()) {
@@ -335,36 +338,51 @@ struct Profiler {  // CUDA-event timing of assignment launches (roofline report)
         BM_CUDA(cudaEventRecord(a, stream));
         return {a, b};
     }
-    void record_end(std::pair<cudaEvent_t, cudaEvent_t> p, uint64_t r, bool fin) {
+    void record_end(std::pair<cudaEvent_t, cudaEvent_t> p, uint64_t r, int k) {
         BM_CUDA(cudaEventRecord(p.second, stream));
         rows.push_back(r);
-        final_flag.push_back(fin);
+        kind.push_back(k);
     }
     void flush(bm_profile& out) {
         for (size_t i = 0; i < rows.size(); ++i) {
             float ms = 0;
             BM_CUDA(cudaEventSynchronize(pool[2 * i + 1]));
             BM_CUDA(cudaEventElapsedTime(&ms, pool[2 * i], pool[2 * i + 1]));
-            if (final_flag[i]) {
+            out.phase_ms[kind[i]] += ms;
+            out.phase_count[kind[i]] += 1;
+            if (kind[i] == PH_FINAL) {
                 out.final_ms += ms;
                 out.final_rows += rows[i];
-            } else {
+            } else if (kind[i] == PH_ASSIGN) {
                 out.assign_ms_total += ms;
                 out.assign_launches += 1;
                 out.assign_rows_total += rows[i];
             }
         }
-        unsigned long long cand = 0;
-        BM_CUDA(cudaMemcpyAsync(&cand, d_cand, sizeof(cand), cudaMemcpyDeviceToHost, stream));
+        unsigned long long cand[2] = {0, 0};
+        BM_CUDA(cudaMemcpyAsync(cand, d_cand, sizeof(cand), cudaMemcpyDeviceToHost, stream));
         BM_CUDA(cudaStreamSynchronize(stream));
-        out.screen_candidates += cand;
-        out.screen_rows += screen_rows;
+        out.screen_candidates += cand[0];
+        out.screen_rows += cand[1];
         used = 0;
         rows.clear();
-        final_flag.clear();
+        kind.clear();
     }
 };
 thread_local Profiler g_prof;
+
+// RAII event bracket around a launch group (no-op unless profiling).
+struct PhaseScope {
+    int k;
+    uint64_t r;
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    PhaseScope(int kind_, uint64_t rows_) : k(kind_), r(rows_) {
+        if (g_profiling) ev = g_prof.record_start();
+    }
+    ~PhaseScope() {
+        if (g_profiling) g_prof.record_end(ev, r, k);
+    }
+};
 
 
 void count_launch(uint64_t n = 1) { g_profile.kernel_launches += n; }
@@ -425,8 +443,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                    unsigned* tile_ctr = nullptr) {
     const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
     if (grid == 0) return;
-    std::pair<cudaEvent_t, cudaEvent_t> ev{};
-    if (g_profiling) ev = g_prof.record_start();
+    PhaseScope ps(final_pass ? PH_FINAL : PH_ASSIGN, P.rows);
     const bool screen = screen_enabled(k);
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
@@ -442,7 +459,6 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out,
                 tile_ctr, g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
-            if (g_profiling) g_prof.screen_rows += P.rows;
         } else {
             dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active,
@@ -451,7 +467,6 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     });
     BM_LAUNCH();
     count_launch();
-    if (g_profiling) g_prof.record_end(ev, P.rows, final_pass);
     if (tile_out && !screen) launch_tile_sums(st, dists, P.rows, 0, 1, tile_out, stop);
 }
 
@@ -472,27 +487,31 @@ void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_
 }
 
 void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* parity, const int* stop) {
+    PhaseScope ps(PH_UPDATE, P.rows);
     const int k = w.k, n = w.n;
     const uint64_t tiles = tiles_of(P.rows);
     // d-slab so that the grid covers the GPU even when there are few tiles.
     int slabs = 1;
-    while (tiles * slabs < 296 && n / (slabs * 2) >= 16) slabs *= 2;
+    while (tiles * slabs < 444 && n / (slabs * 2) >= 4) slabs *= 2;
     const int dslab = (int)ceil_div(n, slabs);
     dim3 grid((unsigned)tiles, (unsigned)ceil_div(n, dslab));
-    const size_t shm = (2 * kTile + 3 * k) * sizeof(int);
+    const size_t shm = kTile * sizeof(short) + (2 * k + dev::kUChunks * k) * sizeof(int);
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
+        if (shm > 48 * 1024)
+            BM_CUDA(cudaFuncSetAttribute(dev::k_update_partials<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)shm));
         dev::k_update_partials<T><<<grid, dev::kUThreads, shm, st>>>(
             static_cast<const T*>(P.X), P.rows, n, P.ld, w.labels.p, w.R, parity, k, dslab, w.psum.p,
             w.pcnt.p, &w.status.p->bad_label, stop);
     });
     BM_LAUNCH();
-    const uint64_t pairs = (uint64_t)k * n;
-    const unsigned mgrid = (unsigned)std::min<uint64_t>(ceil_div(pairs, dev::kUThreads), 1024);
-    const size_t mshm = k * (sizeof(unsigned long long) + sizeof(int));
-    dev::k_update_merge<<<mgrid, dev::kUThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p,
-                                                            w.mask.p, w.Cact.p, w.ldc, w.act.p,
-                                                            &w.status.p->n_active, stop);
+    dim3 mgrid((unsigned)k, (unsigned)ceil_div(n, dev::kMThreads));
+    const size_t mshm = k * sizeof(unsigned long long) + tiles * sizeof(int);
+    if (mshm > 48 * 1024)
+        BM_CUDA(cudaFuncSetAttribute(dev::k_update_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mshm));
+    dev::k_update_merge<<<mgrid, dev::kMThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p, w.mask.p,
+                                                            w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active, stop);
     BM_LAUNCH();
     count_launch(2);
 }
@@ -525,6 +544,7 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
     launch_update(st, P, w, parity, stop);                                                 // :33
     launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop, false,
                   w.tile_buf.p, w.tile_ctr.p);  // :34-35
+    PhaseScope ps(PH_CONTROL, 0);
     dev::k_lloyd_step<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows, max_it,
                                         tol, w.hist_cap ? w.history.p : nullptr);
     BM_LAUNCH();
@@ -583,6 +603,7 @@ void set_row_any(cudaStream_t st, const Points& P, Workspace& w, uint64_t row, i
 
 void launch_dist_rows(cudaStream_t st, const Points& P, const uint32_t* cand, int ncand, const double* d2,
                       double* out) {
+    PhaseScope ps(PH_KMEANSPP, P.rows);
     const unsigned grid = (unsigned)ceil_div(P.rows, 128);
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
@@ -716,6 +737,7 @@ uint32_t* draw_targets(SamplerWs& sw, std::mt19937_64& rng) {
 
 // Enqueue resolution of the drawn targets in buffer sw.cur; result in sw.idx.
 void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
+    PhaseScope ps(PH_SAMPLE, sw.s);
     const int b = sw.cur;
     const uint32_t s = (uint32_t)sw.s;
     BM_CUDA(cudaMemcpyAsync(sw.js.p, sw.h_js[b].p, s * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
@@ -741,6 +763,7 @@ void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
 }
 
 void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
+    PhaseScope ps(PH_GATHER, s);
     const uint64_t row_vecs = d->ld * dtype_size(d->dtype) / 16;
     const unsigned grid = (unsigned)ceil_div((uint64_t)s * 32, 256);
     dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X), row_vecs, idx, s,

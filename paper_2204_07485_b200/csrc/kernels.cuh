@@ -615,7 +615,10 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         }
         if (tid == 31) {
             S.n_items = static_cast<uint32_t>(incl);
-            if (cand_counter) atomicAdd(cand_counter, static_cast<unsigned long long>(incl));
+            if (cand_counter) {
+                atomicAdd(cand_counter, static_cast<unsigned long long>(incl));
+                atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
+            }
         }
     }
     __syncthreads();
@@ -798,7 +801,14 @@ __device__ __forceinline__ double fold_tiles(const double* tiles, uint64_t ntile
 // (:237-239); count 0 -> degenerate row of 0.0 (:231 all_degenerate).
 // ===========================================================================
 constexpr int kUThreads = 256;
+constexpr int kUChunks = kTile / 32;  // 32-point chunks per tile
 
+// Phase A: grid (tile, d-slab).  Stable bucketing: every warp ranks the points
+// of its 32-point chunks with __match_any_sync; a per-label exclusive prefix
+// over the chunks gives each (chunk, label) its base, so `order` lists each
+// label's members in index order.  Then one thread per (label, dim) folds its
+// members' coordinates from 0.0 in that order, with the member loads issued
+// in independent batches ahead of the dependent adds.
 template <typename T>
 __global__ void __launch_bounds__(kUThreads)
 k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
@@ -808,120 +818,171 @@ k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                   const int* __restrict__ stop_ptr) {
     if (stop_ptr && *stop_ptr) return;
     extern __shared__ int ush[];
-    int* lab = ush;                 // [kTile]
-    int* order = lab + kTile;       // [kTile]
-    int* cnt = order + kTile;       // [k]
-    int* off = cnt + k;             // [k]
-    int* run = off + k;             // [k]
+    short* order = reinterpret_cast<short*>(ush);      // [kTile]
+    int* cnt = ush + kTile / 2;                         // [k] tile totals
+    int* off = cnt + k;                                 // [k] label offsets in `order`
+    int* ccount = off + k;                              // [kUChunks][k] per-chunk counts -> bases
 
     const int32_t* labels = labels_pair + (parity_ptr ? (*parity_ptr) * pair_stride : 0);
     const uint64_t tile = blockIdx.x;
     const uint64_t b = tile * kTile;
-    const int len = static_cast<int>(min((uint64_t)kTile, rows - b));
+    const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), rows - b));
     const int d0 = blockIdx.y * dslab;
     const int d1 = min(n, d0 + dslab);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    for (int j = threadIdx.x; j < k; j += blockDim.x) cnt[j] = 0;
+    for (int e = threadIdx.x; e < kUChunks * k; e += blockDim.x) ccount[e] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-        int l = labels[b + i];
-        if (l < 0 || l >= k) {  // update_centroids label range check (core.cpp:189-193)
-            *bad_label = 1;
-            l = 0;
+    // per-chunk label counts and in-chunk ranks
+    int lab_r[kUChunks / (kUThreads / 32)], rank_r[kUChunks / (kUThreads / 32)];
+#pragma unroll
+    for (int q = 0; q < kUChunks / (kUThreads / 32); ++q) {
+        const int c = warp + (kUThreads / 32) * q;
+        const int i = c * 32 + lane;
+        int l = -1 - lane;
+        if (i < len) {
+            l = labels[b + i];
+            if (l < 0 || l >= k) {  // update_centroids label range check (core.cpp:189-193)
+                *bad_label = 1;
+                l = 0;
+            }
         }
-        lab[i] = l;
-        atomicAdd(&cnt[l], 1);
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, l);
+        lab_r[q] = l;
+        rank_r[q] = __popc(peers & ((1u << lane) - 1u));
+        if (i < len && lane == __ffs(peers) - 1) ccount[c * k + l] = __popc(peers);
+    }
+    __syncthreads();
+    // exclusive prefix over chunks per label; tile totals
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        int r = 0;
+        for (int c = 0; c < kUChunks; ++c) {
+            const int v = ccount[c * k + j];
+            ccount[c * k + j] = r;
+            r += v;
+        }
+        cnt[j] = r;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         int r = 0;
         for (int j = 0; j < k; ++j) {
             off[j] = r;
-            run[j] = r;
             r += cnt[j];
         }
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // stable placement, one warp, index order
-        const int lane = threadIdx.x;
-        for (int c0 = 0; c0 < len; c0 += 32) {
-            const int i = c0 + lane;
-            const bool valid = i < len;
-            const int l = valid ? lab[i] : -1 - lane;
-            const unsigned peers = __match_any_sync(0xFFFFFFFFu, l);
-            const int rank = __popc(peers & ((1u << lane) - 1u));
-            const int leader = __ffs(peers) - 1;
-            int basev = 0;
-            if (valid && lane == leader) basev = run[l];
-            basev = __shfl_sync(0xFFFFFFFFu, basev, leader);
-            if (valid) order[basev + rank] = i;
-            __syncwarp();
-            if (valid && lane == leader) run[l] = basev + __popc(peers);
-            __syncwarp();
-        }
+#pragma unroll
+    for (int q = 0; q < kUChunks / (kUThreads / 32); ++q) {
+        const int c = warp + (kUThreads / 32) * q;
+        const int i = c * 32 + lane;
+        if (i < len) order[off[lab_r[q]] + ccount[c * k + lab_r[q]] + rank_r[q]] = static_cast<short>(i);
     }
     __syncthreads();
     const int dl = d1 - d0;
+    if (blockIdx.y == 0)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) pcnt[tile * k + j] = cnt[j];
     if (dl <= 0) return;
+    const T* Xt = X + b * ld;
     for (int e = threadIdx.x; e < k * dl; e += blockDim.x) {
         const int j = e / dl, d = d0 + e % dl;
         const int c = cnt[j];
         if (c == 0) continue;
-        const int o = off[j];
+        const short* ord = order + off[j];
         double acc = 0.0;
-#pragma unroll 4
-        for (int q = 0; q < c; ++q)
-            acc = __dadd_rn(acc, to_f64(X[(b + order[o + q]) * ld + d]));
+        int q = 0;
+        for (; q + 8 <= c; q += 8) {
+            double v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = to_f64(Xt[static_cast<uint64_t>(ord[q + r]) * ld + d]);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) acc = __dadd_rn(acc, v[r]);
+        }
+        for (; q < c; ++q) acc = __dadd_rn(acc, to_f64(Xt[static_cast<uint64_t>(ord[q]) * ld + d]));
         psum[(tile * k + j) * n + d] = acc;
     }
-    if (blockIdx.y == 0)
-        for (int j = threadIdx.x; j < k; j += blockDim.x) pcnt[tile * k + j] = cnt[j];
 }
 
-__global__ void __launch_bounds__(kUThreads)
+// Phase B: grid (label j, 128-dim block).  Each CTA recomputes the label
+// totals and active ranks (integers: order-free), then one thread per dim
+// folds the non-empty tile partials of label j in tile order (:217-229),
+// loads issued in batches ahead of the adds, and applies sum * (1.0/count)
+// (:237-239); count 0 -> degenerate row of 0.0 (:231).
+constexpr int kMThreads = 128;
+
+__global__ void __launch_bounds__(kMThreads)
 k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcnt, uint64_t ntiles,
                int k, int n, double* __restrict__ C, uint8_t* __restrict__ mask,
                double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
                const int* __restrict__ stop_ptr) {
     if (stop_ptr && *stop_ptr) return;
     extern __shared__ unsigned long long msh[];
-    unsigned long long* total = msh;                          // [k]
-    int* rank = reinterpret_cast<int*>(total + k);             // [k]
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        unsigned long long c = 0;
-        for (uint64_t t = 0; t < ntiles; ++t) c += pcnt[t * k + j];
-        total[j] = c;
+    unsigned long long* total = msh;                         // [k]
+    int* tl = reinterpret_cast<int*>(total + k);             // nonempty tiles of label j
+    __shared__ int ntl, rankj;
+    const int j = blockIdx.x;
+    for (int jj = threadIdx.x; jj < k; jj += blockDim.x) total[jj] = 0;
+    if (threadIdx.x == 0) ntl = 0;
+    __syncthreads();
+    for (uint64_t e = threadIdx.x; e < ntiles * k; e += blockDim.x) {
+        const uint32_t c = pcnt[e];
+        if (c) atomicAdd(&total[e % k], static_cast<unsigned long long>(c));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         int r = 0;
-        for (int j = 0; j < k; ++j) {
-            rank[j] = total[j] ? r : -1;
-            if (total[j]) {
-                if (blockIdx.x == 0) act_idx[r] = j;
-                ++r;
+        for (int jj = 0; jj < j; ++jj) r += total[jj] != 0;
+        rankj = r;
+        if (blockIdx.y == 0) {
+            mask[j] = total[j] ? 0 : 1;
+            if (total[j]) act_idx[r] = j;
+            if (j == k - 1) *n_active = r + (total[j] != 0);
+        }
+    }
+    // nonempty tiles of j in ascending order (ballot compaction, 128 per round)
+    __shared__ int wbase[kMThreads / 32];
+    for (uint64_t t0 = 0; t0 < ntiles; t0 += kMThreads) {
+        const uint64_t t = t0 + threadIdx.x;
+        const bool f = t < ntiles && pcnt[t * k + j] != 0;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, f);
+        const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+        if (ln == 0) wbase[wid] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int r = ntl;
+            for (int w = 0; w < kMThreads / 32; ++w) {
+                const int c = wbase[w];
+                wbase[w] = r;
+                r += c;
             }
-            if (blockIdx.x == 0) mask[j] = total[j] ? 0 : 1;
+            ntl = r;
         }
-        if (blockIdx.x == 0) *n_active = r;
+        __syncthreads();
+        if (f) tl[wbase[wid] + __popc(bal & ((1u << ln) - 1u))] = static_cast<int>(t);
+        __syncthreads();
     }
-    __syncthreads();
-    const uint64_t pairs = static_cast<uint64_t>(k) * n;
-    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < pairs;
-         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(e / n), d = static_cast<int>(e % n);
-        if (total[j] == 0) {
-            C[e] = 0.0;
-            continue;
-        }
-        double acc = 0.0;
-        for (uint64_t t = 0; t < ntiles; ++t)
-            if (pcnt[t * k + j]) acc = __dadd_rn(acc, psum[(t * k + j) * n + d]);
-        const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
-        const double v = __dmul_rn(acc, inv);
-        C[e] = v;
-        Cact[static_cast<uint64_t>(rank[j]) * ldc + d] = v;
+    const int d = blockIdx.y * kMThreads + threadIdx.x;
+    if (d >= n) return;
+    const uint64_t e = static_cast<uint64_t>(j) * n + d;
+    if (total[j] == 0) {
+        C[e] = 0.0;
+        return;
     }
+    const int cnt = ntl;
+    double acc = 0.0;
+    int q = 0;
+    for (; q + 8 <= cnt; q += 8) {
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = psum[(static_cast<uint64_t>(tl[q + r]) * k + j) * n + d];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc = __dadd_rn(acc, v[r]);
+    }
+    for (; q < cnt; ++q) acc = __dadd_rn(acc, psum[(static_cast<uint64_t>(tl[q]) * k + j) * n + d]);
+    const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
+    const double v = __dmul_rn(acc, inv);
+    C[e] = v;
+    Cact[static_cast<uint64_t>(rankj) * ldc + d] = v;
 }
 
 // Compact the active rows of (C, mask) for the assignment (single CTA).
