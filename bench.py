@@ -202,6 +202,14 @@ def main():
     for _ in range(args.warmup):
         step()
 
+    # ---- untimed-profile reference: the same steps without event brackets ----
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    unprofiled_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+
     # ---- timed region (device-resident inputs) ----
     bm.set_profiling(True)
     clocks = Clocks(local)
@@ -229,6 +237,10 @@ def main():
     s_cand = sum(r["prof"]["screen_candidates"] for r in res)
     s_rows = sum(r["prof"]["screen_rows"] for r in res)
     objective = res[-1]["objective"]
+    phases = {nm: sum(r["prof"]["phase_ms"][nm] for r in res) / args.steps
+              for nm in res[0]["prof"]["phase_ms"]}
+    phase_n = {nm: sum(r["prof"]["phase_count"][nm] for r in res) / args.steps
+               for nm in res[0]["prof"]["phase_count"]}
     if world > 1:
         t = torch.tensor([ms, evals, chunks], dtype=torch.float64, device=dev)
         mx = t.clone()
@@ -327,6 +339,9 @@ def main():
           "subproblems_per_s": chunks / (ms * 1e-3),
           "final_sse_rel_gap": gap, "objective": objective,
           "gpu_launches": launches, "clocks": ck, "e2e": e2e, "roofline": roofline,
+          "step_breakdown_ms": {nm: round(v, 3) for nm, v in phases.items()},
+          "step_breakdown_launch_groups": phase_n,
+          "ms_per_step_unprofiled": unprofiled_ms,
           "cpu_baseline": cpu})
 
 
