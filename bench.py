@@ -202,16 +202,7 @@ def main():
     for _ in range(args.warmup):
         step()
 
-    # ---- untimed-profile reference: the same steps without event brackets ----
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize()
-    unprofiled_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-
-    # ---- timed region (device-resident inputs) ----
-    bm.set_profiling(True)
+    # ---- timed region (device-resident inputs, no event brackets inside) ----
     clocks = Clocks(local)
     clocks.start()
     barrier()
@@ -224,29 +215,37 @@ def main():
     torch.cuda.synchronize()
     barrier()
     ck = clocks.stop()
-    bm.set_profiling(False)
     ms = e0.elapsed_time(e1)
     evals = sum(r["evals"] for r in res)
     chunks = sum(r["chunks"] for r in res)
     launches = sum(r["launches"] for r in res)
-    a_ms = sum(r["prof"]["assign_ms_total"] for r in res)
-    a_n = sum(r["prof"]["assign_launches"] for r in res)
-    a_rows = sum(r["prof"]["assign_rows_total"] for r in res)
-    f_ms = sum(r["prof"]["final_ms"] for r in res)
-    f_rows = sum(r["prof"]["final_rows"] for r in res)
-    s_cand = sum(r["prof"]["screen_candidates"] for r in res)
-    s_rows = sum(r["prof"]["screen_rows"] for r in res)
     objective = res[-1]["objective"]
-    phases = {nm: sum(r["prof"]["phase_ms"][nm] for r in res) / args.steps
-              for nm in res[0]["prof"]["phase_ms"]}
-    phase_n = {nm: sum(r["prof"]["phase_count"][nm] for r in res) / args.steps
-               for nm in res[0]["prof"]["phase_count"]}
     if world > 1:
         t = torch.tensor([ms, evals, chunks], dtype=torch.float64, device=dev)
         mx = t.clone()
         torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(t)
         ms, evals, chunks = float(mx[0]), int(t[1]), int(t[2])
+
+    # ---- profiled pass: CUDA events around every launch group (roofline) ----
+    bm.set_profiling(True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pres = [step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    profiled_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    bm.set_profiling(False)
+    a_ms = sum(r["prof"]["assign_ms_total"] for r in pres)
+    a_n = sum(r["prof"]["assign_launches"] for r in pres)
+    a_rows = sum(r["prof"]["assign_rows_total"] for r in pres)
+    f_ms = sum(r["prof"]["final_ms"] for r in pres)
+    f_rows = sum(r["prof"]["final_rows"] for r in pres)
+    s_cand = sum(r["prof"]["screen_candidates"] for r in pres)
+    s_rows = sum(r["prof"]["screen_rows"] for r in pres)
+    phases = {nm: sum(r["prof"]["phase_ms"][nm] for r in pres) / args.steps
+              for nm in pres[0]["prof"]["phase_ms"]}
+    phase_n = {nm: sum(r["prof"]["phase_count"][nm] for r in pres) / args.steps
+               for nm in pres[0]["prof"]["phase_count"]}
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
@@ -341,7 +340,7 @@ def main():
           "gpu_launches": launches, "clocks": ck, "e2e": e2e, "roofline": roofline,
           "step_breakdown_ms": {nm: round(v, 3) for nm, v in phases.items()},
           "step_breakdown_launch_groups": phase_n,
-          "ms_per_step_unprofiled": unprofiled_ms,
+          "ms_per_step_profiled_pass": profiled_ms,
           "cpu_baseline": cpu})
 
 

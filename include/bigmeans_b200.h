@@ -118,6 +118,12 @@ uint64_t bm_rng_next(bm_rng* rng);
  * ascending.  Draws from rng on the host; resolution and sort on the device. */
 bm_status bm_sample_chunk(const bm_dataset* data, uint64_t s, bm_rng* rng, uint64_t* out);
 
+/* sample_chunk with caller-side draws: draws[i] = uniform_int(i, m-1) taken
+ * from the caller's own Rng (big_means.cpp:49-51); the Fisher-Yates
+ * resolution and the ascending sort run on `device`.  s < m required. */
+bm_status bm_sample_chunk_draws(uint64_t m, uint64_t s, const uint32_t* draws, int device,
+                                uint64_t* out);
+
 /* assign_nearest core.hpp:112-114 / core.cpp:106-161.  centroids k*n f64,
  * mask k (1 = degenerate).  labels (m) and dists (m, may be NULL) out;
  * *evals += m * active when evals != NULL.  All-degenerate -> BM_STATE_ERROR. */

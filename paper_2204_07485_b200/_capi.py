@@ -64,6 +64,7 @@ PROTOS = {
     "bm_rng_destroy": (C.c_int, [vp]),
     "bm_rng_next": (u64, [vp]),
     "bm_sample_chunk": (C.c_int, [vp, u64, vp, P_u64]),
+    "bm_sample_chunk_draws": (C.c_int, [u64, u64, C.POINTER(C.c_uint32), C.c_int, P_u64]),
     "bm_assign_nearest": (C.c_int, [vp, P_dbl, P_u8, u64, P_i32, P_dbl, P_u64]),
     "bm_objective": (C.c_int, [vp, P_dbl, P_u8, u64, P_dbl, P_u64]),
     "bm_block_sum": (C.c_int, [P_dbl, u64, C.c_int, P_dbl]),

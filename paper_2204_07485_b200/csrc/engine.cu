@@ -709,6 +709,18 @@ void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::v
 // ---------------------------------------------------------------------------
 // Sampling (sample_chunk big_means.cpp:39-56): host draws, device resolution.
 // ---------------------------------------------------------------------------
+SamplerWs& get_sws_dev(int device, uint64_t m, uint64_t s) {
+    DeviceCache& c = cache_of(device);
+    auto key = std::make_pair(m, s);
+    auto it = c.sws.find(key);
+    if (it != c.sws.end()) return *it->second;
+    auto w = std::make_unique<SamplerWs>();
+    w->init(m, s);
+    auto& ref = *w;
+    c.sws.emplace(key, std::move(w));
+    return ref;
+}
+
 SamplerWs& get_sws(const bm_dataset* d, uint64_t s) {
     DeviceCache& c = cache_of(d->device);
     auto key = std::make_pair(d->m, s);
@@ -1119,6 +1131,25 @@ bm_status bm_sample_chunk(const bm_dataset* dc, uint64_t s, bm_rng* rng, uint64_
         std::vector<uint32_t> tmp(s);
         BM_CUDA(cudaMemcpyAsync(tmp.data(), sw.idx.p, s * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream_of(d)));
         BM_CUDA(cudaStreamSynchronize(stream_of(d)));
+        for (uint64_t i = 0; i < s; ++i) out[i] = tmp[i];
+    });
+}
+
+bm_status bm_sample_chunk_draws(uint64_t m, uint64_t s, const uint32_t* draws, int device, uint64_t* out) {
+    return guarded([&] {
+        if (s < 1 || s >= m) throw ConfigError("sample_chunk_draws: need 1 <= s < m");
+        if (m >= 0xFFFFFFFFull) throw ConfigError("dataset too large for 32-bit row indices");
+        for (uint64_t i = 0; i < s; ++i)
+            if (draws[i] < i || draws[i] >= m) throw ConfigError("sample_chunk_draws: draw out of range");
+        DeviceGuard g(device);
+        SamplerWs& sw = get_sws_dev(device, m, s);
+        cudaStream_t st = cache_of(device).stream;
+        BM_CUDA(cudaEventSynchronize(sw.js_done[sw.cur]));
+        std::memcpy(sw.h_js[sw.cur].p, draws, s * sizeof(uint32_t));
+        enqueue_resolve(st, sw);
+        std::vector<uint32_t> tmp(s);
+        BM_CUDA(cudaMemcpyAsync(tmp.data(), sw.idx.p, s * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
         for (uint64_t i = 0; i < s; ++i) out[i] = tmp[i];
     });
 }
