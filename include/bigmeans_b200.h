@@ -113,10 +113,20 @@ bm_status bm_dataset_download(const bm_dataset* data, double* out);
 bm_status bm_rng_create(uint64_t seed, bm_rng** out);
 bm_status bm_rng_destroy(bm_rng* rng);
 uint64_t bm_rng_next(bm_rng* rng);
+/* uniform_int_distribution<size_t>(a,b)(rng) / uniform_real_distribution<double>(a,b)(rng)
+ * with libstdc++ 13 semantics (host only). */
+uint64_t bm_rng_uniform_int(bm_rng* rng, uint64_t a, uint64_t b);
+double bm_rng_uniform_real(bm_rng* rng, double a, double b);
 
 /* sample_chunk big_means.hpp:46 / big_means.cpp:39-56.  out: s indices,
  * ascending.  Draws from rng on the host; resolution and sort on the device. */
 bm_status bm_sample_chunk(const bm_dataset* data, uint64_t s, bm_rng* rng, uint64_t* out);
+
+/* sample_chunk with the draws made ON THE DEVICE from rng's state (the path
+ * big_means uses); rng advances exactly as the host draws would advance it.
+ * force_sequential=1 exercises the exact sequential Lemire-rejection path. */
+bm_status bm_sample_chunk_device(const bm_dataset* data, uint64_t s, bm_rng* rng, int force_sequential,
+                                 uint64_t* out);
 
 /* sample_chunk with caller-side draws: draws[i] = uniform_int(i, m-1) taken
  * from the caller's own Rng (big_means.cpp:49-51); the Fisher-Yates

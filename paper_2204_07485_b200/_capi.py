@@ -63,6 +63,9 @@ PROTOS = {
     "bm_rng_create": (C.c_int, [u64, C.POINTER(vp)]),
     "bm_rng_destroy": (C.c_int, [vp]),
     "bm_rng_next": (u64, [vp]),
+    "bm_rng_uniform_int": (u64, [vp, u64, u64]),
+    "bm_rng_uniform_real": (dbl, [vp, dbl, dbl]),
+    "bm_sample_chunk_device": (C.c_int, [vp, u64, vp, C.c_int, P_u64]),
     "bm_sample_chunk": (C.c_int, [vp, u64, vp, P_u64]),
     "bm_sample_chunk_draws": (C.c_int, [u64, u64, C.POINTER(C.c_uint32), C.c_int, P_u64]),
     "bm_assign_nearest": (C.c_int, [vp, P_dbl, P_u8, u64, P_i32, P_dbl, P_u64]),

@@ -166,6 +166,14 @@ class Rng:
     def __call__(self) -> int:
         return int(self._lib.bm_rng_next(self._h))
 
+    def uniform_int(self, a: int, b: int) -> int:
+        """std::uniform_int_distribution<size_t>(a, b)(rng)."""
+        return int(self._lib.bm_rng_uniform_int(self._h, a, b))
+
+    def uniform_real(self, a: float, b: float) -> float:
+        """std::uniform_real_distribution<double>(a, b)(rng)."""
+        return float(self._lib.bm_rng_uniform_real(self._h, a, b))
+
     def __del__(self):
         try:
             self._lib.bm_rng_destroy(self._h)
@@ -366,6 +374,15 @@ def sample_chunk(data: Dataset, s: int, rng: Rng) -> np.ndarray:
         raise ConfigError("sample_chunk: chunk size must be in [1, m]")
     out = np.empty(s, np.uint64)
     _check(_capi.load().bm_sample_chunk(data.handle, s, rng._h, _ptr(out, _capi.P_u64)))
+    return out
+
+
+def sample_chunk_device(data: Dataset, s: int, rng: Rng, force_sequential: bool = False) -> np.ndarray:
+    """sample_chunk with the draws made on the device from rng's stream (the
+    path big_means takes); rng advances exactly like the host draws."""
+    out = np.empty(s, np.uint64)
+    _check(_capi.load().bm_sample_chunk_device(data.handle, s, rng._h, int(force_sequential),
+                                               _ptr(out, _capi.P_u64)))
     return out
 
 

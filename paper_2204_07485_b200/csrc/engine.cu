@@ -26,9 +26,10 @@
 #include "bigmeans_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "mt64.cuh"
 
 struct bm_rng {
-    std::mt19937_64 eng;  // Rng (common.hpp:13)
+    bm::Mt64 eng;  // Rng (common.hpp:13): std::mt19937_64 stream, libstdc++ distributions
 };
 
 namespace bm {
@@ -191,6 +192,8 @@ struct SamplerWs {
     DevBuf<uint32_t> js, hkeys, bitmap, blockcnt, idx;
     DevBuf<int> LT, hvals;
     DevBuf<uint8_t> kept;
+    DevBuf<Mt64State> mt;           // device-resident RNG stream (big_means chains)
+    HostBuf<Mt64State> h_mt;
     HostBuf<uint32_t> h_js[2];
     cudaEvent_t js_done[2] = {nullptr, nullptr};
     int cur = 0;
@@ -211,6 +214,8 @@ struct SamplerWs {
         idx.alloc(s);
         LT.alloc(s);
         kept.alloc(s);
+        mt.alloc(1);
+        h_mt.alloc(1);
         for (int b = 0; b < 2; ++b) {
             h_js[b].alloc(s);
             if (!js_done[b]) BM_CUDA(cudaEventCreateWithFlags(&js_done[b], cudaEventDisableTiming));
@@ -622,7 +627,7 @@ uint64_t pick_by_mass(const std::vector<double>& cum, double u) {
 }
 
 void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::vector<uint8_t>& mask,
-                          int candidates, std::mt19937_64& rng, uint64_t& evals) {
+                          int candidates, Mt64& rng, uint64_t& evals) {
     if (candidates < 1) throw ConfigError("kmeanspp_fill: candidates_per_step must be at least 1");
     const uint64_t m = P.rows;
     std::vector<int> degenerate;
@@ -638,8 +643,7 @@ void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::v
     const int d2i = candidates;
     size_t first_slot = 0;
     if (active == 0) {  // :144-150
-        std::uniform_int_distribution<std::size_t> pick(0, m - 1);
-        const uint64_t first = pick(rng);
+        const uint64_t first = rng.uniform_int(0, m - 1);
         const int slot = degenerate.front();
         set_row_any(st, P, w, first, slot);
         mask[slot] = 0;
@@ -668,14 +672,12 @@ void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::v
         }
         const double total = cum.back();
         if (total <= 0.0) {  // :174-180
-            std::uniform_int_distribution<std::size_t> pick(0, m - 1);
-            set_row_any(st, P, w, pick(rng), slot);
+            set_row_any(st, P, w, rng.uniform_int(0, m - 1), slot);
             mask[slot] = 0;
             continue;
         }
         for (int c = 0; c < candidates; ++c) {  // :183-185
-            std::uniform_real_distribution<double> draw(0.0, total);
-            picks[c] = pick_by_mass(cum, draw(rng));
+            picks[c] = pick_by_mass(cum, rng.uniform_real(0.0, total));
             w.h_cand.p[c] = (uint32_t)picks[c];
         }
         BM_CUDA(cudaMemcpyAsync(w.cand.p, w.h_cand.p, candidates * sizeof(uint32_t),
@@ -735,26 +737,39 @@ SamplerWs& get_sws(const bm_dataset* d, uint64_t s) {
 
 // Draw the s raw Fisher-Yates targets j_i = uniform_int(i, m-1) into the
 // next pinned buffer (waits until the buffer's previous upload finished).
-uint32_t* draw_targets(SamplerWs& sw, std::mt19937_64& rng) {
+uint32_t* draw_targets(SamplerWs& sw, Mt64& rng) {
     const int b = sw.cur;
     BM_CUDA(cudaEventSynchronize(sw.js_done[b]));
     uint32_t* out = sw.h_js[b].p;
     const uint64_t m = sw.m;
-    for (uint64_t i = 0; i < sw.s; ++i) {
-        std::uniform_int_distribution<std::size_t> pick(i, m - 1);  // :50
-        out[i] = (uint32_t)pick(rng);
-    }
+    for (uint64_t i = 0; i < sw.s; ++i) out[i] = (uint32_t)rng.uniform_int(i, m - 1);  // :50
     return out;
 }
 
-// Enqueue resolution of the drawn targets in buffer sw.cur; result in sw.idx.
-void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
+// Device-side draws (k_mt_draw) from the device-resident stream in sw.mt.
+void enqueue_device_draw(cudaStream_t st, SamplerWs& sw, int force_seq = 0) {
     PhaseScope ps(PH_SAMPLE, sw.s);
-    const int b = sw.cur;
+    dev::k_mt_draw<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.m, (uint32_t)sw.s, sw.js.p, nullptr, force_seq);
+    BM_LAUNCH();
+    count_launch();
+}
+
+void put_stream(cudaStream_t st, SamplerWs& sw, const Mt64& rng) {
+    *sw.h_mt.p = rng.s;
+    BM_CUDA(cudaMemcpyAsync(sw.mt.p, sw.h_mt.p, sizeof(Mt64State), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+}
+
+void get_stream(cudaStream_t st, SamplerWs& sw, Mt64& rng) {
+    BM_CUDA(cudaMemcpyAsync(sw.h_mt.p, sw.mt.p, sizeof(Mt64State), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    rng.s = *sw.h_mt.p;
+}
+
+// Fisher-Yates resolution of the targets already in sw.js; result in sw.idx.
+void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw) {
+    PhaseScope ps(PH_SAMPLE, sw.s);
     const uint32_t s = (uint32_t)sw.s;
-    BM_CUDA(cudaMemcpyAsync(sw.js.p, sw.h_js[b].p, s * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    BM_CUDA(cudaEventRecord(sw.js_done[b], st));
-    sw.cur ^= 1;
     BM_CUDA(cudaMemsetAsync(sw.LT.p, 0xFF, s * sizeof(int), st));
     BM_CUDA(cudaMemsetAsync(sw.hkeys.p, 0xFF, (sw.hmask + 1) * sizeof(uint32_t), st));
     BM_CUDA(cudaMemsetAsync(sw.hvals.p, 0xFF, (sw.hmask + 1) * sizeof(int), st));
@@ -772,6 +787,15 @@ void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
                                                                  sw.idx.p);
     BM_LAUNCH();
     count_launch(6);
+}
+
+// Upload the host-drawn targets of buffer sw.cur, then resolve.
+void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
+    const int b = sw.cur;
+    BM_CUDA(cudaMemcpyAsync(sw.js.p, sw.h_js[b].p, sw.s * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    BM_CUDA(cudaEventRecord(sw.js_done[b], st));
+    sw.cur ^= 1;
+    enqueue_resolve_device(st, sw);
 }
 
 void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
@@ -837,7 +861,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     g_profile = bm_profile{};  // launch counts always; event timing only when profiling
     if (g_profiling) g_prof.begin(st);
     g_prof.stream = st;
-    std::mt19937_64 rng(cfg.seed);  // :62
+    Mt64 rng(cfg.seed);  // :62 — moves to the device for the chunk draws
     Workspace& w = get_ws(d, s, k, cfg.candidates_per_step, 0);
     const bool identity = s == m;  // sample_chunk(s == m): whole range, no draws (:46-48)
     SamplerWs* sw = identity ? nullptr : &get_sws(d, s);
@@ -854,6 +878,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     BM_CUDA(cudaMemsetAsync(w.maskinc.p, 1, k, st));
     const double inf = std::numeric_limits<double>::infinity();
     BM_CUDA(cudaMemcpyAsync(w.fopt.p, &inf, sizeof(double), cudaMemcpyHostToDevice, st));
+    if (!identity) put_stream(st, *sw, rng);
     const uint64_t cap_chunks = cfg.has_max_chunks ? cfg.max_chunks : 0;
     DevBuf<dev::Record> drec(std::max<uint64_t>(cap_chunks ? cap_chunks : 1024, 1));
     std::vector<dev::Record> records;
@@ -862,16 +887,14 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     std::vector<uint8_t> hmask(k);
 
     const auto t_loop = std::chrono::steady_clock::now();
-    bool have_next = false;  // targets for the next chunk already drawn
     for (uint64_t chunk = 0;; ++chunk) {
         if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
         if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
             break;  // :74-77
-        if (!identity) {
-            if (!have_next) draw_targets(*sw, rng);
-            have_next = false;
-            enqueue_resolve(st, *sw);
-            enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);  // :80
+        if (!identity) {  // sample_chunk (:79) on the device stream, gather (:80)
+            enqueue_device_draw(st, *sw);
+            enqueue_resolve_device(st, *sw);
+            enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);
         }
         // start = incumbent (:82), repaired = degenerate_count (:83)
         BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -881,17 +904,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaMemcpyAsync(w.h_mask.p, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
             BM_CUDA(cudaStreamSynchronize(st));
             std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
+            // the repair draws follow this chunk's sample draws in the stream
+            if (!identity) get_stream(st, *sw, rng);
             kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
+            if (!identity) put_stream(st, *sw, rng);
         }
-        // Next chunk's draws come after this chunk's repair draws in the
-        // stream (big_means.hpp:21-23), so they can be drawn while Lloyd runs.
-        const bool next_exists = !identity && (!cfg.has_max_chunks || chunk + 1 < cfg.max_chunks);
-        LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance, [&] {
-            if (next_exists) {
-                draw_targets(*sw, rng);
-                have_next = true;
-            }
-        });
+        LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance);
         evals += lr.evals;  // lloyd accumulate (local_search.cpp:55-58)
         iterations += lr.iterations;
         if (chunk >= drec.n) {  // time-budget runs: grow the record buffer
@@ -1108,12 +1126,32 @@ bm_status bm_dataset_download(const bm_dataset* d, double* out) {
 }
 
 bm_status bm_rng_create(uint64_t seed, bm_rng** out) {
-    return guarded([&] { *out = new bm_rng{std::mt19937_64(seed)}; });
+    return guarded([&] { *out = new bm_rng{Mt64(seed)}; });
 }
 bm_status bm_rng_destroy(bm_rng* r) {
     return guarded([&] { delete r; });
 }
 uint64_t bm_rng_next(bm_rng* r) { return r->eng(); }
+uint64_t bm_rng_uniform_int(bm_rng* r, uint64_t a, uint64_t b) { return r->eng.uniform_int(a, b); }
+double bm_rng_uniform_real(bm_rng* r, double a, double b) { return r->eng.uniform_real(a, b); }
+
+bm_status bm_sample_chunk_device(const bm_dataset* d, uint64_t s, bm_rng* rng, int force_sequential,
+                                 uint64_t* out) {
+    return guarded([&] {
+        const uint64_t m = d->m;
+        if (s < 1 || s >= m) throw ConfigError("sample_chunk_device: need 1 <= s < m");
+        DeviceGuard g(d->device);
+        SamplerWs& sw = get_sws(d, s);
+        cudaStream_t st = stream_of(d);
+        put_stream(st, sw, rng->eng);
+        enqueue_device_draw(st, sw, force_sequential);
+        enqueue_resolve_device(st, sw);
+        std::vector<uint32_t> tmp(s);
+        BM_CUDA(cudaMemcpyAsync(tmp.data(), sw.idx.p, s * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        get_stream(st, sw, rng->eng);
+        for (uint64_t i = 0; i < s; ++i) out[i] = tmp[i];
+    });
+}
 
 bm_status bm_sample_chunk(const bm_dataset* dc, uint64_t s, bm_rng* rng, uint64_t* out) {
     return guarded([&] {
@@ -1301,7 +1339,7 @@ bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uin
         DeviceGuard g(d->device);
         cudaStream_t st = stream_of(d);
         Workspace& w = get_ws(d, d->m, (int)k, candidates, 0);
-        std::mt19937_64 rng(seed);  // local_search.cpp:69
+        Mt64 rng(seed);  // local_search.cpp:69
         const auto t_init = std::chrono::steady_clock::now();
         BM_CUDA(cudaMemsetAsync(w.C.p, 0, k * d->n * sizeof(double), st));
         BM_CUDA(cudaMemsetAsync(w.mask.p, 1, k, st));

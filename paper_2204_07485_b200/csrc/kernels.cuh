@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "mt64.cuh"
 
 namespace bm {
 namespace dev {
@@ -114,6 +115,89 @@ __global__ void k_fy_pass3(const uint8_t* __restrict__ kept, uint32_t s, uint32_
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= s) return;
     if (kept[v]) atomicOr(&bitmap[v >> 5], 1u << (v & 31));
+}
+
+// The s raw targets j_i = uniform_int(i, m-1) (big_means.cpp:49-51) drawn on
+// the device from the device-resident std::mt19937_64 state: one CTA, the
+// twist in two data-parallel halves, the tempering and Lemire's
+// multiply-shift per output in parallel.  A Lemire rejection (probability
+// < 2^-32 per draw for m < 2^32) shifts every later draw; it is detected and
+// the whole draw is redone sequentially from the saved state by thread 0 with
+// the exact rejection loop (also forced by `force_seq` in tests).
+constexpr int kMtThreads = 320;
+
+__device__ uint64_t mt_next_seq(uint64_t* x, int& pos) {
+    if (pos >= kMtN) {
+        for (int i = 0; i < kMtN; ++i) x[i] = mt_mix(x[i], x[(i + 1) % kMtN], x[(i + kMtM) % kMtN]);
+        pos = 0;
+    }
+    return mt_temper(x[pos++]);
+}
+
+__global__ void __launch_bounds__(kMtThreads)
+k_mt_draw(Mt64State* __restrict__ st, uint64_t m, uint32_t s, uint32_t* __restrict__ js,
+          const int* __restrict__ skip, int force_seq) {
+    __shared__ uint64_t x[kMtN];
+    __shared__ uint64_t x0[kMtN];  // state before the draw (sequential fallback)
+    __shared__ int reject;
+    if (skip && *skip) return;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kMtN; i += blockDim.x) x[i] = x0[i] = st->x[i];
+    int pos = static_cast<int>(st->pos);
+    const int pos0 = pos;
+    if (tid == 0) reject = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < s;) {
+        if (pos >= kMtN) {
+            uint64_t v = 0;
+            if (tid < kMtM) v = mt_mix(x[tid], x[tid + 1], x[tid + kMtM]);
+            __syncthreads();
+            if (tid < kMtM) x[tid] = v;
+            __syncthreads();
+            if (tid >= kMtM && tid < kMtN) v = mt_mix(x[tid], x[(tid + 1) % kMtN], x[tid - kMtM]);
+            __syncthreads();
+            if (tid >= kMtM && tid < kMtN) x[tid] = v;
+            __syncthreads();
+            pos = 0;
+        }
+        const uint32_t take = min(static_cast<uint32_t>(kMtN - pos), s - base);
+        if (tid < static_cast<int>(take)) {
+            const uint64_t y = mt_temper(x[pos + tid]);
+            const uint64_t i = base + tid;
+            const uint64_t r = m - i;
+            const uint64_t low = y * r;
+            if (low < r && low < (0 - r) % r) reject = 1;
+            js[i] = static_cast<uint32_t>(i + mul_hi64(y, r));
+        }
+        pos += take;
+        base += take;
+        __syncthreads();
+    }
+    if (reject || force_seq) {  // exact sequential redo from the saved state
+        if (tid == 0) {
+            int p = pos0;
+            for (int i = 0; i < kMtN; ++i) x[i] = x0[i];
+            for (uint32_t i = 0; i < s; ++i) {
+                const uint64_t r = m - i;
+                uint64_t y = mt_next_seq(x, p);
+                uint64_t low = y * r;
+                if (low < r) {
+                    const uint64_t thr = (0 - r) % r;
+                    while (low < thr) {
+                        y = mt_next_seq(x, p);
+                        low = y * r;
+                    }
+                }
+                js[i] = static_cast<uint32_t>(i + mul_hi64(y, r));
+            }
+            pos = p;
+            reject = p;  // broadcast the final position
+        }
+        __syncthreads();
+        pos = reject;
+    }
+    for (int i = tid; i < kMtN; i += blockDim.x) st->x[i] = x[i];
+    if (tid == 0) st->pos = static_cast<uint64_t>(pos);
 }
 
 // Bitmap -> ascending index list (the std::sort of big_means.cpp:54).

@@ -38,6 +38,23 @@ def test_sample_chunk_vs_oracle(port, m, s):
         assert r() == port.rng_next(pr)
 
 
+@pytest.mark.parametrize("m,s", [(2, 1), (33, 32), (1000, 500), (4096, 4095), (13_500, 4_000),
+                                 (100_000, 10_000), (2_500_000, 50_000), (10_500_000, 100_000)])
+@pytest.mark.parametrize("force_seq", [False, True])
+def test_device_stream_sample_chunk_vs_oracle(port, m, s, force_seq):
+    """Draws made on the device (k_mt_draw) from the device-resident stream:
+    same indices and same stream position as the reference's host draws."""
+    if force_seq and s > 20_000:
+        pytest.skip("sequential path is a single-thread fallback; small cases suffice")
+    d = bm.Dataset(np.zeros((m, 1), np.float32))
+    for seed in (0, 7, 123456789):
+        r, pr = bm.Rng(seed), port.rng(seed)
+        for _ in range(3):
+            got = bm.sample_chunk_device(d, s, r, force_sequential=force_seq)
+            assert (got == port.sample_chunk(m, s, pr)).all()
+        assert r() == port.rng_next(pr)
+
+
 def test_sample_chunk_properties():  # test_big_means.cpp:27-54
     d = bm.Dataset(np.random.default_rng(1).uniform(0, 50, (100, 2)))
     idx = bm.sample_chunk(d, 30, bm.Rng(7))

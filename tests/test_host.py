@@ -109,3 +109,27 @@ def test_no_oracle_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in text.replace("CPU oracle", ""), f
+
+
+def test_product_rng_matches_oracle_stream(port):
+    """The product's host engine (bm_rng: MT19937-64 + libstdc++ Lemire /
+    generate_canonical) is bit-identical to the restated std:: stream."""
+    from paper_2204_07485_b200 import Rng
+    rng = np.random.default_rng(0)
+    for seed in (0, 1, 123456789, 2**64 - 1):
+        a, b = Rng(seed), port.rng(seed)
+        for _ in range(200):
+            assert a() == port.rng_next(b)
+        for _ in range(2000):
+            kind = rng.integers(0, 4)
+            if kind == 0:
+                lo = int(rng.integers(0, 1 << 40)); hi = lo + int(rng.integers(0, 1 << 32))
+            elif kind == 1:  # ranges near 2^63..2^64: frequent Lemire rejections
+                lo = 0; hi = (1 << 63) + int(rng.integers(0, 1 << 62))
+            elif kind == 2:
+                lo = hi = int(rng.integers(0, 1 << 20))
+            else:
+                lo, hi = 0, (1 << 64) - 1
+            assert a.uniform_int(lo, hi) == port.uniform_int(b, lo, hi)
+            t = float(rng.uniform(0, 1e6))
+            assert a.uniform_real(0.0, t) == port.uniform_real(b, 0.0, t)
