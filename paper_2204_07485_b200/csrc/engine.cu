@@ -189,7 +189,9 @@ struct SamplerWs {
     uint64_t m = 0, s = 0;
     uint32_t hmask = 0;
     uint32_t nwords = 0, nblocks = 0;
-    DevBuf<uint32_t> js, hkeys, bitmap, blockcnt, idx;
+    DevBuf<uint32_t> js, js2, hkeys, bitmap, blockcnt, idx;  // js2: second target buffer (pipelined draws)
+    cudaStream_t rng_stream = nullptr;                      // device draws of the next chunk
+    cudaEvent_t drawn[2] = {nullptr, nullptr}, resolved[2] = {nullptr, nullptr};
     DevBuf<int> LT, hvals;
     DevBuf<uint8_t> kept;
     DevBuf<Mt64State> mt;           // device-resident RNG stream (big_means chains)
@@ -207,6 +209,7 @@ struct SamplerWs {
         nwords = (uint32_t)ceil_div(m, 32);
         nblocks = (uint32_t)ceil_div(nwords, dev::kWordsPerBlock);
         js.alloc(s);
+        js2.alloc(s);
         hkeys.alloc(h);
         hvals.alloc(h);
         bitmap.alloc(nwords);
@@ -219,11 +222,17 @@ struct SamplerWs {
         for (int b = 0; b < 2; ++b) {
             h_js[b].alloc(s);
             if (!js_done[b]) BM_CUDA(cudaEventCreateWithFlags(&js_done[b], cudaEventDisableTiming));
+            if (!drawn[b]) BM_CUDA(cudaEventCreateWithFlags(&drawn[b], cudaEventDisableTiming));
+            if (!resolved[b]) BM_CUDA(cudaEventCreateWithFlags(&resolved[b], cudaEventDisableTiming));
         }
+        if (!rng_stream) BM_CUDA(cudaStreamCreateWithFlags(&rng_stream, cudaStreamNonBlocking));
     }
+    uint32_t* jsbuf(int b) { return b ? js2.p : js.p; }
     ~SamplerWs() {
-        for (auto& e : js_done)
-            if (e) cudaEventDestroy(e);
+        for (auto* arr : {js_done, drawn, resolved})
+            for (int b = 0; b < 2; ++b)
+                if (arr[b]) cudaEventDestroy(arr[b]);
+        if (rng_stream) cudaStreamDestroy(rng_stream);
     }
 };
 
@@ -747,9 +756,9 @@ uint32_t* draw_targets(SamplerWs& sw, Mt64& rng) {
 }
 
 // Device-side draws (k_mt_draw) from the device-resident stream in sw.mt.
-void enqueue_device_draw(cudaStream_t st, SamplerWs& sw, int force_seq = 0) {
-    PhaseScope ps(PH_SAMPLE, sw.s);
-    dev::k_mt_draw<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.m, (uint32_t)sw.s, sw.js.p, nullptr, force_seq);
+void enqueue_device_draw(cudaStream_t st, SamplerWs& sw, int force_seq = 0, uint32_t* out = nullptr) {
+    dev::k_mt_draw<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.m, (uint32_t)sw.s, out ? out : sw.js.p, nullptr,
+                                                  force_seq);
     BM_LAUNCH();
     count_launch();
 }
@@ -767,17 +776,18 @@ void get_stream(cudaStream_t st, SamplerWs& sw, Mt64& rng) {
 }
 
 // Fisher-Yates resolution of the targets already in sw.js; result in sw.idx.
-void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw) {
+void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw, const uint32_t* js = nullptr) {
     PhaseScope ps(PH_SAMPLE, sw.s);
     const uint32_t s = (uint32_t)sw.s;
+    if (!js) js = sw.js.p;
     BM_CUDA(cudaMemsetAsync(sw.LT.p, 0xFF, s * sizeof(int), st));
     BM_CUDA(cudaMemsetAsync(sw.hkeys.p, 0xFF, (sw.hmask + 1) * sizeof(uint32_t), st));
     BM_CUDA(cudaMemsetAsync(sw.hvals.p, 0xFF, (sw.hmask + 1) * sizeof(int), st));
     BM_CUDA(cudaMemsetAsync(sw.kept.p, 1, s, st));
     BM_CUDA(cudaMemsetAsync(sw.bitmap.p, 0, sw.nwords * sizeof(uint32_t), st));
     const unsigned g = (unsigned)ceil_div(s, 256);
-    dev::k_fy_pass1<<<g, 256, 0, st>>>(sw.js.p, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
-    dev::k_fy_pass2<<<g, 256, 0, st>>>(sw.js.p, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.kept.p,
+    dev::k_fy_pass1<<<g, 256, 0, st>>>(js, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
+    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.kept.p,
                                        sw.bitmap.p);
     dev::k_fy_pass3<<<g, 256, 0, st>>>(sw.kept.p, s, sw.bitmap.p);
     dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.nwords,
@@ -887,15 +897,23 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     std::vector<uint8_t> hmask(k);
 
     const auto t_loop = std::chrono::steady_clock::now();
+    bool drawn_ahead = false;  // next chunk's targets already being drawn on rng_stream
     for (uint64_t chunk = 0;; ++chunk) {
         if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
         if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
             break;  // :74-77
-        if (!identity) {  // sample_chunk (:79) on the device stream, gather (:80)
-            enqueue_device_draw(st, *sw);
-            enqueue_resolve_device(st, *sw);
+        const int jb = (int)(chunk & 1);
+        if (!identity) {  // sample_chunk (:79): draws made on rng_stream, resolution + gather (:80) here
+            if (!drawn_ahead) {
+                enqueue_device_draw(sw->rng_stream, *sw, 0, sw->jsbuf(jb));
+                BM_CUDA(cudaEventRecord(sw->drawn[jb], sw->rng_stream));
+            }
+            BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[jb], 0));
+            enqueue_resolve_device(st, *sw, sw->jsbuf(jb));
+            BM_CUDA(cudaEventRecord(sw->resolved[jb], st));
             enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);
         }
+        drawn_ahead = false;
         // start = incumbent (:82), repaired = degenerate_count (:83)
         BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
         BM_CUDA(cudaMemcpyAsync(w.mask.p, w.maskinc.p, k, cudaMemcpyDeviceToDevice, st));
@@ -905,9 +923,22 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaStreamSynchronize(st));
             std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
             // the repair draws follow this chunk's sample draws in the stream
-            if (!identity) get_stream(st, *sw, rng);
+            if (!identity) {
+                BM_CUDA(cudaStreamSynchronize(sw->rng_stream));
+                get_stream(st, *sw, rng);
+            }
             kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
             if (!identity) put_stream(st, *sw, rng);
+        }
+        // The next chunk's sample draws follow this chunk's (repair) draws:
+        // start them now on rng_stream, overlapping this chunk's Lloyd.  Its
+        // target buffer was last read by the previous chunk's resolution.
+        const bool next_exists = !identity && (!cfg.has_max_chunks || chunk + 1 < cfg.max_chunks);
+        if (next_exists) {
+            if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[jb ^ 1], 0));
+            enqueue_device_draw(sw->rng_stream, *sw, 0, sw->jsbuf(jb ^ 1));
+            BM_CUDA(cudaEventRecord(sw->drawn[jb ^ 1], sw->rng_stream));
+            drawn_ahead = true;
         }
         LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance);
         evals += lr.evals;  // lloyd accumulate (local_search.cpp:55-58)
@@ -933,6 +964,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         inc_degenerate = w.h_status.p->inc_degenerate;
         out->chunks = chunk + 1;
     }
+    if (sw) BM_CUDA(cudaStreamSynchronize(sw->rng_stream));  // a speculative draw may be in flight
     const double cpu_init = seconds_since(t_loop);  // :96
     records.resize(out->chunks);
     if (out->chunks)
