@@ -11,7 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -142,6 +144,27 @@ struct Workspace {
     // incumbent (big_means.cpp:63-64, 89-93)
     DevBuf<double> Cinc, fopt;
     DevBuf<uint8_t> maskinc;
+    DevBuf<dev::Record> drec;              // per-chunk records (big_means trace)
+    DevBuf<unsigned long long> chunk_ctr;  // device-side chunk index
+    // CUDA graphs of one chunk (sample resolution + gather, and the Lloyd loop)
+    std::string graph_sig;
+    cudaGraphExec_t g_prep[2] = {nullptr, nullptr};
+    cudaGraphExec_t g_lloyd = nullptr;
+    cudaStream_t cap2 = nullptr;  // capture stream of the WHILE body
+    void drop_graphs() {
+        for (auto& e : g_prep)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+        if (g_lloyd) cudaGraphExecDestroy(g_lloyd);
+        g_lloyd = nullptr;
+        graph_sig.clear();
+    }
+    ~Workspace() {
+        drop_graphs();
+        if (cap2) cudaStreamDestroy(cap2);
+    }
     // pinned host mirrors
     HostBuf<dev::LloydStatus> h_status;
     HostBuf<double> h_tiles;
@@ -176,6 +199,7 @@ struct Workspace {
         Cinc.alloc((uint64_t)k * n);
         fopt.alloc(1);
         maskinc.alloc(k);
+        chunk_ctr.alloc(1);
         h_status.alloc(1);
         h_tiles.alloc(tiles * ncand);
         h_d2.alloc(R);
@@ -242,6 +266,7 @@ struct SamplerWs {
 // shareable: all per-run state lives in the calling thread's DeviceCache.
 struct bm_dataset {
     int device = 0;
+    uint64_t uid = 0;  // distinguishes handles whose addresses get reused (graph keys)
     uint64_t m = 0, n = 0, ld = 0;
     bm_dtype dtype = BM_F64;
     void* X = nullptr;
@@ -552,7 +577,8 @@ void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w) {
     count_launch();
 }
 
-void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol) {
+void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol,
+                         cudaGraphConditionalHandle cond = 0, int use_cond = 0) {
     const int* parity = &w.status.p->parity;
     const int* stop = &w.status.p->stop;
     launch_update(st, P, w, parity, stop);                                                 // :33
@@ -560,7 +586,7 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
                   w.tile_buf.p, w.tile_ctr.p);  // :34-35
     PhaseScope ps(PH_CONTROL, 0);
     dev::k_lloyd_step<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows, max_it,
-                                        tol, w.hist_cap ? w.history.p : nullptr);
+                                        tol, w.hist_cap ? w.history.p : nullptr, cond, use_cond);
     BM_LAUNCH();
     count_launch();
 }
@@ -860,6 +886,92 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
 // ---------------------------------------------------------------------------
 // big_means (big_means.cpp:58-112)
 // ---------------------------------------------------------------------------
+// ---- CUDA graphs of one steady-state chunk --------------------------------
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_GRAPHS");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+void enqueue_accept(cudaStream_t st, Workspace& w) {
+    PhaseScope ps(PH_CONTROL, 0);
+    dev::k_accept<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p, w.maskinc.p, w.k, w.n,
+                                     w.drec.p, w.chunk_ctr.p);
+    BM_LAUNCH();
+    count_launch();
+}
+
+// prep[b]: Fisher-Yates resolution of target buffer b, gather (:79-80), start := incumbent (:82)
+cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw,
+                             Workspace& w, int b) {
+    cudaGraph_t g = nullptr;
+    BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    enqueue_resolve_device(st, sw, sw.jsbuf(b));
+    BM_CUDA(cudaEventRecordWithFlags(sw.resolved[b], st, cudaEventRecordExternal));
+    enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, dc.chunk.p);
+    BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)w.k * w.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    BM_CUDA(cudaMemcpyAsync(w.mask.p, w.maskinc.p, w.k, cudaMemcpyDeviceToDevice, st));
+    BM_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t e = nullptr;
+    BM_CUDA(cudaGraphInstantiate(&e, g, 0));
+    cudaGraphDestroy(g);
+    return e;
+}
+
+// lloyd (local_search.cpp:16-60) as compact+assign+begin, a WHILE node whose
+// body is one update/assign/step round (k_lloyd_step sets the condition), then
+// the accept (:89-94) and the status readback.
+cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, uint64_t max_it, double tol) {
+    if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
+    BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    lloyd_enqueue_begin(st, P, w);
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    BM_CUDA(cudaGraphConditionalHandleCreate(&h, cg, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams prm = {};
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    cudaGraphNode_t cn;
+    BM_CUDA(cudaGraphAddNode(&cn, cg, deps, nd, &prm));
+    BM_CUDA(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = prm.conditional.phGraph_out[0];
+    BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    lloyd_enqueue_round(w.cap2, P, w, max_it, tol, h, 1);
+    BM_CUDA(cudaStreamEndCapture(w.cap2, &body));
+    enqueue_accept(st, w);
+    BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
+    cudaGraph_t g = nullptr;
+    BM_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t e = nullptr;
+    BM_CUDA(cudaGraphInstantiate(&e, g, 0));
+    cudaGraphDestroy(g);
+    return e;
+}
+
+void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw, Workspace& w,
+                   const Points& P, uint64_t max_it, double tol) {
+    char sig[512];
+    std::snprintf(sig, sizeof(sig), "%llu/%p/%p/%p/%p/%p/%llu/%a/%llu",
+                  (unsigned long long)d->uid, (const void*)d->X, (void*)dc.chunk.p, (void*)&sw, (void*)w.drec.p,
+                  (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n);
+    if (w.graph_sig == sig && w.g_lloyd) return;
+    w.drop_graphs();
+    const uint64_t saved = g_profile.kernel_launches;
+    w.g_prep[0] = capture_prep(st, d, dc, sw, w, 0);
+    w.g_prep[1] = capture_prep(st, d, dc, sw, w, 1);
+    w.g_lloyd = capture_lloyd(st, w, P, max_it, tol);
+    g_profile.kernel_launches = saved;  // capture is not execution
+    w.graph_sig = sig;
+}
+
 void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_chunk_record* trace,
                uint64_t trace_cap) {
     validate(d, cfg);
@@ -883,15 +995,14 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         if (dc.chunk.n < bytes) dc.chunk.alloc(bytes);
         chunkP.X = dc.chunk.p;
     }
-    // incumbent: all degenerate, f_opt = +inf (:63-64)
-    BM_CUDA(cudaMemsetAsync(w.Cinc.p, 0, (size_t)k * n * sizeof(double), st));
-    BM_CUDA(cudaMemsetAsync(w.maskinc.p, 1, k, st));
-    const double inf = std::numeric_limits<double>::infinity();
-    BM_CUDA(cudaMemcpyAsync(w.fopt.p, &inf, sizeof(double), cudaMemcpyHostToDevice, st));
+    const uint64_t want_rec = cfg.has_max_chunks ? cfg.max_chunks : 1024;
+    if (w.drec.n < want_rec) w.drec.alloc(want_rec);
+    // incumbent all degenerate, f_opt = +inf (:63-64), chunk counter 0
+    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.Cinc.p, w.maskinc.p, k, n, w.chunk_ctr.p);
+    BM_LAUNCH();
     if (!identity) put_stream(st, *sw, rng);
-    const uint64_t cap_chunks = cfg.has_max_chunks ? cfg.max_chunks : 0;
-    DevBuf<dev::Record> drec(std::max<uint64_t>(cap_chunks ? cap_chunks : 1024, 1));
-    std::vector<dev::Record> records;
+    const bool use_graphs = !identity && !g_profiling && graphs_enabled();
+    if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
     uint64_t evals = 0, iterations = 0;
     int inc_degenerate = k;
     std::vector<uint8_t> hmask(k);
@@ -902,23 +1013,38 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
         if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
             break;  // :74-77
+        if (chunk >= w.drec.n) {  // time-budget runs: grow the record buffer (graphs re-captured)
+            DevBuf<dev::Record> bigger(w.drec.n * 2);
+            BM_CUDA(cudaMemcpyAsync(bigger.p, w.drec.p, w.drec.n * sizeof(dev::Record), cudaMemcpyDeviceToDevice, st));
+            BM_CUDA(cudaStreamSynchronize(st));
+            std::swap(w.drec.p, bigger.p);
+            std::swap(w.drec.n, bigger.n);
+            if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
+        }
         const int jb = (int)(chunk & 1);
         if (!identity) {  // sample_chunk (:79): draws made on rng_stream, resolution + gather (:80) here
             if (!drawn_ahead) {
                 enqueue_device_draw(sw->rng_stream, *sw, 0, sw->jsbuf(jb));
                 BM_CUDA(cudaEventRecord(sw->drawn[jb], sw->rng_stream));
             }
+            count_launch();
             BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[jb], 0));
-            enqueue_resolve_device(st, *sw, sw->jsbuf(jb));
-            BM_CUDA(cudaEventRecord(sw->resolved[jb], st));
-            enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);
         }
         drawn_ahead = false;
-        // start = incumbent (:82), repaired = degenerate_count (:83)
-        BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        BM_CUDA(cudaMemcpyAsync(w.mask.p, w.maskinc.p, k, cudaMemcpyDeviceToDevice, st));
-        const uint64_t repaired = (uint64_t)inc_degenerate;
-        if (repaired > 0) {  // kmeanspp_fill (:84) consumes draws before the next sample
+        if (use_graphs) {
+            BM_CUDA(cudaGraphLaunch(w.g_prep[jb], st));
+            count_launch(7);
+        } else {
+            if (!identity) {
+                enqueue_resolve_device(st, *sw, sw->jsbuf(jb));
+                BM_CUDA(cudaEventRecord(sw->resolved[jb], st));
+                enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);
+            }
+            // start = incumbent (:82)
+            BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            BM_CUDA(cudaMemcpyAsync(w.mask.p, w.maskinc.p, k, cudaMemcpyDeviceToDevice, st));
+        }
+        if (inc_degenerate > 0) {  // kmeanspp_fill (:84) consumes draws before the next sample
             BM_CUDA(cudaMemcpyAsync(w.h_mask.p, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
             BM_CUDA(cudaStreamSynchronize(st));
             std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
@@ -940,35 +1066,33 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaEventRecord(sw->drawn[jb ^ 1], sw->rng_stream));
             drawn_ahead = true;
         }
-        LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance);
-        evals += lr.evals;  // lloyd accumulate (local_search.cpp:55-58)
-        iterations += lr.iterations;
-        if (chunk >= drec.n) {  // time-budget runs: grow the record buffer
-            records.resize(drec.n);
-            BM_CUDA(cudaMemcpyAsync(records.data(), drec.p, drec.n * sizeof(dev::Record), cudaMemcpyDeviceToHost, st));
+        if (use_graphs) {
+            BM_CUDA(cudaGraphLaunch(w.g_lloyd, st));
             BM_CUDA(cudaStreamSynchronize(st));
-            DevBuf<dev::Record> bigger(drec.n * 2);
-            BM_CUDA(cudaMemcpyAsync(bigger.p, records.data(), records.size() * sizeof(dev::Record),
-                                    cudaMemcpyHostToDevice, st));
+            const dev::LloydStatus& ls = *w.h_status.p;
+            if (ls.state_error) throw StateError("assign_nearest: every centroid is degenerate");
+            if (ls.bad_label) throw ConfigError("update_centroids: label out of range");
+            evals += ls.evals;  // lloyd accumulate (local_search.cpp:55-58)
+            iterations += ls.iterations;
+            inc_degenerate = ls.inc_degenerate;
+            count_launch(4 + 4 * ls.iterations);
+        } else {
+            LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance);
+            evals += lr.evals;
+            iterations += lr.iterations;
+            enqueue_accept(st, w);
+            BM_CUDA(cudaMemcpyAsync(&w.h_status.p->inc_degenerate, &w.status.p->inc_degenerate, sizeof(int),
+                                    cudaMemcpyDeviceToHost, st));
             BM_CUDA(cudaStreamSynchronize(st));
-            std::swap(drec.p, bigger.p);
-            std::swap(drec.n, bigger.n);
+            inc_degenerate = w.h_status.p->inc_degenerate;
         }
-        dev::k_accept<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p, w.maskinc.p, k, n,
-                                         drec.p + chunk, chunk, repaired, &w.status.p->inc_degenerate);
-        BM_LAUNCH();
-        count_launch();
-        BM_CUDA(cudaMemcpyAsync(&w.h_status.p->inc_degenerate, &w.status.p->inc_degenerate, sizeof(int),
-                                cudaMemcpyDeviceToHost, st));
-        BM_CUDA(cudaStreamSynchronize(st));
-        inc_degenerate = w.h_status.p->inc_degenerate;
         out->chunks = chunk + 1;
     }
     if (sw) BM_CUDA(cudaStreamSynchronize(sw->rng_stream));  // a speculative draw may be in flight
     const double cpu_init = seconds_since(t_loop);  // :96
-    records.resize(out->chunks);
+    std::vector<dev::Record> records(out->chunks);
     if (out->chunks)
-        BM_CUDA(cudaMemcpyAsync(records.data(), drec.p, out->chunks * sizeof(dev::Record), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(records.data(), w.drec.p, out->chunks * sizeof(dev::Record), cudaMemcpyDeviceToHost, st));
     double fopt = 0.0;
     BM_CUDA(cudaMemcpyAsync(&fopt, w.fopt.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaMemcpyAsync(out->centroids, w.Cinc.p, (size_t)k * n * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1070,6 +1194,8 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
         if (m >= 0xFFFFFFFFull) throw ConfigError("dataset too large for 32-bit row indices");
         DeviceGuard g(device);
         auto d = std::make_unique<bm_dataset>();
+        static std::atomic<uint64_t> next_uid{1};
+        d->uid = next_uid++;
         d->device = device;
         d->m = m;
         d->n = n;

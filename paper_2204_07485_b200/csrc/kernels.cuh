@@ -1108,45 +1108,53 @@ __global__ void k_lloyd_begin(LloydStatus* st, const double* tiles, uint64_t nti
 }
 
 __global__ void k_lloyd_step(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
-                             unsigned long long max_iterations, double rel_tolerance, double* history) {
+                             unsigned long long max_iterations, double rel_tolerance, double* history,
+                             cudaGraphConditionalHandle cond, int use_cond) {
     if (threadIdx.x != 0) return;
-    if (st->stop) return;
-    const double f_new = fold_tiles(tiles, ntiles);  // :35
-    st->evals += static_cast<unsigned long long>(rows) * st->n_active;
-    if (st->n_active == 0) st->state_error = 1;
-    st->iterations += 1;            // :36
-    st->objective = f_new;          // history.push_back (:37)
-    if (history) history[st->iterations] = f_new;
-    const bool unchanged = st->changed == 0;  // :39
-    st->changed = 0;
-    st->parity ^= 1;                // :40-41 advance
-    const double f = st->f;
-    bool stop = unchanged;                                                      // :42-44
-    if (!stop && f <= 0.0) stop = true;                                         // :45-47
-    if (!stop && rel_tolerance > 0.0 && __ddiv_rn(__dsub_rn(f, f_new), f) < rel_tolerance)
-        stop = true;                                                            // :48-50
-    if (!stop) st->f = f_new;                                                   // :51
-    if (st->iterations >= max_iterations) stop = true;                          // :32
-    st->stop = stop ? 1 : 0;
+    if (!st->stop) {
+        const double f_new = fold_tiles(tiles, ntiles);  // :35
+        st->evals += static_cast<unsigned long long>(rows) * st->n_active;
+        if (st->n_active == 0) st->state_error = 1;
+        st->iterations += 1;            // :36
+        st->objective = f_new;          // history.push_back (:37)
+        if (history) history[st->iterations] = f_new;
+        const bool unchanged = st->changed == 0;  // :39
+        st->changed = 0;
+        st->parity ^= 1;                // :40-41 advance
+        const double f = st->f;
+        bool stop = unchanged;                                                      // :42-44
+        if (!stop && f <= 0.0) stop = true;                                         // :45-47
+        if (!stop && rel_tolerance > 0.0 && __ddiv_rn(__dsub_rn(f, f_new), f) < rel_tolerance)
+            stop = true;                                                            // :48-50
+        if (!stop) st->f = f_new;                                                   // :51
+        if (st->iterations >= max_iterations) stop = true;                          // :32
+        if (st->state_error || st->bad_label) stop = true;
+        st->stop = stop ? 1 : 0;
+    }
+    if (use_cond) cudaGraphSetConditional(cond, st->stop ? 0u : 1u);  // graph WHILE node
 }
 
 // ===========================================================================
 // 7. Accept (big_means.cpp:89-94) on the device.
 // ===========================================================================
-__global__ void k_accept(const LloydStatus* st, double* f_opt, const double* __restrict__ C,
+// rec_base[*chunk_ctr] receives the record; the chunk counter and the
+// incumbent's degenerate count (the next chunk's `repaired`, :83) live on the
+// device so the chunk can run inside a CUDA graph.
+__global__ void k_accept(LloydStatus* st, double* f_opt, const double* __restrict__ C,
                          const uint8_t* __restrict__ mask, double* __restrict__ Cinc,
-                         uint8_t* __restrict__ maskinc, int k, int n, Record* rec,
-                         unsigned long long chunk, unsigned long long repaired, int* inc_degenerate) {
-    // st is const here; the count is written through inc_degenerate (&st->inc_degenerate).
+                         uint8_t* __restrict__ maskinc, int k, int n, Record* rec_base,
+                         unsigned long long* chunk_ctr) {
     __shared__ int accepted;
     if (threadIdx.x == 0) {
+        const unsigned long long chunk = *chunk_ctr;
+        Record* rec = rec_base + chunk;
         accepted = st->objective < *f_opt;  // strict (:89)
         if (accepted) *f_opt = st->objective;
         rec->chunk_index = chunk;
         rec->candidate_objective = st->objective;
         rec->incumbent_objective = *f_opt;
         rec->accepted = accepted;
-        rec->degenerate_repaired = repaired;
+        rec->degenerate_repaired = static_cast<unsigned long long>(st->inc_degenerate);
     }
     __syncthreads();
     if (accepted) {
@@ -1157,7 +1165,20 @@ __global__ void k_accept(const LloydStatus* st, double* f_opt, const double* __r
     if (threadIdx.x == 0) {
         int dcount = 0;
         for (int j = 0; j < k; ++j) dcount += maskinc[j] ? 1 : 0;
-        *inc_degenerate = dcount;
+        st->inc_degenerate = dcount;
+        *chunk_ctr += 1;
+    }
+}
+
+// Reset of the per-run device state (incumbent all degenerate, f_opt = +inf).
+__global__ void k_run_init(LloydStatus* st, double* f_opt, double* Cinc, uint8_t* maskinc, int k, int n,
+                           unsigned long long* chunk_ctr) {
+    for (int e = threadIdx.x; e < k * n; e += blockDim.x) Cinc[e] = 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) maskinc[j] = 1;
+    if (threadIdx.x == 0) {
+        *f_opt = __longlong_as_double(0x7FF0000000000000LL);
+        st->inc_degenerate = k;
+        *chunk_ctr = 0;
     }
 }
 

@@ -161,8 +161,10 @@ def test_screen_adversarial_bitwise(port, case):
     assert bm.objective(bm.Dataset(X), bm.Centroids(C, mask)) == port.block_sum(d2)
 
 
-def test_exact_mode_matches_screen_mode():
-    """BM_ASSIGN_MODE=exact (unscreened kernel) gives the same bits in a fresh process."""
+@pytest.mark.parametrize("var,alt", [("BM_ASSIGN_MODE", "exact"), ("BM_GRAPHS", "0")])
+def test_engine_modes_agree(var, alt):
+    """Unscreened assignment (BM_ASSIGN_MODE=exact) and the host-driven chunk
+    loop (BM_GRAPHS=0) give the same bits as the default path, in fresh processes."""
     import subprocess, sys, os
     code = (
         "import numpy as np, sys; sys.path.insert(0, '.');"
@@ -172,8 +174,8 @@ def test_exact_mode_matches_screen_mode():
         "import hashlib; print(repr(o.objective), o.counter.distance_evals, hashlib.sha1(o.centroids.values.tobytes()).hexdigest())")
     env = dict(os.environ)
     outs = []
-    for mode in ("screen", "exact"):
-        env["BM_ASSIGN_MODE"] = mode
+    for mode in ("default", alt):
+        env[var] = mode
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                                    text=True, check=True).stdout)
     assert outs[0] == outs[1] and outs[0]
