@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
+#include "tma.cuh"
 
 struct bm_rng {
     bm::Mt64 eng;  // Rng (common.hpp:13): std::mt19937_64 stream, libstdc++ distributions
@@ -134,6 +135,8 @@ struct Workspace {
     DevBuf<double> psum;     // tiles * k * n
     DevBuf<uint32_t> pcnt;   // tiles * k
     DevBuf<double> C, Cact;  // k * n
+    DevBuf<float> CT32;      // n * 32: fp32 compacted centroids, transposed [d][j] (TMA screen)
+    CUtensorMap tm_ct{};     // tensor map of CT32
     DevBuf<uint8_t> mask;    // k
     DevBuf<int> act;         // k
     DevBuf<dev::LloydStatus> status;
@@ -172,6 +175,18 @@ struct Workspace {
     HostBuf<uint8_t> h_mask;
     HostBuf<uint32_t> h_cand;
 
+    void encode_ct_map() {
+        auto enc = tmap_encoder();
+        if (!enc) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        const cuuint64_t dims[2] = {(cuuint64_t)dev::kSMaxK, (cuuint64_t)n};
+        const cuuint64_t strides[1] = {(cuuint64_t)dev::kSMaxK * sizeof(float)};
+        const cuuint32_t box[2] = {(cuuint32_t)dev::kSMaxK, (cuuint32_t)dev::kADC};
+        const cuuint32_t es[2] = {1, 1};
+        if (enc(&tm_ct, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, CT32.p, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            throw CudaError("cuTensorMapEncodeTiled(centroids) failed");
+    }
     void init(uint64_t rows, int k_, int n_, int ncand_, uint64_t hist) {
         R = rows;
         k = k_;
@@ -189,6 +204,11 @@ struct Workspace {
         pcnt.alloc(tiles * (uint64_t)k);
         C.alloc((uint64_t)k * n);
         Cact.alloc((uint64_t)k * (n + (n & 1)));
+        if (k <= dev::kSMaxK) {
+            CT32.alloc((uint64_t)n * dev::kSMaxK);
+            BM_CUDA(cudaMemset(CT32.p, 0, (uint64_t)n * dev::kSMaxK * sizeof(float)));
+            encode_ct_map();
+        }
         mask.alloc(k);
         act.alloc(k);
         status.alloc(1);
@@ -461,6 +481,33 @@ dev::ScreenConsts screen_consts(int n) {
     return c;
 }
 
+// Tensor map of a points view: 2-D [rows][n] (stride ld), box 16 dims x 128 rows.
+template <class T>
+CUtensorMap points_map(const Points& P) {
+    CUtensorMap m{};
+    auto enc = tmap_encoder();
+    if (!enc) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)P.n, (cuuint64_t)P.rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(P.ld * sizeof(T))};
+    const cuuint32_t box[2] = {(cuuint32_t)dev::kADC, (cuuint32_t)dev::kABP};
+    const cuuint32_t es[2] = {1, 1};
+    const auto dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const auto sw = sizeof(T) == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    if (enc(&m, dt, 2, const_cast<void*>(P.X), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled(points) failed");
+    return m;
+}
+
+// BM_SCREEN=v4 selects the LDG-staged screen (A/B checks); default: TMA (v5).
+bool tma_screen() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_SCREEN");
+        return !(e && std::string(e) == "v4");
+    }();
+    return on;
+}
+
 // BM_ASSIGN_MODE=exact forces the unscreened kernel (A/B parity checks).
 bool screen_enabled(int k) {
     static const bool exact_forced = [] {
@@ -486,7 +533,20 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     const bool screen = screen_enabled(k);
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
-        if (screen) {
+        if (screen && tma_screen() && P.rows < (1ull << 31)) {
+            constexpr size_t shm = dev::tma_smem_bytes<T>();
+            static bool attr_set = false;  // per template instance
+            if (!attr_set) {
+                BM_CUDA(cudaFuncSetAttribute(dev::k_assign_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)shm));
+                attr_set = true;
+            }
+            const CUtensorMap tmx = points_map<T>(P);
+            dev::k_assign_tma<T><<<grid, dev::kSThreads, shm, st>>>(
+                tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
+                &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
+                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
+        } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
             static bool attr_set = false;  // per template instance
             if (!attr_set) {
@@ -520,7 +580,7 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
 
 void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_t* mask) {
     dev::k_compact<<<1, 256, w.k * sizeof(int), st>>>(C, mask, w.k, w.n, w.Cact.p, w.ldc, w.act.p,
-                                                       &w.status.p->n_active);
+                                                       &w.status.p->n_active, w.CT32.p);
     BM_LAUNCH();
     count_launch();
 }
@@ -550,7 +610,8 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
     if (mshm > 48 * 1024)
         BM_CUDA(cudaFuncSetAttribute(dev::k_update_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mshm));
     dev::k_update_merge<<<mgrid, dev::kMThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p, w.mask.p,
-                                                            w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active, stop);
+                                                            w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active,
+                                                            w.CT32.p, stop);
     BM_LAUNCH();
     count_launch(2);
 }

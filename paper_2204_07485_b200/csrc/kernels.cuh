@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "mt64.cuh"
+#include "tma.cuh"
 
 namespace bm {
 namespace dev {
@@ -832,6 +833,371 @@ k_assign_screen(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
 
 constexpr size_t screen_smem_bytes() { return sizeof(ScreenSmem); }
 
+// ---------------------------------------------------------------------------
+// 3c. Screened exact assignment, TMA pipeline (v5).  Same mathematics and
+// results as k_assign_screen; only the data movement differs:
+//  * one thread issues 2-D TMA tile loads (128 points x 16 dims, hardware
+//    swizzle) of the points and of the fp32 transposed centroids (CT32[d][j])
+//    into a 2-stage ring, completion on one mbarrier per stage;
+//  * all threads convert the landed raw slab once (f64 -> fp32, round to
+//    nearest) into a double-buffered [d][p] fp32 slab, ONE CTA barrier per
+//    slab, after which the stage is refilled with slab+2 while the screen of
+//    the current slab runs.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct TmaSmem {
+    static constexpr int kRawBytes = kABP * kADC * sizeof(T);  // 16 KB (f64) / 8 KB (f32)
+    alignas(1024) unsigned char raw[2][kRawBytes];             // swizzled point tiles
+    alignas(1024) float craw[2][kADC][kSMaxK];                 // centroid tiles [d][j]
+    alignas(16) float xs[2][kADC][kABP];                       // fp32 point slabs [d][p]
+    alignas(16) float cs[2][kADC][kSMaxK];
+    float Ls[kSMaxK][kABP];
+    float red_u[8][kABP];
+    float nx_lo[kABP], nx_hi[kABP], nxr[kABP];
+    float nc_lo[kSMaxK], nc_hi[kSMaxK], ncr[kSMaxK];
+    float umin[kABP];
+    int icount[kABP];
+    uint64_t bar[2];
+    uint32_t n_items;
+    int is_last;
+};
+
+template <typename T>
+__device__ __forceinline__ T raw_at(const unsigned char* raw, int p, int d) {
+    if constexpr (sizeof(T) == 8) {  // 128-byte rows, SWIZZLE_128B: chunk ^= p & 7
+        const int off = p * 128 + ((((d >> 1) ^ p) & 7) << 4) + ((d & 1) << 3);
+        return *reinterpret_cast<const double*>(raw + off);
+    } else {  // 64-byte rows, SWIZZLE_64B: chunk ^= (p >> 1) & 3
+        const int off = p * 64 + ((((d >> 2) ^ (p >> 1)) & 3) << 4) + ((d & 3) << 2);
+        return *reinterpret_cast<const float*>(raw + off);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kSThreads, 3)
+k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmc,
+             const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+             const double* __restrict__ Cact, int ldc, const int* __restrict__ act_idx,
+             const int* __restrict__ n_active_ptr,
+             int32_t* __restrict__ labels_pair, uint64_t pair_stride,
+             const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
+             int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
+             double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
+             unsigned long long* __restrict__ cand_counter, ScreenConsts cst) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // TMA destinations with 128-byte swizzle need 1024-byte alignment
+    unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    TmaSmem<T>& S = *reinterpret_cast<TmaSmem<T>*>(smem_al);
+    constexpr unsigned kStageBytes = TmaSmem<T>::kRawBytes + kADC * kSMaxK * sizeof(float);
+
+    if (stop_ptr && *stop_ptr) return;
+    const int KA = *n_active_ptr;
+    int32_t* labels_out = labels_pair;
+    const int32_t* labels_old = nullptr;
+    if (parity_ptr) {
+        const int par = *parity_ptr;
+        labels_out = labels_pair + (1 - par) * pair_stride;
+        labels_old = labels_pair + par * pair_stride;
+    }
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int KG = (KA + kAK - 1) / kAK;
+    const bool comp = warp < KG;
+    const bool normw = warp == 7;
+    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
+    const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
+    const float finf = __int_as_float(0x7F800000);
+    const int nslab = (n + kADC - 1) / kADC;
+
+    if (tid == 0) {
+        tma_prefetch_map(&tmx);
+        tma_prefetch_map(&tmc);
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int sl) {
+        const int st = sl & 1;
+        mbar_expect_tx(&S.bar[st], kStageBytes);
+        tma_load_2d(S.raw[st], &tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
+        tma_load_2d(&S.craw[st][0][0], &tmc, &S.bar[st], 0, sl * kADC);
+    };
+    if (tid == 0) {
+        issue(0);
+        if (nslab > 1) issue(1);
+    }
+
+    float2 tot[2][kAK];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int u = 0; u < kAK; ++u) tot[h][u] = make_float2(0.f, 0.f);
+    float nxl[4] = {0.f, 0.f, 0.f, 0.f}, nxh[4] = {0.f, 0.f, 0.f, 0.f};
+    float ncl = 0.f, nch = 0.f;
+    const int cp_ = tid & (kABP - 1), chalf = tid >> 7;  // conversion: point, 8-dim half
+
+    for (int sl = 0; sl < nslab; ++sl) {
+        const int st = sl & 1, dl = min(kADC, n - sl * kADC);
+        mbar_wait(&S.bar[st], (sl >> 1) & 1);
+        // raw (swizzled [p][d], storage type) -> fp32 [d][p], once per element
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int d = 8 * chalf + i;
+            S.xs[st][d][cp_] = static_cast<float>(raw_at<T>(S.raw[st], cp_, d));
+        }
+        if (tid < kADC * kSMaxK / 4) {
+            const float4 v = reinterpret_cast<const float4*>(&S.craw[st][0][0])[tid];
+            reinterpret_cast<float4*>(&S.cs[st][0][0])[tid] = v;
+        }
+        __syncthreads();  // slab ready; every thread has left slab sl-1 and stage st is free
+        if (tid == 0 && sl + 2 < nslab) issue(sl + 2);
+        if (comp) {
+            float2 part[2][kAK];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < kAK; ++u) part[h][u] = make_float2(0.f, 0.f);
+#pragma unroll 4
+            for (int d = 0; d < dl; ++d) {
+                const float4 xv = *reinterpret_cast<const float4*>(&S.xs[st][d][4 * lane]);
+                const float4 cv = *reinterpret_cast<const float4*>(&S.cs[st][d][4 * warp]);
+                const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
+                part[0][0] = ffma2(xa, cv.x, part[0][0]);
+                part[0][1] = ffma2(xa, cv.y, part[0][1]);
+                part[0][2] = ffma2(xa, cv.z, part[0][2]);
+                part[0][3] = ffma2(xa, cv.w, part[0][3]);
+                part[1][0] = ffma2(xb, cv.x, part[1][0]);
+                part[1][1] = ffma2(xb, cv.y, part[1][1]);
+                part[1][2] = ffma2(xb, cv.z, part[1][2]);
+                part[1][3] = ffma2(xb, cv.w, part[1][3]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < kAK; ++u) tot[h][u] = fadd2(tot[h][u], part[h][u]);
+        }
+        if (normw) {
+            for (int d = 0; d < dl; ++d) {
+                const float4 xv = *reinterpret_cast<const float4*>(&S.xs[st][d][4 * lane]);
+                nxl[0] = __fmaf_rd(xv.x, xv.x, nxl[0]); nxh[0] = __fmaf_ru(xv.x, xv.x, nxh[0]);
+                nxl[1] = __fmaf_rd(xv.y, xv.y, nxl[1]); nxh[1] = __fmaf_ru(xv.y, xv.y, nxh[1]);
+                nxl[2] = __fmaf_rd(xv.z, xv.z, nxl[2]); nxh[2] = __fmaf_ru(xv.z, xv.z, nxh[2]);
+                nxl[3] = __fmaf_rd(xv.w, xv.w, nxl[3]); nxh[3] = __fmaf_ru(xv.w, xv.w, nxh[3]);
+                const float c = S.cs[st][d][lane];
+                ncl = __fmaf_rd(c, c, ncl);
+                nch = __fmaf_ru(c, c, nch);
+            }
+        }
+    }
+    if (normw) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            S.nx_lo[4 * lane + q] = nxl[q];
+            S.nx_hi[4 * lane + q] = nxh[q];
+            S.nxr[4 * lane + q] = __fsqrt_ru(nxh[q]);
+        }
+        S.nc_lo[lane] = ncl;
+        S.nc_hi[lane] = nch;
+        S.ncr[lane] = __fsqrt_ru(nch);
+    }
+    __syncthreads();
+    // certified bounds (same algebra as k_assign_screen)
+    if (comp) {
+        float un[4] = {finf, finf, finf, finf};
+#pragma unroll
+        for (int u = 0; u < kAK; ++u) {
+            const int j = kAK * warp + u;
+            if (j >= KA) continue;
+            const float cl = S.nc_lo[j], ch = S.nc_hi[j], crr = S.ncr[j];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int p = 4 * lane + q;
+                const float sdot = q & 1 ? tot[q >> 1][u].y : tot[q >> 1][u].x;
+                const float t2 = 2.f * sdot;
+                const float Sn = __fadd_ru(S.nxr[p], crr);
+                const float Al = __fadd_rd(S.nx_lo[p], cl), Ah = __fadd_ru(S.nx_hi[p], ch);
+                float L = 0.f, U = finf;
+                if (fabsf(t2) <= 1.0e37f && Sn <= 1.0e18f && Ah <= 1.0e37f) {
+                    const float D = __fadd_ru(__fmul_ru(__fmul_ru(cst.K, Sn), Sn), cst.dabs);
+                    L = fmaxf(__fsub_rd(__fsub_rd(Al, t2), D), 0.f);
+                    L = __fmul_rd(L, cst.lo64);
+                    U = __fmul_ru(__fadd_ru(__fsub_ru(Ah, t2), D), cst.hi64);
+                }
+                S.Ls[j][p] = L;
+                un[q] = fminf(un[q], U);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S.red_u[warp][4 * lane + q] = un[q];
+    }
+    __syncthreads();
+    if (tid < kABP) {
+        const int p = tid;
+        float m = finf;
+        for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][p]);
+        S.umin[p] = m;
+        int c = 0;
+        if (p < np)
+            for (int j = 0; j < KA; ++j) c += S.Ls[j][p] <= m;
+        S.icount[p] = c;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        int v[4], run = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            v[q] = S.icount[4 * tid + q];
+            run += v[q];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        int ex = incl - run;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            S.icount[4 * tid + q] = ex;
+            ex += v[q];
+        }
+        if (tid == 31) {
+            S.n_items = static_cast<uint32_t>(incl);
+            if (cand_counter) {
+                atomicAdd(cand_counter, static_cast<unsigned long long>(incl));
+                atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t NI = S.n_items;
+    // item buffers alias the (drained) raw ring
+    double* item_d = reinterpret_cast<double*>(&S.raw[0][0]);
+    short* item_p = reinterpret_cast<short*>(item_d + kItemCap);
+    signed char* item_j = reinterpret_cast<signed char*>(item_p + kItemCap);
+    const bool overflow = NI > static_cast<uint32_t>(kItemCap);
+    if (!overflow) {
+        if (tid < np) {
+            const int p = tid;
+            const float m = S.umin[p];
+            uint32_t it = S.icount[p];
+            for (int j = 0; j < KA; ++j)
+                if (S.Ls[j][p] <= m) {
+                    item_p[it] = static_cast<short>(p);
+                    item_j[it] = static_cast<signed char>(j);
+                    ++it;
+                }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < NI; i += kSThreads) {
+            const int p = item_p[i], j = item_j[i];
+            const T* xrow = X + (p0 + p) * ld;
+            const double* crow = Cact + static_cast<uint64_t>(j) * ldc;
+            double a = 0.0;
+            int d = 0;
+            for (; d + 8 <= n; d += 8) {
+                double xv[8], cv[8];
+                if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 t = *reinterpret_cast<const double2*>(xrow + d + 2 * q);
+                        xv[2 * q] = t.x;
+                        xv[2 * q + 1] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const float4 t = *reinterpret_cast<const float4*>(xrow + d + 4 * q);
+                        xv[4 * q] = t.x;
+                        xv[4 * q + 1] = t.y;
+                        xv[4 * q + 2] = t.z;
+                        xv[4 * q + 3] = t.w;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(crow + d + 2 * q));
+                    cv[2 * q] = t.x;
+                    cv[2 * q + 1] = t.y;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) a = dist_step(a, xv[q], cv[q]);
+            }
+            for (; d < n; ++d) a = dist_step(a, to_f64(xrow[d]), crow[d]);
+            item_d[i] = a;
+        }
+        __syncthreads();
+    }
+    if (tid < np) {
+        const int p = tid;
+        const uint64_t gp = p0 + p;
+        double best = __longlong_as_double(0x7FF0000000000000LL);
+        int bj = -1;
+        if (!overflow) {
+            const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(S.icount[p + 1]) : NI;
+            for (uint32_t i = S.icount[p]; i < b1; ++i) {
+                if (item_d[i] < best) {
+                    best = item_d[i];
+                    bj = item_j[i];
+                }
+            }
+        } else {
+            const T* x = X + gp * ld;
+            for (int j = 0; j < KA; ++j) {
+                const double* c = Cact + static_cast<uint64_t>(j) * ldc;
+                double sm = 0.0;
+                for (int d = 0; d < n; ++d) sm = dist_step(sm, to_f64(x[d]), c[d]);
+                if (sm < best) {
+                    best = sm;
+                    bj = j;
+                }
+            }
+        }
+        const int label = bj >= 0 ? act_idx[bj] : -1;
+        labels_out[gp] = label;
+        if (dists_out) dists_out[gp] = best;
+        if (labels_old && labels_old[gp] != label) *changed_flag = 1;
+    }
+    if (!tile_out) return;
+    __syncthreads();
+    const uint64_t tile = p0 / kTile;
+    if (tid == 0) {
+        __threadfence();
+        const uint64_t tb = tile * kTile;
+        const unsigned ctas = static_cast<unsigned>((min(rows, tb + kTile) - tb + kABP - 1) / kABP);
+        const unsigned old = atomicAdd(&tile_counter[tile], 1u);
+        S.is_last = old == ctas - 1;
+    }
+    __syncthreads();
+    if (!S.is_last) return;
+    __threadfence();
+    const uint64_t tb = tile * kTile;
+    const int len = static_cast<int>(min(rows, tb + kTile) - tb);
+    double* fold = reinterpret_cast<double*>(&S.raw[0][0]);
+    for (int i = tid; i < len; i += kSThreads) fold[i] = __ldcg(dists_out + tb + i);
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0;
+        int i = 0;
+        for (; i + 8 <= len; i += 8) {
+            const double2 v0 = *reinterpret_cast<const double2*>(fold + i);
+            const double2 v1 = *reinterpret_cast<const double2*>(fold + i + 2);
+            const double2 v2 = *reinterpret_cast<const double2*>(fold + i + 4);
+            const double2 v3 = *reinterpret_cast<const double2*>(fold + i + 6);
+            a = __dadd_rn(a, v0.x); a = __dadd_rn(a, v0.y);
+            a = __dadd_rn(a, v1.x); a = __dadd_rn(a, v1.y);
+            a = __dadd_rn(a, v2.x); a = __dadd_rn(a, v2.y);
+            a = __dadd_rn(a, v3.x); a = __dadd_rn(a, v3.y);
+        }
+        for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
+        tile_out[tile] = a;
+        tile_counter[tile] = 0u;
+    }
+}
+
+template <typename T>
+constexpr size_t tma_smem_bytes() { return sizeof(TmaSmem<T>) + 1024; }
+
 // ===========================================================================
 // 4. Per-tile sequential sums (block_sum inner loop core.cpp:167-173).
 //    One warp per (array, tile); lanes stage 32 values, all lanes fold them in
@@ -998,7 +1364,7 @@ __global__ void __launch_bounds__(kMThreads)
 k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcnt, uint64_t ntiles,
                int k, int n, double* __restrict__ C, uint8_t* __restrict__ mask,
                double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
-               const int* __restrict__ stop_ptr) {
+               float* __restrict__ CT32, const int* __restrict__ stop_ptr) {
     if (stop_ptr && *stop_ptr) return;
     extern __shared__ unsigned long long msh[];
     unsigned long long* total = msh;                         // [k]
@@ -1067,11 +1433,13 @@ k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcn
     const double v = __dmul_rn(acc, inv);
     C[e] = v;
     Cact[static_cast<uint64_t>(rankj) * ldc + d] = v;
+    if (CT32 && rankj < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rankj] = __double2float_rn(v);
 }
 
 // Compact the active rows of (C, mask) for the assignment (single CTA).
 __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restrict__ mask, int k, int n,
-                          double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active) {
+                          double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
+                          float* __restrict__ CT32) {
     extern __shared__ int csh[];
     if (threadIdx.x == 0) {
         int r = 0;
@@ -1084,7 +1452,10 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
     __syncthreads();
     for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
         const int j = e / n;
-        if (csh[j] >= 0) Cact[static_cast<uint64_t>(csh[j]) * ldc + (e % n)] = C[e];
+        if (csh[j] >= 0) {
+            Cact[static_cast<uint64_t>(csh[j]) * ldc + (e % n)] = C[e];
+            if (CT32 && csh[j] < kSMaxK) CT32[static_cast<uint64_t>(e % n) * kSMaxK + csh[j]] = __double2float_rn(C[e]);
+        }
     }
 }
 
