@@ -851,11 +851,10 @@ struct TmaSmem {
     alignas(1024) float craw[2][kADC][kSMaxK];                 // centroid tiles [d][j]
     alignas(16) float xs[2][kADC][kABP];                       // fp32 point slabs [d][p]
     alignas(16) float cs[2][kADC][kSMaxK];
-    float Ls[kSMaxK][kABP];
-    float red_u[8][kABP];
+    float red_u[8][kABP];                                      // per-warp min upper bound
     float nx_lo[kABP], nx_hi[kABP], nxr[kABP];
     float nc_lo[kSMaxK], nc_hi[kSMaxK], ncr[kSMaxK];
-    float umin[kABP];
+    unsigned cand[kABP];                                       // candidate bitmask per point
     int icount[kABP];
     uint64_t bar[2];
     uint32_t n_items;
@@ -1001,14 +1000,18 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         S.ncr[lane] = __fsqrt_ru(nch);
     }
     __syncthreads();
-    // certified bounds (same algebra as k_assign_screen)
+    // certified bounds (same algebra as k_assign_screen): upper bounds first,
+    // then each warp tests its lower bounds against the point's minimum U and
+    // sets candidate bits (no per-(j,p) bound array is kept).
+    float Lk[4][kAK];
+    if (tid < kABP) S.cand[tid] = 0u;
     if (comp) {
         float un[4] = {finf, finf, finf, finf};
 #pragma unroll
         for (int u = 0; u < kAK; ++u) {
             const int j = kAK * warp + u;
-            if (j >= KA) continue;
-            const float cl = S.nc_lo[j], ch = S.nc_hi[j], crr = S.ncr[j];
+            const float cl = j < KA ? S.nc_lo[j] : 0.f, ch = j < KA ? S.nc_hi[j] : 0.f;
+            const float crr = j < KA ? S.ncr[j] : 0.f;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int p = 4 * lane + q;
@@ -1023,30 +1026,33 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                     L = __fmul_rd(L, cst.lo64);
                     U = __fmul_ru(__fadd_ru(__fsub_ru(Ah, t2), D), cst.hi64);
                 }
-                S.Ls[j][p] = L;
-                un[q] = fminf(un[q], U);
+                Lk[q][u] = j < KA ? L : finf;
+                if (j < KA) un[q] = fminf(un[q], U);
             }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) S.red_u[warp][4 * lane + q] = un[q];
     }
     __syncthreads();
-    if (tid < kABP) {
-        const int p = tid;
-        float m = finf;
-        for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][p]);
-        S.umin[p] = m;
-        int c = 0;
-        if (p < np)
-            for (int j = 0; j < KA; ++j) c += S.Ls[j][p] <= m;
-        S.icount[p] = c;
+    if (comp) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int p = 4 * lane + q;
+            float m = finf;
+            for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][p]);
+            unsigned bits = 0;
+#pragma unroll
+            for (int u = 0; u < kAK; ++u)
+                if (Lk[q][u] <= m) bits |= 1u << (kAK * warp + u);
+            if (bits && p < np) atomicOr(&S.cand[p], bits);
+        }
     }
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 32) {  // exclusive scan of the candidate counts -> item offsets
         int v[4], run = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            v[q] = S.icount[4 * tid + q];
+            v[q] = __popc(S.cand[4 * tid + q]);
             run += v[q];
         }
         int incl = run;
@@ -1079,14 +1085,15 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     if (!overflow) {
         if (tid < np) {
             const int p = tid;
-            const float m = S.umin[p];
             uint32_t it = S.icount[p];
-            for (int j = 0; j < KA; ++j)
-                if (S.Ls[j][p] <= m) {
-                    item_p[it] = static_cast<short>(p);
-                    item_j[it] = static_cast<signed char>(j);
-                    ++it;
-                }
+            unsigned bits = S.cand[p];
+            while (bits) {  // ascending j
+                const int j = __ffs(bits) - 1;
+                bits &= bits - 1;
+                item_p[it] = static_cast<short>(p);
+                item_j[it] = static_cast<signed char>(j);
+                ++it;
+            }
         }
         __syncthreads();
         for (uint32_t i = tid; i < NI; i += kSThreads) {
