@@ -233,11 +233,12 @@ struct SamplerWs {
     uint64_t m = 0, s = 0;
     uint32_t hmask = 0;
     uint32_t nwords = 0, nblocks = 0;
-    DevBuf<uint32_t> js, js2, hkeys, bitmap, blockcnt, idx;  // js2: second target buffer (pipelined draws)
+    DevBuf<uint32_t> js, js2, bitmap, blockcnt, idx;  // js2: second target buffer (pipelined draws)
+    DevBuf<unsigned long long> hkeys, hvals, LT;      // epoch-tagged resolution tables
+    DevBuf<uint32_t> excl;                            // epoch of exclusion per value < s
+    DevBuf<uint32_t> epoch;                           // [0] counter, [1+b] epoch of target buffer b
     cudaStream_t rng_stream = nullptr;                      // device draws of the next chunk
     cudaEvent_t drawn[2] = {nullptr, nullptr}, resolved[2] = {nullptr, nullptr};
-    DevBuf<int> LT, hvals;
-    DevBuf<uint8_t> kept;
     DevBuf<Mt64State> mt;           // device-resident RNG stream (big_means chains)
     HostBuf<Mt64State> h_mt;
     HostBuf<uint32_t> h_js[2];
@@ -256,11 +257,18 @@ struct SamplerWs {
         js2.alloc(s);
         hkeys.alloc(h);
         hvals.alloc(h);
+        BM_CUDA(cudaMemset(hkeys.p, 0, h * sizeof(unsigned long long)));
+        BM_CUDA(cudaMemset(hvals.p, 0, h * sizeof(unsigned long long)));
         bitmap.alloc(nwords);
         blockcnt.alloc(std::max<uint32_t>(nblocks, 1));
         idx.alloc(s);
         LT.alloc(s);
-        kept.alloc(s);
+        excl.alloc(s);
+        epoch.alloc(3);
+        BM_CUDA(cudaMemset(LT.p, 0, s * sizeof(unsigned long long)));
+        BM_CUDA(cudaMemset(excl.p, 0, s * sizeof(uint32_t)));
+        BM_CUDA(cudaMemset(epoch.p, 0, 3 * sizeof(uint32_t)));
+        BM_CUDA(cudaMemset(bitmap.p, 0, nwords * sizeof(uint32_t)));
         mt.alloc(1);
         h_mt.alloc(1);
         for (int b = 0; b < 2; ++b) {
@@ -272,6 +280,7 @@ struct SamplerWs {
         if (!rng_stream) BM_CUDA(cudaStreamCreateWithFlags(&rng_stream, cudaStreamNonBlocking));
     }
     uint32_t* jsbuf(int b) { return b ? js2.p : js.p; }
+    uint32_t* epoch_slot(int b) { return epoch.p + 1 + b; }
     ~SamplerWs() {
         for (auto* arr : {js_done, drawn, resolved})
             for (int b = 0; b < 2; ++b)
@@ -842,10 +851,10 @@ uint32_t* draw_targets(SamplerWs& sw, Mt64& rng) {
     return out;
 }
 
-// Device-side draws (k_mt_draw) from the device-resident stream in sw.mt.
-void enqueue_device_draw(cudaStream_t st, SamplerWs& sw, int force_seq = 0, uint32_t* out = nullptr) {
-    dev::k_mt_draw<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.m, (uint32_t)sw.s, out ? out : sw.js.p, nullptr,
-                                                  force_seq);
+// Device-side draws (k_mt_draw) from the device-resident stream into target buffer b.
+void enqueue_device_draw(cudaStream_t st, SamplerWs& sw, int force_seq = 0, int b = 0) {
+    dev::k_mt_draw<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.m, (uint32_t)sw.s, sw.jsbuf(b), nullptr, force_seq,
+                                                  sw.epoch.p, sw.epoch_slot(b));
     BM_LAUNCH();
     count_launch();
 }
@@ -862,37 +871,34 @@ void get_stream(cudaStream_t st, SamplerWs& sw, Mt64& rng) {
     rng.s = *sw.h_mt.p;
 }
 
-// Fisher-Yates resolution of the targets already in sw.js; result in sw.idx.
-void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw, const uint32_t* js = nullptr) {
+// Fisher-Yates resolution of the targets in buffer b (epoch-tagged tables, no
+// clearing between chunks); result in sw.idx.
+void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw, int b = 0) {
     PhaseScope ps(PH_SAMPLE, sw.s);
     const uint32_t s = (uint32_t)sw.s;
-    if (!js) js = sw.js.p;
-    BM_CUDA(cudaMemsetAsync(sw.LT.p, 0xFF, s * sizeof(int), st));
-    BM_CUDA(cudaMemsetAsync(sw.hkeys.p, 0xFF, (sw.hmask + 1) * sizeof(uint32_t), st));
-    BM_CUDA(cudaMemsetAsync(sw.hvals.p, 0xFF, (sw.hmask + 1) * sizeof(int), st));
-    BM_CUDA(cudaMemsetAsync(sw.kept.p, 1, s, st));
-    BM_CUDA(cudaMemsetAsync(sw.bitmap.p, 0, sw.nwords * sizeof(uint32_t), st));
+    const uint32_t* js = sw.jsbuf(b);
+    const uint32_t* ep = sw.epoch_slot(b);
     const unsigned g = (unsigned)ceil_div(s, 256);
-    dev::k_fy_pass1<<<g, 256, 0, st>>>(js, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
-    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.kept.p,
+    dev::k_fy_pass1<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
+    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.excl.p,
                                        sw.bitmap.p);
-    dev::k_fy_pass3<<<g, 256, 0, st>>>(sw.kept.p, s, sw.bitmap.p);
-    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.nwords,
-                                                                         sw.blockcnt.p);
-    dev::k_scan_block_counts<<<1, dev::kScanThreads, 0, st>>>(sw.blockcnt.p, sw.nblocks);
-    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.nwords, sw.blockcnt.p,
-                                                                 sw.idx.p);
+    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.excl.p, ep, s,
+                                                                         sw.nwords, sw.blockcnt.p);
+    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.excl.p, ep, s, sw.nwords,
+                                                                 sw.blockcnt.p, sw.idx.p);
     BM_LAUNCH();
-    count_launch(6);
+    count_launch(4);
 }
 
-// Upload the host-drawn targets of buffer sw.cur, then resolve.
+// Upload the host-drawn targets of pinned buffer sw.cur into target buffer 0, then resolve.
 void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
     const int b = sw.cur;
     BM_CUDA(cudaMemcpyAsync(sw.js.p, sw.h_js[b].p, sw.s * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
     BM_CUDA(cudaEventRecord(sw.js_done[b], st));
     sw.cur ^= 1;
-    enqueue_resolve_device(st, sw);
+    dev::k_epoch_bump<<<1, 32, 0, st>>>(sw.epoch.p, sw.epoch_slot(0));
+    BM_LAUNCH();
+    enqueue_resolve_device(st, sw, 0);
 }
 
 void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
@@ -969,7 +975,7 @@ cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, DeviceCache& 
                              Workspace& w, int b) {
     cudaGraph_t g = nullptr;
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    enqueue_resolve_device(st, sw, sw.jsbuf(b));
+    enqueue_resolve_device(st, sw, b);
     BM_CUDA(cudaEventRecordWithFlags(sw.resolved[b], st, cudaEventRecordExternal));
     enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, dc.chunk.p);
     BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)w.k * w.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1085,7 +1091,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         const int jb = (int)(chunk & 1);
         if (!identity) {  // sample_chunk (:79): draws made on rng_stream, resolution + gather (:80) here
             if (!drawn_ahead) {
-                enqueue_device_draw(sw->rng_stream, *sw, 0, sw->jsbuf(jb));
+                enqueue_device_draw(sw->rng_stream, *sw, 0, jb);
                 BM_CUDA(cudaEventRecord(sw->drawn[jb], sw->rng_stream));
             }
             count_launch();
@@ -1097,7 +1103,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             count_launch(7);
         } else {
             if (!identity) {
-                enqueue_resolve_device(st, *sw, sw->jsbuf(jb));
+                enqueue_resolve_device(st, *sw, jb);
                 BM_CUDA(cudaEventRecord(sw->resolved[jb], st));
                 enqueue_gather(st, d, sw->idx.p, (uint32_t)s, dc.chunk.p);
             }
@@ -1123,7 +1129,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         const bool next_exists = !identity && (!cfg.has_max_chunks || chunk + 1 < cfg.max_chunks);
         if (next_exists) {
             if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[jb ^ 1], 0));
-            enqueue_device_draw(sw->rng_stream, *sw, 0, sw->jsbuf(jb ^ 1));
+            enqueue_device_draw(sw->rng_stream, *sw, 0, jb ^ 1);
             BM_CUDA(cudaEventRecord(sw->drawn[jb ^ 1], sw->rng_stream));
             drawn_ahead = true;
         }

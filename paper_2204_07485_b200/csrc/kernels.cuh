@@ -76,46 +76,169 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t key, uint32_t hmask) {
     return (key * 2654435761u) & hmask;
 }
 
-__global__ void k_fy_pass1(const uint32_t* __restrict__ js, uint32_t s, int* __restrict__ LT,
-                           uint32_t* __restrict__ hkeys, int* __restrict__ hvals, uint32_t hmask) {
+// All tables are tagged with a per-draw epoch (epoch << 32 | payload): an entry
+// of an older epoch reads as empty, so nothing is cleared between chunks.
+//   LT[t]   = max{t' < t : j_t' = t}            (atomicMax on the tagged value)
+//   hkey/hval: open-addressing map target p >= s -> last step hitting p
+//   excl[v] = epoch  when value v < s leaves the first s positions
+__device__ __forceinline__ unsigned long long tag(uint32_t epoch, uint32_t v) {
+    return (static_cast<unsigned long long>(epoch) << 32) | v;
+}
+
+__global__ void k_fy_pass1(const uint32_t* __restrict__ js, const uint32_t* __restrict__ epoch_slot, uint32_t s,
+                           unsigned long long* __restrict__ LT, unsigned long long* __restrict__ hkeys,
+                           unsigned long long* __restrict__ hvals, uint32_t hmask) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= s) return;
+    const uint32_t ep = *epoch_slot;
     const uint32_t j = js[t];
     if (j < s) {
-        if (j > t) atomicMax(&LT[j], static_cast<int>(t));
+        if (j > t) atomicMax(&LT[j], tag(ep, t));
         return;
     }
     uint32_t h = hash_slot(j, hmask);
+    const unsigned long long mine = tag(ep, j);
     while (true) {
-        const uint32_t prev = atomicCAS(&hkeys[h], 0xFFFFFFFFu, j);
-        if (prev == 0xFFFFFFFFu || prev == j) {
-            atomicMax(&hvals[h], static_cast<int>(t));
+        unsigned long long cur = hkeys[h];
+        if ((cur >> 32) != ep) {  // stale: try to claim it for this epoch
+            const unsigned long long prev = atomicCAS(&hkeys[h], cur, mine);
+            if (prev != cur) continue;  // raced; re-examine this slot
+            cur = mine;
+        }
+        if (cur == mine) {
+            atomicMax(&hvals[h], tag(ep, t));
             return;
         }
         h = (h + 1) & hmask;
     }
 }
 
-__global__ void k_fy_pass2(const uint32_t* __restrict__ js, uint32_t s, const int* __restrict__ LT,
-                           const uint32_t* __restrict__ hkeys, const int* __restrict__ hvals,
-                           uint32_t hmask, uint8_t* __restrict__ kept, uint32_t* __restrict__ bitmap) {
+__global__ void k_fy_pass2(const uint32_t* __restrict__ js, const uint32_t* __restrict__ epoch_slot, uint32_t s,
+                           const unsigned long long* __restrict__ LT, const unsigned long long* __restrict__ hkeys,
+                           const unsigned long long* __restrict__ hvals, uint32_t hmask,
+                           uint32_t* __restrict__ excl, uint32_t* __restrict__ bitmap) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= s) return;
+    const uint32_t ep = *epoch_slot;
     const uint32_t j = js[t];
     if (j < s) return;
+    const unsigned long long mine = tag(ep, j);
     uint32_t h = hash_slot(j, hmask);
-    while (hkeys[h] != j) h = (h + 1) & hmask;
-    if (hvals[h] != static_cast<int>(t)) return;  // not the last swap into j
+    while (hkeys[h] != mine) h = (h + 1) & hmask;
+    if (hvals[h] != tag(ep, t)) return;  // not the last swap into j
     atomicOr(&bitmap[j >> 5], 1u << (j & 31));
-    int w = static_cast<int>(t);
-    while (LT[w] >= 0) w = LT[w];
-    kept[w] = 0;
+    uint32_t w = t;
+    while (true) {
+        const unsigned long long v = LT[w];
+        if ((v >> 32) != ep) break;
+        w = static_cast<uint32_t>(v);
+    }
+    excl[w] = ep;
 }
 
-__global__ void k_fy_pass3(const uint8_t* __restrict__ kept, uint32_t s, uint32_t* __restrict__ bitmap) {
-    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= s) return;
-    if (kept[v]) atomicOr(&bitmap[v >> 5], 1u << (v & 31));
+// Bitmap -> ascending index list (the std::sort of big_means.cpp:54).  Word q
+// covers values 32q..32q+31: bits of values < s come from the exclusion table
+// (kept unless excluded this epoch), bits of values >= s from the target
+// bitmap, which the emit pass clears for the next chunk.
+constexpr int kScanThreads = 256;
+constexpr int kWordsPerThread = 8;
+constexpr int kWordsPerBlock = kScanThreads * kWordsPerThread;
+
+__device__ __forceinline__ uint32_t chunk_word(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
+                                               uint32_t q, uint32_t s, uint32_t ep) {
+    uint32_t w = bitmap[q];
+    const uint32_t v0 = q * 32u;
+    if (v0 < s) {
+        const uint32_t lim = min(32u, s - v0);
+        uint32_t low = 0;
+        for (uint32_t b = 0; b < lim; ++b) low |= (excl[v0 + b] != ep ? 1u : 0u) << b;
+        w |= low;
+    }
+    return w;
+}
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot,
+                                                         uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            const uint32_t x = warp_tot[w];
+            warp_tot[w] = run;
+            run += x;
+        }
+        *total = run;
+    }
+    __syncthreads();
+    return warp_tot[warp] + incl - v;
+}
+
+__global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
+                                      const uint32_t* __restrict__ epoch_slot, uint32_t s, uint32_t nwords,
+                                      uint32_t* __restrict__ block_counts) {
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    __shared__ uint32_t total;
+    const uint32_t ep = *epoch_slot;
+    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q)
+        if (base + q < nwords) c += __popc(chunk_word(bitmap, excl, base + q, s, ep));
+    block_exclusive_scan(c, warp_tot, &total);
+    if (threadIdx.x == 0) block_counts[blockIdx.x] = total;
+}
+
+__global__ void k_bitmap_emit(uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
+                              const uint32_t* __restrict__ epoch_slot, uint32_t s, uint32_t nwords,
+                              const uint32_t* __restrict__ block_counts, uint32_t* __restrict__ out) {
+    __shared__ uint32_t warp_tot[kScanThreads / 32];
+    __shared__ uint32_t total;
+    __shared__ uint32_t block_off;
+    const uint32_t ep = *epoch_slot;
+    if (threadIdx.x < 32) {  // this block's offset: sum of the preceding blocks' counts
+        uint32_t acc = 0;
+        for (uint32_t b = threadIdx.x; b < blockIdx.x; b += 32) acc += block_counts[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+        if (threadIdx.x == 0) block_off = acc;
+    }
+    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
+    uint32_t words[kWordsPerThread];
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        words[q] = base + q < nwords ? chunk_word(bitmap, excl, base + q, s, ep) : 0u;
+        c += __popc(words[q]);
+    }
+    uint32_t pos = block_exclusive_scan(c, warp_tot, &total) + block_off;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        uint32_t w = words[q];
+        if (base + q < nwords && w) bitmap[base + q] = 0u;  // ready for the next chunk
+        while (w) {
+            const int b = __ffs(w) - 1;
+            out[pos++] = (base + q) * 32u + static_cast<uint32_t>(b);
+            w &= w - 1;
+        }
+    }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ out, uint32_t s) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s) out[i] = i;
+}
+
+// Next epoch for host-drawn targets (bm_sample_chunk / bm_sample_chunk_draws).
+__global__ void k_epoch_bump(uint32_t* counter, uint32_t* slot) {
+    if (threadIdx.x == 0) *slot = ++(*counter);
 }
 
 // The s raw targets j_i = uniform_int(i, m-1) (big_means.cpp:49-51) drawn on
@@ -137,7 +260,8 @@ __device__ uint64_t mt_next_seq(uint64_t* x, int& pos) {
 
 __global__ void __launch_bounds__(kMtThreads)
 k_mt_draw(Mt64State* __restrict__ st, uint64_t m, uint32_t s, uint32_t* __restrict__ js,
-          const int* __restrict__ skip, int force_seq) {
+          const int* __restrict__ skip, int force_seq, uint32_t* __restrict__ epoch_counter,
+          uint32_t* __restrict__ epoch_slot) {
     __shared__ uint64_t x[kMtN];
     __shared__ uint64_t x0[kMtN];  // state before the draw (sequential fallback)
     __shared__ int reject;
@@ -198,92 +322,10 @@ k_mt_draw(Mt64State* __restrict__ st, uint64_t m, uint32_t s, uint32_t* __restri
         pos = reject;
     }
     for (int i = tid; i < kMtN; i += blockDim.x) st->x[i] = x[i];
-    if (tid == 0) st->pos = static_cast<uint64_t>(pos);
-}
-
-// Bitmap -> ascending index list (the std::sort of big_means.cpp:54).
-constexpr int kScanThreads = 256;
-constexpr int kWordsPerThread = 8;
-constexpr int kWordsPerBlock = kScanThreads * kWordsPerThread;
-
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot,
-                                                         uint32_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += y;
+    if (tid == 0) {
+        st->pos = static_cast<uint64_t>(pos);
+        *epoch_slot = ++(*epoch_counter);  // tags the resolution tables of these targets
     }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-            const uint32_t x = warp_tot[w];
-            warp_tot[w] = run;
-            run += x;
-        }
-        *total = run;
-    }
-    __syncthreads();
-    return warp_tot[warp] + incl - v;
-}
-
-__global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, uint32_t nwords,
-                                      uint32_t* __restrict__ block_counts) {
-    __shared__ uint32_t warp_tot[kScanThreads / 32];
-    __shared__ uint32_t total;
-    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
-    uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q)
-        if (base + q < nwords) c += __popc(bitmap[base + q]);
-    block_exclusive_scan(c, warp_tot, &total);
-    if (threadIdx.x == 0) block_counts[blockIdx.x] = total;
-}
-
-__global__ void k_scan_block_counts(uint32_t* __restrict__ counts, uint32_t nblocks) {
-    __shared__ uint32_t warp_tot[kScanThreads / 32];
-    __shared__ uint32_t total;
-    uint32_t carry = 0;
-    for (uint32_t b0 = 0; b0 < nblocks; b0 += blockDim.x) {
-        const uint32_t b = b0 + threadIdx.x;
-        const uint32_t v = b < nblocks ? counts[b] : 0;
-        const uint32_t ex = block_exclusive_scan(v, warp_tot, &total);
-        if (b < nblocks) counts[b] = carry + ex;
-        carry += total;
-        __syncthreads();
-    }
-}
-
-__global__ void k_bitmap_emit(const uint32_t* __restrict__ bitmap, uint32_t nwords,
-                              const uint32_t* __restrict__ block_offsets, uint32_t* __restrict__ out) {
-    __shared__ uint32_t warp_tot[kScanThreads / 32];
-    __shared__ uint32_t total;
-    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
-    uint32_t words[kWordsPerThread];
-    uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        words[q] = base + q < nwords ? bitmap[base + q] : 0u;
-        c += __popc(words[q]);
-    }
-    uint32_t pos = block_offsets[blockIdx.x] + block_exclusive_scan(c, warp_tot, &total);
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        uint32_t w = words[q];
-        while (w) {
-            const int b = __ffs(w) - 1;
-            out[pos++] = (base + q) * 32u + static_cast<uint32_t>(b);
-            w &= w - 1;
-        }
-    }
-}
-
-__global__ void k_iota(uint32_t* __restrict__ out, uint32_t s) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < s) out[i] = i;
 }
 
 // ===========================================================================
