@@ -144,17 +144,26 @@ constexpr int kScanThreads = 256;
 constexpr int kWordsPerThread = 8;
 constexpr int kWordsPerBlock = kScanThreads * kWordsPerThread;
 
-__device__ __forceinline__ uint32_t chunk_word(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
-                                               uint32_t q, uint32_t s, uint32_t ep) {
-    uint32_t w = bitmap[q];
-    const uint32_t v0 = q * 32u;
-    if (v0 < s) {
-        const uint32_t lim = min(32u, s - v0);
-        uint32_t low = 0;
-        for (uint32_t b = 0; b < lim; ++b) low |= (excl[v0 + b] != ep ? 1u : 0u) << b;
-        w |= low;
+// The 8 words this thread owns (words base..base+7, base = 8 * global thread
+// id): bitmap bits OR'ed with the kept-bits of values < s.  The kept-bits are
+// built warp-cooperatively: one coalesced load of 32 exclusion tags and one
+// ballot per word.
+__device__ __forceinline__ void chunk_words(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
+                                            uint32_t s, uint32_t ep, uint32_t nwords, uint32_t words[kWordsPerThread]) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) * kWordsPerThread;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) words[q] = base + q < nwords ? bitmap[base + q] : 0u;
+    const uint32_t wbase = (blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * kWordsPerThread;  // warp's first word
+    const uint32_t low_words = (s + 31u) / 32u;
+    if (wbase >= low_words) return;  // no value < s in this warp's range
+    for (int i = 0; i < 32 * kWordsPerThread; ++i) {
+        const uint32_t q = wbase + i;
+        if (q >= low_words) break;
+        const uint32_t v = q * 32u + lane;
+        const unsigned bit = __ballot_sync(0xFFFFFFFFu, v < s && excl[v] != ep);
+        if (lane == i / kWordsPerThread) words[i % kWordsPerThread] |= bit;
     }
-    return w;
 }
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot,
@@ -187,11 +196,11 @@ __global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, const
     __shared__ uint32_t warp_tot[kScanThreads / 32];
     __shared__ uint32_t total;
     const uint32_t ep = *epoch_slot;
-    const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
+    uint32_t words[kWordsPerThread];
+    chunk_words(bitmap, excl, s, ep, nwords, words);
     uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q)
-        if (base + q < nwords) c += __popc(chunk_word(bitmap, excl, base + q, s, ep));
+    for (int q = 0; q < kWordsPerThread; ++q) c += __popc(words[q]);
     block_exclusive_scan(c, warp_tot, &total);
     if (threadIdx.x == 0) block_counts[blockIdx.x] = total;
 }
@@ -212,12 +221,10 @@ __global__ void k_bitmap_emit(uint32_t* __restrict__ bitmap, const uint32_t* __r
     }
     const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
     uint32_t words[kWordsPerThread];
+    chunk_words(bitmap, excl, s, ep, nwords, words);
     uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) {
-        words[q] = base + q < nwords ? chunk_word(bitmap, excl, base + q, s, ep) : 0u;
-        c += __popc(words[q]);
-    }
+    for (int q = 0; q < kWordsPerThread; ++q) c += __popc(words[q]);
     uint32_t pos = block_exclusive_scan(c, warp_tot, &total) + block_off;
 #pragma unroll
     for (int q = 0; q < kWordsPerThread; ++q) {
