@@ -1092,7 +1092,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             unsigned bits = 0;
 #pragma unroll
             for (int u = 0; u < kAK; ++u)
-                if (Lk[q][u] <= m) bits |= 1u << (kAK * warp + u);
+                if (kAK * warp + u < KA && Lk[q][u] <= m) bits |= 1u << (kAK * warp + u);
             if (bits && p < np) atomicOr(&S.cand[p], bits);
         }
     }
