@@ -235,7 +235,7 @@ struct SamplerWs {
     uint32_t nwords = 0, nblocks = 0;
     DevBuf<uint32_t> js, js2, bitmap, blockcnt, idx;  // js2: second target buffer (pipelined draws)
     DevBuf<unsigned long long> hkeys, hvals, LT;      // epoch-tagged resolution tables
-    DevBuf<uint32_t> excl;                            // epoch of exclusion per value < s
+    DevBuf<uint32_t> exclbits;                        // values < s leaving the first s positions
     DevBuf<uint32_t> epoch;                           // [0] counter, [1+b] epoch of target buffer b
     cudaStream_t rng_stream = nullptr;                      // device draws of the next chunk
     cudaEvent_t drawn[2] = {nullptr, nullptr}, resolved[2] = {nullptr, nullptr};
@@ -263,10 +263,10 @@ struct SamplerWs {
         blockcnt.alloc(std::max<uint32_t>(nblocks, 1));
         idx.alloc(s);
         LT.alloc(s);
-        excl.alloc(s);
+        exclbits.alloc(ceil_div(s, 32));
         epoch.alloc(3);
         BM_CUDA(cudaMemset(LT.p, 0, s * sizeof(unsigned long long)));
-        BM_CUDA(cudaMemset(excl.p, 0, s * sizeof(uint32_t)));
+        BM_CUDA(cudaMemset(exclbits.p, 0, ceil_div(s, 32) * sizeof(uint32_t)));
         BM_CUDA(cudaMemset(epoch.p, 0, 3 * sizeof(uint32_t)));
         BM_CUDA(cudaMemset(bitmap.p, 0, nwords * sizeof(uint32_t)));
         mt.alloc(1);
@@ -880,11 +880,11 @@ void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw, int b = 0) {
     const uint32_t* ep = sw.epoch_slot(b);
     const unsigned g = (unsigned)ceil_div(s, 256);
     dev::k_fy_pass1<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
-    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.excl.p,
+    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.exclbits.p,
                                        sw.bitmap.p);
-    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.excl.p, ep, s,
+    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.exclbits.p, s,
                                                                          sw.nwords, sw.blockcnt.p);
-    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.excl.p, ep, s, sw.nwords,
+    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.exclbits.p, s, sw.nwords,
                                                                  sw.blockcnt.p, sw.idx.p);
     BM_LAUNCH();
     count_launch(4);

@@ -116,7 +116,7 @@ __global__ void k_fy_pass1(const uint32_t* __restrict__ js, const uint32_t* __re
 __global__ void k_fy_pass2(const uint32_t* __restrict__ js, const uint32_t* __restrict__ epoch_slot, uint32_t s,
                            const unsigned long long* __restrict__ LT, const unsigned long long* __restrict__ hkeys,
                            const unsigned long long* __restrict__ hvals, uint32_t hmask,
-                           uint32_t* __restrict__ excl, uint32_t* __restrict__ bitmap) {
+                           uint32_t* __restrict__ exclbits, uint32_t* __restrict__ bitmap) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= s) return;
     const uint32_t ep = *epoch_slot;
@@ -133,7 +133,7 @@ __global__ void k_fy_pass2(const uint32_t* __restrict__ js, const uint32_t* __re
         if ((v >> 32) != ep) break;
         w = static_cast<uint32_t>(v);
     }
-    excl[w] = ep;
+    atomicOr(&exclbits[w >> 5], 1u << (w & 31));
 }
 
 // Bitmap -> ascending index list (the std::sort of big_means.cpp:54).  Word q
@@ -145,24 +145,22 @@ constexpr int kWordsPerThread = 8;
 constexpr int kWordsPerBlock = kScanThreads * kWordsPerThread;
 
 // The 8 words this thread owns (words base..base+7, base = 8 * global thread
-// id): bitmap bits OR'ed with the kept-bits of values < s.  The kept-bits are
-// built warp-cooperatively: one coalesced load of 32 exclusion tags and one
-// ballot per word.
-__device__ __forceinline__ void chunk_words(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
-                                            uint32_t s, uint32_t ep, uint32_t nwords, uint32_t words[kWordsPerThread]) {
-    const int lane = threadIdx.x & 31;
+// id): target bits (values >= s) OR'ed with the kept bits of values < s (not
+// excluded this chunk).  Both bitmaps are cleared by the emit pass.
+__device__ __forceinline__ void chunk_words(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ exclbits,
+                                            uint32_t s, uint32_t nwords, uint32_t words[kWordsPerThread]) {
     const uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) * kWordsPerThread;
-#pragma unroll
-    for (int q = 0; q < kWordsPerThread; ++q) words[q] = base + q < nwords ? bitmap[base + q] : 0u;
-    const uint32_t wbase = (blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * kWordsPerThread;  // warp's first word
     const uint32_t low_words = (s + 31u) / 32u;
-    if (wbase >= low_words) return;  // no value < s in this warp's range
-    for (int i = 0; i < 32 * kWordsPerThread; ++i) {
-        const uint32_t q = wbase + i;
-        if (q >= low_words) break;
-        const uint32_t v = q * 32u + lane;
-        const unsigned bit = __ballot_sync(0xFFFFFFFFu, v < s && excl[v] != ep);
-        if (lane == i / kWordsPerThread) words[i % kWordsPerThread] |= bit;
+#pragma unroll
+    for (int q = 0; q < kWordsPerThread; ++q) {
+        const uint32_t w = base + q;
+        uint32_t v = w < nwords ? bitmap[w] : 0u;
+        if (w < low_words) {
+            const uint32_t lim = s - w * 32u;
+            const uint32_t lowmask = lim >= 32u ? 0xFFFFFFFFu : ((1u << lim) - 1u);
+            v |= ~exclbits[w] & lowmask;
+        }
+        words[q] = v;
     }
 }
 
@@ -190,14 +188,12 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
     return warp_tot[warp] + incl - v;
 }
 
-__global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
-                                      const uint32_t* __restrict__ epoch_slot, uint32_t s, uint32_t nwords,
-                                      uint32_t* __restrict__ block_counts) {
+__global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ exclbits,
+                                      uint32_t s, uint32_t nwords, uint32_t* __restrict__ block_counts) {
     __shared__ uint32_t warp_tot[kScanThreads / 32];
     __shared__ uint32_t total;
-    const uint32_t ep = *epoch_slot;
     uint32_t words[kWordsPerThread];
-    chunk_words(bitmap, excl, s, ep, nwords, words);
+    chunk_words(bitmap, exclbits, s, nwords, words);
     uint32_t c = 0;
 #pragma unroll
     for (int q = 0; q < kWordsPerThread; ++q) c += __popc(words[q]);
@@ -205,13 +201,11 @@ __global__ void k_bitmap_block_counts(const uint32_t* __restrict__ bitmap, const
     if (threadIdx.x == 0) block_counts[blockIdx.x] = total;
 }
 
-__global__ void k_bitmap_emit(uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ excl,
-                              const uint32_t* __restrict__ epoch_slot, uint32_t s, uint32_t nwords,
-                              const uint32_t* __restrict__ block_counts, uint32_t* __restrict__ out) {
+__global__ void k_bitmap_emit(uint32_t* __restrict__ bitmap, uint32_t* __restrict__ exclbits, uint32_t s,
+                              uint32_t nwords, const uint32_t* __restrict__ block_counts, uint32_t* __restrict__ out) {
     __shared__ uint32_t warp_tot[kScanThreads / 32];
     __shared__ uint32_t total;
     __shared__ uint32_t block_off;
-    const uint32_t ep = *epoch_slot;
     if (threadIdx.x < 32) {  // this block's offset: sum of the preceding blocks' counts
         uint32_t acc = 0;
         for (uint32_t b = threadIdx.x; b < blockIdx.x; b += 32) acc += block_counts[b];
@@ -221,7 +215,7 @@ __global__ void k_bitmap_emit(uint32_t* __restrict__ bitmap, const uint32_t* __r
     }
     const uint32_t base = blockIdx.x * kWordsPerBlock + threadIdx.x * kWordsPerThread;
     uint32_t words[kWordsPerThread];
-    chunk_words(bitmap, excl, s, ep, nwords, words);
+    chunk_words(bitmap, exclbits, s, nwords, words);
     uint32_t c = 0;
 #pragma unroll
     for (int q = 0; q < kWordsPerThread; ++q) c += __popc(words[q]);
@@ -229,7 +223,8 @@ __global__ void k_bitmap_emit(uint32_t* __restrict__ bitmap, const uint32_t* __r
 #pragma unroll
     for (int q = 0; q < kWordsPerThread; ++q) {
         uint32_t w = words[q];
-        if (base + q < nwords && w) bitmap[base + q] = 0u;  // ready for the next chunk
+        if (base + q < nwords && bitmap[base + q]) bitmap[base + q] = 0u;  // ready for the next chunk
+        if (base + q < (s + 31u) / 32u && exclbits[base + q]) exclbits[base + q] = 0u;
         while (w) {
             const int b = __ffs(w) - 1;
             out[pos++] = (base + q) * 32u + static_cast<uint32_t>(b);
