@@ -132,6 +132,7 @@ struct Workspace {
     DevBuf<double> dists;    // R
     DevBuf<double> tile_buf; // max(ncand,1) * tiles
     DevBuf<unsigned> tile_ctr;  // tiles (fused tile-fold arrival counters)
+    DevBuf<unsigned> tiles_done;  // tiles completed in the current assignment launch (fused control)
     DevBuf<double> psum;     // tiles * k * n
     DevBuf<uint32_t> pcnt;   // tiles * k
     DevBuf<double> C, Cact;  // k * n
@@ -200,6 +201,8 @@ struct Workspace {
         tile_buf.alloc(tiles * ncand);
         tile_ctr.alloc(tiles);
         if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
+        tiles_done.alloc(1);
+        BM_CUDA(cudaMemset(tiles_done.p, 0, sizeof(unsigned)));
         psum.alloc(tiles * (uint64_t)k * n);
         pcnt.alloc(tiles * (uint64_t)k);
         C.alloc((uint64_t)k * n);
@@ -535,7 +538,9 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
 void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_t* labels_pair,
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
                    const int* stop, bool final_pass = false, double* tile_out = nullptr,
-                   unsigned* tile_ctr = nullptr) {
+                   unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr) {
+    const dev::LloydCtl noctl{};
+    bool fused_ctl = false;
     const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
     if (grid == 0) return;
     PhaseScope ps(final_pass ? PH_FINAL : PH_ASSIGN, P.rows);
@@ -551,10 +556,11 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                 attr_set = true;
             }
             const CUtensorMap tmx = points_map<T>(P);
+            fused_ctl = ctl && tile_out;
             dev::k_assign_tma<T><<<grid, dev::kSThreads, shm, st>>>(
                 tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
-                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
+                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl);
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
             static bool attr_set = false;  // per template instance
@@ -576,6 +582,15 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     BM_LAUNCH();
     count_launch();
     if (tile_out && !screen) launch_tile_sums(st, dists, P.rows, 0, 1, tile_out, stop);
+    if (ctl && ctl->mode && !fused_ctl) {  // control as its own kernel
+        if (ctl->mode == 1)
+            dev::k_lloyd_begin<<<1, 32, 0, st>>>(ctl->st, tile_out, ctl->ntiles, P.rows, ctl->history);
+        else
+            dev::k_lloyd_step<<<1, 32, 0, st>>>(ctl->st, tile_out, ctl->ntiles, P.rows, ctl->max_iterations,
+                                                ctl->rel_tolerance, ctl->history, ctl->cond, ctl->use_cond);
+        BM_LAUNCH();
+        count_launch();
+    }
 }
 
 void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t stride, int narrays,
@@ -614,8 +629,8 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
             w.pcnt.p, &w.status.p->bad_label, stop);
     });
     BM_LAUNCH();
-    dim3 mgrid((unsigned)k, (unsigned)ceil_div(n, dev::kMThreads));
-    const size_t mshm = k * sizeof(unsigned long long) + tiles * sizeof(int);
+    const unsigned mgrid = (unsigned)ceil_div((uint64_t)k * n, dev::kMThreads);
+    const size_t mshm = k * (sizeof(unsigned long long) + sizeof(int));
     if (mshm > 48 * 1024)
         BM_CUDA(cudaFuncSetAttribute(dev::k_update_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mshm));
     dev::k_update_merge<<<mgrid, dev::kMThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p, w.mask.p,
@@ -637,28 +652,39 @@ struct LloydResult {
     int parity;
 };
 
-void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w) {
-    launch_compact(st, w, w.C.p, w.mask.p);
-    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr, false,
-                  w.tile_buf.p, w.tile_ctr.p);  // :26-27
-    dev::k_lloyd_begin<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows,
-                                         w.hist_cap ? w.history.p : nullptr);
-    BM_LAUNCH();
-    count_launch();
+dev::LloydCtl make_ctl(Workspace& w, int mode, uint64_t rows, uint64_t max_it = 0, double tol = 0.0,
+                       cudaGraphConditionalHandle cond = 0, int use_cond = 0) {
+    dev::LloydCtl c{};
+    c.mode = mode;
+    c.st = w.status.p;
+    c.tiles_done = w.tiles_done.p;
+    c.ntiles = tiles_of(rows);
+    c.max_iterations = max_it;
+    c.rel_tolerance = tol;
+    c.history = w.hist_cap ? w.history.p : nullptr;
+    c.cond = cond;
+    c.use_cond = use_cond;
+    return c;
 }
 
+// compact (unless the compacted start is already in place) + assign (:26) +
+// begin (:27-28), the latter fused into the assignment where possible.
+void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do_compact = true) {
+    if (do_compact) launch_compact(st, w, w.C.p, w.mask.p);
+    const dev::LloydCtl ctl = make_ctl(w, 1, P.rows);
+    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr, false,
+                  w.tile_buf.p, w.tile_ctr.p, &ctl);
+}
+
+// update (:33) + assign (:34-35) + step (:36-51), the step fused into the assignment.
 void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol,
                          cudaGraphConditionalHandle cond = 0, int use_cond = 0) {
     const int* parity = &w.status.p->parity;
     const int* stop = &w.status.p->stop;
-    launch_update(st, P, w, parity, stop);                                                 // :33
+    launch_update(st, P, w, parity, stop);
+    const dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond);
     launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop, false,
-                  w.tile_buf.p, w.tile_ctr.p);  // :34-35
-    PhaseScope ps(PH_CONTROL, 0);
-    dev::k_lloyd_step<<<1, 32, 0, st>>>(w.status.p, w.tile_buf.p, tiles_of(P.rows), P.rows, max_it,
-                                        tol, w.hist_cap ? w.history.p : nullptr, cond, use_cond);
-    BM_LAUNCH();
-    count_launch();
+                  w.tile_buf.p, w.tile_ctr.p, &ctl);
 }
 
 // Runs the loop to completion; `between` is called once after the first
@@ -964,8 +990,9 @@ bool graphs_enabled() {
 
 void enqueue_accept(cudaStream_t st, Workspace& w) {
     PhaseScope ps(PH_CONTROL, 0);
-    dev::k_accept<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p, w.maskinc.p, w.k, w.n,
-                                     w.drec.p, w.chunk_ctr.p);
+    dev::k_accept<<<1, 256, w.k * sizeof(int), st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p,
+                                                     w.maskinc.p, w.k, w.n, w.drec.p, w.chunk_ctr.p, w.Cact.p,
+                                                     w.ldc, w.act.p, w.CT32.p);
     BM_LAUNCH();
     count_launch();
 }
@@ -993,7 +1020,7 @@ cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, DeviceCache& 
 cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, uint64_t max_it, double tol) {
     if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    lloyd_enqueue_begin(st, P, w);
+    lloyd_enqueue_begin(st, P, w, /*do_compact=*/false);  // accept (or the repair path) compacted the start
     cudaStreamCaptureStatus cs;
     cudaGraph_t cg = nullptr;
     const cudaGraphNode_t* deps = nullptr;
@@ -1122,6 +1149,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             }
             kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
             if (!identity) put_stream(st, *sw, rng);
+            if (use_graphs) launch_compact(st, w, w.C.p, w.mask.p);  // the graph starts from Cact
         }
         // The next chunk's sample draws follow this chunk's (repair) draws:
         // start them now on rng_stream, overlapping this chunk's Lloyd.  Its

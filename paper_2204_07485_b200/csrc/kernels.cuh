@@ -344,6 +344,97 @@ __global__ void k_gather(const uint4* __restrict__ X, uint64_t row_vecs, const u
     for (uint64_t v = lane; v < row_vecs; v += 32) dst[v] = __ldg(src + v);
 }
 
+// Ordered fold of tile partials (block_sum outer loop core.cpp:172).
+__device__ __forceinline__ double fold_tiles(const double* tiles, uint64_t ntiles) {
+    double total = 0.0;
+    for (uint64_t t = 0; t < ntiles; ++t) total = __dadd_rn(total, __ldcg(tiles + t));  // written by other CTAs
+    return total;
+}
+
+// ===========================================================================
+// 6. Lloyd control (local_search.cpp:26-54), single thread.  Either its own
+// kernel or run by the CTA that completes an assignment's last tile.
+// ===========================================================================
+__device__ void lloyd_begin_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+                                 double* history) {
+    const double f = fold_tiles(tiles, ntiles);  // :27
+    if (history) history[0] = f;                 // :28
+    st->f = f;
+    st->objective = f;
+    st->evals = static_cast<unsigned long long>(rows) * st->n_active;  // :26 counter
+    st->iterations = 0;
+    st->parity = 0;
+    st->stop = 0;
+    st->changed = 0;
+    st->state_error = st->n_active == 0;
+    st->bad_label = 0;
+}
+
+__device__ void lloyd_step_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+                                unsigned long long max_iterations, double rel_tolerance, double* history,
+                                cudaGraphConditionalHandle cond, int use_cond) {
+    if (!st->stop) {
+        const double f_new = fold_tiles(tiles, ntiles);  // :35
+        st->evals += static_cast<unsigned long long>(rows) * st->n_active;
+        if (st->n_active == 0) st->state_error = 1;
+        st->iterations += 1;            // :36
+        st->objective = f_new;          // history.push_back (:37)
+        if (history) history[st->iterations] = f_new;
+        const bool unchanged = __ldcg(&st->changed) == 0;  // :39 (set by other CTAs of this launch)
+        st->changed = 0;
+        st->parity ^= 1;                // :40-41 advance
+        const double f = st->f;
+        bool stop = unchanged;                                                      // :42-44
+        if (!stop && f <= 0.0) stop = true;                                         // :45-47
+        if (!stop && rel_tolerance > 0.0 && __ddiv_rn(__dsub_rn(f, f_new), f) < rel_tolerance)
+            stop = true;                                                            // :48-50
+        if (!stop) st->f = f_new;                                                   // :51
+        if (st->iterations >= max_iterations) stop = true;                          // :32
+        if (st->state_error || st->bad_label) stop = true;
+        st->stop = stop ? 1 : 0;
+    }
+    if (use_cond) cudaGraphSetConditional(cond, st->stop ? 0u : 1u);  // graph WHILE node
+}
+
+__global__ void k_lloyd_begin(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+                              double* history) {
+    if (threadIdx.x == 0) lloyd_begin_body(st, tiles, ntiles, rows, history);
+}
+
+__global__ void k_lloyd_step(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+                             unsigned long long max_iterations, double rel_tolerance, double* history,
+                             cudaGraphConditionalHandle cond, int use_cond) {
+    if (threadIdx.x == 0)
+        lloyd_step_body(st, tiles, ntiles, rows, max_iterations, rel_tolerance, history, cond, use_cond);
+}
+
+// Control fused into an assignment launch: mode 1 = begin, 2 = step.
+struct LloydCtl {
+    int mode;
+    LloydStatus* st;
+    unsigned* tiles_done;   // arrival counter over the launch's tiles
+    uint64_t ntiles;
+    unsigned long long max_iterations;
+    double rel_tolerance;
+    double* history;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+};
+
+// Called by thread 0 of the CTA that folded a tile: the CTA completing the last
+// tile runs the Lloyd control over all tile partials.
+__device__ __forceinline__ void tile_done_control(const LloydCtl& c, const double* tiles, uint64_t rows) {
+    if (!c.mode) return;
+    __threadfence();
+    const unsigned done = atomicAdd(c.tiles_done, 1u);
+    if (done != c.ntiles - 1) return;
+    __threadfence();
+    *c.tiles_done = 0u;
+    if (c.mode == 1) lloyd_begin_body(c.st, tiles, c.ntiles, rows, c.history);
+    else lloyd_step_body(c.st, tiles, c.ntiles, rows, c.max_iterations, c.rel_tolerance, c.history, c.cond,
+                         c.use_cond);
+}
+
 // ===========================================================================
 // 3. Exact nearest-centroid assignment (assign_nearest core.cpp:106-161).
 //
@@ -926,7 +1017,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
              int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
-             unsigned long long* __restrict__ cand_counter, ScreenConsts cst) {
+             unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
     unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1243,6 +1334,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
         tile_out[tile] = a;
         tile_counter[tile] = 0u;
+        tile_done_control(ctl, tile_out, rows);
     }
 }
 
@@ -1282,12 +1374,6 @@ __global__ void k_tile_sums(const double* __restrict__ v, uint64_t count, uint64
     tiles[a * ntiles + t] = acc;
 }
 
-// Ordered fold of tile partials (block_sum outer loop core.cpp:172).
-__device__ __forceinline__ double fold_tiles(const double* tiles, uint64_t ntiles) {
-    double total = 0.0;
-    for (uint64_t t = 0; t < ntiles; ++t) total = __dadd_rn(total, tiles[t]);
-    return total;
-}
 
 // ===========================================================================
 // 5. Centroid update (update_centroids core.cpp:183-244), bit-exact order.
@@ -1404,11 +1490,11 @@ k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     }
 }
 
-// Phase B: grid (label j, 128-dim block).  Each CTA recomputes the label
-// totals and active ranks (integers: order-free), then one thread per dim
-// folds the non-empty tile partials of label j in tile order (:217-229),
-// loads issued in batches ahead of the adds, and applies sum * (1.0/count)
-// (:237-239); count 0 -> degenerate row of 0.0 (:231).
+// Phase B: one thread per (label j, dim d).  Every CTA recomputes the label
+// totals and active ranks (integers: order-free), then folds the tile
+// partials of label j in tile order (:217-229) with the loads issued in
+// batches ahead of the adds (empty tiles contribute +0.0 and are skipped),
+// and applies sum * (1.0/count) (:237-239); count 0 -> degenerate row of 0.0.
 constexpr int kMThreads = 128;
 
 __global__ void __launch_bounds__(kMThreads)
@@ -1418,12 +1504,9 @@ k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcn
                float* __restrict__ CT32, const int* __restrict__ stop_ptr) {
     if (stop_ptr && *stop_ptr) return;
     extern __shared__ unsigned long long msh[];
-    unsigned long long* total = msh;                         // [k]
-    int* tl = reinterpret_cast<int*>(total + k);             // nonempty tiles of label j
-    __shared__ int ntl, rankj;
-    const int j = blockIdx.x;
+    unsigned long long* total = msh;                  // [k]
+    int* rank = reinterpret_cast<int*>(total + k);    // [k]
     for (int jj = threadIdx.x; jj < k; jj += blockDim.x) total[jj] = 0;
-    if (threadIdx.x == 0) ntl = 0;
     __syncthreads();
     for (uint64_t e = threadIdx.x; e < ntiles * k; e += blockDim.x) {
         const uint32_t c = pcnt[e];
@@ -1432,59 +1515,46 @@ k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcn
     __syncthreads();
     if (threadIdx.x == 0) {
         int r = 0;
-        for (int jj = 0; jj < j; ++jj) r += total[jj] != 0;
-        rankj = r;
-        if (blockIdx.y == 0) {
-            mask[j] = total[j] ? 0 : 1;
-            if (total[j]) act_idx[r] = j;
-            if (j == k - 1) *n_active = r + (total[j] != 0);
-        }
-    }
-    // nonempty tiles of j in ascending order (ballot compaction, 128 per round)
-    __shared__ int wbase[kMThreads / 32];
-    for (uint64_t t0 = 0; t0 < ntiles; t0 += kMThreads) {
-        const uint64_t t = t0 + threadIdx.x;
-        const bool f = t < ntiles && pcnt[t * k + j] != 0;
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, f);
-        const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
-        if (ln == 0) wbase[wid] = __popc(bal);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int r = ntl;
-            for (int w = 0; w < kMThreads / 32; ++w) {
-                const int c = wbase[w];
-                wbase[w] = r;
-                r += c;
+        for (int jj = 0; jj < k; ++jj) {
+            rank[jj] = total[jj] ? r : -1;
+            if (blockIdx.x == 0) {
+                mask[jj] = total[jj] ? 0 : 1;
+                if (total[jj]) act_idx[r] = jj;
             }
-            ntl = r;
+            r += total[jj] != 0;
         }
-        __syncthreads();
-        if (f) tl[wbase[wid] + __popc(bal & ((1u << ln) - 1u))] = static_cast<int>(t);
-        __syncthreads();
+        if (blockIdx.x == 0) *n_active = r;
     }
-    const int d = blockIdx.y * kMThreads + threadIdx.x;
-    if (d >= n) return;
-    const uint64_t e = static_cast<uint64_t>(j) * n + d;
+    __syncthreads();
+    const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<uint64_t>(k) * n) return;
+    const int j = static_cast<int>(e / n), d = static_cast<int>(e % n);
     if (total[j] == 0) {
         C[e] = 0.0;
         return;
     }
-    const int cnt = ntl;
     double acc = 0.0;
-    int q = 0;
-    for (; q + 8 <= cnt; q += 8) {
+    uint64_t t = 0;
+    for (; t + 8 <= ntiles; t += 8) {
         double v[8];
+        uint32_t c[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) v[r] = psum[(static_cast<uint64_t>(tl[q + r]) * k + j) * n + d];
+        for (int r = 0; r < 8; ++r) {
+            c[r] = pcnt[(t + r) * k + j];
+            v[r] = psum[((t + r) * k + j) * n + d];
+        }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) acc = __dadd_rn(acc, v[r]);
+        for (int r = 0; r < 8; ++r)
+            if (c[r]) acc = __dadd_rn(acc, v[r]);
     }
-    for (; q < cnt; ++q) acc = __dadd_rn(acc, psum[(static_cast<uint64_t>(tl[q]) * k + j) * n + d]);
+    for (; t < ntiles; ++t)
+        if (pcnt[t * k + j]) acc = __dadd_rn(acc, psum[(t * k + j) * n + d]);
     const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
     const double v = __dmul_rn(acc, inv);
     C[e] = v;
-    Cact[static_cast<uint64_t>(rankj) * ldc + d] = v;
-    if (CT32 && rankj < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rankj] = __double2float_rn(v);
+    const int rk = rank[j];
+    Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
+    if (CT32 && rk < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
 }
 
 // Compact the active rows of (C, mask) for the assignment (single CTA).
@@ -1511,61 +1581,19 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
 }
 
 // ===========================================================================
-// 6. Lloyd control (local_search.cpp:26-54), single thread.
-// ===========================================================================
-__global__ void k_lloyd_begin(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
-                              double* history) {
-    if (threadIdx.x != 0) return;
-    const double f = fold_tiles(tiles, ntiles);  // :27
-    if (history) history[0] = f;                 // :28
-    st->f = f;
-    st->objective = f;
-    st->evals = static_cast<unsigned long long>(rows) * st->n_active;  // :26 counter
-    st->iterations = 0;
-    st->parity = 0;
-    st->stop = 0;
-    st->changed = 0;
-    st->state_error = st->n_active == 0;
-    st->bad_label = 0;
-}
-
-__global__ void k_lloyd_step(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
-                             unsigned long long max_iterations, double rel_tolerance, double* history,
-                             cudaGraphConditionalHandle cond, int use_cond) {
-    if (threadIdx.x != 0) return;
-    if (!st->stop) {
-        const double f_new = fold_tiles(tiles, ntiles);  // :35
-        st->evals += static_cast<unsigned long long>(rows) * st->n_active;
-        if (st->n_active == 0) st->state_error = 1;
-        st->iterations += 1;            // :36
-        st->objective = f_new;          // history.push_back (:37)
-        if (history) history[st->iterations] = f_new;
-        const bool unchanged = st->changed == 0;  // :39
-        st->changed = 0;
-        st->parity ^= 1;                // :40-41 advance
-        const double f = st->f;
-        bool stop = unchanged;                                                      // :42-44
-        if (!stop && f <= 0.0) stop = true;                                         // :45-47
-        if (!stop && rel_tolerance > 0.0 && __ddiv_rn(__dsub_rn(f, f_new), f) < rel_tolerance)
-            stop = true;                                                            // :48-50
-        if (!stop) st->f = f_new;                                                   // :51
-        if (st->iterations >= max_iterations) stop = true;                          // :32
-        if (st->state_error || st->bad_label) stop = true;
-        st->stop = stop ? 1 : 0;
-    }
-    if (use_cond) cudaGraphSetConditional(cond, st->stop ? 0u : 1u);  // graph WHILE node
-}
-
-// ===========================================================================
 // 7. Accept (big_means.cpp:89-94) on the device.
 // ===========================================================================
 // rec_base[*chunk_ctr] receives the record; the chunk counter and the
 // incumbent's degenerate count (the next chunk's `repaired`, :83) live on the
-// device so the chunk can run inside a CUDA graph.
+// device so the chunk can run inside a CUDA graph.  The incumbent is also
+// written in compacted form (Cact/act/n_active/CT32): it is the next chunk's
+// start (:82) when no repair is needed.
 __global__ void k_accept(LloydStatus* st, double* f_opt, const double* __restrict__ C,
                          const uint8_t* __restrict__ mask, double* __restrict__ Cinc,
                          uint8_t* __restrict__ maskinc, int k, int n, Record* rec_base,
-                         unsigned long long* chunk_ctr) {
+                         unsigned long long* chunk_ctr, double* __restrict__ Cact, int ldc,
+                         int* __restrict__ act_idx, float* __restrict__ CT32) {
+    extern __shared__ int arank[];  // [k]
     __shared__ int accepted;
     if (threadIdx.x == 0) {
         const unsigned long long chunk = *chunk_ctr;
@@ -1585,10 +1613,23 @@ __global__ void k_accept(LloydStatus* st, double* f_opt, const double* __restric
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        int dcount = 0;
-        for (int j = 0; j < k; ++j) dcount += maskinc[j] ? 1 : 0;
+        int dcount = 0, r = 0;
+        for (int j = 0; j < k; ++j) {
+            dcount += maskinc[j] ? 1 : 0;
+            arank[j] = maskinc[j] ? -1 : r;
+            if (!maskinc[j]) act_idx[r++] = j;
+        }
         st->inc_degenerate = dcount;
+        st->n_active = r;
         *chunk_ctr += 1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+        const int j = e / n, d = e % n, rk = arank[j];
+        if (rk < 0) continue;
+        const double v = Cinc[e];
+        Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
+        if (CT32 && rk < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
     }
 }
 
