@@ -155,6 +155,7 @@ struct Workspace {
     cudaGraphExec_t g_prep[2] = {nullptr, nullptr};
     cudaGraphExec_t g_lloyd = nullptr;
     cudaStream_t cap2 = nullptr;  // capture stream of the WHILE body
+    cudaEvent_t ev_lloyd = nullptr;  // end of a chunk's Lloyd graph
     void drop_graphs() {
         for (auto& e : g_prep)
             if (e) {
@@ -168,6 +169,7 @@ struct Workspace {
     ~Workspace() {
         drop_graphs();
         if (cap2) cudaStreamDestroy(cap2);
+        if (ev_lloyd) cudaEventDestroy(ev_lloyd);
     }
     // pinned host mirrors
     HostBuf<dev::LloydStatus> h_status;
@@ -280,7 +282,11 @@ struct SamplerWs {
             if (!drawn[b]) BM_CUDA(cudaEventCreateWithFlags(&drawn[b], cudaEventDisableTiming));
             if (!resolved[b]) BM_CUDA(cudaEventCreateWithFlags(&resolved[b], cudaEventDisableTiming));
         }
-        if (!rng_stream) BM_CUDA(cudaStreamCreateWithFlags(&rng_stream, cudaStreamNonBlocking));
+        if (!rng_stream) {  // highest priority: its single CTA must not wait behind full-GPU Lloyd kernels
+            int lo = 0, hi = 0;
+            BM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            BM_CUDA(cudaStreamCreateWithPriority(&rng_stream, cudaStreamNonBlocking, hi));
+        }
     }
     uint32_t* jsbuf(int b) { return b ? js2.p : js.p; }
     uint32_t* epoch_slot(int b) { return epoch.p + 1 + b; }
@@ -1102,6 +1108,68 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     std::vector<uint8_t> hmask(k);
 
     const auto t_loop = std::chrono::steady_clock::now();
+    if (use_graphs) {
+        // Graph mode: chunk c+1's prep graph (resolution, gather, start copy) is
+        // queued behind chunk c's Lloyd graph before the host waits, so the GPU
+        // stays busy through the host's per-chunk turnaround.  The draws for
+        // chunk c+1 start as soon as chunk c's repair (if any) has consumed
+        // its draws (big_means.hpp:21-23).
+        if (!w.ev_lloyd) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd, cudaEventDisableTiming));
+        enqueue_device_draw(sw->rng_stream, *sw, 0, 0);
+        BM_CUDA(cudaEventRecord(sw->drawn[0], sw->rng_stream));
+        BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[0], 0));
+        BM_CUDA(cudaGraphLaunch(w.g_prep[0], st));
+        count_launch(6);
+        for (uint64_t chunk = 0;; ++chunk) {
+            if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
+            if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
+                break;  // :74-77
+            if (chunk >= w.drec.n) {  // time-budget runs: grow the record buffer (graphs re-captured)
+                BM_CUDA(cudaStreamSynchronize(st));
+                DevBuf<dev::Record> bigger(w.drec.n * 2);
+                BM_CUDA(cudaMemcpyAsync(bigger.p, w.drec.p, w.drec.n * sizeof(dev::Record),
+                                        cudaMemcpyDeviceToDevice, st));
+                BM_CUDA(cudaStreamSynchronize(st));
+                std::swap(w.drec.p, bigger.p);
+                std::swap(w.drec.n, bigger.n);
+                ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
+            }
+            const int jb = (int)(chunk & 1);
+            if (inc_degenerate > 0) {  // kmeanspp_fill (:84): prep(chunk) has run; its draws are done
+                BM_CUDA(cudaMemcpyAsync(w.h_mask.p, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
+                BM_CUDA(cudaStreamSynchronize(st));
+                std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
+                BM_CUDA(cudaStreamSynchronize(sw->rng_stream));
+                get_stream(st, *sw, rng);
+                kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
+                put_stream(st, *sw, rng);
+                launch_compact(st, w, w.C.p, w.mask.p);  // the Lloyd graph starts from Cact
+            }
+            const bool next_exists = !cfg.has_max_chunks || chunk + 1 < cfg.max_chunks;
+            if (next_exists) {  // draws of chunk+1 (the stream is past this chunk's repair)
+                if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[jb ^ 1], 0));
+                enqueue_device_draw(sw->rng_stream, *sw, 0, jb ^ 1);
+                BM_CUDA(cudaEventRecord(sw->drawn[jb ^ 1], sw->rng_stream));
+            }
+            BM_CUDA(cudaGraphLaunch(w.g_lloyd, st));
+            BM_CUDA(cudaEventRecord(w.ev_lloyd, st));
+            if (next_exists) {
+                BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[jb ^ 1], 0));
+                BM_CUDA(cudaGraphLaunch(w.g_prep[jb ^ 1], st));
+                count_launch(6);
+            }
+            BM_CUDA(cudaEventSynchronize(w.ev_lloyd));
+            const dev::LloydStatus& ls = *w.h_status.p;
+            if (ls.state_error) throw StateError("assign_nearest: every centroid is degenerate");
+            if (ls.bad_label) throw ConfigError("update_centroids: label out of range");
+            evals += ls.evals;  // lloyd accumulate (local_search.cpp:55-58)
+            iterations += ls.iterations;
+            inc_degenerate = ls.inc_degenerate;
+            count_launch(2 + 3 * ls.iterations);
+            out->chunks = chunk + 1;
+        }
+        BM_CUDA(cudaStreamSynchronize(st));
+    } else {  // host-driven chunk loop (profiling, BM_GRAPHS=0, s == m)
     bool drawn_ahead = false;  // next chunk's targets already being drawn on rng_stream
     for (uint64_t chunk = 0;; ++chunk) {
         if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
@@ -1182,6 +1250,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             inc_degenerate = w.h_status.p->inc_degenerate;
         }
         out->chunks = chunk + 1;
+    }
     }
     if (sw) BM_CUDA(cudaStreamSynchronize(sw->rng_stream));  // a speculative draw may be in flight
     const double cpu_init = seconds_since(t_loop);  // :96

@@ -355,7 +355,7 @@ __device__ __forceinline__ double fold_tiles(const double* tiles, uint64_t ntile
 // 6. Lloyd control (local_search.cpp:26-54), single thread.  Either its own
 // kernel or run by the CTA that completes an assignment's last tile.
 // ===========================================================================
-__device__ void lloyd_begin_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+__device__ __noinline__ void lloyd_begin_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
                                  double* history) {
     const double f = fold_tiles(tiles, ntiles);  // :27
     if (history) history[0] = f;                 // :28
@@ -370,7 +370,7 @@ __device__ void lloyd_begin_body(LloydStatus* st, const double* tiles, uint64_t 
     st->bad_label = 0;
 }
 
-__device__ void lloyd_step_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
+__device__ __noinline__ void lloyd_step_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
                                 unsigned long long max_iterations, double rel_tolerance, double* history,
                                 cudaGraphConditionalHandle cond, int use_cond) {
     if (!st->stop) {
