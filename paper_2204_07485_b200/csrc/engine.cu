@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -1115,10 +1116,24 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         // chunk c+1 start as soon as chunk c's repair (if any) has consumed
         // its draws (big_means.hpp:21-23).
         if (!w.ev_lloyd) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd, cudaEventDisableTiming));
+        // BM_TIMELINE=1: in-stream events after every graph (GPU durations incl. gaps)
+        static const bool timeline = std::getenv("BM_TIMELINE") != nullptr;
+        std::vector<cudaEvent_t> tl_ev;
+        std::vector<int> tl_kind;
+        auto tl_mark = [&](int kind) {
+            if (!timeline) return;
+            cudaEvent_t e;
+            BM_CUDA(cudaEventCreate(&e));
+            BM_CUDA(cudaEventRecord(e, st));
+            tl_ev.push_back(e);
+            tl_kind.push_back(kind);
+        };
+        tl_mark(-1);
         enqueue_device_draw(sw->rng_stream, *sw, 0, 0);
         BM_CUDA(cudaEventRecord(sw->drawn[0], sw->rng_stream));
         BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[0], 0));
         BM_CUDA(cudaGraphLaunch(w.g_prep[0], st));
+        tl_mark(0);
         count_launch(6);
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
@@ -1144,6 +1159,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
                 put_stream(st, *sw, rng);
                 launch_compact(st, w, w.C.p, w.mask.p);  // the Lloyd graph starts from Cact
+                tl_mark(2);
             }
             const bool next_exists = !cfg.has_max_chunks || chunk + 1 < cfg.max_chunks;
             if (next_exists) {  // draws of chunk+1 (the stream is past this chunk's repair)
@@ -1153,9 +1169,11 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             }
             BM_CUDA(cudaGraphLaunch(w.g_lloyd, st));
             BM_CUDA(cudaEventRecord(w.ev_lloyd, st));
+            tl_mark(1);
             if (next_exists) {
                 BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[jb ^ 1], 0));
                 BM_CUDA(cudaGraphLaunch(w.g_prep[jb ^ 1], st));
+                tl_mark(0);
                 count_launch(6);
             }
             BM_CUDA(cudaEventSynchronize(w.ev_lloyd));
@@ -1169,6 +1187,22 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             out->chunks = chunk + 1;
         }
         BM_CUDA(cudaStreamSynchronize(st));
+        if (timeline && tl_ev.size() > 1) {
+            double acc[3] = {0, 0, 0};
+            int cnt[3] = {0, 0, 0};
+            for (size_t i = 1; i < tl_ev.size(); ++i) {
+                float ms = 0;
+                BM_CUDA(cudaEventElapsedTime(&ms, tl_ev[i - 1], tl_ev[i]));
+                acc[tl_kind[i]] += ms;
+                cnt[tl_kind[i]] += 1;
+            }
+            float total = 0;
+            BM_CUDA(cudaEventElapsedTime(&total, tl_ev.front(), tl_ev.back()));
+            std::fprintf(stderr, "[timeline] total %.3f ms | prep %d x %.1f us | lloyd %d x %.1f us | repair %d x %.1f us\n",
+                         total, cnt[0], cnt[0] ? 1e3 * acc[0] / cnt[0] : 0.0, cnt[1], cnt[1] ? 1e3 * acc[1] / cnt[1] : 0.0,
+                         cnt[2], cnt[2] ? 1e3 * acc[2] / cnt[2] : 0.0);
+            for (auto e : tl_ev) cudaEventDestroy(e);
+        }
     } else {  // host-driven chunk loop (profiling, BM_GRAPHS=0, s == m)
     bool drawn_ahead = false;  // next chunk's targets already being drawn on rng_stream
     for (uint64_t chunk = 0;; ++chunk) {
