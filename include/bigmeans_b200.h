@@ -196,6 +196,8 @@ typedef struct bm_profile {
     uint64_t phase_count[8];
 } bm_profile;
 bm_status bm_set_profiling(int enabled);
+/* Debug builds (-DBM_KTRACE): per-CTA phase timestamps of the screened assignment. */
+bm_status bm_debug_ktrace(uint64_t* out, uint64_t count);
 bm_status bm_last_profile(bm_profile* out);
 
 #ifdef __cplusplus

@@ -80,6 +80,7 @@ PROTOS = {
                                C.POINTER(bm_chunk_record), u64]),
     "bm_assign_rows": (C.c_int, [vp, P_dbl, P_u8, u64, u64, u64, P_i32, P_dbl, P_u64]),
     "bm_set_profiling": (C.c_int, [C.c_int]),
+    "bm_debug_ktrace": (C.c_int, [P_u64, u64]),
     "bm_last_profile": (C.c_int, [C.POINTER(bm_profile)]),
 }
 

@@ -1726,6 +1726,19 @@ bm_status bm_big_means(bm_dataset* d, const bm_config* cfg, bm_outcome* out, bm_
     return guarded([&] { big_means(d, *cfg, out, trace, trace_capacity); });
 }
 
+// Debug: per-CTA phase timestamps of the screened assignment (-DBM_KTRACE builds only).
+bm_status bm_debug_ktrace(uint64_t* out, uint64_t count) {
+    return guarded([&] {
+#ifdef BM_KTRACE
+        BM_CUDA(cudaMemcpyFromSymbol(out, dev::g_ktrace, std::min<uint64_t>(count, 1u << 20) * sizeof(uint64_t)));
+#else
+        (void)out;
+        (void)count;
+        throw ConfigError("library built without -DBM_KTRACE");
+#endif
+    });
+}
+
 bm_status bm_set_profiling(int enabled) {
     g_profiling = enabled != 0;
     return BM_OK;

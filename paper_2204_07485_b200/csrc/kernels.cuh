@@ -49,6 +49,20 @@ struct Record {
     unsigned long long degenerate_repaired;
 };
 
+// Optional per-CTA phase timestamps (build with -DBM_KTRACE; tools/ktrace.py).
+#ifdef BM_KTRACE
+__device__ unsigned long long g_ktrace[1 << 20];
+__device__ __forceinline__ void ktrace(int slot) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_ktrace[(blockIdx.x & 2047) * 16 + slot] = t;
+    }
+}
+#else
+__device__ __forceinline__ void ktrace(int) {}
+#endif
+
 // Exact promotion of the storage type (P11).
 __device__ __forceinline__ double to_f64(double v) { return v; }
 __device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v); }
@@ -1042,6 +1056,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     const float finf = __int_as_float(0x7F800000);
     const int nslab = (n + kADC - 1) / kADC;
 
+    ktrace(0);
     if (tid == 0) {
         tma_prefetch_map(&tmx);
         tma_prefetch_map(&tmc);
@@ -1073,6 +1088,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     for (int sl = 0; sl < nslab; ++sl) {
         const int st = sl & 1, dl = min(kADC, n - sl * kADC);
         mbar_wait(&S.bar[st], (sl >> 1) & 1);
+        if (sl < 6) ktrace(1 + sl);
         // raw (swizzled [p][d], storage type) -> fp32 [d][p], once per element
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -1135,6 +1151,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         S.ncr[lane] = __fsqrt_ru(nch);
     }
     __syncthreads();
+    ktrace(7);
     // certified bounds (same algebra as k_assign_screen): upper bounds first,
     // then each warp tests its lower bounds against the point's minimum U and
     // sets candidate bits (no per-(j,p) bound array is kept).
@@ -1217,6 +1234,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     short* item_p = reinterpret_cast<short*>(item_d + kItemCap);
     signed char* item_j = reinterpret_cast<signed char*>(item_p + kItemCap);
     const bool overflow = NI > static_cast<uint32_t>(kItemCap);
+    ktrace(8);
     if (!overflow) {
         if (tid < np) {
             const int p = tid;
@@ -1270,6 +1288,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         }
         __syncthreads();
     }
+    ktrace(9);
     if (tid < np) {
         const int p = tid;
         const uint64_t gp = p0 + p;
@@ -1300,6 +1319,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         if (dists_out) dists_out[gp] = best;
         if (labels_old && labels_old[gp] != label) *changed_flag = 1;
     }
+    ktrace(10);
     if (!tile_out) return;
     __syncthreads();
     const uint64_t tile = p0 / kTile;
@@ -1311,6 +1331,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         S.is_last = old == ctas - 1;
     }
     __syncthreads();
+    ktrace(11);
     if (!S.is_last) return;
     __threadfence();
     const uint64_t tb = tile * kTile;
@@ -1333,6 +1354,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         }
         for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
         tile_out[tile] = a;
+        ktrace(12);
         tile_counter[tile] = 0u;
         tile_done_control(ctl, tile_out, rows);
     }
