@@ -102,6 +102,9 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
                             int device, bm_dataset** out);
 bm_status bm_dataset_destroy(bm_dataset* data);
 bm_status bm_dataset_shape(const bm_dataset* data, uint64_t* m, uint64_t* n);
+/* Device storage type: fp64 input whose every value is exactly representable
+ * in fp32 is stored as fp32 (lossless; results unchanged). */
+bm_status bm_dataset_storage(const bm_dataset* data, bm_dtype* storage);
 /* Dataset::gather core.hpp:30 / core.cpp:34-44: new dataset with the listed
  * rows in the listed order (index >= m -> BM_CONFIG_ERROR). */
 bm_status bm_dataset_gather(const bm_dataset* data, const uint64_t* rows, uint64_t count,

@@ -124,6 +124,13 @@ class Dataset:
     def handle(self):
         return self._h
 
+    @property
+    def storage(self) -> str:
+        """Device storage type ("f64" or "f32"; fp64 input narrows losslessly)."""
+        v = C.c_int()
+        _check(self._lib.bm_dataset_storage(self._h, C.byref(v)))
+        return "f64" if v.value == _capi.BM_F64 else "f32"
+
     def gather(self, rows) -> "Dataset":
         """New dataset holding the listed rows in the listed order (core.cpp:34-44)."""
         idx = np.ascontiguousarray(rows, dtype=np.uint64)

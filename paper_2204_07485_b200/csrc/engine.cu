@@ -518,6 +518,15 @@ CUtensorMap points_map(const Points& P) {
     return m;
 }
 
+// BM_STORAGE=native keeps fp64 datasets in fp64 even when fp32 is lossless.
+bool narrow_storage() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_STORAGE");
+        return !(e && std::string(e) == "native");
+    }();
+    return on;
+}
+
 // BM_SCREEN=v4 selects the LDG-staged screen (A/B checks); default: TMA (v5).
 bool tma_screen() {
     static const bool on = [] {
@@ -1398,28 +1407,52 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
         d->m = m;
         d->n = n;
         d->dtype = dtype;
-        d->ld = padded_ld(n, dtype);
-        const size_t es = dtype_size(dtype);
         BM_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
-        BM_CUDA(cudaMalloc(&d->X, m * d->ld * es));
-        if (d->ld == n) {
-            BM_CUDA(cudaMemcpyAsync(d->X, values, m * n * es, cudaMemcpyHostToDevice, d->stream));
+        DevBuf<int> flags(2);  // [0] non-finite, [1] not exactly representable in fp32
+        BM_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), d->stream));
+        int hf[2] = {0, 0};
+        if (dtype == BM_F64 && narrow_storage()) {
+            // Stage the fp64 values, check them (Dataset ctor scan core.cpp:27-31 +
+            // fp32 round trip), keep fp32 storage when lossless.
+            DevBuf<double> tmp(m * n);
+            BM_CUDA(cudaMemcpyAsync(tmp.p, values, m * n * sizeof(double), cudaMemcpyHostToDevice, d->stream));
+            dev::k_check_narrow<<<1184, 256, 0, d->stream>>>(tmp.p, m * n, flags.p, flags.p + 1);
+            BM_LAUNCH();
+            BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, d->stream));
+            BM_CUDA(cudaStreamSynchronize(d->stream));
+            if (hf[0]) throw ConfigError("dataset contains a non-finite value");
+            d->dtype = hf[1] ? BM_F64 : BM_F32;
+            d->ld = padded_ld(n, d->dtype);
+            BM_CUDA(cudaMalloc(&d->X, m * d->ld * dtype_size(d->dtype)));
+            if (d->dtype == BM_F32) {
+                dev::k_narrow<<<1184, 256, 0, d->stream>>>(tmp.p, m, (int)n, static_cast<float*>(d->X), d->ld);
+                BM_LAUNCH();
+            } else {
+                BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * sizeof(double), tmp.p, n * sizeof(double), n * sizeof(double),
+                                          m, cudaMemcpyDeviceToDevice, d->stream));
+            }
+            BM_CUDA(cudaStreamSynchronize(d->stream));
         } else {
-            BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * es, values, n * es, n * es, m, cudaMemcpyHostToDevice,
-                                      d->stream));
+            d->ld = padded_ld(n, dtype);
+            const size_t es = dtype_size(dtype);
+            BM_CUDA(cudaMalloc(&d->X, m * d->ld * es));
+            if (d->ld == n) {
+                BM_CUDA(cudaMemcpyAsync(d->X, values, m * n * es, cudaMemcpyHostToDevice, d->stream));
+            } else {
+                BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * es, values, n * es, n * es, m, cudaMemcpyHostToDevice,
+                                          d->stream));
+            }
+            // Dataset ctor finiteness scan (core.cpp:27-31)
+            dispatch(dtype, [&](auto tag) {
+                using T = decltype(tag);
+                dev::k_check_finite<T><<<1184, 256, 0, d->stream>>>(static_cast<const T*>(d->X), m, (int)n, d->ld,
+                                                                    flags.p);
+            });
+            BM_LAUNCH();
+            BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+            BM_CUDA(cudaStreamSynchronize(d->stream));
+            if (hf[0]) throw ConfigError("dataset contains a non-finite value");
         }
-        // Dataset ctor finiteness scan (core.cpp:27-31)
-        DevBuf<int> bad(1);
-        BM_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), d->stream));
-        dispatch(dtype, [&](auto tag) {
-            using T = decltype(tag);
-            dev::k_check_finite<T><<<1184, 256, 0, d->stream>>>(static_cast<const T*>(d->X), m, (int)n, d->ld, bad.p);
-        });
-        BM_LAUNCH();
-        int hbad = 0;
-        BM_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
-        BM_CUDA(cudaStreamSynchronize(d->stream));
-        if (hbad) throw ConfigError("dataset contains a non-finite value");
         *out = d.release();
     });
 }
@@ -1430,6 +1463,10 @@ bm_status bm_dataset_destroy(bm_dataset* d) {
         DeviceGuard g(d->device);
         delete d;
     });
+}
+
+bm_status bm_dataset_storage(const bm_dataset* d, bm_dtype* storage) {
+    return guarded([&] { *storage = d->dtype; });
 }
 
 bm_status bm_dataset_shape(const bm_dataset* d, uint64_t* m, uint64_t* n) {

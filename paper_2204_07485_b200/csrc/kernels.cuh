@@ -614,7 +614,7 @@ struct ScreenConsts {
 constexpr int kSMaxK = 32;        // centroids handled by the screened path
 constexpr int kSThreads = 256;    // 8 warps: warp w < KG owns centroids 4w..4w+3
 constexpr int kSXS = kABP + 4;    // fp32 slab stride (16-byte aligned rows)
-constexpr int kItemCap = 4 * kABP + 64;  // (point, candidate) items per CTA
+constexpr int kItemCap = 4 * kABP;  // (point, candidate) items per CTA (2 per thread)
 
 struct ScreenSmem {
     union {
@@ -1229,10 +1229,23 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
     __syncthreads();
     const uint32_t NI = S.n_items;
-    // item buffers alias the (drained) raw ring
-    double* item_d = reinterpret_cast<double*>(&S.raw[0][0]);
+    // ---- pass 2: exact fp64 recheck, staged through shared memory ----
+    // The drained pass-1 buffers (raw ring .. cs) form one reusable block: the
+    // item list sits at its end, the rest holds dimension blocks of the tile's
+    // rows and of the active centroid rows, loaded with coalesced cp.async;
+    // every item's sequential fp64 chain (core.cpp:142-146) then runs from
+    // shared memory, carried in a register across blocks.
+    unsigned char* reuse = &S.raw[0][0];
+    const size_t reuse_bytes = static_cast<size_t>(reinterpret_cast<unsigned char*>(&S.red_u[0][0]) - reuse);
+    double* item_d = reinterpret_cast<double*>(reuse + reuse_bytes - kItemCap * (sizeof(double) + 3));
     short* item_p = reinterpret_cast<short*>(item_d + kItemCap);
     signed char* item_j = reinterpret_cast<signed char*>(item_p + kItemCap);
+    const size_t stage_bytes = reuse_bytes - kItemCap * (sizeof(double) + 3) - 64;
+    // dims per block: 128 rows of T + up to 32 centroid rows of f64, stride DB+1
+    const int DB = min(n, static_cast<int>(stage_bytes / (kABP * sizeof(T) + kSMaxK * sizeof(double)) - 1));
+    // (DB >= 39 for every storage type; the +1 row padding keeps item loads conflict-light)
+    T* xst = reinterpret_cast<T*>(reuse);
+    double* cst_ = reinterpret_cast<double*>(reuse + ((static_cast<size_t>(kABP) * (DB + 1) * sizeof(T) + 15) & ~size_t(15)));
     const bool overflow = NI > static_cast<uint32_t>(kItemCap);
     ktrace(8);
     if (!overflow) {
@@ -1248,44 +1261,48 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 ++it;
             }
         }
-        __syncthreads();
-        for (uint32_t i = tid; i < NI; i += kSThreads) {
-            const int p = item_p[i], j = item_j[i];
-            const T* xrow = X + (p0 + p) * ld;
-            const double* crow = Cact + static_cast<uint64_t>(j) * ldc;
-            double a = 0.0;
-            int d = 0;
-            for (; d + 8 <= n; d += 8) {
-                double xv[8], cv[8];
-                if constexpr (sizeof(T) == 8) {
+        double acc[2] = {0.0, 0.0};  // up to 2 items per thread (NI <= 512 here)
+        int ip[2], ij[2];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const double2 t = *reinterpret_cast<const double2*>(xrow + d + 2 * q);
-                        xv[2 * q] = t.x;
-                        xv[2 * q + 1] = t.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const float4 t = *reinterpret_cast<const float4*>(xrow + d + 4 * q);
-                        xv[4 * q] = t.x;
-                        xv[4 * q + 1] = t.y;
-                        xv[4 * q + 2] = t.z;
-                        xv[4 * q + 3] = t.w;
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const double2 t = __ldg(reinterpret_cast<const double2*>(crow + d + 2 * q));
-                    cv[2 * q] = t.x;
-                    cv[2 * q + 1] = t.y;
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) a = dist_step(a, xv[q], cv[q]);
-            }
-            for (; d < n; ++d) a = dist_step(a, to_f64(xrow[d]), crow[d]);
-            item_d[i] = a;
+        for (int r = 0; r < 2; ++r) {
+            ip[r] = -1;
+            ij[r] = 0;
         }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint32_t i = tid + r * kSThreads;
+            if (i < NI) {
+                ip[r] = item_p[i];
+                ij[r] = item_j[i];
+            }
+        }
+        for (int d0 = 0; d0 < n; d0 += DB) {
+            const int dl = min(DB, n - d0);
+            __syncthreads();  // previous block consumed
+            for (int e = tid; e < np * dl; e += kSThreads) {
+                const int p = e / dl, dd = e % dl;
+                xst[p * (DB + 1) + dd] = X[(p0 + p) * ld + d0 + dd];
+            }
+            for (int e = tid; e < KA * dl; e += kSThreads) {
+                const int j = e / dl, dd = e % dl;
+                cst_[j * (DB + 1) + dd] = Cact[static_cast<uint64_t>(j) * ldc + d0 + dd];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (ip[r] < 0) continue;
+                const T* xr = xst + ip[r] * (DB + 1);
+                const double* cr = cst_ + ij[r] * (DB + 1);
+                double a = acc[r];
+#pragma unroll 8
+                for (int dd = 0; dd < dl; ++dd) a = dist_step(a, to_f64(xr[dd]), cr[dd]);
+                acc[r] = a;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (ip[r] >= 0) item_d[tid + r * kSThreads] = acc[r];
         __syncthreads();
     }
     ktrace(9);
@@ -1711,6 +1728,25 @@ __global__ void k_check_finite(const T* __restrict__ X, uint64_t rows, int n, ui
         const double v = to_f64(X[(e / n) * ld + (e % n)]);
         if (!isfinite(v)) *bad = 1;
     }
+}
+
+// Lossless storage narrowing: an fp64 dataset whose every value round-trips
+// through fp32 exactly is stored as fp32 (every kernel promotes exactly, so all
+// results are unchanged) — half the HBM and L2 bytes.
+__global__ void k_check_narrow(const double* __restrict__ v, uint64_t count, int* bad, int* inexact) {
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double x = v[e];
+        if (!isfinite(x)) *bad = 1;
+        else if (static_cast<double>(static_cast<float>(x)) != x) *inexact = 1;
+    }
+}
+
+__global__ void k_narrow(const double* __restrict__ in, uint64_t rows, int n, float* __restrict__ out, uint64_t ld) {
+    const uint64_t total = rows * static_cast<uint64_t>(n);
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[(e / n) * ld + (e % n)] = static_cast<float>(in[e]);
 }
 
 template <typename T>

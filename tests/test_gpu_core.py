@@ -161,7 +161,8 @@ def test_screen_adversarial_bitwise(port, case):
     assert bm.objective(bm.Dataset(X), bm.Centroids(C, mask)) == port.block_sum(d2)
 
 
-@pytest.mark.parametrize("var,alt", [("BM_ASSIGN_MODE", "exact"), ("BM_GRAPHS", "0")])
+@pytest.mark.parametrize("var,alt", [("BM_ASSIGN_MODE", "exact"), ("BM_GRAPHS", "0"),
+                                     ("BM_STORAGE", "native"), ("BM_SCREEN", "v4")])
 def test_engine_modes_agree(var, alt):
     """Unscreened assignment (BM_ASSIGN_MODE=exact) and the host-driven chunk
     loop (BM_GRAPHS=0) give the same bits as the default path, in fresh processes."""
@@ -169,7 +170,7 @@ def test_engine_modes_agree(var, alt):
     code = (
         "import numpy as np, sys; sys.path.insert(0, '.');"
         "import paper_2204_07485_b200 as bm;"
-        "X = np.random.default_rng(5).normal(size=(20000, 16)) * 4;"
+        "X = np.rint(np.random.default_rng(5).normal(size=(20000, 16)) * 4);"
         "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=10, chunk_size=3000, max_chunks=6, seed=3));"
         "import hashlib; print(repr(o.objective), o.counter.distance_evals, hashlib.sha1(o.centroids.values.tobytes()).hexdigest())")
     env = dict(os.environ)
@@ -179,3 +180,16 @@ def test_engine_modes_agree(var, alt):
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                                    text=True, check=True).stdout)
     assert outs[0] == outs[1] and outs[0]
+
+
+def test_lossless_fp32_storage():
+    """fp64 input that round-trips through fp32 is stored as fp32; anything else stays fp64."""
+    Xi = np.rint(np.random.default_rng(1).normal(size=(1000, 5)) * 100)
+    assert bm.Dataset(Xi).storage == "f32"
+    Xr = np.random.default_rng(1).normal(size=(1000, 5))
+    assert bm.Dataset(Xr).storage == "f64"
+    assert bm.Dataset(Xr.astype(np.float32)).storage == "f32"
+    d = bm.Dataset(Xi)
+    assert (d.values() == Xi).all()
+    with pytest.raises(bm.ConfigError):
+        bm.Dataset(np.array([[1.0, np.nan]]))
