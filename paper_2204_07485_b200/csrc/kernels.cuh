@@ -993,6 +993,15 @@ constexpr size_t screen_smem_bytes() { return sizeof(ScreenSmem); }
 //    slab, after which the stage is refilled with slab+2 while the screen of
 //    the current slab runs.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_el(void* smem, const void* gmem, int bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <typename T>
 struct TmaSmem {
     static constexpr int kRawBytes = kABP * kADC * sizeof(T);  // 16 KB (f64) / 8 KB (f32)
@@ -1282,12 +1291,13 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             __syncthreads();  // previous block consumed
             for (int e = tid; e < np * dl; e += kSThreads) {
                 const int p = e / dl, dd = e % dl;
-                xst[p * (DB + 1) + dd] = X[(p0 + p) * ld + d0 + dd];
+                cp_async_el(&xst[p * (DB + 1) + dd], X + (p0 + p) * ld + d0 + dd, sizeof(T));
             }
             for (int e = tid; e < KA * dl; e += kSThreads) {
                 const int j = e / dl, dd = e % dl;
-                cst_[j * (DB + 1) + dd] = Cact[static_cast<uint64_t>(j) * ldc + d0 + dd];
+                cp_async_el(&cst_[j * (DB + 1) + dd], Cact + static_cast<uint64_t>(j) * ldc + d0 + dd, 8);
             }
+            cp_async_commit_wait_all();
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
