@@ -143,6 +143,9 @@ struct Workspace {
     DevBuf<int> act;         // k
     DevBuf<dev::LloydStatus> status;
     DevBuf<double> history;
+    // certified bounds for the Lloyd-round fast path of the screened assignment
+    DevBuf<float> lb;        // R: lower bound (distance units) to every non-chosen centroid
+    DevBuf<double> drift2;   // k: squared centroid movement of the last update
     // K-means++ (init.cpp:123-201)
     DevBuf<double> d2pool;   // (ncand + 1) * R
     DevBuf<uint32_t> cand;   // ncand
@@ -154,23 +157,25 @@ struct Workspace {
     // CUDA graphs of one chunk (sample resolution + gather, and the Lloyd loop)
     std::string graph_sig;
     cudaGraphExec_t g_prep[2] = {nullptr, nullptr};
-    cudaGraphExec_t g_lloyd = nullptr;
-    cudaStream_t cap2 = nullptr;  // capture stream of the WHILE body
-    cudaEvent_t ev_lloyd = nullptr;  // end of a chunk's Lloyd graph
+    cudaGraphExec_t g_lloyd[2] = {nullptr, nullptr};  // per chunk buffer
+    cudaStream_t cap1 = nullptr, cap2 = nullptr;  // capture streams of the IF and WHILE bodies
+    cudaEvent_t ev_lloyd[2] = {nullptr, nullptr};  // end of the Lloyd graph of chunk buffer b
+    cudaEvent_t ev_prep[2] = {nullptr, nullptr};   // chunk buffer b gathered
     void drop_graphs() {
-        for (auto& e : g_prep)
-            if (e) {
-                cudaGraphExecDestroy(e);
-                e = nullptr;
-            }
-        if (g_lloyd) cudaGraphExecDestroy(g_lloyd);
-        g_lloyd = nullptr;
+        for (auto* v : {&g_prep, &g_lloyd})
+            for (auto& e : *v)
+                if (e) {
+                    cudaGraphExecDestroy(e);
+                    e = nullptr;
+                }
         graph_sig.clear();
     }
     ~Workspace() {
         drop_graphs();
-        if (cap2) cudaStreamDestroy(cap2);
-        if (ev_lloyd) cudaEventDestroy(ev_lloyd);
+        for (auto q : {cap1, cap2})
+            if (q) cudaStreamDestroy(q);
+        for (auto e : {ev_lloyd[0], ev_lloyd[1], ev_prep[0], ev_prep[1]})
+            if (e) cudaEventDestroy(e);
     }
     // pinned host mirrors
     HostBuf<dev::LloydStatus> h_status;
@@ -201,6 +206,7 @@ struct Workspace {
         hist_cap = hist;
         labels.alloc(2 * R);
         dists.alloc(R);
+        lb.alloc(R);
         tile_buf.alloc(tiles * ncand);
         tile_ctr.alloc(tiles);
         if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
@@ -209,6 +215,7 @@ struct Workspace {
         psum.alloc(tiles * (uint64_t)k * n);
         pcnt.alloc(tiles * (uint64_t)k);
         C.alloc((uint64_t)k * n);
+        drift2.alloc(k);
         Cact.alloc((uint64_t)k * (n + (n & 1)));
         if (k <= dev::kSMaxK) {
             CT32.alloc((uint64_t)n * dev::kSMaxK);
@@ -226,7 +233,7 @@ struct Workspace {
         fopt.alloc(1);
         maskinc.alloc(k);
         chunk_ctr.alloc(1);
-        h_status.alloc(1);
+        h_status.alloc(2);  // [1]: second chunk buffer of the pipelined loop
         h_tiles.alloc(tiles * ncand);
         h_d2.alloc(R);
         h_mask.alloc(k);
@@ -326,6 +333,8 @@ struct DeviceCache {
     std::map<std::tuple<uint64_t, int, int, int, uint64_t>, std::unique_ptr<Workspace>> ws;
     std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SamplerWs>> sws;
     DevBuf<uint8_t> chunk;        // gathered chunk, s * ld * elem
+    DevBuf<uint8_t> chunk1;       // second chunk buffer (graph mode: gather c+1 during Lloyd c)
+    cudaStream_t pstream = nullptr;  // graph mode: prep (resolution + gather) of the next chunk
     DevBuf<int32_t> flabels;      // final pass
     DevBuf<double> fdists, ftiles;
     DevBuf<unsigned> fctr;
@@ -333,6 +342,7 @@ struct DeviceCache {
         ws.clear();
         sws.clear();
         if (stream) cudaStreamDestroy(stream);
+        if (pstream) cudaStreamDestroy(pstream);
     }
     void ensure_final(uint64_t rows) {
         if (flabels.n < rows) flabels.alloc(rows);
@@ -536,6 +546,15 @@ bool tma_screen() {
     return on;
 }
 
+// BM_HAMERLY=0 disables the bound-based Lloyd-round fast path (A/B checks).
+bool hamerly_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_HAMERLY");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
 // BM_ASSIGN_MODE=exact forces the unscreened kernel (A/B parity checks).
 bool screen_enabled(int k) {
     static const bool exact_forced = [] {
@@ -554,7 +573,7 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
 void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_t* labels_pair,
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
                    const int* stop, bool final_pass = false, double* tile_out = nullptr,
-                   unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr) {
+                   unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr, int hmode = 0) {
     const dev::LloydCtl noctl{};
     bool fused_ctl = false;
     const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
@@ -576,7 +595,8 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             dev::k_assign_tma<T><<<grid, dev::kSThreads, shm, st>>>(
                 tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
-                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl);
+                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
+                hamerly_enabled() ? hmode : 0, w.lb.p, w.drift2.p, k);
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
             static bool attr_set = false;  // per template instance
@@ -642,7 +662,7 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
                                          (int)shm));
         dev::k_update_partials<T><<<grid, dev::kUThreads, shm, st>>>(
             static_cast<const T*>(P.X), P.rows, n, P.ld, w.labels.p, w.R, parity, k, dslab, w.psum.p,
-            w.pcnt.p, &w.status.p->bad_label, stop);
+            w.pcnt.p, &w.status.p->bad_label, stop, w.drift2.p);
     });
     BM_LAUNCH();
     const unsigned mgrid = (unsigned)ceil_div((uint64_t)k * n, dev::kMThreads);
@@ -651,7 +671,7 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
         BM_CUDA(cudaFuncSetAttribute(dev::k_update_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mshm));
     dev::k_update_merge<<<mgrid, dev::kMThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p, w.mask.p,
                                                             w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active,
-                                                            w.CT32.p, stop);
+                                                            w.CT32.p, stop, w.drift2.p);
     BM_LAUNCH();
     count_launch(2);
 }
@@ -689,7 +709,7 @@ void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do
     if (do_compact) launch_compact(st, w, w.C.p, w.mask.p);
     const dev::LloydCtl ctl = make_ctl(w, 1, P.rows);
     launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr, false,
-                  w.tile_buf.p, w.tile_ctr.p, &ctl);
+                  w.tile_buf.p, w.tile_ctr.p, &ctl, 1);
 }
 
 // update (:33) + assign (:34-35) + step (:36-51), the step fused into the assignment.
@@ -700,7 +720,7 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
     launch_update(st, P, w, parity, stop);
     const dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond);
     launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop, false,
-                  w.tile_buf.p, w.tile_ctr.p, &ctl);
+                  w.tile_buf.p, w.tile_ctr.p, &ctl, 2);
 }
 
 // Runs the loop to completion; `between` is called once after the first
@@ -1014,15 +1034,12 @@ void enqueue_accept(cudaStream_t st, Workspace& w) {
 }
 
 // prep[b]: Fisher-Yates resolution of target buffer b, gather (:79-80), start := incumbent (:82)
-cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw,
-                             Workspace& w, int b) {
+cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, SamplerWs& sw, int b, void* chunk) {
     cudaGraph_t g = nullptr;
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     enqueue_resolve_device(st, sw, b);
     BM_CUDA(cudaEventRecordWithFlags(sw.resolved[b], st, cudaEventRecordExternal));
-    enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, dc.chunk.p);
-    BM_CUDA(cudaMemcpyAsync(w.C.p, w.Cinc.p, (size_t)w.k * w.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    BM_CUDA(cudaMemcpyAsync(w.mask.p, w.maskinc.p, w.k, cudaMemcpyDeviceToDevice, st));
+    enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, chunk);
     BM_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t e = nullptr;
     BM_CUDA(cudaGraphInstantiate(&e, g, 0));
@@ -1030,34 +1047,66 @@ cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, DeviceCache& 
     return e;
 }
 
-// lloyd (local_search.cpp:16-60) as compact+assign+begin, a WHILE node whose
-// body is one update/assign/step round (k_lloyd_step sets the condition), then
-// the accept (:89-94) and the status readback.
-cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, uint64_t max_it, double tol) {
-    if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
-    BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    lloyd_enqueue_begin(st, P, w, /*do_compact=*/false);  // accept (or the repair path) compacted the start
+// One chunk's Lloyd (local_search.cpp:16-60) + accept (:89-94) as a graph:
+//   k_guard -> IF(st->go) { assign+begin, WHILE { update, assign+step }, accept } -> status D2H
+// The IF lets the host queue chunk c+1 before chunk c's accept is known: when
+// that accept leaves degenerate incumbent rows the graph does nothing and the
+// host repairs (:83-85) and relaunches it.
+void add_conditional(cudaStream_t st, cudaGraphConditionalHandle* h, cudaGraph_t* body, cudaGraphConditionalNodeType type,
+                     unsigned dflt) {
     cudaStreamCaptureStatus cs;
     cudaGraph_t cg = nullptr;
     const cudaGraphNode_t* deps = nullptr;
     size_t nd = 0;
     BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
-    cudaGraphConditionalHandle h;
-    BM_CUDA(cudaGraphConditionalHandleCreate(&h, cg, 1, cudaGraphCondAssignDefault));
+    BM_CUDA(cudaGraphConditionalHandleCreate(h, cg, dflt, cudaGraphCondAssignDefault));
     cudaGraphNodeParams prm = {};
     prm.type = cudaGraphNodeTypeConditional;
-    prm.conditional.handle = h;
-    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.handle = *h;
+    prm.conditional.type = type;
     prm.conditional.size = 1;
     cudaGraphNode_t cn;
     BM_CUDA(cudaGraphAddNode(&cn, cg, deps, nd, &prm));
     BM_CUDA(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
-    cudaGraph_t body = prm.conditional.phGraph_out[0];
-    BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    lloyd_enqueue_round(w.cap2, P, w, max_it, tol, h, 1);
-    BM_CUDA(cudaStreamEndCapture(w.cap2, &body));
-    enqueue_accept(st, w);
-    BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
+    *body = prm.conditional.phGraph_out[0];
+}
+
+cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, uint64_t max_it, double tol, int b) {
+    if (!w.cap1) BM_CUDA(cudaStreamCreateWithFlags(&w.cap1, cudaStreamNonBlocking));
+    if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
+    BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    {  // the guard sets the IF condition inside the graph that owns it
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr));
+        cudaGraphConditionalHandle hif;
+        BM_CUDA(cudaGraphConditionalHandleCreate(&hif, cg, 0, cudaGraphCondAssignDefault));
+        dev::k_guard<<<1, 1, 0, st>>>(w.status.p, hif);
+        BM_LAUNCH();
+        cudaGraphNodeParams prm = {};
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+        prm.type = cudaGraphNodeTypeConditional;
+        prm.conditional.handle = hif;
+        prm.conditional.type = cudaGraphCondTypeIf;
+        prm.conditional.size = 1;
+        cudaGraphNode_t cn;
+        BM_CUDA(cudaGraphAddNode(&cn, cg, deps, nd, &prm));
+        BM_CUDA(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
+        cudaGraph_t ifbody = prm.conditional.phGraph_out[0];
+        BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap1, ifbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        lloyd_enqueue_begin(w.cap1, P, w, /*do_compact=*/false);  // accept (or the repair) compacted the start
+        cudaGraphConditionalHandle hw;
+        cudaGraph_t wbody = nullptr;
+        add_conditional(w.cap1, &hw, &wbody, cudaGraphCondTypeWhile, 1);
+        BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1);
+        BM_CUDA(cudaStreamEndCapture(w.cap2, &wbody));
+        enqueue_accept(w.cap1, w);
+        BM_CUDA(cudaStreamEndCapture(w.cap1, &ifbody));
+    }
+    BM_CUDA(cudaMemcpyAsync(w.h_status.p + b, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
     cudaGraph_t g = nullptr;
     BM_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t e = nullptr;
@@ -1069,15 +1118,19 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
 void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw, Workspace& w,
                    const Points& P, uint64_t max_it, double tol) {
     char sig[512];
-    std::snprintf(sig, sizeof(sig), "%llu/%p/%p/%p/%p/%p/%llu/%a/%llu",
-                  (unsigned long long)d->uid, (const void*)d->X, (void*)dc.chunk.p, (void*)&sw, (void*)w.drec.p,
-                  (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n);
-    if (w.graph_sig == sig && w.g_lloyd) return;
+    std::snprintf(sig, sizeof(sig), "%llu/%p/%p/%p/%p/%p/%p/%llu/%a/%llu",
+                  (unsigned long long)d->uid, (const void*)d->X, (void*)dc.chunk.p, (void*)dc.chunk1.p, (void*)&sw,
+                  (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n);
+    if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
-    w.g_prep[0] = capture_prep(st, d, dc, sw, w, 0);
-    w.g_prep[1] = capture_prep(st, d, dc, sw, w, 1);
-    w.g_lloyd = capture_lloyd(st, w, P, max_it, tol);
+    void* bufs[2] = {dc.chunk.p, dc.chunk1.p};
+    for (int b = 0; b < 2; ++b) {
+        Points Pb = P;
+        Pb.X = bufs[b];
+        w.g_prep[b] = capture_prep(st, d, sw, b, bufs[b]);
+        w.g_lloyd[b] = capture_lloyd(st, w, Pb, max_it, tol, b);
+    }
     g_profile.kernel_launches = saved;  // capture is not execution
     w.graph_sig = sig;
 }
@@ -1104,11 +1157,13 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         const size_t bytes = s * d->ld * dtype_size(d->dtype);
         if (dc.chunk.n < bytes) dc.chunk.alloc(bytes);
         chunkP.X = dc.chunk.p;
+        if (!g_profiling && graphs_enabled() && dc.chunk1.n < bytes) dc.chunk1.alloc(bytes);
     }
     const uint64_t want_rec = cfg.has_max_chunks ? cfg.max_chunks : 1024;
     if (w.drec.n < want_rec) w.drec.alloc(want_rec);
     // incumbent all degenerate, f_opt = +inf (:63-64), chunk counter 0
-    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.Cinc.p, w.maskinc.p, k, n, w.chunk_ctr.p);
+    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
+                                       w.chunk_ctr.p);
     BM_LAUNCH();
     if (!identity) put_stream(st, *sw, rng);
     const bool use_graphs = !identity && !g_profiling && graphs_enabled();
@@ -1119,37 +1174,62 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
 
     const auto t_loop = std::chrono::steady_clock::now();
     if (use_graphs) {
-        // Graph mode: chunk c+1's prep graph (resolution, gather, start copy) is
-        // queued behind chunk c's Lloyd graph before the host waits, so the GPU
-        // stays busy through the host's per-chunk turnaround.  The draws for
-        // chunk c+1 start as soon as chunk c's repair (if any) has consumed
-        // its draws (big_means.hpp:21-23).
-        if (!w.ev_lloyd) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd, cudaEventDisableTiming));
-        // BM_TIMELINE=1: in-stream events after every graph (GPU durations incl. gaps)
+        // Graph mode, two chunk buffers b = chunk & 1.  Chunk c+1's draws and
+        // prep (resolution + gather into buffer b^1) run on their own streams
+        // while chunk c's Lloyd graph runs, and chunk c+1's Lloyd graph is
+        // queued behind it before the host waits for chunk c; it runs only if
+        // chunk c's accept leaves no degenerate incumbent rows (k_guard).  The
+        // RNG order (big_means.hpp:21-23) is kept: chunk c+1's sample draws are
+        // enqueued after chunk c's repair draws, chunk c+2's after c+1's.
+        if (!dc.pstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.pstream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            if (!w.ev_lloyd[b]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd[b], cudaEventDisableTiming));
+            if (!w.ev_prep[b]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_prep[b], cudaEventDisableTiming));
+        }
+        const cudaStream_t pst = dc.pstream;
+        Points bufP[2] = {chunkP, chunkP};
+        bufP[1].X = dc.chunk1.p;
+        // BM_TIMELINE=1: in-stream events after every Lloyd graph (GPU time per chunk incl. gaps)
         static const bool timeline = std::getenv("BM_TIMELINE") != nullptr;
         std::vector<cudaEvent_t> tl_ev;
-        std::vector<int> tl_kind;
-        auto tl_mark = [&](int kind) {
+        auto tl_mark = [&] {
             if (!timeline) return;
             cudaEvent_t e;
             BM_CUDA(cudaEventCreate(&e));
             BM_CUDA(cudaEventRecord(e, st));
             tl_ev.push_back(e);
-            tl_kind.push_back(kind);
         };
-        tl_mark(-1);
+        // a chunk's prep: draws on rng_stream are already enqueued (drawn[b])
+        auto launch_prep = [&](int b) {
+            BM_CUDA(cudaStreamWaitEvent(pst, sw->drawn[b], 0));
+            BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[b], 0));  // buffer b's previous reader
+            BM_CUDA(cudaGraphLaunch(w.g_prep[b], pst));
+            BM_CUDA(cudaEventRecord(w.ev_prep[b], pst));
+            count_launch(6);
+        };
+        auto launch_lloyd = [&](int b) {
+            BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[b], 0));
+            BM_CUDA(cudaGraphLaunch(w.g_lloyd[b], st));
+            BM_CUDA(cudaEventRecord(w.ev_lloyd[b], st));
+            tl_mark();
+        };
+        // speculation needs the chunk count to be known in advance (no time budget)
+        const bool speculate = !cfg.has_max_cpu_seconds;
+        auto exists = [&](uint64_t c) { return !cfg.has_max_chunks || c < cfg.max_chunks; };
+        tl_mark();
+        BM_CUDA(cudaEventRecord(w.ev_lloyd[0], st));
+        BM_CUDA(cudaEventRecord(w.ev_lloyd[1], st));
         enqueue_device_draw(sw->rng_stream, *sw, 0, 0);
         BM_CUDA(cudaEventRecord(sw->drawn[0], sw->rng_stream));
-        BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[0], 0));
-        BM_CUDA(cudaGraphLaunch(w.g_prep[0], st));
-        tl_mark(0);
-        count_launch(6);
+        launch_prep(0);
+        bool queued = false;  // chunk `chunk`'s Lloyd graph is already queued (guarded)
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
             if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
                 break;  // :74-77
             if (chunk >= w.drec.n) {  // time-budget runs: grow the record buffer (graphs re-captured)
                 BM_CUDA(cudaStreamSynchronize(st));
+                BM_CUDA(cudaStreamSynchronize(pst));
                 DevBuf<dev::Record> bigger(w.drec.n * 2);
                 BM_CUDA(cudaMemcpyAsync(bigger.p, w.drec.p, w.drec.n * sizeof(dev::Record),
                                         cudaMemcpyDeviceToDevice, st));
@@ -1158,58 +1238,48 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 std::swap(w.drec.n, bigger.n);
                 ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
             }
-            const int jb = (int)(chunk & 1);
-            if (inc_degenerate > 0) {  // kmeanspp_fill (:84): prep(chunk) has run; its draws are done
+            const int b = (int)(chunk & 1);
+            if (inc_degenerate > 0) {  // kmeanspp_fill (:84) after this chunk's sample draws
+                // (a queued Lloyd graph of this chunk found st->go == 0 and did nothing)
+                BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[b], 0));
                 BM_CUDA(cudaMemcpyAsync(w.h_mask.p, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
                 BM_CUDA(cudaStreamSynchronize(st));
                 std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
                 BM_CUDA(cudaStreamSynchronize(sw->rng_stream));
                 get_stream(st, *sw, rng);
-                kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
+                kmeanspp_fill_device(st, bufP[b], w, hmask, cfg.candidates_per_step, rng, evals);
                 put_stream(st, *sw, rng);
                 launch_compact(st, w, w.C.p, w.mask.p);  // the Lloyd graph starts from Cact
-                tl_mark(2);
+                BM_CUDA(cudaMemsetAsync(&w.status.p->go, 0x01, sizeof(int), st));
+                queued = false;
             }
-            const bool next_exists = !cfg.has_max_chunks || chunk + 1 < cfg.max_chunks;
-            if (next_exists) {  // draws of chunk+1 (the stream is past this chunk's repair)
-                if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[jb ^ 1], 0));
-                enqueue_device_draw(sw->rng_stream, *sw, 0, jb ^ 1);
-                BM_CUDA(cudaEventRecord(sw->drawn[jb ^ 1], sw->rng_stream));
+            const bool next = exists(chunk + 1);
+            if (next) {  // chunk+1's draws: the stream is past this chunk's repair
+                if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[b ^ 1], 0));
+                enqueue_device_draw(sw->rng_stream, *sw, 0, b ^ 1);
+                BM_CUDA(cudaEventRecord(sw->drawn[b ^ 1], sw->rng_stream));
             }
-            BM_CUDA(cudaGraphLaunch(w.g_lloyd, st));
-            BM_CUDA(cudaEventRecord(w.ev_lloyd, st));
-            tl_mark(1);
-            if (next_exists) {
-                BM_CUDA(cudaStreamWaitEvent(st, sw->drawn[jb ^ 1], 0));
-                BM_CUDA(cudaGraphLaunch(w.g_prep[jb ^ 1], st));
-                tl_mark(0);
-                count_launch(6);
-            }
-            BM_CUDA(cudaEventSynchronize(w.ev_lloyd));
-            const dev::LloydStatus& ls = *w.h_status.p;
+            if (!queued) launch_lloyd(b);
+            if (next) launch_prep(b ^ 1);
+            queued = next && speculate;
+            if (queued) launch_lloyd(b ^ 1);  // runs iff this chunk's accept needs no repair
+            BM_CUDA(cudaEventSynchronize(w.ev_lloyd[b]));
+            const dev::LloydStatus& ls = w.h_status.p[b];
             if (ls.state_error) throw StateError("assign_nearest: every centroid is degenerate");
             if (ls.bad_label) throw ConfigError("update_centroids: label out of range");
             evals += ls.evals;  // lloyd accumulate (local_search.cpp:55-58)
             iterations += ls.iterations;
             inc_degenerate = ls.inc_degenerate;
-            count_launch(2 + 3 * ls.iterations);
+            count_launch(3 + 3 * ls.iterations);
             out->chunks = chunk + 1;
         }
         BM_CUDA(cudaStreamSynchronize(st));
+        BM_CUDA(cudaStreamSynchronize(pst));
         if (timeline && tl_ev.size() > 1) {
-            double acc[3] = {0, 0, 0};
-            int cnt[3] = {0, 0, 0};
-            for (size_t i = 1; i < tl_ev.size(); ++i) {
-                float ms = 0;
-                BM_CUDA(cudaEventElapsedTime(&ms, tl_ev[i - 1], tl_ev[i]));
-                acc[tl_kind[i]] += ms;
-                cnt[tl_kind[i]] += 1;
-            }
             float total = 0;
             BM_CUDA(cudaEventElapsedTime(&total, tl_ev.front(), tl_ev.back()));
-            std::fprintf(stderr, "[timeline] total %.3f ms | prep %d x %.1f us | lloyd %d x %.1f us | repair %d x %.1f us\n",
-                         total, cnt[0], cnt[0] ? 1e3 * acc[0] / cnt[0] : 0.0, cnt[1], cnt[1] ? 1e3 * acc[1] / cnt[1] : 0.0,
-                         cnt[2], cnt[2] ? 1e3 * acc[2] / cnt[2] : 0.0);
+            std::fprintf(stderr, "[timeline] total %.3f ms | %zu Lloyd graphs | %.1f us per chunk\n", total,
+                         tl_ev.size() - 1, 1e3 * total / (tl_ev.size() - 1));
             for (auto e : tl_ev) cudaEventDestroy(e);
         }
     } else {  // host-driven chunk loop (profiling, BM_GRAPHS=0, s == m)
@@ -1260,7 +1330,6 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             }
             kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
             if (!identity) put_stream(st, *sw, rng);
-            if (use_graphs) launch_compact(st, w, w.C.p, w.mask.p);  // the graph starts from Cact
         }
         // The next chunk's sample draws follow this chunk's (repair) draws:
         // start them now on rng_stream, overlapping this chunk's Lloyd.  Its
@@ -1272,17 +1341,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaEventRecord(sw->drawn[jb ^ 1], sw->rng_stream));
             drawn_ahead = true;
         }
-        if (use_graphs) {
-            BM_CUDA(cudaGraphLaunch(w.g_lloyd, st));
-            BM_CUDA(cudaStreamSynchronize(st));
-            const dev::LloydStatus& ls = *w.h_status.p;
-            if (ls.state_error) throw StateError("assign_nearest: every centroid is degenerate");
-            if (ls.bad_label) throw ConfigError("update_centroids: label out of range");
-            evals += ls.evals;  // lloyd accumulate (local_search.cpp:55-58)
-            iterations += ls.iterations;
-            inc_degenerate = ls.inc_degenerate;
-            count_launch(4 + 4 * ls.iterations);
-        } else {
+        {
             LloydResult lr = lloyd_run(st, chunkP, w, cfg.max_iterations, cfg.rel_tolerance);
             evals += lr.evals;
             iterations += lr.iterations;

@@ -37,7 +37,7 @@ struct LloydStatus {
     int state_error;     // assign against all-degenerate centroids (core.cpp:115-118)
     int inc_degenerate;  // degenerate rows of the incumbent after the accept step
     int bad_label;       // update saw a label outside [0,k) (core.cpp:189-193)
-    int pad;
+    int go;              // the next chunk starts from the incumbent as is (no repair, :83-85)
 };
 
 // Per-chunk accept record (ChunkRecord big_means.hpp:28-34).
@@ -56,7 +56,10 @@ __device__ __forceinline__ void ktrace(int slot) {
     if (threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_ktrace[(blockIdx.x & 2047) * 16 + slot] = t;
+        unsigned long long* row = g_ktrace + (blockIdx.x & 2047) * 32;
+        if (slot == 0)
+            for (int i = 1; i < 32; ++i) row[i] = 0;
+        row[slot] = t;
     }
 }
 #else
@@ -612,6 +615,7 @@ struct ScreenConsts {
 };
 
 constexpr int kSMaxK = 32;        // centroids handled by the screened path
+constexpr int kFailMax = 24;      // Lloyd-round bound failures handled per point
 constexpr int kSThreads = 256;    // 8 warps: warp w < KG owns centroids 4w..4w+3
 constexpr int kSXS = kABP + 4;    // fp32 slab stride (16-byte aligned rows)
 constexpr int kItemCap = 4 * kABP;  // (point, candidate) items per CTA (2 per thread)
@@ -998,6 +1002,13 @@ __device__ __forceinline__ void cp_async_el(void* smem, const void* gmem, int by
     if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
     else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void cp_async_commit_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -1014,6 +1025,11 @@ struct TmaSmem {
     float nc_lo[kSMaxK], nc_hi[kSMaxK], ncr[kSMaxK];
     unsigned cand[kABP];                                       // candidate bitmask per point
     int icount[kABP];
+    int lab_rank[kABP];                                        // chosen compacted centroid per point
+    int rank_of[kSMaxK];                                       // label -> compacted index
+    short fail_list[kABP];                                     // points whose bound test failed
+    int nfail;
+    float dmax;
     uint64_t bar[2];
     uint32_t n_items;
     int is_last;
@@ -1030,6 +1046,127 @@ __device__ __forceinline__ T raw_at(const unsigned char* raw, int p, int d) {
     }
 }
 
+// Exact fp64 distance of one stored row to one centroid row: the reference's
+// sequential chain (core.cpp:142-146) with vector loads (rows are 16-byte aligned
+// whenever the TMA path runs: TMA strides are multiples of 16 bytes).
+template <typename T>
+__device__ __forceinline__ double exact_row_dist(const T* __restrict__ x, const double* __restrict__ c, int n) {
+    double a = 0.0;
+    int d = 0;
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll 4
+        for (; d + 4 <= n; d += 4) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + d));
+            const double2 c0 = __ldg(reinterpret_cast<const double2*>(c + d));
+            const double2 c1 = __ldg(reinterpret_cast<const double2*>(c + d + 2));
+            a = dist_step(a, xv.x, c0.x);
+            a = dist_step(a, xv.y, c0.y);
+            a = dist_step(a, xv.z, c1.x);
+            a = dist_step(a, xv.w, c1.y);
+        }
+    } else {
+#pragma unroll 4
+        for (; d + 2 <= n; d += 2) {
+            const double2 xv = __ldg(reinterpret_cast<const double2*>(x + d));
+            const double2 cv = __ldg(reinterpret_cast<const double2*>(c + d));
+            a = dist_step(a, xv.x, cv.x);
+            a = dist_step(a, xv.y, cv.y);
+        }
+    }
+    for (; d < n; ++d) a = dist_step(a, to_f64(x[d]), c[d]);
+    return a;
+}
+
+// Exact fp64 distances (core.cpp:142-146) of `ni` (point, compacted centroid)
+// items (ni <= 2 * kSThreads, up to 2 per thread), each chain carried in a
+// register in dimension order.  The CTA's 128-row point block streams through
+// the raw TMA ring again (one 16-dim slab per stage; slab i is TMA sequence
+// number qb + i of this CTA), the matching centroid slabs through cp.async.
+template <typename T>
+__device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx, uint64_t p0, int n, int nslab,
+                                           int qb, const double* __restrict__ Cact, int ldc, int KA, uint32_t ni,
+                                           const short* item_p, const signed char* item_j, double* item_d) {
+    constexpr int kCS = 18;  // centroid slab row stride (doubles): 16-byte rows, spread banks
+    const int tid = threadIdx.x;
+    double(*c64)[kSMaxK][kCS] = reinterpret_cast<double(*)[kSMaxK][kCS]>(&S.xs[0][0][0]);
+    __syncthreads();  // item list complete; the ring and the staging area are free
+    double acc[2] = {0.0, 0.0};
+    int ip[2] = {-1, -1}, ij[2] = {0, 0};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const uint32_t i = tid + r * kSThreads;
+        if (i < ni) {
+            ip[r] = item_p[i];
+            ij[r] = item_j[i];
+        }
+    }
+    auto issue = [&](int sl) {
+        const int st = (qb + sl) & 1;
+        if (tid == 0) {
+            mbar_expect_tx(&S.bar[st], TmaSmem<T>::kRawBytes);
+            tma_load_2d(S.raw[st], tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
+        }
+        if (tid < KA * (kADC / 2)) {
+            const int j = tid >> 3, h = tid & 7, d = sl * kADC + 2 * h;
+            if (d < n) cp_async_16(&c64[st][j][2 * h], Cact + static_cast<uint64_t>(j) * ldc + d);
+        }
+        cp_async_commit();
+    };
+    issue(0);
+    if (nslab > 1) issue(1);
+    for (int sl = 0; sl < nslab; ++sl) {
+        const int q = qb + sl, st = q & 1;
+        if (sl + 1 < nslab) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        mbar_wait(&S.bar[st], (q >> 1) & 1);
+        if (qb == 0 && sl < 5) ktrace(16 + 2 * sl);
+        __syncthreads();  // everyone's centroid pieces landed
+        const int dl = min(kADC, n - sl * kADC);
+        const unsigned char* raw = S.raw[st];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (ip[r] < 0) continue;
+            const int p = ip[r];
+            const double* cr = c64[st][ij[r]];
+            double a = acc[r];
+            if (dl == kADC) {
+                if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float4 xv = *reinterpret_cast<const float4*>(raw + p * 64 + (((c ^ (p >> 1)) & 3) << 4));
+                        a = dist_step(a, xv.x, cr[4 * c]);
+                        a = dist_step(a, xv.y, cr[4 * c + 1]);
+                        a = dist_step(a, xv.z, cr[4 * c + 2]);
+                        a = dist_step(a, xv.w, cr[4 * c + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const double2 xv = *reinterpret_cast<const double2*>(raw + p * 128 + (((c ^ p) & 7) << 4));
+                        a = dist_step(a, xv.x, cr[2 * c]);
+                        a = dist_step(a, xv.y, cr[2 * c + 1]);
+                    }
+                }
+            } else {
+                for (int d = 0; d < dl; ++d) a = dist_step(a, to_f64(raw_at<T>(raw, p, d)), cr[d]);
+            }
+            acc[r] = a;
+        }
+        __syncthreads();  // stage st consumed
+        if (qb == 0 && sl < 5) ktrace(17 + 2 * sl);
+        if (sl + 2 < nslab) issue(sl + 2);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+        if (ip[r] >= 0) item_d[tid + r * kSThreads] = acc[r];
+    __syncthreads();
+}
+
+// hmode: 0 = screen; 1 = screen and record each point's certified lower bound
+// on its distance to every non-chosen centroid (lb_r, r-space); 2 = Lloyd round:
+// first the exact distance to the previous label, accepted for the whole CTA
+// when every point beats (lb_r - max centroid drift)^2 (1-g64) — the reference's
+// argmin is then provably unchanged and unique — else the full screen.
 template <typename T>
 __global__ void __launch_bounds__(kSThreads, 3)
 k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmc,
@@ -1040,7 +1177,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
              int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
-             unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl) {
+             unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl,
+             int hmode, float* __restrict__ lb_r, const double* __restrict__ drift2, int kfull) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
     unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1064,7 +1202,15 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
     const float finf = __int_as_float(0x7F800000);
     const int nslab = (n + kADC - 1) / kADC;
-
+    // reusable block (pass-1 buffers) for the staged exact chains; item list at its end
+    unsigned char* reuse = &S.raw[0][0];
+    const size_t reuse_bytes = static_cast<size_t>(reinterpret_cast<unsigned char*>(&S.red_u[0][0]) - reuse);
+    double* item_d = reinterpret_cast<double*>(reuse + reuse_bytes - kItemCap * (sizeof(double) + 3));
+    short* item_p = reinterpret_cast<short*>(item_d + kItemCap);
+    signed char* item_j = reinterpret_cast<signed char*>(item_p + kItemCap);
+    static_assert(offsetof(TmaSmem<T>, red_u) - kItemCap * (sizeof(double) + 3) >=
+                      offsetof(TmaSmem<T>, xs) + 2 * kSMaxK * 18 * sizeof(double),
+                  "centroid staging of tma_chains overlaps the item list");
     ktrace(0);
     if (tid == 0) {
         tma_prefetch_map(&tmx);
@@ -1073,9 +1219,108 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         mbar_init(&S.bar[1], 1);
         fence_mbar_init();
     }
+    int qb = 0;  // TMA slabs this CTA has consumed (ring position)
+
+    // ---------------- Lloyd-round fast path (exact, certified) ----------------
+    if (hmode == 2 && labels_old && lb_r && drift2) {
+        if (tid < kSMaxK) S.rank_of[tid] = -1;
+        if (tid == 0) S.nfail = 0;
+        __syncthreads();
+        if (tid < KA) S.rank_of[act_idx[tid]] = tid;
+        if (tid == 32) {  // max drift of the active centroids since the bounds were taken
+            double dm = 0.0;
+            for (int r = 0; r < KA; ++r) dm = fmax(dm, drift2[act_idx[r]]);
+            // sqrt of an upper bound, rounded up with margin (atomic fp64 sums: order-free bound)
+            S.dmax = __double2float_ru(__dsqrt_ru(dm * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+        }
+        __syncthreads();
+        ktrace(13);
+        if (tid < np) {
+            const int a = labels_old[p0 + tid];
+            const int ra = (a >= 0 && a < kfull) ? S.rank_of[a] : -1;
+            S.lab_rank[tid] = ra;
+            item_p[tid] = static_cast<short>(tid);
+            item_j[tid] = static_cast<signed char>(ra < 0 ? 0 : ra);
+        }
+        ktrace(26);
+        tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, static_cast<uint32_t>(np), item_p, item_j, item_d);
+        qb += nslab;
+        if (tid < np) {
+            const uint64_t gp = p0 + tid;
+            const int ra = S.lab_rank[tid];
+            bool ok = false;
+            if (ra >= 0) {
+                const double dn = item_d[tid];
+                // every other centroid is now at least lb - dmax away (triangle inequality)
+                const float lbn = fmaxf(__fsub_rd(lb_r[gp], S.dmax), 0.f);
+                const float Lnew = __fmul_rd(__fmul_rd(lbn, lbn), cst.lo64);
+                ok = dn < static_cast<double>(Lnew);
+                if (ok) {  // the reference's scan provably returns the old label, uniquely
+                    labels_out[gp] = labels_old[gp];
+                    if (dists_out) dists_out[gp] = dn;
+                    lb_r[gp] = lbn;
+                }
+            }
+            if (!ok) S.fail_list[atomicAdd(&S.nfail, 1)] = static_cast<short>(tid);
+        }
+        __syncthreads();
+        ktrace(14);
+        const int nfail = S.nfail;
+        if (tid == 0 && cand_counter) {
+            atomicAdd(cand_counter, static_cast<unsigned long long>(np - nfail + nfail * KA));
+            atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
+        }
+        if (nfail <= kFailMax) {
+            // the few points whose bound failed: a warp scans all active centroids
+            // exactly (lane j: centroid j), first minimum wins as in core.cpp:147
+            for (int f = warp; f < nfail; f += kSThreads / 32) {
+                const int p = S.fail_list[f];
+                const uint64_t gp = p0 + p;
+                double v = __longlong_as_double(0x7FF0000000000000LL);
+                if (lane < KA) {
+                    const double dj = exact_row_dist(X + gp * ld, Cact + static_cast<uint64_t>(lane) * ldc, n);
+                    if (!isnan(dj)) v = dj;
+                }
+                double bv = v;
+                int bj = lane;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+                    const int oj = __shfl_xor_sync(0xFFFFFFFFu, bj, o);
+                    if (ov < bv || (ov == bv && oj < bj)) {
+                        bv = ov;
+                        bj = oj;
+                    }
+                }
+                const bool found = bv < __longlong_as_double(0x7FF0000000000000LL);
+                double m2 = lane == bj ? __longlong_as_double(0x7FF0000000000000LL) : v;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) m2 = fmin(m2, __shfl_xor_sync(0xFFFFFFFFu, m2, o));
+                if (lane == 0) {
+                    const int label = found ? act_idx[bj] : -1;
+                    labels_out[gp] = label;
+                    if (dists_out) dists_out[gp] = found ? bv : __longlong_as_double(0x7FF0000000000000LL);
+                    if (labels_old[gp] != label) *changed_flag = 1;
+                    // true distance to every other centroid >= fl64 distance / hi64
+                    float lb = 3.0e38f;
+                    if (m2 < __longlong_as_double(0x7FF0000000000000LL)) {
+                        const double q = __dsub_rd(__ddiv_rd(m2, static_cast<double>(cst.hi64)), 1e-300);
+                        lb = q > 0.0 ? __fsqrt_rd(__double2float_rd(q)) : 0.f;
+                    }
+                    lb_r[gp] = lb;
+                }
+            }
+            ktrace(15);
+            goto fold;
+        }
+        // many failures: full screen of the block
+        // (the fast-path writes above are recomputed identically)
+        __syncthreads();
+    }
+    {
     __syncthreads();
     auto issue = [&](int sl) {
-        const int st = sl & 1;
+        const int st = (qb + sl) & 1;
         mbar_expect_tx(&S.bar[st], kStageBytes);
         tma_load_2d(S.raw[st], &tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
         tma_load_2d(&S.craw[st][0][0], &tmc, &S.bar[st], 0, sl * kADC);
@@ -1095,8 +1340,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     const int cp_ = tid & (kABP - 1), chalf = tid >> 7;  // conversion: point, 8-dim half
 
     for (int sl = 0; sl < nslab; ++sl) {
-        const int st = sl & 1, dl = min(kADC, n - sl * kADC);
-        mbar_wait(&S.bar[st], (sl >> 1) & 1);
+        const int q = qb + sl, st = q & 1, dl = min(kADC, n - sl * kADC);
+        mbar_wait(&S.bar[st], (q >> 1) & 1);
         if (sl < 6) ktrace(1 + sl);
         // raw (swizzled [p][d], storage type) -> fp32 [d][p], once per element
 #pragma unroll
@@ -1161,9 +1406,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
     __syncthreads();
     ktrace(7);
-    // certified bounds (same algebra as k_assign_screen): upper bounds first,
-    // then each warp tests its lower bounds against the point's minimum U and
-    // sets candidate bits (no per-(j,p) bound array is kept).
+    // certified bounds: upper bounds first, then each warp tests its lower
+    // bounds against the point's minimum U and sets candidate bits.
     float Lk[4][kAK];
     if (tid < kABP) S.cand[tid] = 0u;
     if (comp) {
@@ -1238,25 +1482,9 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
     __syncthreads();
     const uint32_t NI = S.n_items;
-    // ---- pass 2: exact fp64 recheck, staged through shared memory ----
-    // The drained pass-1 buffers (raw ring .. cs) form one reusable block: the
-    // item list sits at its end, the rest holds dimension blocks of the tile's
-    // rows and of the active centroid rows, loaded with coalesced cp.async;
-    // every item's sequential fp64 chain (core.cpp:142-146) then runs from
-    // shared memory, carried in a register across blocks.
-    unsigned char* reuse = &S.raw[0][0];
-    const size_t reuse_bytes = static_cast<size_t>(reinterpret_cast<unsigned char*>(&S.red_u[0][0]) - reuse);
-    double* item_d = reinterpret_cast<double*>(reuse + reuse_bytes - kItemCap * (sizeof(double) + 3));
-    short* item_p = reinterpret_cast<short*>(item_d + kItemCap);
-    signed char* item_j = reinterpret_cast<signed char*>(item_p + kItemCap);
-    const size_t stage_bytes = reuse_bytes - kItemCap * (sizeof(double) + 3) - 64;
-    // dims per block: 128 rows of T + up to 32 centroid rows of f64, stride DB+1
-    const int DB = min(n, static_cast<int>(stage_bytes / (kABP * sizeof(T) + kSMaxK * sizeof(double)) - 1));
-    // (DB >= 39 for every storage type; the +1 row padding keeps item loads conflict-light)
-    T* xst = reinterpret_cast<T*>(reuse);
-    double* cst_ = reinterpret_cast<double*>(reuse + ((static_cast<size_t>(kABP) * (DB + 1) * sizeof(T) + 15) & ~size_t(15)));
     const bool overflow = NI > static_cast<uint32_t>(kItemCap);
     ktrace(8);
+    // ---- pass 2: exact fp64 recheck of the candidates ----
     if (!overflow) {
         if (tid < np) {
             const int p = tid;
@@ -1270,50 +1498,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 ++it;
             }
         }
-        double acc[2] = {0.0, 0.0};  // up to 2 items per thread (NI <= 512 here)
-        int ip[2], ij[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            ip[r] = -1;
-            ij[r] = 0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const uint32_t i = tid + r * kSThreads;
-            if (i < NI) {
-                ip[r] = item_p[i];
-                ij[r] = item_j[i];
-            }
-        }
-        for (int d0 = 0; d0 < n; d0 += DB) {
-            const int dl = min(DB, n - d0);
-            __syncthreads();  // previous block consumed
-            for (int e = tid; e < np * dl; e += kSThreads) {
-                const int p = e / dl, dd = e % dl;
-                cp_async_el(&xst[p * (DB + 1) + dd], X + (p0 + p) * ld + d0 + dd, sizeof(T));
-            }
-            for (int e = tid; e < KA * dl; e += kSThreads) {
-                const int j = e / dl, dd = e % dl;
-                cp_async_el(&cst_[j * (DB + 1) + dd], Cact + static_cast<uint64_t>(j) * ldc + d0 + dd, 8);
-            }
-            cp_async_commit_wait_all();
-            __syncthreads();
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                if (ip[r] < 0) continue;
-                const T* xr = xst + ip[r] * (DB + 1);
-                const double* cr = cst_ + ij[r] * (DB + 1);
-                double a = acc[r];
-#pragma unroll 8
-                for (int dd = 0; dd < dl; ++dd) a = dist_step(a, to_f64(xr[dd]), cr[dd]);
-                acc[r] = a;
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-            if (ip[r] >= 0) item_d[tid + r * kSThreads] = acc[r];
-        __syncthreads();
+        tma_chains<T>(S, &tmx, p0, n, nslab, qb + nslab, Cact, ldc, KA, NI, item_p, item_j, item_d);
     }
     ktrace(9);
     if (tid < np) {
@@ -1321,7 +1506,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         const uint64_t gp = p0 + p;
         double best = __longlong_as_double(0x7FF0000000000000LL);
         int bj = -1;
-        if (!overflow) {
+        if (!overflow) {  // ascending j, strict < (core.cpp:147)
             const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(S.icount[p + 1]) : NI;
             for (uint32_t i = S.icount[p]; i < b1; ++i) {
                 if (item_d[i] < best) {
@@ -1329,7 +1514,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                     bj = item_j[i];
                 }
             }
-        } else {
+        } else {  // candidate sets too large for the item buffer: full exact scan
             const T* x = X + gp * ld;
             for (int j = 0; j < KA; ++j) {
                 const double* c = Cact + static_cast<uint64_t>(j) * ldc;
@@ -1345,7 +1530,30 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         labels_out[gp] = label;
         if (dists_out) dists_out[gp] = best;
         if (labels_old && labels_old[gp] != label) *changed_flag = 1;
+        S.lab_rank[p] = bj;
     }
+    if (hmode >= 1 && lb_r) {  // lower bound to every centroid but the chosen one (r-space)
+        __syncthreads();
+        if (comp) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int p = 4 * lane + q;
+                float m = finf;
+#pragma unroll
+                for (int u = 0; u < kAK; ++u)
+                    if (kAK * warp + u != S.lab_rank[p]) m = fminf(m, Lk[q][u]);
+                S.red_u[warp][p] = m;
+            }
+        }
+        __syncthreads();
+        if (tid < np) {
+            float m = finf;
+            for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][tid]);
+            lb_r[p0 + tid] = m < finf ? __fsqrt_rd(m) : 3.0e38f;
+        }
+    }
+    }
+fold:
     ktrace(10);
     if (!tile_out) return;
     __syncthreads();
@@ -1451,8 +1659,10 @@ k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                   const int32_t* __restrict__ labels_pair, uint64_t pair_stride,
                   const int* __restrict__ parity_ptr, int k, int dslab,
                   double* __restrict__ psum, uint32_t* __restrict__ pcnt, int* __restrict__ bad_label,
-                  const int* __restrict__ stop_ptr) {
+                  const int* __restrict__ stop_ptr, double* __restrict__ drift2) {
     if (stop_ptr && *stop_ptr) return;
+    if (drift2 && blockIdx.x == 0 && blockIdx.y == 0)  // zeroed for k_update_merge
+        for (int j = threadIdx.x; j < k; j += blockDim.x) drift2[j] = 0.0;
     extern __shared__ int ush[];
     short* order = reinterpret_cast<short*>(ush);      // [kTile]
     int* cnt = ush + kTile / 2;                         // [k] tile totals
@@ -1550,7 +1760,7 @@ __global__ void __launch_bounds__(kMThreads)
 k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcnt, uint64_t ntiles,
                int k, int n, double* __restrict__ C, uint8_t* __restrict__ mask,
                double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
-               float* __restrict__ CT32, const int* __restrict__ stop_ptr) {
+               float* __restrict__ CT32, const int* __restrict__ stop_ptr, double* __restrict__ drift2) {
     if (stop_ptr && *stop_ptr) return;
     extern __shared__ unsigned long long msh[];
     unsigned long long* total = msh;                  // [k]
@@ -1600,6 +1810,10 @@ k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcn
         if (pcnt[t * k + j]) acc = __dadd_rn(acc, psum[(t * k + j) * n + d]);
     const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
     const double v = __dmul_rn(acc, inv);
+    if (drift2) {  // squared movement of centroid j (bounds of the next assignment)
+        const double dv = __dsub_rn(v, C[e]);
+        atomicAdd(&drift2[j], __dmul_rn(dv, dv));
+    }
     C[e] = v;
     const int rk = rank[j];
     Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
@@ -1637,8 +1851,8 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
 // device so the chunk can run inside a CUDA graph.  The incumbent is also
 // written in compacted form (Cact/act/n_active/CT32): it is the next chunk's
 // start (:82) when no repair is needed.
-__global__ void k_accept(LloydStatus* st, double* f_opt, const double* __restrict__ C,
-                         const uint8_t* __restrict__ mask, double* __restrict__ Cinc,
+__global__ void k_accept(LloydStatus* st, double* f_opt, double* __restrict__ C,
+                         uint8_t* __restrict__ mask, double* __restrict__ Cinc,
                          uint8_t* __restrict__ maskinc, int k, int n, Record* rec_base,
                          unsigned long long* chunk_ctr, double* __restrict__ Cact, int ldc,
                          int* __restrict__ act_idx, float* __restrict__ CT32) {
@@ -1669,27 +1883,39 @@ __global__ void k_accept(LloydStatus* st, double* f_opt, const double* __restric
             if (!maskinc[j]) act_idx[r++] = j;
         }
         st->inc_degenerate = dcount;
+        st->go = dcount == 0;
         st->n_active = r;
         *chunk_ctr += 1;
     }
     __syncthreads();
+    // the next chunk's start (:82): (C, mask) := incumbent, and its compacted form
+    if (!accepted)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) mask[j] = maskinc[j];
     for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
         const int j = e / n, d = e % n, rk = arank[j];
-        if (rk < 0) continue;
         const double v = Cinc[e];
+        if (!accepted) C[e] = v;
+        if (rk < 0) continue;
         Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
         if (CT32 && rk < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
     }
 }
 
+// Head of a chunk's Lloyd graph: the chunk runs only when the previous accept
+// left no degenerate incumbent rows, or the host has repaired them (st->go).
+__global__ void k_guard(const LloydStatus* st, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, st->go != 0 ? 1u : 0u);
+}
+
 // Reset of the per-run device state (incumbent all degenerate, f_opt = +inf).
-__global__ void k_run_init(LloydStatus* st, double* f_opt, double* Cinc, uint8_t* maskinc, int k, int n,
-                           unsigned long long* chunk_ctr) {
-    for (int e = threadIdx.x; e < k * n; e += blockDim.x) Cinc[e] = 0.0;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) maskinc[j] = 1;
+__global__ void k_run_init(LloydStatus* st, double* f_opt, double* Cinc, uint8_t* maskinc, double* C,
+                           uint8_t* mask, int k, int n, unsigned long long* chunk_ctr) {
+    for (int e = threadIdx.x; e < k * n; e += blockDim.x) Cinc[e] = C[e] = 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) maskinc[j] = mask[j] = 1;
     if (threadIdx.x == 0) {
         *f_opt = __longlong_as_double(0x7FF0000000000000LL);
         st->inc_degenerate = k;
+        st->go = 0;
         *chunk_ctr = 0;
     }
 }

@@ -150,3 +150,38 @@ def test_lloyd_vs_oracle_random(port, dtype):
     assert (bits(o.centroids.values) == bits(p["centroids"])).all()
     assert (o.assignment == p["labels"]).all()
     assert (bits(o.objective_history) == bits(p["history"])).all()
+
+
+def _blobs(rng, m, n, k, spread):
+    centers = rng.normal(size=(k, n)) * spread
+    return centers[rng.integers(0, k, m)] + rng.normal(size=(m, n))
+
+
+@pytest.mark.parametrize("case", ["ties", "blobs", "blobs_f32", "tight", "huge", "tiny"])
+def test_lloyd_bound_fast_path_vs_oracle(port, case):
+    """Lloyd rounds take the certified bound test (labels kept when every point
+    beats its drifted lower bound); every regime must still match the oracle's
+    bits: exact ties, well separated blobs (the fast path almost always holds),
+    touching blobs, values outside fp32 range (no bounds) and tiny magnitudes."""
+    rng = np.random.default_rng(11)
+    if case == "ties":
+        X = rng.integers(0, 4, (6000, 3)).astype(np.float64)
+    elif case in ("blobs", "blobs_f32"):
+        X = _blobs(rng, 20000, 20, 8, 20.0)
+    elif case == "tight":
+        X = _blobs(rng, 20000, 9, 12, 1.5)
+    elif case == "huge":
+        X = _blobs(rng, 5000, 6, 5, 10.0) * 1e30
+    else:
+        X = _blobs(rng, 5000, 6, 5, 10.0) * 1e-30
+    if case == "blobs_f32":
+        X = X.astype(np.float32)
+    Xd = X.astype(np.float64)
+    k = 7 if case == "ties" else 10
+    start = Xd[rng.choice(len(Xd), k, replace=False)]
+    o = bm.lloyd(bm.Dataset(X), bm.Centroids.from_rows(start), bm.SearchConfig(rel_tolerance=0.0))
+    p = port.lloyd(Xd, start, np.zeros(k, np.uint8), 300, 0.0)
+    assert (bits(o.centroids.values) == bits(p["centroids"])).all()
+    assert (o.centroids.mask == p["mask"]).all()
+    assert (o.assignment == p["labels"]).all()
+    assert (bits(o.objective_history) == bits(p["history"])).all()

@@ -2,6 +2,7 @@
 
   python tools/ktrace.py --build        # builds tools/_ktrace/libbigmeans_b200.so with -DBM_KTRACE
   python tools/ktrace.py [m] [n] [k]    # one assign_nearest launch, prints phase percentiles (us)
+  python tools/ktrace.py lloyd [m] [n] [k]  # the last launch of a 1-round Lloyd (bound fast path)
 """
 import ctypes as C
 import os
@@ -24,24 +25,36 @@ from paper_2204_07485_b200 import _capi  # noqa: E402
 _capi.LIB_PATH = LIB
 import paper_2204_07485_b200 as bm  # noqa: E402
 
-m = int(sys.argv[1]) if len(sys.argv) > 1 else 50_000
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 68
-k = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+args = [a for a in sys.argv[1:] if a != "lloyd"]
+lloyd_mode = "lloyd" in sys.argv
+m = int(args[0]) if len(args) > 0 else 50_000
+n = int(args[1]) if len(args) > 1 else 68
+k = int(args[2]) if len(args) > 2 else 25
 rng = np.random.default_rng(0)
 X = np.rint(rng.normal(size=(m, n)) * 5 + rng.integers(0, 20, (m, 1)))
 C0 = X[rng.choice(m, k, replace=False)] + 0.3
+if lloyd_mode:  # a c2-like chunk started from centroids converged on another chunk
+    from paper_2204_07485_b200 import synthetic
+    full = synthetic.generate("c2", 2 * m)
+    X, n = full[m:], full.shape[1]
+    warm = bm.lloyd(bm.Dataset(full[:m]), bm.Centroids(full[:k].astype(np.float64), np.zeros(k, np.uint8)))
+    C0 = warm.centroids.values
 d = bm.Dataset(X)
 cent = bm.Centroids(C0, np.zeros(k, np.uint8))
 for _ in range(3):
-    bm.assign_nearest(d, cent)
-buf = np.zeros(2048 * 16, np.uint64)
+    if lloyd_mode:
+        bm.lloyd(d, cent, bm.SearchConfig(max_iterations=1))
+    else:
+        bm.assign_nearest(d, cent)
+buf = np.zeros(2048 * 32, np.uint64)
 lib = _capi.load()
 assert lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size) == 0
 ctas = (m + 127) // 128
-T = buf[: min(ctas, 2048) * 16].reshape(-1, 16).astype(np.int64)
+T = buf[: min(ctas, 2048) * 32].reshape(-1, 32).astype(np.int64)
 t0 = T[:, 0].min()
 names = ["start", "slab0", "slab1", "slab2", "slab3", "slab4", "slab5", "bounds", "items", "recheck",
-         "out", "lastwait", "fold"]
+         "out", "lastwait", "fold", "fp_setup", "fp_own", "fp_fails"] + \
+    [f"c{i//2}{'wait' if i % 2 == 0 else 'done'}" for i in range(10)] + ["fp_items"]
 print(f"m={m} n={n} k={k} ctas={ctas}")
 for i, nm in enumerate(names):
     col = T[:, i]
