@@ -34,7 +34,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define BM_CUDA(x) ::bm::cuda_check((x), #x, __FILE__, __LINE__)
 #define BM_LAUNCH() ::bm::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
-inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
-inline uint64_t tiles_of(uint64_t rows) { return ceil_div(rows, kTile); }
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline uint64_t tiles_of(uint64_t rows) { return ceil_div(rows, kTile); }
 
 }  // namespace bm

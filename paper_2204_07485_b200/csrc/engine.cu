@@ -135,7 +135,6 @@ struct Workspace {
     DevBuf<unsigned> tile_ctr;  // tiles (fused tile-fold arrival counters)
     DevBuf<unsigned> tiles_done;  // tiles completed in the current assignment launch (fused control)
     DevBuf<double> psum;     // tiles * k * n
-    DevBuf<uint32_t> pcnt;   // tiles * k
     DevBuf<double> C, Cact;  // k * n
     DevBuf<float> CT32;      // n * 32: fp32 compacted centroids, transposed [d][j] (TMA screen)
     CUtensorMap tm_ct{};     // tensor map of CT32
@@ -145,7 +144,9 @@ struct Workspace {
     DevBuf<double> history;
     // certified bounds for the Lloyd-round fast path of the screened assignment
     DevBuf<float> lb;        // R: lower bound (distance units) to every non-chosen centroid
-    DevBuf<double> drift2;   // k: squared centroid movement of the last update
+    DevBuf<double> drift_part;  // [n][k]: squared centroid movement of the last update, per d-slab
+    int drift_slabs = 0;        // d-slabs of the last update launch (host view at enqueue/capture time)
+    DevBuf<unsigned> slab_ctr, slab_done, slab_tot;  // [n], [n], [n][k]: fused update counters / label totals
     // K-means++ (init.cpp:123-201)
     DevBuf<double> d2pool;   // (ncand + 1) * R
     DevBuf<uint32_t> cand;   // ncand
@@ -205,17 +206,23 @@ struct Workspace {
         tiles = tiles_of(rows);
         hist_cap = hist;
         labels.alloc(2 * R);
-        dists.alloc(R);
+        dists.alloc(2 * R);  // [R, 2R): second slot of the fast-sum Lloyd control
         lb.alloc(R);
         tile_buf.alloc(tiles * ncand);
         tile_ctr.alloc(tiles);
         if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
         tiles_done.alloc(1);
         BM_CUDA(cudaMemset(tiles_done.p, 0, sizeof(unsigned)));
-        psum.alloc(tiles * (uint64_t)k * n);
-        pcnt.alloc(tiles * (uint64_t)k);
+        psum.alloc((tiles + (tiles & 1)) * (uint64_t)k * n);
         C.alloc((uint64_t)k * n);
-        drift2.alloc(k);
+        drift_part.alloc((uint64_t)n * k * 8);  // [slabs x mergers][k], slabs x mergers <= n * 8
+        BM_CUDA(cudaMemset(drift_part.p, 0, (uint64_t)n * k * 8 * sizeof(double)));
+        slab_ctr.alloc(n);
+        BM_CUDA(cudaMemset(slab_ctr.p, 0, n * sizeof(unsigned)));
+        slab_done.alloc(n);
+        BM_CUDA(cudaMemset(slab_done.p, 0, n * sizeof(unsigned)));
+        slab_tot.alloc((uint64_t)n * k);
+        BM_CUDA(cudaMemset(slab_tot.p, 0, (uint64_t)n * k * sizeof(unsigned)));
         Cact.alloc((uint64_t)k * (n + (n & 1)));
         if (k <= dev::kSMaxK) {
             CT32.alloc((uint64_t)n * dev::kSMaxK);
@@ -225,6 +232,7 @@ struct Workspace {
         mask.alloc(k);
         act.alloc(k);
         status.alloc(1);
+        BM_CUDA(cudaMemset(status.p, 0, sizeof(dev::LloydStatus)));
         BM_CUDA(cudaMemset(status.p, 0, sizeof(dev::LloydStatus)));
         history.alloc(hist_cap);
         d2pool.alloc((uint64_t)(ncand + 1) * R);
@@ -252,7 +260,9 @@ struct SamplerWs {
     DevBuf<uint32_t> epoch;                           // [0] counter, [1+b] epoch of target buffer b
     cudaStream_t rng_stream = nullptr;                      // device draws of the next chunk
     cudaEvent_t drawn[2] = {nullptr, nullptr}, resolved[2] = {nullptr, nullptr};
-    DevBuf<Mt64State> mt;           // device-resident RNG stream (big_means chains)
+    DevBuf<Mt64State> mt;           // [0] device-resident RNG stream, [1+b] input state of the draw into buffer b
+    DevBuf<uint64_t> raw;           // untempered words of the current draw
+    DevBuf<int> mtflag;             // a draw may have been rejected (k_mt_fix redoes it)
     HostBuf<Mt64State> h_mt;
     HostBuf<uint32_t> h_js[2];
     cudaEvent_t js_done[2] = {nullptr, nullptr};
@@ -282,7 +292,9 @@ struct SamplerWs {
         BM_CUDA(cudaMemset(exclbits.p, 0, ceil_div(s, 32) * sizeof(uint32_t)));
         BM_CUDA(cudaMemset(epoch.p, 0, 3 * sizeof(uint32_t)));
         BM_CUDA(cudaMemset(bitmap.p, 0, nwords * sizeof(uint32_t)));
-        mt.alloc(1);
+        mt.alloc(3);
+        raw.alloc(s);
+        mtflag.alloc(1);
         h_mt.alloc(1);
         for (int b = 0; b < 2; ++b) {
             h_js[b].alloc(s);
@@ -573,7 +585,8 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
 void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_t* labels_pair,
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
                    const int* stop, bool final_pass = false, double* tile_out = nullptr,
-                   unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr, int hmode = 0) {
+                   unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr, int hmode = 0,
+                   uint64_t dstride = 0) {
     const dev::LloydCtl noctl{};
     bool fused_ctl = false;
     const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
@@ -591,12 +604,14 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                 attr_set = true;
             }
             const CUtensorMap tmx = points_map<T>(P);
-            fused_ctl = ctl && tile_out;
+            fused_ctl = ctl && (tile_out || ctl->fast);
             dev::k_assign_tma<T><<<grid, dev::kSThreads, shm, st>>>(
                 tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                 g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
-                hamerly_enabled() ? hmode : 0, w.lb.p, w.drift2.p, k);
+                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, w.lb.p, w.drift_part.p,
+                w.drift_slabs, k,
+                dstride);
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
             static bool attr_set = false;  // per template instance
@@ -645,35 +660,43 @@ void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_
     count_launch();
 }
 
+// update_centroids (core.cpp:183-244) in one launch: grid (tile, d-slab), the
+// slab's last CTA merges it.  Slabs split the dimensions so that the grid
+// covers the GPU when there are few tiles and the staged slab fits in shared memory.
 void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* parity, const int* stop) {
     PhaseScope ps(PH_UPDATE, P.rows);
     const int k = w.k, n = w.n;
     const uint64_t tiles = tiles_of(P.rows);
-    // d-slab so that the grid covers the GPU even when there are few tiles.
-    int slabs = 1;
-    while (tiles * slabs < 444 && n / (slabs * 2) >= 4) slabs *= 2;
-    const int dslab = (int)ceil_div(n, slabs);
-    dim3 grid((unsigned)tiles, (unsigned)ceil_div(n, dslab));
-    const size_t shm = kTile * sizeof(short) + (2 * k + dev::kUChunks * k) * sizeof(int);
+    if (tiles == 0) return;
+    const size_t es = dtype_size(P.dtype);
+    const int V = (int)(16 / es);  // staged rows are whole 16-byte vectors
+    const size_t base = ((size_t)(kTile / 2 + (2 + dev::kUWarps) * k) * 4 + 15) & ~size_t(15);
+    // about two CTAs per SM in one wave; the staged slab within ~100 KB of shared memory
+    int slabs = (int)std::max<uint64_t>(1, std::min<uint64_t>((296 + tiles / 2) / tiles, ceil_div(n, V)));
+    int dslab = (int)(ceil_div(ceil_div(n, slabs), V) * V);
+    while (dslab > V && base + (size_t)kTile * dslab * es > 100 * 1024) dslab -= V;
+    slabs = (int)ceil_div(n, dslab);
+    const uint64_t tstride = tiles + (tiles & 1);
+    const size_t merge_min = ((((size_t)2 * k * 4 + 15) & ~size_t(15)) + (size_t)k * dslab * 8 + 15) / 16 * 16 +
+                             (tstride + 1) * 8 * 16;  // at least 16 (dim, label) pairs per merge round
+    const size_t shm = std::max(base + (size_t)kTile * dslab * es, merge_min);
+    dim3 grid((unsigned)tiles, (unsigned)slabs);
+    // mergers per slab: about 48 (dim, label) pairs each
+    // (waiting mergers never exceed one per SM, so the CTAs they wait for always get a slot)
+    int G = (int)std::min<uint64_t>({tiles, (uint64_t)8, std::max<uint64_t>(1, ceil_div((uint64_t)k * dslab, 48))});
+    while (G > 1 && (uint64_t)G * slabs > 148) --G;
+    dev::UpdateArgs u{w.psum.p, tstride, shm, w.slab_ctr.p, w.slab_done.p, G, w.slab_tot.p, w.C.p, w.mask.p, w.Cact.p, w.ldc,
+                      w.act.p, &w.status.p->n_active, w.CT32.p, w.drift_part.p, &w.status.p->bad_label, stop};
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         if (shm > 48 * 1024)
-            BM_CUDA(cudaFuncSetAttribute(dev::k_update_partials<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)shm));
-        dev::k_update_partials<T><<<grid, dev::kUThreads, shm, st>>>(
-            static_cast<const T*>(P.X), P.rows, n, P.ld, w.labels.p, w.R, parity, k, dslab, w.psum.p,
-            w.pcnt.p, &w.status.p->bad_label, stop, w.drift2.p);
+            BM_CUDA(cudaFuncSetAttribute(dev::k_update<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        dev::k_update<T><<<grid, dev::kUThreads, shm, st>>>(static_cast<const T*>(P.X), P.rows, n, P.ld,
+                                                             w.labels.p, w.R, parity, k, dslab, u);
     });
     BM_LAUNCH();
-    const unsigned mgrid = (unsigned)ceil_div((uint64_t)k * n, dev::kMThreads);
-    const size_t mshm = k * (sizeof(unsigned long long) + sizeof(int));
-    if (mshm > 48 * 1024)
-        BM_CUDA(cudaFuncSetAttribute(dev::k_update_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mshm));
-    dev::k_update_merge<<<mgrid, dev::kMThreads, mshm, st>>>(w.psum.p, w.pcnt.p, tiles, k, n, w.C.p, w.mask.p,
-                                                            w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active,
-                                                            w.CT32.p, stop, w.drift2.p);
-    BM_LAUNCH();
-    count_launch(2);
+    count_launch(1);
+    w.drift_slabs = slabs * G;
 }
 
 // ---------------------------------------------------------------------------
@@ -688,9 +711,19 @@ struct LloydResult {
     int parity;
 };
 
+// BM_FORCE_EXACT_CONTROL=1: every fast-sum stop test takes the exact path (test hook).
+bool force_exact_control() {
+    static const bool on = std::getenv("BM_FORCE_EXACT_CONTROL") != nullptr;
+    return on;
+}
+
 dev::LloydCtl make_ctl(Workspace& w, int mode, uint64_t rows, uint64_t max_it = 0, double tol = 0.0,
-                       cudaGraphConditionalHandle cond = 0, int use_cond = 0) {
+                       cudaGraphConditionalHandle cond = 0, int use_cond = 0, bool fast = false) {
     dev::LloydCtl c{};
+    c.fast = fast ? 1 : 0;
+    c.force_exact = force_exact_control() ? 1 : 0;
+    c.dists_pair = w.dists.p;
+    c.dstride = w.R;
     c.mode = mode;
     c.st = w.status.p;
     c.tiles_done = w.tiles_done.p;
@@ -705,22 +738,24 @@ dev::LloydCtl make_ctl(Workspace& w, int mode, uint64_t rows, uint64_t max_it = 
 
 // compact (unless the compacted start is already in place) + assign (:26) +
 // begin (:27-28), the latter fused into the assignment where possible.
-void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do_compact = true) {
+void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do_compact = true,
+                         bool fast = false, const int* go = nullptr) {
     if (do_compact) launch_compact(st, w, w.C.p, w.mask.p);
-    const dev::LloydCtl ctl = make_ctl(w, 1, P.rows);
+    dev::LloydCtl ctl = make_ctl(w, 1, P.rows, 0, 0.0, 0, 0, fast);
+    ctl.go = go;
     launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr, false,
-                  w.tile_buf.p, w.tile_ctr.p, &ctl, 1);
+                  fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1);
 }
 
 // update (:33) + assign (:34-35) + step (:36-51), the step fused into the assignment.
 void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol,
-                         cudaGraphConditionalHandle cond = 0, int use_cond = 0) {
+                         cudaGraphConditionalHandle cond = 0, int use_cond = 0, bool fast = false) {
     const int* parity = &w.status.p->parity;
     const int* stop = &w.status.p->stop;
     launch_update(st, P, w, parity, stop);
-    const dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond);
+    const dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond, fast);
     launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop, false,
-                  w.tile_buf.p, w.tile_ctr.p, &ctl, 2);
+                  fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 2, fast ? w.R : 0);
 }
 
 // Runs the loop to completion; `between` is called once after the first
@@ -913,12 +948,17 @@ uint32_t* draw_targets(SamplerWs& sw, Mt64& rng) {
     return out;
 }
 
-// Device-side draws (k_mt_draw) from the device-resident stream into target buffer b.
+// Device-side draws (k_mt_twist, k_mt_emit, k_mt_fix) from the device-resident stream into target buffer b.
 void enqueue_device_draw(cudaStream_t st, SamplerWs& sw, int force_seq = 0, int b = 0) {
-    dev::k_mt_draw<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.m, (uint32_t)sw.s, sw.jsbuf(b), nullptr, force_seq,
-                                                  sw.epoch.p, sw.epoch_slot(b));
+    const uint32_t s = (uint32_t)sw.s;
+    dev::k_mt_twist<<<1, dev::kMtThreads, 0, st>>>(sw.mt.p, sw.mt.p + 1 + b, s, sw.raw.p, sw.mtflag.p);
     BM_LAUNCH();
-    count_launch();
+    dev::k_mt_emit<<<(unsigned)ceil_div(s, 256), 256, 0, st>>>(sw.raw.p, sw.m, s, sw.jsbuf(b), sw.mtflag.p);
+    BM_LAUNCH();
+    dev::k_mt_fix<<<1, 32, 0, st>>>(sw.mt.p, sw.mt.p + 1 + b, sw.m, s, sw.jsbuf(b), sw.mtflag.p, force_seq,
+                                     sw.epoch.p, sw.epoch_slot(b));
+    BM_LAUNCH();
+    count_launch(3);
 }
 
 void put_stream(cudaStream_t st, SamplerWs& sw, const Mt64& rng) {
@@ -927,8 +967,9 @@ void put_stream(cudaStream_t st, SamplerWs& sw, const Mt64& rng) {
     BM_CUDA(cudaStreamSynchronize(st));
 }
 
-void get_stream(cudaStream_t st, SamplerWs& sw, Mt64& rng) {
-    BM_CUDA(cudaMemcpyAsync(sw.h_mt.p, sw.mt.p, sizeof(Mt64State), cudaMemcpyDeviceToHost, st));
+// slot 0: the live stream; 1 + b: the input state of the last draw into buffer b
+void get_stream(cudaStream_t st, SamplerWs& sw, Mt64& rng, int slot = 0) {
+    BM_CUDA(cudaMemcpyAsync(sw.h_mt.p, sw.mt.p + slot, sizeof(Mt64State), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaStreamSynchronize(st));
     rng.s = *sw.h_mt.p;
 }
@@ -1024,11 +1065,16 @@ bool graphs_enabled() {
     return on;
 }
 
-void enqueue_accept(cudaStream_t st, Workspace& w) {
+// fast: the Lloyd loop ran the fast-sum control, so the accept first computes
+// the exact objective of the final assignment (one CTA per 1024-row tile).
+void enqueue_accept(cudaStream_t st, Workspace& w, bool fast = false, const int* go = nullptr,
+                    dev::LloydStatus* host_st = nullptr) {
     PhaseScope ps(PH_CONTROL, 0);
-    dev::k_accept<<<1, 256, w.k * sizeof(int), st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p,
-                                                     w.maskinc.p, w.k, w.n, w.drec.p, w.chunk_ctr.p, w.Cact.p,
-                                                     w.ldc, w.act.p, w.CT32.p);
+    const unsigned grid = fast ? (unsigned)tiles_of(w.R) : 1u;
+    dev::k_accept<<<grid, 256, w.k * sizeof(int), st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p,
+                                                        w.maskinc.p, w.k, w.n, w.drec.p, w.chunk_ctr.p, w.Cact.p,
+                                                        w.ldc, w.act.p, w.CT32.p, fast ? w.dists.p : nullptr, w.R,
+                                                        w.R, w.tile_buf.p, w.tiles_done.p, go, host_st);
     BM_LAUNCH();
     count_launch();
 }
@@ -1075,7 +1121,38 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
     if (!w.cap1) BM_CUDA(cudaStreamCreateWithFlags(&w.cap1, cudaStreamNonBlocking));
     if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    {  // the guard sets the IF condition inside the graph that owns it
+    // fast-sum control whenever the TMA screen (which implements it) runs
+    const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
+    if (fast) {
+        // begin -> round 1 -> WHILE { round } -> accept, no IF: every kernel of
+        // a skipped chunk (st->go == 0) returns at once (the begin and the
+        // accept test go; the rounds see the previous loop's stop), and round
+        // 1's control opens the WHILE node (default closed).
+        const int* go = &w.status.p->go;
+        lloyd_enqueue_begin(st, P, w, /*do_compact=*/false, true, go);
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr));
+        cudaGraphConditionalHandle hw;
+        BM_CUDA(cudaGraphConditionalHandleCreate(&hw, cg, 0, cudaGraphCondAssignDefault));
+        lloyd_enqueue_round(st, P, w, max_it, tol, hw, 1, true);
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
+        cudaGraphNodeParams prm = {};
+        prm.type = cudaGraphNodeTypeConditional;
+        prm.conditional.handle = hw;
+        prm.conditional.type = cudaGraphCondTypeWhile;
+        prm.conditional.size = 1;
+        cudaGraphNode_t cn;
+        BM_CUDA(cudaGraphAddNode(&cn, cg, deps, nd, &prm));
+        BM_CUDA(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
+        cudaGraph_t wbody = prm.conditional.phGraph_out[0];
+        BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1, true);
+        BM_CUDA(cudaStreamEndCapture(w.cap2, &wbody));
+        enqueue_accept(st, w, true, go, w.h_status.p + b);
+    } else {  // the guard sets the IF condition inside the graph that owns it
         cudaStreamCaptureStatus cs;
         cudaGraph_t cg = nullptr;
         BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr));
@@ -1096,17 +1173,17 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
         BM_CUDA(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
         cudaGraph_t ifbody = prm.conditional.phGraph_out[0];
         BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap1, ifbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        lloyd_enqueue_begin(w.cap1, P, w, /*do_compact=*/false);  // accept (or the repair) compacted the start
+        lloyd_enqueue_begin(w.cap1, P, w, /*do_compact=*/false, false);  // accept (or the repair) compacted the start
         cudaGraphConditionalHandle hw;
         cudaGraph_t wbody = nullptr;
         add_conditional(w.cap1, &hw, &wbody, cudaGraphCondTypeWhile, 1);
         BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1);
+        lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1, false);
         BM_CUDA(cudaStreamEndCapture(w.cap2, &wbody));
-        enqueue_accept(w.cap1, w);
+        enqueue_accept(w.cap1, w, false);
         BM_CUDA(cudaStreamEndCapture(w.cap1, &ifbody));
+        BM_CUDA(cudaMemcpyAsync(w.h_status.p + b, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
     }
-    BM_CUDA(cudaMemcpyAsync(w.h_status.p + b, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
     cudaGraph_t g = nullptr;
     BM_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t e = nullptr;
@@ -1186,43 +1263,51 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             if (!w.ev_lloyd[b]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd[b], cudaEventDisableTiming));
             if (!w.ev_prep[b]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_prep[b], cudaEventDisableTiming));
         }
-        const cudaStream_t pst = dc.pstream;
+        // BM_PIPE=0: preps on the Lloyd stream (no overlap; timeline diagnostics)
+        static const bool pipe = !(std::getenv("BM_PIPE") && std::string(std::getenv("BM_PIPE")) == "0");
+        const cudaStream_t pst = pipe ? dc.pstream : st;
         Points bufP[2] = {chunkP, chunkP};
         bufP[1].X = dc.chunk1.p;
         // BM_TIMELINE=1: in-stream events after every Lloyd graph (GPU time per chunk incl. gaps)
         static const bool timeline = std::getenv("BM_TIMELINE") != nullptr;
-        std::vector<cudaEvent_t> tl_ev;
-        auto tl_mark = [&] {
-            if (!timeline) return;
-            cudaEvent_t e;
-            BM_CUDA(cudaEventCreate(&e));
-            BM_CUDA(cudaEventRecord(e, st));
-            tl_ev.push_back(e);
+        // per graph launch: (kind 0 = prep / 1 = Lloyd, start event, end event)
+        struct TlRec { int kind; cudaEvent_t a, b; };
+        std::vector<TlRec> tl;
+        auto tl_ev = [&](cudaStream_t q) {
+            cudaEvent_t e = nullptr;
+            if (timeline) {
+                BM_CUDA(cudaEventCreate(&e));
+                BM_CUDA(cudaEventRecord(e, q));
+            }
+            return e;
         };
         // a chunk's prep: draws on rng_stream are already enqueued (drawn[b])
         auto launch_prep = [&](int b) {
             BM_CUDA(cudaStreamWaitEvent(pst, sw->drawn[b], 0));
             BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[b], 0));  // buffer b's previous reader
+            cudaEvent_t e0 = tl_ev(pst);
             BM_CUDA(cudaGraphLaunch(w.g_prep[b], pst));
+            if (timeline) tl.push_back({0, e0, tl_ev(pst)});
             BM_CUDA(cudaEventRecord(w.ev_prep[b], pst));
             count_launch(6);
         };
         auto launch_lloyd = [&](int b) {
             BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[b], 0));
+            cudaEvent_t e0 = tl_ev(st);
             BM_CUDA(cudaGraphLaunch(w.g_lloyd[b], st));
+            if (timeline) tl.push_back({1, e0, tl_ev(st)});
             BM_CUDA(cudaEventRecord(w.ev_lloyd[b], st));
-            tl_mark();
         };
         // speculation needs the chunk count to be known in advance (no time budget)
         const bool speculate = !cfg.has_max_cpu_seconds;
         auto exists = [&](uint64_t c) { return !cfg.has_max_chunks || c < cfg.max_chunks; };
-        tl_mark();
         BM_CUDA(cudaEventRecord(w.ev_lloyd[0], st));
         BM_CUDA(cudaEventRecord(w.ev_lloyd[1], st));
         enqueue_device_draw(sw->rng_stream, *sw, 0, 0);
         BM_CUDA(cudaEventRecord(sw->drawn[0], sw->rng_stream));
         launch_prep(0);
-        bool queued = false;  // chunk `chunk`'s Lloyd graph is already queued (guarded)
+        bool queued = false;     // chunk `chunk`'s Lloyd graph is already queued (guarded)
+        bool spec_next = false;  // chunk+1's draws are already enqueued (speculatively)
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
             if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
@@ -1246,21 +1331,31 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 BM_CUDA(cudaStreamSynchronize(st));
                 std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
                 BM_CUDA(cudaStreamSynchronize(sw->rng_stream));
-                get_stream(st, *sw, rng);
+                // the stream right after this chunk's draws: live, or the input
+                // state of chunk+1's speculative draws (which are discarded)
+                get_stream(st, *sw, rng, spec_next ? 1 + (b ^ 1) : 0);
                 kmeanspp_fill_device(st, bufP[b], w, hmask, cfg.candidates_per_step, rng, evals);
                 put_stream(st, *sw, rng);
                 launch_compact(st, w, w.C.p, w.mask.p);  // the Lloyd graph starts from Cact
                 BM_CUDA(cudaMemsetAsync(&w.status.p->go, 0x01, sizeof(int), st));
                 queued = false;
+                spec_next = false;
             }
             const bool next = exists(chunk + 1);
-            if (next) {  // chunk+1's draws: the stream is past this chunk's repair
+            if (next && !spec_next) {  // chunk+1's draws: the stream is past this chunk's repair
                 if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[b ^ 1], 0));
                 enqueue_device_draw(sw->rng_stream, *sw, 0, b ^ 1);
                 BM_CUDA(cudaEventRecord(sw->drawn[b ^ 1], sw->rng_stream));
             }
             if (!queued) launch_lloyd(b);
             if (next) launch_prep(b ^ 1);
+            // chunk+2's draws, assuming chunk+1 needs no repair (else redone above)
+            spec_next = next && speculate && exists(chunk + 2);
+            if (spec_next) {
+                BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[b], 0));  // chunk's resolution read buffer b
+                enqueue_device_draw(sw->rng_stream, *sw, 0, b);
+                BM_CUDA(cudaEventRecord(sw->drawn[b], sw->rng_stream));
+            }
             queued = next && speculate;
             if (queued) launch_lloyd(b ^ 1);  // runs iff this chunk's accept needs no repair
             BM_CUDA(cudaEventSynchronize(w.ev_lloyd[b]));
@@ -1275,12 +1370,37 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         }
         BM_CUDA(cudaStreamSynchronize(st));
         BM_CUDA(cudaStreamSynchronize(pst));
-        if (timeline && tl_ev.size() > 1) {
+        if (timeline && tl.size() > 2) {
+            double dur[2] = {0, 0}, gap = 0;
+            int cnt[2] = {0, 0}, ngap = 0;
+            cudaEvent_t prev_end = nullptr, first = nullptr, last = nullptr;
+            for (auto& r : tl) {
+                float ms = 0;
+                BM_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+                dur[r.kind] += ms;
+                cnt[r.kind] += 1;
+                if (r.kind == 1) {
+                    if (prev_end) {
+                        BM_CUDA(cudaEventElapsedTime(&ms, prev_end, r.a));
+                        gap += ms;
+                        ++ngap;
+                    }
+                    prev_end = r.b;
+                    if (!first) first = r.a;
+                    last = r.b;
+                }
+            }
             float total = 0;
-            BM_CUDA(cudaEventElapsedTime(&total, tl_ev.front(), tl_ev.back()));
-            std::fprintf(stderr, "[timeline] total %.3f ms | %zu Lloyd graphs | %.1f us per chunk\n", total,
-                         tl_ev.size() - 1, 1e3 * total / (tl_ev.size() - 1));
-            for (auto e : tl_ev) cudaEventDestroy(e);
+            BM_CUDA(cudaEventElapsedTime(&total, first, last));
+            std::fprintf(stderr,
+                         "[timeline] %.3f ms over %d Lloyd graphs: %.1f us per chunk | Lloyd graph %.1f us | gap "
+                         "before the next %.1f us | prep graph %.1f us (%d)\n",
+                         total, cnt[1], 1e3 * total / cnt[1], 1e3 * dur[1] / cnt[1], ngap ? 1e3 * gap / ngap : 0.0,
+                         cnt[0] ? 1e3 * dur[0] / cnt[0] : 0.0, cnt[0]);
+            for (auto& r : tl) {
+                cudaEventDestroy(r.a);
+                cudaEventDestroy(r.b);
+            }
         }
     } else {  // host-driven chunk loop (profiling, BM_GRAPHS=0, s == m)
     bool drawn_ahead = false;  // next chunk's targets already being drawn on rng_stream

@@ -38,7 +38,15 @@ struct LloydStatus {
     int inc_degenerate;  // degenerate rows of the incumbent after the accept step
     int bad_label;       // update saw a label outside [0,k) (core.cpp:189-193)
     int go;              // the next chunk starts from the incumbent as is (no repair, :83-85)
+    // fast-sum control (graph mode): the stop test runs on certified intervals
+    // of the objectives, the exact block_sum only when the interval test cannot
+    // decide (and for the final objective, in k_accept)
+    double f_lo, f_hi;   // interval of the exact f around the fast sum kept in `f`
+    double fsum;         // accumulator of the current launch's CTA distance sums
+    unsigned ctas_done;  // CTAs of the current launch that have added their sum
+    int exact_checks;    // decisions that needed the exact sums (diagnostics)
 };
+static_assert(sizeof(LloydStatus) % 8 == 0, "status is copied as 8-byte words");
 
 // Per-chunk accept record (ChunkRecord big_means.hpp:28-34).
 struct Record {
@@ -62,8 +70,41 @@ __device__ __forceinline__ void ktrace(int slot) {
         row[slot] = t;
     }
 }
+// region 1: k_update CTAs (linear block id)
+__device__ __forceinline__ void ktrace_u(int slot) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const unsigned id = (blockIdx.y * gridDim.x + blockIdx.x) & 2047;
+        unsigned long long* row = g_ktrace + 65536 + id * 32;
+        if (slot == 0)
+            for (int i = 1; i < 32; ++i) row[i] = 0;
+        row[slot] = t;
+    }
+}
+// region 2 (index 200000): kernel log.  klog_start by CTA (0,0), klog_end by
+// the launch's last CTA: [200000] = count, then (id, start, end) triples.
+__device__ unsigned long long g_kstart[32];
+__device__ __forceinline__ void klog_start(int id) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_kstart[id] = t;
+    }
+}
+__device__ __forceinline__ void klog_end(int id) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long i = atomicAdd(&g_ktrace[200000], 1ull) % 60000ull;
+    g_ktrace[200001 + 3 * i] = static_cast<unsigned long long>(id);
+    g_ktrace[200002 + 3 * i] = g_kstart[id];
+    g_ktrace[200003 + 3 * i] = t;
+}
 #else
 __device__ __forceinline__ void ktrace(int) {}
+__device__ __forceinline__ void ktrace_u(int) {}
+__device__ __forceinline__ void klog_start(int) {}
+__device__ __forceinline__ void klog_end(int) {}
 #endif
 
 // Exact promotion of the storage type (P11).
@@ -261,12 +302,11 @@ __global__ void k_epoch_bump(uint32_t* counter, uint32_t* slot) {
 }
 
 // The s raw targets j_i = uniform_int(i, m-1) (big_means.cpp:49-51) drawn on
-// the device from the device-resident std::mt19937_64 state: one CTA, the
-// twist in two data-parallel halves, the tempering and Lemire's
-// multiply-shift per output in parallel.  A Lemire rejection (probability
-// < 2^-32 per draw for m < 2^32) shifts every later draw; it is detected and
-// the whole draw is redone sequentially from the saved state by thread 0 with
-// the exact rejection loop (also forced by `force_seq` in tests).
+// the device from the device-resident std::mt19937_64 state.  A Lemire
+// rejection (probability < 2^-32 per draw for m < 2^32) shifts every later
+// draw; a possible one is detected and the whole draw is redone sequentially
+// from the saved state with the exact rejection loop (also forced by
+// `force_seq` in tests).
 constexpr int kMtThreads = 320;
 
 __device__ uint64_t mt_next_seq(uint64_t* x, int& pos) {
@@ -277,74 +317,101 @@ __device__ uint64_t mt_next_seq(uint64_t* x, int& pos) {
     return mt_temper(x[pos++]);
 }
 
+// Draw = k_mt_twist (one CTA: the state recurrence, words stored untempered
+// in consumption order) + k_mt_emit (all SMs: tempering and Lemire's
+// multiply-shift per draw) + k_mt_fix (one thread: the exact sequential redo
+// if any draw may have been rejected, or when forced).  The twist is the
+// in-place recurrence x[i] = mix(x[i], x[i+1], x[i+156]) with x[j<i] already
+// new; double-buffered (A -> B) it is two data-parallel halves per 312 words.
+// `snap` receives the input state (host repairs after a speculative draw
+// restart from it).
 __global__ void __launch_bounds__(kMtThreads)
-k_mt_draw(Mt64State* __restrict__ st, uint64_t m, uint32_t s, uint32_t* __restrict__ js,
-          const int* __restrict__ skip, int force_seq, uint32_t* __restrict__ epoch_counter,
-          uint32_t* __restrict__ epoch_slot) {
-    __shared__ uint64_t x[kMtN];
-    __shared__ uint64_t x0[kMtN];  // state before the draw (sequential fallback)
-    __shared__ int reject;
-    if (skip && *skip) return;
+k_mt_twist(Mt64State* __restrict__ st, Mt64State* __restrict__ snap, uint32_t s, uint64_t* __restrict__ raw,
+           int* __restrict__ flag) {
+    __shared__ uint64_t xa[kMtN], xb[kMtN];
     const int tid = threadIdx.x;
-    for (int i = tid; i < kMtN; i += blockDim.x) x[i] = x0[i] = st->x[i];
+    for (int i = tid; i < kMtN; i += blockDim.x) {
+        const uint64_t v = st->x[i];
+        xa[i] = v;
+        snap->x[i] = v;
+    }
     int pos = static_cast<int>(st->pos);
-    const int pos0 = pos;
-    if (tid == 0) reject = 0;
+    if (tid == 0) {
+        snap->pos = static_cast<uint64_t>(pos);
+        *flag = 0;
+    }
     __syncthreads();
-    for (uint32_t base = 0; base < s;) {
-        if (pos >= kMtN) {
-            uint64_t v = 0;
-            if (tid < kMtM) v = mt_mix(x[tid], x[tid + 1], x[tid + kMtM]);
-            __syncthreads();
-            if (tid < kMtM) x[tid] = v;
-            __syncthreads();
-            if (tid >= kMtM && tid < kMtN) v = mt_mix(x[tid], x[(tid + 1) % kMtN], x[tid - kMtM]);
-            __syncthreads();
-            if (tid >= kMtM && tid < kMtN) x[tid] = v;
-            __syncthreads();
-            pos = 0;
+    uint64_t* A = xa;
+    uint64_t* B = xb;
+    uint32_t base = 0;
+    if (pos < kMtN) {  // rest of the current block
+        const uint32_t take = min(static_cast<uint32_t>(kMtN - pos), s);
+        if (tid < static_cast<int>(take)) raw[tid] = A[pos + tid];
+        pos += static_cast<int>(take);
+        base = take;
+    }
+    while (base < s) {
+        if (tid < kMtM) {
+            const uint64_t v = mt_mix(A[tid], A[tid + 1], A[tid + kMtM]);
+            B[tid] = v;
+            if (base + tid < s) raw[base + tid] = v;
         }
-        const uint32_t take = min(static_cast<uint32_t>(kMtN - pos), s - base);
-        if (tid < static_cast<int>(take)) {
-            const uint64_t y = mt_temper(x[pos + tid]);
-            const uint64_t i = base + tid;
+        __syncthreads();
+        if (tid >= kMtM && tid < kMtN) {
+            const uint64_t v = mt_mix(A[tid], tid + 1 < kMtN ? A[tid + 1] : B[0], B[tid - kMtM]);
+            B[tid] = v;
+            if (base + tid < s) raw[base + tid] = v;
+        }
+        __syncthreads();
+        uint64_t* t = A;
+        A = B;
+        B = t;
+        const uint32_t take = min(static_cast<uint32_t>(kMtN), s - base);
+        pos = static_cast<int>(take);
+        base += take;
+    }
+    for (int i = tid; i < kMtN; i += blockDim.x) st->x[i] = A[i];
+    if (tid == 0) st->pos = static_cast<uint64_t>(pos);
+}
+
+// j_i = uniform_int(i, m-1) from raw word i (Lemire, uniform_int_dist.h:252-331).
+// low < r is necessary for a rejection (threshold (2^64-r) mod r < r); k_mt_fix
+// applies the exact test sequentially when any draw sees it.
+__global__ void k_mt_emit(const uint64_t* __restrict__ raw, uint64_t m, uint32_t s, uint32_t* __restrict__ js,
+                          int* __restrict__ flag) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= s) return;
+    const uint64_t y = mt_temper(raw[i]);
+    const uint64_t r = m - i;
+    if (y * r < r) *flag = 1;
+    js[i] = static_cast<uint32_t>(i + mul_hi64(y, r));
+}
+
+__global__ void k_mt_fix(Mt64State* __restrict__ st, const Mt64State* __restrict__ snap, uint64_t m, uint32_t s,
+                         uint32_t* __restrict__ js, const int* __restrict__ flag, int force_seq,
+                         uint32_t* __restrict__ epoch_counter, uint32_t* __restrict__ epoch_slot) {
+    __shared__ uint64_t x[kMtN];
+    if (threadIdx.x != 0) return;
+    if (*flag || force_seq) {  // exact sequential redo from the input state
+        for (int i = 0; i < kMtN; ++i) x[i] = snap->x[i];
+        int p = static_cast<int>(snap->pos);
+        for (uint32_t i = 0; i < s; ++i) {
             const uint64_t r = m - i;
-            const uint64_t low = y * r;
-            if (low < r && low < (0 - r) % r) reject = 1;
+            uint64_t y = mt_next_seq(x, p);
+            uint64_t low = y * r;
+            if (low < r) {
+                const uint64_t thr = (0 - r) % r;
+                while (low < thr) {
+                    y = mt_next_seq(x, p);
+                    low = y * r;
+                }
+            }
             js[i] = static_cast<uint32_t>(i + mul_hi64(y, r));
         }
-        pos += take;
-        base += take;
-        __syncthreads();
+        for (int i = 0; i < kMtN; ++i) st->x[i] = x[i];
+        st->pos = static_cast<uint64_t>(p);
     }
-    if (reject || force_seq) {  // exact sequential redo from the saved state
-        if (tid == 0) {
-            int p = pos0;
-            for (int i = 0; i < kMtN; ++i) x[i] = x0[i];
-            for (uint32_t i = 0; i < s; ++i) {
-                const uint64_t r = m - i;
-                uint64_t y = mt_next_seq(x, p);
-                uint64_t low = y * r;
-                if (low < r) {
-                    const uint64_t thr = (0 - r) % r;
-                    while (low < thr) {
-                        y = mt_next_seq(x, p);
-                        low = y * r;
-                    }
-                }
-                js[i] = static_cast<uint32_t>(i + mul_hi64(y, r));
-            }
-            pos = p;
-            reject = p;  // broadcast the final position
-        }
-        __syncthreads();
-        pos = reject;
-    }
-    for (int i = tid; i < kMtN; i += blockDim.x) st->x[i] = x[i];
-    if (tid == 0) {
-        st->pos = static_cast<uint64_t>(pos);
-        *epoch_slot = ++(*epoch_counter);  // tags the resolution tables of these targets
-    }
+    *epoch_slot = ++(*epoch_counter);  // tags the resolution tables of these targets
 }
 
 // ===========================================================================
@@ -364,8 +431,34 @@ __global__ void k_gather(const uint4* __restrict__ X, uint64_t row_vecs, const u
 // Ordered fold of tile partials (block_sum outer loop core.cpp:172).
 __device__ __forceinline__ double fold_tiles(const double* tiles, uint64_t ntiles) {
     double total = 0.0;
-    for (uint64_t t = 0; t < ntiles; ++t) total = __dadd_rn(total, __ldcg(tiles + t));  // written by other CTAs
+    uint64_t t = 0;
+    for (; t + 8 <= ntiles; t += 8) {  // loads issued ahead of the dependent adds
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = __ldcg(tiles + t + r);  // written by other CTAs
+#pragma unroll
+        for (int r = 0; r < 8; ++r) total = __dadd_rn(total, v[r]);
+    }
+    for (; t < ntiles; ++t) total = __dadd_rn(total, __ldcg(tiles + t));
     return total;
+}
+
+// Left fold from 0.0 of a 16-byte aligned shared-memory array (one thread).
+__device__ __forceinline__ double seq_fold_smem(const double* v, int len) {
+    double a = 0.0;
+    int i = 0;
+    for (; i + 8 <= len; i += 8) {
+        const double2 v0 = *reinterpret_cast<const double2*>(v + i);
+        const double2 v1 = *reinterpret_cast<const double2*>(v + i + 2);
+        const double2 v2 = *reinterpret_cast<const double2*>(v + i + 4);
+        const double2 v3 = *reinterpret_cast<const double2*>(v + i + 6);
+        a = __dadd_rn(a, v0.x); a = __dadd_rn(a, v0.y);
+        a = __dadd_rn(a, v1.x); a = __dadd_rn(a, v1.y);
+        a = __dadd_rn(a, v2.x); a = __dadd_rn(a, v2.y);
+        a = __dadd_rn(a, v3.x); a = __dadd_rn(a, v3.y);
+    }
+    for (; i < len; ++i) a = __dadd_rn(a, v[i]);
+    return a;
 }
 
 // ===========================================================================
@@ -436,7 +529,105 @@ struct LloydCtl {
     double* history;
     cudaGraphConditionalHandle cond;
     int use_cond;
+    int fast;               // fast-sum control (no history; objective computed by k_accept)
+    int force_exact;        // test hook: every fast-sum decision takes the exact path
+    const double* dists_pair;  // distances of the last two assignments (slot = labels slot)
+    uint64_t dstride;
+    const int* go;          // when set and *go == 0 the launch does nothing (skipped chunk)
 };
+
+// block_sum (core.cpp:165-175) by one thread: ordered tile folds, ordered fold of the tiles.
+__device__ __noinline__ double exact_block_sum(const double* v, uint64_t count) {
+    double total = 0.0;
+    for (uint64_t t0 = 0; t0 < count; t0 += kTile) {
+        const uint64_t e = min(count, t0 + kTile);
+        double a = 0.0;
+        for (uint64_t i = t0; i < e; ++i) a = __dadd_rn(a, __ldcg(v + i));
+        total = __dadd_rn(total, a);
+    }
+    return total;
+}
+
+// Certified interval of the exact blocked sum around an unordered sum `s` of
+// the same nonnegative terms: both differ from the real sum by at most
+// gamma_(additions on the longest path) times that sum.
+__device__ __forceinline__ void sum_interval(double s, uint64_t rows, unsigned ctas, double* lo, double* hi) {
+    const double adds = static_cast<double>(tiles_of(rows) + ctas + kTile + 16);
+    const double rel = __dmul_ru(adds, 0x1.02p-53);  // (1 - n u)^-1 <= 1.01 for n u < 0.01
+    const double e = __dadd_ru(__dmul_ru(s, rel), 0x1p-1000);
+    *lo = __dsub_rd(s, e);
+    *hi = __dadd_ru(s, e);
+}
+
+// Fast-sum Lloyd control (thread 0 of the CTA that arrived last).
+__device__ __noinline__ void lloyd_fast_control(const LloydCtl& c, uint64_t rows, unsigned ctas) {
+    LloydStatus* st = c.st;
+    const double s = __ldcg(&st->fsum);
+    st->fsum = 0.0;
+    st->ctas_done = 0u;
+    double lo, hi;
+    sum_interval(s, rows, ctas, &lo, &hi);
+    const double nan = __longlong_as_double(0x7FF8000000000000LL);
+    if (c.mode == 1) {  // :26-28
+        st->f = s;
+        st->f_lo = lo;
+        st->f_hi = hi;
+        st->objective = nan;  // exact value: k_accept
+        st->evals = static_cast<unsigned long long>(rows) * st->n_active;
+        st->iterations = 0;
+        st->parity = 0;
+        st->stop = 0;
+        st->changed = 0;
+        st->state_error = st->n_active == 0;
+        st->bad_label = 0;
+        st->exact_checks = 0;
+        return;
+    }
+    if (!st->stop) {
+        st->evals += static_cast<unsigned long long>(rows) * st->n_active;
+        if (st->n_active == 0) st->state_error = 1;
+        st->iterations += 1;  // :36
+        st->objective = nan;
+        const bool unchanged = __ldcg(&st->changed) == 0;  // :39
+        st->changed = 0;
+        const int par = st->parity;
+        st->parity ^= 1;  // :40-41
+        bool stop = unchanged;  // :42-44
+        if (!stop) {
+            // f <= 0 (:45): terms are >= 0, so the exact f is 0 iff the fast sum is
+            if (st->f <= 0.0) {
+                stop = true;
+            } else if (c.rel_tolerance > 0.0) {  // :48-50 on intervals
+                const double flo = fmax(st->f_lo, 0x1p-1074), fhi = st->f_hi;
+                bool decided = !c.force_exact && isfinite(fhi) && isfinite(hi);
+                if (decided) {
+                    const double a_lo = __dsub_rn(flo, hi), a_hi = __dsub_rn(fhi, lo);
+                    const double g0 = __ddiv_rn(a_lo, flo), g1 = __ddiv_rn(a_lo, fhi);
+                    const double g2 = __ddiv_rn(a_hi, flo), g3 = __ddiv_rn(a_hi, fhi);
+                    const double gmin = fmin(fmin(g0, g1), fmin(g2, g3));
+                    const double gmax = fmax(fmax(g0, g1), fmax(g2, g3));
+                    if (gmax < c.rel_tolerance) stop = true;
+                    else if (!(gmin >= c.rel_tolerance)) decided = false;
+                }
+                if (!decided) {  // exact block sums of both assignments
+                    st->exact_checks += 1;
+                    const double f = exact_block_sum(c.dists_pair + par * c.dstride, rows);
+                    const double f_new = exact_block_sum(c.dists_pair + (1 - par) * c.dstride, rows);
+                    stop = __ddiv_rn(__dsub_rn(f, f_new), f) < c.rel_tolerance;
+                }
+            }
+        }
+        if (!stop) {  // :51
+            st->f = s;
+            st->f_lo = lo;
+            st->f_hi = hi;
+        }
+        if (st->iterations >= c.max_iterations) stop = true;  // :32
+        if (st->state_error || st->bad_label) stop = true;
+        st->stop = stop ? 1 : 0;
+    }
+    if (c.use_cond) cudaGraphSetConditional(c.cond, st->stop ? 0u : 1u);
+}
 
 // Called by thread 0 of the CTA that folded a tile: the CTA completing the last
 // tile runs the Lloyd control over all tile partials.
@@ -1178,14 +1369,17 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
              unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl,
-             int hmode, float* __restrict__ lb_r, const double* __restrict__ drift2, int kfull) {
+             int hmode, float* __restrict__ lb_r, const double* __restrict__ drift_part, int drift_slabs, int kfull,
+             uint64_t dstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
     unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     TmaSmem<T>& S = *reinterpret_cast<TmaSmem<T>*>(smem_al);
     constexpr unsigned kStageBytes = TmaSmem<T>::kRawBytes + kADC * kSMaxK * sizeof(float);
 
+    klog_start(10 + hmode);
     if (stop_ptr && *stop_ptr) return;
+    if (ctl.go && !*ctl.go) return;
     const int KA = *n_active_ptr;
     int32_t* labels_out = labels_pair;
     const int32_t* labels_old = nullptr;
@@ -1193,6 +1387,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         const int par = *parity_ptr;
         labels_out = labels_pair + (1 - par) * pair_stride;
         labels_old = labels_pair + par * pair_stride;
+        if (dists_out) dists_out += (1 - par) * dstride;  // dstride 0: one distance buffer
     }
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KG = (KA + kAK - 1) / kAK;
@@ -1222,14 +1417,19 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     int qb = 0;  // TMA slabs this CTA has consumed (ring position)
 
     // ---------------- Lloyd-round fast path (exact, certified) ----------------
-    if (hmode == 2 && labels_old && lb_r && drift2) {
+    if (hmode == 2 && labels_old && lb_r && drift_part) {
         if (tid < kSMaxK) S.rank_of[tid] = -1;
         if (tid == 0) S.nfail = 0;
         __syncthreads();
         if (tid < KA) S.rank_of[act_idx[tid]] = tid;
         if (tid == 32) {  // max drift of the active centroids since the bounds were taken
             double dm = 0.0;
-            for (int r = 0; r < KA; ++r) dm = fmax(dm, drift2[act_idx[r]]);
+            for (int r = 0; r < KA; ++r) {
+                const int j = act_idx[r];
+                double sj = 0.0;
+                for (int sl = 0; sl < drift_slabs; ++sl) sj += drift_part[sl * kfull + j];
+                dm = fmax(dm, sj);
+            }
             // sqrt of an upper bound, rounded up with margin (atomic fp64 sums: order-free bound)
             S.dmax = __double2float_ru(__dsqrt_ru(dm * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
         }
@@ -1270,6 +1470,13 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             atomicAdd(cand_counter, static_cast<unsigned long long>(np - nfail + nfail * KA));
             atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
         }
+#ifdef BM_KTRACE
+        if (tid == 0) {  // fast-path statistics: [199990] CTAs, [199991] fallbacks, [199992] failed points
+            atomicAdd(&g_ktrace[199990], 1ull);
+            if (nfail > kFailMax) atomicAdd(&g_ktrace[199991], 1ull);
+            atomicAdd(&g_ktrace[199992], static_cast<unsigned long long>(nfail));
+        }
+#endif
         if (nfail <= kFailMax) {
             // the few points whose bound failed: a warp scans all active centroids
             // exactly (lane j: centroid j), first minimum wins as in core.cpp:147
@@ -1555,6 +1762,28 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
 fold:
     ktrace(10);
+    if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
+        __syncthreads();  // distances of this CTA written (some by other threads)
+        double v = tid < np ? dists_out[p0 + tid] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+        double* wsum = reinterpret_cast<double*>(&S.red_u[0][0]);
+        if (lane == 0) wsum[warp] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double c = 0.0;
+            for (int w = 0; w < kSThreads / 32; ++w) c += wsum[w];
+            atomicAdd(&ctl.st->fsum, c);
+            __threadfence();
+            const unsigned done = atomicAdd(&ctl.st->ctas_done, 1u);
+            if (done == gridDim.x - 1) {
+                __threadfence();
+                lloyd_fast_control(ctl, rows, gridDim.x);
+                klog_end(10 + hmode);
+            }
+        }
+        return;
+    }
     if (!tile_out) return;
     __syncthreads();
     const uint64_t tile = p0 / kTile;
@@ -1633,191 +1862,267 @@ __global__ void k_tile_sums(const double* __restrict__ v, uint64_t count, uint64
 
 
 // ===========================================================================
-// 5. Centroid update (update_centroids core.cpp:183-244), bit-exact order.
+// 5. Centroid update (update_centroids core.cpp:183-244), bit-exact order,
+//    one kernel, grid (tile, d-slab).
 //
-// Phase A, grid (tile, d-slab): stable per-tile bucketing of points by label
-// (warp-synchronous, index order preserved), then one thread per
-// (label, dim) folds its members' coordinates in index order from 0.0 — the
-// reference's per-block partial row[d] += x[d] (:206-214).
-// Phase B: one thread per (label, dim) folds the non-empty tile partials in
-// tile order (:217-229; empty partials are +0.0 and adding +0.0 to a sum that
-// is never -0.0 is the identity, so they are skipped), then sum * (1.0/count)
-// (:237-239); count 0 -> degenerate row of 0.0 (:231 all_degenerate).
+// Per CTA: stable bucketing of the tile's points by label (warp-synchronous,
+// index order preserved); the tile's coordinate slab staged in shared memory
+// with coalesced loads; one thread per (label, dim) folds its members'
+// coordinates in index order from 0.0 — the reference's per-block partial
+// row[d] += x[d] (:206-214) — into psum (+0.0 when the label is absent).
+// The CTA that completes a slab (arrival counter) merges it: one thread per
+// (label, dim) folds the tile partials in tile order (:217-229; absent labels
+// add +0.0 to a sum that is never -0.0, the identity), then sum * (1.0/count)
+// (:237-239); count 0 -> degenerate row of 0.0 (:231 all_degenerate).  The
+// merge also writes the compacted centroids (Cact, CT32), the active list and
+// the squared movement per label of this slab (bounds of the next assignment).
 // ===========================================================================
 constexpr int kUThreads = 256;
+constexpr int kUWarps = kUThreads / 32;
 constexpr int kUChunks = kTile / 32;  // 32-point chunks per tile
 
-// Phase A: grid (tile, d-slab).  Stable bucketing: every warp ranks the points
-// of its 32-point chunks with __match_any_sync; a per-label exclusive prefix
-// over the chunks gives each (chunk, label) its base, so `order` lists each
-// label's members in index order.  Then one thread per (label, dim) folds its
-// members' coordinates from 0.0 in that order, with the member loads issued
-// in independent batches ahead of the dependent adds.
+struct UpdateArgs {
+    double* psum;            // [n][k][tstride]: tile partials, contiguous per (dim, label)
+    uint64_t tstride;        // tiles rounded up to even
+    uint64_t shm_bytes;      // dynamic shared memory of the launch (the merge streams partials through it)
+    unsigned* slab_ctr;      // [slabs] arrival counters (reset by the last merger)
+    unsigned* slab_done;     // [slabs] mergers finished
+    int mergers;             // G: CTAs merging each slab
+    unsigned* slab_tot;      // [slabs][k] label totals (reset by the merging CTA)
+    double* C;               // [k][n]
+    uint8_t* mask;
+    double* Cact;
+    int ldc;
+    int* act_idx;
+    int* n_active;
+    float* CT32;
+    double* drift_part;      // [slabs][k] squared movement of this slab's dims
+    int* bad_label;
+    const int* stop;
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kUThreads)
-k_update_partials(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
-                  const int32_t* __restrict__ labels_pair, uint64_t pair_stride,
-                  const int* __restrict__ parity_ptr, int k, int dslab,
-                  double* __restrict__ psum, uint32_t* __restrict__ pcnt, int* __restrict__ bad_label,
-                  const int* __restrict__ stop_ptr, double* __restrict__ drift2) {
-    if (stop_ptr && *stop_ptr) return;
-    if (drift2 && blockIdx.x == 0 && blockIdx.y == 0)  // zeroed for k_update_merge
-        for (int j = threadIdx.x; j < k; j += blockDim.x) drift2[j] = 0.0;
-    extern __shared__ int ush[];
+k_update(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+         const int32_t* __restrict__ labels_pair, uint64_t pair_stride,
+         const int* __restrict__ parity_ptr, int k, int dslab, UpdateArgs u) {
+    klog_start(2);
+    if (u.stop && *u.stop) return;
+    extern __shared__ __align__(16) unsigned char ush_raw[];
+    ktrace_u(0);
+    int* ush = reinterpret_cast<int*>(ush_raw);
     short* order = reinterpret_cast<short*>(ush);      // [kTile]
     int* cnt = ush + kTile / 2;                         // [k] tile totals
     int* off = cnt + k;                                 // [k] label offsets in `order`
-    int* ccount = off + k;                              // [kUChunks][k] per-chunk counts -> bases
+    int* wcount = off + k;                              // [warps][k] per-warp counts -> bases
+    T* xs = reinterpret_cast<T*>(ush_raw + ((static_cast<size_t>(kTile / 2 + (2 + kUWarps) * k) * 4 + 15) & ~size_t(15)));
 
     const int32_t* labels = labels_pair + (parity_ptr ? (*parity_ptr) * pair_stride : 0);
-    const uint64_t tile = blockIdx.x;
+    const uint64_t tile = blockIdx.x, ntiles = gridDim.x;
     const uint64_t b = tile * kTile;
     const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), rows - b));
-    const int d0 = blockIdx.y * dslab;
-    const int d1 = min(n, d0 + dslab);
+    const int slab = blockIdx.y;
+    const int d0 = slab * dslab;
+    const int dl = min(n, d0 + dslab) - d0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    for (int e = threadIdx.x; e < kUChunks * k; e += blockDim.x) ccount[e] = 0;
+    // stage the coordinate slab with 16-byte cp.async (independent of the
+    // bucketing; dslab, d0 and ld are multiples of 16 bytes / sizeof(T))
+    constexpr int kV = 16 / sizeof(T);
+    const int dv = (dl + kV - 1) / kV, dlp = dv * kV;  // padded row of the staged slab
+    {
+        const T* Xt = X + b * ld + d0;
+        for (int e = threadIdx.x; e < len * dv; e += blockDim.x) {
+            const int p = e / dv, v = e - p * dv;
+            cp_async_16(xs + p * dlp + v * kV, Xt + static_cast<uint64_t>(p) * ld + v * kV);
+        }
+        cp_async_commit();
+    }
+    for (int e = threadIdx.x; e < kUWarps * k; e += blockDim.x) wcount[e] = 0;
     __syncthreads();
-    // per-chunk label counts and in-chunk ranks
-    int lab_r[kUChunks / (kUThreads / 32)], rank_r[kUChunks / (kUThreads / 32)];
+    ktrace_u(1);
+    // Stable bucketing.  Warp w owns the contiguous points [128 w, 128 w + 128)
+    // as 4 chunks of 32 in index order; per chunk __match_any_sync gives each
+    // point its rank among equal labels, and the label's running count in the
+    // warp (kept by the group leader) gives the chunk's base.
+    constexpr int kQ = kUChunks / kUWarps;
+    int lab_r[kQ], pos_r[kQ];
 #pragma unroll
-    for (int q = 0; q < kUChunks / (kUThreads / 32); ++q) {
-        const int c = warp + (kUThreads / 32) * q;
-        const int i = c * 32 + lane;
+    for (int q = 0; q < kQ; ++q) {
+        const int i = (warp * kQ + q) * 32 + lane;
         int l = -1 - lane;
         if (i < len) {
             l = labels[b + i];
             if (l < 0 || l >= k) {  // update_centroids label range check (core.cpp:189-193)
-                *bad_label = 1;
+                *u.bad_label = 1;
                 l = 0;
             }
         }
         const unsigned peers = __match_any_sync(0xFFFFFFFFu, l);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (i < len && lane == leader) {
+            base = wcount[warp * k + l];
+            wcount[warp * k + l] = base + __popc(peers);
+        }
+        base = __shfl_sync(0xFFFFFFFFu, base, leader);
         lab_r[q] = l;
-        rank_r[q] = __popc(peers & ((1u << lane) - 1u));
-        if (i < len && lane == __ffs(peers) - 1) ccount[c * k + l] = __popc(peers);
+        pos_r[q] = base + __popc(peers & ((1u << lane) - 1u));
+        __syncwarp();
     }
     __syncthreads();
-    // exclusive prefix over chunks per label; tile totals
+    ktrace_u(2);
+    // exclusive prefix over the warps per label; tile totals
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
         int r = 0;
-        for (int c = 0; c < kUChunks; ++c) {
-            const int v = ccount[c * k + j];
-            ccount[c * k + j] = r;
+#pragma unroll
+        for (int w = 0; w < kUWarps; ++w) {
+            const int v = wcount[w * k + j];
+            wcount[w * k + j] = r;
             r += v;
         }
         cnt[j] = r;
+        if (r) atomicAdd(&u.slab_tot[slab * k + j], static_cast<unsigned>(r));
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int r = 0;
-        for (int j = 0; j < k; ++j) {
-            off[j] = r;
-            r += cnt[j];
+    if (warp == 0) {  // label offsets: exclusive scan of the totals
+        int carry = 0;
+        for (int j0 = 0; j0 < k; j0 += 32) {
+            const int j = j0 + lane;
+            const int v = j < k ? cnt[j] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (j < k) off[j] = carry + incl - v;
+            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
     }
     __syncthreads();
+    ktrace_u(3);
 #pragma unroll
-    for (int q = 0; q < kUChunks / (kUThreads / 32); ++q) {
-        const int c = warp + (kUThreads / 32) * q;
-        const int i = c * 32 + lane;
-        if (i < len) order[off[lab_r[q]] + ccount[c * k + lab_r[q]] + rank_r[q]] = static_cast<short>(i);
+    for (int q = 0; q < kQ; ++q) {
+        const int i = (warp * kQ + q) * 32 + lane;
+        if (i < len) order[off[lab_r[q]] + wcount[warp * k + lab_r[q]] + pos_r[q]] = static_cast<short>(i);
     }
+    cp_async_wait<0>();
     __syncthreads();
-    const int dl = d1 - d0;
-    if (blockIdx.y == 0)
-        for (int j = threadIdx.x; j < k; j += blockDim.x) pcnt[tile * k + j] = cnt[j];
-    if (dl <= 0) return;
-    const T* Xt = X + b * ld;
+    ktrace_u(4);
     for (int e = threadIdx.x; e < k * dl; e += blockDim.x) {
-        const int j = e / dl, d = d0 + e % dl;
+        const int j = e / dl, dd = e - j * dl;
         const int c = cnt[j];
-        if (c == 0) continue;
         const short* ord = order + off[j];
         double acc = 0.0;
         int q = 0;
         for (; q + 8 <= c; q += 8) {
             double v[8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) v[r] = to_f64(Xt[static_cast<uint64_t>(ord[q + r]) * ld + d]);
+            for (int r = 0; r < 8; ++r) v[r] = to_f64(xs[ord[q + r] * dlp + dd]);
 #pragma unroll
             for (int r = 0; r < 8; ++r) acc = __dadd_rn(acc, v[r]);
         }
-        for (; q < c; ++q) acc = __dadd_rn(acc, to_f64(Xt[static_cast<uint64_t>(ord[q]) * ld + d]));
-        psum[(tile * k + j) * n + d] = acc;
+        for (; q < c; ++q) acc = __dadd_rn(acc, to_f64(xs[ord[q] * dlp + dd]));
+        u.psum[(static_cast<uint64_t>(d0 + dd) * k + j) * u.tstride + tile] = acc;
     }
-}
 
-// Phase B: one thread per (label j, dim d).  Every CTA recomputes the label
-// totals and active ranks (integers: order-free), then folds the tile
-// partials of label j in tile order (:217-229) with the loads issued in
-// batches ahead of the adds (empty tiles contribute +0.0 and are skipped),
-// and applies sum * (1.0/count) (:237-239); count 0 -> degenerate row of 0.0.
-constexpr int kMThreads = 128;
-
-__global__ void __launch_bounds__(kMThreads)
-k_update_merge(const double* __restrict__ psum, const uint32_t* __restrict__ pcnt, uint64_t ntiles,
-               int k, int n, double* __restrict__ C, uint8_t* __restrict__ mask,
-               double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
-               float* __restrict__ CT32, const int* __restrict__ stop_ptr, double* __restrict__ drift2) {
-    if (stop_ptr && *stop_ptr) return;
-    extern __shared__ unsigned long long msh[];
-    unsigned long long* total = msh;                  // [k]
-    int* rank = reinterpret_cast<int*>(total + k);    // [k]
-    for (int jj = threadIdx.x; jj < k; jj += blockDim.x) total[jj] = 0;
+    // ---- the last G CTAs of this slab merge it, pairs g, g + G, ... each ----
+    // (they wait for the slab's other CTAs: those hold no resources the
+    // waiting ones need, so they always complete)
+    __shared__ int mg;
+    __threadfence();
     __syncthreads();
-    for (uint64_t e = threadIdx.x; e < ntiles * k; e += blockDim.x) {
-        const uint32_t c = pcnt[e];
-        if (c) atomicAdd(&total[e % k], static_cast<unsigned long long>(c));
+    ktrace_u(5);
+    const int G = u.mergers;
+    if (threadIdx.x == 0) {
+        const int a = static_cast<int>(atomicAdd(&u.slab_ctr[slab], 1u));
+        mg = a - (static_cast<int>(ntiles) - G);
+        if (mg >= 0)
+            while (__ldcg(&u.slab_ctr[slab]) < ntiles) __nanosleep(64);
     }
     __syncthreads();
+    if (mg < 0) return;
+    __threadfence();
+    ktrace_u(6);
+    // reuse the shared memory: totals, ranks, squared movements, staged partials
+    int* tot = ush;                                          // [k]
+    int* rank = tot + k;                                     // [k]
+    const size_t o_sq = (static_cast<size_t>(2 * k) * 4 + 15) & ~size_t(15);
+    double* sq = reinterpret_cast<double*>(ush_raw + o_sq);  // [k] this merger's movement per label
+    const size_t o_m = (o_sq + static_cast<size_t>(k) * 8 + 15) & ~size_t(15);
+    double* mbuf = reinterpret_cast<double*>(ush_raw + o_m);
+    const int mstride = static_cast<int>(u.tstride) + 1;     // odd: conflict-free folds
+    const int cap = static_cast<int>((u.shm_bytes - o_m) / (static_cast<size_t>(mstride) * 8));
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        tot[j] = static_cast<int>(__ldcg(&u.slab_tot[slab * k + j]));
+        sq[j] = 0.0;
+    }
+    __syncthreads();
+    ktrace_u(7);
     if (threadIdx.x == 0) {
         int r = 0;
-        for (int jj = 0; jj < k; ++jj) {
-            rank[jj] = total[jj] ? r : -1;
-            if (blockIdx.x == 0) {
-                mask[jj] = total[jj] ? 0 : 1;
-                if (total[jj]) act_idx[r] = jj;
+        for (int j = 0; j < k; ++j) {
+            rank[j] = tot[j] ? r : -1;
+            if (slab == 0 && mg == 0) {
+                u.mask[j] = tot[j] ? 0 : 1;
+                if (tot[j]) u.act_idx[r] = j;
             }
-            r += total[jj] != 0;
+            r += tot[j] != 0;
         }
-        if (blockIdx.x == 0) *n_active = r;
+        if (slab == 0 && mg == 0) *u.n_active = r;
     }
+    // This merger's pairs (dim, label) = q G + mg; each pair's tile partials are
+    // contiguous in psum: staged through shared memory with cp.async (a warp per
+    // pair), then one thread per pair folds them in tile order.
+    const int npairs = k * dl;
+    const int mine = npairs > mg ? (npairs - mg + G - 1) / G : 0;
+    const double* src = u.psum + static_cast<uint64_t>(d0) * k * u.tstride;
+    for (int q0 = 0; q0 < mine; q0 += cap) {
+        const int nq = min(cap, mine - q0);
+        for (int pl = warp; pl < nq; pl += kUWarps) {
+            const double* sp = src + static_cast<uint64_t>((q0 + pl) * G + mg) * u.tstride;
+            for (int t = lane; t < static_cast<int>(ntiles); t += 32) cp_async_el(mbuf + pl * mstride + t, sp + t, 8);
+        }
+        cp_async_commit_wait_all();
+        __syncthreads();
+        if (q0 == 0) ktrace_u(9);
+        for (int e = threadIdx.x; e < nq; e += blockDim.x) {
+            const int pair = (q0 + e) * G + mg;
+            const int j = pair % k, d = d0 + pair / k;
+            const uint64_t ce = static_cast<uint64_t>(j) * n + d;
+            if (tot[j] == 0) {
+                u.C[ce] = 0.0;
+                continue;
+            }
+            const double* mp = mbuf + static_cast<uint64_t>(e) * mstride;
+            double acc = 0.0;
+            for (int t = 0; t < static_cast<int>(ntiles); ++t) acc = __dadd_rn(acc, mp[t]);
+            const double inv = __ddiv_rn(1.0, static_cast<double>(tot[j]));
+            const double v = __dmul_rn(acc, inv);
+            const double dv = __dsub_rn(v, u.C[ce]);
+            atomicAdd(&sq[j], __dmul_rn(dv, dv));  // order-free: only bounds use it
+            u.C[ce] = v;
+            const int rk = rank[j];
+            u.Cact[static_cast<uint64_t>(rk) * u.ldc + d] = v;
+            if (u.CT32 && rk < kSMaxK) u.CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+        }
+        __syncthreads();
+        if (q0 == 0) ktrace_u(10);
+    }
+    ktrace_u(8);
+    if (u.drift_part)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) u.drift_part[(slab * G + mg) * k + j] = sq[j];
+    // the last merger to finish resets the slab's counters for the next launch
+    __threadfence();
     __syncthreads();
-    const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= static_cast<uint64_t>(k) * n) return;
-    const int j = static_cast<int>(e / n), d = static_cast<int>(e % n);
-    if (total[j] == 0) {
-        C[e] = 0.0;
-        return;
+    if (threadIdx.x == 0 && atomicAdd(&u.slab_done[slab], 1u) == static_cast<unsigned>(G) - 1) {
+        for (int j = 0; j < k; ++j) u.slab_tot[slab * k + j] = 0u;
+        u.slab_done[slab] = 0u;
+        __threadfence();
+        u.slab_ctr[slab] = 0u;
+        if (slab == gridDim.y - 1) klog_end(2);
     }
-    double acc = 0.0;
-    uint64_t t = 0;
-    for (; t + 8 <= ntiles; t += 8) {
-        double v[8];
-        uint32_t c[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            c[r] = pcnt[(t + r) * k + j];
-            v[r] = psum[((t + r) * k + j) * n + d];
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-            if (c[r]) acc = __dadd_rn(acc, v[r]);
-    }
-    for (; t < ntiles; ++t)
-        if (pcnt[t * k + j]) acc = __dadd_rn(acc, psum[(t * k + j) * n + d]);
-    const double inv = __ddiv_rn(1.0, static_cast<double>(total[j]));
-    const double v = __dmul_rn(acc, inv);
-    if (drift2) {  // squared movement of centroid j (bounds of the next assignment)
-        const double dv = __dsub_rn(v, C[e]);
-        atomicAdd(&drift2[j], __dmul_rn(dv, dv));
-    }
-    C[e] = v;
-    const int rk = rank[j];
-    Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
-    if (CT32 && rk < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
 }
 
 // Compact the active rows of (C, mask) for the assignment (single CTA).
@@ -1855,9 +2160,38 @@ __global__ void k_accept(LloydStatus* st, double* f_opt, double* __restrict__ C,
                          uint8_t* __restrict__ mask, double* __restrict__ Cinc,
                          uint8_t* __restrict__ maskinc, int k, int n, Record* rec_base,
                          unsigned long long* chunk_ctr, double* __restrict__ Cact, int ldc,
-                         int* __restrict__ act_idx, float* __restrict__ CT32) {
+                         int* __restrict__ act_idx, float* __restrict__ CT32,
+                         const double* __restrict__ dists_pair, uint64_t dstride, uint64_t rows,
+                         double* __restrict__ tile_buf, unsigned* __restrict__ counter, const int* go,
+                         LloydStatus* host_st) {
     extern __shared__ int arank[];  // [k]
     __shared__ int accepted;
+    klog_start(3);
+    if (go && !*go) return;
+    if (dists_pair && gridDim.x <= kTile) {  // fast-sum control: the exact objective (:53-54) = block_sum of the final distances
+        __shared__ __align__(16) double fbuf[kTile];
+        __shared__ int last;
+        const double* dv = dists_pair + st->parity * dstride;
+        const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
+        const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), rows - tb));
+        for (int i = threadIdx.x; i < len; i += blockDim.x) fbuf[i] = __ldcg(dv + tb + i);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            tile_buf[blockIdx.x] = seq_fold_smem(fbuf, len);
+            __threadfence();
+            last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) fbuf[i] = __ldcg(tile_buf + i);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            *counter = 0u;
+            st->objective = seq_fold_smem(fbuf, gridDim.x);
+        }
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
         const unsigned long long chunk = *chunk_ctr;
         Record* rec = rec_base + chunk;
@@ -1899,12 +2233,23 @@ __global__ void k_accept(LloydStatus* st, double* f_opt, double* __restrict__ C,
         Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
         if (CT32 && rk < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
     }
+    if (host_st) {  // the status straight into mapped pinned host memory (no copy node)
+        __syncthreads();
+        constexpr int kW = sizeof(LloydStatus) / 8;
+        for (int i = threadIdx.x; i < kW; i += blockDim.x)
+            reinterpret_cast<volatile unsigned long long*>(host_st)[i] =
+                reinterpret_cast<const volatile unsigned long long*>(st)[i];
+        __threadfence_system();
+    }
+    if (threadIdx.x == 0) klog_end(3);
 }
 
 // Head of a chunk's Lloyd graph: the chunk runs only when the previous accept
 // left no degenerate incumbent rows, or the host has repaired them (st->go).
 __global__ void k_guard(const LloydStatus* st, cudaGraphConditionalHandle h) {
+    klog_start(0);
     cudaGraphSetConditional(h, st->go != 0 ? 1u : 0u);
+    klog_end(0);
 }
 
 // Reset of the per-run device state (incumbent all degenerate, f_opt = +inf).
@@ -1916,6 +2261,7 @@ __global__ void k_run_init(LloydStatus* st, double* f_opt, double* Cinc, uint8_t
         *f_opt = __longlong_as_double(0x7FF0000000000000LL);
         st->inc_degenerate = k;
         st->go = 0;
+        st->stop = 1;  // a skipped chunk's rounds see a finished loop
         *chunk_ctr = 0;
     }
 }

@@ -5,7 +5,7 @@
 // per chunk the s sample draws uniform_int(i, m-1) (big_means.cpp:49-51), then
 // only when the incumbent has degenerate rows the K-means++ draws
 // (init.cpp:144-196).  The sample draws of a steady-state chunk are produced on
-// the device (k_mt_draw), so the state lives on the device and visits the host
+// the device (k_mt_twist, k_mt_emit, k_mt_fix), so the state lives on the device and visits the host
 // only for repairs.  Bit-identity with std::mt19937_64 +
 // std::uniform_int_distribution / uniform_real_distribution is checked by the
 // CPU tests (tests/test_host.py) and the golden vectors.

@@ -142,3 +142,26 @@ def test_configs_bitwise_vs_oracle(port, key):
     assert (bits(out.centroids.values) == bits(p.centroids)).all()
     assert (out.assignment == p.labels).all()
     assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+@pytest.mark.parametrize("case", ["tiny_chunks", "duplicates"])
+def test_mid_run_repairs_vs_oracle(port, case):
+    """Accepted candidates with empty clusters force K-means++ repairs in later
+    chunks: the pipelined loop's speculative draws and queued Lloyd graphs for
+    those chunks must be discarded and redone in the reference's RNG order."""
+    rng = np.random.default_rng(77)
+    if case == "tiny_chunks":  # small chunks of coarse data: empty clusters are common
+        X = np.rint(rng.normal(size=(4000, 5)) * 0.5)
+        k, s, chunks = 8, 20, 40
+    else:  # heavy duplication: many coincident points, degenerate clusters
+        X = np.rint(rng.normal(size=(3000, 3)))
+        k, s, chunks = 16, 40, 40
+    out, trace = bm.big_means(bm.Dataset(X), cfg(k, s, chunks, seed=5))
+    p = port.big_means(X.astype(np.float64), k, s, chunks, seed=5)
+    got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+            r.degenerate_repaired) for r in trace.records]
+    assert sum(1 for r in p.trace[1:] if r[4] > 0) >= 2  # repairs after the first chunk
+    assert got == p.trace
+    assert out.objective == p.objective
+    assert (bits(out.centroids.values) == bits(p.centroids)).all()
+    assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)

@@ -163,7 +163,7 @@ def test_screen_adversarial_bitwise(port, case):
 
 @pytest.mark.parametrize("var,alt", [("BM_ASSIGN_MODE", "exact"), ("BM_GRAPHS", "0"),
                                      ("BM_STORAGE", "native"), ("BM_SCREEN", "v4"),
-                                     ("BM_HAMERLY", "0")])
+                                     ("BM_HAMERLY", "0"), ("BM_FORCE_EXACT_CONTROL", "1")])
 def test_engine_modes_agree(var, alt):
     """Unscreened assignment (BM_ASSIGN_MODE=exact) and the host-driven chunk
     loop (BM_GRAPHS=0) give the same bits as the default path, in fresh processes."""
@@ -173,11 +173,14 @@ def test_engine_modes_agree(var, alt):
         "import paper_2204_07485_b200 as bm;"
         "X = np.rint(np.random.default_rng(5).normal(size=(20000, 16)) * 4);"
         "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=10, chunk_size=3000, max_chunks=6, seed=3));"
-        "import hashlib; print(repr(o.objective), o.counter.distance_evals, hashlib.sha1(o.centroids.values.tobytes()).hexdigest())")
+        "import hashlib; print(repr(o.objective), o.counter.distance_evals, o.counter.iterations,"
+        " hashlib.sha1(o.centroids.values.tobytes()).hexdigest(), repr(t.records))")
     env = dict(os.environ)
     outs = []
-    for mode in ("default", alt):
-        env[var] = mode
+    for mode in (None, alt):
+        env.pop(var, None)
+        if mode is not None:
+            env[var] = mode
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                                    text=True, check=True).stdout)
     assert outs[0] == outs[1] and outs[0]

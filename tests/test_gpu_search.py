@@ -42,7 +42,7 @@ def test_sample_chunk_vs_oracle(port, m, s):
                                  (100_000, 10_000), (2_500_000, 50_000), (10_500_000, 100_000)])
 @pytest.mark.parametrize("force_seq", [False, True])
 def test_device_stream_sample_chunk_vs_oracle(port, m, s, force_seq):
-    """Draws made on the device (k_mt_draw) from the device-resident stream:
+    """Draws made on the device (k_mt_twist, k_mt_emit, k_mt_fix) from the device-resident stream:
     same indices and same stream position as the reference's host draws."""
     if force_seq and s > 20_000:
         pytest.skip("sequential path is a single-thread fallback; small cases suffice")

@@ -1,0 +1,58 @@
+"""Kernel log of the Lloyd graphs (debug tool; library built with -DBM_KTRACE
+via `python tools/ktrace.py --build`): per kernel kind, in-graph durations and
+the gaps between consecutive kernels of the chain loop.
+
+  python tools/klog.py [chunks]
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2204_07485_b200 import _capi  # noqa: E402
+_capi.LIB_PATH = os.path.join(ROOT, "tools", "_ktrace", "libbigmeans_b200.so")
+import paper_2204_07485_b200 as bm  # noqa: E402
+from paper_2204_07485_b200 import synthetic  # noqa: E402
+
+chunks = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+w = synthetic.CONFIGS["c2"]
+d = bm.Dataset(synthetic.generate("c2"))
+cfg = bm.BigMeansConfig(k=w.k, chunk_size=w.s, max_chunks=chunks, seed=0)
+bm.big_means(d, cfg, want_labels=False)
+buf = np.zeros(200001 + 3 * 60000, np.uint64)
+lib = _capi.load()
+lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
+n0 = int(buf[200000])
+st0 = buf[199990:199993].astype(np.int64)
+bm.big_means(d, cfg, want_labels=False)
+lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
+n1 = int(buf[200000])
+st1 = buf[199990:199993].astype(np.int64)
+E = buf[200001:200001 + 3 * 60000].reshape(-1, 3).astype(np.int64)[n0 % 60000:n1 % 60000]
+names = {0: "guard", 2: "update", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)"}
+E = E[np.argsort(E[:, 1])]
+print(f"{len(E)} kernels over {chunks} chunks; span {(E[-1, 2] - E[0, 1]) / 1e3:.1f} us "
+      f"({(E[-1, 2] - E[0, 1]) / 1e3 / chunks:.1f} us per chunk)")
+dur = {}
+for kid, a, b in E:
+    dur.setdefault(int(kid), []).append(b - a)
+busy = 0
+for kid in sorted(dur):
+    v = np.array(dur[kid]) / 1e3
+    busy += v.sum()
+    print(f"{names.get(kid, kid):14s} n={len(v):5d} mean={v.mean():7.2f} p50={np.median(v):7.2f} "
+          f"p90={np.percentile(v, 90):7.2f} us  total/chunk={v.sum() / chunks:7.2f} us")
+gaps = (E[1:, 1] - E[:-1, 2]) / 1e3
+print(f"kernel busy {busy / chunks:.1f} us per chunk; gaps between consecutive kernels: mean {gaps.mean():.2f} "
+      f"p50 {np.median(gaps):.2f} p90 {np.percentile(gaps, 90):.2f} us, {gaps.sum() / chunks:.1f} us per chunk")
+pairs = {}
+for i in range(1, len(E)):
+    key = (names.get(int(E[i - 1, 0])), names.get(int(E[i, 0])))
+    pairs.setdefault(key, []).append((E[i, 1] - E[i - 1, 2]) / 1e3)
+for key, v in sorted(pairs.items(), key=lambda kv: -sum(kv[1])):
+    print(f"  gap {key[0]:>14s} -> {key[1]:14s} n={len(v):5d} mean={np.mean(v):6.2f} us")
+ds = st1 - st0
+print(f"round fast path: {ds[0]} CTAs, {ds[1]} fell back to the screen ({100 * ds[1] / max(ds[0], 1):.1f}%), "
+      f"{ds[2] / max(ds[0], 1):.2f} failed points per CTA")

@@ -46,7 +46,7 @@ for _ in range(3):
         bm.lloyd(d, cent, bm.SearchConfig(max_iterations=1))
     else:
         bm.assign_nearest(d, cent)
-buf = np.zeros(2048 * 32, np.uint64)
+buf = np.zeros(65536 + 2048 * 32, np.uint64)
 lib = _capi.load()
 assert lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size) == 0
 ctas = (m + 127) // 128
@@ -62,3 +62,16 @@ for i, nm in enumerate(names):
     if v.size:
         print(f"{nm:9s} n={v.size:5d}  p10={np.percentile(v,10)/1e3:8.2f}  p50={np.percentile(v,50)/1e3:8.2f}  "
               f"p90={np.percentile(v,90)/1e3:8.2f}  max={v.max()/1e3:8.2f} us")
+
+if lloyd_mode:  # the last k_update launch (region 1)
+    U = buf[65536:].reshape(-1, 32).astype(np.int64)
+    U = U[U[:, 0] > 0]
+    t0 = U[:, 0].min()
+    print(f"k_update ctas={len(U)}")
+    for i, nm in enumerate(["start", "staged", "bucketed", "prefix", "order", "folded", "merger", "totals",
+                            "merged", "m0_copied", "m0_folded"]):
+        col = U[:, i]
+        v = col[col > 0] - t0
+        if v.size:
+            print(f"{nm:9s} n={v.size:5d}  p10={np.percentile(v,10)/1e3:8.2f}  p50={np.percentile(v,50)/1e3:8.2f}  "
+                  f"p90={np.percentile(v,90)/1e3:8.2f}  max={v.max()/1e3:8.2f} us")
