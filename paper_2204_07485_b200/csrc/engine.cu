@@ -130,7 +130,9 @@ struct Workspace {
     uint64_t tiles = 0;
 
     DevBuf<int32_t> labels;  // 2 * R (ping-pong)
-    DevBuf<double> dists;    // R
+    DevBuf<double> dists;    // 4 * R
+    DevBuf<double> fix_tiles;  // tiles: tile partials of a chunk's exact objective (deferred records)
+    DevBuf<dev::AcceptArgs> accd;  // device copy of the accept arguments (controls that accept)
     DevBuf<double> tile_buf; // max(ncand,1) * tiles
     DevBuf<unsigned> tile_ctr;  // tiles (fused tile-fold arrival counters)
     DevBuf<unsigned> tiles_done;  // tiles completed in the current assignment launch (fused control)
@@ -143,7 +145,7 @@ struct Workspace {
     DevBuf<dev::LloydStatus> status;
     DevBuf<double> history;
     // certified bounds for the Lloyd-round fast path of the screened assignment
-    DevBuf<float> lb;        // R: lower bound (distance units) to every non-chosen centroid
+    DevBuf<float> lbk;       // R x 32: lower bound (distance units) of every (point, label) distance
     DevBuf<double> drift_part;  // [n][k]: squared centroid movement of the last update, per d-slab
     int drift_slabs = 0;        // d-slabs of the last update launch (host view at enqueue/capture time)
     DevBuf<unsigned> slab_ctr, slab_done, slab_tot;  // [n], [n], [n][k]: fused update counters / label totals
@@ -159,11 +161,12 @@ struct Workspace {
     std::string graph_sig;
     cudaGraphExec_t g_prep[2] = {nullptr, nullptr};
     cudaGraphExec_t g_lloyd[2] = {nullptr, nullptr};  // per chunk buffer
+    cudaGraphExec_t g_cont[2] = {nullptr, nullptr};   // continuation of an incomplete chunk
     cudaStream_t cap1 = nullptr, cap2 = nullptr;  // capture streams of the IF and WHILE bodies
     cudaEvent_t ev_lloyd[2] = {nullptr, nullptr};  // end of the Lloyd graph of chunk buffer b
     cudaEvent_t ev_prep[2] = {nullptr, nullptr};   // chunk buffer b gathered
     void drop_graphs() {
-        for (auto* v : {&g_prep, &g_lloyd})
+        for (auto* v : {&g_prep, &g_lloyd, &g_cont})
             for (auto& e : *v)
                 if (e) {
                     cudaGraphExecDestroy(e);
@@ -206,8 +209,9 @@ struct Workspace {
         tiles = tiles_of(rows);
         hist_cap = hist;
         labels.alloc(2 * R);
-        dists.alloc(2 * R);  // [R, 2R): second slot of the fast-sum Lloyd control
-        lb.alloc(R);
+        dists.alloc(4 * R);  // [chunk buffer][slot][R]: the fast-sum control's two slots per chunk buffer
+        fix_tiles.alloc(std::max<uint64_t>(tiles, 1));
+        lbk.alloc(R * dev::kSMaxK);
         tile_buf.alloc(tiles * ncand);
         tile_ctr.alloc(tiles);
         if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
@@ -487,6 +491,33 @@ struct PhaseScope {
 
 void count_launch(uint64_t n = 1) { g_profile.kernel_launches += n; }
 
+// BM_PDL=0 disables programmatic dependent launch.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_PDL");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+// Launch with programmatic stream serialization: the kernel's CTAs may start
+// while the previous kernel on the stream drains; they wait for its completion
+// (griddepcontrol.wait) before touching its results.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    BM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 int assign_threads(int k) {
     const int kg = std::min<int>(dev::kAMaxCG, (int)ceil_div(std::max(k, 1), dev::kAK));
     return dev::kAPG * kg;
@@ -586,10 +617,10 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
                    const int* stop, bool final_pass = false, double* tile_out = nullptr,
                    unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr, int hmode = 0,
-                   uint64_t dstride = 0) {
+                   uint64_t dstride = 0, unsigned extra_ctas = 0) {
     const dev::LloydCtl noctl{};
     bool fused_ctl = false;
-    const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP);
+    const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP) + extra_ctas;  // extra: fixup CTAs (TMA path)
     if (grid == 0) return;
     PhaseScope ps(final_pass ? PH_FINAL : PH_ASSIGN, P.rows);
     const bool screen = screen_enabled(k);
@@ -605,11 +636,11 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             }
             const CUtensorMap tmx = points_map<T>(P);
             fused_ctl = ctl && (tile_out || ctl->fast);
-            dev::k_assign_tma<T><<<grid, dev::kSThreads, shm, st>>>(
+            launch_pdl(dev::k_assign_tma<T>, grid, dev::kSThreads, shm, st,
                 tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                 g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
-                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, w.lb.p, w.drift_part.p,
+                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, w.lbk.p, w.drift_part.p,
                 w.drift_slabs, k,
                 dstride);
         } else if (screen) {
@@ -663,7 +694,8 @@ void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_
 // update_centroids (core.cpp:183-244) in one launch: grid (tile, d-slab), the
 // slab's last CTA merges it.  Slabs split the dimensions so that the grid
 // covers the GPU when there are few tiles and the staged slab fits in shared memory.
-void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* parity, const int* stop) {
+void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* parity, const int* stop,
+                   const int* go = nullptr) {
     PhaseScope ps(PH_UPDATE, P.rows);
     const int k = w.k, n = w.n;
     const uint64_t tiles = tiles_of(P.rows);
@@ -685,14 +717,14 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
     // (waiting mergers never exceed one per SM, so the CTAs they wait for always get a slot)
     int G = (int)std::min<uint64_t>({tiles, (uint64_t)8, std::max<uint64_t>(1, ceil_div((uint64_t)k * dslab, 48))});
     while (G > 1 && (uint64_t)G * slabs > 148) --G;
-    dev::UpdateArgs u{w.psum.p, tstride, shm, w.slab_ctr.p, w.slab_done.p, G, w.slab_tot.p, w.C.p, w.mask.p, w.Cact.p, w.ldc,
+    dev::UpdateArgs u{w.psum.p, tstride, shm, w.slab_ctr.p, w.slab_done.p, G, go, w.slab_tot.p, w.C.p, w.mask.p, w.Cact.p, w.ldc,
                       w.act.p, &w.status.p->n_active, w.CT32.p, w.drift_part.p, &w.status.p->bad_label, stop};
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         if (shm > 48 * 1024)
             BM_CUDA(cudaFuncSetAttribute(dev::k_update<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-        dev::k_update<T><<<grid, dev::kUThreads, shm, st>>>(static_cast<const T*>(P.X), P.rows, n, P.ld,
-                                                             w.labels.p, w.R, parity, k, dslab, u);
+        launch_pdl(dev::k_update<T>, grid, dev::kUThreads, shm, st, static_cast<const T*>(P.X), P.rows, n, P.ld,
+                   w.labels.p, w.R, parity, k, dslab, u);
     });
     BM_LAUNCH();
     count_launch(1);
@@ -738,24 +770,55 @@ dev::LloydCtl make_ctl(Workspace& w, int mode, uint64_t rows, uint64_t max_it = 
 
 // compact (unless the compacted start is already in place) + assign (:26) +
 // begin (:27-28), the latter fused into the assignment where possible.
+// Graph-mode extras of a Lloyd launch sequence.
+struct GraphRound {
+    double* dbase = nullptr;        // distance slots of this chunk buffer (default: w.dists.p)
+    const int* go = nullptr;        // skip everything when *go == 0
+    bool accept = false;            // the control runs the accept when the loop stops
+    dev::LloydStatus* host_st = nullptr;
+    unsigned long long incomplete_after = 0;
+    bool fix = false;               // begin: fixup CTAs for the pending chunk's record
+};
+
+void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
+    if (!g) return;
+    if (g->dbase) c.dists_pair = g->dbase;
+    c.go = g->go;
+    if (g->accept || g->fix) c.acc = w.accd.p;
+    c.accept_run = g->accept ? 1 : 0;
+    c.host_st = g->host_st;
+    c.incomplete_after = g->incomplete_after;
+    if (g->fix) {
+        c.dists_all = w.dists.p;
+        c.fix_rows = w.R;
+        c.fix_tiles = w.fix_tiles.p;
+    }
+}
+
+// compact (unless the compacted start is already in place) + assign (:26) +
+// begin (:27-28), the latter fused into the assignment where possible.
 void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do_compact = true,
-                         bool fast = false, const int* go = nullptr) {
+                         bool fast = false, const GraphRound* g = nullptr) {
     if (do_compact) launch_compact(st, w, w.C.p, w.mask.p);
     dev::LloydCtl ctl = make_ctl(w, 1, P.rows, 0, 0.0, 0, 0, fast);
-    ctl.go = go;
-    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, w.dists.p, nullptr, nullptr, false,
-                  fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1);
+    apply_graph(ctl, w, g);
+    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, g && g->dbase ? g->dbase : w.dists.p, nullptr, nullptr,
+                  false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1, 0,
+                  g && g->fix ? (unsigned)tiles_of(w.R) : 0u);
 }
 
 // update (:33) + assign (:34-35) + step (:36-51), the step fused into the assignment.
 void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol,
-                         cudaGraphConditionalHandle cond = 0, int use_cond = 0, bool fast = false) {
+                         cudaGraphConditionalHandle cond = 0, int use_cond = 0, bool fast = false,
+                         const GraphRound* g = nullptr) {
     const int* parity = &w.status.p->parity;
     const int* stop = &w.status.p->stop;
-    launch_update(st, P, w, parity, stop);
-    const dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond, fast);
-    launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, w.dists.p, &w.status.p->changed, stop, false,
-                  fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 2, fast ? w.R : 0);
+    launch_update(st, P, w, parity, stop, g ? g->go : nullptr);
+    dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond, fast);
+    apply_graph(ctl, w, g);
+    launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, g && g->dbase ? g->dbase : w.dists.p,
+                  &w.status.p->changed, stop, false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 2,
+                  fast ? w.R : 0);
 }
 
 // Runs the loop to completion; `between` is called once after the first
@@ -1065,16 +1128,29 @@ bool graphs_enabled() {
     return on;
 }
 
-// fast: the Lloyd loop ran the fast-sum control, so the accept first computes
-// the exact objective of the final assignment (one CTA per 1024-row tile).
-void enqueue_accept(cudaStream_t st, Workspace& w, bool fast = false, const int* go = nullptr,
-                    dev::LloydStatus* host_st = nullptr) {
+dev::AcceptArgs accept_args(Workspace& w) {
+    dev::AcceptArgs A{};
+    A.f_opt = w.fopt.p;
+    A.C = w.C.p;
+    A.mask = w.mask.p;
+    A.Cinc = w.Cinc.p;
+    A.maskinc = w.maskinc.p;
+    A.k = w.k;
+    A.n = w.n;
+    A.rec_base = w.drec.p;
+    A.chunk_ctr = w.chunk_ctr.p;
+    A.Cact = w.Cact.p;
+    A.ldc = w.ldc;
+    A.act_idx = w.act.p;
+    A.CT32 = w.CT32.p;
+    return A;
+}
+
+// The accept (:89-94) with the exact objective of the finished Lloyd loop.
+void enqueue_accept(cudaStream_t st, Workspace& w) {
     PhaseScope ps(PH_CONTROL, 0);
-    const unsigned grid = fast ? (unsigned)tiles_of(w.R) : 1u;
-    dev::k_accept<<<grid, 256, w.k * sizeof(int), st>>>(w.status.p, w.fopt.p, w.C.p, w.mask.p, w.Cinc.p,
-                                                        w.maskinc.p, w.k, w.n, w.drec.p, w.chunk_ctr.p, w.Cact.p,
-                                                        w.ldc, w.act.p, w.CT32.p, fast ? w.dists.p : nullptr, w.R,
-                                                        w.R, w.tile_buf.p, w.tiles_done.p, go, host_st);
+    launch_pdl(dev::k_accept, 1, 256, 2 * w.k * sizeof(int), st, w.status.p, accept_args(w),
+               (dev::LloydStatus*)nullptr);
     BM_LAUNCH();
     count_launch();
 }
@@ -1124,34 +1200,23 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
     // fast-sum control whenever the TMA screen (which implements it) runs
     const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
     if (fast) {
-        // begin -> round 1 -> WHILE { round } -> accept, no IF: every kernel of
-        // a skipped chunk (st->go == 0) returns at once (the begin and the
-        // accept test go; the rounds see the previous loop's stop), and round
-        // 1's control opens the WHILE node (default closed).
-        const int* go = &w.status.p->go;
-        lloyd_enqueue_begin(st, P, w, /*do_compact=*/false, true, go);
-        cudaStreamCaptureStatus cs;
-        cudaGraph_t cg = nullptr;
-        BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr));
-        cudaGraphConditionalHandle hw;
-        BM_CUDA(cudaGraphConditionalHandleCreate(&hw, cg, 0, cudaGraphCondAssignDefault));
-        lloyd_enqueue_round(st, P, w, max_it, tol, hw, 1, true);
-        const cudaGraphNode_t* deps = nullptr;
-        size_t nd = 0;
-        BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd));
-        cudaGraphNodeParams prm = {};
-        prm.type = cudaGraphNodeTypeConditional;
-        prm.conditional.handle = hw;
-        prm.conditional.type = cudaGraphCondTypeWhile;
-        prm.conditional.size = 1;
-        cudaGraphNode_t cn;
-        BM_CUDA(cudaGraphAddNode(&cn, cg, deps, nd, &prm));
-        BM_CUDA(cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies));
-        cudaGraph_t wbody = prm.conditional.phGraph_out[0];
-        BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-        lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1, true);
-        BM_CUDA(cudaStreamEndCapture(w.cap2, &wbody));
-        enqueue_accept(st, w, true, go, w.h_status.p + b);
+        // begin (+ fixup CTAs: the previous chunk's exact objective for its
+        // record) -> round 1 -> round 2; the control of the round that stops
+        // runs the accept.  A chunk still running after round 2 is marked
+        // incomplete and continued by the host (capture_cont).  Every kernel of
+        // a skipped chunk (st->go == 0) returns at once.
+        GraphRound g;
+        g.dbase = w.dists.p + 2 * (uint64_t)b * w.R;
+        g.go = &w.status.p->go;
+        g.fix = true;
+        lloyd_enqueue_begin(st, P, w, /*do_compact=*/false, true, &g);  // accept (or the repair) compacted the start
+        GraphRound r = g;
+        r.fix = false;
+        r.accept = true;
+        r.host_st = w.h_status.p + b;
+        lloyd_enqueue_round(st, P, w, max_it, tol, 0, 0, true, &r);
+        r.incomplete_after = 2;
+        lloyd_enqueue_round(st, P, w, max_it, tol, 0, 0, true, &r);
     } else {  // the guard sets the IF condition inside the graph that owns it
         cudaStreamCaptureStatus cs;
         cudaGraph_t cg = nullptr;
@@ -1180,10 +1245,33 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
         BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1, false);
         BM_CUDA(cudaStreamEndCapture(w.cap2, &wbody));
-        enqueue_accept(w.cap1, w, false);
+        enqueue_accept(w.cap1, w);
         BM_CUDA(cudaStreamEndCapture(w.cap1, &ifbody));
         BM_CUDA(cudaMemcpyAsync(w.h_status.p + b, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
     }
+    cudaGraph_t g = nullptr;
+    BM_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t e = nullptr;
+    BM_CUDA(cudaGraphInstantiate(&e, g, 0));
+    cudaGraphDestroy(g);
+    return e;
+}
+
+// The rest of an incomplete chunk's Lloyd loop: WHILE { update, assign + step },
+// the stopping control running the accept.
+cudaGraphExec_t capture_cont(cudaStream_t st, Workspace& w, const Points& P, uint64_t max_it, double tol, int b) {
+    if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
+    BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    cudaGraphConditionalHandle hw;
+    cudaGraph_t wbody = nullptr;
+    add_conditional(st, &hw, &wbody, cudaGraphCondTypeWhile, 1);
+    BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    GraphRound r;
+    r.dbase = w.dists.p + 2 * (uint64_t)b * w.R;
+    r.accept = true;
+    r.host_st = w.h_status.p + b;
+    lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1, true, &r);
+    BM_CUDA(cudaStreamEndCapture(w.cap2, &wbody));
     cudaGraph_t g = nullptr;
     BM_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t e = nullptr;
@@ -1201,12 +1289,17 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
+    if (!w.accd.n) w.accd.alloc(1);
+    const dev::AcceptArgs A = accept_args(w);
+    BM_CUDA(cudaMemcpy(w.accd.p, &A, sizeof(A), cudaMemcpyHostToDevice));
     void* bufs[2] = {dc.chunk.p, dc.chunk1.p};
+    const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
     for (int b = 0; b < 2; ++b) {
         Points Pb = P;
         Pb.X = bufs[b];
         w.g_prep[b] = capture_prep(st, d, sw, b, bufs[b]);
         w.g_lloyd[b] = capture_lloyd(st, w, Pb, max_it, tol, b);
+        if (fast) w.g_cont[b] = capture_cont(st, w, Pb, max_it, tol, b);
     }
     g_profile.kernel_launches = saved;  // capture is not execution
     w.graph_sig = sig;
@@ -1359,6 +1452,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             queued = next && speculate;
             if (queued) launch_lloyd(b ^ 1);  // runs iff this chunk's accept needs no repair
             BM_CUDA(cudaEventSynchronize(w.ev_lloyd[b]));
+            if (w.h_status.p[b].incomplete) {  // more rounds than the graph unrolls
+                BM_CUDA(cudaGraphLaunch(w.g_cont[b], st));
+                BM_CUDA(cudaEventRecord(w.ev_lloyd[b], st));
+                BM_CUDA(cudaEventSynchronize(w.ev_lloyd[b]));
+                queued = false;  // the queued next chunk found go == 0 and did nothing
+            }
             const dev::LloydStatus& ls = w.h_status.p[b];
             if (ls.state_error) throw StateError("assign_nearest: every centroid is degenerate");
             if (ls.bad_label) throw ConfigError("update_centroids: label out of range");
@@ -1368,6 +1467,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             count_launch(3 + 3 * ls.iterations);
             out->chunks = chunk + 1;
         }
+        // the last chunk's record gets its exact objective
+        dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.status.p, accept_args(w), w.dists.p, w.R,
+                                                                   w.fix_tiles.p, w.tiles_done.p);
+        BM_LAUNCH();
         BM_CUDA(cudaStreamSynchronize(st));
         BM_CUDA(cudaStreamSynchronize(pst));
         if (timeline && tl.size() > 2) {

@@ -45,8 +45,17 @@ struct LloydStatus {
     double fsum;         // accumulator of the current launch's CTA distance sums
     unsigned ctas_done;  // CTAs of the current launch that have added their sum
     int exact_checks;    // decisions that needed the exact sums (diagnostics)
+    // deferred exact objectives (graph mode): a chunk's exact objective is
+    // folded while the next chunk's first assignment runs
+    double fopt_exact;   // exact f_opt (big_means.cpp:63, :89-93) of the chunks fixed up so far
+    int pending_fix;     // chunk whose record awaits its exact objective (-1: none)
+    int fix_par;         // distance slot of that chunk's final assignment
+    int incomplete;      // the graph's unrolled rounds ended without a stop: continue on the host's order
+    int pad2;
 };
 static_assert(sizeof(LloydStatus) % 8 == 0, "status is copied as 8-byte words");
+
+constexpr int kSMaxK = 32;  // centroids handled by the screened path
 
 // Per-chunk accept record (ChunkRecord big_means.hpp:28-34).
 struct Record {
@@ -113,6 +122,11 @@ __device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v
 
 // One step of the reference distance loop core.cpp:144-145 / init.cpp:34-35:
 // diff = x - c; sum += diff * diff  (three separately rounded operations).
+// Programmatic dependent launch: wait for the previous kernel's completion and
+// memory (no-op when not launched as a dependent); allow the next kernel to launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ double dist_step(double sum, double x, double c) {
     const double diff = __dsub_rn(x, c);
     return __dadd_rn(sum, __dmul_rn(diff, diff));
@@ -534,7 +548,124 @@ struct LloydCtl {
     const double* dists_pair;  // distances of the last two assignments (slot = labels slot)
     uint64_t dstride;
     const int* go;          // when set and *go == 0 the launch does nothing (skipped chunk)
+    const struct AcceptArgs* acc;  // accept state (device copy)
+    int accept_run;         // the control runs the accept (:89-94) when the loop stops
+    LloydStatus* host_st;   // with acc: the status is also written to mapped host memory
+    unsigned long long incomplete_after;  // > 0: no stop after this many rounds -> st->incomplete
+    // begin launches with fixup CTAs: exact objective of the pending chunk
+    const double* dists_all;  // [2 chunk buffers][2 slots][fix_rows]
+    uint64_t fix_rows;
+    double* fix_tiles;
 };
+
+// The status straight into mapped pinned host memory (no copy node); CTA-wide.
+__device__ __forceinline__ void status_to_host(const LloydStatus* st, LloydStatus* host_st) {
+    constexpr int kW = sizeof(LloydStatus) / 8;
+    for (int i = threadIdx.x; i < kW; i += blockDim.x)
+        reinterpret_cast<volatile unsigned long long*>(host_st)[i] =
+            reinterpret_cast<const volatile unsigned long long*>(st)[i];
+    __threadfence_system();
+}
+
+// Accept step state (big_means.cpp:63-64, 89-94).
+struct AcceptArgs {
+    double* f_opt;
+    double* C;
+    uint8_t* mask;
+    double* Cinc;
+    uint8_t* maskinc;
+    int k, n;
+    Record* rec_base;
+    unsigned long long* chunk_ctr;
+    double* Cact;
+    int ldc;
+    int* act_idx;
+    float* CT32;
+};
+
+// The accept of the chunk's candidate (all threads of one CTA; sm: 2k ints).
+// deferred: the record's objectives are filled later by fix_record (the
+// exact candidate objective is folded during the next chunk).
+__device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, int accepted, bool deferred,
+                                         LloydStatus* host_st, int* sm) {
+    const int k = A.k, n = A.n;
+    __shared__ int acc_s;
+    if (threadIdx.x == 0) {
+        const unsigned long long chunk = *A.chunk_ctr;
+        Record* rec = A.rec_base + chunk;
+        if (deferred) {
+            rec->candidate_objective = __longlong_as_double(0x7FF8000000000000LL);
+            rec->incumbent_objective = __longlong_as_double(0x7FF8000000000000LL);
+            st->pending_fix = static_cast<int>(chunk);
+            st->fix_par = st->parity;
+        } else {
+            if (accepted) *A.f_opt = st->objective;
+            rec->candidate_objective = st->objective;
+            rec->incumbent_objective = *A.f_opt;
+        }
+        rec->chunk_index = chunk;
+        rec->accepted = accepted;
+        rec->degenerate_repaired = static_cast<unsigned long long>(st->inc_degenerate);
+        acc_s = accepted;
+    }
+    __syncthreads();
+    accepted = acc_s;
+    int* arank = sm;
+    int* mk = sm + k;  // incumbent mask staged in shared memory (the rank loop below is serial)
+    if (accepted) {
+        for (int e = threadIdx.x; e < k * n; e += blockDim.x) A.Cinc[e] = A.C[e];
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            const uint8_t v = A.mask[j];
+            A.maskinc[j] = v;
+            mk[j] = v;
+        }
+    } else {
+        for (int j = threadIdx.x; j < k; j += blockDim.x) mk[j] = A.maskinc[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int dcount = 0, r = 0;
+        for (int j = 0; j < k; ++j) {
+            dcount += mk[j] ? 1 : 0;
+            arank[j] = mk[j] ? -1 : r;
+            if (!mk[j]) A.act_idx[r++] = j;
+        }
+        st->inc_degenerate = dcount;
+        st->go = dcount == 0;
+        st->n_active = r;
+        st->incomplete = 0;
+        *A.chunk_ctr += 1;
+    }
+    __syncthreads();
+    // the next chunk's start (:82): (C, mask) := incumbent, and its compacted form
+    if (!accepted)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) A.mask[j] = static_cast<uint8_t>(mk[j]);
+    for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+        const int j = e / n, d = e - j * n, rk = arank[j];
+        const double v = A.Cinc[e];
+        if (!accepted) A.C[e] = v;
+        if (rk < 0) continue;
+        A.Cact[static_cast<uint64_t>(rk) * A.ldc + d] = v;
+        if (A.CT32 && rk < kSMaxK) A.CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+    }
+    if (host_st) {
+        __syncthreads();
+        status_to_host(st, host_st);
+    }
+}
+
+// The pending chunk's record gets its exact objectives (thread 0; tiles: the
+// ordered tile partials of its final distances).
+__device__ __forceinline__ void fix_record(LloydStatus* st, const AcceptArgs& A, const double* tiles, uint64_t ntiles) {
+    if (st->pending_fix < 0) return;
+    const double fc = fold_tiles(tiles, ntiles);  // block_sum (:53-54)
+    Record* rec = A.rec_base + st->pending_fix;
+    rec->candidate_objective = fc;
+    if (rec->accepted) st->fopt_exact = fc;  // :89-93
+    rec->incumbent_objective = st->fopt_exact;
+    *A.f_opt = st->fopt_exact;
+    st->pending_fix = -1;
+}
 
 // block_sum (core.cpp:165-175) by one thread: ordered tile folds, ordered fold of the tiles.
 __device__ __noinline__ double exact_block_sum(const double* v, uint64_t count) {
@@ -559,8 +690,10 @@ __device__ __forceinline__ void sum_interval(double s, uint64_t rows, unsigned c
     *hi = __dadd_ru(s, e);
 }
 
-// Fast-sum Lloyd control (thread 0 of the CTA that arrived last).
-__device__ __noinline__ void lloyd_fast_control(const LloydCtl& c, uint64_t rows, unsigned ctas) {
+// Fast-sum Lloyd control (thread 0 of the CTA that arrived last).  Returns the
+// accept decision (0/1) when the loop stopped and the control runs the accept,
+// else -1.
+__device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, uint64_t rows, unsigned ctas) {
     LloydStatus* st = c.st;
     const double s = __ldcg(&st->fsum);
     st->fsum = 0.0;
@@ -581,8 +714,10 @@ __device__ __noinline__ void lloyd_fast_control(const LloydCtl& c, uint64_t rows
         st->state_error = st->n_active == 0;
         st->bad_label = 0;
         st->exact_checks = 0;
-        return;
+        if (c.acc && c.fix_tiles) fix_record(st, *c.acc, c.fix_tiles, tiles_of(c.fix_rows));
+        return -1;
     }
+    int decision = -1;
     if (!st->stop) {
         st->evals += static_cast<unsigned long long>(rows) * st->n_active;
         if (st->n_active == 0) st->state_error = 1;
@@ -625,8 +760,18 @@ __device__ __noinline__ void lloyd_fast_control(const LloydCtl& c, uint64_t rows
         if (st->iterations >= c.max_iterations) stop = true;  // :32
         if (st->state_error || st->bad_label) stop = true;
         st->stop = stop ? 1 : 0;
+        if (stop && c.accept_run) {  // accept (:89): f < f_opt, strict, on the candidate's interval
+            const double fo = st->fopt_exact;
+            if (!c.force_exact && hi < fo) decision = 1;
+            else if (!c.force_exact && !(lo < fo)) decision = 0;
+            else decision = exact_block_sum(c.dists_pair + st->parity * c.dstride, rows) < fo;
+        } else if (!stop && c.incomplete_after && st->iterations >= c.incomplete_after) {
+            st->incomplete = 1;  // the host continues this chunk; the queued next chunk stays idle
+            st->go = 0;
+        }
     }
     if (c.use_cond) cudaGraphSetConditional(c.cond, st->stop ? 0u : 1u);
+    return decision;
 }
 
 // Called by thread 0 of the CTA that folded a tile: the CTA completing the last
@@ -805,7 +950,6 @@ struct ScreenConsts {
     float hi64;   // 1+g64, rounded up
 };
 
-constexpr int kSMaxK = 32;        // centroids handled by the screened path
 constexpr int kFailMax = 24;      // Lloyd-round bound failures handled per point
 constexpr int kSThreads = 256;    // 8 warps: warp w < KG owns centroids 4w..4w+3
 constexpr int kSXS = kABP + 4;    // fp32 slab stride (16-byte aligned rows)
@@ -1218,9 +1362,7 @@ struct TmaSmem {
     int icount[kABP];
     int lab_rank[kABP];                                        // chosen compacted centroid per point
     int rank_of[kSMaxK];                                       // label -> compacted index
-    short fail_list[kABP];                                     // points whose bound test failed
-    int nfail;
-    float dmax;
+    float delta[kSMaxK];                                       // centroid movement per label (rounded up)
     uint64_t bar[2];
     uint32_t n_items;
     int is_last;
@@ -1353,11 +1495,11 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx
     __syncthreads();
 }
 
-// hmode: 0 = screen; 1 = screen and record each point's certified lower bound
-// on its distance to every non-chosen centroid (lb_r, r-space); 2 = Lloyd round:
-// first the exact distance to the previous label, accepted for the whole CTA
-// when every point beats (lb_r - max centroid drift)^2 (1-g64) — the reference's
-// argmin is then provably unchanged and unique — else the full screen.
+// hmode: 0 = screen; 1 = screen and record the certified lower bound of every
+// (point, active label) distance (lbk, distance units); 2 = Lloyd round: the
+// exact distance to the previous label, then the bounds decayed by each
+// label's centroid movement decide which labels need an exact recheck
+// (Elkan-style; the reference's argmin is certified), else the full screen.
 template <typename T>
 __global__ void __launch_bounds__(kSThreads, 3)
 k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmc,
@@ -1369,7 +1511,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
              unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl,
-             int hmode, float* __restrict__ lb_r, const double* __restrict__ drift_part, int drift_slabs, int kfull,
+             int hmode, float* __restrict__ lbk, const double* __restrict__ drift_part, int drift_slabs, int kfull,
              uint64_t dstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
@@ -1378,6 +1520,15 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     constexpr unsigned kStageBytes = TmaSmem<T>::kRawBytes + kADC * kSMaxK * sizeof(float);
 
     klog_start(10 + hmode);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {  // independent of the previous kernel: overlaps its tail under PDL
+        tma_prefetch_map(&tmx);
+        tma_prefetch_map(&tmc);
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        fence_mbar_init();
+    }
+    pdl_wait();
     if (stop_ptr && *stop_ptr) return;
     if (ctl.go && !*ctl.go) return;
     const int KA = *n_active_ptr;
@@ -1389,12 +1540,11 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         labels_old = labels_pair + par * pair_stride;
         if (dists_out) dists_out += (1 - par) * dstride;  // dstride 0: one distance buffer
     }
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KG = (KA + kAK - 1) / kAK;
     const bool comp = warp < KG;
     const bool normw = warp == 7;
     const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
-    const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
+    const int np = p0 < rows ? static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0)) : 0;
     const float finf = __int_as_float(0x7F800000);
     const int nslab = (n + kADC - 1) / kADC;
     // reusable block (pass-1 buffers) for the staged exact chains; item list at its end
@@ -1407,121 +1557,176 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                       offsetof(TmaSmem<T>, xs) + 2 * kSMaxK * 18 * sizeof(double),
                   "centroid staging of tma_chains overlaps the item list");
     ktrace(0);
-    if (tid == 0) {
-        tma_prefetch_map(&tmx);
-        tma_prefetch_map(&tmc);
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
-        fence_mbar_init();
-    }
-    int qb = 0;  // TMA slabs this CTA has consumed (ring position)
+    int qb = 0;
+    if (np == 0) {  // fixup CTA of a begin launch: one tile of the pending chunk's final distances
+        const LloydStatus* st = ctl.st;
+        const int pend = st->pending_fix;
+        if (ctl.fix_tiles && pend >= 0) {
+            const uint64_t t = (p0 - rows) / kABP;  // fixup CTAs follow the point blocks
+            const uint64_t R = ctl.fix_rows, tb = t * kTile;
+            if (tb < R) {
+                const double* dv = ctl.dists_all + (2 * static_cast<uint64_t>(pend & 1) + st->fix_par) * R + tb;
+                const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), R - tb));
+                double* fbuf = reinterpret_cast<double*>(&S.raw[0][0]);
+                for (int i = tid; i < len; i += kSThreads) fbuf[i] = __ldcg(dv + i);
+                __syncthreads();
+                if (tid == 0) ctl.fix_tiles[t] = seq_fold_smem(fbuf, len);
+            }
+        }
+        goto fold;
+    }  // TMA slabs this CTA has consumed (ring position)
 
     // ---------------- Lloyd-round fast path (exact, certified) ----------------
-    if (hmode == 2 && labels_old && lb_r && drift_part) {
-        if (tid < kSMaxK) S.rank_of[tid] = -1;
-        if (tid == 0) S.nfail = 0;
+    // Per (point, label) lower bounds in distance units (lbk, written by the
+    // previous assignment) minus the label's centroid movement stay lower
+    // bounds.  A label whose decayed bound squared (x (1-g64)) exceeds the
+    // exact distance to the previous label cannot win or tie the reference's
+    // scan; the others are rechecked exactly.  Too many rechecks: full screen.
+    if (hmode == 2 && labels_old && lbk && drift_part) {
+        if (tid < kSMaxK) {
+            S.rank_of[tid] = -1;
+            S.delta[tid] = 0.f;
+        }
         __syncthreads();
         if (tid < KA) S.rank_of[act_idx[tid]] = tid;
-        if (tid == 32) {  // max drift of the active centroids since the bounds were taken
-            double dm = 0.0;
-            for (int r = 0; r < KA; ++r) {
-                const int j = act_idx[r];
-                double sj = 0.0;
-                for (int sl = 0; sl < drift_slabs; ++sl) sj += drift_part[sl * kfull + j];
-                dm = fmax(dm, sj);
-            }
-            // sqrt of an upper bound, rounded up with margin (atomic fp64 sums: order-free bound)
-            S.dmax = __double2float_ru(__dsqrt_ru(dm * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+        // per-label movement: a warp per label sums its slab parts (any order:
+        // a bound, taken with margin), square root rounded up
+        for (int r = warp; r < KA; r += kSThreads / 32) {
+            const int j = act_idx[r];
+            double sj = 0.0;
+            for (int sl = lane; sl < drift_slabs; sl += 32) sj += drift_part[sl * kfull + j];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) sj += __shfl_xor_sync(0xFFFFFFFFu, sj, o);
+            if (lane == 0) S.delta[j] = __double2float_ru(__dsqrt_ru(sj * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
         }
         __syncthreads();
         ktrace(13);
+        int a = -1, ra = -1;
         if (tid < np) {
-            const int a = labels_old[p0 + tid];
-            const int ra = (a >= 0 && a < kfull) ? S.rank_of[a] : -1;
-            S.lab_rank[tid] = ra;
+            a = labels_old[p0 + tid];
+            ra = (a >= 0 && a < kfull) ? S.rank_of[a] : -1;
             item_p[tid] = static_cast<short>(tid);
             item_j[tid] = static_cast<signed char>(ra < 0 ? 0 : ra);
         }
         ktrace(26);
         tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, static_cast<uint32_t>(np), item_p, item_j, item_d);
         qb += nslab;
+        // decay the bounds, test every other active label
+        unsigned fails = 0;
+        double dn = 0.0;
         if (tid < np) {
-            const uint64_t gp = p0 + tid;
-            const int ra = S.lab_rank[tid];
-            bool ok = false;
-            if (ra >= 0) {
-                const double dn = item_d[tid];
-                // every other centroid is now at least lb - dmax away (triangle inequality)
-                const float lbn = fmaxf(__fsub_rd(lb_r[gp], S.dmax), 0.f);
-                const float Lnew = __fmul_rd(__fmul_rd(lbn, lbn), cst.lo64);
-                ok = dn < static_cast<double>(Lnew);
-                if (ok) {  // the reference's scan provably returns the old label, uniquely
-                    labels_out[gp] = labels_old[gp];
-                    if (dists_out) dists_out[gp] = dn;
-                    lb_r[gp] = lbn;
+            dn = item_d[tid];
+            float4* row = reinterpret_cast<float4*>(lbk + (p0 + tid) * kSMaxK);
+#pragma unroll
+            for (int c4 = 0; c4 < kSMaxK / 4; ++c4) {
+                float4 v = __ldcg(row + c4);
+                float* vv = reinterpret_cast<float*>(&v);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = 4 * c4 + e;
+                    if (S.rank_of[j] < 0 || j == a) continue;
+                    const float lbn = fmaxf(__fsub_rd(vv[e], S.delta[j]), 0.f);
+                    vv[e] = lbn;
+                    const float L = __fmul_rd(__fmul_rd(lbn, lbn), cst.lo64);
+                    if (ra < 0 || !(dn < static_cast<double>(L))) fails |= 1u << j;
                 }
+                row[c4] = v;
             }
-            if (!ok) S.fail_list[atomicAdd(&S.nfail, 1)] = static_cast<short>(tid);
+        }
+        if (tid < kABP) S.cand[tid] = fails;
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of the per-point recheck counts -> item offsets
+            int v[4], run = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                v[q] = __popc(S.cand[4 * tid + q]);
+                run += v[q];
+            }
+            int incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            int ex = incl - run;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                S.icount[4 * tid + q] = ex;
+                ex += v[q];
+            }
+            if (tid == 31) S.n_items = static_cast<uint32_t>(incl);
         }
         __syncthreads();
-        ktrace(14);
-        const int nfail = S.nfail;
+        const uint32_t NI = S.n_items;
         if (tid == 0 && cand_counter) {
-            atomicAdd(cand_counter, static_cast<unsigned long long>(np - nfail + nfail * KA));
+            atomicAdd(cand_counter, static_cast<unsigned long long>(np + NI));
             atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
         }
 #ifdef BM_KTRACE
-        if (tid == 0) {  // fast-path statistics: [199990] CTAs, [199991] fallbacks, [199992] failed points
+        if (tid == 0) {  // fast-path statistics: [199990] CTAs, [199991] fallbacks, [199992] rechecked pairs
             atomicAdd(&g_ktrace[199990], 1ull);
-            if (nfail > kFailMax) atomicAdd(&g_ktrace[199991], 1ull);
-            atomicAdd(&g_ktrace[199992], static_cast<unsigned long long>(nfail));
+            if (NI > static_cast<uint32_t>(kItemCap)) atomicAdd(&g_ktrace[199991], 1ull);
+            atomicAdd(&g_ktrace[199992], static_cast<unsigned long long>(NI));
+            unsigned pts = 0;
+            for (int q = 0; q < kABP; ++q) pts += S.cand[q] != 0;
+            atomicAdd(&g_ktrace[199993], static_cast<unsigned long long>(pts));
         }
 #endif
-        if (nfail <= kFailMax) {
-            // the few points whose bound failed: a warp scans all active centroids
-            // exactly (lane j: centroid j), first minimum wins as in core.cpp:147
-            for (int f = warp; f < nfail; f += kSThreads / 32) {
-                const int p = S.fail_list[f];
-                const uint64_t gp = p0 + p;
-                double v = __longlong_as_double(0x7FF0000000000000LL);
-                if (lane < KA) {
-                    const double dj = exact_row_dist(X + gp * ld, Cact + static_cast<uint64_t>(lane) * ldc, n);
-                    if (!isnan(dj)) v = dj;
+        if (NI <= static_cast<uint32_t>(kItemCap)) {
+            // own-label distances stay in registers; the item list is rebuilt for the rechecks
+            if (tid < np) {
+                uint32_t it = S.icount[tid];
+                unsigned bits = fails;
+                while (bits) {  // ascending label = ascending compacted rank
+                    const int j = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    item_p[it] = static_cast<short>(tid);
+                    item_j[it] = static_cast<signed char>(S.rank_of[j]);
+                    ++it;
                 }
-                double bv = v;
-                int bj = lane;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
-                    const int oj = __shfl_xor_sync(0xFFFFFFFFu, bj, o);
-                    if (ov < bv || (ov == bv && oj < bj)) {
-                        bv = ov;
-                        bj = oj;
+            }
+            if (NI > static_cast<uint32_t>(kSThreads)) {
+                tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, NI, item_p, item_j, item_d);
+                qb += nslab;
+            } else if (NI > 0) {  // few rechecks: one thread per item, rows straight from L2
+                __syncthreads();
+                if (tid < static_cast<int>(NI))
+                    item_d[tid] = exact_row_dist(X + (p0 + item_p[tid]) * ld,
+                                                 Cact + static_cast<uint64_t>(item_j[tid]) * ldc, n);
+                __syncthreads();
+            }
+            if (tid < np) {
+                const uint64_t gp = p0 + tid;
+                // (value, label) minimum over the previous label and the rechecked ones:
+                // every other label is certified strictly farther (core.cpp:147)
+                const double inf = __longlong_as_double(0x7FF0000000000000LL);
+                double best = ra >= 0 ? dn : inf;
+                int bl = ra >= 0 ? a : -1;
+                const uint32_t i0 = S.icount[tid], i1 = i0 + __popc(fails);
+                float* row = lbk + gp * kSMaxK;
+                const double hi = static_cast<double>(cst.hi64);
+                auto lbound = [&](double d) {  // true distance >= fl64 distance / (1+g64)
+                    const double q = __dsub_rd(__ddiv_rd(d, hi), 1e-300);
+                    return q > 0.0 ? (q < 3.0e38 ? __fsqrt_rd(__double2float_rd(q)) : 1.0e19f) : 0.f;
+                };
+                for (uint32_t i = i0; i < i1; ++i) {
+                    const double d = item_d[i];
+                    const int l = act_idx[item_j[i]];
+                    row[l] = lbound(d);
+                    if (d < best || (d == best && l < bl)) {
+                        best = d;
+                        bl = l;
                     }
                 }
-                const bool found = bv < __longlong_as_double(0x7FF0000000000000LL);
-                double m2 = lane == bj ? __longlong_as_double(0x7FF0000000000000LL) : v;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) m2 = fmin(m2, __shfl_xor_sync(0xFFFFFFFFu, m2, o));
-                if (lane == 0) {
-                    const int label = found ? act_idx[bj] : -1;
-                    labels_out[gp] = label;
-                    if (dists_out) dists_out[gp] = found ? bv : __longlong_as_double(0x7FF0000000000000LL);
-                    if (labels_old[gp] != label) *changed_flag = 1;
-                    // true distance to every other centroid >= fl64 distance / hi64
-                    float lb = 3.0e38f;
-                    if (m2 < __longlong_as_double(0x7FF0000000000000LL)) {
-                        const double q = __dsub_rd(__ddiv_rd(m2, static_cast<double>(cst.hi64)), 1e-300);
-                        lb = q > 0.0 ? __fsqrt_rd(__double2float_rd(q)) : 0.f;
-                    }
-                    lb_r[gp] = lb;
-                }
+                if (ra >= 0) row[a] = lbound(dn);
+                labels_out[gp] = bl;
+                if (dists_out) dists_out[gp] = best;
+                if (bl != a) *changed_flag = 1;
             }
             ktrace(15);
             goto fold;
         }
-        // many failures: full screen of the block
-        // (the fast-path writes above are recomputed identically)
+        // many rechecks: full screen of the block (rewrites labels, distances, bounds)
         __syncthreads();
     }
     {
@@ -1739,29 +1944,35 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         if (labels_old && labels_old[gp] != label) *changed_flag = 1;
         S.lab_rank[p] = bj;
     }
-    if (hmode >= 1 && lb_r) {  // lower bound to every centroid but the chosen one (r-space)
+    if (hmode >= 1 && lbk) {  // per (point, label) lower bounds in distance units, staged for coalesced rows
         __syncthreads();
+        float* lbt = reinterpret_cast<float*>(&S.raw[0][0]);  // [128][32], column j ^ (p & 31)
         if (comp) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int p = 4 * lane + q;
-                float m = finf;
 #pragma unroll
-                for (int u = 0; u < kAK; ++u)
-                    if (kAK * warp + u != S.lab_rank[p]) m = fminf(m, Lk[q][u]);
-                S.red_u[warp][p] = m;
+                for (int u = 0; u < kAK; ++u) {
+                    const int c = kAK * warp + u;
+                    if (c < KA) lbt[p * kSMaxK + (act_idx[c] ^ (p & 31))] = __fsqrt_rd(Lk[q][u]);
+                }
             }
         }
         __syncthreads();
-        if (tid < np) {
-            float m = finf;
-            for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][tid]);
-            lb_r[p0 + tid] = m < finf ? __fsqrt_rd(m) : 3.0e38f;
+        for (int e = tid; e < np * (kSMaxK / 4); e += kSThreads) {
+            const int p = e >> 3, c4 = (e & 7) * 4;
+            float4 v;
+            v.x = lbt[p * kSMaxK + ((c4 + 0) ^ (p & 31))];
+            v.y = lbt[p * kSMaxK + ((c4 + 1) ^ (p & 31))];
+            v.z = lbt[p * kSMaxK + ((c4 + 2) ^ (p & 31))];
+            v.w = lbt[p * kSMaxK + ((c4 + 3) ^ (p & 31))];
+            reinterpret_cast<float4*>(lbk + (p0 + p) * kSMaxK)[e & 7] = v;
         }
     }
     }
 fold:
     ktrace(10);
+    pdl_trigger();
     if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
         __syncthreads();  // distances of this CTA written (some by other threads)
         double v = tid < np ? dists_out[p0 + tid] : 0.0;
@@ -1776,12 +1987,19 @@ fold:
             atomicAdd(&ctl.st->fsum, c);
             __threadfence();
             const unsigned done = atomicAdd(&ctl.st->ctas_done, 1u);
-            if (done == gridDim.x - 1) {
-                __threadfence();
-                lloyd_fast_control(ctl, rows, gridDim.x);
-                klog_end(10 + hmode);
-            }
+            S.is_last = done == gridDim.x - 1;
         }
+        __syncthreads();
+        if (!S.is_last) return;
+        __threadfence();
+        if (tid == 0) S.n_items = static_cast<uint32_t>(lloyd_fast_control(ctl, rows, gridDim.x));
+        __syncthreads();
+        const int decision = static_cast<int>(S.n_items);
+        if (decision >= 0)
+            accept_body(ctl.st, *ctl.acc, decision, true, ctl.host_st, reinterpret_cast<int*>(&S.raw[0][0]));
+        else if (ctl.host_st && ctl.st->incomplete)
+            status_to_host(ctl.st, ctl.host_st);
+        if (tid == 0) klog_end(10 + hmode);
         return;
     }
     if (!tile_out) return;
@@ -1888,6 +2106,7 @@ struct UpdateArgs {
     unsigned* slab_ctr;      // [slabs] arrival counters (reset by the last merger)
     unsigned* slab_done;     // [slabs] mergers finished
     int mergers;             // G: CTAs merging each slab
+    const int* go;           // when set and *go == 0 the launch does nothing (skipped chunk)
     unsigned* slab_tot;      // [slabs][k] label totals (reset by the merging CTA)
     double* C;               // [k][n]
     uint8_t* mask;
@@ -1907,7 +2126,9 @@ k_update(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
          const int32_t* __restrict__ labels_pair, uint64_t pair_stride,
          const int* __restrict__ parity_ptr, int k, int dslab, UpdateArgs u) {
     klog_start(2);
+    pdl_wait();
     if (u.stop && *u.stop) return;
+    if (u.go && !*u.go) return;
     extern __shared__ __align__(16) unsigned char ush_raw[];
     ktrace_u(0);
     int* ush = reinterpret_cast<int*>(ush_raw);
@@ -2027,6 +2248,7 @@ k_update(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         u.psum[(static_cast<uint64_t>(d0 + dd) * k + j) * u.tstride + tile] = acc;
     }
 
+    pdl_trigger();
     // ---- the last G CTAs of this slab merge it, pairs g, g + G, ... each ----
     // (they wait for the slab's other CTAs: those hold no resources the
     // waiting ones need, so they always complete)
@@ -2130,11 +2352,14 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
                           double* __restrict__ Cact, int ldc, int* __restrict__ act_idx, int* __restrict__ n_active,
                           float* __restrict__ CT32) {
     extern __shared__ int csh[];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) csh[j] = mask[j];  // staged: the rank loop is serial
+    __syncthreads();
     if (threadIdx.x == 0) {
         int r = 0;
         for (int j = 0; j < k; ++j) {
-            csh[j] = mask[j] ? -1 : r;
-            if (!mask[j]) act_idx[r++] = j;
+            const bool deg = csh[j] != 0;
+            csh[j] = deg ? -1 : r;
+            if (!deg) act_idx[r++] = j;
         }
         *n_active = r;
     }
@@ -2156,91 +2381,15 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
 // device so the chunk can run inside a CUDA graph.  The incumbent is also
 // written in compacted form (Cact/act/n_active/CT32): it is the next chunk's
 // start (:82) when no repair is needed.
-__global__ void k_accept(LloydStatus* st, double* f_opt, double* __restrict__ C,
-                         uint8_t* __restrict__ mask, double* __restrict__ Cinc,
-                         uint8_t* __restrict__ maskinc, int k, int n, Record* rec_base,
-                         unsigned long long* chunk_ctr, double* __restrict__ Cact, int ldc,
-                         int* __restrict__ act_idx, float* __restrict__ CT32,
-                         const double* __restrict__ dists_pair, uint64_t dstride, uint64_t rows,
-                         double* __restrict__ tile_buf, unsigned* __restrict__ counter, const int* go,
-                         LloydStatus* host_st) {
-    extern __shared__ int arank[];  // [k]
+__global__ void k_accept(LloydStatus* st, AcceptArgs A, LloydStatus* host_st) {
+    extern __shared__ int asm_[];  // [2k]
     __shared__ int accepted;
     klog_start(3);
-    if (go && !*go) return;
-    if (dists_pair && gridDim.x <= kTile) {  // fast-sum control: the exact objective (:53-54) = block_sum of the final distances
-        __shared__ __align__(16) double fbuf[kTile];
-        __shared__ int last;
-        const double* dv = dists_pair + st->parity * dstride;
-        const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
-        const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), rows - tb));
-        for (int i = threadIdx.x; i < len; i += blockDim.x) fbuf[i] = __ldcg(dv + tb + i);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            tile_buf[blockIdx.x] = seq_fold_smem(fbuf, len);
-            __threadfence();
-            last = atomicAdd(counter, 1u) == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (!last) return;
-        __threadfence();
-        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) fbuf[i] = __ldcg(tile_buf + i);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            *counter = 0u;
-            st->objective = seq_fold_smem(fbuf, gridDim.x);
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const unsigned long long chunk = *chunk_ctr;
-        Record* rec = rec_base + chunk;
-        accepted = st->objective < *f_opt;  // strict (:89)
-        if (accepted) *f_opt = st->objective;
-        rec->chunk_index = chunk;
-        rec->candidate_objective = st->objective;
-        rec->incumbent_objective = *f_opt;
-        rec->accepted = accepted;
-        rec->degenerate_repaired = static_cast<unsigned long long>(st->inc_degenerate);
-    }
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x == 0) accepted = st->objective < *A.f_opt;  // strict (:89)
     __syncthreads();
-    if (accepted) {
-        for (int e = threadIdx.x; e < k * n; e += blockDim.x) Cinc[e] = C[e];
-        for (int j = threadIdx.x; j < k; j += blockDim.x) maskinc[j] = mask[j];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int dcount = 0, r = 0;
-        for (int j = 0; j < k; ++j) {
-            dcount += maskinc[j] ? 1 : 0;
-            arank[j] = maskinc[j] ? -1 : r;
-            if (!maskinc[j]) act_idx[r++] = j;
-        }
-        st->inc_degenerate = dcount;
-        st->go = dcount == 0;
-        st->n_active = r;
-        *chunk_ctr += 1;
-    }
-    __syncthreads();
-    // the next chunk's start (:82): (C, mask) := incumbent, and its compacted form
-    if (!accepted)
-        for (int j = threadIdx.x; j < k; j += blockDim.x) mask[j] = maskinc[j];
-    for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
-        const int j = e / n, d = e % n, rk = arank[j];
-        const double v = Cinc[e];
-        if (!accepted) C[e] = v;
-        if (rk < 0) continue;
-        Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
-        if (CT32 && rk < kSMaxK) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
-    }
-    if (host_st) {  // the status straight into mapped pinned host memory (no copy node)
-        __syncthreads();
-        constexpr int kW = sizeof(LloydStatus) / 8;
-        for (int i = threadIdx.x; i < kW; i += blockDim.x)
-            reinterpret_cast<volatile unsigned long long*>(host_st)[i] =
-                reinterpret_cast<const volatile unsigned long long*>(st)[i];
-        __threadfence_system();
-    }
+    accept_body(st, A, accepted, false, host_st, asm_);
     if (threadIdx.x == 0) klog_end(3);
 }
 
@@ -2250,6 +2399,30 @@ __global__ void k_guard(const LloydStatus* st, cudaGraphConditionalHandle h) {
     klog_start(0);
     cudaGraphSetConditional(h, st->go != 0 ? 1u : 0u);
     klog_end(0);
+}
+
+// The last chunk's record: its exact objective (graph mode, after the loop).
+__global__ void k_fix_final(LloydStatus* st, AcceptArgs A, const double* __restrict__ dists_all, uint64_t R,
+                            double* __restrict__ tiles, unsigned* __restrict__ counter) {
+    __shared__ __align__(16) double fbuf[kTile];
+    __shared__ int last;
+    const int pend = st->pending_fix;
+    if (pend < 0) return;
+    const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
+    const double* dv = dists_all + (2 * static_cast<uint64_t>(pend & 1) + st->fix_par) * R + tb;
+    const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), R - tb));
+    for (int i = threadIdx.x; i < len; i += blockDim.x) fbuf[i] = __ldcg(dv + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tiles[blockIdx.x] = seq_fold_smem(fbuf, len);
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        if (last) {
+            __threadfence();
+            *counter = 0u;
+            fix_record(st, A, tiles, gridDim.x);
+        }
+    }
 }
 
 // Reset of the per-run device state (incumbent all degenerate, f_opt = +inf).
@@ -2262,6 +2435,9 @@ __global__ void k_run_init(LloydStatus* st, double* f_opt, double* Cinc, uint8_t
         st->inc_degenerate = k;
         st->go = 0;
         st->stop = 1;  // a skipped chunk's rounds see a finished loop
+        st->fopt_exact = __longlong_as_double(0x7FF0000000000000LL);
+        st->pending_fix = -1;
+        st->incomplete = 0;
         *chunk_ctr = 0;
     }
 }

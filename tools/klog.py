@@ -25,13 +25,23 @@ buf = np.zeros(200001 + 3 * 60000, np.uint64)
 lib = _capi.load()
 lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
 n0 = int(buf[200000])
-st0 = buf[199990:199993].astype(np.int64)
+st0 = buf[199990:199994].astype(np.int64)
 bm.big_means(d, cfg, want_labels=False)
 lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
 n1 = int(buf[200000])
-st1 = buf[199990:199993].astype(np.int64)
+st1 = buf[199990:199994].astype(np.int64)
 E = buf[200001:200001 + 3 * 60000].reshape(-1, 3).astype(np.int64)[n0 % 60000:n1 % 60000]
-names = {0: "guard", 2: "update", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)"}
+names = {0: "guard", 2: "update", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)",
+         4: "accept:folded", 5: "accept:objective", 6: "accept:record", 7: "accept:ranks"}
+sub = E[(E[:, 0] >= 4) & (E[:, 0] <= 7)]
+E = E[(E[:, 0] < 4) | (E[:, 0] > 7)]
+acc = E[E[:, 0] == 3]
+for kid in range(4, 8):  # sub-phase marks: end time relative to the enclosing accept's start
+    ends = sub[sub[:, 0] == kid, 2]
+    offs = [t - acc[(acc[:, 1] <= t) & (acc[:, 2] >= t), 1][0] for t in ends
+            if ((acc[:, 1] <= t) & (acc[:, 2] >= t)).any()]
+    if offs:
+        print(f"  {names[kid]:18s} at {np.mean(offs) / 1e3:7.2f} us after the accept's start")
 E = E[np.argsort(E[:, 1])]
 print(f"{len(E)} kernels over {chunks} chunks; span {(E[-1, 2] - E[0, 1]) / 1e3:.1f} us "
       f"({(E[-1, 2] - E[0, 1]) / 1e3 / chunks:.1f} us per chunk)")
@@ -55,4 +65,4 @@ for key, v in sorted(pairs.items(), key=lambda kv: -sum(kv[1])):
     print(f"  gap {key[0]:>14s} -> {key[1]:14s} n={len(v):5d} mean={np.mean(v):6.2f} us")
 ds = st1 - st0
 print(f"round fast path: {ds[0]} CTAs, {ds[1]} fell back to the screen ({100 * ds[1] / max(ds[0], 1):.1f}%), "
-      f"{ds[2] / max(ds[0], 1):.2f} failed points per CTA")
+      f"{ds[2] / max(ds[0], 1):.2f} rechecked pairs and {ds[3] / max(ds[0], 1):.2f} points with rechecks per CTA")
