@@ -148,6 +148,8 @@ struct Workspace {
     DevBuf<float> lbk;       // R x 32: lower bound (distance units) of every (point, label) distance
     DevBuf<double> drift_part;  // [n][k]: squared centroid movement of the last update, per d-slab
     int drift_slabs = 0;        // d-slabs of the last update launch (host view at enqueue/capture time)
+    DevBuf<float> delta;        // [k]: movement per label of the last update (distance units, rounded up)
+    DevBuf<unsigned> all_done;  // fused update: mergers finished
     DevBuf<unsigned> slab_ctr, slab_done, slab_tot;  // [n], [n], [n][k]: fused update counters / label totals
     // K-means++ (init.cpp:123-201)
     DevBuf<double> d2pool;   // (ncand + 1) * R
@@ -223,6 +225,10 @@ struct Workspace {
         BM_CUDA(cudaMemset(drift_part.p, 0, (uint64_t)n * k * 8 * sizeof(double)));
         slab_ctr.alloc(n);
         BM_CUDA(cudaMemset(slab_ctr.p, 0, n * sizeof(unsigned)));
+        delta.alloc(k);
+        BM_CUDA(cudaMemset(delta.p, 0, k * sizeof(float)));
+        all_done.alloc(1);
+        BM_CUDA(cudaMemset(all_done.p, 0, sizeof(unsigned)));
         slab_done.alloc(n);
         BM_CUDA(cudaMemset(slab_done.p, 0, n * sizeof(unsigned)));
         slab_tot.alloc((uint64_t)n * k);
@@ -640,8 +646,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                 tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                 g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
-                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, w.lbk.p, w.drift_part.p,
-                w.drift_slabs, k,
+                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, w.lbk.p, w.delta.p, k,
                 dstride);
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
@@ -717,7 +722,7 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
     // (waiting mergers never exceed one per SM, so the CTAs they wait for always get a slot)
     int G = (int)std::min<uint64_t>({tiles, (uint64_t)8, std::max<uint64_t>(1, ceil_div((uint64_t)k * dslab, 48))});
     while (G > 1 && (uint64_t)G * slabs > 148) --G;
-    dev::UpdateArgs u{w.psum.p, tstride, shm, w.slab_ctr.p, w.slab_done.p, G, go, w.slab_tot.p, w.C.p, w.mask.p, w.Cact.p, w.ldc,
+    dev::UpdateArgs u{w.psum.p, tstride, shm, w.slab_ctr.p, w.slab_done.p, G, go, w.all_done.p, w.delta.p, w.slab_tot.p, w.C.p, w.mask.p, w.Cact.p, w.ldc,
                       w.act.p, &w.status.p->n_active, w.CT32.p, w.drift_part.p, &w.status.p->bad_label, stop};
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);

@@ -69,11 +69,11 @@ struct Record {
 // Optional per-CTA phase timestamps (build with -DBM_KTRACE; tools/ktrace.py).
 #ifdef BM_KTRACE
 __device__ unsigned long long g_ktrace[1 << 20];
-__device__ __forceinline__ void ktrace(int slot) {
+__device__ __forceinline__ void ktrace(int slot, int hm = 0) {  // region by assignment mode (0 / 1 / 2)
     if (threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        unsigned long long* row = g_ktrace + (blockIdx.x & 2047) * 32;
+        unsigned long long* row = g_ktrace + (hm == 0 ? 0 : hm == 1 ? 400000 : 470000) + (blockIdx.x & 2047) * 32;
         if (slot == 0)
             for (int i = 1; i < 32; ++i) row[i] = 0;
         row[slot] = t;
@@ -110,7 +110,7 @@ __device__ __forceinline__ void klog_end(int id) {
     g_ktrace[200003 + 3 * i] = t;
 }
 #else
-__device__ __forceinline__ void ktrace(int) {}
+__device__ __forceinline__ void ktrace(int, int = 0) {}
 __device__ __forceinline__ void ktrace_u(int) {}
 __device__ __forceinline__ void klog_start(int) {}
 __device__ __forceinline__ void klog_end(int) {}
@@ -559,12 +559,13 @@ struct LloydCtl {
 };
 
 // The status straight into mapped pinned host memory (no copy node); CTA-wide.
+// The host reads it after synchronizing with the kernel's completion, which
+// orders the writes (no system fence needed here).
 __device__ __forceinline__ void status_to_host(const LloydStatus* st, LloydStatus* host_st) {
     constexpr int kW = sizeof(LloydStatus) / 8;
     for (int i = threadIdx.x; i < kW; i += blockDim.x)
         reinterpret_cast<volatile unsigned long long*>(host_st)[i] =
             reinterpret_cast<const volatile unsigned long long*>(st)[i];
-    __threadfence_system();
 }
 
 // Accept step state (big_means.cpp:63-64, 89-94).
@@ -590,8 +591,10 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
                                          LloydStatus* host_st, int* sm) {
     const int k = A.k, n = A.n;
     __shared__ int acc_s;
+    __shared__ unsigned long long chunk_s;
     if (threadIdx.x == 0) {
         const unsigned long long chunk = *A.chunk_ctr;
+        chunk_s = chunk;
         Record* rec = A.rec_base + chunk;
         if (deferred) {
             rec->candidate_objective = __longlong_as_double(0x7FF8000000000000LL);
@@ -609,11 +612,24 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         acc_s = accepted;
     }
     __syncthreads();
+    ktrace(11, 2);
     accepted = acc_s;
     int* arank = sm;
     int* mk = sm + k;  // incumbent mask staged in shared memory (the rank loop below is serial)
     if (accepted) {
-        for (int e = threadIdx.x; e < k * n; e += blockDim.x) A.Cinc[e] = A.C[e];
+        for (int e0 = threadIdx.x; e0 < k * n; e0 += 8 * blockDim.x) {  // loads batched ahead of the stores
+            double v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int e = e0 + r * blockDim.x;
+                v[r] = e < k * n ? A.C[e] : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int e = e0 + r * blockDim.x;
+                if (e < k * n) A.Cinc[e] = v[r];
+            }
+        }
         for (int j = threadIdx.x; j < k; j += blockDim.x) {
             const uint8_t v = A.mask[j];
             A.maskinc[j] = v;
@@ -634,19 +650,30 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         st->go = dcount == 0;
         st->n_active = r;
         st->incomplete = 0;
-        *A.chunk_ctr += 1;
+        *A.chunk_ctr = chunk_s + 1;
     }
     __syncthreads();
+    ktrace(12, 2);
     // the next chunk's start (:82): (C, mask) := incumbent, and its compacted form
     if (!accepted)
         for (int j = threadIdx.x; j < k; j += blockDim.x) A.mask[j] = static_cast<uint8_t>(mk[j]);
-    for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
-        const int j = e / n, d = e - j * n, rk = arank[j];
-        const double v = A.Cinc[e];
-        if (!accepted) A.C[e] = v;
-        if (rk < 0) continue;
-        A.Cact[static_cast<uint64_t>(rk) * A.ldc + d] = v;
-        if (A.CT32 && rk < kSMaxK) A.CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+    for (int e0 = threadIdx.x; e0 < k * n; e0 += 8 * blockDim.x) {  // loads batched ahead of the stores
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = e0 + r * blockDim.x;
+            v[r] = e < k * n ? A.Cinc[e] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = e0 + r * blockDim.x;
+            if (e >= k * n) continue;
+            const int j = e / n, d = e - j * n, rk = arank[j];
+            if (!accepted) A.C[e] = v[r];
+            if (rk < 0) continue;
+            A.Cact[static_cast<uint64_t>(rk) * A.ldc + d] = v[r];
+            if (A.CT32 && rk < kSMaxK) A.CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v[r]);
+        }
     }
     if (host_st) {
         __syncthreads();
@@ -658,7 +685,16 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
 // ordered tile partials of its final distances).
 __device__ __forceinline__ void fix_record(LloydStatus* st, const AcceptArgs& A, const double* tiles, uint64_t ntiles) {
     if (st->pending_fix < 0) return;
-    const double fc = fold_tiles(tiles, ntiles);  // block_sum (:53-54)
+    double fc = 0.0;  // block_sum (:53-54): ordered fold of the tile partials (shared or fresh global memory)
+    uint64_t t = 0;
+    for (; t + 8 <= ntiles; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = tiles[t + r];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) fc = __dadd_rn(fc, v[r]);
+    }
+    for (; t < ntiles; ++t) fc = __dadd_rn(fc, tiles[t]);
     Record* rec = A.rec_base + st->pending_fix;
     rec->candidate_objective = fc;
     if (rec->accepted) st->fopt_exact = fc;  // :89-93
@@ -693,9 +729,8 @@ __device__ __forceinline__ void sum_interval(double s, uint64_t rows, unsigned c
 // Fast-sum Lloyd control (thread 0 of the CTA that arrived last).  Returns the
 // accept decision (0/1) when the loop stopped and the control runs the accept,
 // else -1.
-__device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, uint64_t rows, unsigned ctas) {
-    LloydStatus* st = c.st;
-    const double s = __ldcg(&st->fsum);
+__device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* st, uint64_t rows, unsigned ctas) {
+    const double s = st->fsum;
     st->fsum = 0.0;
     st->ctas_done = 0u;
     double lo, hi;
@@ -723,7 +758,7 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, uint64_t rows,
         if (st->n_active == 0) st->state_error = 1;
         st->iterations += 1;  // :36
         st->objective = nan;
-        const bool unchanged = __ldcg(&st->changed) == 0;  // :39
+        const bool unchanged = st->changed == 0;  // :39
         st->changed = 0;
         const int par = st->parity;
         st->parity ^= 1;  // :40-41
@@ -1452,7 +1487,7 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx
         if (sl + 1 < nslab) cp_async_wait<1>();
         else cp_async_wait<0>();
         mbar_wait(&S.bar[st], (q >> 1) & 1);
-        if (qb == 0 && sl < 5) ktrace(16 + 2 * sl);
+        if (qb == 0 && sl < 5) ktrace(16 + 2 * sl, 2);
         __syncthreads();  // everyone's centroid pieces landed
         const int dl = min(kADC, n - sl * kADC);
         const unsigned char* raw = S.raw[st];
@@ -1486,7 +1521,7 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx
             acc[r] = a;
         }
         __syncthreads();  // stage st consumed
-        if (qb == 0 && sl < 5) ktrace(17 + 2 * sl);
+        if (qb == 0 && sl < 5) ktrace(17 + 2 * sl, 2);
         if (sl + 2 < nslab) issue(sl + 2);
     }
 #pragma unroll
@@ -1511,7 +1546,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
              unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl,
-             int hmode, float* __restrict__ lbk, const double* __restrict__ drift_part, int drift_slabs, int kfull,
+             int hmode, float* __restrict__ lbk, const float* __restrict__ delta, int kfull,
              uint64_t dstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
@@ -1556,7 +1591,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     static_assert(offsetof(TmaSmem<T>, red_u) - kItemCap * (sizeof(double) + 3) >=
                       offsetof(TmaSmem<T>, xs) + 2 * kSMaxK * 18 * sizeof(double),
                   "centroid staging of tma_chains overlaps the item list");
-    ktrace(0);
+    ktrace(0, hmode);
     int qb = 0;
     if (np == 0) {  // fixup CTA of a begin launch: one tile of the pending chunk's final distances
         const LloydStatus* st = ctl.st;
@@ -1582,25 +1617,19 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     // bounds.  A label whose decayed bound squared (x (1-g64)) exceeds the
     // exact distance to the previous label cannot win or tie the reference's
     // scan; the others are rechecked exactly.  Too many rechecks: full screen.
-    if (hmode == 2 && labels_old && lbk && drift_part) {
+    if (hmode == 2 && labels_old && lbk && delta) {
         if (tid < kSMaxK) {
             S.rank_of[tid] = -1;
             S.delta[tid] = 0.f;
         }
         __syncthreads();
         if (tid < KA) S.rank_of[act_idx[tid]] = tid;
-        // per-label movement: a warp per label sums its slab parts (any order:
-        // a bound, taken with margin), square root rounded up
-        for (int r = warp; r < KA; r += kSThreads / 32) {
-            const int j = act_idx[r];
-            double sj = 0.0;
-            for (int sl = lane; sl < drift_slabs; sl += 32) sj += drift_part[sl * kfull + j];
-#pragma unroll
-            for (int o = 16; o; o >>= 1) sj += __shfl_xor_sync(0xFFFFFFFFu, sj, o);
-            if (lane == 0) S.delta[j] = __double2float_ru(__dsqrt_ru(sj * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+        if (tid < KA) {  // per-label movement of the last update (k_update's last merger)
+            const int j = act_idx[tid];
+            S.delta[j] = delta[j];
         }
         __syncthreads();
-        ktrace(13);
+        ktrace(13, hmode);
         int a = -1, ra = -1;
         if (tid < np) {
             a = labels_old[p0 + tid];
@@ -1608,7 +1637,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             item_p[tid] = static_cast<short>(tid);
             item_j[tid] = static_cast<signed char>(ra < 0 ? 0 : ra);
         }
-        ktrace(26);
+        ktrace(26, hmode);
         tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, static_cast<uint32_t>(np), item_p, item_j, item_d);
         qb += nslab;
         // decay the bounds, test every other active label
@@ -1723,7 +1752,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 if (dists_out) dists_out[gp] = best;
                 if (bl != a) *changed_flag = 1;
             }
-            ktrace(15);
+            ktrace(15, hmode);
             goto fold;
         }
         // many rechecks: full screen of the block (rewrites labels, distances, bounds)
@@ -1754,7 +1783,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     for (int sl = 0; sl < nslab; ++sl) {
         const int q = qb + sl, st = q & 1, dl = min(kADC, n - sl * kADC);
         mbar_wait(&S.bar[st], (q >> 1) & 1);
-        if (sl < 6) ktrace(1 + sl);
+        if (sl < 6) ktrace(1 + sl, hmode);
         // raw (swizzled [p][d], storage type) -> fp32 [d][p], once per element
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -1817,7 +1846,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         S.ncr[lane] = __fsqrt_ru(nch);
     }
     __syncthreads();
-    ktrace(7);
+    ktrace(7, hmode);
     // certified bounds: upper bounds first, then each warp tests its lower
     // bounds against the point's minimum U and sets candidate bits.
     float Lk[4][kAK];
@@ -1895,7 +1924,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     __syncthreads();
     const uint32_t NI = S.n_items;
     const bool overflow = NI > static_cast<uint32_t>(kItemCap);
-    ktrace(8);
+    ktrace(8, hmode);
     // ---- pass 2: exact fp64 recheck of the candidates ----
     if (!overflow) {
         if (tid < np) {
@@ -1912,7 +1941,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         }
         tma_chains<T>(S, &tmx, p0, n, nslab, qb + nslab, Cact, ldc, KA, NI, item_p, item_j, item_d);
     }
-    ktrace(9);
+    ktrace(9, hmode);
     if (tid < np) {
         const int p = tid;
         const uint64_t gp = p0 + p;
@@ -1968,10 +1997,11 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             v.w = lbt[p * kSMaxK + ((c4 + 3) ^ (p & 31))];
             reinterpret_cast<float4*>(lbk + (p0 + p) * kSMaxK)[e & 7] = v;
         }
+        ktrace(27, hmode);
     }
     }
 fold:
-    ktrace(10);
+    ktrace(10, hmode);
     pdl_trigger();
     if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
         __syncthreads();  // distances of this CTA written (some by other threads)
@@ -1992,13 +2022,33 @@ fold:
         __syncthreads();
         if (!S.is_last) return;
         __threadfence();
-        if (tid == 0) S.n_items = static_cast<uint32_t>(lloyd_fast_control(ctl, rows, gridDim.x));
+        ktrace(28, hmode);
+        // the status in shared memory while this CTA runs the control (and the accept)
+        LloydStatus* sst = reinterpret_cast<LloydStatus*>(&S.red_u[0][0]);
+        constexpr int kW = sizeof(LloydStatus) / 8;
+        for (int i = tid; i < kW; i += kSThreads)
+            reinterpret_cast<unsigned long long*>(sst)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(ctl.st) + i);
+        LloydCtl cl = ctl;  // the fixup tile partials staged in shared memory for the control's fold
+        if (ctl.fix_tiles) {
+            double* ft = reinterpret_cast<double*>(&S.raw[0][0]) + 1024;
+            const int nt = static_cast<int>(tiles_of(ctl.fix_rows));
+            if (nt <= 1024) {
+                for (int i = tid; i < nt; i += kSThreads) ft[i] = __ldcg(ctl.fix_tiles + i);
+                cl.fix_tiles = ft;
+            }
+        }
         __syncthreads();
+        if (tid == 0) S.n_items = static_cast<uint32_t>(lloyd_fast_control(cl, sst, rows, gridDim.x));
+        __syncthreads();
+        ktrace(29, hmode);
         const int decision = static_cast<int>(S.n_items);
         if (decision >= 0)
-            accept_body(ctl.st, *ctl.acc, decision, true, ctl.host_st, reinterpret_cast<int*>(&S.raw[0][0]));
-        else if (ctl.host_st && ctl.st->incomplete)
-            status_to_host(ctl.st, ctl.host_st);
+            accept_body(sst, *ctl.acc, decision, true, nullptr, reinterpret_cast<int*>(&S.raw[0][0]));
+        __syncthreads();
+        for (int i = tid; i < kW; i += kSThreads)
+            reinterpret_cast<unsigned long long*>(ctl.st)[i] = reinterpret_cast<const unsigned long long*>(sst)[i];
+        if (ctl.host_st && (decision >= 0 || sst->incomplete)) status_to_host(sst, ctl.host_st);
+        ktrace(30, hmode);
         if (tid == 0) klog_end(10 + hmode);
         return;
     }
@@ -2013,7 +2063,7 @@ fold:
         S.is_last = old == ctas - 1;
     }
     __syncthreads();
-    ktrace(11);
+    ktrace(11, hmode);
     if (!S.is_last) return;
     __threadfence();
     const uint64_t tb = tile * kTile;
@@ -2036,7 +2086,7 @@ fold:
         }
         for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
         tile_out[tile] = a;
-        ktrace(12);
+        ktrace(12, hmode);
         tile_counter[tile] = 0u;
         tile_done_control(ctl, tile_out, rows);
     }
@@ -2107,6 +2157,8 @@ struct UpdateArgs {
     unsigned* slab_done;     // [slabs] mergers finished
     int mergers;             // G: CTAs merging each slab
     const int* go;           // when set and *go == 0 the launch does nothing (skipped chunk)
+    unsigned* all_done;      // mergers finished (all slabs)
+    float* delta;            // [k] movement per label of this update (rounded up)
     unsigned* slab_tot;      // [slabs][k] label totals (reset by the merging CTA)
     double* C;               // [k][n]
     uint8_t* mask;
@@ -2343,7 +2395,25 @@ k_update(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         u.slab_done[slab] = 0u;
         __threadfence();
         u.slab_ctr[slab] = 0u;
-        if (slab == gridDim.y - 1) klog_end(2);
+    }
+    // the very last merger turns the parts into each label's movement (distance
+    // units, rounded up with margin: only bounds use it)
+    __shared__ int lastm;
+    if (threadIdx.x == 0) lastm = atomicAdd(u.all_done, 1u) == static_cast<unsigned>(G) * gridDim.y - 1;
+    __syncthreads();
+    if (!lastm) return;
+    __threadfence();
+    const int parts = G * static_cast<int>(gridDim.y);
+    for (int j = warp; j < k; j += kUWarps) {  // a warp per label, lanes over the parts (any order)
+        double sj = 0.0;
+        for (int q = lane; q < parts; q += 32) sj += __ldcg(&u.drift_part[q * k + j]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sj += __shfl_xor_sync(0xFFFFFFFFu, sj, o);
+        if (lane == 0) u.delta[j] = __double2float_ru(__dsqrt_ru(sj * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+    }
+    if (threadIdx.x == 0) {
+        *u.all_done = 0u;
+        klog_end(2);
     }
 }
 

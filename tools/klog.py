@@ -21,7 +21,7 @@ w = synthetic.CONFIGS["c2"]
 d = bm.Dataset(synthetic.generate("c2"))
 cfg = bm.BigMeansConfig(k=w.k, chunk_size=w.s, max_chunks=chunks, seed=0)
 bm.big_means(d, cfg, want_labels=False)
-buf = np.zeros(200001 + 3 * 60000, np.uint64)
+buf = np.zeros(540000, np.uint64)
 lib = _capi.load()
 lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
 n0 = int(buf[200000])
@@ -66,3 +66,22 @@ for key, v in sorted(pairs.items(), key=lambda kv: -sum(kv[1])):
 ds = st1 - st0
 print(f"round fast path: {ds[0]} CTAs, {ds[1]} fell back to the screen ({100 * ds[1] / max(ds[0], 1):.1f}%), "
       f"{ds[2] / max(ds[0], 1):.2f} rechecked pairs and {ds[3] / max(ds[0], 1):.2f} points with rechecks per CTA")
+
+# per-CTA phase marks of the last begin (region 400000) and round (region 470000) launches
+names_k = {0: "start", 1: "slab0", 2: "slab1", 3: "slab2", 4: "slab3", 5: "slab4", 6: "slab5", 7: "bounds",
+           8: "items", 9: "recheck", 10: "out/fold", 13: "fp_setup", 15: "fp_done", 16: "c0wait", 17: "c0done",
+           24: "c4wait", 25: "c4done", 26: "fp_items", 11: "acc:record", 12: "acc:ranks", 27: "lbk_written", 28: "last:arrived", 29: "last:control",
+           30: "last:accept"}
+for base, title in ((400000, "begin"), (470000, "round")):
+    T = buf[base:base + 2048 * 32].reshape(-1, 32).astype(np.int64)
+    T = T[T[:, 0] > 0]
+    if not len(T):
+        continue
+    t0 = T[:, 0].min()
+    print(f"--- last {title} launch: {len(T)} CTAs")
+    for i in sorted(names_k):
+        col = T[:, i]
+        v = col[col > 0] - t0
+        if v.size:
+            print(f"  {names_k[i]:13s} n={v.size:5d} p10={np.percentile(v, 10) / 1e3:7.2f} p50={np.percentile(v, 50) / 1e3:7.2f} "
+                  f"p90={np.percentile(v, 90) / 1e3:7.2f} max={v.max() / 1e3:7.2f} us")
