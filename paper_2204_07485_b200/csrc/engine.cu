@@ -140,6 +140,12 @@ struct Workspace {
     DevBuf<double> C, Cact;  // k * n
     DevBuf<float> CT32;      // n * 32: fp32 compacted centroids, transposed [d][j] (TMA screen)
     CUtensorMap tm_ct{};     // tensor map of CT32
+    // the incumbent's compacted copy (speculative begins of the next chunk read it)
+    DevBuf<double> CactI;
+    DevBuf<int> actI;
+    DevBuf<float> CT32I;
+    CUtensorMap tm_ctI{};
+    DevBuf<dev::GState> gs;  // chain state shared by the chunk buffers
     DevBuf<uint8_t> mask;    // k
     DevBuf<int> act;         // k
     DevBuf<dev::LloydStatus> status;
@@ -161,14 +167,17 @@ struct Workspace {
     DevBuf<unsigned long long> chunk_ctr;  // device-side chunk index
     // CUDA graphs of one chunk (sample resolution + gather, and the Lloyd loop)
     std::string graph_sig;
-    cudaGraphExec_t g_prep[2] = {nullptr, nullptr};
-    cudaGraphExec_t g_lloyd[2] = {nullptr, nullptr};  // per chunk buffer
-    cudaGraphExec_t g_cont[2] = {nullptr, nullptr};   // continuation of an incomplete chunk
+    // graph mode: chunk c uses graphs [c % 6]: data buffer c % 3, state and draw buffer c % 2
+    cudaGraphExec_t g_prep[6] = {};
+    cudaGraphExec_t g_lloyd[6] = {};
+    cudaGraphExec_t g_cont[6] = {};   // continuation of an incomplete chunk
+    cudaGraphExec_t g_spec[6] = {};   // speculative begin (first assignment against the incumbent's copy)
+    cudaEvent_t ev_spec[6] = {};
     cudaStream_t cap1 = nullptr, cap2 = nullptr;  // capture streams of the IF and WHILE bodies
-    cudaEvent_t ev_lloyd[2] = {nullptr, nullptr};  // end of the Lloyd graph of chunk buffer b
-    cudaEvent_t ev_prep[2] = {nullptr, nullptr};   // chunk buffer b gathered
+    cudaEvent_t ev_lloyd[6] = {};  // end of the Lloyd graph of the chunk in slot c % 6
+    cudaEvent_t ev_prep[6] = {};   // its chunk gathered
     void drop_graphs() {
-        for (auto* v : {&g_prep, &g_lloyd, &g_cont})
+        for (auto* v : {&g_prep, &g_lloyd, &g_cont, &g_spec})
             for (auto& e : *v)
                 if (e) {
                     cudaGraphExecDestroy(e);
@@ -180,8 +189,9 @@ struct Workspace {
         drop_graphs();
         for (auto q : {cap1, cap2})
             if (q) cudaStreamDestroy(q);
-        for (auto e : {ev_lloyd[0], ev_lloyd[1], ev_prep[0], ev_prep[1]})
-            if (e) cudaEventDestroy(e);
+        for (auto* v : {&ev_lloyd, &ev_prep, &ev_spec})
+            for (auto e : *v)
+                if (e) cudaEventDestroy(e);
     }
     // pinned host mirrors
     HostBuf<dev::LloydStatus> h_status;
@@ -190,14 +200,14 @@ struct Workspace {
     HostBuf<uint8_t> h_mask;
     HostBuf<uint32_t> h_cand;
 
-    void encode_ct_map() {
+    static void encode_ct_map(CUtensorMap* map, float* base, int n) {
         auto enc = tmap_encoder();
         if (!enc) throw CudaError("cuTensorMapEncodeTiled unavailable");
         const cuuint64_t dims[2] = {(cuuint64_t)dev::kSMaxK, (cuuint64_t)n};
         const cuuint64_t strides[1] = {(cuuint64_t)dev::kSMaxK * sizeof(float)};
         const cuuint32_t box[2] = {(cuuint32_t)dev::kSMaxK, (cuuint32_t)dev::kADC};
         const cuuint32_t es[2] = {1, 1};
-        if (enc(&tm_ct, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, CT32.p, dims, strides, box, es,
+        if (enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             throw CudaError("cuTensorMapEncodeTiled(centroids) failed");
@@ -210,10 +220,10 @@ struct Workspace {
         ldc = n + (n & 1);
         tiles = tiles_of(rows);
         hist_cap = hist;
-        labels.alloc(2 * R);
-        dists.alloc(4 * R);  // [chunk buffer][slot][R]: the fast-sum control's two slots per chunk buffer
+        labels.alloc(6 * R);  // [chunk buffer][slot 0..2][R] (non-graph paths: buffer 0, slots 0/1)
+        dists.alloc(6 * R);  // [chunk buffer][slot 0..2][R], like the labels
         fix_tiles.alloc(std::max<uint64_t>(tiles, 1));
-        lbk.alloc(R * dev::kSMaxK);
+        lbk.alloc(2 * R * dev::kSMaxK);  // per chunk buffer
         tile_buf.alloc(tiles * ncand);
         tile_ctr.alloc(tiles);
         if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
@@ -234,16 +244,22 @@ struct Workspace {
         slab_tot.alloc((uint64_t)n * k);
         BM_CUDA(cudaMemset(slab_tot.p, 0, (uint64_t)n * k * sizeof(unsigned)));
         Cact.alloc((uint64_t)k * (n + (n & 1)));
+        CactI.alloc((uint64_t)k * (n + (n & 1)));
         if (k <= dev::kSMaxK) {
             CT32.alloc((uint64_t)n * dev::kSMaxK);
             BM_CUDA(cudaMemset(CT32.p, 0, (uint64_t)n * dev::kSMaxK * sizeof(float)));
-            encode_ct_map();
+            encode_ct_map(&tm_ct, CT32.p, n);
+            CT32I.alloc((uint64_t)n * dev::kSMaxK);
+            BM_CUDA(cudaMemset(CT32I.p, 0, (uint64_t)n * dev::kSMaxK * sizeof(float)));
+            encode_ct_map(&tm_ctI, CT32I.p, n);
         }
         mask.alloc(k);
         act.alloc(k);
-        status.alloc(1);
-        BM_CUDA(cudaMemset(status.p, 0, sizeof(dev::LloydStatus)));
-        BM_CUDA(cudaMemset(status.p, 0, sizeof(dev::LloydStatus)));
+        actI.alloc(k);
+        status.alloc(2);  // per chunk buffer (non-graph paths: [0])
+        BM_CUDA(cudaMemset(status.p, 0, 2 * sizeof(dev::LloydStatus)));
+        gs.alloc(1);
+        BM_CUDA(cudaMemset(gs.p, 0, sizeof(dev::GState)));
         history.alloc(hist_cap);
         d2pool.alloc((uint64_t)(ncand + 1) * R);
         cand.alloc(ncand);
@@ -355,8 +371,9 @@ struct DeviceCache {
     std::map<std::tuple<uint64_t, int, int, int, uint64_t>, std::unique_ptr<Workspace>> ws;
     std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SamplerWs>> sws;
     DevBuf<uint8_t> chunk;        // gathered chunk, s * ld * elem
-    DevBuf<uint8_t> chunk1;       // second chunk buffer (graph mode: gather c+1 during Lloyd c)
+    DevBuf<uint8_t> chunk1, chunk2;  // graph mode: chunk c+2 is gathered while chunk c runs
     cudaStream_t pstream = nullptr;  // graph mode: prep (resolution + gather) of the next chunk
+    cudaStream_t sstream = nullptr;  // graph mode: speculative begin of the next chunk
     DevBuf<int32_t> flabels;      // final pass
     DevBuf<double> fdists, ftiles;
     DevBuf<unsigned> fctr;
@@ -365,6 +382,7 @@ struct DeviceCache {
         sws.clear();
         if (stream) cudaStreamDestroy(stream);
         if (pstream) cudaStreamDestroy(pstream);
+        if (sstream) cudaStreamDestroy(sstream);
     }
     void ensure_final(uint64_t rows) {
         if (flabels.n < rows) flabels.alloc(rows);
@@ -616,6 +634,16 @@ bool screen_enabled(int k) {
 void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t stride, int narrays,
                       double* tiles, const int* stop);
 
+// Centroid source of an assignment (default: the working compacted rows; a
+// speculative begin reads the incumbent's copy) and its bound storage.
+struct AssignSrc {
+    const double* Cact;
+    const int* act;
+    const int* n_active;
+    const CUtensorMap* tmc;
+    float* lbk;
+};
+
 // assign_nearest over P with the compacted centroids of ws (Cact/act/n_active).
 // With tile_out the per-1024-row tile partials of the distances are produced
 // too (fused into the screened kernel; a separate fold after the exact one).
@@ -623,8 +651,10 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
                    const int* stop, bool final_pass = false, double* tile_out = nullptr,
                    unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr, int hmode = 0,
-                   uint64_t dstride = 0, unsigned extra_ctas = 0) {
+                   uint64_t dstride = 0, unsigned extra_ctas = 0, const AssignSrc* src = nullptr) {
     const dev::LloydCtl noctl{};
+    const AssignSrc def{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, w.lbk.p};
+    const AssignSrc& S = src ? *src : def;
     bool fused_ctl = false;
     const unsigned grid = (unsigned)ceil_div(P.rows, dev::kABP) + extra_ctas;  // extra: fixup CTAs (TMA path)
     if (grid == 0) return;
@@ -643,10 +673,10 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             const CUtensorMap tmx = points_map<T>(P);
             fused_ctl = ctl && (tile_out || ctl->fast);
             launch_pdl(dev::k_assign_tma<T>, grid, dev::kSThreads, shm, st,
-                tmx, w.tm_ct, static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
-                &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
+                tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
+                S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                 g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
-                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, w.lbk.p, w.delta.p, k,
+                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
                 dstride);
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
@@ -658,11 +688,11 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             }
             dev::k_assign_screen<T><<<grid, dev::kSThreads, shm, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
-                &w.status.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out,
+                &w.gs.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out,
                 tile_ctr, g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
         } else {
             dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
-                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p, &w.status.p->n_active,
+                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p, &w.gs.p->n_active,
                 labels_pair, pair_stride, parity, dists, changed, stop);
         }
     });
@@ -671,10 +701,11 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     if (tile_out && !screen) launch_tile_sums(st, dists, P.rows, 0, 1, tile_out, stop);
     if (ctl && ctl->mode && !fused_ctl) {  // control as its own kernel
         if (ctl->mode == 1)
-            dev::k_lloyd_begin<<<1, 32, 0, st>>>(ctl->st, tile_out, ctl->ntiles, P.rows, ctl->history);
+            dev::k_lloyd_begin<<<1, 32, 0, st>>>(ctl->st, tile_out, ctl->ntiles, P.rows, ctl->history, S.n_active);
         else
             dev::k_lloyd_step<<<1, 32, 0, st>>>(ctl->st, tile_out, ctl->ntiles, P.rows, ctl->max_iterations,
-                                                ctl->rel_tolerance, ctl->history, ctl->cond, ctl->use_cond);
+                                                ctl->rel_tolerance, ctl->history, ctl->cond, ctl->use_cond,
+                                                S.n_active);
         BM_LAUNCH();
         count_launch();
     }
@@ -691,7 +722,7 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
 
 void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_t* mask) {
     dev::k_compact<<<1, 256, w.k * sizeof(int), st>>>(C, mask, w.k, w.n, w.Cact.p, w.ldc, w.act.p,
-                                                       &w.status.p->n_active, w.CT32.p);
+                                                       &w.gs.p->n_active, w.CT32.p);
     BM_LAUNCH();
     count_launch();
 }
@@ -700,7 +731,7 @@ void launch_compact(cudaStream_t st, Workspace& w, const double* C, const uint8_
 // slab's last CTA merges it.  Slabs split the dimensions so that the grid
 // covers the GPU when there are few tiles and the staged slab fits in shared memory.
 void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* parity, const int* stop,
-                   const int* go = nullptr) {
+                   const int* go = nullptr, int32_t* labels = nullptr, int* bad_label = nullptr) {
     PhaseScope ps(PH_UPDATE, P.rows);
     const int k = w.k, n = w.n;
     const uint64_t tiles = tiles_of(P.rows);
@@ -723,13 +754,14 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
     int G = (int)std::min<uint64_t>({tiles, (uint64_t)8, std::max<uint64_t>(1, ceil_div((uint64_t)k * dslab, 48))});
     while (G > 1 && (uint64_t)G * slabs > 148) --G;
     dev::UpdateArgs u{w.psum.p, tstride, shm, w.slab_ctr.p, w.slab_done.p, G, go, w.all_done.p, w.delta.p, w.slab_tot.p, w.C.p, w.mask.p, w.Cact.p, w.ldc,
-                      w.act.p, &w.status.p->n_active, w.CT32.p, w.drift_part.p, &w.status.p->bad_label, stop};
+                      w.act.p, &w.gs.p->n_active, w.CT32.p, w.drift_part.p,
+                      bad_label ? bad_label : &w.status.p->bad_label, stop};
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         if (shm > 48 * 1024)
             BM_CUDA(cudaFuncSetAttribute(dev::k_update<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
         launch_pdl(dev::k_update<T>, grid, dev::kUThreads, shm, st, static_cast<const T*>(P.X), P.rows, n, P.ld,
-                   w.labels.p, w.R, parity, k, dslab, u);
+                   labels ? labels : w.labels.p, w.R, parity, k, dslab, u);
     });
     BM_LAUNCH();
     count_launch(1);
@@ -763,6 +795,7 @@ dev::LloydCtl make_ctl(Workspace& w, int mode, uint64_t rows, uint64_t max_it = 
     c.dstride = w.R;
     c.mode = mode;
     c.st = w.status.p;
+    c.gs = w.gs.p;
     c.tiles_done = w.tiles_done.p;
     c.ntiles = tiles_of(rows);
     c.max_iterations = max_it;
@@ -777,18 +810,30 @@ dev::LloydCtl make_ctl(Workspace& w, int mode, uint64_t rows, uint64_t max_it = 
 // begin (:27-28), the latter fused into the assignment where possible.
 // Graph-mode extras of a Lloyd launch sequence.
 struct GraphRound {
-    double* dbase = nullptr;        // distance slots of this chunk buffer (default: w.dists.p)
+    int buf = 0;                    // chunk buffer: labels/dists/bounds/status of this buffer
     const int* go = nullptr;        // skip everything when *go == 0
+    int begin_kind = 0;             // begin: 1 speculative (incumbent copy), 2 redo unless current
     bool accept = false;            // the control runs the accept when the loop stops
     dev::LloydStatus* host_st = nullptr;
     unsigned long long incomplete_after = 0;
-    bool fix = false;               // begin: fixup CTAs for the pending chunk's record
+    bool fix = false;               // round 1: fixup CTAs for the previous chunk's record
 };
+
+// Per-buffer storage in graph mode: 3 slots of labels/distances (slot 2: the
+// begin's assignment), bounds and status.
+int32_t* gr_labels(Workspace& w, const GraphRound* g) { return w.labels.p + (g ? 3 * (uint64_t)g->buf * w.R : 0); }
+double* gr_dists(Workspace& w, const GraphRound* g) { return w.dists.p + (g ? 3 * (uint64_t)g->buf * w.R : 0); }
+dev::LloydStatus* gr_status(Workspace& w, const GraphRound* g) { return w.status.p + (g ? g->buf : 0); }
+float* gr_lbk(Workspace& w, const GraphRound* g) {
+    return w.lbk.p + (g ? (uint64_t)g->buf * w.R * dev::kSMaxK : 0);
+}
 
 void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
     if (!g) return;
-    if (g->dbase) c.dists_pair = g->dbase;
+    c.dists_pair = gr_dists(w, g);
+    c.st = gr_status(w, g);
     c.go = g->go;
+    c.begin_kind = g->begin_kind;
     if (g->accept || g->fix) c.acc = w.accd.p;
     c.accept_run = g->accept ? 1 : 0;
     c.host_st = g->host_st;
@@ -801,29 +846,35 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
 }
 
 // compact (unless the compacted start is already in place) + assign (:26) +
-// begin (:27-28), the latter fused into the assignment where possible.
+// begin (:27-28), the latter fused into the assignment where possible.  In
+// graph mode the begin's assignment goes to slot 2 of the chunk buffer.
 void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do_compact = true,
                          bool fast = false, const GraphRound* g = nullptr) {
     if (do_compact) launch_compact(st, w, w.C.p, w.mask.p);
     dev::LloydCtl ctl = make_ctl(w, 1, P.rows, 0, 0.0, 0, 0, fast);
     apply_graph(ctl, w, g);
-    launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, g && g->dbase ? g->dbase : w.dists.p, nullptr, nullptr,
-                  false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1, 0,
-                  g && g->fix ? (unsigned)tiles_of(w.R) : 0u);
+    const uint64_t slot = g ? 2 : 0;
+    ctl.begin_slot = (int)slot;
+    AssignSrc src{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, gr_lbk(w, g)};
+    if (g && g->begin_kind == 1) src = AssignSrc{w.CactI.p, w.actI.p, &w.gs.p->n_active_inc, &w.tm_ctI, gr_lbk(w, g)};
+    launch_assign(st, P, w, w.k, gr_labels(w, g) + slot * w.R, 0, nullptr, gr_dists(w, g) + slot * w.R, nullptr,
+                  nullptr, false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1, 0, 0u, &src);
 }
 
 // update (:33) + assign (:34-35) + step (:36-51), the step fused into the assignment.
 void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_t max_it, double tol,
                          cudaGraphConditionalHandle cond = 0, int use_cond = 0, bool fast = false,
                          const GraphRound* g = nullptr) {
-    const int* parity = &w.status.p->parity;
-    const int* stop = &w.status.p->stop;
-    launch_update(st, P, w, parity, stop, g ? g->go : nullptr);
+    dev::LloydStatus* sts = gr_status(w, g);
+    const int* parity = &sts->parity;
+    const int* stop = &sts->stop;
+    launch_update(st, P, w, parity, stop, g ? g->go : nullptr, gr_labels(w, g), &sts->bad_label);
     dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond, fast);
     apply_graph(ctl, w, g);
-    launch_assign(st, P, w, w.k, w.labels.p, w.R, parity, g && g->dbase ? g->dbase : w.dists.p,
-                  &w.status.p->changed, stop, false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 2,
-                  fast ? w.R : 0);
+    AssignSrc src{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, gr_lbk(w, g)};
+    launch_assign(st, P, w, w.k, gr_labels(w, g), w.R, parity, gr_dists(w, g), &sts->changed, stop, false,
+                  fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 2, fast ? w.R : 0,
+                  g && g->fix ? (unsigned)tiles_of(w.R) : 0u, &src);
 }
 
 // Runs the loop to completion; `between` is called once after the first
@@ -1115,10 +1166,11 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
     BM_CUDA(cudaMemcpyAsync(tiles_host, c.ftiles.p, tiles_of(P.rows) * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (labels_host)
         BM_CUDA(cudaMemcpyAsync(labels_host, c.flabels.p, P.rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, st));
+    int na = 0;
+    BM_CUDA(cudaMemcpyAsync(&na, &w.gs.p->n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaStreamSynchronize(st));
-    if (w.h_status.p->n_active == 0) throw StateError("assign_nearest: every centroid is degenerate");
-    if (evals) *evals += P.rows * (uint64_t)w.h_status.p->n_active;
+    if (na == 0) throw StateError("assign_nearest: every centroid is degenerate");
+    if (evals) *evals += P.rows * (uint64_t)na;
 }
 
 // ---------------------------------------------------------------------------
@@ -1148,6 +1200,10 @@ dev::AcceptArgs accept_args(Workspace& w) {
     A.ldc = w.ldc;
     A.act_idx = w.act.p;
     A.CT32 = w.CT32.p;
+    A.CactI = w.CactI.p;
+    A.actI = w.actI.p;
+    A.CT32I = w.CT32I.p;
+    A.gs = w.gs.p;
     return A;
 }
 
@@ -1205,21 +1261,24 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
     // fast-sum control whenever the TMA screen (which implements it) runs
     const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
     if (fast) {
-        // begin (+ fixup CTAs: the previous chunk's exact objective for its
-        // record) -> round 1 -> round 2; the control of the round that stops
-        // runs the accept.  A chunk still running after round 2 is marked
-        // incomplete and continued by the host (capture_cont).  Every kernel of
-        // a skipped chunk (st->go == 0) returns at once.
+        // begin unless the speculative begin (capture_spec) is current ->
+        // round 1 (+ fixup CTAs: the previous chunk's exact objective for its
+        // record) -> round 2; the control of the round that stops runs the
+        // accept.  A chunk still running after round 2 is marked incomplete and
+        // continued by the host (capture_cont).  Every kernel of a skipped
+        // chunk (go == 0) returns at once.
         GraphRound g;
-        g.dbase = w.dists.p + 2 * (uint64_t)b * w.R;
-        g.go = &w.status.p->go;
-        g.fix = true;
+        g.buf = b;
+        g.go = &w.gs.p->go;
+        g.begin_kind = 2;
         lloyd_enqueue_begin(st, P, w, /*do_compact=*/false, true, &g);  // accept (or the repair) compacted the start
         GraphRound r = g;
-        r.fix = false;
+        r.begin_kind = 0;
+        r.fix = true;
         r.accept = true;
         r.host_st = w.h_status.p + b;
         lloyd_enqueue_round(st, P, w, max_it, tol, 0, 0, true, &r);
+        r.fix = false;
         r.incomplete_after = 2;
         lloyd_enqueue_round(st, P, w, max_it, tol, 0, 0, true, &r);
     } else {  // the guard sets the IF condition inside the graph that owns it
@@ -1228,7 +1287,7 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
         BM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, nullptr, nullptr));
         cudaGraphConditionalHandle hif;
         BM_CUDA(cudaGraphConditionalHandleCreate(&hif, cg, 0, cudaGraphCondAssignDefault));
-        dev::k_guard<<<1, 1, 0, st>>>(w.status.p, hif);
+        dev::k_guard<<<1, 1, 0, st>>>(w.gs.p, hif);
         BM_LAUNCH();
         cudaGraphNodeParams prm = {};
         const cudaGraphNode_t* deps = nullptr;
@@ -1272,7 +1331,7 @@ cudaGraphExec_t capture_cont(cudaStream_t st, Workspace& w, const Points& P, uin
     add_conditional(st, &hw, &wbody, cudaGraphCondTypeWhile, 1);
     BM_CUDA(cudaStreamBeginCaptureToGraph(w.cap2, wbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     GraphRound r;
-    r.dbase = w.dists.p + 2 * (uint64_t)b * w.R;
+    r.buf = b;
     r.accept = true;
     r.host_st = w.h_status.p + b;
     lloyd_enqueue_round(w.cap2, P, w, max_it, tol, hw, 1, true, &r);
@@ -1285,11 +1344,30 @@ cudaGraphExec_t capture_cont(cudaStream_t st, Workspace& w, const Points& P, uin
     return e;
 }
 
+// The speculative begin of the chunk in buffer b: its first assignment against
+// the incumbent's compacted copy, run while the previous chunk's rounds run.
+// Valid only if no accept published a new incumbent meanwhile (inc_version).
+cudaGraphExec_t capture_spec(cudaStream_t st, Workspace& w, const Points& P, int b) {
+    BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    BM_CUDA(cudaMemsetAsync(&w.status.p[b].bv_min, 0xFF, sizeof(long long), st));
+    GraphRound g;
+    g.buf = b;
+    g.begin_kind = 1;
+    lloyd_enqueue_begin(st, P, w, /*do_compact=*/false, true, &g);
+    cudaGraph_t gr = nullptr;
+    BM_CUDA(cudaStreamEndCapture(st, &gr));
+    cudaGraphExec_t e = nullptr;
+    BM_CUDA(cudaGraphInstantiate(&e, gr, 0));
+    cudaGraphDestroy(gr);
+    return e;
+}
+
 void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw, Workspace& w,
                    const Points& P, uint64_t max_it, double tol) {
     char sig[512];
-    std::snprintf(sig, sizeof(sig), "%llu/%p/%p/%p/%p/%p/%p/%llu/%a/%llu",
-                  (unsigned long long)d->uid, (const void*)d->X, (void*)dc.chunk.p, (void*)dc.chunk1.p, (void*)&sw,
+    std::snprintf(sig, sizeof(sig), "%llu/%p/%p/%p/%p/%p/%p/%p/%llu/%a/%llu",
+                  (unsigned long long)d->uid, (const void*)d->X, (void*)dc.chunk.p, (void*)dc.chunk1.p,
+                  (void*)dc.chunk2.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n);
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
@@ -1297,14 +1375,18 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
     if (!w.accd.n) w.accd.alloc(1);
     const dev::AcceptArgs A = accept_args(w);
     BM_CUDA(cudaMemcpy(w.accd.p, &A, sizeof(A), cudaMemcpyHostToDevice));
-    void* bufs[2] = {dc.chunk.p, dc.chunk1.p};
+    void* bufs[3] = {dc.chunk.p, dc.chunk1.p, dc.chunk2.p};
     const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
-    for (int b = 0; b < 2; ++b) {
+    for (int i = 0; i < 6; ++i) {  // data buffer i % 3, state / draw buffer i % 2
+        const int b = i % 2;
         Points Pb = P;
-        Pb.X = bufs[b];
-        w.g_prep[b] = capture_prep(st, d, sw, b, bufs[b]);
-        w.g_lloyd[b] = capture_lloyd(st, w, Pb, max_it, tol, b);
-        if (fast) w.g_cont[b] = capture_cont(st, w, Pb, max_it, tol, b);
+        Pb.X = bufs[i % 3];
+        w.g_prep[i] = capture_prep(st, d, sw, b, bufs[i % 3]);
+        w.g_lloyd[i] = capture_lloyd(st, w, Pb, max_it, tol, b);
+        if (fast) {
+            w.g_cont[i] = capture_cont(st, w, Pb, max_it, tol, b);
+            w.g_spec[i] = capture_spec(st, w, Pb, b);
+        }
     }
     g_profile.kernel_launches = saved;  // capture is not execution
     w.graph_sig = sig;
@@ -1333,11 +1415,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         if (dc.chunk.n < bytes) dc.chunk.alloc(bytes);
         chunkP.X = dc.chunk.p;
         if (!g_profiling && graphs_enabled() && dc.chunk1.n < bytes) dc.chunk1.alloc(bytes);
+        if (!g_profiling && graphs_enabled() && dc.chunk2.n < bytes) dc.chunk2.alloc(bytes);
     }
     const uint64_t want_rec = cfg.has_max_chunks ? cfg.max_chunks : 1024;
     if (w.drec.n < want_rec) w.drec.alloc(want_rec);
     // incumbent all degenerate, f_opt = +inf (:63-64), chunk counter 0
-    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
+    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, 2, w.gs.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
                                        w.chunk_ctr.p);
     BM_LAUNCH();
     if (!identity) put_stream(st, *sw, rng);
@@ -1349,26 +1432,33 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
 
     const auto t_loop = std::chrono::steady_clock::now();
     if (use_graphs) {
-        // Graph mode, two chunk buffers b = chunk & 1.  Chunk c+1's draws and
-        // prep (resolution + gather into buffer b^1) run on their own streams
-        // while chunk c's Lloyd graph runs, and chunk c+1's Lloyd graph is
-        // queued behind it before the host waits for chunk c; it runs only if
-        // chunk c's accept leaves no degenerate incumbent rows (k_guard).  The
-        // RNG order (big_means.hpp:21-23) is kept: chunk c+1's sample draws are
-        // enqueued after chunk c's repair draws, chunk c+2's after c+1's.
+        // Graph mode.  Chunk c uses graph slot c % 6: data buffer c % 3, state
+        // and draw buffer c % 2.  While chunk c's Lloyd graph runs, chunk c+1's
+        // speculative begin (its first assignment against the incumbent's
+        // copy) runs on sstream and chunk c+2's draws and prep (resolution +
+        // gather) on rng_stream / pstream; chunk c+1's Lloyd graph is queued
+        // behind chunk c's before the host waits.  It runs only if chunk c's
+        // accept leaves no degenerate incumbent rows (go) and redoes its begin
+        // if an accept published a new incumbent meanwhile (inc_version).  The
+        // RNG order (big_means.hpp:21-23) is kept: draws made ahead of a repair
+        // are discarded and redone after it.
         if (!dc.pstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.pstream, cudaStreamNonBlocking));
-        for (int b = 0; b < 2; ++b) {
-            if (!w.ev_lloyd[b]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd[b], cudaEventDisableTiming));
-            if (!w.ev_prep[b]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_prep[b], cudaEventDisableTiming));
+        for (int i = 0; i < 6; ++i) {
+            if (!w.ev_lloyd[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd[i], cudaEventDisableTiming));
+            if (!w.ev_prep[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_prep[i], cudaEventDisableTiming));
+            if (!w.ev_spec[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_spec[i], cudaEventDisableTiming));
+            BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
+            BM_CUDA(cudaEventRecord(w.ev_spec[i], st));
         }
         // BM_PIPE=0: preps on the Lloyd stream (no overlap; timeline diagnostics)
         static const bool pipe = !(std::getenv("BM_PIPE") && std::string(std::getenv("BM_PIPE")) == "0");
         const cudaStream_t pst = pipe ? dc.pstream : st;
-        Points bufP[2] = {chunkP, chunkP};
+        Points bufP[3] = {chunkP, chunkP, chunkP};
         bufP[1].X = dc.chunk1.p;
-        // BM_TIMELINE=1: in-stream events after every Lloyd graph (GPU time per chunk incl. gaps)
+        bufP[2].X = dc.chunk2.p;
+        // BM_TIMELINE=1: in-stream events around every graph (GPU durations incl. gaps)
         static const bool timeline = std::getenv("BM_TIMELINE") != nullptr;
-        // per graph launch: (kind 0 = prep / 1 = Lloyd, start event, end event)
+        // per graph launch: (kind 0 = prep / 1 = Lloyd / 2 = speculative begin, start event, end event)
         struct TlRec { int kind; cudaEvent_t a, b; };
         std::vector<TlRec> tl;
         auto tl_ev = [&](cudaStream_t q) {
@@ -1379,33 +1469,52 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             }
             return e;
         };
-        // a chunk's prep: draws on rng_stream are already enqueued (drawn[b])
-        auto launch_prep = [&](int b) {
-            BM_CUDA(cudaStreamWaitEvent(pst, sw->drawn[b], 0));
-            BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[b], 0));  // buffer b's previous reader
+        // chunk c's prep (its draws are enqueued on rng_stream: drawn[c % 2])
+        auto launch_prep = [&](uint64_t c) {
+            const int i = (int)(c % 6);
+            BM_CUDA(cudaStreamWaitEvent(pst, sw->drawn[c & 1], 0));
+            BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[(c + 3) % 6], 0));  // data buffer's previous chunk (c-3)
             cudaEvent_t e0 = tl_ev(pst);
-            BM_CUDA(cudaGraphLaunch(w.g_prep[b], pst));
+            BM_CUDA(cudaGraphLaunch(w.g_prep[i], pst));
             if (timeline) tl.push_back({0, e0, tl_ev(pst)});
-            BM_CUDA(cudaEventRecord(w.ev_prep[b], pst));
+            BM_CUDA(cudaEventRecord(w.ev_prep[i], pst));
             count_launch(6);
         };
-        auto launch_lloyd = [&](int b) {
-            BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[b], 0));
+        // BM_SPEC=0: no speculative begins (every chunk graph runs its own)
+        static const bool spec_on = !(std::getenv("BM_SPEC") && std::string(std::getenv("BM_SPEC")) == "0");
+        const bool spec = spec_on && w.g_spec[0] != nullptr;
+        if (spec && !dc.sstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.sstream, cudaStreamNonBlocking));
+        auto launch_spec = [&](uint64_t c) {  // chunk c's first assignment, overlapping chunk c-1
+            const int i = (int)(c % 6);
+            BM_CUDA(cudaStreamWaitEvent(dc.sstream, w.ev_prep[i], 0));
+            BM_CUDA(cudaStreamWaitEvent(dc.sstream, w.ev_lloyd[(c + 4) % 6], 0));  // state buffer's chunk c-2
+            cudaEvent_t e0 = tl_ev(dc.sstream);
+            BM_CUDA(cudaGraphLaunch(w.g_spec[i], dc.sstream));
+            if (timeline) tl.push_back({2, e0, tl_ev(dc.sstream)});
+            BM_CUDA(cudaEventRecord(w.ev_spec[i], dc.sstream));
+            count_launch(1);
+        };
+        auto launch_lloyd = [&](uint64_t c) {
+            const int i = (int)(c % 6);
+            BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i], 0));
+            if (spec) BM_CUDA(cudaStreamWaitEvent(st, w.ev_spec[i], 0));
             cudaEvent_t e0 = tl_ev(st);
-            BM_CUDA(cudaGraphLaunch(w.g_lloyd[b], st));
+            BM_CUDA(cudaGraphLaunch(w.g_lloyd[i], st));
             if (timeline) tl.push_back({1, e0, tl_ev(st)});
-            BM_CUDA(cudaEventRecord(w.ev_lloyd[b], st));
+            BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
+        };
+        auto draw = [&](uint64_t c) {  // chunk c's sample draws into target buffer c % 2
+            if (c >= 2) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[c & 1], 0));  // read by chunk c-2
+            enqueue_device_draw(sw->rng_stream, *sw, 0, (int)(c & 1));
+            BM_CUDA(cudaEventRecord(sw->drawn[c & 1], sw->rng_stream));
         };
         // speculation needs the chunk count to be known in advance (no time budget)
         const bool speculate = !cfg.has_max_cpu_seconds;
         auto exists = [&](uint64_t c) { return !cfg.has_max_chunks || c < cfg.max_chunks; };
-        BM_CUDA(cudaEventRecord(w.ev_lloyd[0], st));
-        BM_CUDA(cudaEventRecord(w.ev_lloyd[1], st));
-        enqueue_device_draw(sw->rng_stream, *sw, 0, 0);
-        BM_CUDA(cudaEventRecord(sw->drawn[0], sw->rng_stream));
+        draw(0);
         launch_prep(0);
         bool queued = false;     // chunk `chunk`'s Lloyd graph is already queued (guarded)
-        bool spec_next = false;  // chunk+1's draws are already enqueued (speculatively)
+        bool spec_next = false;  // chunk+1's draws (and prep) are already enqueued, ahead of this chunk's repair
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
             if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
@@ -1413,6 +1522,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             if (chunk >= w.drec.n) {  // time-budget runs: grow the record buffer (graphs re-captured)
                 BM_CUDA(cudaStreamSynchronize(st));
                 BM_CUDA(cudaStreamSynchronize(pst));
+                if (dc.sstream) BM_CUDA(cudaStreamSynchronize(dc.sstream));
                 DevBuf<dev::Record> bigger(w.drec.n * 2);
                 BM_CUDA(cudaMemcpyAsync(bigger.p, w.drec.p, w.drec.n * sizeof(dev::Record),
                                         cudaMemcpyDeviceToDevice, st));
@@ -1421,10 +1531,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 std::swap(w.drec.n, bigger.n);
                 ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
             }
-            const int b = (int)(chunk & 1);
+            const int b = (int)(chunk & 1), i6 = (int)(chunk % 6);
             if (inc_degenerate > 0) {  // kmeanspp_fill (:84) after this chunk's sample draws
-                // (a queued Lloyd graph of this chunk found st->go == 0 and did nothing)
-                BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[b], 0));
+                // (a queued Lloyd graph of this chunk found go == 0 and did nothing)
+                BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i6], 0));
                 BM_CUDA(cudaMemcpyAsync(w.h_mask.p, w.maskinc.p, k, cudaMemcpyDeviceToHost, st));
                 BM_CUDA(cudaStreamSynchronize(st));
                 std::copy(w.h_mask.p, w.h_mask.p + k, hmask.begin());
@@ -1432,35 +1542,35 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 // the stream right after this chunk's draws: live, or the input
                 // state of chunk+1's speculative draws (which are discarded)
                 get_stream(st, *sw, rng, spec_next ? 1 + (b ^ 1) : 0);
-                kmeanspp_fill_device(st, bufP[b], w, hmask, cfg.candidates_per_step, rng, evals);
+                kmeanspp_fill_device(st, bufP[chunk % 3], w, hmask, cfg.candidates_per_step, rng, evals);
                 put_stream(st, *sw, rng);
                 launch_compact(st, w, w.C.p, w.mask.p);  // the Lloyd graph starts from Cact
-                BM_CUDA(cudaMemsetAsync(&w.status.p->go, 0x01, sizeof(int), st));
+                BM_CUDA(cudaMemsetAsync(&w.gs.p->go, 0x01, sizeof(int), st));
+                dev::k_bump_version<<<1, 1, 0, st>>>(w.gs.p);  // the start is no longer the incumbent's copy
+                BM_LAUNCH();
                 queued = false;
-                spec_next = false;
+                spec_next = false;  // chunk+1's draws and prep are redone
             }
             const bool next = exists(chunk + 1);
-            if (next && !spec_next) {  // chunk+1's draws: the stream is past this chunk's repair
-                if (chunk >= 1) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[b ^ 1], 0));
-                enqueue_device_draw(sw->rng_stream, *sw, 0, b ^ 1);
-                BM_CUDA(cudaEventRecord(sw->drawn[b ^ 1], sw->rng_stream));
+            if (next && !spec_next) {  // chunk+1's draws and prep: the stream is past this chunk's repair
+                draw(chunk + 1);
+                launch_prep(chunk + 1);
             }
-            if (!queued) launch_lloyd(b);
-            if (next) launch_prep(b ^ 1);
-            // chunk+2's draws, assuming chunk+1 needs no repair (else redone above)
+            if (!queued) launch_lloyd(chunk);
+            if (next && spec) launch_spec(chunk + 1);
+            // chunk+2's draws and prep, assuming chunk+1 needs no repair (else redone above)
             spec_next = next && speculate && exists(chunk + 2);
             if (spec_next) {
-                BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[b], 0));  // chunk's resolution read buffer b
-                enqueue_device_draw(sw->rng_stream, *sw, 0, b);
-                BM_CUDA(cudaEventRecord(sw->drawn[b], sw->rng_stream));
+                draw(chunk + 2);
+                launch_prep(chunk + 2);
             }
             queued = next && speculate;
-            if (queued) launch_lloyd(b ^ 1);  // runs iff this chunk's accept needs no repair
-            BM_CUDA(cudaEventSynchronize(w.ev_lloyd[b]));
+            if (queued) launch_lloyd(chunk + 1);  // runs iff this chunk's accept needs no repair
+            BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
             if (w.h_status.p[b].incomplete) {  // more rounds than the graph unrolls
-                BM_CUDA(cudaGraphLaunch(w.g_cont[b], st));
-                BM_CUDA(cudaEventRecord(w.ev_lloyd[b], st));
-                BM_CUDA(cudaEventSynchronize(w.ev_lloyd[b]));
+                BM_CUDA(cudaGraphLaunch(w.g_cont[i6], st));
+                BM_CUDA(cudaEventRecord(w.ev_lloyd[i6], st));
+                BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
                 queued = false;  // the queued next chunk found go == 0 and did nothing
             }
             const dev::LloydStatus& ls = w.h_status.p[b];
@@ -1473,14 +1583,15 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             out->chunks = chunk + 1;
         }
         // the last chunk's record gets its exact objective
-        dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.status.p, accept_args(w), w.dists.p, w.R,
+        dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.gs.p, accept_args(w), w.dists.p, w.R,
                                                                    w.fix_tiles.p, w.tiles_done.p);
         BM_LAUNCH();
         BM_CUDA(cudaStreamSynchronize(st));
         BM_CUDA(cudaStreamSynchronize(pst));
+        if (dc.sstream) BM_CUDA(cudaStreamSynchronize(dc.sstream));
         if (timeline && tl.size() > 2) {
-            double dur[2] = {0, 0}, gap = 0;
-            int cnt[2] = {0, 0}, ngap = 0;
+            double dur[3] = {0, 0, 0}, gap = 0;
+            int cnt[3] = {0, 0, 0}, ngap = 0;
             cudaEvent_t prev_end = nullptr, first = nullptr, last = nullptr;
             for (auto& r : tl) {
                 float ms = 0;
@@ -1502,9 +1613,9 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaEventElapsedTime(&total, first, last));
             std::fprintf(stderr,
                          "[timeline] %.3f ms over %d Lloyd graphs: %.1f us per chunk | Lloyd graph %.1f us | gap "
-                         "before the next %.1f us | prep graph %.1f us (%d)\n",
+                         "before the next %.1f us | prep graph %.1f us (%d) | speculative begin %.1f us (%d)\n",
                          total, cnt[1], 1e3 * total / cnt[1], 1e3 * dur[1] / cnt[1], ngap ? 1e3 * gap / ngap : 0.0,
-                         cnt[0] ? 1e3 * dur[0] / cnt[0] : 0.0, cnt[0]);
+                         cnt[0] ? 1e3 * dur[0] / cnt[0] : 0.0, cnt[0], cnt[2] ? 1e3 * dur[2] / cnt[2] : 0.0, cnt[2]);
             for (auto& r : tl) {
                 cudaEventDestroy(r.a);
                 cudaEventDestroy(r.b);
@@ -1885,13 +1996,14 @@ bm_status bm_assign_nearest(const bm_dataset* dc, const double* C, const uint8_t
         DevBuf<double> dd(d->m);
         Points P = dataset_points(d);
         launch_assign(stream_of(d), P, w, (int)k, dl.p, 0, nullptr, dd.p, nullptr, nullptr);
-        BM_CUDA(cudaMemcpyAsync(w.h_status.p, w.status.p, sizeof(dev::LloydStatus), cudaMemcpyDeviceToHost, stream_of(d)));
+        int na = 0;
+        BM_CUDA(cudaMemcpyAsync(&na, &w.gs.p->n_active, sizeof(int), cudaMemcpyDeviceToHost, stream_of(d)));
         BM_CUDA(cudaStreamSynchronize(stream_of(d)));
-        if (w.h_status.p->n_active == 0) throw StateError("assign_nearest: every centroid is degenerate");
+        if (na == 0) throw StateError("assign_nearest: every centroid is degenerate");
         BM_CUDA(cudaMemcpyAsync(labels, dl.p, d->m * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_of(d)));
         if (dists) BM_CUDA(cudaMemcpyAsync(dists, dd.p, d->m * sizeof(double), cudaMemcpyDeviceToHost, stream_of(d)));
         BM_CUDA(cudaStreamSynchronize(stream_of(d)));
-        if (evals) *evals += d->m * (uint64_t)w.h_status.p->n_active;
+        if (evals) *evals += d->m * (uint64_t)na;
     });
 }
 

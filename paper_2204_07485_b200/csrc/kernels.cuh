@@ -30,14 +30,12 @@ struct LloydStatus {
     double objective;    // history.back() (:54)
     unsigned long long evals;       // this run's distance evals (core.cpp:157-159)
     unsigned long long iterations;  // ++iterations (:36)
-    int parity;          // labels[parity] holds the current assignment
+    int parity;          // labels[parity] holds the current assignment (slot 2: a graph-mode begin)
     int stop;            // loop finished
     int changed;         // set by the assignment when a label differs (:39)
-    int n_active;        // active rows of the centroid buffer last assigned with
     int state_error;     // assign against all-degenerate centroids (core.cpp:115-118)
-    int inc_degenerate;  // degenerate rows of the incumbent after the accept step
+    int inc_degenerate;  // host copy: degenerate rows of the incumbent after the accept step
     int bad_label;       // update saw a label outside [0,k) (core.cpp:189-193)
-    int go;              // the next chunk starts from the incumbent as is (no repair, :83-85)
     // fast-sum control (graph mode): the stop test runs on certified intervals
     // of the objectives, the exact block_sum only when the interval test cannot
     // decide (and for the final objective, in k_accept)
@@ -45,13 +43,22 @@ struct LloydStatus {
     double fsum;         // accumulator of the current launch's CTA distance sums
     unsigned ctas_done;  // CTAs of the current launch that have added their sum
     int exact_checks;    // decisions that needed the exact sums (diagnostics)
-    // deferred exact objectives (graph mode): a chunk's exact objective is
-    // folded while the next chunk's first assignment runs
-    double fopt_exact;   // exact f_opt (big_means.cpp:63, :89-93) of the chunks fixed up so far
+    int incomplete;      // the graph's unrolled rounds ended without a stop: the host continues
+    int pad2;
+    long long begin_version;  // incumbent version the begin's assignment used (-1: none / stale)
+    long long bv_min;         // lowest version its CTAs saw when they started (atomicMin; host resets)
+};
+
+// Chain state shared by the two chunk buffers (big_means.cpp:62-94).
+struct GState {
+    double fopt_exact;   // exact f_opt of the chunks whose records are final (deferred exact objectives)
+    long long inc_version;  // bumped whenever the next chunk's start stops being the incumbent's copy
+    int n_active;        // active rows of the working compacted centroids (Cact / CT32 / act)
+    int n_active_inc;    // active rows of the incumbent's compacted copy (CactI / CT32I / actI)
+    int inc_degenerate;  // degenerate rows of the incumbent
+    int go;              // the next chunk starts from the incumbent as is (no repair, :83-85)
     int pending_fix;     // chunk whose record awaits its exact objective (-1: none)
     int fix_par;         // distance slot of that chunk's final assignment
-    int incomplete;      // the graph's unrolled rounds ended without a stop: continue on the host's order
-    int pad2;
 };
 static_assert(sizeof(LloydStatus) % 8 == 0, "status is copied as 8-byte words");
 
@@ -480,33 +487,33 @@ __device__ __forceinline__ double seq_fold_smem(const double* v, int len) {
 // kernel or run by the CTA that completes an assignment's last tile.
 // ===========================================================================
 __device__ __noinline__ void lloyd_begin_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
-                                 double* history) {
+                                 double* history, const int* n_active) {
     const double f = fold_tiles(tiles, ntiles);  // :27
     if (history) history[0] = f;                 // :28
     st->f = f;
     st->objective = f;
-    st->evals = static_cast<unsigned long long>(rows) * st->n_active;  // :26 counter
+    st->evals = static_cast<unsigned long long>(rows) * *n_active;  // :26 counter
     st->iterations = 0;
     st->parity = 0;
     st->stop = 0;
     st->changed = 0;
-    st->state_error = st->n_active == 0;
+    st->state_error = *n_active == 0;
     st->bad_label = 0;
 }
 
 __device__ __noinline__ void lloyd_step_body(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
                                 unsigned long long max_iterations, double rel_tolerance, double* history,
-                                cudaGraphConditionalHandle cond, int use_cond) {
+                                cudaGraphConditionalHandle cond, int use_cond, const int* n_active) {
     if (!st->stop) {
         const double f_new = fold_tiles(tiles, ntiles);  // :35
-        st->evals += static_cast<unsigned long long>(rows) * st->n_active;
-        if (st->n_active == 0) st->state_error = 1;
+        st->evals += static_cast<unsigned long long>(rows) * *n_active;
+        if (*n_active == 0) st->state_error = 1;
         st->iterations += 1;            // :36
         st->objective = f_new;          // history.push_back (:37)
         if (history) history[st->iterations] = f_new;
         const bool unchanged = __ldcg(&st->changed) == 0;  // :39 (set by other CTAs of this launch)
         st->changed = 0;
-        st->parity ^= 1;                // :40-41 advance
+        st->parity = st->parity == 0 ? 1 : 0;  // :40-41 advance (the slot the assignment wrote)
         const double f = st->f;
         bool stop = unchanged;                                                      // :42-44
         if (!stop && f <= 0.0) stop = true;                                         // :45-47
@@ -521,21 +528,22 @@ __device__ __noinline__ void lloyd_step_body(LloydStatus* st, const double* tile
 }
 
 __global__ void k_lloyd_begin(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
-                              double* history) {
-    if (threadIdx.x == 0) lloyd_begin_body(st, tiles, ntiles, rows, history);
+                              double* history, const int* n_active) {
+    if (threadIdx.x == 0) lloyd_begin_body(st, tiles, ntiles, rows, history, n_active);
 }
 
 __global__ void k_lloyd_step(LloydStatus* st, const double* tiles, uint64_t ntiles, uint64_t rows,
                              unsigned long long max_iterations, double rel_tolerance, double* history,
-                             cudaGraphConditionalHandle cond, int use_cond) {
+                             cudaGraphConditionalHandle cond, int use_cond, const int* n_active) {
     if (threadIdx.x == 0)
-        lloyd_step_body(st, tiles, ntiles, rows, max_iterations, rel_tolerance, history, cond, use_cond);
+        lloyd_step_body(st, tiles, ntiles, rows, max_iterations, rel_tolerance, history, cond, use_cond, n_active);
 }
 
 // Control fused into an assignment launch: mode 1 = begin, 2 = step.
 struct LloydCtl {
     int mode;
     LloydStatus* st;
+    GState* gs;
     unsigned* tiles_done;   // arrival counter over the launch's tiles
     uint64_t ntiles;
     unsigned long long max_iterations;
@@ -548,6 +556,8 @@ struct LloydCtl {
     const double* dists_pair;  // distances of the last two assignments (slot = labels slot)
     uint64_t dstride;
     const int* go;          // when set and *go == 0 the launch does nothing (skipped chunk)
+    int begin_kind;         // begin launches: 0 plain, 1 speculative (incumbent copy), 2 redo unless current
+    int begin_slot;         // begin launches: the slot the assignment writes (parity after the begin)
     const struct AcceptArgs* acc;  // accept state (device copy)
     int accept_run;         // the control runs the accept (:89-94) when the loop stops
     LloydStatus* host_st;   // with acc: the status is also written to mapped host memory
@@ -582,6 +592,10 @@ struct AcceptArgs {
     int ldc;
     int* act_idx;
     float* CT32;
+    double* CactI;   // incumbent's compacted copy (speculative begins read it)
+    int* actI;
+    float* CT32I;
+    GState* gs;
 };
 
 // The accept of the chunk's candidate (all threads of one CTA; sm: 2k ints).
@@ -599,8 +613,8 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         if (deferred) {
             rec->candidate_objective = __longlong_as_double(0x7FF8000000000000LL);
             rec->incumbent_objective = __longlong_as_double(0x7FF8000000000000LL);
-            st->pending_fix = static_cast<int>(chunk);
-            st->fix_par = st->parity;
+            A.gs->pending_fix = static_cast<int>(chunk);
+            A.gs->fix_par = st->parity;
         } else {
             if (accepted) *A.f_opt = st->objective;
             rec->candidate_objective = st->objective;
@@ -608,7 +622,7 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         }
         rec->chunk_index = chunk;
         rec->accepted = accepted;
-        rec->degenerate_repaired = static_cast<unsigned long long>(st->inc_degenerate);
+        rec->degenerate_repaired = static_cast<unsigned long long>(A.gs->inc_degenerate);
         acc_s = accepted;
     }
     __syncthreads();
@@ -644,11 +658,17 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         for (int j = 0; j < k; ++j) {
             dcount += mk[j] ? 1 : 0;
             arank[j] = mk[j] ? -1 : r;
-            if (!mk[j]) A.act_idx[r++] = j;
+            if (!mk[j]) {
+                A.act_idx[r] = j;
+                if (accepted && A.actI) A.actI[r] = j;
+                ++r;
+            }
         }
+        A.gs->inc_degenerate = dcount;
+        A.gs->go = dcount == 0;
+        A.gs->n_active = r;
+        if (accepted) A.gs->n_active_inc = r;
         st->inc_degenerate = dcount;
-        st->go = dcount == 0;
-        st->n_active = r;
         st->incomplete = 0;
         *A.chunk_ctr = chunk_s + 1;
     }
@@ -673,6 +693,17 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
             if (rk < 0) continue;
             A.Cact[static_cast<uint64_t>(rk) * A.ldc + d] = v[r];
             if (A.CT32 && rk < kSMaxK) A.CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v[r]);
+            if (accepted && A.CactI) {  // the incumbent's compacted copy
+                A.CactI[static_cast<uint64_t>(rk) * A.ldc + d] = v[r];
+                if (rk < kSMaxK) A.CT32I[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v[r]);
+            }
+        }
+    }
+    if (accepted) {  // published after the copy: a begin that saw the old version is redone
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(reinterpret_cast<unsigned long long*>(&A.gs->inc_version), 1ull);
         }
     }
     if (host_st) {
@@ -683,8 +714,8 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
 
 // The pending chunk's record gets its exact objectives (thread 0; tiles: the
 // ordered tile partials of its final distances).
-__device__ __forceinline__ void fix_record(LloydStatus* st, const AcceptArgs& A, const double* tiles, uint64_t ntiles) {
-    if (st->pending_fix < 0) return;
+__device__ __forceinline__ void fix_record(GState* gs, const AcceptArgs& A, const double* tiles, uint64_t ntiles) {
+    if (gs->pending_fix < 0) return;
     double fc = 0.0;  // block_sum (:53-54): ordered fold of the tile partials (shared or fresh global memory)
     uint64_t t = 0;
     for (; t + 8 <= ntiles; t += 8) {
@@ -695,12 +726,12 @@ __device__ __forceinline__ void fix_record(LloydStatus* st, const AcceptArgs& A,
         for (int r = 0; r < 8; ++r) fc = __dadd_rn(fc, v[r]);
     }
     for (; t < ntiles; ++t) fc = __dadd_rn(fc, tiles[t]);
-    Record* rec = A.rec_base + st->pending_fix;
+    Record* rec = A.rec_base + gs->pending_fix;
     rec->candidate_objective = fc;
-    if (rec->accepted) st->fopt_exact = fc;  // :89-93
-    rec->incumbent_objective = st->fopt_exact;
-    *A.f_opt = st->fopt_exact;
-    st->pending_fix = -1;
+    if (rec->accepted) gs->fopt_exact = fc;  // :89-93
+    rec->incumbent_objective = gs->fopt_exact;
+    *A.f_opt = gs->fopt_exact;
+    gs->pending_fix = -1;
 }
 
 // block_sum (core.cpp:165-175) by one thread: ordered tile folds, ordered fold of the tiles.
@@ -729,7 +760,8 @@ __device__ __forceinline__ void sum_interval(double s, uint64_t rows, unsigned c
 // Fast-sum Lloyd control (thread 0 of the CTA that arrived last).  Returns the
 // accept decision (0/1) when the loop stopped and the control runs the accept,
 // else -1.
-__device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* st, uint64_t rows, unsigned ctas) {
+__device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* st, uint64_t rows, unsigned ctas,
+                                               int n_active) {
     const double s = st->fsum;
     st->fsum = 0.0;
     st->ctas_done = 0u;
@@ -740,28 +772,35 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
         st->f = s;
         st->f_lo = lo;
         st->f_hi = hi;
-        st->objective = nan;  // exact value: k_accept
-        st->evals = static_cast<unsigned long long>(rows) * st->n_active;
+        st->objective = nan;  // exact value: deferred (fix_record)
+        st->evals = static_cast<unsigned long long>(rows) * n_active;
         st->iterations = 0;
-        st->parity = 0;
+        st->parity = c.begin_slot;
         st->stop = 0;
         st->changed = 0;
-        st->state_error = st->n_active == 0;
+        st->state_error = n_active == 0;
         st->bad_label = 0;
         st->exact_checks = 0;
-        if (c.acc && c.fix_tiles) fix_record(st, *c.acc, c.fix_tiles, tiles_of(c.fix_rows));
+        st->incomplete = 0;
+        // which incumbent this assignment is valid for: a speculative begin is
+        // current only if no accept published a new incumbent since its CTAs started
+        const long long v = static_cast<long long>(__ldcg(reinterpret_cast<const unsigned long long*>(&c.gs->inc_version)));
+        // (only a speculative begin's result may stand in for a later begin)
+        st->begin_version = c.begin_kind == 1 && st->bv_min == v ? v : -1;
         return -1;
     }
+    // the previous chunk's record: its exact objective, before this chunk's accept
+    if (c.acc && c.fix_tiles) fix_record(c.gs, *c.acc, c.fix_tiles, tiles_of(c.fix_rows));
     int decision = -1;
     if (!st->stop) {
-        st->evals += static_cast<unsigned long long>(rows) * st->n_active;
-        if (st->n_active == 0) st->state_error = 1;
+        st->evals += static_cast<unsigned long long>(rows) * n_active;
+        if (n_active == 0) st->state_error = 1;
         st->iterations += 1;  // :36
         st->objective = nan;
         const bool unchanged = st->changed == 0;  // :39
         st->changed = 0;
-        const int par = st->parity;
-        st->parity ^= 1;  // :40-41
+        const int par = st->parity, out = par == 0 ? 1 : 0;
+        st->parity = out;  // :40-41 (the slot this assignment wrote)
         bool stop = unchanged;  // :42-44
         if (!stop) {
             // f <= 0 (:45): terms are >= 0, so the exact f is 0 iff the fast sum is
@@ -782,7 +821,7 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
                 if (!decided) {  // exact block sums of both assignments
                     st->exact_checks += 1;
                     const double f = exact_block_sum(c.dists_pair + par * c.dstride, rows);
-                    const double f_new = exact_block_sum(c.dists_pair + (1 - par) * c.dstride, rows);
+                    const double f_new = exact_block_sum(c.dists_pair + out * c.dstride, rows);
                     stop = __ddiv_rn(__dsub_rn(f, f_new), f) < c.rel_tolerance;
                 }
             }
@@ -796,13 +835,13 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
         if (st->state_error || st->bad_label) stop = true;
         st->stop = stop ? 1 : 0;
         if (stop && c.accept_run) {  // accept (:89): f < f_opt, strict, on the candidate's interval
-            const double fo = st->fopt_exact;
+            const double fo = c.gs->fopt_exact;
             if (!c.force_exact && hi < fo) decision = 1;
             else if (!c.force_exact && !(lo < fo)) decision = 0;
             else decision = exact_block_sum(c.dists_pair + st->parity * c.dstride, rows) < fo;
         } else if (!stop && c.incomplete_after && st->iterations >= c.incomplete_after) {
             st->incomplete = 1;  // the host continues this chunk; the queued next chunk stays idle
-            st->go = 0;
+            c.gs->go = 0;
         }
     }
     if (c.use_cond) cudaGraphSetConditional(c.cond, st->stop ? 0u : 1u);
@@ -818,9 +857,9 @@ __device__ __forceinline__ void tile_done_control(const LloydCtl& c, const doubl
     if (done != c.ntiles - 1) return;
     __threadfence();
     *c.tiles_done = 0u;
-    if (c.mode == 1) lloyd_begin_body(c.st, tiles, c.ntiles, rows, c.history);
+    if (c.mode == 1) lloyd_begin_body(c.st, tiles, c.ntiles, rows, c.history, &c.gs->n_active);
     else lloyd_step_body(c.st, tiles, c.ntiles, rows, c.max_iterations, c.rel_tolerance, c.history, c.cond,
-                         c.use_cond);
+                         c.use_cond, &c.gs->n_active);
 }
 
 // ===========================================================================
@@ -1566,14 +1605,25 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     pdl_wait();
     if (stop_ptr && *stop_ptr) return;
     if (ctl.go && !*ctl.go) return;
+    if (ctl.begin_kind == 2 && ctl.st->begin_version ==
+                                   static_cast<long long>(*reinterpret_cast<const volatile long long*>(&ctl.gs->inc_version)))
+        return;  // the speculative begin of this chunk is current
+    if (ctl.begin_kind == 1) {  // speculative begin: the incumbent version before any of its reads
+        if (threadIdx.x == 0) {
+            const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(&ctl.gs->inc_version));
+            atomicMin(reinterpret_cast<unsigned long long*>(&ctl.st->bv_min), v);
+            __threadfence();
+        }
+        __syncthreads();
+    }
     const int KA = *n_active_ptr;
     int32_t* labels_out = labels_pair;
     const int32_t* labels_old = nullptr;
-    if (parity_ptr) {
-        const int par = *parity_ptr;
-        labels_out = labels_pair + (1 - par) * pair_stride;
+    if (parity_ptr) {  // rounds: read slot par (0, 1, or 2 after a graph-mode begin), write the other of 0/1
+        const int par = *parity_ptr, out = par == 0 ? 1 : 0;
+        labels_out = labels_pair + out * pair_stride;
         labels_old = labels_pair + par * pair_stride;
-        if (dists_out) dists_out += (1 - par) * dstride;  // dstride 0: one distance buffer
+        if (dists_out) dists_out += out * dstride;  // dstride 0: one distance buffer
     }
     const int KG = (KA + kAK - 1) / kAK;
     const bool comp = warp < KG;
@@ -1593,14 +1643,14 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                   "centroid staging of tma_chains overlaps the item list");
     ktrace(0, hmode);
     int qb = 0;
-    if (np == 0) {  // fixup CTA of a begin launch: one tile of the pending chunk's final distances
-        const LloydStatus* st = ctl.st;
-        const int pend = st->pending_fix;
+    if (np == 0) {  // fixup CTA of a round-1 launch: one tile of the pending chunk's final distances
+        const GState* gst = ctl.gs;
+        const int pend = gst->pending_fix;
         if (ctl.fix_tiles && pend >= 0) {
             const uint64_t t = (p0 - rows) / kABP;  // fixup CTAs follow the point blocks
             const uint64_t R = ctl.fix_rows, tb = t * kTile;
             if (tb < R) {
-                const double* dv = ctl.dists_all + (2 * static_cast<uint64_t>(pend & 1) + st->fix_par) * R + tb;
+                const double* dv = ctl.dists_all + (3 * static_cast<uint64_t>(pend & 1) + gst->fix_par) * R + tb;
                 const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), R - tb));
                 double* fbuf = reinterpret_cast<double*>(&S.raw[0][0]);
                 for (int i = tid; i < len; i += kSThreads) fbuf[i] = __ldcg(dv + i);
@@ -1939,7 +1989,15 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 ++it;
             }
         }
-        tma_chains<T>(S, &tmx, p0, n, nslab, qb + nslab, Cact, ldc, KA, NI, item_p, item_j, item_d);
+        if (NI > static_cast<uint32_t>(kSThreads)) {
+            tma_chains<T>(S, &tmx, p0, n, nslab, qb + nslab, Cact, ldc, KA, NI, item_p, item_j, item_d);
+        } else {  // one item per thread, rows straight from L2
+            __syncthreads();
+            if (tid < static_cast<int>(NI))
+                item_d[tid] = exact_row_dist(X + (p0 + item_p[tid]) * ld,
+                                             Cact + static_cast<uint64_t>(item_j[tid]) * ldc, n);
+            __syncthreads();
+        }
     }
     ktrace(9, hmode);
     if (tid < np) {
@@ -2038,7 +2096,7 @@ fold:
             }
         }
         __syncthreads();
-        if (tid == 0) S.n_items = static_cast<uint32_t>(lloyd_fast_control(cl, sst, rows, gridDim.x));
+        if (tid == 0) S.n_items = static_cast<uint32_t>(lloyd_fast_control(cl, sst, rows, gridDim.x, KA));
         __syncthreads();
         ktrace(29, hmode);
         const int decision = static_cast<int>(S.n_items);
@@ -2465,21 +2523,21 @@ __global__ void k_accept(LloydStatus* st, AcceptArgs A, LloydStatus* host_st) {
 
 // Head of a chunk's Lloyd graph: the chunk runs only when the previous accept
 // left no degenerate incumbent rows, or the host has repaired them (st->go).
-__global__ void k_guard(const LloydStatus* st, cudaGraphConditionalHandle h) {
+__global__ void k_guard(const GState* gs, cudaGraphConditionalHandle h) {
     klog_start(0);
-    cudaGraphSetConditional(h, st->go != 0 ? 1u : 0u);
+    cudaGraphSetConditional(h, gs->go != 0 ? 1u : 0u);
     klog_end(0);
 }
 
 // The last chunk's record: its exact objective (graph mode, after the loop).
-__global__ void k_fix_final(LloydStatus* st, AcceptArgs A, const double* __restrict__ dists_all, uint64_t R,
+__global__ void k_fix_final(GState* gs, AcceptArgs A, const double* __restrict__ dists_all, uint64_t R,
                             double* __restrict__ tiles, unsigned* __restrict__ counter) {
     __shared__ __align__(16) double fbuf[kTile];
     __shared__ int last;
-    const int pend = st->pending_fix;
+    const int pend = gs->pending_fix;
     if (pend < 0) return;
     const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
-    const double* dv = dists_all + (2 * static_cast<uint64_t>(pend & 1) + st->fix_par) * R + tb;
+    const double* dv = dists_all + (3 * static_cast<uint64_t>(pend & 1) + gs->fix_par) * R + tb;
     const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), R - tb));
     for (int i = threadIdx.x; i < len; i += blockDim.x) fbuf[i] = __ldcg(dv + i);
     __syncthreads();
@@ -2490,24 +2548,33 @@ __global__ void k_fix_final(LloydStatus* st, AcceptArgs A, const double* __restr
         if (last) {
             __threadfence();
             *counter = 0u;
-            fix_record(st, A, tiles, gridDim.x);
+            fix_record(gs, A, tiles, gridDim.x);
         }
     }
 }
 
+__global__ void k_bump_version(GState* gs) { gs->inc_version += 1; }
+
 // Reset of the per-run device state (incumbent all degenerate, f_opt = +inf).
-__global__ void k_run_init(LloydStatus* st, double* f_opt, double* Cinc, uint8_t* maskinc, double* C,
-                           uint8_t* mask, int k, int n, unsigned long long* chunk_ctr) {
+__global__ void k_run_init(LloydStatus* st, int nst, GState* gs, double* f_opt, double* Cinc, uint8_t* maskinc,
+                           double* C, uint8_t* mask, int k, int n, unsigned long long* chunk_ctr) {
     for (int e = threadIdx.x; e < k * n; e += blockDim.x) Cinc[e] = C[e] = 0.0;
     for (int j = threadIdx.x; j < k; j += blockDim.x) maskinc[j] = mask[j] = 1;
     if (threadIdx.x == 0) {
         *f_opt = __longlong_as_double(0x7FF0000000000000LL);
-        st->inc_degenerate = k;
-        st->go = 0;
-        st->stop = 1;  // a skipped chunk's rounds see a finished loop
-        st->fopt_exact = __longlong_as_double(0x7FF0000000000000LL);
-        st->pending_fix = -1;
-        st->incomplete = 0;
+        for (int b = 0; b < nst; ++b) {
+            st[b].inc_degenerate = k;
+            st[b].stop = 1;  // a skipped chunk's rounds see a finished loop
+            st[b].incomplete = 0;
+            st[b].begin_version = -1;
+        }
+        gs->fopt_exact = __longlong_as_double(0x7FF0000000000000LL);
+        gs->inc_version = 0;
+        gs->n_active_inc = 0;
+        gs->inc_degenerate = k;
+        gs->go = 0;
+        gs->pending_fix = -1;
+        gs->fix_par = 0;
         *chunk_ctr = 0;
     }
 }
