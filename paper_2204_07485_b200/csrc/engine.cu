@@ -160,6 +160,10 @@ struct Workspace {
     // K-means++ (init.cpp:123-201)
     DevBuf<double> d2pool;   // (ncand + 1) * R
     DevBuf<uint32_t> cand;   // ncand
+    DevBuf<Mt64State> ppmt;  // device K-means++: the RNG stream during the device steps
+    DevBuf<dev::PPState> pps;
+    DevBuf<long long> pprefix;  // R: exact integer prefix sums of the D^2 weights (per 1024-tile)
+    DevBuf<long long> pptiles;  // tile totals
     // incumbent (big_means.cpp:63-64, 89-93)
     DevBuf<double> Cinc, fopt;
     DevBuf<uint8_t> maskinc;
@@ -199,6 +203,7 @@ struct Workspace {
     HostBuf<double> h_d2;
     HostBuf<uint8_t> h_mask;
     HostBuf<uint32_t> h_cand;
+    HostBuf<Mt64State> h_mt;
 
     static void encode_ct_map(CUtensorMap* map, float* base, int n) {
         auto enc = tmap_encoder();
@@ -272,6 +277,7 @@ struct Workspace {
         h_d2.alloc(R);
         h_mask.alloc(k);
         h_cand.alloc(ncand);
+        h_mt.alloc(1);
     }
 };
 
@@ -928,13 +934,13 @@ void set_row_any(cudaStream_t st, const Points& P, Workspace& w, uint64_t row, i
 }
 
 void launch_dist_rows(cudaStream_t st, const Points& P, const uint32_t* cand, int ncand, const double* d2,
-                      double* out) {
+                      double* out, const int* skip = nullptr) {
     PhaseScope ps(PH_KMEANSPP, P.rows);
-    const unsigned grid = (unsigned)ceil_div(P.rows, 128);
+    const dim3 grid((unsigned)ceil_div(P.rows, 128), (unsigned)std::max(1, ncand));
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         dev::k_dist_rows<T><<<grid, 128, 0, st>>>(static_cast<const T*>(P.X), P.rows, P.n, P.ld, cand,
-                                                  ncand, d2, out);
+                                                  ncand, d2, out, skip);
     });
     BM_LAUNCH();
     count_launch();
@@ -978,10 +984,62 @@ void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::v
         launch_assign(st, P, w, w.k, w.labels.p, 0, nullptr, buf(d2i), nullptr, nullptr);
         evals += m * (uint64_t)active;
     }
-    std::vector<double> cum(m);
-    std::vector<double> pot(candidates);
-    std::vector<uint64_t> picks(candidates);
     const uint64_t ntiles = tiles_of(m);
+    // Device steps while the D^2 weights are integers (exact prefix sums); the
+    // host path below continues from the first step that is not.
+    static const bool dev_pp = !(std::getenv("BM_PP") && std::string(std::getenv("BM_PP")) == "host");
+    if (dev_pp && candidates <= 8 && first_slot < degenerate.size()) {
+        if (!w.ppmt.n) w.ppmt.alloc(1);
+        if (!w.pps.n) w.pps.alloc(1);
+        if (w.pprefix.n < w.R) w.pprefix.alloc(w.R);
+        if (w.pptiles.n < ceil_div(w.R, dev::kPPThreads)) w.pptiles.alloc(ceil_div(w.R, dev::kPPThreads));
+        *w.h_mt.p = rng.s;
+        BM_CUDA(cudaMemcpyAsync(w.ppmt.p, w.h_mt.p, sizeof(Mt64State), cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaMemsetAsync(w.pps.p, 0, sizeof(dev::PPState), st));
+        const unsigned cgrid = (unsigned)std::min<uint64_t>(ceil_div(m, 256), 296);
+        for (size_t q = first_slot; q < degenerate.size(); ++q) {
+            dev::k_pp_scan<<<(unsigned)ceil_div(m, dev::kPPThreads), dev::kPPThreads, 0, st>>>(
+                buf(d2i), m, w.pprefix.p, w.pptiles.p, w.pps.p);
+            BM_LAUNCH();
+            dev::k_pp_pick<<<1, dev::kPPThreads, 0, st>>>(m, w.ppmt.p, candidates, w.cand.p, w.pprefix.p,
+                                                          w.pptiles.p, w.pps.p);
+            BM_LAUNCH();
+            // (skipped after a fallback or a direct pick: the first two PPState fields)
+            launch_dist_rows(st, P, w.cand.p, candidates, buf(d2i), buf(0), &w.pps.p->fallback);  // :186-189
+            launch_tile_sums(st, buf(0), m, w.R, candidates, w.tile_buf.p, &w.pps.p->fallback);  // :190
+            dispatch(P.dtype, [&](auto tag) {
+                using T = decltype(tag);
+                dev::k_pp_best<T><<<1, 128, 0, st>>>(w.tile_buf.p, ntiles, candidates, w.cand.p, w.pps.p,
+                                                     static_cast<const T*>(P.X), P.ld, P.n, w.C.p, w.mask.p,
+                                                     degenerate[q]);
+            });
+            BM_LAUNCH();
+            dev::k_pp_take<<<cgrid, 256, 0, st>>>(w.d2pool.p, w.R, m, d2i, w.pps.p);
+            BM_LAUNCH();
+            count_launch(3);
+        }
+        dev::PPState ps{};
+        BM_CUDA(cudaMemcpyAsync(&ps, w.pps.p, sizeof(ps), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(w.h_mt.p, w.ppmt.p, sizeof(Mt64State), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        rng.s = *w.h_mt.p;  // the stream after the device steps (a failed step drew nothing)
+        evals += m * (uint64_t)candidates * (uint64_t)ps.cand_slots;
+        // the slots done on the device: candidate slots + direct picks, in order,
+        // up to the first failed one
+        if (!ps.fallback) {
+            for (size_t q = first_slot; q < degenerate.size(); ++q) mask[degenerate[q]] = 0;
+            return;
+        }
+        // find how many slots completed: the device counts candidate slots only,
+        // so replay the completed count from the masks written on the device
+        std::vector<uint8_t> dmask(w.k);
+        BM_CUDA(cudaMemcpy(dmask.data(), w.mask.p, w.k, cudaMemcpyDeviceToHost));
+        size_t q0 = first_slot;
+        while (q0 < degenerate.size() && dmask[degenerate[q0]] == 0) mask[degenerate[q0++]] = 0;
+        first_slot = q0;
+    }
+    std::vector<double> cum(m);
+    std::vector<uint64_t> picks(candidates);
     for (size_t q = first_slot; q < degenerate.size(); ++q) {  // :171-199
         const int slot = degenerate[q];
         BM_CUDA(cudaMemcpyAsync(w.h_d2.p, buf(d2i), m * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -2587,11 +2587,12 @@ __global__ void k_run_init(LloydStatus* st, int nst, GState* gs, double* f_opt, 
 template <typename T>
 __global__ void k_dist_rows(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                             const uint32_t* __restrict__ cand, int ncand,
-                            const double* __restrict__ d2, double* __restrict__ out) {
+                            const double* __restrict__ d2, double* __restrict__ out, const int* skip) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= rows) return;
+    if (skip && (skip[0] || skip[1])) return;  // device K-means++ step: fallback or direct pick
     const T* x = X + i * ld;
-    for (int c = 0; c < ncand; ++c) {
+    for (int c = blockIdx.y; c < ncand; c += gridDim.y) {  // one candidate per grid row
         const T* r = X + static_cast<uint64_t>(cand[c]) * ld;
         double sum = 0.0;
         for (int d = 0; d < n; ++d) sum = dist_step(sum, to_f64(x[d]), to_f64(r[d]));
@@ -2601,6 +2602,208 @@ __global__ void k_dist_rows(const T* __restrict__ X, uint64_t rows, int n, uint6
         }
         out[static_cast<uint64_t>(c) * rows + i] = sum;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Device K-means++ step (init.cpp:171-199) for integer D^2 weights.
+// prefix_sums (init.cpp:81-88) is a sequential fp64 fold; when every weight is
+// an integer and the total stays below 2^53 every partial sum is exact, so an
+// integer scan reproduces it bit for bit.  Otherwise the step reports
+// `fallback` (before consuming any draw) and the host path takes over.
+// ---------------------------------------------------------------------------
+struct PPState {
+    int fallback;     // this slot needs the host path (non-integer or huge weights)
+    int direct;       // total <= 0: uniform pick, no candidates (:174-180)
+    int best;         // candidate chosen by k_pp_best (-1: none)
+    int cand_slots;   // slots that evaluated candidates (n_d accounting)
+    long long direct_idx;
+};
+
+__device__ uint64_t mt_uniform_int(uint64_t* x, int& pos, uint64_t a, uint64_t b) {  // uniform_int_dist.h:252-331
+    const uint64_t urange = b - a;
+    if (urange == ~0ull) return mt_next_seq(x, pos) + a;
+    const uint64_t r = urange + 1;
+    uint64_t y = mt_next_seq(x, pos);
+    uint64_t low = y * r;
+    if (low < r) {
+        const uint64_t thr = (0 - r) % r;
+        while (low < thr) {
+            y = mt_next_seq(x, pos);
+            low = y * r;
+        }
+    }
+    return mul_hi64(y, r) + a;
+}
+
+__device__ double mt_uniform_real(uint64_t* x, int& pos, double a, double b) {  // generate_canonical<double,53>
+    double c = __dmul_rn(__ull2double_rn(mt_next_seq(x, pos)), 0x1p-64);
+    if (c >= 1.0) c = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
+    return __dadd_rn(__dmul_rn(c, __dsub_rn(b, a)), a);
+}
+
+constexpr int kPPThreads = 1024;
+
+// Step A, one CTA per 1024-weight tile: integrality check and the tile's
+// inclusive integer scan (coalesced).
+__global__ void __launch_bounds__(kPPThreads)
+k_pp_scan(const double* __restrict__ d2, uint64_t m, long long* __restrict__ prefix,
+          long long* __restrict__ tile_tot, PPState* ps) {
+    __shared__ long long wsum[kPPThreads / 32];
+    if (ps->fallback) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kPPThreads + tid;
+    long long v = 0;
+    bool bad = false;
+    if (i < m) {
+        const double x = d2[i];
+        if (!(x >= 0.0 && x < 0x1p53 && x == rint(x))) bad = true;
+        else v = static_cast<long long>(x);
+    }
+    if (__syncthreads_or(bad)) {
+        if (tid == 0) ps->fallback = 1;  // every tile sees its own weights; any one suffices
+        return;
+    }
+    long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const long long x = wsum[lane];
+        long long w = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+            if (lane >= o) w += y;
+        }
+        wsum[lane] = w - x;
+        if (lane == 31) tile_tot[blockIdx.x] = w;
+    }
+    __syncthreads();
+    if (i < m) prefix[i] = wsum[warp] + incl;
+}
+
+// Step B, one CTA: tile offsets, total, the draws (one thread, the reference's
+// order) and pick_by_mass (init.cpp:73-79) for each draw.
+__global__ void __launch_bounds__(kPPThreads)
+k_pp_pick(uint64_t m, Mt64State* __restrict__ mt, int candidates, uint32_t* __restrict__ cand,
+          const long long* __restrict__ prefix, const long long* __restrict__ tile_tot, PPState* ps) {
+    __shared__ uint64_t xs[kMtN];
+    __shared__ long long toff[kPPThreads + 1];
+    __shared__ double us[8];
+    __shared__ int direct_s, tsel, first;
+    if (ps->fallback) return;
+    const int tid = threadIdx.x;
+    const int ntiles = static_cast<int>((m + kPPThreads - 1) / kPPThreads);
+    if (ntiles > kPPThreads) {  // beyond one CTA's offset table: host path
+        if (tid == 0) ps->fallback = 1;
+        return;
+    }
+    if (tid == 0) {  // exclusive offsets of the tiles (<= 1024 exact integer adds)
+        long long r = 0;
+        for (int t = 0; t < ntiles; ++t) {
+            toff[t] = r;
+            r += tile_tot[t];
+        }
+        toff[ntiles] = r;
+    }
+    if (tid < kMtN) xs[tid] = mt->x[tid];
+    __syncthreads();
+    const long long total = toff[ntiles];
+    if (total >= (1ll << 53)) {  // partial sums could round
+        if (tid == 0) ps->fallback = 1;
+        return;
+    }
+    if (tid == 0) {
+        int pos = static_cast<int>(mt->pos);
+        if (total <= 0) {  // :174-180
+            ps->direct_idx = static_cast<long long>(mt_uniform_int(xs, pos, 0, m - 1));
+            direct_s = 1;
+        } else {
+            for (int c = 0; c < candidates; ++c) us[c] = mt_uniform_real(xs, pos, 0.0, static_cast<double>(total));
+            direct_s = 0;
+            ps->cand_slots += 1;
+        }
+        ps->direct = direct_s;
+        mt->pos = static_cast<uint64_t>(pos);
+    }
+    __syncthreads();
+    if (tid < kMtN) mt->x[tid] = xs[tid];
+    if (direct_s) return;
+    for (int c = 0; c < candidates; ++c) {  // first index whose cumulative exceeds u
+        const double u = us[c];
+        if (tid == 0) {
+            tsel = ntiles;
+            first = kPPThreads;
+        }
+        __syncthreads();
+        if (tid < ntiles && static_cast<double>(toff[tid + 1]) > u) atomicMin(&tsel, tid);
+        __syncthreads();
+        const int t = tsel;
+        if (t < ntiles) {
+            const uint64_t i = static_cast<uint64_t>(t) * kPPThreads + tid;
+            if (i < m && static_cast<double>(toff[t] + prefix[i]) > u) atomicMin(&first, tid);
+            __syncthreads();
+            if (tid == 0) cand[c] = static_cast<uint32_t>(static_cast<uint64_t>(t) * kPPThreads + first);
+        } else if (tid == 0) {
+            cand[c] = static_cast<uint32_t>(m - 1);  // upper_bound == end: the last index
+        }
+        __syncthreads();
+    }
+}
+
+// Best candidate by potential (block_sum of the trial, :190-195, strict <)
+// and set_row(slot) (:197).
+template <typename T>
+__global__ void k_pp_best(const double* __restrict__ tiles, uint64_t ntiles, int candidates,
+                          const uint32_t* __restrict__ cand, PPState* ps, const T* __restrict__ X, uint64_t ld,
+                          int n, double* __restrict__ C, uint8_t* __restrict__ mask, int slot) {
+    __shared__ long long row_s;
+    __shared__ __align__(16) double tl[4 * 1024];
+    if (ps->fallback) return;
+    const bool staged = static_cast<uint64_t>(candidates) * ntiles <= 4 * 1024;
+    if (staged && !ps->direct)
+        for (uint64_t e = threadIdx.x; e < static_cast<uint64_t>(candidates) * ntiles; e += blockDim.x) tl[e] = tiles[e];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long row = 0;
+        int bi = -1;
+        if (ps->direct) {
+            row = ps->direct_idx;
+        } else {
+            double best = __longlong_as_double(0x7FF0000000000000LL);
+            for (int c = 0; c < candidates; ++c) {
+                const double* tc = (staged ? tl : tiles) + static_cast<uint64_t>(c) * ntiles;
+                double pot = 0.0;  // block_sum outer fold
+                for (uint64_t t = 0; t < ntiles; ++t) pot = __dadd_rn(pot, tc[t]);
+                if (pot < best) {
+                    best = pot;
+                    bi = c;
+                    row = cand[c];
+                }
+            }
+        }
+        ps->best = bi;
+        row_s = row;
+    }
+    __syncthreads();
+    const uint64_t r = static_cast<uint64_t>(row_s);
+    for (int d = threadIdx.x; d < n; d += blockDim.x)
+        C[static_cast<uint64_t>(slot) * n + d] = to_f64(X[r * ld + d]);
+    if (threadIdx.x == 0) mask[slot] = 0;
+}
+
+// dist2 := best_trial (:198)
+__global__ void k_pp_take(double* __restrict__ pool, uint64_t R, uint64_t m, int d2i, const PPState* ps) {
+    if (ps->fallback || ps->direct || ps->best < 0) return;
+    const double* src = pool + static_cast<uint64_t>(ps->best) * R;
+    double* dst = pool + static_cast<uint64_t>(d2i) * R;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
 }
 
 // set_row (core.cpp:78-83 / init.cpp:146,197): centroid j := pool row.

@@ -185,3 +185,36 @@ def test_lloyd_bound_fast_path_vs_oracle(port, case):
     assert (o.centroids.mask == p["mask"]).all()
     assert (o.assignment == p["labels"]).all()
     assert (bits(o.objective_history) == bits(p["history"])).all()
+
+
+@pytest.mark.parametrize("case", ["integer", "real", "huge_integer", "partial_integer", "zeros"])
+def test_kmeanspp_device_steps_vs_oracle(port, case):
+    """K-means++ steps run on the device while the D^2 weights are integers
+    (exact prefix sums), else on the host from the same stream position."""
+    rng = np.random.default_rng(21)
+    k, cands = 9, 3
+    mask = np.ones(k, np.uint8)
+    Cn = np.zeros((k, 5))
+    if case == "integer":
+        X = np.rint(rng.normal(size=(7000, 5)) * 6)
+    elif case == "real":
+        X = rng.normal(size=(7000, 5)) * 6
+    elif case == "huge_integer":  # totals beyond 2^53: host prefix sums
+        X = np.rint(rng.normal(size=(7000, 5)) * 2e7)
+    elif case == "partial_integer":  # active rows are data points: integer weights
+        X = np.rint(rng.normal(size=(7000, 5)) * 6)
+        Cn[:3] = X[:3]
+        mask[:3] = 0
+    else:  # many coincident points: zero weights, total <= 0 branch
+        X = np.zeros((500, 5))
+        X[:3] = [[1, 0, 0, 0, 0], [2, 0, 0, 0, 0], [3, 0, 0, 0, 0]]
+    counter = bm.EvalCounter()
+    r = bm.Rng(44)
+    got = bm.kmeanspp_fill(bm.Dataset(X), bm.Centroids(Cn.copy(), mask.copy()),
+                           bm.InitConfig(candidates_per_step=cands), r, counter)
+    pr = port.rng(44)
+    Ce, me, ev = port.kmeanspp_fill(X, Cn.copy(), mask.copy(), cands, pr)
+    assert (bits(got.values) == bits(Ce)).all()
+    assert (got.mask == me).all()
+    assert counter.distance_evals == ev
+    assert r() == port.rng_next(pr)
