@@ -1603,7 +1603,10 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         fence_mbar_init();
     }
     pdl_wait();
-    if (stop_ptr && *stop_ptr) return;
+    if (stop_ptr && *stop_ptr) {  // a finished loop: close the WHILE node if this launch drives one
+        if (ctl.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(ctl.cond, 0u);
+        return;
+    }
     if (ctl.go && !*ctl.go) return;
     if (ctl.begin_kind == 2 && ctl.st->begin_version ==
                                    static_cast<long long>(*reinterpret_cast<const volatile long long*>(&ctl.gs->inc_version)))
