@@ -1437,6 +1437,7 @@ struct TmaSmem {
     int lab_rank[kABP];                                        // chosen compacted centroid per point
     int rank_of[kSMaxK];                                       // label -> compacted index
     float delta[kSMaxK];                                       // centroid movement per label (rounded up)
+    alignas(16) float lbs[sizeof(T) == 4 ? kABP : 1][kSMaxK];  // fp32 round fast path: the bound rows (16-byte chunks swizzled)
     uint64_t bar[2];
     uint32_t n_items;
     int is_last;
@@ -1481,6 +1482,25 @@ __device__ __forceinline__ double exact_row_dist(const T* __restrict__ x, const 
         }
     }
     for (; d < n; ++d) a = dist_step(a, to_f64(x[d]), c[d]);
+    return a;
+}
+
+// Exact fp64 distance (core.cpp:142-146) of a point row staged in shared memory
+// (fp32 storage, 16-byte aligned) to a centroid row read from L1/L2.
+__device__ __forceinline__ double chain_smem_row(const float* x, const double* __restrict__ c, int n) {
+    double a = 0.0;
+    int d = 0;
+#pragma unroll 4
+    for (; d + 4 <= n; d += 4) {
+        const float4 xv = *reinterpret_cast<const float4*>(x + d);
+        const double2 c0 = __ldg(reinterpret_cast<const double2*>(c + d));
+        const double2 c1 = __ldg(reinterpret_cast<const double2*>(c + d + 2));
+        a = dist_step(a, xv.x, c0.x);
+        a = dist_step(a, xv.y, c0.y);
+        a = dist_step(a, xv.z, c1.x);
+        a = dist_step(a, xv.w, c1.y);
+    }
+    for (; d < n; ++d) a = dist_step(a, x[d], c[d]);
     return a;
 }
 
@@ -1664,13 +1684,157 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         goto fold;
     }  // TMA slabs this CTA has consumed (ring position)
 
+    // ------- Lloyd-round fast path, fp32 storage (exact, certified) -------
+    // As the generic path below, but the CTA's point rows and bound rows are
+    // fetched once with cp.async at the start (overlapping the setup), and
+    // every exact chain reads its point from shared memory.
+    if constexpr (sizeof(T) == 4) {
+        const int ldr = static_cast<int>(ld);  // floats per row, a multiple of 4
+        const size_t rows_cap = static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse);
+        if (hmode == 2 && labels_old && lbk && delta && static_cast<size_t>(kABP) * ldr * 4 <= rows_cap) {
+            float* xr = reinterpret_cast<float*>(reuse);  // [128][ldr]
+            const int vpr = ldr / 4;
+            for (int e = tid; e < np * vpr; e += kSThreads) {
+                const int p = e / vpr, v = e - p * vpr;
+                cp_async_16(xr + p * ldr + 4 * v, X + (p0 + p) * ld + 4 * v);
+            }
+            for (int e = tid; e < np * (kSMaxK / 4); e += kSThreads) {
+                const int p = e >> 3, c = e & 7;
+                cp_async_16(&S.lbs[p][4 * ((c ^ p) & 7)], lbk + (p0 + p) * kSMaxK + 4 * c);
+            }
+            cp_async_commit();
+            if (tid < kSMaxK) {
+                S.rank_of[tid] = -1;
+                S.delta[tid] = 0.f;
+            }
+            __syncthreads();
+            if (tid < KA) {
+                const int j = act_idx[tid];
+                S.rank_of[j] = tid;
+                S.delta[j] = delta[j];  // movement of label j in the last update (rounded up)
+            }
+            int a = -1, ra = -1;
+            if (tid < np) a = labels_old[p0 + tid];
+            cp_async_wait<0>();
+            __syncthreads();  // rows, bounds, ranks and movements in place
+            if (tid < np) ra = (a >= 0 && a < kfull) ? S.rank_of[a] : -1;
+            ktrace(13, hmode);
+            // the exact distance to the previous label; decayed bounds of the others
+            unsigned fails = 0;
+            double dn = 0.0;
+            if (tid < np) {
+                if (ra >= 0) dn = chain_smem_row(xr + tid * ldr, Cact + static_cast<uint64_t>(ra) * ldc, n);
+#pragma unroll
+                for (int c4 = 0; c4 < kSMaxK / 4; ++c4) {
+                    float* vv = &S.lbs[tid][4 * ((c4 ^ tid) & 7)];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int j = 4 * c4 + e;
+                        if (S.rank_of[j] < 0 || j == a) continue;
+                        const float lbn = fmaxf(__fsub_rd(vv[e], S.delta[j]), 0.f);
+                        vv[e] = lbn;
+                        const float L = __fmul_rd(__fmul_rd(lbn, lbn), cst.lo64);
+                        if (ra < 0 || !(dn < static_cast<double>(L))) fails |= 1u << j;
+                    }
+                }
+            }
+            if (tid < kABP) S.cand[tid] = fails;
+            __syncthreads();
+            if (tid < 32) {  // exclusive scan of the per-point recheck counts -> item offsets
+                int v[4], run = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    v[q] = __popc(S.cand[4 * tid + q]);
+                    run += v[q];
+                }
+                int incl = run;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (tid >= o) incl += y;
+                }
+                int ex = incl - run;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    S.icount[4 * tid + q] = ex;
+                    ex += v[q];
+                }
+                if (tid == 31) S.n_items = static_cast<uint32_t>(incl);
+            }
+            __syncthreads();
+            const uint32_t NI = S.n_items;
+            if (tid == 0 && cand_counter) {
+                atomicAdd(cand_counter, static_cast<unsigned long long>(np + NI));
+                atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
+            }
+            if (NI <= static_cast<uint32_t>(kItemCap)) {
+                if (tid < np) {
+                    uint32_t it = S.icount[tid];
+                    unsigned bits = fails;
+                    while (bits) {  // ascending label = ascending compacted rank
+                        const int j = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        item_p[it] = static_cast<short>(tid);
+                        item_j[it] = static_cast<signed char>(S.rank_of[j]);
+                        ++it;
+                    }
+                }
+                __syncthreads();
+                for (uint32_t i = tid; i < NI; i += kSThreads)
+                    item_d[i] = chain_smem_row(xr + item_p[i] * ldr, Cact + static_cast<uint64_t>(item_j[i]) * ldc, n);
+                __syncthreads();
+                if (tid < np) {
+                    const uint64_t gp = p0 + tid;
+                    // (value, label) minimum over the previous label and the rechecked ones:
+                    // every other label is certified strictly farther (core.cpp:147)
+                    const double inf = __longlong_as_double(0x7FF0000000000000LL);
+                    double best = ra >= 0 ? dn : inf;
+                    int bl = ra >= 0 ? a : -1;
+                    const uint32_t i0 = S.icount[tid], i1 = i0 + __popc(fails);
+                    const double hi = static_cast<double>(cst.hi64);
+                    auto lbound = [&](double d) {  // true distance >= fl64 distance / (1+g64)
+                        const double q = __dsub_rd(__ddiv_rd(d, hi), 1e-300);
+                        return q > 0.0 ? (q < 3.0e38 ? __fsqrt_rd(__double2float_rd(q)) : 1.0e19f) : 0.f;
+                    };
+                    for (uint32_t i = i0; i < i1; ++i) {
+                        const double d = item_d[i];
+                        const int l = act_idx[item_j[i]];
+                        S.lbs[tid][4 * (((l >> 2) ^ tid) & 7) + (l & 3)] = lbound(d);
+                        if (d < best || (d == best && l < bl)) {
+                            best = d;
+                            bl = l;
+                        }
+                    }
+                    if (ra >= 0) S.lbs[tid][4 * (((a >> 2) ^ tid) & 7) + (a & 3)] = lbound(dn);
+                    labels_out[gp] = bl;
+                    if (dists_out) dists_out[gp] = best;
+                    if (bl != a) *changed_flag = 1;
+                }
+                __syncthreads();
+                for (int e = tid; e < np * (kSMaxK / 4); e += kSThreads) {  // bound rows back, coalesced
+                    const int p = e >> 3, c = e & 7;
+                    reinterpret_cast<float4*>(lbk + (p0 + p) * kSMaxK)[c] =
+                        *reinterpret_cast<const float4*>(&S.lbs[p][4 * ((c ^ p) & 7)]);
+                }
+                ktrace(15, hmode);
+                goto fold;
+            }
+            // many rechecks: the full screen below rewrites everything; its TMA
+            // writes (async proxy) follow our generic writes to the same bytes
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+        }
+    }
+
     // ---------------- Lloyd-round fast path (exact, certified) ----------------
     // Per (point, label) lower bounds in distance units (lbk, written by the
     // previous assignment) minus the label's centroid movement stay lower
     // bounds.  A label whose decayed bound squared (x (1-g64)) exceeds the
     // exact distance to the previous label cannot win or tie the reference's
     // scan; the others are rechecked exactly.  Too many rechecks: full screen.
-    if (hmode == 2 && labels_old && lbk && delta) {
+    if (hmode == 2 && labels_old && lbk && delta &&
+        !(sizeof(T) == 4 && static_cast<size_t>(kABP) * ld * 4 <=
+                                static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse))) {
         if (tid < kSMaxK) {
             S.rank_of[tid] = -1;
             S.delta[tid] = 0.f;
