@@ -1616,14 +1616,14 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             }
             if (!queued) launch_lloyd(chunk);
             if (next && spec) launch_spec(chunk + 1);
+            queued = next && speculate;
+            if (queued) launch_lloyd(chunk + 1);  // runs iff this chunk's accept needs no repair
             // chunk+2's draws and prep, assuming chunk+1 needs no repair (else redone above)
             spec_next = next && speculate && exists(chunk + 2);
             if (spec_next) {
                 draw(chunk + 2);
                 launch_prep(chunk + 2);
             }
-            queued = next && speculate;
-            if (queued) launch_lloyd(chunk + 1);  // runs iff this chunk's accept needs no repair
             BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
             if (w.h_status.p[b].incomplete) {  // more rounds than the graph unrolls
                 BM_CUDA(cudaGraphLaunch(w.g_cont[i6], st));

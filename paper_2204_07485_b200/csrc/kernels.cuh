@@ -131,6 +131,8 @@ __device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v
 // diff = x - c; sum += diff * diff  (three separately rounded operations).
 // Programmatic dependent launch: wait for the previous kernel's completion and
 // memory (no-op when not launched as a dependent); allow the next kernel to launch.
+// (The assignment and the update do not trigger early: dependents that wait
+// on SM slots starve the prep and speculative kernels on the other streams.)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
@@ -2227,7 +2229,6 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
 fold:
     ktrace(10, hmode);
-    pdl_trigger();
     if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
         __syncthreads();  // distances of this CTA written (some by other threads)
         double v = tid < np ? dists_out[p0 + tid] : 0.0;
@@ -2525,7 +2526,6 @@ k_update(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
         u.psum[(static_cast<uint64_t>(d0 + dd) * k + j) * u.tstride + tile] = acc;
     }
 
-    pdl_trigger();
     // ---- the last G CTAs of this slab merge it, pairs g, g + G, ... each ----
     // (they wait for the slab's other CTAs: those hold no resources the
     // waiting ones need, so they always complete)
