@@ -295,6 +295,7 @@ struct SamplerWs {
     DevBuf<Mt64State> mt;           // [0] device-resident RNG stream, [1+b] input state of the draw into buffer b
     DevBuf<uint64_t> raw;           // untempered words of the current draw
     DevBuf<int> mtflag;             // a draw may have been rejected (k_mt_fix redoes it)
+    DevBuf<const void*> xslot;      // dataset base read by the prep graphs' gather
     HostBuf<Mt64State> h_mt;
     HostBuf<uint32_t> h_js[2];
     cudaEvent_t js_done[2] = {nullptr, nullptr};
@@ -327,6 +328,7 @@ struct SamplerWs {
         mt.alloc(3);
         raw.alloc(s);
         mtflag.alloc(1);
+        xslot.alloc(1);
         h_mt.alloc(1);
         for (int b = 0; b < 2; ++b) {
             h_js[b].alloc(s);
@@ -356,13 +358,19 @@ struct SamplerWs {
 // shareable: all per-run state lives in the calling thread's DeviceCache.
 struct bm_dataset {
     int device = 0;
-    uint64_t uid = 0;  // distinguishes handles whose addresses get reused (graph keys)
     uint64_t m = 0, n = 0, ld = 0;
     bm_dtype dtype = BM_F64;
     void* X = nullptr;
     cudaStream_t stream = nullptr;  // upload / download only
-    ~bm_dataset() {
-        if (X) cudaFree(X);
+    ~bm_dataset() {  // X comes from the stream-ordered pool
+        if (X) {
+            if (stream) {
+                cudaFreeAsync(X, stream);
+                cudaStreamSynchronize(stream);
+            } else {
+                cudaFree(X);
+            }
+        }
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -1181,11 +1189,13 @@ void enqueue_resolve(cudaStream_t st, SamplerWs& sw) {
     enqueue_resolve_device(st, sw, 0);
 }
 
-void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, uint32_t s, void* out) {
+void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, uint32_t s, void* out,
+                    const void* const* xslot = nullptr) {
     PhaseScope ps(PH_GATHER, s);
     const uint64_t row_vecs = d->ld * dtype_size(d->dtype) / 16;
     const unsigned grid = (unsigned)ceil_div((uint64_t)s * 32, 256);
-    dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X), row_vecs, idx, s,
+    dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X),
+                                        reinterpret_cast<const uint4* const*>(xslot), row_vecs, idx, s,
                                         static_cast<uint4*>(out));
     BM_LAUNCH();
     count_launch();
@@ -1280,7 +1290,7 @@ cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, SamplerWs& sw
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     enqueue_resolve_device(st, sw, b);
     BM_CUDA(cudaEventRecordWithFlags(sw.resolved[b], st, cudaEventRecordExternal));
-    enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, chunk);
+    enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, chunk, sw.xslot.p);
     BM_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t e = nullptr;
     BM_CUDA(cudaGraphInstantiate(&e, g, 0));
@@ -1423,8 +1433,9 @@ cudaGraphExec_t capture_spec(cudaStream_t st, Workspace& w, const Points& P, int
 void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw, Workspace& w,
                    const Points& P, uint64_t max_it, double tol) {
     char sig[512];
-    std::snprintf(sig, sizeof(sig), "%llu/%p/%p/%p/%p/%p/%p/%p/%llu/%a/%llu",
-                  (unsigned long long)d->uid, (const void*)d->X, (void*)dc.chunk.p, (void*)dc.chunk1.p,
+    // the dataset enters only through shape: its base is read from sw.xslot
+    std::snprintf(sig, sizeof(sig), "%llu/%llu/%d/%p/%p/%p/%p/%p/%p/%llu/%a/%llu",
+                  (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
                   (void*)dc.chunk2.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n);
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
@@ -1481,7 +1492,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, 2, w.gs.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
                                        w.chunk_ctr.p);
     BM_LAUNCH();
-    if (!identity) put_stream(st, *sw, rng);
+    if (!identity) {
+        put_stream(st, *sw, rng);
+        BM_CUDA(cudaMemcpyAsync(sw->xslot.p, &d->X, sizeof(void*), cudaMemcpyHostToDevice, st));
+    }
     const bool use_graphs = !identity && !g_profiling && graphs_enabled();
     if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
     uint64_t evals = 0, iterations = 0;
@@ -1726,7 +1740,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 get_stream(st, *sw, rng);
             }
             kmeanspp_fill_device(st, chunkP, w, hmask, cfg.candidates_per_step, rng, evals);
-            if (!identity) put_stream(st, *sw, rng);
+            if (!identity) {
+        put_stream(st, *sw, rng);
+        BM_CUDA(cudaMemcpyAsync(sw->xslot.p, &d->X, sizeof(void*), cudaMemcpyHostToDevice, st));
+    }
         }
         // The next chunk's sample draws follow this chunk's (repair) draws:
         // start them now on rng_stream, overlapping this chunk's Lloyd.  Its
@@ -1857,8 +1874,6 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
         if (m >= 0xFFFFFFFFull) throw ConfigError("dataset too large for 32-bit row indices");
         DeviceGuard g(device);
         auto d = std::make_unique<bm_dataset>();
-        static std::atomic<uint64_t> next_uid{1};
-        d->uid = next_uid++;
         d->device = device;
         d->m = m;
         d->n = n;
@@ -1867,31 +1882,47 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
         DevBuf<int> flags(2);  // [0] non-finite, [1] not exactly representable in fp32
         BM_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), d->stream));
         int hf[2] = {0, 0};
+        // datasets come and go (one per e2e step): stream-ordered allocations from a
+        // pool that keeps its memory, instead of a fresh cudaMalloc each time
+        {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            cudaGetLastError();
+        }
         if (dtype == BM_F64 && narrow_storage()) {
             // Stage the fp64 values, check them (Dataset ctor scan core.cpp:27-31 +
             // fp32 round trip), keep fp32 storage when lossless.
-            DevBuf<double> tmp(m * n);
-            BM_CUDA(cudaMemcpyAsync(tmp.p, values, m * n * sizeof(double), cudaMemcpyHostToDevice, d->stream));
-            dev::k_check_narrow<<<1184, 256, 0, d->stream>>>(tmp.p, m * n, flags.p, flags.p + 1);
+            double* tmp = nullptr;
+            BM_CUDA(cudaMallocAsync(&tmp, m * n * sizeof(double), d->stream));
+            struct Tmp {
+                double* p;
+                cudaStream_t s;
+                ~Tmp() { cudaFreeAsync(p, s); }
+            } tmp_guard{tmp, d->stream};
+            BM_CUDA(cudaMemcpyAsync(tmp, values, m * n * sizeof(double), cudaMemcpyHostToDevice, d->stream));
+            dev::k_check_narrow<<<1184, 256, 0, d->stream>>>(tmp, m * n, flags.p, flags.p + 1);
             BM_LAUNCH();
             BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, d->stream));
             BM_CUDA(cudaStreamSynchronize(d->stream));
             if (hf[0]) throw ConfigError("dataset contains a non-finite value");
             d->dtype = hf[1] ? BM_F64 : BM_F32;
             d->ld = padded_ld(n, d->dtype);
-            BM_CUDA(cudaMalloc(&d->X, m * d->ld * dtype_size(d->dtype)));
+            BM_CUDA(cudaMallocAsync(&d->X, m * d->ld * dtype_size(d->dtype), d->stream));
             if (d->dtype == BM_F32) {
-                dev::k_narrow<<<1184, 256, 0, d->stream>>>(tmp.p, m, (int)n, static_cast<float*>(d->X), d->ld);
+                dev::k_narrow<<<1184, 256, 0, d->stream>>>(tmp, m, (int)n, static_cast<float*>(d->X), d->ld);
                 BM_LAUNCH();
             } else {
-                BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * sizeof(double), tmp.p, n * sizeof(double), n * sizeof(double),
+                BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * sizeof(double), tmp, n * sizeof(double), n * sizeof(double),
                                           m, cudaMemcpyDeviceToDevice, d->stream));
             }
             BM_CUDA(cudaStreamSynchronize(d->stream));
         } else {
             d->ld = padded_ld(n, dtype);
             const size_t es = dtype_size(dtype);
-            BM_CUDA(cudaMalloc(&d->X, m * d->ld * es));
+            BM_CUDA(cudaMallocAsync(&d->X, m * d->ld * es, d->stream));
             if (d->ld == n) {
                 BM_CUDA(cudaMemcpyAsync(d->X, values, m * n * es, cudaMemcpyHostToDevice, d->stream));
             } else {
@@ -1946,7 +1977,7 @@ bm_status bm_dataset_gather(const bm_dataset* d, const uint64_t* rows, uint64_t 
         o->dtype = d->dtype;
         o->ld = d->ld;
         BM_CUDA(cudaStreamCreateWithFlags(&o->stream, cudaStreamNonBlocking));
-        BM_CUDA(cudaMalloc(&o->X, count * o->ld * dtype_size(o->dtype)));
+        BM_CUDA(cudaMallocAsync(&o->X, count * o->ld * dtype_size(o->dtype), o->stream));
         DevBuf<uint64_t> idx(count);
         BM_CUDA(cudaMemcpyAsync(idx.p, rows, count * sizeof(uint64_t), cudaMemcpyHostToDevice, o->stream));
         dispatch(d->dtype, [&](auto tag) {

@@ -441,11 +441,14 @@ __global__ void k_mt_fix(Mt64State* __restrict__ st, const Mt64State* __restrict
 // 2. Row gather (Dataset::gather core.cpp:34-44): one warp per output row,
 //    16-byte vectors (rows are padded to 16-byte multiples).
 // ===========================================================================
-__global__ void k_gather(const uint4* __restrict__ X, uint64_t row_vecs, const uint32_t* __restrict__ idx,
-                         uint32_t s, uint4* __restrict__ out) {
+//    Xslot (when set) holds the dataset base: graphs captured once serve every
+//    dataset of the same shape.
+__global__ void k_gather(const uint4* __restrict__ X, const uint4* const* Xslot, uint64_t row_vecs,
+                         const uint32_t* __restrict__ idx, uint32_t s, uint4* __restrict__ out) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= s) return;
+    if (Xslot) X = *Xslot;
     const uint4* src = X + static_cast<uint64_t>(idx[warp]) * row_vecs;
     uint4* dst = out + static_cast<uint64_t>(warp) * row_vecs;
     for (uint64_t v = lane; v < row_vecs; v += 32) dst[v] = __ldg(src + v);

@@ -165,3 +165,22 @@ def test_mid_run_repairs_vs_oracle(port, case):
     assert out.objective == p.objective
     assert (bits(out.centroids.values) == bits(p.centroids)).all()
     assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+def test_graphs_shared_across_datasets(port):
+    """The chunk graphs are captured once per shape and read the dataset base
+    from a device slot: alternating datasets of one shape (the second freed
+    before the third is created, so its address can be reused) must each
+    match the oracle."""
+    rng = np.random.default_rng(91)
+    xs = [np.rint(rng.normal(size=(6000, 12)) * (3 + i)) for i in range(3)]
+    k, s, chunks = 6, 700, 6
+    for i in (0, 1, 0, 2):
+        d = bm.Dataset(xs[i])
+        out, trace = bm.big_means(d, cfg(k, s, chunks, seed=11))
+        d.close()
+        p = port.big_means(xs[i], k, s, chunks, seed=11)
+        assert [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+                 r.degenerate_repaired) for r in trace.records] == p.trace
+        assert (bits(out.centroids.values) == bits(p.centroids)).all()
+        assert (out.assignment == p.labels).all()
