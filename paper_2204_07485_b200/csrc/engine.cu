@@ -417,7 +417,13 @@ DeviceCache& cache_of(int device) {
     if (it != t_cache.end()) return *it->second;
     auto c = std::make_unique<DeviceCache>();
     c->device = device;
-    BM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // The engine stream (the chunk chain's critical path) gets a priority above
+    // the speculative begins and chunk preps (default priority), the draw
+    // stream stays highest.  BM_PRIO=0: default priority (A/B diagnostics).
+    static const bool prio = !(std::getenv("BM_PRIO") && std::string(std::getenv("BM_PRIO")) == "0");
+    int lo = 0, hi = 0;
+    BM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    BM_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio && hi < lo ? hi + 1 : lo));
     auto& ref = *c;
     t_cache.emplace(device, std::move(c));
     return ref;
@@ -1688,6 +1694,13 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                          "before the next %.1f us | prep graph %.1f us (%d) | speculative begin %.1f us (%d)\n",
                          total, cnt[1], 1e3 * total / cnt[1], 1e3 * dur[1] / cnt[1], ngap ? 1e3 * gap / ngap : 0.0,
                          cnt[0] ? 1e3 * dur[0] / cnt[0] : 0.0, cnt[0], cnt[2] ? 1e3 * dur[2] / cnt[2] : 0.0, cnt[2]);
+            if (std::string(std::getenv("BM_TIMELINE")) == "2")  // raw: kind, start, end (us from the first Lloyd graph)
+                for (auto& r : tl) {
+                    float a = 0, b2 = 0;
+                    BM_CUDA(cudaEventElapsedTime(&a, first, r.a));
+                    BM_CUDA(cudaEventElapsedTime(&b2, first, r.b));
+                    std::fprintf(stderr, "[tl] %d %.2f %.2f\n", r.kind, 1e3 * a, 1e3 * b2);
+                }
             for (auto& r : tl) {
                 cudaEventDestroy(r.a);
                 cudaEventDestroy(r.b);

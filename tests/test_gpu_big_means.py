@@ -184,3 +184,27 @@ def test_graphs_shared_across_datasets(port):
                  r.degenerate_repaired) for r in trace.records] == p.trace
         assert (bits(out.centroids.values) == bits(p.centroids)).all()
         assert (out.assignment == p.labels).all()
+
+
+@pytest.mark.parametrize("case", ["f32_storage", "f64_storage", "ragged"])
+def test_long_runs_vs_oracle(port, case):
+    """Long runs where the incumbent settles early (most chunks rejected, the
+    speculative begins of the pipeline current), fp32 and fp64 storage and
+    ragged tiles, bitwise against the oracle."""
+    rng = np.random.default_rng(31)
+    m, n, k, s, chunks = {"f32_storage": (30000, 9, 7, 1500, 30),
+                          "f64_storage": (20000, 6, 5, 1000, 30),
+                          "ragged": (12345, 13, 11, 777, 25)}[case]
+    centers = rng.uniform(0, 40, (k, n))
+    X = centers[rng.integers(0, k, m)] + rng.normal(size=(m, n))
+    if case != "f64_storage":
+        X = np.rint(X * 4)  # exactly representable in fp32: fp32 storage
+    out, trace = bm.big_means(bm.Dataset(X), cfg(k, s, chunks, seed=2))
+    p = port.big_means(X, k, s, chunks, seed=2)
+    got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+            r.degenerate_repaired) for r in trace.records]
+    assert got == p.trace
+    assert out.objective == p.objective
+    assert (bits(out.centroids.values) == bits(p.centroids)).all()
+    assert (out.assignment == p.labels).all()
+    assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
