@@ -132,7 +132,6 @@ struct Workspace {
     DevBuf<int32_t> labels;  // 2 * R (ping-pong)
     DevBuf<double> dists;    // 4 * R
     DevBuf<double> fix_tiles;  // tiles: tile partials of a chunk's exact objective (deferred records)
-    DevBuf<dev::AcceptArgs> accd;  // device copy of the accept arguments (controls that accept)
     DevBuf<double> tile_buf; // max(ncand,1) * tiles
     DevBuf<unsigned> tile_ctr;  // tiles (fused tile-fold arrival counters)
     DevBuf<unsigned> tiles_done;  // tiles completed in the current assignment launch (fused control)
@@ -848,13 +847,18 @@ float* gr_lbk(Workspace& w, const GraphRound* g) {
     return w.lbk.p + (g ? (uint64_t)g->buf * w.R * dev::kSMaxK : 0);
 }
 
+dev::AcceptArgs accept_args(Workspace& w);
+
 void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
     if (!g) return;
     c.dists_pair = gr_dists(w, g);
     c.st = gr_status(w, g);
     c.go = g->go;
     c.begin_kind = g->begin_kind;
-    if (g->accept || g->fix) c.acc = w.accd.p;
+    if (g->accept || g->fix) {
+        c.acc = accept_args(w);
+        c.has_acc = 1;
+    }
     c.accept_run = g->accept ? 1 : 0;
     c.host_st = g->host_st;
     c.incomplete_after = g->incomplete_after;
@@ -1447,9 +1451,6 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
-    if (!w.accd.n) w.accd.alloc(1);
-    const dev::AcceptArgs A = accept_args(w);
-    BM_CUDA(cudaMemcpy(w.accd.p, &A, sizeof(A), cudaMemcpyHostToDevice));
     void* bufs[3] = {dc.chunk.p, dc.chunk1.p, dc.chunk2.p};
     const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
     for (int i = 0; i < 6; ++i) {  // data buffer i % 3, state / draw buffer i % 2

@@ -59,6 +59,8 @@ struct GState {
     int go;              // the next chunk starts from the incumbent as is (no repair, :83-85)
     int pending_fix;     // chunk whose record awaits its exact objective (-1: none)
     int fix_par;         // distance slot of that chunk's final assignment
+    int fix_acc;         // that chunk's accept decision
+    int pad;
 };
 static_assert(sizeof(LloydStatus) % 8 == 0, "status is copied as 8-byte words");
 
@@ -544,45 +546,6 @@ __global__ void k_lloyd_step(LloydStatus* st, const double* tiles, uint64_t ntil
         lloyd_step_body(st, tiles, ntiles, rows, max_iterations, rel_tolerance, history, cond, use_cond, n_active);
 }
 
-// Control fused into an assignment launch: mode 1 = begin, 2 = step.
-struct LloydCtl {
-    int mode;
-    LloydStatus* st;
-    GState* gs;
-    unsigned* tiles_done;   // arrival counter over the launch's tiles
-    uint64_t ntiles;
-    unsigned long long max_iterations;
-    double rel_tolerance;
-    double* history;
-    cudaGraphConditionalHandle cond;
-    int use_cond;
-    int fast;               // fast-sum control (no history; objective computed by k_accept)
-    int force_exact;        // test hook: every fast-sum decision takes the exact path
-    const double* dists_pair;  // distances of the last two assignments (slot = labels slot)
-    uint64_t dstride;
-    const int* go;          // when set and *go == 0 the launch does nothing (skipped chunk)
-    int begin_kind;         // begin launches: 0 plain, 1 speculative (incumbent copy), 2 redo unless current
-    int begin_slot;         // begin launches: the slot the assignment writes (parity after the begin)
-    const struct AcceptArgs* acc;  // accept state (device copy)
-    int accept_run;         // the control runs the accept (:89-94) when the loop stops
-    LloydStatus* host_st;   // with acc: the status is also written to mapped host memory
-    unsigned long long incomplete_after;  // > 0: no stop after this many rounds -> st->incomplete
-    // begin launches with fixup CTAs: exact objective of the pending chunk
-    const double* dists_all;  // [2 chunk buffers][2 slots][fix_rows]
-    uint64_t fix_rows;
-    double* fix_tiles;
-};
-
-// The status straight into mapped pinned host memory (no copy node); CTA-wide.
-// The host reads it after synchronizing with the kernel's completion, which
-// orders the writes (no system fence needed here).
-__device__ __forceinline__ void status_to_host(const LloydStatus* st, LloydStatus* host_st) {
-    constexpr int kW = sizeof(LloydStatus) / 8;
-    for (int i = threadIdx.x; i < kW; i += blockDim.x)
-        reinterpret_cast<volatile unsigned long long*>(host_st)[i] =
-            reinterpret_cast<const volatile unsigned long long*>(st)[i];
-}
-
 // Accept step state (big_means.cpp:63-64, 89-94).
 struct AcceptArgs {
     double* f_opt;
@@ -603,11 +566,50 @@ struct AcceptArgs {
     GState* gs;
 };
 
-// The accept of the chunk's candidate (all threads of one CTA; sm: 2k ints).
-// deferred: the record's objectives are filled later by fix_record (the
-// exact candidate objective is folded during the next chunk).
-__device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, int accepted, bool deferred,
-                                         LloydStatus* host_st, int* sm) {
+// Control fused into an assignment launch: mode 1 = begin, 2 = step.
+struct LloydCtl {
+    int mode;
+    LloydStatus* st;
+    GState* gs;
+    unsigned* tiles_done;   // arrival counter over the launch's tiles
+    uint64_t ntiles;
+    unsigned long long max_iterations;
+    double rel_tolerance;
+    double* history;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+    int fast;               // fast-sum control (no history; objective computed by k_accept)
+    int force_exact;        // test hook: every fast-sum decision takes the exact path
+    const double* dists_pair;  // distances of the last two assignments (slot = labels slot)
+    uint64_t dstride;
+    const int* go;          // when set and *go == 0 the launch does nothing (skipped chunk)
+    int begin_kind;         // begin launches: 0 plain, 1 speculative (incumbent copy), 2 redo unless current
+    int begin_slot;         // begin launches: the slot the assignment writes (parity after the begin)
+    AcceptArgs acc;         // accept state (valid when has_acc)
+    int has_acc;
+    int accept_run;         // the control runs the accept (:89-94) when the loop stops
+    LloydStatus* host_st;   // with acc: the status is also written to mapped host memory
+    unsigned long long incomplete_after;  // > 0: no stop after this many rounds -> st->incomplete
+    // begin launches with fixup CTAs: exact objective of the pending chunk
+    const double* dists_all;  // [2 chunk buffers][2 slots][fix_rows]
+    uint64_t fix_rows;
+    double* fix_tiles;
+};
+
+// The status straight into mapped pinned host memory (no copy node); CTA-wide.
+// The host reads it after synchronizing with the kernel's completion, which
+// orders the writes (no system fence needed here).
+__device__ __forceinline__ void status_to_host(const LloydStatus* st, LloydStatus* host_st) {
+    constexpr int kW = sizeof(LloydStatus) / 8;
+    for (int i = threadIdx.x; i < kW; i += blockDim.x)
+        reinterpret_cast<volatile unsigned long long*>(host_st)[i] =
+            reinterpret_cast<const volatile unsigned long long*>(st)[i];
+}
+
+// The accept of the chunk's candidate with its exact objective in
+// st->objective (k_accept: all threads of one CTA; sm: 2k ints).
+__device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, int accepted, LloydStatus* host_st,
+                                         int* sm) {
     const int k = A.k, n = A.n;
     __shared__ int acc_s;
     __shared__ unsigned long long chunk_s;
@@ -615,23 +617,15 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         const unsigned long long chunk = *A.chunk_ctr;
         chunk_s = chunk;
         Record* rec = A.rec_base + chunk;
-        if (deferred) {
-            rec->candidate_objective = __longlong_as_double(0x7FF8000000000000LL);
-            rec->incumbent_objective = __longlong_as_double(0x7FF8000000000000LL);
-            A.gs->pending_fix = static_cast<int>(chunk);
-            A.gs->fix_par = st->parity;
-        } else {
-            if (accepted) *A.f_opt = st->objective;
-            rec->candidate_objective = st->objective;
-            rec->incumbent_objective = *A.f_opt;
-        }
+        if (accepted) *A.f_opt = st->objective;
+        rec->candidate_objective = st->objective;
+        rec->incumbent_objective = *A.f_opt;
         rec->chunk_index = chunk;
         rec->accepted = accepted;
         rec->degenerate_repaired = static_cast<unsigned long long>(A.gs->inc_degenerate);
         acc_s = accepted;
     }
     __syncthreads();
-    ktrace(11, 2);
     accepted = acc_s;
     int* arank = sm;
     int* mk = sm + k;  // incumbent mask staged in shared memory (the rank loop below is serial)
@@ -678,7 +672,6 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
         *A.chunk_ctr = chunk_s + 1;
     }
     __syncthreads();
-    ktrace(12, 2);
     // the next chunk's start (:82): (C, mask) := incumbent, and its compacted form
     if (!accepted)
         for (int j = threadIdx.x; j < k; j += blockDim.x) A.mask[j] = static_cast<uint8_t>(mk[j]);
@@ -717,10 +710,142 @@ __device__ __noinline__ void accept_body(LloydStatus* st, const AcceptArgs& A, i
     }
 }
 
-// The pending chunk's record gets its exact objectives (thread 0; tiles: the
-// ordered tile partials of its final distances).
-__device__ __forceinline__ void fix_record(GState* gs, const AcceptArgs& A, const double* tiles, uint64_t ntiles) {
-    if (gs->pending_fix < 0) return;
+// What the accept of the fused control reads, fetched by the last CTA in one
+// round trip together with the status (shared memory; k <= kSMaxK).
+struct TailIn {
+    GState gs;                     // copy; fields this tail changes are written through to global
+    unsigned long long chunk;      // *A.chunk_ctr
+    unsigned char mk_inc[kSMaxK];  // incumbent mask
+    unsigned char mk_cand[kSMaxK]; // candidate mask
+    int arank[kSMaxK];             // label -> rank in the next start's compacted rows (-1: degenerate)
+    int act[kSMaxK];               // rank -> label
+    int na;                        // active labels of the next start
+};
+
+// The accept (:89-94) run by the fused control of the stopping round, with a
+// deferred exact objective: the record's objectives are filled by fix_commit
+// during the next chunk.  All threads of the CTA; inputs prefetched in T;
+// stage: k x n doubles of shared memory holding the incumbent's centroids
+// (cinc_staged), or room for them, or null.
+__device__ __noinline__ void accept_fast(LloydStatus* st, const AcceptArgs& A, int accepted, TailIn* T,
+                                         double* stage, bool cinc_staged) {
+    const int k = A.k, n = A.n;
+    const unsigned char* mk = accepted ? T->mk_cand : T->mk_inc;
+    // Thread-serial code issues its global stores last: a generic load
+    // behind an outstanding global store of the same thread waits for it.
+    if (threadIdx.x < 32) {  // warp 0: ranks of the next start's active labels (k <= 32)
+        const int lane = threadIdx.x;
+        const bool live = lane < k && !mk[lane];
+        const unsigned act = __ballot_sync(0xFFFFFFFFu, live);
+        const int r = __popc(act & ((1u << lane) - 1u));
+        if (lane < k) T->arank[lane] = live ? r : -1;
+        if (live) {
+            T->act[r] = lane;
+            A.act_idx[r] = lane;
+            if (accepted && A.actI) A.actI[r] = lane;
+        }
+        if (lane == 0) {
+            const int na = __popc(act), dcount = k - na;
+            T->na = na;
+            const unsigned long long chunk = T->chunk;
+            const unsigned long long repaired = static_cast<unsigned long long>(T->gs.inc_degenerate);
+            const int par = st->parity;
+            st->inc_degenerate = dcount;
+            st->incomplete = 0;
+            ktrace(11, 2);
+            Record* rec = A.rec_base + chunk;
+            rec->candidate_objective = __longlong_as_double(0x7FF8000000000000LL);
+            rec->incumbent_objective = __longlong_as_double(0x7FF8000000000000LL);
+            rec->chunk_index = chunk;
+            rec->accepted = accepted;
+            rec->degenerate_repaired = repaired;
+            A.gs->pending_fix = static_cast<int>(chunk);
+            A.gs->fix_par = par;
+            A.gs->fix_acc = accepted;
+            A.gs->inc_degenerate = dcount;
+            A.gs->go = dcount == 0;
+            A.gs->n_active = na;
+            if (accepted) A.gs->n_active_inc = na;
+            *A.chunk_ctr = chunk + 1;
+            ktrace(9, 2);
+        }
+    }
+    if (threadIdx.x < k) {  // accepted: incumbent mask := candidate's, else the next start's := incumbent's
+        if (accepted) A.maskinc[threadIdx.x] = T->mk_cand[threadIdx.x];
+        else A.mask[threadIdx.x] = T->mk_inc[threadIdx.x];
+    }
+    const int kn = k * n;
+    if (stage && accepted)  // the candidate becomes the incumbent
+        for (int e = threadIdx.x; e < kn; e += blockDim.x) stage[e] = __ldcg(A.C + e);
+    __syncthreads();
+    if (stage && (accepted || cinc_staged)) {
+        // accepted: Cinc := C; the next chunk's start (:82) := incumbent; its
+        // compacted forms row by row (Cact) and dimension by dimension (CT32,
+        // [d][rank]), all coalesced
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5, na = T->na;
+        for (int e = threadIdx.x; e < kn; e += blockDim.x) {
+            if (accepted) A.Cinc[e] = stage[e];
+            else A.C[e] = stage[e];
+        }
+        for (int rk = warp; rk < na; rk += nw) {
+            const double* src = stage + T->act[rk] * n;
+            for (int d = lane; d < n; d += 32) {
+                A.Cact[static_cast<uint64_t>(rk) * A.ldc + d] = src[d];
+                if (accepted && A.CactI) A.CactI[static_cast<uint64_t>(rk) * A.ldc + d] = src[d];
+            }
+        }
+        if (A.CT32 && lane < na) {
+            const double* src = stage + T->act[lane] * n;
+            for (int d = warp; d < n; d += nw) {
+                const float f = __double2float_rn(src[d]);
+                A.CT32[static_cast<uint64_t>(d) * kSMaxK + lane] = f;
+                if (accepted && A.CactI) A.CT32I[static_cast<uint64_t>(d) * kSMaxK + lane] = f;
+            }
+        }
+    } else
+    for (int e0 = threadIdx.x; e0 < kn; e0 += 8 * blockDim.x) {  // loads batched ahead of the stores
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = e0 + r * blockDim.x;
+            v[r] = e >= kn ? 0.0 : accepted ? A.C[e] : A.Cinc[e];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = e0 + r * blockDim.x;
+            if (e >= k * n) continue;
+            const int j = e / n, d = e - j * n, rk = T->arank[j];
+            if (accepted) A.Cinc[e] = v[r];
+            else A.C[e] = v[r];
+            if (rk < 0) continue;
+            A.Cact[static_cast<uint64_t>(rk) * A.ldc + d] = v[r];
+            if (A.CT32 && rk < kSMaxK) A.CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v[r]);
+            if (accepted && A.CactI) {  // the incumbent's compacted copy
+                A.CactI[static_cast<uint64_t>(rk) * A.ldc + d] = v[r];
+                if (rk < kSMaxK) A.CT32I[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v[r]);
+            }
+        }
+    }
+    if (accepted) {  // published after the copy: a begin that saw the old version is redone
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(reinterpret_cast<unsigned long long*>(&A.gs->inc_version), 1ull);
+        }
+    }
+}
+
+// The pending chunk's record gets its exact objective (thread 0; tiles: the
+// ordered tile partials of its final distances).  fix_compute works on the
+// state as read (gm: gs itself, or the tail's shared-memory copy, updated);
+// fix_commit then writes the record and the state (stores last, see accept_fast).
+struct FixOut {
+    int pend;
+    double fc, fo;
+};
+
+__device__ __forceinline__ bool fix_compute(GState* gm, const double* tiles, uint64_t ntiles, FixOut* o) {
+    if (gm->pending_fix < 0) return false;
     double fc = 0.0;  // block_sum (:53-54): ordered fold of the tile partials (shared or fresh global memory)
     uint64_t t = 0;
     for (; t + 8 <= ntiles; t += 8) {
@@ -731,11 +856,20 @@ __device__ __forceinline__ void fix_record(GState* gs, const AcceptArgs& A, cons
         for (int r = 0; r < 8; ++r) fc = __dadd_rn(fc, v[r]);
     }
     for (; t < ntiles; ++t) fc = __dadd_rn(fc, tiles[t]);
-    Record* rec = A.rec_base + gs->pending_fix;
-    rec->candidate_objective = fc;
-    if (rec->accepted) gs->fopt_exact = fc;  // :89-93
-    rec->incumbent_objective = gs->fopt_exact;
-    *A.f_opt = gs->fopt_exact;
+    o->pend = gm->pending_fix;
+    o->fc = fc;
+    o->fo = gm->fix_acc ? fc : gm->fopt_exact;  // :89-93
+    gm->fopt_exact = o->fo;
+    gm->pending_fix = -1;
+    return true;
+}
+
+__device__ __forceinline__ void fix_commit(GState* gs, const AcceptArgs& A, const FixOut& o) {
+    Record* rec = A.rec_base + o.pend;
+    rec->candidate_objective = o.fc;
+    rec->incumbent_objective = o.fo;
+    *A.f_opt = o.fo;
+    gs->fopt_exact = o.fo;
     gs->pending_fix = -1;
 }
 
@@ -764,9 +898,9 @@ __device__ __forceinline__ void sum_interval(double s, uint64_t rows, unsigned c
 
 // Fast-sum Lloyd control (thread 0 of the CTA that arrived last).  Returns the
 // accept decision (0/1) when the loop stopped and the control runs the accept,
-// else -1.
+// else -1.  gm: the chain state as read (c.gs, or the tail's prefetched copy).
 __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* st, uint64_t rows, unsigned ctas,
-                                               int n_active) {
+                                               int n_active, GState* gm, const double* fix_tiles) {
     const double s = st->fsum;
     st->fsum = 0.0;
     st->ctas_done = 0u;
@@ -777,7 +911,7 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
         st->f = s;
         st->f_lo = lo;
         st->f_hi = hi;
-        st->objective = nan;  // exact value: deferred (fix_record)
+        st->objective = nan;  // exact value: deferred (fix_compute / fix_commit)
         st->evals = static_cast<unsigned long long>(rows) * n_active;
         st->iterations = 0;
         st->parity = c.begin_slot;
@@ -795,7 +929,10 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
         return -1;
     }
     // the previous chunk's record: its exact objective, before this chunk's accept
-    if (c.acc && c.fix_tiles) fix_record(c.gs, *c.acc, c.fix_tiles, tiles_of(c.fix_rows));
+    ktrace(6, 2);
+    FixOut fx;
+    const bool fixed = c.has_acc && fix_tiles && fix_compute(gm, fix_tiles, tiles_of(c.fix_rows), &fx);
+    ktrace(7, 2);
     int decision = -1;
     if (!st->stop) {
         st->evals += static_cast<unsigned long long>(rows) * n_active;
@@ -840,7 +977,7 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
         if (st->state_error || st->bad_label) stop = true;
         st->stop = stop ? 1 : 0;
         if (stop && c.accept_run) {  // accept (:89): f < f_opt, strict, on the candidate's interval
-            const double fo = c.gs->fopt_exact;
+            const double fo = gm->fopt_exact;
             if (!c.force_exact && hi < fo) decision = 1;
             else if (!c.force_exact && !(lo < fo)) decision = 0;
             else decision = exact_block_sum(c.dists_pair + st->parity * c.dstride, rows) < fo;
@@ -849,6 +986,8 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
             c.gs->go = 0;
         }
     }
+    ktrace(8, 2);
+    if (fixed) fix_commit(c.gs, c.acc, fx);
     if (c.use_cond) cudaGraphSetConditional(c.cond, st->stop ? 0u : 1u);
     return decision;
 }
@@ -1609,7 +1748,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              const int* __restrict__ parity_ptr, double* __restrict__ dists_out,
              int* __restrict__ changed_flag, const int* __restrict__ stop_ptr,
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
-             unsigned long long* __restrict__ cand_counter, ScreenConsts cst, LloydCtl ctl,
+             unsigned long long* __restrict__ cand_counter, ScreenConsts cst, const __grid_constant__ LloydCtl ctl,
              int hmode, float* __restrict__ lbk, const float* __restrict__ delta, int kfull,
              uint64_t dstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2252,30 +2391,60 @@ fold:
         if (!S.is_last) return;
         __threadfence();
         ktrace(28, hmode);
-        // the status in shared memory while this CTA runs the control (and the accept)
+        // Everything the control and the accept read, in one round trip: the
+        // status, the chain state, the chunk counter, both masks, the fixup
+        // tile partials and the incumbent's centroids (the usual next start),
+        // staged in shared memory (the pass-1 buffers are free now).
         LloydStatus* sst = reinterpret_cast<LloydStatus*>(&S.red_u[0][0]);
         constexpr int kW = sizeof(LloydStatus) / 8;
         for (int i = tid; i < kW; i += kSThreads)
             reinterpret_cast<unsigned long long*>(sst)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(ctl.st) + i);
-        LloydCtl cl = ctl;  // the fixup tile partials staged in shared memory for the control's fold
-        if (ctl.fix_tiles) {
+        const bool tail_acc = ctl.has_acc && ctl.mode == 2;
+        TailIn* tin = reinterpret_cast<TailIn*>(reuse);
+        double* stage = nullptr;  // k x n doubles for the accept's copies
+        bool cinc_staged = false;
+        if (tail_acc) {
+            constexpr int kG = sizeof(GState) / 8;
+            if (tid < kG)
+                reinterpret_cast<unsigned long long*>(&tin->gs)[tid] =
+                    __ldcg(reinterpret_cast<const unsigned long long*>(ctl.gs) + tid);
+            if (tid == 32) tin->chunk = __ldcg(ctl.acc.chunk_ctr);
+            if (tid >= 64 && tid < 64 + kfull) {
+                tin->mk_inc[tid - 64] = ctl.acc.maskinc[tid - 64];
+                tin->mk_cand[tid - 64] = ctl.acc.mask[tid - 64];
+            }
+            const int kn = kfull * n;
+            if (ctl.accept_run && 16384 + static_cast<size_t>(kn) * 8 <= reuse_bytes) {
+                stage = reinterpret_cast<double*>(reuse + 16384);
+                for (int e = tid; e < kn; e += kSThreads) stage[e] = __ldcg(ctl.acc.Cinc + e);
+                cinc_staged = true;
+            }
+        }
+        const double* fix_tiles = ctl.fix_tiles;  // the fixup tile partials, staged for the control's fold
+        if (fix_tiles) {
             double* ft = reinterpret_cast<double*>(&S.raw[0][0]) + 1024;
             const int nt = static_cast<int>(tiles_of(ctl.fix_rows));
             if (nt <= 1024) {
                 for (int i = tid; i < nt; i += kSThreads) ft[i] = __ldcg(ctl.fix_tiles + i);
-                cl.fix_tiles = ft;
+                fix_tiles = ft;
             }
         }
         __syncthreads();
-        if (tid == 0) S.n_items = static_cast<uint32_t>(lloyd_fast_control(cl, sst, rows, gridDim.x, KA));
+        ktrace(1, hmode);
+        if (tid == 0)
+            S.n_items = static_cast<uint32_t>(
+                lloyd_fast_control(ctl, sst, rows, gridDim.x, KA, tail_acc ? &tin->gs : ctl.gs, fix_tiles));
+        ktrace(2, hmode);
         __syncthreads();
         ktrace(29, hmode);
         const int decision = static_cast<int>(S.n_items);
-        if (decision >= 0)
-            accept_body(sst, *ctl.acc, decision, true, nullptr, reinterpret_cast<int*>(&S.raw[0][0]));
+        if (decision >= 0) accept_fast(sst, ctl.acc, decision, tin, stage, cinc_staged);
+        ktrace(3, hmode);
         __syncthreads();
+        ktrace(4, hmode);
         for (int i = tid; i < kW; i += kSThreads)
             reinterpret_cast<unsigned long long*>(ctl.st)[i] = reinterpret_cast<const unsigned long long*>(sst)[i];
+        ktrace(5, hmode);
         if (ctl.host_st && (decision >= 0 || sst->incomplete)) status_to_host(sst, ctl.host_st);
         ktrace(30, hmode);
         if (tid == 0) klog_end(10 + hmode);
@@ -2687,7 +2856,7 @@ __global__ void k_accept(LloydStatus* st, AcceptArgs A, LloydStatus* host_st) {
     pdl_trigger();
     if (threadIdx.x == 0) accepted = st->objective < *A.f_opt;  // strict (:89)
     __syncthreads();
-    accept_body(st, A, accepted, false, host_st, asm_);
+    accept_body(st, A, accepted, host_st, asm_);
     if (threadIdx.x == 0) klog_end(3);
 }
 
@@ -2718,7 +2887,8 @@ __global__ void k_fix_final(GState* gs, AcceptArgs A, const double* __restrict__
         if (last) {
             __threadfence();
             *counter = 0u;
-            fix_record(gs, A, tiles, gridDim.x);
+            FixOut fx;
+            if (fix_compute(gs, tiles, gridDim.x, &fx)) fix_commit(gs, A, fx);
         }
     }
 }

@@ -68,7 +68,7 @@ print(f"round fast path: {ds[0]} CTAs, {ds[1]} fell back to the screen ({100 * d
       f"{ds[2] / max(ds[0], 1):.2f} rechecked pairs and {ds[3] / max(ds[0], 1):.2f} points with rechecks per CTA")
 
 # per-CTA phase marks of the last begin (region 400000) and round (region 470000) launches
-names_k = {0: "start", 1: "slab0", 2: "slab1", 3: "slab2", 4: "slab3", 5: "slab4", 6: "slab5", 7: "bounds",
+names_k = {14: "probe1", 0: "start", 1: "slab0", 2: "slab1", 3: "slab2", 4: "slab3", 5: "slab4", 6: "slab5", 7: "bounds",
            8: "items", 9: "recheck", 10: "out/fold", 13: "fp_setup", 15: "fp_done", 16: "c0wait", 17: "c0done",
            24: "c4wait", 25: "c4done", 26: "fp_items", 11: "acc:record", 12: "acc:ranks", 27: "lbk_written", 28: "last:arrived", 29: "last:control",
            30: "last:accept"}
