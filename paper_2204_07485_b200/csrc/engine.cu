@@ -1203,9 +1203,13 @@ void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, u
                     const void* const* xslot = nullptr) {
     PhaseScope ps(PH_GATHER, s);
     const uint64_t row_vecs = d->ld * dtype_size(d->dtype) / 16;
-    const unsigned grid = (unsigned)ceil_div((uint64_t)s * 32, 256);
+    static const unsigned cap = [] {  // 4 CTAs per SM (148 SMs); BM_GATHER_CTAS overrides (A/B)
+        const char* e = std::getenv("BM_GATHER_CTAS");
+        return e ? (unsigned)std::max(1, std::atoi(e)) : 592u;
+    }();
+    const unsigned grid = (unsigned)std::min<uint64_t>(cap, ceil_div((uint64_t)s * row_vecs, 4 * 256));
     dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X),
-                                        reinterpret_cast<const uint4* const*>(xslot), row_vecs, idx, s,
+                                        reinterpret_cast<const uint4* const*>(xslot), (uint32_t)row_vecs, idx, s,
                                         static_cast<uint4*>(out));
     BM_LAUNCH();
     count_launch();

@@ -445,15 +445,32 @@ __global__ void k_mt_fix(Mt64State* __restrict__ st, const Mt64State* __restrict
 // ===========================================================================
 //    Xslot (when set) holds the dataset base: graphs captured once serve every
 //    dataset of the same shape.
-__global__ void k_gather(const uint4* __restrict__ X, const uint4* const* Xslot, uint64_t row_vecs,
-                         const uint32_t* __restrict__ idx, uint32_t s, uint4* __restrict__ out) {
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= s) return;
+//    A grid of a few CTAs per SM strides over the chunk's 16-byte vectors
+//    (every lane busy, four loads in flight per thread) instead of one warp
+//    per row (17 of 32 lanes busy on c2) and thousands of short CTAs that
+//    compete with the concurrent Lloyd kernels for SM slots.
+__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ X, const uint4* const* Xslot,
+                                                uint32_t row_vecs, const uint32_t* __restrict__ idx, uint32_t s,
+                                                uint4* __restrict__ out) {
     if (Xslot) X = *Xslot;
-    const uint4* src = X + static_cast<uint64_t>(idx[warp]) * row_vecs;
-    uint4* dst = out + static_cast<uint64_t>(warp) * row_vecs;
-    for (uint64_t v = lane; v < row_vecs; v += 32) dst[v] = __ldg(src + v);
+    const uint64_t total = static_cast<uint64_t>(s) * row_vecs;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < total; v0 += 4 * stride) {
+        uint4 val[4];
+        uint64_t dst[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint64_t v = v0 + r * stride;
+            dst[r] = v;
+            if (v < total) {
+                const uint32_t row = static_cast<uint32_t>(v / row_vecs), col = static_cast<uint32_t>(v - static_cast<uint64_t>(row) * row_vecs);
+                val[r] = __ldg(X + static_cast<uint64_t>(__ldg(idx + row)) * row_vecs + col);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (dst[r] < total) out[dst[r]] = val[r];
+    }
 }
 
 // Ordered fold of tile partials (block_sum outer loop core.cpp:172).
