@@ -2818,9 +2818,16 @@ k_update(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
     if (!lastm) return;
     __threadfence();
     const int parts = G * static_cast<int>(gridDim.y);
+    // all parts staged in one round trip (not one per label), when they fit
+    double* dp = reinterpret_cast<double*>(ush_raw + o_m);
+    const bool staged = static_cast<size_t>(parts) * k * 8 <= u.shm_bytes - o_m;
+    if (staged) {
+        for (int i = threadIdx.x; i < parts * k; i += blockDim.x) dp[i] = __ldcg(u.drift_part + i);
+        __syncthreads();
+    }
     for (int j = warp; j < k; j += kUWarps) {  // a warp per label, lanes over the parts (any order)
         double sj = 0.0;
-        for (int q = lane; q < parts; q += 32) sj += __ldcg(&u.drift_part[q * k + j]);
+        for (int q = lane; q < parts; q += 32) sj += staged ? dp[q * k + j] : __ldcg(&u.drift_part[q * k + j]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) sj += __shfl_xor_sync(0xFFFFFFFFu, sj, o);
         if (lane == 0) u.delta[j] = __double2float_ru(__dsqrt_ru(sj * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
