@@ -105,6 +105,11 @@ bm_status bm_dataset_shape(const bm_dataset* data, uint64_t* m, uint64_t* n);
 /* Device storage type: fp64 input whose every value is exactly representable
  * in fp32 is stored as fp32 (lossless; results unchanged). */
 bm_status bm_dataset_storage(const bm_dataset* data, bm_dtype* storage);
+/* Exact-sum property (no reference counterpart; it changes no result): every
+ * value is an integer multiple of 2^exponent and m * max|x| < 2^52 * 2^exponent,
+ * so the ordered fp64 sums of update_centroids (core.cpp:206-229) are exact and
+ * the device keeps per-label integer sums instead of re-summing each round. */
+bm_status bm_dataset_sum_mode(const bm_dataset* data, int32_t* exact, int32_t* exponent);
 /* Dataset::gather core.hpp:30 / core.cpp:34-44: new dataset with the listed
  * rows in the listed order (index >= m -> BM_CONFIG_ERROR). */
 bm_status bm_dataset_gather(const bm_dataset* data, const uint64_t* rows, uint64_t count,

@@ -131,6 +131,14 @@ class Dataset:
         _check(self._lib.bm_dataset_storage(self._h, C.byref(v)))
         return "f64" if v.value == _capi.BM_F64 else "f32"
 
+    @property
+    def exact_sums(self):
+        """(exact, exponent): whether every value is a multiple of 2^exponent with
+        m * max|x| < 2^52 * 2^exponent, so update sums are exact in any order."""
+        a, e = C.c_int32(), C.c_int32()
+        _check(self._lib.bm_dataset_sum_mode(self._h, C.byref(a), C.byref(e)))
+        return bool(a.value), int(e.value)
+
     def gather(self, rows) -> "Dataset":
         """New dataset holding the listed rows in the listed order (core.cpp:34-44)."""
         idx = np.ascontiguousarray(rows, dtype=np.uint64)

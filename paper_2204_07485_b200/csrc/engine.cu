@@ -154,6 +154,18 @@ struct Workspace {
     DevBuf<double> drift_part;  // [n][k]: squared centroid movement of the last update, per d-slab
     int drift_slabs = 0;        // d-slabs of the last update launch (host view at enqueue/capture time)
     DevBuf<float> delta;        // [k]: movement per label of the last update (distance units, rounded up)
+    // exact-sum mode (graph chunks of exact-sum datasets): per chunk buffer two
+    // halves (speculative begin / redo begin) of [kSMaxK][n] integer sums + [kSMaxK] counts
+    DevBuf<long long> sums;
+    bool sums_on = false;
+    double sum_scale = 1.0, sum_unscale = 1.0;
+    bool sum_small = false;  // per-CTA sums of the value units below 2^31 (bm_dataset::sum_units_max < 2^23)
+    uint64_t sum_half() const { return (uint64_t)dev::kSumCopies * dev::kSMaxK * (n + 1); }
+    long long* sums_of(int buf) { return sums.p + (uint64_t)buf * 2 * sum_half(); }
+    DevBuf<long long> sum_parts;  // begins: per-CTA partials, per chunk buffer
+    DevBuf<unsigned> grp_ctr;     // begins: group arrival counters, per chunk buffer
+    uint64_t part_ctas() const { return (R + dev::kABP - 1) / dev::kABP; }
+    uint64_t part_len() const { return (uint64_t)dev::kSMaxK * n + dev::kSMaxK; }
     DevBuf<unsigned> all_done;  // fused update: mergers finished
     DevBuf<unsigned> slab_ctr, slab_done, slab_tot;  // [n], [n], [n][k]: fused update counters / label totals
     // K-means++ (init.cpp:123-201)
@@ -170,15 +182,15 @@ struct Workspace {
     DevBuf<unsigned long long> chunk_ctr;  // device-side chunk index
     // CUDA graphs of one chunk (sample resolution + gather, and the Lloyd loop)
     std::string graph_sig;
-    // graph mode: chunk c uses graphs [c % 6]: data buffer c % 3, state and draw buffer c % 2
-    cudaGraphExec_t g_prep[6] = {};
-    cudaGraphExec_t g_lloyd[6] = {};
-    cudaGraphExec_t g_cont[6] = {};   // continuation of an incomplete chunk
-    cudaGraphExec_t g_spec[6] = {};   // speculative begin (first assignment against the incumbent's copy)
-    cudaEvent_t ev_spec[6] = {};
+    // graph mode: chunk c uses graphs [c % 4]: data and state buffer c % 4, draw buffer c % 2
+    cudaGraphExec_t g_prep[dev::kStateBufs] = {};
+    cudaGraphExec_t g_lloyd[dev::kStateBufs] = {};
+    cudaGraphExec_t g_cont[dev::kStateBufs] = {};   // continuation of an incomplete chunk
+    cudaGraphExec_t g_spec[dev::kStateBufs] = {};   // speculative begin (first assignment against the incumbent's copy)
+    cudaEvent_t ev_spec[dev::kStateBufs] = {};
     cudaStream_t cap1 = nullptr, cap2 = nullptr;  // capture streams of the IF and WHILE bodies
-    cudaEvent_t ev_lloyd[6] = {};  // end of the Lloyd graph of the chunk in slot c % 6
-    cudaEvent_t ev_prep[6] = {};   // its chunk gathered
+    cudaEvent_t ev_lloyd[dev::kStateBufs] = {};  // end of the Lloyd graph of the chunk in slot c % 4
+    cudaEvent_t ev_prep[dev::kStateBufs] = {};   // its chunk gathered
     void drop_graphs() {
         for (auto* v : {&g_prep, &g_lloyd, &g_cont, &g_spec})
             for (auto& e : *v)
@@ -224,10 +236,10 @@ struct Workspace {
         ldc = n + (n & 1);
         tiles = tiles_of(rows);
         hist_cap = hist;
-        labels.alloc(6 * R);  // [chunk buffer][slot 0..2][R] (non-graph paths: buffer 0, slots 0/1)
-        dists.alloc(6 * R);  // [chunk buffer][slot 0..2][R], like the labels
+        labels.alloc(3 * dev::kStateBufs * R);  // [chunk buffer][slot 0..2][R] (non-graph paths: buffer 0, slots 0/1)
+        dists.alloc(3 * dev::kStateBufs * R);   // [chunk buffer][slot 0..2][R], like the labels
         fix_tiles.alloc(std::max<uint64_t>(tiles, 1));
-        lbk.alloc(2 * R * dev::kSMaxK);  // per chunk buffer
+        lbk.alloc(dev::kStateBufs * R * dev::kSMaxK);  // per chunk buffer
         tile_buf.alloc(tiles * ncand);
         tile_ctr.alloc(tiles);
         if (tiles) BM_CUDA(cudaMemset(tile_ctr.p, 0, tiles * sizeof(unsigned)));
@@ -260,8 +272,8 @@ struct Workspace {
         mask.alloc(k);
         act.alloc(k);
         actI.alloc(k);
-        status.alloc(2);  // per chunk buffer (non-graph paths: [0])
-        BM_CUDA(cudaMemset(status.p, 0, 2 * sizeof(dev::LloydStatus)));
+        status.alloc(dev::kStateBufs);  // per chunk buffer (non-graph paths: [0])
+        BM_CUDA(cudaMemset(status.p, 0, dev::kStateBufs * sizeof(dev::LloydStatus)));
         gs.alloc(1);
         BM_CUDA(cudaMemset(gs.p, 0, sizeof(dev::GState)));
         history.alloc(hist_cap);
@@ -271,7 +283,7 @@ struct Workspace {
         fopt.alloc(1);
         maskinc.alloc(k);
         chunk_ctr.alloc(1);
-        h_status.alloc(2);  // [1]: second chunk buffer of the pipelined loop
+        h_status.alloc(dev::kStateBufs);  // per chunk buffer of the pipelined loop
         h_tiles.alloc(tiles * ncand);
         h_d2.alloc(R);
         h_mask.alloc(k);
@@ -360,6 +372,11 @@ struct bm_dataset {
     uint64_t m = 0, n = 0, ld = 0;
     bm_dtype dtype = BM_F64;
     void* X = nullptr;
+    // exact-sum mode (kernels.cuh §5b): every value is a multiple of 2^sum_exp and
+    // m * max|x| < 2^53 * 2^sum_exp, so label sums are exact in any order
+    bool exact_sums = false;
+    int sum_exp = 0;
+    double sum_units_max = 0.0;  // max|x| / 2^sum_exp
     cudaStream_t stream = nullptr;  // upload / download only
     ~bm_dataset() {  // X comes from the stream-ordered pool
         if (X) {
@@ -384,7 +401,7 @@ struct DeviceCache {
     std::map<std::tuple<uint64_t, int, int, int, uint64_t>, std::unique_ptr<Workspace>> ws;
     std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SamplerWs>> sws;
     DevBuf<uint8_t> chunk;        // gathered chunk, s * ld * elem
-    DevBuf<uint8_t> chunk1, chunk2;  // graph mode: chunk c+2 is gathered while chunk c runs
+    DevBuf<uint8_t> chunk1, chunk2, chunk3;  // graph mode: chunks c+1..c+3 are gathered while chunk c runs
     cudaStream_t pstream = nullptr;  // graph mode: prep (resolution + gather) of the next chunk
     cudaStream_t sstream = nullptr;  // graph mode: speculative begin of the next chunk
     DevBuf<int32_t> flabels;      // final pass
@@ -624,6 +641,15 @@ bool narrow_storage() {
 }
 
 // BM_SCREEN=v4 selects the LDG-staged screen (A/B checks); default: TMA (v5).
+// BM_SUMS=0 disables the exact-sum update (kernels.cuh §5b) for A/B checks.
+bool exact_sums_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_SUMS");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
 bool tma_screen() {
     static const bool on = [] {
         const char* e = std::getenv("BM_SCREEN");
@@ -787,6 +813,18 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
     w.drift_slabs = slabs * G;
 }
 
+// update_centroids in exact-sum mode (kernels.cuh §5b): the label sums the
+// assignments keep give the centroids directly (one CTA).
+void launch_centroids(cudaStream_t st, Workspace& w, int buf, dev::LloydStatus* sts, const int* go) {
+    PhaseScope ps(PH_UPDATE, 0);
+    launch_pdl(dev::k_centroids, 1, 1024, 0, st, (const dev::LloydStatus*)sts, (const int*)&sts->stop, go,
+               (const long long*)w.sums_of(buf), w.sum_half(), w.sum_unscale, w.k, w.n, w.C.p, w.mask.p, w.Cact.p,
+               w.ldc, w.act.p, &w.gs.p->n_active, w.CT32.p, w.delta.p);
+    BM_LAUNCH();
+    count_launch(1);
+    w.drift_slabs = 1;
+}
+
 // ---------------------------------------------------------------------------
 // lloyd (local_search.cpp:16-60) with the loop state on the device.
 // Start centroids in w.C / w.mask.  Kernels of a finished loop early-exit, so
@@ -860,6 +898,18 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
         c.has_acc = 1;
     }
     c.accept_run = g->accept ? 1 : 0;
+    if (w.sums_on) {  // exact-sum mode: the begins fill a half, the rounds move points in the live one
+        c.sums = w.sums_of(g->buf);
+        c.sum_half = w.sum_half();
+        c.sum_scale = w.sum_scale;
+        c.sum_which = g->begin_kind == 1 ? 0 : g->begin_kind == 2 ? 1 : -1;
+        if (g->begin_kind != 0) {
+            c.parts = w.sum_parts.p + (uint64_t)g->buf * w.part_ctas() * w.part_len();
+            c.grp_ctr = w.grp_ctr.p + (uint64_t)g->buf * ceil_div(w.part_ctas(), 8);
+            c.pts_rows = w.R;
+        }
+        c.sum_small = w.sum_small ? 1 : 0;
+    }
     c.host_st = g->host_st;
     c.incomplete_after = g->incomplete_after;
     if (g->fix) {
@@ -892,7 +942,8 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
     dev::LloydStatus* sts = gr_status(w, g);
     const int* parity = &sts->parity;
     const int* stop = &sts->stop;
-    launch_update(st, P, w, parity, stop, g ? g->go : nullptr, gr_labels(w, g), &sts->bad_label);
+    if (g && w.sums_on) launch_centroids(st, w, g->buf, sts, g->go);
+    else launch_update(st, P, w, parity, stop, g ? g->go : nullptr, gr_labels(w, g), &sts->bad_label);
     dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond, fast);
     apply_graph(ctl, w, g);
     AssignSrc src{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, gr_lbk(w, g)};
@@ -1432,6 +1483,9 @@ cudaGraphExec_t capture_cont(cudaStream_t st, Workspace& w, const Points& P, uin
 cudaGraphExec_t capture_spec(cudaStream_t st, Workspace& w, const Points& P, int b) {
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     BM_CUDA(cudaMemsetAsync(&w.status.p[b].bv_min, 0xFF, sizeof(long long), st));
+    // exact-sum mode: both halves of this buffer's sums start at zero (the redo
+    // begin of this chunk, if any, runs after this graph)
+    if (w.sums_on) BM_CUDA(cudaMemsetAsync(w.sums_of(b), 0, 2 * w.sum_half() * sizeof(long long), st));
     GraphRound g;
     g.buf = b;
     g.begin_kind = 1;
@@ -1448,20 +1502,21 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
                    const Points& P, uint64_t max_it, double tol) {
     char sig[512];
     // the dataset enters only through shape: its base is read from sw.xslot
-    std::snprintf(sig, sizeof(sig), "%llu/%llu/%d/%p/%p/%p/%p/%p/%p/%llu/%a/%llu",
+    std::snprintf(sig, sizeof(sig), "%llu/%llu/%d/%p/%p/%p/%p/%p/%p/%llu/%a/%llu/%d/%a/%p",
                   (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
-                  (void*)dc.chunk2.p, (void*)&sw,
-                  (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n);
+                  (void*)dc.chunk3.p, (void*)&sw,
+                  (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n,
+                  (int)w.sums_on + 2 * (int)w.sum_small, w.sum_scale, (void*)w.sums.p);
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
-    void* bufs[3] = {dc.chunk.p, dc.chunk1.p, dc.chunk2.p};
+    void* bufs[dev::kStateBufs] = {dc.chunk.p, dc.chunk1.p, dc.chunk2.p, dc.chunk3.p};
     const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
-    for (int i = 0; i < 6; ++i) {  // data buffer i % 3, state / draw buffer i % 2
-        const int b = i % 2;
+    for (int i = 0; i < dev::kStateBufs; ++i) {  // data and state buffer i, draw buffer i % 2
+        const int b = i;
         Points Pb = P;
-        Pb.X = bufs[i % 3];
-        w.g_prep[i] = capture_prep(st, d, sw, b, bufs[i % 3]);
+        Pb.X = bufs[i];
+        w.g_prep[i] = capture_prep(st, d, sw, i % 2, bufs[i]);
         w.g_lloyd[i] = capture_lloyd(st, w, Pb, max_it, tol, b);
         if (fast) {
             w.g_cont[i] = capture_cont(st, w, Pb, max_it, tol, b);
@@ -1496,11 +1551,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         chunkP.X = dc.chunk.p;
         if (!g_profiling && graphs_enabled() && dc.chunk1.n < bytes) dc.chunk1.alloc(bytes);
         if (!g_profiling && graphs_enabled() && dc.chunk2.n < bytes) dc.chunk2.alloc(bytes);
+        if (!g_profiling && graphs_enabled() && dc.chunk3.n < bytes) dc.chunk3.alloc(bytes);
     }
     const uint64_t want_rec = cfg.has_max_chunks ? cfg.max_chunks : 1024;
     if (w.drec.n < want_rec) w.drec.alloc(want_rec);
     // incumbent all degenerate, f_opt = +inf (:63-64), chunk counter 0
-    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, 2, w.gs.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
+    dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, dev::kStateBufs, w.gs.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
                                        w.chunk_ctr.p);
     BM_LAUNCH();
     if (!identity) {
@@ -1508,6 +1564,21 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         BM_CUDA(cudaMemcpyAsync(sw->xslot.p, &d->X, sizeof(void*), cudaMemcpyHostToDevice, st));
     }
     const bool use_graphs = !identity && !g_profiling && graphs_enabled();
+    // exact-sum mode for the graph chunks (kernels.cuh §5b)
+    w.sums_on = use_graphs && d->exact_sums && exact_sums_enabled() && screen_enabled(k) && tma_screen() &&
+                s < (1ull << 31) && !w.hist_cap;
+    if (w.sums_on) {
+        w.sum_scale = std::ldexp(1.0, -d->sum_exp);
+        w.sum_unscale = std::ldexp(1.0, d->sum_exp);
+        w.sum_small = d->sum_units_max < 0x1p23;  // 128 points per CTA: partial sums below 2^30
+        const uint64_t nb = dev::kStateBufs;
+        if (w.sums.n < 2 * nb * w.sum_half()) w.sums.alloc(2 * nb * w.sum_half());
+        if (w.sum_parts.n < nb * w.part_ctas() * w.part_len()) w.sum_parts.alloc(nb * w.part_ctas() * w.part_len());
+        if (w.grp_ctr.n < nb * ceil_div(w.part_ctas(), 8)) {
+            w.grp_ctr.alloc(nb * ceil_div(w.part_ctas(), 8));
+            BM_CUDA(cudaMemsetAsync(w.grp_ctr.p, 0, w.grp_ctr.n * sizeof(unsigned), st));
+        }
+    }
     if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
     uint64_t evals = 0, iterations = 0;
     int inc_degenerate = k;
@@ -1515,18 +1586,19 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
 
     const auto t_loop = std::chrono::steady_clock::now();
     if (use_graphs) {
-        // Graph mode.  Chunk c uses graph slot c % 6: data buffer c % 3, state
-        // and draw buffer c % 2.  While chunk c's Lloyd graph runs, chunk c+1's
-        // speculative begin (its first assignment against the incumbent's
-        // copy) runs on sstream and chunk c+2's draws and prep (resolution +
-        // gather) on rng_stream / pstream; chunk c+1's Lloyd graph is queued
+        // Graph mode.  Chunk c uses graph slot c % 4: data and state buffer
+        // c % 4, draw buffer c % 2.  While chunk c's Lloyd graph runs, chunk
+        // c+3's draws, prep (resolution + gather) and speculative begin (its
+        // first assignment against the incumbent's copy) run on rng_stream /
+        // pstream / sstream (those of chunks c+1, c+2 were enqueued during
+        // chunks c-2, c-1); chunk c+1's Lloyd graph is queued
         // behind chunk c's before the host waits.  It runs only if chunk c's
         // accept leaves no degenerate incumbent rows (go) and redoes its begin
         // if an accept published a new incumbent meanwhile (inc_version).  The
         // RNG order (big_means.hpp:21-23) is kept: draws made ahead of a repair
         // are discarded and redone after it.
         if (!dc.pstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.pstream, cudaStreamNonBlocking));
-        for (int i = 0; i < 6; ++i) {
+        for (int i = 0; i < dev::kStateBufs; ++i) {
             if (!w.ev_lloyd[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd[i], cudaEventDisableTiming));
             if (!w.ev_prep[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_prep[i], cudaEventDisableTiming));
             if (!w.ev_spec[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_spec[i], cudaEventDisableTiming));
@@ -1536,9 +1608,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         // BM_PIPE=0: preps on the Lloyd stream (no overlap; timeline diagnostics)
         static const bool pipe = !(std::getenv("BM_PIPE") && std::string(std::getenv("BM_PIPE")) == "0");
         const cudaStream_t pst = pipe ? dc.pstream : st;
-        Points bufP[3] = {chunkP, chunkP, chunkP};
+        Points bufP[dev::kStateBufs] = {chunkP, chunkP, chunkP, chunkP};
         bufP[1].X = dc.chunk1.p;
         bufP[2].X = dc.chunk2.p;
+        bufP[3].X = dc.chunk3.p;
         // BM_TIMELINE=1: in-stream events around every graph (GPU durations incl. gaps)
         static const bool timeline = std::getenv("BM_TIMELINE") != nullptr;
         // per graph launch: (kind 0 = prep / 1 = Lloyd / 2 = speculative begin, start event, end event)
@@ -1554,9 +1627,9 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         };
         // chunk c's prep (its draws are enqueued on rng_stream: drawn[c % 2])
         auto launch_prep = [&](uint64_t c) {
-            const int i = (int)(c % 6);
+            const int i = (int)(c % dev::kStateBufs);
             BM_CUDA(cudaStreamWaitEvent(pst, sw->drawn[c & 1], 0));
-            BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[(c + 3) % 6], 0));  // data buffer's previous chunk (c-3)
+            BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[i], 0));  // the data buffer's previous chunk (c-4)
             cudaEvent_t e0 = tl_ev(pst);
             BM_CUDA(cudaGraphLaunch(w.g_prep[i], pst));
             if (timeline) tl.push_back({0, e0, tl_ev(pst)});
@@ -1567,10 +1640,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         static const bool spec_on = !(std::getenv("BM_SPEC") && std::string(std::getenv("BM_SPEC")) == "0");
         const bool spec = spec_on && w.g_spec[0] != nullptr;
         if (spec && !dc.sstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.sstream, cudaStreamNonBlocking));
-        auto launch_spec = [&](uint64_t c) {  // chunk c's first assignment, overlapping chunk c-1
-            const int i = (int)(c % 6);
+        auto launch_spec = [&](uint64_t c) {  // chunk c's first assignment, overlapping chunks c-2 and c-1
+            const int i = (int)(c % dev::kStateBufs);
             BM_CUDA(cudaStreamWaitEvent(dc.sstream, w.ev_prep[i], 0));
-            BM_CUDA(cudaStreamWaitEvent(dc.sstream, w.ev_lloyd[(c + 4) % 6], 0));  // state buffer's chunk c-2
+            BM_CUDA(cudaStreamWaitEvent(dc.sstream, w.ev_lloyd[i], 0));  // the state buffer's previous chunk (c-4)
             cudaEvent_t e0 = tl_ev(dc.sstream);
             BM_CUDA(cudaGraphLaunch(w.g_spec[i], dc.sstream));
             if (timeline) tl.push_back({2, e0, tl_ev(dc.sstream)});
@@ -1578,7 +1651,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             count_launch(1);
         };
         auto launch_lloyd = [&](uint64_t c) {
-            const int i = (int)(c % 6);
+            const int i = (int)(c % dev::kStateBufs);
+            if (w.sums_on && (c == 0 || !spec))  // no speculative begin zeroed this buffer's sums
+                BM_CUDA(cudaMemsetAsync(w.sums_of((int)(c % dev::kStateBufs)), 0, 2 * w.sum_half() * sizeof(long long),
+                                        st));
             BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i], 0));
             if (spec) BM_CUDA(cudaStreamWaitEvent(st, w.ev_spec[i], 0));
             cudaEvent_t e0 = tl_ev(st);
@@ -1597,7 +1673,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         draw(0);
         launch_prep(0);
         bool queued = false;     // chunk `chunk`'s Lloyd graph is already queued (guarded)
-        bool spec_next = false;  // chunk+1's draws (and prep) are already enqueued, ahead of this chunk's repair
+        uint64_t ahead = 0;  // chunks after this one whose draws, prep and speculative begin are enqueued
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
             if (chunk > 0 && cfg.has_max_cpu_seconds && seconds_since(t_loop) >= cfg.max_cpu_seconds)
@@ -1614,7 +1690,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 std::swap(w.drec.n, bigger.n);
                 ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
             }
-            const int b = (int)(chunk & 1), i6 = (int)(chunk % 6);
+            const int b = (int)(chunk % dev::kStateBufs), i6 = b;
             if (inc_degenerate > 0) {  // kmeanspp_fill (:84) after this chunk's sample draws
                 // (a queued Lloyd graph of this chunk found go == 0 and did nothing)
                 BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i6], 0));
@@ -1624,31 +1700,33 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 BM_CUDA(cudaStreamSynchronize(sw->rng_stream));
                 // the stream right after this chunk's draws: live, or the input
                 // state of chunk+1's speculative draws (which are discarded)
-                get_stream(st, *sw, rng, spec_next ? 1 + (b ^ 1) : 0);
-                kmeanspp_fill_device(st, bufP[chunk % 3], w, hmask, cfg.candidates_per_step, rng, evals);
+                get_stream(st, *sw, rng, ahead > 0 ? 1 + (int)((chunk + 1) & 1) : 0);
+                kmeanspp_fill_device(st, bufP[b], w, hmask, cfg.candidates_per_step, rng, evals);
                 put_stream(st, *sw, rng);
                 launch_compact(st, w, w.C.p, w.mask.p);  // the Lloyd graph starts from Cact
                 BM_CUDA(cudaMemsetAsync(&w.gs.p->go, 0x01, sizeof(int), st));
                 dev::k_bump_version<<<1, 1, 0, st>>>(w.gs.p);  // the start is no longer the incumbent's copy
                 BM_LAUNCH();
                 queued = false;
-                spec_next = false;  // chunk+1's draws and prep are redone
+                ahead = 0;  // the draws, preps and begins made ahead are redone
             }
             const bool next = exists(chunk + 1);
-            if (next && !spec_next) {  // chunk+1's draws and prep: the stream is past this chunk's repair
-                draw(chunk + 1);
-                launch_prep(chunk + 1);
-            }
             if (!queued) launch_lloyd(chunk);
-            if (next && spec) launch_spec(chunk + 1);
+            // chunks chunk+1 .. chunk+3: draws (the stream is past this chunk's
+            // repair, if any), prep and speculative begin, each as soon as its
+            // buffers' previous chunk (c-4) is done.  Beyond chunk+1 they assume
+            // no repair in between (else they are redone above) and need the
+            // chunk count in advance (no time budget).
+            const uint64_t depth = speculate ? 3 : 1;
+            while (ahead < depth && exists(chunk + 1 + ahead)) {
+                const uint64_t c2 = chunk + 1 + ahead;
+                draw(c2);
+                launch_prep(c2);
+                if (spec) launch_spec(c2);
+                ++ahead;
+            }
             queued = next && speculate;
             if (queued) launch_lloyd(chunk + 1);  // runs iff this chunk's accept needs no repair
-            // chunk+2's draws and prep, assuming chunk+1 needs no repair (else redone above)
-            spec_next = next && speculate && exists(chunk + 2);
-            if (spec_next) {
-                draw(chunk + 2);
-                launch_prep(chunk + 2);
-            }
             BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
             if (w.h_status.p[b].incomplete) {  // more rounds than the graph unrolls
                 BM_CUDA(cudaGraphLaunch(w.g_cont[i6], st));
@@ -1664,6 +1742,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             inc_degenerate = ls.inc_degenerate;
             count_launch(3 + 3 * ls.iterations);
             out->chunks = chunk + 1;
+            if (ahead) --ahead;
         }
         // the last chunk's record gets its exact objective
         dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.gs.p, accept_args(w), w.dists.p, w.R,
@@ -1897,9 +1976,13 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
         d->n = n;
         d->dtype = dtype;
         BM_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
-        DevBuf<int> flags(2);  // [0] non-finite, [1] not exactly representable in fp32
-        BM_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), d->stream));
-        int hf[2] = {0, 0};
+        // [0] non-finite, [1] not exactly representable in fp32, [2] lowest set
+        // bit exponent, [4:6] largest |value| (bits): the exact-sum test
+        DevBuf<int> flags(6);
+        BM_CUDA(cudaMemsetAsync(flags.p, 0, 6 * sizeof(int), d->stream));
+        BM_CUDA(cudaMemsetAsync(flags.p + 2, 0x7F, sizeof(int), d->stream));
+        int hf[6] = {0, 0, 0, 0, 0, 0};
+        unsigned long long* maxbits = reinterpret_cast<unsigned long long*>(flags.p + 4);
         // datasets come and go (one per e2e step): stream-ordered allocations from a
         // pool that keeps its memory, instead of a fresh cudaMalloc each time
         {
@@ -1921,7 +2004,7 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
                 ~Tmp() { cudaFreeAsync(p, s); }
             } tmp_guard{tmp, d->stream};
             BM_CUDA(cudaMemcpyAsync(tmp, values, m * n * sizeof(double), cudaMemcpyHostToDevice, d->stream));
-            dev::k_check_narrow<<<1184, 256, 0, d->stream>>>(tmp, m * n, flags.p, flags.p + 1);
+            dev::k_check_narrow<<<1184, 256, 0, d->stream>>>(tmp, m * n, flags.p, flags.p + 1, flags.p + 2, maxbits);
             BM_LAUNCH();
             BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, d->stream));
             BM_CUDA(cudaStreamSynchronize(d->stream));
@@ -1951,12 +2034,25 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
             dispatch(dtype, [&](auto tag) {
                 using T = decltype(tag);
                 dev::k_check_finite<T><<<1184, 256, 0, d->stream>>>(static_cast<const T*>(d->X), m, (int)n, d->ld,
-                                                                    flags.p);
+                                                                    flags.p, flags.p + 2, maxbits);
             });
             BM_LAUNCH();
-            BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+            BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, d->stream));
             BM_CUDA(cudaStreamSynchronize(d->stream));
             if (hf[0]) throw ConfigError("dataset contains a non-finite value");
+        }
+        {  // exact-sum test (kernels.cuh §5b): every value k * 2^e, m * max|x| < 2^52 * 2^e
+            unsigned long long mb = 0;
+            std::memcpy(&mb, hf + 4, sizeof(mb));
+            double mx = 0.0;
+            std::memcpy(&mx, &mb, sizeof(mx));
+            const int e = hf[2] == 0x7F7F7F7F ? 0 : hf[2];  // all zeros: any exponent
+            if (e >= -960 && e <= 960) {
+                const double units = std::ldexp(mx, -e);  // an integer (exact)
+                d->exact_sums = units * (double)m < 0x1p52;
+                d->sum_exp = e;
+                d->sum_units_max = units;
+            }
         }
         *out = d.release();
     });
@@ -1972,6 +2068,13 @@ bm_status bm_dataset_destroy(bm_dataset* d) {
 
 bm_status bm_dataset_storage(const bm_dataset* d, bm_dtype* storage) {
     return guarded([&] { *storage = d->dtype; });
+}
+
+bm_status bm_dataset_sum_mode(const bm_dataset* d, int32_t* exact, int32_t* exponent) {
+    return guarded([&] {
+        *exact = d->exact_sums ? 1 : 0;
+        *exponent = d->sum_exp;
+    });
 }
 
 bm_status bm_dataset_shape(const bm_dataset* d, uint64_t* m, uint64_t* n) {
@@ -1994,6 +2097,9 @@ bm_status bm_dataset_gather(const bm_dataset* d, const uint64_t* rows, uint64_t 
         o->n = d->n;
         o->dtype = d->dtype;
         o->ld = d->ld;
+        o->exact_sums = d->exact_sums;  // a subset of the rows keeps the exact-sum property
+        o->sum_exp = d->sum_exp;
+        o->sum_units_max = d->sum_units_max;
         BM_CUDA(cudaStreamCreateWithFlags(&o->stream, cudaStreamNonBlocking));
         BM_CUDA(cudaMallocAsync(&o->X, count * o->ld * dtype_size(o->dtype), o->stream));
         DevBuf<uint64_t> idx(count);

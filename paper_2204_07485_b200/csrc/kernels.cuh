@@ -44,7 +44,7 @@ struct LloydStatus {
     unsigned ctas_done;  // CTAs of the current launch that have added their sum
     int exact_checks;    // decisions that needed the exact sums (diagnostics)
     int incomplete;      // the graph's unrolled rounds ended without a stop: the host continues
-    int pad2;
+    int sum_sel;         // exact-sum mode: which half of the chunk buffer's label sums is live (1: the redo begin's)
     long long begin_version;  // incumbent version the begin's assignment used (-1: none / stale)
     long long bv_min;         // lowest version its CTAs saw when they started (atomicMin; host resets)
 };
@@ -65,6 +65,7 @@ struct GState {
 static_assert(sizeof(LloydStatus) % 8 == 0, "status is copied as 8-byte words");
 
 constexpr int kSMaxK = 32;  // centroids handled by the screened path
+constexpr int kStateBufs = 4;  // graph mode: chunk c's data, labels / distances / bounds / status live in buffer c % 4
 
 // Per-chunk accept record (ChunkRecord big_means.hpp:28-34).
 struct Record {
@@ -603,6 +604,16 @@ struct LloydCtl {
     int begin_kind;         // begin launches: 0 plain, 1 speculative (incumbent copy), 2 redo unless current
     int begin_slot;         // begin launches: the slot the assignment writes (parity after the begin)
     AcceptArgs acc;         // accept state (valid when has_acc)
+    // exact-sum mode (sums != nullptr): per-label integer sums of the chunk's
+    // points, updated by the assignment (§5b)
+    long long* sums;        // this chunk buffer's two halves, each [kSMaxK][n] sums + [kSMaxK] counts
+    uint64_t sum_half;      // elements per half
+    double sum_scale;       // 2^-e: a stored value times this is an integer
+    int sum_which;          // half the launch accumulates into: 0 / 1, or -1: st->sum_sel
+    long long* parts;       // begins: per-CTA partial sums [CTA][kSMaxK * n + kSMaxK], merged per group of 8 CTAs
+    unsigned* grp_ctr;      // begins: arrival counters of the groups (reset by each group's merger)
+    uint64_t pts_rows;      // rows of the launch (point CTAs = ceil(rows / 128))
+    int sum_small;          // per-CTA sums of the value units stay below 2^31 (32-bit shared accumulators)
     int has_acc;
     int accept_run;         // the control runs the accept (:89-94) when the loop stops
     LloydStatus* host_st;   // with acc: the status is also written to mapped host memory
@@ -943,6 +954,7 @@ __device__ __noinline__ int lloyd_fast_control(const LloydCtl& c, LloydStatus* s
         const long long v = static_cast<long long>(__ldcg(reinterpret_cast<const unsigned long long*>(&c.gs->inc_version)));
         // (only a speculative begin's result may stand in for a later begin)
         st->begin_version = c.begin_kind == 1 && st->bv_min == v ? v : -1;
+        st->sum_sel = c.begin_kind == 2 ? 1 : 0;  // exact-sum mode: the redo begin used the second half
         return -1;
     }
     // the previous chunk's record: its exact objective, before this chunk's accept
@@ -1596,6 +1608,7 @@ struct TmaSmem {
     unsigned cand[kABP];                                       // candidate bitmask per point
     int icount[kABP];
     int lab_rank[kABP];                                        // chosen compacted centroid per point
+    int lab_new[kABP], lab_old[kABP];                          // exact-sum mode: this launch's label change per point
     int rank_of[kSMaxK];                                       // label -> compacted index
     float delta[kSMaxK];                                       // centroid movement per label (rounded up)
     alignas(16) float lbs[sizeof(T) == 4 ? kABP : 1][kSMaxK];  // fp32 round fast path: the bound rows (16-byte chunks swizzled)
@@ -1603,6 +1616,172 @@ struct TmaSmem {
     uint32_t n_items;
     int is_last;
 };
+
+// ---------------------------------------------------------------------------
+// 5b. Exact-sum mode.  When every stored value is an integer multiple of 2^e
+// and m * max|x| < 2^53 * 2^e (checked once per dataset, bm_dataset_create),
+// every partial sum of any subset of the values of one dimension is exactly
+// representable in fp64: the reference's ordered sums (per-tile folds in index
+// order, tile merge in order, core.cpp:206-229) then equal the exact sums,
+// whatever the order.  The label sums are kept as integers (x * 2^-e) per
+// chunk buffer: a begin adds every point, a Lloyd round moves only the points
+// whose label changed, and k_centroids turns them into the next centroids
+// (sum * (1.0/count), core.cpp:237-239) — no ordered update pass at all.
+// ---------------------------------------------------------------------------
+constexpr int kSumCopies = 8;  // CTA b adds into copy b % 8 (spreads same-address atomics)
+
+__device__ __forceinline__ long long sum_units(double x, double scale) {
+    return __double2ll_rn(__dmul_rn(x, scale));  // exact: x * 2^-e is an integer below 2^53
+}
+
+template <typename T>
+__device__ __noinline__ void label_sums(TmaSmem<T>& S, const LloydCtl& ctl, const T* __restrict__ X, uint64_t ld,
+                                        int n, uint64_t p0, int np, bool full, int kfull, unsigned char* scratch,
+                                        size_t scratch_bytes) {
+    __syncthreads();  // every point's (new, old) label recorded; the scratch area is free
+    const int tid = threadIdx.x;
+    const int which = ctl.sum_which >= 0 ? ctl.sum_which : ctl.st->sum_sel;
+    // this CTA's copy: [kSumCopies][kSMaxK][n] sums, then [kSumCopies][kSMaxK] counts
+    const int cp = static_cast<int>(blockIdx.x % kSumCopies);
+    long long* half = ctl.sums + static_cast<uint64_t>(which) * ctl.sum_half;
+    long long* sg = half + static_cast<uint64_t>(cp) * kSMaxK * n;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n +
+                                                                    cp * kSMaxK);
+    // Per label, the points that join it (+x) and the points that leave it (-x)
+    // (a begin: every point joins its label), bucketed by a counting sort; then
+    // one thread per (label, dim) sums its members' coordinates.  The partial
+    // sums are exact in fp64 (§5b: multiples of 2^e below 2^52 * 2^e), so the
+    // order is free.
+    // (the lists live in red_u, free until the control tail; the moved rows are
+    // staged in the scratch area when they fit)
+    int* pc = reinterpret_cast<int*>(&S.red_u[0][0]);  // [kSMaxK + 1] join offsets
+    int* mc = pc + (kSMaxK + 1);                 // [kSMaxK + 1] leave offsets
+    int* pcur = mc + (kSMaxK + 1);               // [kSMaxK] cursors
+    int* mcur = pcur + kSMaxK;                   // [kSMaxK]
+    short* plist = reinterpret_cast<short*>(mcur + kSMaxK);  // [kABP]
+    short* mlist = plist + kABP;                             // [kABP]
+    int* flag = reinterpret_cast<int*>(mlist + kABP);        // [2]: any move, group leader
+    if (tid < kSMaxK) {
+        pcur[tid] = 0;
+        mcur[tid] = 0;
+    }
+    if (tid == 0) flag[0] = 0;
+    __syncthreads();
+    int a = -1, b = -1;
+    int* rslot = flag + 2;  // [kABP] staged row of each moved point
+    if (tid == 0) flag[1] = 0;
+    __syncthreads();
+    if (tid < np) {
+        a = full ? -1 : S.lab_old[tid];
+        b = S.lab_new[tid];
+        if (a == b) a = b = -1;
+        if (b >= 0) atomicAdd(&pcur[b], 1);
+        if (a >= 0) atomicAdd(&mcur[a], 1);
+        if (b >= 0 || a >= 0) rslot[tid] = atomicAdd(&flag[1], 1);
+    }
+    __syncthreads();
+    const int nm = flag[1];
+    if (nm == 0) return;  // nothing moved in this CTA
+    // stage the moved rows (whole 16-byte vectors) with cp.async
+    constexpr int kV = 16 / sizeof(T);
+    const int vpr = static_cast<int>((n + kV - 1) / kV);
+    const bool staged = (ld % kV) == 0 && static_cast<size_t>(nm) * vpr * 16 <= scratch_bytes;
+    T* xs = reinterpret_cast<T*>(scratch);
+    if (staged) {
+        for (int e = tid; e < np * vpr; e += blockDim.x) {
+            const int p = e / vpr, v = e - p * vpr;
+            const int la = full ? -1 : S.lab_old[p], lb = S.lab_new[p];
+            if (la != lb && (la >= 0 || lb >= 0))
+                cp_async_16(xs + static_cast<size_t>(rslot[p]) * vpr * kV + v * kV, X + (p0 + p) * ld + v * kV);
+        }
+        cp_async_commit();
+    }
+    if (tid < 32) {  // exclusive scans of the join / leave counts (k <= 32)
+        const int lane = tid;
+        const int vp = pcur[lane], vm = mcur[lane];
+        int ip = vp, im = vm;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yp = __shfl_up_sync(0xFFFFFFFFu, ip, o), ym = __shfl_up_sync(0xFFFFFFFFu, im, o);
+            if (lane >= o) {
+                ip += yp;
+                im += ym;
+            }
+        }
+        pc[lane] = ip - vp;
+        mc[lane] = im - vm;
+        if (lane == 31) {
+            pc[32] = ip;
+            mc[32] = im;
+        }
+        pcur[lane] = ip - vp;
+        mcur[lane] = im - vm;
+    }
+    __syncthreads();
+    if (b >= 0) plist[atomicAdd(&pcur[b], 1)] = static_cast<short>(staged ? rslot[tid] : tid);
+    if (a >= 0) mlist[atomicAdd(&mcur[a], 1)] = static_cast<short>(staged ? rslot[tid] : tid);
+    if (staged) cp_async_wait<0>();
+    __syncthreads();
+    const double sc = ctl.sum_scale;
+    const bool grouped = full && ctl.parts;
+    const uint64_t slot_len = static_cast<uint64_t>(kSMaxK) * n + kSMaxK;
+    long long* slot = grouped ? ctl.parts + blockIdx.x * slot_len : nullptr;
+    const T* Xb = staged ? xs : X + p0 * ld;
+    const uint64_t rs = staged ? static_cast<uint64_t>(vpr) * kV : ld;  // row stride of Xb
+    for (int e = tid; e < kfull * n; e += blockDim.x) {
+        const int j = e / n, d = e - j * n;
+        double s = 0.0;
+        int q = pc[j];
+        const int q1 = pc[j + 1];
+        for (; q + 4 <= q1; q += 4) {
+            const double x0 = to_f64(Xb[plist[q] * rs + d]), x1 = to_f64(Xb[plist[q + 1] * rs + d]);
+            const double x2 = to_f64(Xb[plist[q + 2] * rs + d]), x3 = to_f64(Xb[plist[q + 3] * rs + d]);
+            s = __dadd_rn(__dadd_rn(s, x0), __dadd_rn(__dadd_rn(x1, x2), x3));
+        }
+        for (; q < q1; ++q) s = __dadd_rn(s, to_f64(Xb[plist[q] * rs + d]));
+        for (int r = mc[j]; r < mc[j + 1]; ++r) s = __dsub_rn(s, to_f64(Xb[mlist[r] * rs + d]));
+        const long long v = sum_units(s, sc);
+        if (grouped) slot[e] = v;
+        else if (v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&sg[e]), static_cast<unsigned long long>(v));
+    }
+    if (!grouped) {
+        if (tid < kfull) {
+            const long long c = (pc[tid + 1] - pc[tid]) - (mc[tid + 1] - mc[tid]);
+            if (c != 0) atomicAdd(&cnt[tid], static_cast<unsigned long long>(c));
+        }
+        return;
+    }
+    // A begin: the partials of 8 CTAs are merged by the last of them (8x fewer
+    // global atomics, which are the bottleneck at this volume).
+    if (tid < kfull) slot[static_cast<uint64_t>(kSMaxK) * n + tid] = pc[tid + 1] - pc[tid];
+    __threadfence();
+    __syncthreads();
+    const int g = static_cast<int>(blockIdx.x / 8);
+    const int pts_ctas = static_cast<int>((ctl.pts_rows + kABP - 1) / kABP);
+    const int members = min(8, pts_ctas - 8 * g);
+    if (tid == 0) flag[1] = atomicAdd(&ctl.grp_ctr[g], 1u) == static_cast<unsigned>(members) - 1;
+    __syncthreads();
+    if (!flag[1]) return;
+    __threadfence();
+    long long* gsg = half + static_cast<uint64_t>(g % kSumCopies) * kSMaxK * n;
+    unsigned long long* gcnt = reinterpret_cast<unsigned long long*>(
+        half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n + (g % kSumCopies) * kSMaxK);
+    const long long* gbase = ctl.parts + static_cast<uint64_t>(8 * g) * slot_len;
+    const int kn = kfull * n;
+    for (int e = tid; e < kn + kfull; e += blockDim.x) {
+        const bool is_cnt = e >= kn;
+        const uint64_t off = is_cnt ? static_cast<uint64_t>(kSMaxK) * n + (e - kn) : static_cast<uint64_t>(e);
+        long long v = 0;
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+            if (m < members) v += __ldcg(gbase + m * slot_len + off);
+        if (v != 0) {
+            if (is_cnt) atomicAdd(&gcnt[e - kn], static_cast<unsigned long long>(v));
+            else atomicAdd(reinterpret_cast<unsigned long long*>(&gsg[off]), static_cast<unsigned long long>(v));
+        }
+    }
+    if (tid == 0) ctl.grp_ctr[g] = 0u;
+}
 
 template <typename T>
 __device__ __forceinline__ T raw_at(const unsigned char* raw, int p, int d) {
@@ -1834,7 +2013,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             const uint64_t t = (p0 - rows) / kABP;  // fixup CTAs follow the point blocks
             const uint64_t R = ctl.fix_rows, tb = t * kTile;
             if (tb < R) {
-                const double* dv = ctl.dists_all + (3 * static_cast<uint64_t>(pend & 1) + gst->fix_par) * R + tb;
+                const double* dv = ctl.dists_all + (3 * static_cast<uint64_t>(pend % kStateBufs) + gst->fix_par) * R + tb;
                 const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), R - tb));
                 double* fbuf = reinterpret_cast<double*>(&S.raw[0][0]);
                 for (int i = tid; i < len; i += kSThreads) fbuf[i] = __ldcg(dv + i);
@@ -1970,6 +2149,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                     labels_out[gp] = bl;
                     if (dists_out) dists_out[gp] = best;
                     if (bl != a) *changed_flag = 1;
+                    S.lab_new[tid] = bl;
+                    S.lab_old[tid] = a;
                 }
                 __syncthreads();
                 for (int e = tid; e < np * (kSMaxK / 4); e += kSThreads) {  // bound rows back, coalesced
@@ -2129,6 +2310,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 labels_out[gp] = bl;
                 if (dists_out) dists_out[gp] = best;
                 if (bl != a) *changed_flag = 1;
+                    S.lab_new[tid] = bl;
+                    S.lab_old[tid] = a;
             }
             ktrace(15, hmode);
             goto fold;
@@ -2356,8 +2539,11 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         const int label = bj >= 0 ? act_idx[bj] : -1;
         labels_out[gp] = label;
         if (dists_out) dists_out[gp] = best;
-        if (labels_old && labels_old[gp] != label) *changed_flag = 1;
+        const int lold = labels_old ? labels_old[gp] : -1;
+        if (labels_old && lold != label) *changed_flag = 1;
         S.lab_rank[p] = bj;
+        S.lab_new[p] = label;
+        S.lab_old[p] = lold;
     }
     if (hmode >= 1 && lbk) {  // per (point, label) lower bounds in distance units, staged for coalesced rows
         __syncthreads();
@@ -2388,6 +2574,9 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
 fold:
     ktrace(10, hmode);
+    if (ctl.sums && np > 0) label_sums<T>(S, ctl, X, ld, n, p0, np, labels_old == nullptr, kfull, reuse,
+                                          static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse));
+    ktrace(31, hmode);
     if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
         __syncthreads();  // distances of this CTA written (some by other threads)
         double v = tid < np ? dists_out[p0 + tid] : 0.0;
@@ -2864,6 +3053,70 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
     }
 }
 
+// Exact-sum mode update (update_centroids core.cpp:183-244 via §5b): the
+// label sums kept by the assignments give sum * (1.0/count) per (label, dim)
+// (:237-239), count 0 a degenerate row of 0.0; plus everything k_update's
+// merge writes (mask, active list, Cact, CT32, per-label movement).  One CTA,
+// a warp per label.
+__global__ void __launch_bounds__(1024)
+k_centroids(const LloydStatus* __restrict__ st, const int* __restrict__ stop, const int* __restrict__ go,
+            const long long* __restrict__ sums, uint64_t sum_half, double unscale, int k, int n,
+            double* __restrict__ C, uint8_t* __restrict__ mask, double* __restrict__ Cact, int ldc,
+            int* __restrict__ act_idx, int* __restrict__ n_active, float* __restrict__ CT32, float* __restrict__ delta) {
+    klog_start(1);
+    pdl_wait();
+    if (stop && *stop) return;
+    if (go && !*go) return;
+    __shared__ long long tot[kSMaxK];
+    __shared__ int rank[kSMaxK];
+    const long long* half = sums + static_cast<uint64_t>(st->sum_sel) * sum_half;
+    const long long* cnts = half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) {
+        long long c = 0;
+        if (lane < k)
+#pragma unroll
+            for (int q = 0; q < kSumCopies; ++q) c += __ldcg(cnts + q * kSMaxK + lane);
+        const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
+        if (lane < k) {
+            tot[lane] = c;
+            const int r = __popc(live & ((1u << lane) - 1u));
+            rank[lane] = c > 0 ? r : -1;
+            mask[lane] = c > 0 ? 0 : 1;
+            if (c > 0) act_idx[r] = lane;
+        }
+        if (lane == 0) *n_active = __popc(live);
+    }
+    __syncthreads();
+    for (int j = warp; j < k; j += blockDim.x / 32) {
+        const long long c = tot[j];
+        const uint64_t row = static_cast<uint64_t>(j) * n;
+        if (c <= 0) {
+            for (int d = lane; d < n; d += 32) C[row + d] = 0.0;
+            continue;
+        }
+        const double inv = __ddiv_rn(1.0, static_cast<double>(c));
+        const int rk = rank[j];
+        double sq = 0.0;
+        for (int d = lane; d < n; d += 32) {
+            long long s = 0;
+#pragma unroll
+            for (int q = 0; q < kSumCopies; ++q) s += __ldcg(half + (static_cast<uint64_t>(q) * kSMaxK * n) + row + d);
+            const double sum = __dmul_rn(static_cast<double>(s), unscale);  // exact (§5b)
+            const double v = __dmul_rn(sum, inv);
+            const double dv = __dsub_rn(v, C[row + d]);
+            sq = __dadd_rn(sq, __dmul_rn(dv, dv));  // order-free: only bounds use it
+            C[row + d] = v;
+            Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
+            if (CT32) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+        if (lane == 0) delta[j] = __double2float_ru(__dsqrt_ru(sq * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+    }
+    if (tid == 0) klog_end(1);
+}
+
 // ===========================================================================
 // 7. Accept (big_means.cpp:89-94) on the device.
 // ===========================================================================
@@ -2900,7 +3153,7 @@ __global__ void k_fix_final(GState* gs, AcceptArgs A, const double* __restrict__
     const int pend = gs->pending_fix;
     if (pend < 0) return;
     const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
-    const double* dv = dists_all + (3 * static_cast<uint64_t>(pend & 1) + gs->fix_par) * R + tb;
+    const double* dv = dists_all + (3 * static_cast<uint64_t>(pend % kStateBufs) + gs->fix_par) * R + tb;
     const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), R - tb));
     for (int i = threadIdx.x; i < len; i += blockDim.x) fbuf[i] = __ldcg(dv + i);
     __syncthreads();
@@ -3182,26 +3435,65 @@ __global__ void k_set_row(const T* __restrict__ X, uint64_t ld, int n, uint64_t 
 // ===========================================================================
 // 9. Dataset helpers.
 // ===========================================================================
+// Exact-sum statistics (§5b) of one finite value: exponent of its lowest set
+// bit, and |x| as bits (ordered like the values for x >= 0).
+__device__ __forceinline__ void exact_stats(double x, int& lowexp, unsigned long long& maxbits) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7FFFFFFFFFFFFFFFull;
+    if (b == 0) return;
+    const int E = static_cast<int>(b >> 52);
+    const unsigned long long M = b & 0xFFFFFFFFFFFFFull;
+    const int le = E == 0 ? -1074 + __ffsll(static_cast<long long>(M)) - 1
+                          : E - 1075 + __ffsll(static_cast<long long>(M | (1ull << 52))) - 1;
+    lowexp = min(lowexp, le);
+    maxbits = max(maxbits, b);
+}
+
+__device__ __forceinline__ void exact_stats_flush(int lowexp, unsigned long long maxbits, int* lowexp_out,
+                                                  unsigned long long* maxbits_out) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lowexp = min(lowexp, __shfl_xor_sync(0xFFFFFFFFu, lowexp, o));
+        maxbits = max(maxbits, __shfl_xor_sync(0xFFFFFFFFu, maxbits, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lowexp != 0x7F7F7F7F) atomicMin(lowexp_out, lowexp);
+        if (maxbits) atomicMax(maxbits_out, maxbits);
+    }
+}
+
 template <typename T>
-__global__ void k_check_finite(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld, int* bad) {
+__global__ void k_check_finite(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld, int* bad, int* lowexp_out,
+                               unsigned long long* maxbits_out) {
     const uint64_t total = rows * static_cast<uint64_t>(n);
+    int lowexp = 0x7F7F7F7F;
+    unsigned long long maxbits = 0;
     for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const double v = to_f64(X[(e / n) * ld + (e % n)]);
         if (!isfinite(v)) *bad = 1;
+        else exact_stats(v, lowexp, maxbits);
     }
+    exact_stats_flush(lowexp, maxbits, lowexp_out, maxbits_out);
 }
 
 // Lossless storage narrowing: an fp64 dataset whose every value round-trips
 // through fp32 exactly is stored as fp32 (every kernel promotes exactly, so all
 // results are unchanged) — half the HBM and L2 bytes.
-__global__ void k_check_narrow(const double* __restrict__ v, uint64_t count, int* bad, int* inexact) {
+__global__ void k_check_narrow(const double* __restrict__ v, uint64_t count, int* bad, int* inexact,
+                               int* lowexp_out, unsigned long long* maxbits_out) {
+    int lowexp = 0x7F7F7F7F;
+    unsigned long long maxbits = 0;
     for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const double x = v[e];
-        if (!isfinite(x)) *bad = 1;
-        else if (static_cast<double>(static_cast<float>(x)) != x) *inexact = 1;
+        if (!isfinite(x)) {
+            *bad = 1;
+            continue;
+        }
+        if (static_cast<double>(static_cast<float>(x)) != x) *inexact = 1;
+        exact_stats(x, lowexp, maxbits);
     }
+    exact_stats_flush(lowexp, maxbits, lowexp_out, maxbits_out);
 }
 
 __global__ void k_narrow(const double* __restrict__ in, uint64_t rows, int n, float* __restrict__ out, uint64_t ld) {

@@ -208,3 +208,42 @@ def test_long_runs_vs_oracle(port, case):
     assert (bits(out.centroids.values) == bits(p.centroids)).all()
     assert (out.assignment == p.labels).all()
     assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+# Exact-sum regimes (kernels.cuh §5b): the device keeps integer label sums when
+# every value is a multiple of 2^e and m * max|x| < 2^52 * 2^e; the results
+# must stay bitwise equal to the reference's ordered sums in every regime,
+# including datasets just inside and just outside the test.
+def _sum_regimes():
+    r = np.random.default_rng(77)
+    return {
+        "small_ints": (np.rint(r.normal(size=(12000, 12)) * 40), True, 0),
+        "even_ints": (np.rint(r.normal(size=(12000, 9)) * 40) * 8, True, 3),
+        "quarter_steps": (np.rint(r.normal(size=(12000, 7)) * 400) / 4, True, -2),
+        "fine_steps_f64": (np.rint(r.normal(size=(12000, 6)) * 2.0**36) * 2.0**-40, True, -40),
+        "huge_ints": (np.rint(r.normal(size=(12000, 5)) * 2.0**36), True, 0),
+        "too_wide": (np.rint(r.normal(size=(12000, 5)) * 2.0**40), False, None),
+        "gaussian": (r.normal(size=(12000, 8)), False, None),
+        "fp32_ints": (np.rint(r.normal(size=(12000, 10)) * 30).astype(np.float32), True, 0),
+    }
+
+
+@pytest.mark.parametrize("case", sorted(_sum_regimes()))
+def test_exact_sum_regimes_vs_oracle(port, case):
+    X, exact, e = _sum_regimes()[case]
+    d = bm.Dataset(X)
+    got_exact, got_e = d.exact_sums
+    assert got_exact == exact
+    if exact:
+        # the lowest set bit over the data can only be at or above the construction's step
+        assert got_e >= e
+    for k, s, chunks, seed in ((7, 1500, 10, 1), (25, 3000, 6, 2)):
+        out, trace = bm.big_means(d, cfg(k, s, chunks, seed=seed))
+        p = port.big_means(X.astype(np.float64), k, s, chunks, seed=seed)
+        got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+                r.degenerate_repaired) for r in trace.records]
+        assert got == p.trace
+        assert out.objective == p.objective
+        assert (bits(out.centroids.values) == bits(p.centroids)).all()
+        assert (out.assignment == p.labels).all()
+        assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)

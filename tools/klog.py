@@ -31,7 +31,7 @@ lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
 n1 = int(buf[200000])
 st1 = buf[199990:199994].astype(np.int64)
 E = buf[200001:200001 + 3 * 60000].reshape(-1, 3).astype(np.int64)[n0 % 60000:n1 % 60000]
-names = {0: "guard", 2: "update", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)",
+names = {0: "guard", 1: "centroids", 2: "update", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)",
          4: "accept:folded", 5: "accept:objective", 6: "accept:record", 7: "accept:ranks"}
 sub = E[(E[:, 0] >= 4) & (E[:, 0] <= 7)]
 E = E[(E[:, 0] < 4) | (E[:, 0] > 7)]
@@ -71,7 +71,7 @@ print(f"round fast path: {ds[0]} CTAs, {ds[1]} fell back to the screen ({100 * d
 names_k = {14: "probe1", 0: "start", 1: "slab0", 2: "slab1", 3: "slab2", 4: "slab3", 5: "slab4", 6: "slab5", 7: "bounds",
            8: "items", 9: "recheck", 10: "out/fold", 13: "fp_setup", 15: "fp_done", 16: "c0wait", 17: "c0done",
            24: "c4wait", 25: "c4done", 26: "fp_items", 11: "acc:record", 12: "acc:ranks", 27: "lbk_written", 28: "last:arrived", 29: "last:control",
-           30: "last:accept"}
+           30: "last:accept", 31: "sums_done", 18: "s:moved", 19: "s:aggregated", 20: "s:slot_fenced"}
 for base, title in ((400000, "begin"), (470000, "round")):
     T = buf[base:base + 2048 * 32].reshape(-1, 32).astype(np.int64)
     T = T[T[:, 0] > 0]
