@@ -159,6 +159,7 @@ struct Workspace {
     DevBuf<long long> sums;
     bool sums_on = false;
     double sum_scale = 1.0, sum_unscale = 1.0;
+    bool sums_fuse = false;  // the update runs in the control CTA of the previous launch (LloydCtl::sum_fuse)
     bool sum_small = false;  // per-CTA sums of the value units below 2^31 (bm_dataset::sum_units_max < 2^23)
     uint64_t sum_half() const { return (uint64_t)dev::kSumCopies * dev::kSMaxK * (n + 1); }
     long long* sums_of(int buf) { return sums.p + (uint64_t)buf * 2 * sum_half(); }
@@ -909,6 +910,18 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
             c.pts_rows = w.R;
         }
         c.sum_small = w.sum_small ? 1 : 0;
+        if (w.sums_fuse && g->begin_kind != 1) {  // never the speculative begin: the working centroids are in use
+            c.sum_fuse = 1;
+            c.sum_unscale = w.sum_unscale;
+            c.cC = w.C.p;
+            c.cmask = w.mask.p;
+            c.cCact = w.Cact.p;
+            c.cldc = w.ldc;
+            c.cact = w.act.p;
+            c.cn_active = &w.gs.p->n_active;
+            c.cCT32 = w.CT32.p;
+            c.cdelta = w.delta.p;
+        }
     }
     c.host_st = g->host_st;
     c.incomplete_after = g->incomplete_after;
@@ -942,7 +955,8 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
     dev::LloydStatus* sts = gr_status(w, g);
     const int* parity = &sts->parity;
     const int* stop = &sts->stop;
-    if (g && w.sums_on) launch_centroids(st, w, g->buf, sts, g->go);
+    if (g && w.sums_on && w.sums_fuse) w.drift_slabs = 1;  // computed by the previous launch's control CTA
+    else if (g && w.sums_on) launch_centroids(st, w, g->buf, sts, g->go);
     else launch_update(st, P, w, parity, stop, g ? g->go : nullptr, gr_labels(w, g), &sts->bad_label);
     dev::LloydCtl ctl = make_ctl(w, 2, P.rows, max_it, tol, cond, use_cond, fast);
     apply_graph(ctl, w, g);
@@ -1506,7 +1520,7 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
                   (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
                   (void*)dc.chunk3.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n,
-                  (int)w.sums_on + 2 * (int)w.sum_small, w.sum_scale, (void*)w.sums.p);
+                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse, w.sum_scale, (void*)w.sums.p);
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
@@ -1571,6 +1585,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         w.sum_scale = std::ldexp(1.0, -d->sum_exp);
         w.sum_unscale = std::ldexp(1.0, d->sum_exp);
         w.sum_small = d->sum_units_max < 0x1p23;  // 128 points per CTA: partial sums below 2^30
+        static const bool fuse = !(std::getenv("BM_SUMS_FUSE") && std::string(std::getenv("BM_SUMS_FUSE")) == "0");
+        w.sums_fuse = fuse;
         const uint64_t nb = dev::kStateBufs;
         if (w.sums.n < 2 * nb * w.sum_half()) w.sums.alloc(2 * nb * w.sum_half());
         if (w.sum_parts.n < nb * w.part_ctas() * w.part_len()) w.sum_parts.alloc(nb * w.part_ctas() * w.part_len());

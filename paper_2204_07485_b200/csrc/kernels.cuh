@@ -614,6 +614,19 @@ struct LloydCtl {
     unsigned* grp_ctr;      // begins: arrival counters of the groups (reset by each group's merger)
     uint64_t pts_rows;      // rows of the launch (point CTAs = ceil(rows / 128))
     int sum_small;          // per-CTA sums of the value units stay below 2^31 (32-bit shared accumulators)
+    // exact-sum mode, fused update: the CTA that runs the control (or CTA 0 of
+    // a begin that finds the speculative one current) computes the centroids
+    // of the next round from the sums when the loop goes on (no k_centroids)
+    int sum_fuse;
+    double sum_unscale;
+    double* cC;
+    uint8_t* cmask;
+    double* cCact;
+    int cldc;
+    int* cact;
+    int* cn_active;
+    float* cCT32;
+    float* cdelta;
     int has_acc;
     int accept_run;         // the control runs the accept (:89-94) when the loop stops
     LloydStatus* host_st;   // with acc: the status is also written to mapped host memory
@@ -1783,6 +1796,69 @@ __device__ __noinline__ void label_sums(TmaSmem<T>& S, const LloydCtl& ctl, cons
     if (tid == 0) ctl.grp_ctr[g] = 0u;
 }
 
+// Exact-sum mode update (update_centroids core.cpp:183-244 via §5b): the
+// label sums kept by the assignments give sum * (1.0/count) per (label, dim)
+// (:237-239), count 0 a degenerate row of 0.0; plus everything k_update's
+// merge writes (mask, active list, Cact, CT32, per-label movement).  CTA-wide
+// (any whole number of warps), a warp per label; tot / rank: shared scratch.
+__device__ __noinline__ void centroids_from_sums(const long long* __restrict__ half, int k, int n, double unscale,
+                                                 double* __restrict__ C, uint8_t* __restrict__ mask,
+                                                 double* __restrict__ Cact, int ldc, int* __restrict__ act_idx,
+                                                 int* __restrict__ n_active, float* __restrict__ CT32,
+                                                 float* __restrict__ delta, long long* tot, int* rank) {
+    const long long* cnts = half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (warp == 0) {
+        long long c = 0;
+        if (lane < k)
+#pragma unroll
+            for (int q = 0; q < kSumCopies; ++q) c += __ldcg(cnts + q * kSMaxK + lane);
+        const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
+        if (lane < k) {
+            tot[lane] = c;
+            const int r = __popc(live & ((1u << lane) - 1u));
+            rank[lane] = c > 0 ? r : -1;
+            mask[lane] = c > 0 ? 0 : 1;
+            if (c > 0) act_idx[r] = lane;
+        }
+        if (lane == 0) *n_active = __popc(live);
+    }
+    __syncthreads();
+    for (int j = warp; j < k; j += blockDim.x / 32) {
+        const long long c = tot[j];
+        const uint64_t row = static_cast<uint64_t>(j) * n;
+        if (c <= 0) {
+            for (int d = lane; d < n; d += 32) C[row + d] = 0.0;
+            continue;
+        }
+        const double inv = __ddiv_rn(1.0, static_cast<double>(c));
+        const int rk = rank[j];
+        double sq = 0.0;
+        for (int d = lane; d < n; d += 32) {
+            long long s = 0;
+#pragma unroll
+            for (int q = 0; q < kSumCopies; ++q) s += __ldcg(half + (static_cast<uint64_t>(q) * kSMaxK * n) + row + d);
+            const double sum = __dmul_rn(static_cast<double>(s), unscale);  // exact (§5b)
+            const double v = __dmul_rn(sum, inv);
+            const double dv = __dsub_rn(v, C[row + d]);
+            sq = __dadd_rn(sq, __dmul_rn(dv, dv));  // order-free: only bounds use it
+            C[row + d] = v;
+            Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
+            if (CT32) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+        if (lane == 0) delta[j] = __double2float_ru(__dsqrt_ru(sq * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+    }
+}
+
+// The fused form (LloydCtl::sum_fuse): the live half of this chunk buffer's sums.
+__device__ __forceinline__ void centroids_fused(const LloydCtl& c, int sum_sel, int k, int n, long long* tot,
+                                                int* rank) {
+    centroids_from_sums(c.sums + static_cast<uint64_t>(sum_sel) * c.sum_half, k, n, c.sum_unscale, c.cC, c.cmask,
+                        c.cCact, c.cldc, c.cact, c.cn_active, c.cCT32, c.cdelta, tot, rank);
+}
+
 template <typename T>
 __device__ __forceinline__ T raw_at(const unsigned char* raw, int p, int d) {
     if constexpr (sizeof(T) == 8) {  // 128-byte rows, SWIZZLE_128B: chunk ^= p & 7
@@ -1969,8 +2045,13 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
     if (ctl.go && !*ctl.go) return;
     if (ctl.begin_kind == 2 && ctl.st->begin_version ==
-                                   static_cast<long long>(*reinterpret_cast<const volatile long long*>(&ctl.gs->inc_version)))
-        return;  // the speculative begin of this chunk is current
+                                   static_cast<long long>(*reinterpret_cast<const volatile long long*>(&ctl.gs->inc_version))) {
+        // the speculative begin of this chunk is current; with the fused exact-sum
+        // update CTA 0 turns its sums into round 1's centroids
+        if (ctl.sum_fuse && blockIdx.x == 0)
+            centroids_fused(ctl, ctl.st->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
+        return;
+    }
     if (ctl.begin_kind == 1) {  // speculative begin: the incumbent version before any of its reads
         if (threadIdx.x == 0) {
             const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(&ctl.gs->inc_version));
@@ -2653,6 +2734,9 @@ fold:
         ktrace(5, hmode);
         if (ctl.host_st && (decision >= 0 || sst->incomplete)) status_to_host(sst, ctl.host_st);
         ktrace(30, hmode);
+        // fused exact-sum update: the next round's centroids when the loop goes on
+        if (ctl.sum_fuse && !sst->stop && !sst->state_error)
+            centroids_fused(ctl, sst->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
         if (tid == 0) klog_end(10 + hmode);
         return;
     }
@@ -3053,11 +3137,7 @@ __global__ void k_compact(const double* __restrict__ C, const uint8_t* __restric
     }
 }
 
-// Exact-sum mode update (update_centroids core.cpp:183-244 via §5b): the
-// label sums kept by the assignments give sum * (1.0/count) per (label, dim)
-// (:237-239), count 0 a degenerate row of 0.0; plus everything k_update's
-// merge writes (mask, active list, Cact, CT32, per-label movement).  One CTA,
-// a warp per label.
+// Exact-sum mode update as its own launch (the unfused form, BM_SUMS_FUSE=0).
 __global__ void __launch_bounds__(1024)
 k_centroids(const LloydStatus* __restrict__ st, const int* __restrict__ stop, const int* __restrict__ go,
             const long long* __restrict__ sums, uint64_t sum_half, double unscale, int k, int n,
@@ -3069,52 +3149,9 @@ k_centroids(const LloydStatus* __restrict__ st, const int* __restrict__ stop, co
     if (go && !*go) return;
     __shared__ long long tot[kSMaxK];
     __shared__ int rank[kSMaxK];
-    const long long* half = sums + static_cast<uint64_t>(st->sum_sel) * sum_half;
-    const long long* cnts = half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (warp == 0) {
-        long long c = 0;
-        if (lane < k)
-#pragma unroll
-            for (int q = 0; q < kSumCopies; ++q) c += __ldcg(cnts + q * kSMaxK + lane);
-        const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
-        if (lane < k) {
-            tot[lane] = c;
-            const int r = __popc(live & ((1u << lane) - 1u));
-            rank[lane] = c > 0 ? r : -1;
-            mask[lane] = c > 0 ? 0 : 1;
-            if (c > 0) act_idx[r] = lane;
-        }
-        if (lane == 0) *n_active = __popc(live);
-    }
-    __syncthreads();
-    for (int j = warp; j < k; j += blockDim.x / 32) {
-        const long long c = tot[j];
-        const uint64_t row = static_cast<uint64_t>(j) * n;
-        if (c <= 0) {
-            for (int d = lane; d < n; d += 32) C[row + d] = 0.0;
-            continue;
-        }
-        const double inv = __ddiv_rn(1.0, static_cast<double>(c));
-        const int rk = rank[j];
-        double sq = 0.0;
-        for (int d = lane; d < n; d += 32) {
-            long long s = 0;
-#pragma unroll
-            for (int q = 0; q < kSumCopies; ++q) s += __ldcg(half + (static_cast<uint64_t>(q) * kSMaxK * n) + row + d);
-            const double sum = __dmul_rn(static_cast<double>(s), unscale);  // exact (§5b)
-            const double v = __dmul_rn(sum, inv);
-            const double dv = __dsub_rn(v, C[row + d]);
-            sq = __dadd_rn(sq, __dmul_rn(dv, dv));  // order-free: only bounds use it
-            C[row + d] = v;
-            Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
-            if (CT32) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
-        if (lane == 0) delta[j] = __double2float_ru(__dsqrt_ru(sq * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
-    }
-    if (tid == 0) klog_end(1);
+    centroids_from_sums(sums + static_cast<uint64_t>(st->sum_sel) * sum_half, k, n, unscale, C, mask, Cact, ldc,
+                        act_idx, n_active, CT32, delta, tot, rank);
+    if (threadIdx.x == 0) klog_end(1);
 }
 
 // ===========================================================================
