@@ -642,6 +642,17 @@ bool narrow_storage() {
 }
 
 // BM_SCREEN=v4 selects the LDG-staged screen (A/B checks); default: TMA (v5).
+// BM_SPEC_CTAS: cap on the CTAs of a speculative begin, which then loop over its
+// blocks (default 0: one CTA per block; capping measured slower on c2).
+unsigned spec_ctas() {
+    static const unsigned v = [] {
+        const char* e = std::getenv("BM_SPEC_CTAS");
+        const long x = e ? std::atol(e) : 0;
+        return x > 0 ? (unsigned)x : ~0u;
+    }();
+    return v;
+}
+
 // BM_SUMS=0 disables the exact-sum update (kernels.cuh §5b) for A/B checks.
 bool exact_sums_enabled() {
     static const bool on = [] {
@@ -718,7 +729,10 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             }
             const CUtensorMap tmx = points_map<T>(P);
             fused_ctl = ctl && (tile_out || ctl->fast);
-            launch_pdl(dev::k_assign_tma<T>, grid, dev::kSThreads, shm, st,
+            // a speculative begin loops over its blocks with at most spec_ctas() CTAs
+            // (one per SM by default), leaving SM slots to the engine stream's rounds
+            const unsigned lgrid = fused_ctl && ctl->nblk ? std::min<unsigned>(grid, spec_ctas()) : grid;
+            launch_pdl(dev::k_assign_tma<T>, lgrid, dev::kSThreads, shm, st,
                 tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
                 S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                 g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
@@ -899,6 +913,7 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
         c.has_acc = 1;
     }
     c.accept_run = g->accept ? 1 : 0;
+    if (g->begin_kind == 1) c.nblk = (unsigned)ceil_div(w.R, dev::kABP);  // capped in CTAs (launch_assign)
     if (w.sums_on) {  // exact-sum mode: the begins fill a half, the rounds move points in the live one
         c.sums = w.sums_of(g->buf);
         c.sum_half = w.sum_half();

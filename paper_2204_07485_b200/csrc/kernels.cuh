@@ -119,7 +119,19 @@ __device__ __forceinline__ void klog_end(int id) {
     g_ktrace[200002 + 3 * i] = g_kstart[id];
     g_ktrace[200003 + 3 * i] = t;
 }
+// an early-exit launch (id + 10): CTA 0's exit time
+__device__ __forceinline__ void klog_exit(int id) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const unsigned long long i = atomicAdd(&g_ktrace[200000], 1ull) % 60000ull;
+        g_ktrace[200001 + 3 * i] = static_cast<unsigned long long>(id + 10);
+        g_ktrace[200002 + 3 * i] = g_kstart[id];
+        g_ktrace[200003 + 3 * i] = t;
+    }
+}
 #else
+__device__ __forceinline__ void klog_exit(int) {}
 __device__ __forceinline__ void ktrace(int, int = 0) {}
 __device__ __forceinline__ void ktrace_u(int) {}
 __device__ __forceinline__ void klog_start(int) {}
@@ -619,6 +631,7 @@ struct LloydCtl {
     // of the next round from the sums when the loop goes on (no k_centroids)
     int sum_fuse;
     double sum_unscale;
+    unsigned nblk;          // point blocks when the CTAs loop over them (0: one block per CTA)
     double* cC;
     uint8_t* cmask;
     double* cCact;
@@ -1650,12 +1663,12 @@ __device__ __forceinline__ long long sum_units(double x, double scale) {
 template <typename T>
 __device__ __noinline__ void label_sums(TmaSmem<T>& S, const LloydCtl& ctl, const T* __restrict__ X, uint64_t ld,
                                         int n, uint64_t p0, int np, bool full, int kfull, unsigned char* scratch,
-                                        size_t scratch_bytes) {
+                                        size_t scratch_bytes, unsigned blk) {
     __syncthreads();  // every point's (new, old) label recorded; the scratch area is free
     const int tid = threadIdx.x;
     const int which = ctl.sum_which >= 0 ? ctl.sum_which : ctl.st->sum_sel;
     // this CTA's copy: [kSumCopies][kSMaxK][n] sums, then [kSumCopies][kSMaxK] counts
-    const int cp = static_cast<int>(blockIdx.x % kSumCopies);
+    const int cp = static_cast<int>(blk % kSumCopies);
     long long* half = ctl.sums + static_cast<uint64_t>(which) * ctl.sum_half;
     long long* sg = half + static_cast<uint64_t>(cp) * kSMaxK * n;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n +
@@ -1738,7 +1751,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T>& S, const LloydCtl& ctl, cons
     const double sc = ctl.sum_scale;
     const bool grouped = full && ctl.parts;
     const uint64_t slot_len = static_cast<uint64_t>(kSMaxK) * n + kSMaxK;
-    long long* slot = grouped ? ctl.parts + blockIdx.x * slot_len : nullptr;
+    long long* slot = grouped ? ctl.parts + blk * slot_len : nullptr;
     const T* Xb = staged ? xs : X + p0 * ld;
     const uint64_t rs = staged ? static_cast<uint64_t>(vpr) * kV : ld;  // row stride of Xb
     for (int e = tid; e < kfull * n; e += blockDim.x) {
@@ -1769,7 +1782,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T>& S, const LloydCtl& ctl, cons
     if (tid < kfull) slot[static_cast<uint64_t>(kSMaxK) * n + tid] = pc[tid + 1] - pc[tid];
     __threadfence();
     __syncthreads();
-    const int g = static_cast<int>(blockIdx.x / 8);
+    const int g = static_cast<int>(blk / 8);
     const int pts_ctas = static_cast<int>((ctl.pts_rows + kABP - 1) / kABP);
     const int members = min(8, pts_ctas - 8 * g);
     if (tid == 0) flag[1] = atomicAdd(&ctl.grp_ctr[g], 1u) == static_cast<unsigned>(members) - 1;
@@ -2041,15 +2054,20 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     pdl_wait();
     if (stop_ptr && *stop_ptr) {  // a finished loop: close the WHILE node if this launch drives one
         if (ctl.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(ctl.cond, 0u);
+        klog_exit(10 + hmode);
         return;
     }
-    if (ctl.go && !*ctl.go) return;
+    if (ctl.go && !*ctl.go) {
+        klog_exit(10 + hmode);
+        return;
+    }
     if (ctl.begin_kind == 2 && ctl.st->begin_version ==
                                    static_cast<long long>(*reinterpret_cast<const volatile long long*>(&ctl.gs->inc_version))) {
         // the speculative begin of this chunk is current; with the fused exact-sum
         // update CTA 0 turns its sums into round 1's centroids
         if (ctl.sum_fuse && blockIdx.x == 0)
             centroids_fused(ctl, ctl.st->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
+        klog_exit(10 + hmode);
         return;
     }
     if (ctl.begin_kind == 1) {  // speculative begin: the incumbent version before any of its reads
@@ -2072,8 +2090,6 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     const int KG = (KA + kAK - 1) / kAK;
     const bool comp = warp < KG;
     const bool normw = warp == 7;
-    const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * kABP;
-    const int np = p0 < rows ? static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0)) : 0;
     const float finf = __int_as_float(0x7F800000);
     const int nslab = (n + kADC - 1) / kADC;
     // reusable block (pass-1 buffers) for the staged exact chains; item list at its end
@@ -2086,7 +2102,13 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                       offsetof(TmaSmem<T>, xs) + 2 * kSMaxK * 18 * sizeof(double),
                   "centroid staging of tma_chains overlaps the item list");
     ktrace(0, hmode);
-    int qb = 0;
+    int qb = 0;  // TMA slabs this CTA has consumed (ring position)
+    // one 128-point block per CTA, or (ctl.nblk: a speculative begin capped in
+    // CTAs so that it leaves SM slots to the engine stream) a loop over blocks
+    const unsigned nblk = ctl.nblk ? ctl.nblk : gridDim.x;
+    for (unsigned blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const uint64_t p0 = static_cast<uint64_t>(blk) * kABP;
+    const int np = p0 < rows ? static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0)) : 0;
     if (np == 0) {  // fixup CTA of a round-1 launch: one tile of the pending chunk's final distances
         const GState* gst = ctl.gs;
         const int pend = gst->pending_fix;
@@ -2476,6 +2498,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             }
         }
     }
+    qb += nslab;  // (the screen's slabs; a streamed recheck takes them again below)
     if (normw) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -2582,7 +2605,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             }
         }
         if (NI > static_cast<uint32_t>(kSThreads)) {
-            tma_chains<T>(S, &tmx, p0, n, nslab, qb + nslab, Cact, ldc, KA, NI, item_p, item_j, item_d);
+            tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, NI, item_p, item_j, item_d);
+            qb += nslab;
         } else {  // one item per thread, rows straight from L2
             __syncthreads();
             if (tid < static_cast<int>(NI))
@@ -2656,7 +2680,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
 fold:
     ktrace(10, hmode);
     if (ctl.sums && np > 0) label_sums<T>(S, ctl, X, ld, n, p0, np, labels_old == nullptr, kfull, reuse,
-                                          static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse));
+                                          static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse), blk);
     ktrace(31, hmode);
     if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
         __syncthreads();  // distances of this CTA written (some by other threads)
@@ -2670,6 +2694,55 @@ fold:
             double c = 0.0;
             for (int w = 0; w < kSThreads / 32; ++w) c += wsum[w];
             atomicAdd(&ctl.st->fsum, c);
+        }
+        if (blk + gridDim.x < nblk) {  // the next block's TMA loads land in buffers written generically
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+        }
+        continue;
+    }
+    if (!tile_out) return;
+    __syncthreads();
+    const uint64_t tile = p0 / kTile;
+    if (tid == 0) {
+        __threadfence();
+        const uint64_t tb = tile * kTile;
+        const unsigned ctas = static_cast<unsigned>((min(rows, tb + kTile) - tb + kABP - 1) / kABP);
+        const unsigned old = atomicAdd(&tile_counter[tile], 1u);
+        S.is_last = old == ctas - 1;
+    }
+    __syncthreads();
+    ktrace(11, hmode);
+    if (!S.is_last) return;
+    __threadfence();
+    const uint64_t tb = tile * kTile;
+    const int len = static_cast<int>(min(rows, tb + kTile) - tb);
+    double* fold = reinterpret_cast<double*>(&S.raw[0][0]);
+    for (int i = tid; i < len; i += kSThreads) fold[i] = __ldcg(dists_out + tb + i);
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0;
+        int i = 0;
+        for (; i + 8 <= len; i += 8) {
+            const double2 v0 = *reinterpret_cast<const double2*>(fold + i);
+            const double2 v1 = *reinterpret_cast<const double2*>(fold + i + 2);
+            const double2 v2 = *reinterpret_cast<const double2*>(fold + i + 4);
+            const double2 v3 = *reinterpret_cast<const double2*>(fold + i + 6);
+            a = __dadd_rn(a, v0.x); a = __dadd_rn(a, v0.y);
+            a = __dadd_rn(a, v1.x); a = __dadd_rn(a, v1.y);
+            a = __dadd_rn(a, v2.x); a = __dadd_rn(a, v2.y);
+            a = __dadd_rn(a, v3.x); a = __dadd_rn(a, v3.y);
+        }
+        for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
+        tile_out[tile] = a;
+        ktrace(12, hmode);
+        tile_counter[tile] = 0u;
+        tile_done_control(ctl, tile_out, rows);
+    }
+    }  // point blocks
+    if (!ctl.fast) return;
+    {
+        if (tid == 0) {  // this CTA's arrival (its blocks' sums are in st->fsum)
             __threadfence();
             const unsigned done = atomicAdd(&ctl.st->ctas_done, 1u);
             S.is_last = done == gridDim.x - 1;
@@ -2720,7 +2793,7 @@ fold:
         ktrace(1, hmode);
         if (tid == 0)
             S.n_items = static_cast<uint32_t>(
-                lloyd_fast_control(ctl, sst, rows, gridDim.x, KA, tail_acc ? &tin->gs : ctl.gs, fix_tiles));
+                lloyd_fast_control(ctl, sst, rows, nblk, KA, tail_acc ? &tin->gs : ctl.gs, fix_tiles));
         ktrace(2, hmode);
         __syncthreads();
         ktrace(29, hmode);
@@ -2739,44 +2812,6 @@ fold:
             centroids_fused(ctl, sst->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
         if (tid == 0) klog_end(10 + hmode);
         return;
-    }
-    if (!tile_out) return;
-    __syncthreads();
-    const uint64_t tile = p0 / kTile;
-    if (tid == 0) {
-        __threadfence();
-        const uint64_t tb = tile * kTile;
-        const unsigned ctas = static_cast<unsigned>((min(rows, tb + kTile) - tb + kABP - 1) / kABP);
-        const unsigned old = atomicAdd(&tile_counter[tile], 1u);
-        S.is_last = old == ctas - 1;
-    }
-    __syncthreads();
-    ktrace(11, hmode);
-    if (!S.is_last) return;
-    __threadfence();
-    const uint64_t tb = tile * kTile;
-    const int len = static_cast<int>(min(rows, tb + kTile) - tb);
-    double* fold = reinterpret_cast<double*>(&S.raw[0][0]);
-    for (int i = tid; i < len; i += kSThreads) fold[i] = __ldcg(dists_out + tb + i);
-    __syncthreads();
-    if (tid == 0) {
-        double a = 0.0;
-        int i = 0;
-        for (; i + 8 <= len; i += 8) {
-            const double2 v0 = *reinterpret_cast<const double2*>(fold + i);
-            const double2 v1 = *reinterpret_cast<const double2*>(fold + i + 2);
-            const double2 v2 = *reinterpret_cast<const double2*>(fold + i + 4);
-            const double2 v3 = *reinterpret_cast<const double2*>(fold + i + 6);
-            a = __dadd_rn(a, v0.x); a = __dadd_rn(a, v0.y);
-            a = __dadd_rn(a, v1.x); a = __dadd_rn(a, v1.y);
-            a = __dadd_rn(a, v2.x); a = __dadd_rn(a, v2.y);
-            a = __dadd_rn(a, v3.x); a = __dadd_rn(a, v3.y);
-        }
-        for (; i < len; ++i) a = __dadd_rn(a, fold[i]);
-        tile_out[tile] = a;
-        ktrace(12, hmode);
-        tile_counter[tile] = 0u;
-        tile_done_control(ctl, tile_out, rows);
     }
 }
 

@@ -31,7 +31,7 @@ lib.bm_debug_ktrace(buf.ctypes.data_as(_capi.P_u64), buf.size)
 n1 = int(buf[200000])
 st1 = buf[199990:199994].astype(np.int64)
 E = buf[200001:200001 + 3 * 60000].reshape(-1, 3).astype(np.int64)[n0 % 60000:n1 % 60000]
-names = {0: "guard", 1: "centroids", 2: "update", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)",
+names = {0: "guard", 1: "centroids", 2: "update", 21: "begin(exit)", 22: "round(exit)", 3: "accept", 10: "assign(h0)", 11: "assign(begin)", 12: "assign(round)",
          4: "accept:folded", 5: "accept:objective", 6: "accept:record", 7: "accept:ranks"}
 sub = E[(E[:, 0] >= 4) & (E[:, 0] <= 7)]
 E = E[(E[:, 0] < 4) | (E[:, 0] > 7)]
@@ -85,3 +85,10 @@ for base, title in ((400000, "begin"), (470000, "round")):
         if v.size:
             print(f"  {names_k[i]:13s} n={v.size:5d} p10={np.percentile(v, 10) / 1e3:7.2f} p50={np.percentile(v, 50) / 1e3:7.2f} "
                   f"p90={np.percentile(v, 90) / 1e3:7.2f} max={v.max() / 1e3:7.2f} us")
+
+# raw sequence of the last logged kernels (start / end, us from the first shown)
+if os.environ.get("KLOG_RAW"):
+    R = E[-int(os.environ["KLOG_RAW"]):]
+    t0 = R[0, 1]
+    for kid, a, b in R:
+        print(f"  raw {names.get(int(kid), kid):14s} {(a - t0) / 1e3:9.2f} {(b - t0) / 1e3:9.2f}")
