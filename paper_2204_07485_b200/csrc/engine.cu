@@ -653,6 +653,16 @@ unsigned spec_ctas() {
     return v;
 }
 
+// BM_FINAL=tma: the final pass through k_assign_tma (one 128-point block per
+// CTA) instead of the streaming k_final.
+bool final_streaming() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_FINAL");
+        return !(e && std::string(e) == "tma");
+    }();
+    return on;
+}
+
 // BM_SUMS=0 disables the exact-sum update (kernels.cuh §5b) for A/B checks.
 bool exact_sums_enabled() {
     static const bool on = [] {
@@ -1323,8 +1333,34 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
     P.X = static_cast<const uint8_t*>(d->X) + r0 * d->ld * dtype_size(d->dtype);
     P.rows = r1 - r0;
     c.ensure_final(P.rows);
-    launch_assign(st, P, w, w.k, c.flabels.p, 0, nullptr, c.fdists.p, nullptr, nullptr, true, c.ftiles.p,
-                  c.fctr.p);
+    if (final_streaming() && screen_enabled(w.k) && P.n <= dev::kFMaxD && tma_screen() && P.rows < (1ull << 31)) {
+        // streaming form (k_final): persistent CTAs, one continuous TMA ring; then the tile partials
+        PhaseScope ps(PH_FINAL, P.rows);
+        dispatch(P.dtype, [&](auto tag) {
+            using T = decltype(tag);
+            constexpr size_t shm = dev::final_smem_bytes<T>();
+            static bool attr_set = false;  // per template instance
+            if (!attr_set) {
+                BM_CUDA(cudaFuncSetAttribute(dev::k_final<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+                attr_set = true;
+            }
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+            const uint64_t blocks = ceil_div(P.rows, dev::kABP);
+            const unsigned grid = (unsigned)std::min<uint64_t>(blocks, 2ull * (uint64_t)sms);
+            const CUtensorMap tmx = points_map<T>(P);
+            launch_pdl(dev::k_final<T>, grid, dev::kSThreads, shm, st, tmx, static_cast<const T*>(P.X), P.rows, P.n,
+                       P.ld, (const double*)w.Cact.p, w.ldc, (const int*)w.act.p, (const int*)&w.gs.p->n_active,
+                       (const float*)w.CT32.p, c.flabels.p, c.fdists.p, g_profiling ? g_prof.d_cand : nullptr,
+                       screen_consts(P.n));
+        });
+        BM_LAUNCH();
+        count_launch();
+        launch_tile_sums(st, c.fdists.p, P.rows, 0, 1, c.ftiles.p, nullptr);
+    } else {
+        launch_assign(st, P, w, w.k, c.flabels.p, 0, nullptr, c.fdists.p, nullptr, nullptr, true, c.ftiles.p,
+                      c.fctr.p);
+    }
     BM_CUDA(cudaMemcpyAsync(tiles_host, c.ftiles.p, tiles_of(P.rows) * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (labels_host)
         BM_CUDA(cudaMemcpyAsync(labels_host, c.flabels.p, P.rows * sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -2815,6 +2815,307 @@ fold:
     }
 }
 
+// ---------------------------------------------------------------------------
+// 3d. Final full-data pass (big_means.cpp:102-107: assign_nearest over all m
+// rows), throughput form.  Same certified screen and exact recheck as
+// k_assign_tma (identical labels and distances, bit for bit), organised for
+// HBM streaming instead of latency: persistent CTAs (2 per SM) walk their
+// 128-point blocks through ONE continuous TMA ring of 16-dim slabs (kFS
+// stages), so the next block's slabs are in flight while the current block
+// does its bounds, candidates and exact rechecks; the fp32 centroids and their
+// norms are staged once per CTA.  Rows up to kFMaxD dims; the tile partials of
+// block_sum come from k_tile_sums afterwards.
+// ---------------------------------------------------------------------------
+constexpr int kFMaxD = 80;  // dims of the streaming final pass (5 slabs; c1-c3)
+template <typename T>
+struct FinalSmem {
+    static constexpr int kNS = sizeof(T) == 4 ? 4 : 3;           // ring stages
+    static constexpr int kRawBytes = kABP * kADC * sizeof(T);   // one swizzled slab
+    alignas(1024) unsigned char raw[kNS][kRawBytes];
+    // fp32 points [d][p]: the whole block (exact copies of fp32 storage, so the
+    // exact recheck reads its rows from here; fp64 storage rechecks from L2)
+    alignas(16) float xs[kFMaxD][kABP];
+    alignas(16) float ct[kFMaxD][kSMaxK];                       // fp32 centroids [d][j]
+    float red_u[8][kABP];
+    float nx_lo[kABP], nx_hi[kABP], nxr[kABP];
+    float nc_lo[kSMaxK], nc_hi[kSMaxK], ncr[kSMaxK];
+    unsigned cand[kABP];
+    int icount[kABP];
+    double item_d[kItemCap];
+    short item_p[kItemCap];
+    signed char item_j[kItemCap];
+    uint64_t bar[kNS];
+    uint32_t n_items;
+};
+
+template <typename T>
+constexpr size_t final_smem_bytes() { return sizeof(FinalSmem<T>) + 1024; }
+
+template <typename T>
+__global__ void __launch_bounds__(kSThreads, 2)
+k_final(const __grid_constant__ CUtensorMap tmx, const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+        const double* __restrict__ Cact, int ldc, const int* __restrict__ act_idx, const int* __restrict__ n_active_ptr,
+        const float* __restrict__ CT32, int32_t* __restrict__ labels_out, double* __restrict__ dists_out,
+        unsigned long long* __restrict__ cand_counter, ScreenConsts cst) {
+    extern __shared__ __align__(16) unsigned char fsm_raw[];
+    unsigned char* fsm_al = fsm_raw + ((1024u - (smem_u32(fsm_raw) & 1023u)) & 1023u);
+    FinalSmem<T>& S = *reinterpret_cast<FinalSmem<T>*>(fsm_al);
+    constexpr int NS = FinalSmem<T>::kNS;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int KA = *n_active_ptr;
+    const int KG = (KA + kAK - 1) / kAK;
+    const bool comp = warp < KG;
+    const bool normw = warp == 7;
+    const float finf = __int_as_float(0x7F800000);
+    const int nslab = (n + kADC - 1) / kADC;
+    const uint64_t nblk_all = (rows + kABP - 1) / kABP;
+    const uint64_t my_blocks = blockIdx.x < nblk_all ? (nblk_all - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t total_q = my_blocks * nslab;  // slabs this CTA streams, in order
+    auto issue = [&](uint64_t q) {               // thread 0: slab q of this CTA's sequence
+        const int st = static_cast<int>(q % NS);
+        const uint64_t b = blockIdx.x + (q / nslab) * gridDim.x;
+        const int sl = static_cast<int>(q % nslab);
+        mbar_expect_tx(&S.bar[st], FinalSmem<T>::kRawBytes);
+        tma_load_2d(S.raw[st], &tmx, &S.bar[st], sl * kADC, static_cast<int>(b * kABP));
+    };
+    if (tid == 0) {
+        tma_prefetch_map(&tmx);
+        for (int i = 0; i < NS; ++i) mbar_init(&S.bar[i], 1);
+        fence_mbar_init();
+        for (uint64_t q = 0; q < static_cast<uint64_t>(NS) && q < total_q; ++q) issue(q);
+    }
+    // the fp32 centroids [d][j] and their norms (rounded down / up), once
+    for (int e = tid; e < n * kSMaxK; e += kSThreads) S.ct[e / kSMaxK][e % kSMaxK] = CT32[e];
+    __syncthreads();
+    if (tid < kSMaxK) {
+        float ncl = 0.f, nch = 0.f;
+        for (int d = 0; d < n; ++d) {
+            const float c = S.ct[d][tid];
+            ncl = __fmaf_rd(c, c, ncl);
+            nch = __fmaf_ru(c, c, nch);
+        }
+        S.nc_lo[tid] = ncl;
+        S.nc_hi[tid] = nch;
+        S.ncr[tid] = __fsqrt_ru(nch);
+    }
+    __syncthreads();
+    uint64_t q = 0;
+    const int cp_ = tid & (kABP - 1), chalf = tid >> 7;  // conversion: point, 8-dim half
+    for (uint64_t bi = 0; bi < my_blocks; ++bi) {
+        __syncthreads();  // the previous block's rows in xs are no longer read
+        const uint64_t p0 = (blockIdx.x + bi * gridDim.x) * kABP;
+        const int np = static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0));
+        float2 tot[2][kAK];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < kAK; ++u) tot[h][u] = make_float2(0.f, 0.f);
+        float nxl[4] = {0.f, 0.f, 0.f, 0.f}, nxh[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int sl = 0; sl < nslab; ++sl, ++q) {
+            const int st = static_cast<int>(q % NS);
+            const int d0 = sl * kADC;
+            const int dl = min(kADC, n - d0);
+            mbar_wait(&S.bar[st], static_cast<unsigned>((q / NS) & 1));
+            float(*xsl)[kABP] = &S.xs[d0];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int d = 8 * chalf + i;
+                if (d0 + d < kFMaxD) xsl[d][cp_] = static_cast<float>(raw_at<T>(S.raw[st], cp_, d));
+            }
+            __syncthreads();  // slab converted; stage st is free
+            if (tid == 0 && q + NS < total_q) issue(q + NS);
+            if (comp) {
+                float2 part[2][kAK];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int u = 0; u < kAK; ++u) part[h][u] = make_float2(0.f, 0.f);
+                auto step = [&](int d) {
+                    const float4 xv = *reinterpret_cast<const float4*>(&xsl[d][4 * lane]);
+                    const float4 cv = *reinterpret_cast<const float4*>(&S.ct[d0 + d][4 * warp]);
+                    const float2 xa = make_float2(xv.x, xv.y), xb2 = make_float2(xv.z, xv.w);
+                    part[0][0] = ffma2(xa, cv.x, part[0][0]);
+                    part[0][1] = ffma2(xa, cv.y, part[0][1]);
+                    part[0][2] = ffma2(xa, cv.z, part[0][2]);
+                    part[0][3] = ffma2(xa, cv.w, part[0][3]);
+                    part[1][0] = ffma2(xb2, cv.x, part[1][0]);
+                    part[1][1] = ffma2(xb2, cv.y, part[1][1]);
+                    part[1][2] = ffma2(xb2, cv.z, part[1][2]);
+                    part[1][3] = ffma2(xb2, cv.w, part[1][3]);
+                };
+                if (dl == kADC) {
+#pragma unroll
+                    for (int d = 0; d < kADC; ++d) step(d);
+                } else {
+                    for (int d = 0; d < dl; ++d) step(d);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int u = 0; u < kAK; ++u) tot[h][u] = fadd2(tot[h][u], part[h][u]);
+            }
+            if (normw) {
+                for (int d = 0; d < dl; ++d) {
+                    const float4 xv = *reinterpret_cast<const float4*>(&xsl[d][4 * lane]);
+                    nxl[0] = __fmaf_rd(xv.x, xv.x, nxl[0]); nxh[0] = __fmaf_ru(xv.x, xv.x, nxh[0]);
+                    nxl[1] = __fmaf_rd(xv.y, xv.y, nxl[1]); nxh[1] = __fmaf_ru(xv.y, xv.y, nxh[1]);
+                    nxl[2] = __fmaf_rd(xv.z, xv.z, nxl[2]); nxh[2] = __fmaf_ru(xv.z, xv.z, nxh[2]);
+                    nxl[3] = __fmaf_rd(xv.w, xv.w, nxl[3]); nxh[3] = __fmaf_ru(xv.w, xv.w, nxh[3]);
+                }
+            }
+        }
+        if (normw) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                S.nx_lo[4 * lane + qq] = nxl[qq];
+                S.nx_hi[4 * lane + qq] = nxh[qq];
+                S.nxr[4 * lane + qq] = __fsqrt_ru(nxh[qq]);
+            }
+        }
+        if (tid < kABP) S.cand[tid] = 0u;
+        __syncthreads();
+        // certified bounds (as k_assign_tma): upper bounds first, then each warp
+        // tests its lower bounds against the point's minimum U
+        float Lk[4][kAK];
+        if (comp) {
+            float un[4] = {finf, finf, finf, finf};
+#pragma unroll
+            for (int u = 0; u < kAK; ++u) {
+                const int j = kAK * warp + u;
+                const float cl = j < KA ? S.nc_lo[j] : 0.f, ch = j < KA ? S.nc_hi[j] : 0.f;
+                const float crr = j < KA ? S.ncr[j] : 0.f;
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    const int p = 4 * lane + qq;
+                    const float sdot = qq & 1 ? tot[qq >> 1][u].y : tot[qq >> 1][u].x;
+                    const float t2 = 2.f * sdot;
+                    const float Sn = __fadd_ru(S.nxr[p], crr);
+                    const float Al = __fadd_rd(S.nx_lo[p], cl), Ah = __fadd_ru(S.nx_hi[p], ch);
+                    float L = 0.f, U = finf;
+                    if (fabsf(t2) <= 1.0e37f && Sn <= 1.0e18f && Ah <= 1.0e37f) {
+                        const float D = __fadd_ru(__fmul_ru(__fmul_ru(cst.K, Sn), Sn), cst.dabs);
+                        L = fmaxf(__fsub_rd(__fsub_rd(Al, t2), D), 0.f);
+                        L = __fmul_rd(L, cst.lo64);
+                        U = __fmul_ru(__fadd_ru(__fsub_ru(Ah, t2), D), cst.hi64);
+                    }
+                    Lk[qq][u] = j < KA ? L : finf;
+                    if (j < KA) un[qq] = fminf(un[qq], U);
+                }
+            }
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) S.red_u[warp][4 * lane + qq] = un[qq];
+        }
+        __syncthreads();
+        if (comp) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int p = 4 * lane + qq;
+                float m = finf;
+                for (int g = 0; g < KG; ++g) m = fminf(m, S.red_u[g][p]);
+                unsigned bits = 0;
+#pragma unroll
+                for (int u = 0; u < kAK; ++u)
+                    if (kAK * warp + u < KA && Lk[qq][u] <= m) bits |= 1u << (kAK * warp + u);
+                if (bits && p < np) atomicOr(&S.cand[p], bits);
+            }
+        }
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of the candidate counts -> item offsets
+            int v[4], run = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                v[qq] = __popc(S.cand[4 * tid + qq]);
+                run += v[qq];
+            }
+            int incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            int ex = incl - run;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                S.icount[4 * tid + qq] = ex;
+                ex += v[qq];
+            }
+            if (tid == 31) {
+                S.n_items = static_cast<uint32_t>(incl);
+                if (cand_counter) {
+                    atomicAdd(cand_counter, static_cast<unsigned long long>(incl));
+                    atomicAdd(cand_counter + 1, static_cast<unsigned long long>(np));
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t NI = S.n_items;
+        const bool overflow = NI > static_cast<uint32_t>(kItemCap);
+        // exact fp64 recheck of the candidates (core.cpp:142-146), rows from L2
+        if (!overflow) {
+            if (tid < np) {
+                uint32_t it = S.icount[tid];
+                unsigned bits = S.cand[tid];
+                while (bits) {  // ascending j
+                    const int j = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    S.item_p[it] = static_cast<short>(tid);
+                    S.item_j[it] = static_cast<signed char>(j);
+                    ++it;
+                }
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < NI; i += kSThreads) {
+                const int p = S.item_p[i];
+                const double* c = Cact + static_cast<uint64_t>(S.item_j[i]) * ldc;
+                if constexpr (sizeof(T) == 4) {  // the row from shared memory (exact fp32 copies)
+                    double a = 0.0;
+                    int d = 0;
+#pragma unroll 4
+                    for (; d + 2 <= n; d += 2) {
+                        const double2 cv = __ldg(reinterpret_cast<const double2*>(c + d));
+                        a = dist_step(a, S.xs[d][p], cv.x);
+                        a = dist_step(a, S.xs[d + 1][p], cv.y);
+                    }
+                    for (; d < n; ++d) a = dist_step(a, S.xs[d][p], c[d]);
+                    S.item_d[i] = a;
+                } else {
+                    S.item_d[i] = exact_row_dist(X + (p0 + p) * ld, c, n);
+                }
+            }
+            __syncthreads();
+        }
+        if (tid < np) {
+            const int p = tid;
+            const uint64_t gp = p0 + p;
+            double best = __longlong_as_double(0x7FF0000000000000LL);
+            int bj = -1;
+            if (!overflow) {  // ascending j, strict < (core.cpp:147)
+                const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(S.icount[p + 1]) : NI;
+                for (uint32_t i = S.icount[p]; i < b1; ++i) {
+                    if (S.item_d[i] < best) {
+                        best = S.item_d[i];
+                        bj = S.item_j[i];
+                    }
+                }
+            } else {  // candidate sets too large for the item buffer: full exact scan
+                const T* x = X + gp * ld;
+                for (int j = 0; j < KA; ++j) {
+                    const double* c = Cact + static_cast<uint64_t>(j) * ldc;
+                    double sm = 0.0;
+                    for (int d = 0; d < n; ++d) sm = dist_step(sm, to_f64(x[d]), c[d]);
+                    if (sm < best) {
+                        best = sm;
+                        bj = j;
+                    }
+                }
+            }
+            labels_out[gp] = bj >= 0 ? act_idx[bj] : -1;
+            dists_out[gp] = best;
+        }
+        __syncthreads();  // cand / icount / items of this block consumed
+    }
+}
+
 template <typename T>
 constexpr size_t tma_smem_bytes() { return sizeof(TmaSmem<T>) + 1024; }
 
