@@ -171,6 +171,23 @@ bm_status bm_kmeans_pp(const bm_dataset* data, uint64_t k, int32_t candidates_pe
                        uint64_t seed, uint64_t max_iterations, double rel_tolerance,
                        bm_outcome* out);
 
+/* InitConfig init.hpp:16-27: method 0 forgy, 1 kmeans_pp, 2 kmeans_parallel
+ * (InitMethod); rounds_rule 0 fixed, 1 log_phi (RoundsRule). */
+typedef struct {
+    int32_t method;
+    int32_t candidates_per_step; /* 3 */
+    int32_t oversampling_l;      /* 0: 2k */
+    int32_t rounds_r;            /* 5 */
+    int32_t rounds_rule;
+    uint64_t seed;
+} bm_init_config;
+
+/* kmeans local_search.hpp:44 / local_search.cpp:62-94 with any InitMethod:
+ * forgy_init (init.cpp:92-115), kmeanspp_fill (:123-201) or
+ * kmeans_parallel_init (:209-347), then lloyd.  out->labels may be NULL. */
+bm_status bm_kmeans(const bm_dataset* data, uint64_t k, const bm_init_config* init,
+                    uint64_t max_iterations, double rel_tolerance, bm_outcome* out);
+
 /* big_means big_means.hpp:56-57 / big_means.cpp:58-112.  trace may be NULL;
  * at most trace_capacity records are written, out->chunks holds the count. */
 bm_status bm_big_means(bm_dataset* data, const bm_config* cfg, bm_outcome* out,

@@ -481,3 +481,200 @@ int orc_kmeans_pp(const double* X, uint64_t m, uint64_t n, uint64_t k, int candi
     out->chunks = 1;
     return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * forgy_init init.cpp:92-115: partial Fisher-Yates over the row indices; the
+ * first k slots (in slot order) are the centroids.  No distance evaluations.
+ * ------------------------------------------------------------------------- */
+int orc_forgy_init(const double* X, uint64_t m, uint64_t n, uint64_t k, orc_rng* r, double* C) {
+    if (k < 1 || m < k) return ORC_CONFIG_ERROR; /* :95-100 */
+    uint64_t* idx = (uint64_t*)malloc(m * sizeof(uint64_t));
+    for (uint64_t i = 0; i < m; ++i) idx[i] = i; /* :101-102 */
+    for (uint64_t i = 0; i < k; ++i) {          /* :104-107 */
+        const uint64_t j = orc_uniform_int(r, i, m - 1);
+        const uint64_t t = idx[i];
+        idx[i] = idx[j];
+        idx[j] = t;
+    }
+    for (uint64_t i = 0; i < k; ++i) memcpy(C + i * n, X + idx[i] * n, n * sizeof(double)); /* :108-113 */
+    free(idx);
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * kmeans_parallel_init init.cpp:209-347.
+ * ------------------------------------------------------------------------- */
+int orc_kmeans_parallel_init(const double* X, uint64_t m, uint64_t n, uint64_t k, const orc_init* cfg,
+                             orc_rng* r, double* C, uint64_t* evals) {
+    if (k < 1 || m < k) return ORC_CONFIG_ERROR;       /* :213-218 */
+    const uint64_t first = orc_uniform_int(r, 0, m - 1); /* :220-221 */
+    if (k == 1) {                                        /* :222-225 */
+        memcpy(C, X + first * n, n * sizeof(double));
+        return ORC_OK;
+    }
+    const double l = cfg->oversampling_l > 0 ? (double)cfg->oversampling_l : 2.0 * (double)k; /* :227-228 */
+    uint64_t cap = 1024, nc = 0;
+    uint64_t* cand = (uint64_t*)malloc(cap * sizeof(uint64_t));
+    cand[nc++] = first;
+    double* dist2 = (double*)malloc(m * sizeof(double));
+    distances_to_row(X, m, n, X + first * n, dist2, evals); /* :232 */
+    int rounds = cfg->rounds_r;                             /* :234-238 */
+    if (cfg->rounds_rule == 1) {
+        const double phi1 = orc_block_sum(dist2, m);
+        rounds = phi1 > 1.0 ? (int)floor(log(phi1)) : 1;
+        if (rounds < 1) rounds = 1;
+    }
+    if (rounds < 1) { /* :239-241 */
+        free(cand);
+        free(dist2);
+        return ORC_CONFIG_ERROR;
+    }
+    uint64_t* fresh = (uint64_t*)malloc(m * sizeof(uint64_t));
+    for (int round = 0; round < rounds; ++round) { /* :244-263 */
+        const double phi = orc_block_sum(dist2, m);
+        if (phi <= 0.0) break;
+        uint64_t nf = 0;
+        for (uint64_t i = 0; i < m; ++i) { /* one draw per point, index order :251-258 */
+            const double u = orc_uniform_real(r, 0.0, 1.0);
+            double p = l * dist2[i] / phi;
+            if (p > 1.0) p = 1.0; /* std::min(1.0, .) */
+            if (u < p) fresh[nf++] = i;
+        }
+        for (uint64_t f = 0; f < nf; ++f) { /* :259-262 */
+            if (nc == cap) {
+                cap *= 2;
+                cand = (uint64_t*)realloc(cand, cap * sizeof(uint64_t));
+            }
+            cand[nc++] = fresh[f];
+            lower_to_row(X, m, n, X + fresh[f] * n, dist2, evals);
+        }
+    }
+    free(fresh);
+    if (nc < k) { /* top-up with distinct uniform rows :266-278 */
+        uint8_t* used = (uint8_t*)calloc(m, 1);
+        for (uint64_t i = 0; i < nc; ++i) used[cand[i]] = 1;
+        if (cap < k) {
+            cap = k;
+            cand = (uint64_t*)realloc(cand, cap * sizeof(uint64_t));
+        }
+        while (nc < k) {
+            const uint64_t i = orc_uniform_int(r, 0, m - 1);
+            if (!used[i]) {
+                used[i] = 1;
+                cand[nc++] = i;
+            }
+        }
+        free(used);
+    }
+    /* the candidate set (data.gather :280) and its weights: points nearest each :287-295 */
+    double* cr = (double*)malloc(nc * n * sizeof(double));
+    for (uint64_t q = 0; q < nc; ++q) memcpy(cr + q * n, X + cand[q] * n, n * sizeof(double));
+    uint8_t* cmask = (uint8_t*)calloc(nc, 1);
+    int32_t* lab = (int32_t*)malloc(m * sizeof(int32_t));
+    double* dd = (double*)malloc(m * sizeof(double));
+    int rc = orc_assign_nearest(X, m, n, cr, cmask, nc, lab, dd, evals);
+    double* weight = (double*)calloc(nc, sizeof(double));
+    if (rc == ORC_OK)
+        for (uint64_t i = 0; i < m; ++i) weight[lab[i]] += 1.0;
+    free(lab);
+    free(dd);
+    free(cmask);
+    if (rc != ORC_OK) {
+        free(cand);
+        free(dist2);
+        free(cr);
+        free(weight);
+        return rc;
+    }
+    /* weighted greedy k-means++ over the candidates :297-339 */
+    double* wcum = (double*)malloc(nc * sizeof(double));
+    prefix_sums(weight, nc, wcum);
+    const uint64_t chosen_first = pick_by_mass(wcum, nc, orc_uniform_real(r, 0.0, wcum[nc - 1]));
+    uint64_t* chosen = (uint64_t*)malloc(k * sizeof(uint64_t));
+    uint64_t nch = 0;
+    chosen[nch++] = chosen_first;
+    double* cdist2 = (double*)malloc(nc * sizeof(double));
+    distances_to_row(cr, nc, n, cr + chosen_first * n, cdist2, evals);
+    const int candidates = cfg->candidates_per_step > 1 ? cfg->candidates_per_step : 1;
+    double* mass = (double*)malloc(nc * sizeof(double));
+    double* cum = (double*)malloc(nc * sizeof(double));
+    double* trial = (double*)malloc(nc * sizeof(double));
+    double* best_trial = (double*)malloc(nc * sizeof(double));
+    while (nch < k) {
+        for (uint64_t q = 0; q < nc; ++q) mass[q] = weight[q] * cdist2[q];
+        prefix_sums(mass, nc, cum);
+        const double total = cum[nc - 1];
+        if (total <= 0.0) { /* :318-322 */
+            chosen[nch++] = orc_uniform_int(r, 0, nc - 1);
+            continue;
+        }
+        double best_potential = INFINITY;
+        uint64_t best_index = 0;
+        for (int c = 0; c < candidates; ++c) { /* :323-336 */
+            const uint64_t index = pick_by_mass(cum, nc, orc_uniform_real(r, 0.0, total));
+            distances_to_row(cr, nc, n, cr + index * n, trial, evals);
+            double potential = 0.0;
+            for (uint64_t q = 0; q < nc; ++q) {
+                if (cdist2[q] < trial[q]) trial[q] = cdist2[q]; /* std::min(trial, cdist2) */
+                potential += weight[q] * trial[q];
+            }
+            if (potential < best_potential) {
+                best_potential = potential;
+                best_index = index;
+                double* t = trial;
+                trial = best_trial;
+                best_trial = t;
+            }
+        }
+        chosen[nch++] = best_index;
+        double* t = cdist2; /* std::swap(cdist2, best_trial) :338 */
+        cdist2 = best_trial;
+        best_trial = t;
+    }
+    for (uint64_t j = 0; j < k; ++j) memcpy(C + j * n, cr + chosen[j] * n, n * sizeof(double)); /* :341-346 */
+    free(cand);
+    free(dist2);
+    free(cr);
+    free(weight);
+    free(wcum);
+    free(chosen);
+    free(cdist2);
+    free(mass);
+    free(cum);
+    free(trial);
+    free(best_trial);
+    return ORC_OK;
+}
+
+/* kmeans local_search.cpp:62-94: init per method (seeded by init.seed), then lloyd. */
+int orc_kmeans(const double* X, uint64_t m, uint64_t n, uint64_t k, const orc_init* init,
+               uint64_t max_iterations, double rel_tolerance, double* C, uint8_t* mask, int32_t* labels,
+               orc_outcome* out) {
+    if (k < 1 || m < k) return ORC_CONFIG_ERROR; /* :64-69 */
+    memset(out, 0, sizeof(*out));
+    orc_rng* rng = (orc_rng*)malloc(sizeof(orc_rng));
+    orc_rng_seed(rng, init->seed); /* :71 */
+    for (uint64_t i = 0; i < k * n; ++i) C[i] = 0.0;
+    for (uint64_t j = 0; j < k; ++j) mask[j] = 1;
+    uint64_t init_evals = 0;
+    int rc = ORC_CONFIG_ERROR;
+    if (init->method == 0) {
+        rc = orc_forgy_init(X, m, n, k, rng, C);
+        if (rc == ORC_OK) memset(mask, 0, k);
+    } else if (init->method == 1) {
+        rc = orc_kmeanspp_fill(X, m, n, C, mask, k, init->candidates_per_step, rng, &init_evals);
+    } else if (init->method == 2) {
+        rc = orc_kmeans_parallel_init(X, m, n, k, init, rng, C, &init_evals);
+        if (rc == ORC_OK) memset(mask, 0, k);
+    }
+    free(rng);
+    if (rc != ORC_OK) return rc;
+    orc_lloyd_out lo;
+    rc = orc_lloyd(X, m, n, C, mask, k, max_iterations, rel_tolerance, labels, NULL, 0, &lo);
+    if (rc != ORC_OK) return rc;
+    out->objective = lo.objective;
+    out->iterations = lo.iterations;
+    out->evals = lo.evals + init_evals;
+    out->chunks = 1;
+    return ORC_OK;
+}

@@ -112,6 +112,29 @@ int orc_kmeans_pp(const double* X, uint64_t m, uint64_t n, uint64_t k, int candi
                   uint64_t seed, uint64_t max_iterations, double rel_tolerance, double* C,
                   uint8_t* mask, int32_t* labels, orc_outcome* out);
 
+/* InitConfig (init.hpp:16-27): method 0 forgy, 1 kmeans_pp, 2 kmeans_parallel;
+ * rounds_rule 0 fixed, 1 log_phi. */
+typedef struct {
+    int method;
+    int candidates_per_step;
+    int oversampling_l;
+    int rounds_r;
+    int rounds_rule;
+    uint64_t seed;
+} orc_init;
+
+/* forgy_init init.cpp:92-115: k distinct rows by partial Fisher-Yates. */
+int orc_forgy_init(const double* X, uint64_t m, uint64_t n, uint64_t k, orc_rng* r, double* C);
+
+/* kmeans_parallel_init init.cpp:209-347 (all k rows active on return). */
+int orc_kmeans_parallel_init(const double* X, uint64_t m, uint64_t n, uint64_t k, const orc_init* cfg,
+                             orc_rng* r, double* C, uint64_t* evals);
+
+/* kmeans local_search.cpp:62-94, any init method. */
+int orc_kmeans(const double* X, uint64_t m, uint64_t n, uint64_t k, const orc_init* init,
+               uint64_t max_iterations, double rel_tolerance, double* C, uint8_t* mask, int32_t* labels,
+               orc_outcome* out);
+
 #ifdef __cplusplus
 }
 #endif

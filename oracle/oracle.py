@@ -36,6 +36,11 @@ class OracleError(RuntimeError):
         self.code = code
 
 
+class _Init(C.Structure):  # orc_init / ref_init (InitConfig init.hpp:16-27)
+    _fields_ = [("method", C.c_int), ("candidates_per_step", C.c_int), ("oversampling_l", C.c_int),
+                ("rounds_r", C.c_int), ("rounds_rule", C.c_int), ("seed", C.c_uint64)]
+
+
 class _RefConfig(C.Structure):
     _fields_ = [("k", _u64), ("chunk_size", _u64), ("has_max_chunks", C.c_int),
                 ("max_chunks", _u64), ("has_max_cpu_seconds", C.c_int),
@@ -269,6 +274,43 @@ class Oracle:
                                           _u64(max_iterations), C.c_double(rel_tolerance),
                                           _p(Cn, _dp), _p(mask, _u8p), _p(labels, _i32p),
                                           C.byref(out)))
+        return BigMeansResult(Cn, mask, labels, float(out.objective), int(out.evals),
+                              int(out.iterations), 1)
+
+    # -- kmeans drivers with every InitMethod (init.hpp:8; local_search.cpp:62-94) --
+    def _init(self, method, seed, candidates, oversampling_l, rounds_r, rounds_rule):
+        return _Init(int(method), int(candidates), int(oversampling_l), int(rounds_r), int(rounds_rule),
+                     _u64(seed))
+
+    def forgy_init(self, X, k, r):
+        X = _f64(X)
+        m, n = X.shape
+        Cn = np.empty((k, n), np.float64)
+        self._check(self._fn("forgy_init")(_p(X, _dp), _u64(m), _u64(n), _u64(k), r, _p(Cn, _dp)))
+        return Cn
+
+    def kmeans_parallel_init(self, X, k, r, candidates=3, oversampling_l=0, rounds_r=5, rounds_rule=0):
+        X = _f64(X)
+        m, n = X.shape
+        Cn = np.empty((k, n), np.float64)
+        cfg = self._init(2, 0, candidates, oversampling_l, rounds_r, rounds_rule)
+        ev = _u64(0)
+        self._check(self._fn("kmeans_parallel_init")(_p(X, _dp), _u64(m), _u64(n), _u64(k), C.byref(cfg), r,
+                                                     _p(Cn, _dp), C.byref(ev)))
+        return Cn, int(ev.value)
+
+    def kmeans(self, X, k, method, seed, candidates=3, oversampling_l=0, rounds_r=5, rounds_rule=0,
+               max_iterations=300, rel_tolerance=1e-4):
+        X = _f64(X)
+        m, n = X.shape
+        Cn = np.empty((k, n), np.float64)
+        mask = np.empty(k, np.uint8)
+        labels = np.empty(m, np.int32)
+        cfg = self._init(method, seed, candidates, oversampling_l, rounds_r, rounds_rule)
+        out = _PortOutcome() if self.kind == "port" else _RefOutcome()
+        self._check(self._fn("kmeans")(_p(X, _dp), _u64(m), _u64(n), _u64(k), C.byref(cfg),
+                                       _u64(max_iterations), C.c_double(rel_tolerance), _p(Cn, _dp),
+                                       _p(mask, _u8p), _p(labels, _i32p), C.byref(out)))
         return BigMeansResult(Cn, mask, labels, float(out.objective), int(out.evals),
                               int(out.iterations), 1)
 

@@ -241,4 +241,65 @@ int ref_kmeans_pp(const double* X, uint64_t m, uint64_t n, uint64_t k, int candi
     });
 }
 
+struct ref_init {  // InitConfig init.hpp:16-27 (method / rounds_rule as their enum values)
+    int method;
+    int candidates_per_step;
+    int oversampling_l;
+    int rounds_r;
+    int rounds_rule;
+    uint64_t seed;
+};
+
+static InitConfig to_init(const ref_init* c) {
+    InitConfig init;
+    init.method = static_cast<InitMethod>(c->method);
+    init.candidates_per_step = c->candidates_per_step;
+    init.oversampling_l = c->oversampling_l;
+    init.rounds_r = c->rounds_r;
+    init.rounds_rule = static_cast<RoundsRule>(c->rounds_rule);
+    init.seed = c->seed;
+    return init;
+}
+
+// forgy_init init.hpp:31 (explicit stream)
+int ref_forgy_init(const double* X, uint64_t m, uint64_t n, uint64_t k, Rng* rng, double* C) {
+    return guarded([&] {
+        Dataset d = make_dataset(X, m, n);
+        Centroids c = forgy_init(d, k, *rng);
+        std::memcpy(C, c.values().data(), k * n * sizeof(double));
+    });
+}
+
+// kmeans_parallel_init init.hpp:50 (explicit stream)
+int ref_kmeans_parallel_init(const double* X, uint64_t m, uint64_t n, uint64_t k, const ref_init* cfg, Rng* rng,
+                             double* C, uint64_t* evals) {
+    return guarded([&] {
+        Dataset d = make_dataset(X, m, n);
+        EvalCounter counter;
+        Centroids c = kmeans_parallel_init(d, k, to_init(cfg), *rng, &counter);
+        std::memcpy(C, c.values().data(), k * n * sizeof(double));
+        *evals = counter.distance_evals;
+    });
+}
+
+// kmeans local_search.hpp:44 (any init method)
+int ref_kmeans(const double* X, uint64_t m, uint64_t n, uint64_t k, const ref_init* init, uint64_t max_iterations,
+               double rel_tolerance, double* C, uint8_t* mask, int32_t* labels, ref_outcome* out) {
+    return guarded([&] {
+        Dataset d = make_dataset(X, m, n);
+        SearchConfig search;
+        search.max_iterations = max_iterations;
+        search.rel_tolerance = rel_tolerance;
+        ClusteringOutcome o = kmeans(d, k, to_init(init), search);
+        export_centroids(o.centroids, C, mask);
+        std::memcpy(labels, o.assignment.labels.data(), m * sizeof(int32_t));
+        out->objective = o.objective;
+        out->evals = o.counter.distance_evals;
+        out->iterations = o.counter.iterations;
+        out->chunks = 1;
+        out->cpu_init = o.counter.cpu_init;
+        out->cpu_full = o.counter.cpu_full;
+    });
+}
+
 }  // extern "C"

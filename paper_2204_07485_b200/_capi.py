@@ -31,6 +31,11 @@ class bm_config(C.Structure):
                 ("candidates_per_step", i32), ("seed", u64), ("final_assignment", i32)]
 
 
+class bm_init_config(C.Structure):  # InitConfig init.hpp:16-27
+    _fields_ = [("method", C.c_int32), ("candidates_per_step", C.c_int32), ("oversampling_l", C.c_int32),
+                ("rounds_r", C.c_int32), ("rounds_rule", C.c_int32), ("seed", C.c_uint64)]
+
+
 class bm_outcome(C.Structure):
     _fields_ = [("centroids", P_dbl), ("mask", P_u8), ("labels", P_i32), ("objective", dbl),
                 ("distance_evals", u64), ("iterations", u64), ("cpu_init", dbl),
@@ -78,6 +83,7 @@ PROTOS = {
     "bm_lloyd": (C.c_int, [vp, P_dbl, P_u8, u64, u64, dbl, P_i32, P_dbl, u64, P_u64, P_dbl,
                            P_u64, P_u64]),
     "bm_kmeans_pp": (C.c_int, [vp, u64, i32, u64, u64, dbl, C.POINTER(bm_outcome)]),
+    "bm_kmeans": (C.c_int, [vp, u64, C.POINTER(bm_init_config), u64, dbl, C.POINTER(bm_outcome)]),
     "bm_big_means": (C.c_int, [vp, C.POINTER(bm_config), C.POINTER(bm_outcome),
                                C.POINTER(bm_chunk_record), u64]),
     "bm_assign_rows": (C.c_int, [vp, P_dbl, P_u8, u64, u64, u64, P_i32, P_dbl, P_u64]),

@@ -273,11 +273,28 @@ class EvalCounter:
         self.cpu_full += o.cpu_full
 
 
+class InitMethod:
+    """init.hpp:8 (enum values as in the reference)."""
+    forgy = 0
+    kmeans_pp = 1
+    kmeans_parallel = 2
+
+
+class RoundsRule:
+    """init.hpp:10-13."""
+    fixed = 0
+    log_phi = 1
+
+
 @dataclass
 class InitConfig:
-    """init.hpp:14-24 (kmeans_pp only)."""
+    """init.hpp:16-27."""
     candidates_per_step: int = 3
     seed: int = K_DEFAULT_SEED
+    method: int = InitMethod.kmeans_pp
+    oversampling_l: int = 0
+    rounds_r: int = 5
+    rounds_rule: int = RoundsRule.fixed
 
 
 @dataclass
@@ -442,7 +459,8 @@ def lloyd(data: Dataset, start: Centroids, cfg: SearchConfig = SearchConfig(),
 
 def kmeans(data: Dataset, k: int, init: InitConfig = InitConfig(),
            search: SearchConfig = SearchConfig()) -> ClusteringOutcome:
-    """local_search.hpp:44 with InitMethod::kmeans_pp."""
+    """kmeans local_search.hpp:44 / local_search.cpp:62-94 with init.method
+    (forgy, kmeans_pp or kmeans_parallel) seeded by init.seed, then lloyd."""
     cv = np.empty((k, data.n), np.float64)
     cm = np.empty(k, np.uint8)
     labels = np.empty(data.m, np.int32)
@@ -450,9 +468,10 @@ def kmeans(data: Dataset, k: int, init: InitConfig = InitConfig(),
     out.centroids = _ptr(cv, _capi.P_dbl)
     out.mask = _ptr(cm, _capi.P_u8)
     out.labels = _ptr(labels, _capi.P_i32)
-    _check(_capi.load().bm_kmeans_pp(data.handle, k, init.candidates_per_step, init.seed,
-                                     int(search.max_iterations), float(search.rel_tolerance),
-                                     C.byref(out)))
+    ic = _capi.bm_init_config(int(init.method), int(init.candidates_per_step), int(init.oversampling_l),
+                              int(init.rounds_r), int(init.rounds_rule), int(init.seed))
+    _check(_capi.load().bm_kmeans(data.handle, k, C.byref(ic), int(search.max_iterations),
+                                  float(search.rel_tolerance), C.byref(out)))
     counter = EvalCounter(out.distance_evals, out.iterations, out.cpu_init, out.cpu_full)
     return ClusteringOutcome(Centroids(cv, cm), labels, out.objective, [], counter)
 

@@ -20,6 +20,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <random>
 #include <string>
@@ -2008,6 +2009,221 @@ void upload_centroids(cudaStream_t st, Workspace& w, const double* C, const uint
 // ===========================================================================
 using namespace bm;
 
+namespace bm {
+
+// block_sum (core.cpp:163-175) of a device array: ordered 1024-tile folds on
+// the device, the tile partials folded in order here.
+double device_block_sum(cudaStream_t st, Workspace& w, const double* v, uint64_t count) {
+    const uint64_t tiles = tiles_of(count);
+    launch_tile_sums(st, v, count, 0, 1, w.tile_buf.p, nullptr);
+    std::vector<double> t(tiles);
+    BM_CUDA(cudaMemcpyAsync(t.data(), w.tile_buf.p, tiles * sizeof(double), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    double total = 0.0;
+    for (double x : t) total += x;
+    return total;
+}
+
+// forgy_init (init.cpp:92-115): the partial Fisher-Yates touches k slots, so
+// the swapped positions are kept in a map instead of the reference's iota(m);
+// the chosen rows go to w.C (all active).  No distance evaluations.
+void forgy_device(cudaStream_t st, const Points& P, Workspace& w, uint64_t k, Mt64& rng) {
+    std::unordered_map<uint64_t, uint64_t> moved;
+    auto at = [&](uint64_t i) {
+        auto it = moved.find(i);
+        return it == moved.end() ? i : it->second;
+    };
+    std::vector<uint64_t> rows(k);
+    for (uint64_t i = 0; i < k; ++i) {
+        const uint64_t j = rng.uniform_int(i, P.rows - 1);
+        const uint64_t vi = at(i), vj = at(j);
+        moved[i] = vj;
+        moved[j] = vi;
+        rows[i] = vj;
+    }
+    for (uint64_t i = 0; i < k; ++i) set_row_any(st, P, w, rows[i], (int)i);
+}
+
+// kmeans_parallel_init (init.cpp:209-347) on the device: D^2 passes, per-point
+// round draws, candidate weights and the weighted reduction run as kernels;
+// the host keeps the stream between them and the short index bookkeeping.
+void kmeans_parallel_device(cudaStream_t st, const bm_dataset* d, const Points& P, Workspace& w, uint64_t k,
+                            const bm_init_config& cfg, Mt64& rng, uint64_t& evals) {
+    const uint64_t m = P.rows;
+    const int n = P.n;
+    const uint64_t first = rng.uniform_int(0, m - 1);  // :220-221
+    if (k == 1) {                                       // :222-225
+        set_row_any(st, P, w, first, 0);
+        return;
+    }
+    const double l = cfg.oversampling_l > 0 ? (double)cfg.oversampling_l : 2.0 * (double)k;  // :227-228
+    std::vector<uint32_t> cand{(uint32_t)first};
+    DevBuf<uint32_t> dcand(1);
+    double* d2 = w.d2pool.p;  // dist2 (m)
+    BM_CUDA(cudaMemcpyAsync(dcand.p, cand.data(), sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    launch_dist_rows(st, P, dcand.p, 1, nullptr, d2);  // :232
+    evals += m;
+    int rounds = cfg.rounds_r;  // :234-238
+    if (cfg.rounds_rule == 1) {
+        const double phi1 = device_block_sum(st, w, d2, m);
+        rounds = phi1 > 1.0 ? std::max(1, (int)std::floor(std::log(phi1))) : 1;
+    }
+    if (rounds < 1) throw ConfigError("kmeans_parallel_init: rounds_r must be at least 1");  // :239-241
+    const uint64_t words = ceil_div(m, 32);
+    DevBuf<uint32_t> bits(words);
+    std::vector<uint32_t> hbits(words);
+    DevBuf<Mt64State> dmt(2);
+    DevBuf<uint64_t> raw;
+    DevBuf<int> flag(1);
+    HostBuf<Mt64State> hmt;
+    hmt.alloc(1);
+    for (int round = 0; round < rounds; ++round) {  // :244-263
+        const double phi = device_block_sum(st, w, d2, m);
+        if (phi <= 0.0) break;
+        // one uniform_real(0, 1) per point, in index order (:251-258)
+        if (!raw.n) raw.alloc(m);
+        *hmt.p = rng.s;
+        BM_CUDA(cudaMemcpyAsync(dmt.p, hmt.p, sizeof(Mt64State), cudaMemcpyHostToDevice, st));
+        if (m > 0xFFFFFFFFull) throw ConfigError("kmeans_parallel_init: too many rows for the device draws");
+        dev::k_mt_twist<<<1, dev::kMtThreads, 0, st>>>(dmt.p, dmt.p + 1, (uint32_t)m, raw.p, flag.p);
+        BM_LAUNCH();
+        dev::k_kpar_bern<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(raw.p, d2, m, l, phi, bits.p);
+        BM_LAUNCH();
+        BM_CUDA(cudaMemcpyAsync(hmt.p, dmt.p, sizeof(Mt64State), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(hbits.data(), bits.p, words * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        rng.s = *hmt.p;
+        count_launch(2);
+        std::vector<uint32_t> fresh;
+        for (uint64_t wi = 0; wi < words; ++wi)
+            for (uint32_t b = hbits[wi]; b; b &= b - 1) fresh.push_back((uint32_t)(wi * 32 + __builtin_ctz(b)));
+        if (fresh.empty()) continue;
+        cand.insert(cand.end(), fresh.begin(), fresh.end());  // :259-262 (lower_to_row per fresh row)
+        DevBuf<uint32_t> df(fresh.size());
+        BM_CUDA(cudaMemcpyAsync(df.p, fresh.data(), fresh.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        dispatch(P.dtype, [&](auto tag) {
+            using T = decltype(tag);
+            dev::k_kpar_lower<T><<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(static_cast<const T*>(P.X), m, n, P.ld,
+                                                                             df.p, (int)fresh.size(), d2);
+        });
+        BM_LAUNCH();
+        BM_CUDA(cudaStreamSynchronize(st));
+        count_launch();
+        evals += m * (uint64_t)fresh.size();
+    }
+    if (cand.size() < k) {  // top-up with distinct uniform rows (:266-278)
+        std::vector<uint8_t> used(m, 0);
+        for (uint32_t i : cand) used[i] = 1;
+        while (cand.size() < k) {
+            const uint64_t i = rng.uniform_int(0, m - 1);
+            if (!used[i]) {
+                used[i] = 1;
+                cand.push_back((uint32_t)i);
+            }
+        }
+    }
+    const uint64_t nc = cand.size();
+    // candidate rows (fp64) and weights: points nearest each candidate (:280-295)
+    DevBuf<uint32_t> dall(nc);
+    BM_CUDA(cudaMemcpyAsync(dall.p, cand.data(), nc * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    DevBuf<double> Cc(nc * n);
+    dispatch(P.dtype, [&](auto tag) {
+        using T = decltype(tag);
+        dev::k_rows_f64<T><<<(unsigned)std::min<uint64_t>(ceil_div(nc * n, 256), 1184), 256, 0, st>>>(
+            static_cast<const T*>(P.X), P.ld, n, dall.p, nc, Cc.p);
+    });
+    BM_LAUNCH();
+    DevBuf<int> act(nc), nact(1);
+    {
+        std::vector<int> a(nc);
+        for (uint64_t q = 0; q < nc; ++q) a[q] = (int)q;
+        const int na = (int)nc;
+        BM_CUDA(cudaMemcpyAsync(act.p, a.data(), nc * sizeof(int), cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaMemcpyAsync(nact.p, &na, sizeof(int), cudaMemcpyHostToDevice, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+    }
+    int32_t* lab = w.labels.p;
+    double* dd = w.dists.p;
+    dispatch(P.dtype, [&](auto tag) {  // exact assign_nearest over the candidates (core.cpp:106-161)
+        using T = decltype(tag);
+        dev::k_assign<T><<<(unsigned)ceil_div(m, dev::kABP), assign_threads((int)nc), 0, st>>>(
+            static_cast<const T*>(P.X), m, n, P.ld, Cc.p, n, act.p, nact.p, lab, 0, nullptr, dd, nullptr, nullptr);
+    });
+    BM_LAUNCH();
+    evals += m * nc;
+    DevBuf<unsigned long long> cnt(nc);
+    BM_CUDA(cudaMemsetAsync(cnt.p, 0, nc * sizeof(unsigned long long), st));
+    dev::k_kpar_count<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(lab, m, cnt.p);
+    BM_LAUNCH();
+    // weighted greedy k-means++ over the candidates (:297-339), one CTA
+    DevBuf<double> scratch(4 * nc);
+    DevBuf<uint32_t> chosen(k);
+    DevBuf<unsigned long long> dev_ev(1);
+    *hmt.p = rng.s;
+    BM_CUDA(cudaMemcpyAsync(dmt.p, hmt.p, sizeof(Mt64State), cudaMemcpyHostToDevice, st));
+    dev::k_kpar_reduce<<<1, 256, 0, st>>>(Cc.p, n, cnt.p, nc, (int)k, std::max(1, cfg.candidates_per_step), dmt.p,
+                                          scratch.p, chosen.p, dev_ev.p);
+    BM_LAUNCH();
+    count_launch(5);
+    std::vector<uint32_t> hch(k);
+    unsigned long long hev = 0;
+    BM_CUDA(cudaMemcpyAsync(hmt.p, dmt.p, sizeof(Mt64State), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(hch.data(), chosen.p, k * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(&hev, dev_ev.p, sizeof(hev), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    rng.s = *hmt.p;
+    evals += hev;
+    for (uint64_t j = 0; j < k; ++j)  // :341-346
+        BM_CUDA(cudaMemcpyAsync(w.C.p + j * n, Cc.p + (uint64_t)hch[j] * n, n * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    BM_CUDA(cudaMemsetAsync(w.mask.p, 0, k, st));
+    (void)d;
+}
+
+// kmeans (local_search.cpp:62-94): init per method (init.seed), then lloyd.
+void kmeans(const bm_dataset* d, uint64_t k, const bm_init_config& init, uint64_t max_iterations,
+            double rel_tolerance, bm_outcome* out) {
+    if (k < 1) throw ConfigError("kmeans: k must be at least 1");
+    if (d->m < k) throw ConfigError("kmeans: dataset has fewer points than clusters");
+    if (max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
+    if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
+    if (init.method < 0 || init.method > 2) throw ConfigError("kmeans: unknown initialization method");
+    DeviceGuard g(d->device);
+    cudaStream_t st = stream_of(d);
+    Workspace& w = get_ws(d, d->m, (int)k, std::max(1, init.candidates_per_step), 0);
+    Mt64 rng(init.seed);  // :71
+    const auto t_init = std::chrono::steady_clock::now();
+    BM_CUDA(cudaMemsetAsync(w.C.p, 0, k * d->n * sizeof(double), st));
+    BM_CUDA(cudaMemsetAsync(w.mask.p, 1, k, st));
+    uint64_t init_evals = 0;
+    Points P = dataset_points(d);
+    if (init.method == 0) {
+        forgy_device(st, P, w, k, rng);
+    } else if (init.method == 1) {
+        std::vector<uint8_t> hmask(k, 1);
+        kmeanspp_fill_device(st, P, w, hmask, init.candidates_per_step, rng, init_evals);
+    } else {
+        kmeans_parallel_device(st, d, P, w, k, init, rng, init_evals);
+    }
+    BM_CUDA(cudaStreamSynchronize(st));
+    out->cpu_init = seconds_since(t_init);
+    const auto t_search = std::chrono::steady_clock::now();
+    LloydResult r = lloyd_run(st, P, w, max_iterations, rel_tolerance);
+    BM_CUDA(cudaMemcpyAsync(out->centroids, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaMemcpyAsync(out->mask, w.mask.p, k, cudaMemcpyDeviceToHost, st));
+    if (out->labels)
+        BM_CUDA(cudaMemcpyAsync(out->labels, w.labels.p + (uint64_t)r.parity * w.R, d->m * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+    BM_CUDA(cudaStreamSynchronize(st));
+    out->cpu_full = seconds_since(t_search);
+    out->objective = r.objective;
+    out->distance_evals = r.evals + init_evals;
+    out->iterations = r.iterations;
+    out->chunks = 1;
+}
+
+}  // namespace bm
+
 extern "C" {
 
 const char* bm_last_error(void) { return g_last_error.c_str(); }
@@ -2398,6 +2614,11 @@ bm_status bm_lloyd(const bm_dataset* dc, double* C, uint8_t* mask, uint64_t k, u
         *evals = r.evals;
         *iterations = r.iterations;
     });
+}
+
+bm_status bm_kmeans(const bm_dataset* data, uint64_t k, const bm_init_config* init, uint64_t max_iterations,
+                    double rel_tolerance, bm_outcome* out) {
+    return guarded([&] { kmeans(data, k, *init, max_iterations, rel_tolerance, out); });
 }
 
 bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uint64_t seed,

@@ -3806,6 +3806,185 @@ __global__ void k_set_row(const T* __restrict__ X, uint64_t ld, int n, uint64_t 
 }
 
 // ===========================================================================
+// 8b. K-means|| seeding (kmeans_parallel_init init.cpp:209-347) on the device.
+// ===========================================================================
+// Round draws (:251-258): one uniform_real(0,1) per point in index order (raw
+// words from k_mt_twist, tempered here); point i joins with probability
+// min(1, l * D2[i] / phi).  Result: one bit per point (ascending order).
+__global__ void k_kpar_bern(const uint64_t* __restrict__ raw, const double* __restrict__ d2, uint64_t m, double l,
+                            double phi, uint32_t* __restrict__ bits) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool take = false;
+    if (i < m) {
+        double u = __dmul_rn(__ull2double_rn(mt_temper(raw[i])), 0x1p-64);  // generate_canonical
+        if (u >= 1.0) u = 0x1.fffffffffffffp-1;
+        u = __dadd_rn(__dmul_rn(u, 1.0), 0.0);  // unit(rng): canon * (1 - 0) + 0
+        double p = __ddiv_rn(__dmul_rn(l, d2[i]), phi);
+        if (!(p < 1.0)) p = 1.0;  // std::min(1.0, p)
+        take = u < p;
+    }
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, take);
+    if ((threadIdx.x & 31) == 0 && i < m) bits[i >> 5] = b;
+}
+
+// lower_to_row (init.cpp:46-70) for a batch of rows: D2[i] = min(D2[i], min over
+// the batch of the exact distance).  min is exact, so one pass equals the
+// reference's row-by-row passes.
+template <typename T>
+__global__ void k_kpar_lower(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+                             const uint32_t* __restrict__ cand, int ncand, double* __restrict__ d2) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const T* x = X + i * ld;
+    double best = d2[i];
+    for (int c = 0; c < ncand; ++c) {
+        const T* r = X + static_cast<uint64_t>(cand[c]) * ld;
+        double sum = 0.0;
+        for (int d = 0; d < n; ++d) sum = dist_step(sum, to_f64(x[d]), to_f64(r[d]));
+        if (sum < best) best = sum;
+    }
+    d2[i] = best;
+}
+
+// data.gather(cand_index) (:280) promoted to fp64 rows [count][n].
+template <typename T>
+__global__ void k_rows_f64(const T* __restrict__ X, uint64_t ld, int n, const uint32_t* __restrict__ idx,
+                           uint64_t count, double* __restrict__ out) {
+    const uint64_t total = count * static_cast<uint64_t>(n);
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[e] = to_f64(X[static_cast<uint64_t>(idx[e / n]) * ld + (e % n)]);
+}
+
+// Candidate weights (:292-295): points nearest each candidate (exact integer counts).
+__global__ void k_kpar_count(const int32_t* __restrict__ labels, uint64_t m, unsigned long long* __restrict__ cnt) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m && labels[i] >= 0) atomicAdd(&cnt[labels[i]], 1ull);
+}
+
+// Exact fp64 distance (init.cpp:32-36) between two fp64 rows.
+__device__ __forceinline__ double row_dist64(const double* __restrict__ a, const double* __restrict__ b, int n) {
+    double sum = 0.0;
+    for (int d = 0; d < n; ++d) sum = dist_step(sum, a[d], b[d]);
+    return sum;
+}
+
+// Weighted greedy k-means++ over the candidates (:297-339), one CTA: the draws
+// from the device-resident stream, the sequential sums (prefix_sums, potential)
+// by thread 0, distances by all threads.  scratch: 4 * nc doubles.
+__global__ void __launch_bounds__(256)
+k_kpar_reduce(const double* __restrict__ Cc, int n, const unsigned long long* __restrict__ cnt, uint64_t nc, int k,
+              int candidates, Mt64State* __restrict__ mt, double* __restrict__ scratch, uint32_t* __restrict__ chosen,
+              unsigned long long* __restrict__ evals) {
+    __shared__ uint64_t xs[kMtN];
+    __shared__ int pos;
+    __shared__ double total_s;
+    __shared__ uint64_t pick_s;
+    __shared__ int flip_s;  // which of (trial, best_trial) buffers holds best_trial
+    const int tid = threadIdx.x;
+    double* cdist2 = scratch;
+    double* cum = scratch + nc;
+    double* tb[2] = {scratch + 2 * nc, scratch + 3 * nc};
+    for (int i = tid; i < kMtN; i += blockDim.x) xs[i] = mt->x[i];
+    if (tid == 0) pos = static_cast<int>(mt->pos);
+    __syncthreads();
+    unsigned long long ev = 0;
+    // wcum = prefix_sums(weight); chosen_first = pick_by_mass(wcum, wdraw)  (:297-300)
+    if (tid == 0) {
+        double run = 0.0;
+        for (uint64_t q = 0; q < nc; ++q) {
+            run = __dadd_rn(run, static_cast<double>(cnt[q]));
+            cum[q] = run;
+        }
+        int p = pos;
+        const double u = mt_uniform_real(xs, p, 0.0, run);
+        pos = p;
+        uint64_t lo = 0, hi = nc;  // upper_bound, clamped
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (u < cum[mid]) hi = mid;
+            else lo = mid + 1;
+        }
+        pick_s = lo == nc ? nc - 1 : lo;
+        chosen[0] = static_cast<uint32_t>(pick_s);
+    }
+    __syncthreads();
+    {
+        const double* r = Cc + pick_s * n;
+        for (uint64_t q = tid; q < nc; q += blockDim.x) cdist2[q] = row_dist64(Cc + q * n, r, n);  // :302
+        ev += nc;
+    }
+    __syncthreads();
+    for (int nch = 1; nch < k; ++nch) {
+        if (tid == 0) {  // mass = weight * cdist2; prefix sums (:309-313)
+            double run = 0.0;
+            for (uint64_t q = 0; q < nc; ++q) {
+                run = __dadd_rn(run, __dmul_rn(static_cast<double>(cnt[q]), cdist2[q]));
+                cum[q] = run;
+            }
+            total_s = run;
+            flip_s = 0;
+        }
+        __syncthreads();
+        const double total = total_s;
+        if (total <= 0.0) {  // :314-317
+            if (tid == 0) {
+                int p = pos;
+                chosen[nch] = static_cast<uint32_t>(mt_uniform_int(xs, p, 0, nc - 1));
+                pos = p;
+            }
+            __syncthreads();
+            continue;
+        }
+        double best_potential = __longlong_as_double(0x7FF0000000000000LL);  // thread 0's view
+        uint64_t best_index = 0;
+        for (int c = 0; c < candidates; ++c) {  // :321-335
+            if (tid == 0) {
+                int p = pos;
+                const double u = mt_uniform_real(xs, p, 0.0, total);
+                pos = p;
+                uint64_t lo = 0, hi = nc;
+                while (lo < hi) {
+                    const uint64_t mid = lo + (hi - lo) / 2;
+                    if (u < cum[mid]) hi = mid;
+                    else lo = mid + 1;
+                }
+                pick_s = lo == nc ? nc - 1 : lo;
+            }
+            __syncthreads();
+            double* trial = tb[flip_s ^ 1];
+            const double* r = Cc + pick_s * n;
+            for (uint64_t q = tid; q < nc; q += blockDim.x) {
+                const double t = row_dist64(Cc + q * n, r, n);
+                trial[q] = cdist2[q] < t ? cdist2[q] : t;  // std::min(trial, cdist2)
+            }
+            ev += nc;
+            __syncthreads();
+            if (tid == 0) {
+                double potential = 0.0;
+                for (uint64_t q = 0; q < nc; ++q)
+                    potential = __dadd_rn(potential, __dmul_rn(static_cast<double>(cnt[q]), trial[q]));
+                if (potential < best_potential) {
+                    best_potential = potential;
+                    best_index = pick_s;
+                    flip_s ^= 1;  // swap(trial, best_trial)
+                }
+            }
+            __syncthreads();
+        }
+        if (tid == 0) chosen[nch] = static_cast<uint32_t>(best_index);
+        const double* bt = tb[flip_s];
+        for (uint64_t q = tid; q < nc; q += blockDim.x) cdist2[q] = bt[q];  // swap(cdist2, best_trial)
+        __syncthreads();
+    }
+    for (int i = tid; i < kMtN; i += blockDim.x) mt->x[i] = xs[i];
+    if (tid == 0) {
+        mt->pos = static_cast<uint64_t>(pos);
+        *evals = ev;
+    }
+}
+
+// ===========================================================================
 // 9. Dataset helpers.
 // ===========================================================================
 // Exact-sum statistics (§5b) of one finite value: exponent of its lowest set

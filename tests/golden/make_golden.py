@@ -128,6 +128,28 @@ def main() -> None:
     g["ident_obj"] = np.array([o.objective, km.objective])
     g["ident_stats"] = np.array([o.evals, o.iterations, km.evals, km.iterations], np.uint64)
 
+    # kmeans with every InitMethod (local_search.cpp:62-94; init.cpp:92-115, 209-347):
+    # (method, rounds_rule, oversampling_l, k, seed) on integer and real data
+    km_cases = [(0, 0, 0, 5, 41), (1, 0, 0, 5, 42), (2, 0, 0, 6, 43), (2, 1, 0, 6, 44), (2, 0, 3, 9, 45),
+                (2, 0, 0, 1, 46)]
+    for i, (meth, rule, l, k, seed) in enumerate(km_cases):
+        X = gen.normal(0, 4, (700 + 50 * i, 3))
+        if i % 2:
+            X = np.rint(X)
+        o = R.kmeans(X, k, meth, seed, rounds_rule=rule, oversampling_l=l)
+        g[f"km{i}_X"] = X
+        g[f"km{i}_cfg"] = np.array([meth, rule, l, k, seed], np.uint64)
+        g[f"km{i}_C"], g[f"km{i}_labels"] = o.centroids, o.labels
+        g[f"km{i}_obj"] = np.array([o.objective])
+        g[f"km{i}_stats"] = np.array([o.evals, o.iterations], np.uint64)
+    # the init functions alone on an explicit stream
+    X = gen.uniform(0, 10, (400, 4))
+    r = R.rng(77)
+    g["init_X"] = X
+    g["init_forgy"] = R.forgy_init(X, 5, r)
+    g["init_kpar"], ev = R.kmeans_parallel_init(X, 7, r)
+    g["init_kpar_evals"] = np.array([ev], np.uint64)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(g)} arrays)")
 

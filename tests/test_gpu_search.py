@@ -218,3 +218,49 @@ def test_kmeanspp_device_steps_vs_oracle(port, case):
     assert (got.mask == me).all()
     assert counter.distance_evals == ev
     assert r() == port.rng_next(pr)
+
+
+# kmeans with every InitMethod (local_search.cpp:62-94): forgy (init.cpp:92-115),
+# kmeans_pp (:123-201), kmeans_parallel with both rounds rules (:209-347).
+@pytest.mark.parametrize("meth,rule,l", [(0, 0, 0), (1, 0, 0), (2, 0, 0), (2, 1, 0), (2, 0, 4)])
+@pytest.mark.parametrize("seed", range(3))
+def test_kmeans_methods_vs_oracle(port, meth, rule, l, seed):
+    rng = np.random.default_rng(900 + 7 * seed + meth)
+    m, n, k = int(rng.integers(300, 6000)), int(rng.integers(1, 24)), int(rng.integers(1, 28))
+    X = rng.normal(size=(m, n)) * rng.uniform(0.5, 20)
+    if seed == 1:
+        X = np.rint(X)
+    if seed == 2:
+        X = X.astype(np.float32)
+    init = bm.InitConfig(seed=seed, method=meth, rounds_rule=rule, oversampling_l=l)
+    out = bm.kmeans(bm.Dataset(X), k, init, bm.SearchConfig())
+    p = port.kmeans(X.astype(np.float64), k, meth, seed, rounds_rule=rule, oversampling_l=l)
+    assert out.objective == p.objective
+    assert (bits(out.centroids.values) == bits(p.centroids)).all()
+    assert (out.centroids.mask == p.mask).all()
+    assert (out.assignment == p.labels).all()
+    assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+def test_kmeans_golden_methods(golden):
+    for i in range(6):
+        X = golden[f"km{i}_X"]
+        meth, rule, l, k, seed = (int(v) for v in golden[f"km{i}_cfg"])
+        out = bm.kmeans(bm.Dataset(X), k, bm.InitConfig(seed=seed, method=meth, rounds_rule=rule,
+                                                        oversampling_l=l), bm.SearchConfig())
+        assert (bits(out.centroids.values) == bits(golden[f"km{i}_C"])).all()
+        assert (out.assignment == golden[f"km{i}_labels"]).all()
+        assert out.objective == golden[f"km{i}_obj"][0]
+        assert [out.counter.distance_evals, out.counter.iterations] == golden[f"km{i}_stats"].tolist()
+
+
+def test_kmeans_config_errors():
+    X = np.random.default_rng(1).normal(size=(30, 2))
+    d = bm.Dataset(X)
+    for meth in (0, 1, 2):
+        with pytest.raises(bm.ConfigError):
+            bm.kmeans(d, 31, bm.InitConfig(method=meth), bm.SearchConfig())
+    with pytest.raises(bm.ConfigError):
+        bm.kmeans(d, 3, bm.InitConfig(method=2, rounds_r=0), bm.SearchConfig())
+    with pytest.raises(bm.ConfigError):
+        bm.kmeans(d, 3, bm.InitConfig(method=7), bm.SearchConfig())
