@@ -188,6 +188,16 @@ typedef struct {
 bm_status bm_kmeans(const bm_dataset* data, uint64_t k, const bm_init_config* init,
                     uint64_t max_iterations, double rel_tolerance, bm_outcome* out);
 
+/* choose_chunk_size_hint big_means.hpp:72-73 / big_means.cpp:114-160 (ChunkHintConfig
+ * :60-68): ladder NULL / empty = m/64 .. m; best mean objective of
+ * runs_per_candidate big_means probes (seeds seed + run) wins, ties to the
+ * smaller size.  best_mean may be NULL. */
+bm_status bm_choose_chunk_size_hint(bm_dataset* data, uint64_t k, const uint64_t* ladder,
+                                    uint64_t ladder_len, uint64_t chunks_per_candidate,
+                                    uint64_t runs_per_candidate, uint64_t max_iterations,
+                                    double rel_tolerance, int32_t candidates_per_step,
+                                    uint64_t seed, uint64_t* chunk_size, double* best_mean);
+
 /* big_means big_means.hpp:56-57 / big_means.cpp:58-112.  trace may be NULL;
  * at most trace_capacity records are written, out->chunks holds the count. */
 bm_status bm_big_means(bm_dataset* data, const bm_config* cfg, bm_outcome* out,

@@ -314,6 +314,41 @@ class Oracle:
         return BigMeansResult(Cn, mask, labels, float(out.objective), int(out.evals),
                               int(out.iterations), 1)
 
+    def choose_chunk_size_hint(self, X, k, ladder=(), chunks_per_candidate=3, runs_per_candidate=3,
+                               max_iterations=300, rel_tolerance=1e-4, candidates=3, seed=123456789):
+        """big_means.cpp:114-160.  The port restates the probe loop here over its
+        own big_means; the reference calls its library function."""
+        X = _f64(X)
+        m, n = X.shape
+        if self.kind == "ref":
+            lad = np.ascontiguousarray(ladder, np.uint64)
+            out = _u64(0)
+            self._check(self.lib.ref_choose_chunk_size_hint(
+                _p(X, _dp), _u64(m), _u64(n), _u64(k), _p(lad, _u64p), _u64(lad.size),
+                _u64(chunks_per_candidate), _u64(runs_per_candidate), _u64(max_iterations),
+                C.c_double(rel_tolerance), C.c_int(candidates), _u64(seed), C.byref(out)))
+            return int(out.value)
+        if k < 1 or m < k or chunks_per_candidate < 1 or runs_per_candidate < 1:
+            raise OracleError(1, "choose_chunk_size_hint: invalid arguments")  # :117-123
+        lad = list(ladder)
+        if not lad:  # :125-130
+            div = 64
+            while div >= 1:
+                lad.append(max(k, m // div))
+                div //= 2
+        lad = sorted(set(min(max(s, k), m) for s in lad))  # clamp, sort, unique :131-135
+        best_mean, best_s = float("inf"), lad[0]
+        for s in lad:  # :139-157
+            tot = 0.0
+            for run in range(runs_per_candidate):
+                tot += self.big_means(X, k, s, chunks_per_candidate, seed=seed + run,
+                                      max_iterations=max_iterations, rel_tolerance=rel_tolerance,
+                                      candidates_per_step=candidates).objective
+            mean = tot / float(runs_per_candidate)
+            if mean < best_mean:
+                best_mean, best_s = mean, s
+        return best_s
+
     def set_worker_count(self, n: int):
         if self.kind == "ref":
             self.lib.ref_set_worker_count(C.c_uint(n))

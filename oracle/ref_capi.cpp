@@ -302,4 +302,22 @@ int ref_kmeans(const double* X, uint64_t m, uint64_t n, uint64_t k, const ref_in
     });
 }
 
+// choose_chunk_size_hint big_means.hpp:72-73
+int ref_choose_chunk_size_hint(const double* X, uint64_t m, uint64_t n, uint64_t k, const uint64_t* ladder,
+                               uint64_t ladder_len, uint64_t chunks_per, uint64_t runs_per, uint64_t max_iterations,
+                               double rel_tolerance, int candidates, uint64_t seed, uint64_t* out) {
+    return guarded([&] {
+        Dataset d = make_dataset(X, m, n);
+        ChunkHintConfig cfg;
+        cfg.ladder.assign(ladder, ladder + ladder_len);
+        cfg.chunks_per_candidate = chunks_per;
+        cfg.runs_per_candidate = runs_per;
+        cfg.search.max_iterations = max_iterations;
+        cfg.search.rel_tolerance = rel_tolerance;
+        cfg.init.candidates_per_step = candidates;
+        cfg.seed = seed;
+        *out = choose_chunk_size_hint(d, k, cfg);
+    });
+}
+
 }  // extern "C"

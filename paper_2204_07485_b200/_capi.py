@@ -84,6 +84,7 @@ PROTOS = {
                            P_u64, P_u64]),
     "bm_kmeans_pp": (C.c_int, [vp, u64, i32, u64, u64, dbl, C.POINTER(bm_outcome)]),
     "bm_kmeans": (C.c_int, [vp, u64, C.POINTER(bm_init_config), u64, dbl, C.POINTER(bm_outcome)]),
+    "bm_choose_chunk_size_hint": (C.c_int, [vp, u64, P_u64, u64, u64, u64, u64, dbl, i32, u64, P_u64, P_dbl]),
     "bm_big_means": (C.c_int, [vp, C.POINTER(bm_config), C.POINTER(bm_outcome),
                                C.POINTER(bm_chunk_record), u64]),
     "bm_assign_rows": (C.c_int, [vp, P_dbl, P_u8, u64, u64, u64, P_i32, P_dbl, P_u64]),

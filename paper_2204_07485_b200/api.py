@@ -476,6 +476,31 @@ def kmeans(data: Dataset, k: int, init: InitConfig = InitConfig(),
     return ClusteringOutcome(Centroids(cv, cm), labels, out.objective, [], counter)
 
 
+@dataclass
+class ChunkHintConfig:
+    """big_means.hpp:60-68."""
+    ladder: list = field(default_factory=list)
+    chunks_per_candidate: int = 3
+    runs_per_candidate: int = 3
+    search: SearchConfig = field(default_factory=SearchConfig)
+    init: InitConfig = field(default_factory=InitConfig)
+    seed: int = K_DEFAULT_SEED
+
+
+def choose_chunk_size_hint(data: Dataset, k: int, cfg: ChunkHintConfig = ChunkHintConfig()) -> int:
+    """big_means.hpp:72-73 / big_means.cpp:114-160: the ladder size with the best
+    mean final objective over short big_means probes (ties: the smaller size)."""
+    lad = np.ascontiguousarray(cfg.ladder, np.uint64)
+    out = C.c_uint64()
+    mean = C.c_double()
+    _check(_capi.load().bm_choose_chunk_size_hint(
+        data.handle, int(k), _ptr(lad, _capi.P_u64) if lad.size else None, lad.size,
+        int(cfg.chunks_per_candidate), int(cfg.runs_per_candidate), int(cfg.search.max_iterations),
+        float(cfg.search.rel_tolerance), int(cfg.init.candidates_per_step), int(cfg.seed),
+        C.byref(out), C.byref(mean)))
+    return int(out.value)
+
+
 def _native_config(cfg: BigMeansConfig) -> _capi.bm_config:
     c = _capi.bm_config()
     _capi.load().bm_config_init(C.byref(c))

@@ -2180,6 +2180,53 @@ void kmeans_parallel_device(cudaStream_t st, const bm_dataset* d, const Points& 
     (void)d;
 }
 
+// choose_chunk_size_hint (big_means.cpp:114-160): short big_means probes per
+// ladder size; the best mean final objective wins, ties to the smaller size.
+uint64_t choose_chunk_size_hint(bm_dataset* d, uint64_t k, std::vector<uint64_t> ladder, uint64_t chunks_per,
+                                uint64_t runs_per, uint64_t max_iterations, double rel_tolerance, int candidates,
+                                uint64_t seed, double* best_mean_out) {
+    const uint64_t m = d->m;
+    if (k < 1 || m < k) throw ConfigError("choose_chunk_size_hint: need at least k points");
+    if (chunks_per < 1 || runs_per < 1) throw ConfigError("choose_chunk_size_hint: probe budget must be positive");
+    if (ladder.empty())
+        for (uint64_t div = 64; div >= 1; div /= 2) ladder.push_back(std::max(k, m / div));
+    for (uint64_t& s : ladder) s = std::clamp(s, k, m);
+    std::sort(ladder.begin(), ladder.end());
+    ladder.erase(std::unique(ladder.begin(), ladder.end()), ladder.end());
+    double best_mean = std::numeric_limits<double>::infinity();
+    uint64_t best_s = ladder.front();
+    std::vector<double> C(k * d->n);
+    std::vector<uint8_t> mask(k);
+    for (uint64_t s : ladder) {
+        double sum = 0.0;
+        for (uint64_t run = 0; run < runs_per; ++run) {
+            bm_config probe{};
+            bm_config_init(&probe);
+            probe.k = k;
+            probe.chunk_size = s;
+            probe.has_max_chunks = 1;
+            probe.max_chunks = chunks_per;
+            probe.max_iterations = max_iterations;
+            probe.rel_tolerance = rel_tolerance;
+            probe.candidates_per_step = candidates;
+            probe.seed = seed + run;
+            probe.final_assignment = 1;
+            bm_outcome o{};
+            o.centroids = C.data();
+            o.mask = mask.data();
+            big_means(d, probe, &o, nullptr, 0);
+            sum += o.objective;
+        }
+        const double mean = sum / static_cast<double>(runs_per);
+        if (mean < best_mean) {  // strict: ties keep the smaller size
+            best_mean = mean;
+            best_s = s;
+        }
+    }
+    if (best_mean_out) *best_mean_out = best_mean;
+    return best_s;
+}
+
 // kmeans (local_search.cpp:62-94): init per method (init.seed), then lloyd.
 void kmeans(const bm_dataset* d, uint64_t k, const bm_init_config& init, uint64_t max_iterations,
             double rel_tolerance, bm_outcome* out) {
@@ -2613,6 +2660,17 @@ bm_status bm_lloyd(const bm_dataset* dc, double* C, uint8_t* mask, uint64_t k, u
         *objective = r.objective;
         *evals = r.evals;
         *iterations = r.iterations;
+    });
+}
+
+bm_status bm_choose_chunk_size_hint(bm_dataset* data, uint64_t k, const uint64_t* ladder, uint64_t ladder_len,
+                                    uint64_t chunks_per_candidate, uint64_t runs_per_candidate,
+                                    uint64_t max_iterations, double rel_tolerance, int32_t candidates_per_step,
+                                    uint64_t seed, uint64_t* chunk_size, double* best_mean) {
+    return guarded([&] {
+        std::vector<uint64_t> l(ladder, ladder + (ladder ? ladder_len : 0));
+        *chunk_size = choose_chunk_size_hint(data, k, l, chunks_per_candidate, runs_per_candidate, max_iterations,
+                                             rel_tolerance, candidates_per_step, seed, best_mean);
     });
 }
 

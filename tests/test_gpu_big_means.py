@@ -247,3 +247,19 @@ def test_exact_sum_regimes_vs_oracle(port, case):
         assert (bits(out.centroids.values) == bits(p.centroids)).all()
         assert (out.assignment == p.labels).all()
         assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+def test_chunk_size_hint_known_answers(port):
+    """test_big_means.cpp:197-215: within [k, m], deterministic, custom ladder respected;
+    equal to the oracle's probe loop."""
+    X = np.random.default_rng(8).uniform(0, 10, (512, 2))
+    d = bm.Dataset(X)
+    hint = bm.choose_chunk_size_hint(d, 4, bm.ChunkHintConfig())
+    assert 4 <= hint <= 512 and hint == bm.choose_chunk_size_hint(d, 4, bm.ChunkHintConfig())
+    assert hint == port.choose_chunk_size_hint(X, 4)
+    h2 = bm.choose_chunk_size_hint(d, 3, bm.ChunkHintConfig(ladder=[32, 64, 128]))
+    assert h2 in (32, 64, 128) and h2 == port.choose_chunk_size_hint(X, 3, (32, 64, 128))
+    with pytest.raises(bm.ConfigError):
+        bm.choose_chunk_size_hint(d, 600, bm.ChunkHintConfig())
+    with pytest.raises(bm.ConfigError):
+        bm.choose_chunk_size_hint(d, 3, bm.ChunkHintConfig(runs_per_candidate=0))
