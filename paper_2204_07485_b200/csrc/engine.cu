@@ -664,6 +664,15 @@ bool final_streaming() {
     return on;
 }
 
+// BM_RING=2: the 2-stage TMA ring for wide rows too (A/B of the 6-stage ring).
+bool wide_ring() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_RING");
+        return !(e && std::string(e) == "2");
+    }();
+    return on;
+}
+
 // BM_SUMS=0 disables the exact-sum update (kernels.cuh §5b) for A/B checks.
 bool exact_sums_enabled() {
     static const bool on = [] {
@@ -731,24 +740,32 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
         if (screen && tma_screen() && P.rows < (1ull << 31)) {
-            constexpr size_t shm = dev::tma_smem_bytes<T>();
-            static bool attr_set = false;  // per template instance
-            if (!attr_set) {
-                BM_CUDA(cudaFuncSetAttribute(dev::k_assign_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)shm));
-                attr_set = true;
-            }
-            const CUtensorMap tmx = points_map<T>(P);
             fused_ctl = ctl && (tile_out || ctl->fast);
-            // a speculative begin loops over its blocks with at most spec_ctas() CTAs
-            // (one per SM by default), leaving SM slots to the engine stream's rounds
-            const unsigned lgrid = fused_ctl && ctl->nblk ? std::min<unsigned>(grid, spec_ctas()) : grid;
-            launch_pdl(dev::k_assign_tma<T>, lgrid, dev::kSThreads, shm, st,
-                tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
-                S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
-                g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
-                !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
-                dstride);
+            // NS-stage TMA slab ring: 2 stages (3 CTAs per SM) for rows of up to
+            // 8 slabs, 6 stages (2 CTAs per SM) for wide rows, whose CTAs stream
+            // tens to hundreds of slabs each
+            auto go = [&](auto ns_tag) {
+                constexpr int NS = decltype(ns_tag)::value;
+                constexpr size_t shm = dev::tma_smem_bytes<T, NS>();
+                static bool attr_set = false;  // per template instance
+                if (!attr_set) {
+                    BM_CUDA(cudaFuncSetAttribute(dev::k_assign_tma<T, NS>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+                    attr_set = true;
+                }
+                const CUtensorMap tmx = points_map<T>(P);
+                // a speculative begin loops over its blocks with at most spec_ctas() CTAs
+                // (BM_SPEC_CTAS), leaving SM slots to the engine stream's rounds
+                const unsigned lgrid = fused_ctl && ctl->nblk ? std::min<unsigned>(grid, spec_ctas()) : grid;
+                launch_pdl(dev::k_assign_tma<T, NS>, lgrid, dev::kSThreads, shm, st,
+                    tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
+                    S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
+                    g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
+                    !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
+                    dstride);
+            };
+            if (P.n > 8 * dev::kADC && wide_ring()) go(std::integral_constant<int, 6>{});
+            else go(std::integral_constant<int, 2>{});
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
             static bool attr_set = false;  // per template instance

@@ -1621,11 +1621,11 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-template <typename T>
+template <typename T, int NS = 2>
 struct TmaSmem {
     static constexpr int kRawBytes = kABP * kADC * sizeof(T);  // 16 KB (f64) / 8 KB (f32)
-    alignas(1024) unsigned char raw[2][kRawBytes];             // swizzled point tiles
-    alignas(1024) float craw[2][kADC][kSMaxK];                 // centroid tiles [d][j]
+    alignas(1024) unsigned char raw[NS][kRawBytes];            // swizzled point tiles (NS-stage ring)
+    alignas(1024) float craw[NS][kADC][kSMaxK];                // centroid tiles [d][j]
     alignas(16) float xs[2][kADC][kABP];                       // fp32 point slabs [d][p]
     alignas(16) float cs[2][kADC][kSMaxK];
     float red_u[8][kABP];                                      // per-warp min upper bound
@@ -1638,7 +1638,7 @@ struct TmaSmem {
     int rank_of[kSMaxK];                                       // label -> compacted index
     float delta[kSMaxK];                                       // centroid movement per label (rounded up)
     alignas(16) float lbs[sizeof(T) == 4 ? kABP : 1][kSMaxK];  // fp32 round fast path: the bound rows (16-byte chunks swizzled)
-    uint64_t bar[2];
+    uint64_t bar[NS];
     uint32_t n_items;
     int is_last;
 };
@@ -1660,8 +1660,8 @@ __device__ __forceinline__ long long sum_units(double x, double scale) {
     return __double2ll_rn(__dmul_rn(x, scale));  // exact: x * 2^-e is an integer below 2^53
 }
 
-template <typename T>
-__device__ __noinline__ void label_sums(TmaSmem<T>& S, const LloydCtl& ctl, const T* __restrict__ X, uint64_t ld,
+template <typename T, int NS>
+__device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, const T* __restrict__ X, uint64_t ld,
                                         int n, uint64_t p0, int np, bool full, int kfull, unsigned char* scratch,
                                         size_t scratch_bytes, unsigned blk) {
     __syncthreads();  // every point's (new, old) label recorded; the scratch area is free
@@ -1938,8 +1938,8 @@ __device__ __forceinline__ double chain_smem_row(const float* x, const double* _
 // register in dimension order.  The CTA's 128-row point block streams through
 // the raw TMA ring again (one 16-dim slab per stage; slab i is TMA sequence
 // number qb + i of this CTA), the matching centroid slabs through cp.async.
-template <typename T>
-__device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx, uint64_t p0, int n, int nslab,
+template <typename T, int NS>
+__device__ __forceinline__ void tma_chains(TmaSmem<T, NS>& S, const CUtensorMap* tmx, uint64_t p0, int n, int nslab,
                                            int qb, const double* __restrict__ Cact, int ldc, int KA, uint32_t ni,
                                            const short* item_p, const signed char* item_j, double* item_d) {
     constexpr int kCS = 18;  // centroid slab row stride (doubles): 16-byte rows, spread banks
@@ -1957,24 +1957,24 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx
         }
     }
     auto issue = [&](int sl) {
-        const int st = (qb + sl) & 1;
+        const int st = (qb + sl) % NS, cb = (qb + sl) & 1;
         if (tid == 0) {
-            mbar_expect_tx(&S.bar[st], TmaSmem<T>::kRawBytes);
+            mbar_expect_tx(&S.bar[st], TmaSmem<T, NS>::kRawBytes);
             tma_load_2d(S.raw[st], tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
         }
         if (tid < KA * (kADC / 2)) {
             const int j = tid >> 3, h = tid & 7, d = sl * kADC + 2 * h;
-            if (d < n) cp_async_16(&c64[st][j][2 * h], Cact + static_cast<uint64_t>(j) * ldc + d);
+            if (d < n) cp_async_16(&c64[cb][j][2 * h], Cact + static_cast<uint64_t>(j) * ldc + d);
         }
         cp_async_commit();
     };
     issue(0);
     if (nslab > 1) issue(1);
     for (int sl = 0; sl < nslab; ++sl) {
-        const int q = qb + sl, st = q & 1;
+        const int q = qb + sl, st = q % NS, cb = q & 1;
         if (sl + 1 < nslab) cp_async_wait<1>();
         else cp_async_wait<0>();
-        mbar_wait(&S.bar[st], (q >> 1) & 1);
+        mbar_wait(&S.bar[st], (q / NS) & 1);
         if (qb == 0 && sl < 5) ktrace(16 + 2 * sl, 2);
         __syncthreads();  // everyone's centroid pieces landed
         const int dl = min(kADC, n - sl * kADC);
@@ -1983,7 +1983,7 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx
         for (int r = 0; r < 2; ++r) {
             if (ip[r] < 0) continue;
             const int p = ip[r];
-            const double* cr = c64[st][ij[r]];
+            const double* cr = c64[cb][ij[r]];
             double a = acc[r];
             if (dl == kADC) {
                 if constexpr (sizeof(T) == 4) {
@@ -2023,8 +2023,8 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T>& S, const CUtensorMap* tmx
 // exact distance to the previous label, then the bounds decayed by each
 // label's centroid movement decide which labels need an exact recheck
 // (Elkan-style; the reference's argmin is certified), else the full screen.
-template <typename T>
-__global__ void __launch_bounds__(kSThreads, 3)
+template <typename T, int NS>
+__global__ void __launch_bounds__(kSThreads, NS <= 2 ? 3 : 2)
 k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmc,
              const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
              const double* __restrict__ Cact, int ldc, const int* __restrict__ act_idx,
@@ -2039,16 +2039,15 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
     unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    TmaSmem<T>& S = *reinterpret_cast<TmaSmem<T>*>(smem_al);
-    constexpr unsigned kStageBytes = TmaSmem<T>::kRawBytes + kADC * kSMaxK * sizeof(float);
+    TmaSmem<T, NS>& S = *reinterpret_cast<TmaSmem<T, NS>*>(smem_al);
+    constexpr unsigned kStageBytes = TmaSmem<T, NS>::kRawBytes + kADC * kSMaxK * sizeof(float);
 
     klog_start(10 + hmode);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {  // independent of the previous kernel: overlaps its tail under PDL
         tma_prefetch_map(&tmx);
         tma_prefetch_map(&tmc);
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
+        for (int i = 0; i < NS; ++i) mbar_init(&S.bar[i], 1);
         fence_mbar_init();
     }
     pdl_wait();
@@ -2098,8 +2097,9 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     double* item_d = reinterpret_cast<double*>(reuse + reuse_bytes - kItemCap * (sizeof(double) + 3));
     short* item_p = reinterpret_cast<short*>(item_d + kItemCap);
     signed char* item_j = reinterpret_cast<signed char*>(item_p + kItemCap);
-    static_assert(offsetof(TmaSmem<T>, red_u) - kItemCap * (sizeof(double) + 3) >=
-                      offsetof(TmaSmem<T>, xs) + 2 * kSMaxK * 18 * sizeof(double),
+    using SmemT = TmaSmem<T, NS>;
+    static_assert(offsetof(SmemT, red_u) - kItemCap * (sizeof(double) + 3) >=
+                      offsetof(SmemT, xs) + 2 * kSMaxK * 18 * sizeof(double),
                   "centroid staging of tma_chains overlaps the item list");
     ktrace(0, hmode);
     int qb = 0;  // TMA slabs this CTA has consumed (ring position)
@@ -2425,15 +2425,13 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     {
     __syncthreads();
     auto issue = [&](int sl) {
-        const int st = (qb + sl) & 1;
+        const int st = (qb + sl) % NS;
         mbar_expect_tx(&S.bar[st], kStageBytes);
         tma_load_2d(S.raw[st], &tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
         tma_load_2d(&S.craw[st][0][0], &tmc, &S.bar[st], 0, sl * kADC);
     };
-    if (tid == 0) {
-        issue(0);
-        if (nslab > 1) issue(1);
-    }
+    if (tid == 0)
+        for (int i = 0; i < NS && i < nslab; ++i) issue(i);
 
     float2 tot[2][kAK];
 #pragma unroll
@@ -2445,21 +2443,21 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     const int cp_ = tid & (kABP - 1), chalf = tid >> 7;  // conversion: point, 8-dim half
 
     for (int sl = 0; sl < nslab; ++sl) {
-        const int q = qb + sl, st = q & 1, dl = min(kADC, n - sl * kADC);
-        mbar_wait(&S.bar[st], (q >> 1) & 1);
+        const int q = qb + sl, st = q % NS, xb = q & 1, dl = min(kADC, n - sl * kADC);
+        mbar_wait(&S.bar[st], (q / NS) & 1);
         if (sl < 6) ktrace(1 + sl, hmode);
         // raw (swizzled [p][d], storage type) -> fp32 [d][p], once per element
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int d = 8 * chalf + i;
-            S.xs[st][d][cp_] = static_cast<float>(raw_at<T>(S.raw[st], cp_, d));
+            S.xs[xb][d][cp_] = static_cast<float>(raw_at<T>(S.raw[st], cp_, d));
         }
         if (tid < kADC * kSMaxK / 4) {
             const float4 v = reinterpret_cast<const float4*>(&S.craw[st][0][0])[tid];
-            reinterpret_cast<float4*>(&S.cs[st][0][0])[tid] = v;
+            reinterpret_cast<float4*>(&S.cs[xb][0][0])[tid] = v;
         }
         __syncthreads();  // slab ready; every thread has left slab sl-1 and stage st is free
-        if (tid == 0 && sl + 2 < nslab) issue(sl + 2);
+        if (tid == 0 && sl + NS < nslab) issue(sl + NS);
         if (comp) {
             float2 part[2][kAK];
 #pragma unroll
@@ -2468,8 +2466,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 for (int u = 0; u < kAK; ++u) part[h][u] = make_float2(0.f, 0.f);
 #pragma unroll 4
             for (int d = 0; d < dl; ++d) {
-                const float4 xv = *reinterpret_cast<const float4*>(&S.xs[st][d][4 * lane]);
-                const float4 cv = *reinterpret_cast<const float4*>(&S.cs[st][d][4 * warp]);
+                const float4 xv = *reinterpret_cast<const float4*>(&S.xs[xb][d][4 * lane]);
+                const float4 cv = *reinterpret_cast<const float4*>(&S.cs[xb][d][4 * warp]);
                 const float2 xa = make_float2(xv.x, xv.y), xb = make_float2(xv.z, xv.w);
                 part[0][0] = ffma2(xa, cv.x, part[0][0]);
                 part[0][1] = ffma2(xa, cv.y, part[0][1]);
@@ -2487,12 +2485,12 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         }
         if (normw) {
             for (int d = 0; d < dl; ++d) {
-                const float4 xv = *reinterpret_cast<const float4*>(&S.xs[st][d][4 * lane]);
+                const float4 xv = *reinterpret_cast<const float4*>(&S.xs[xb][d][4 * lane]);
                 nxl[0] = __fmaf_rd(xv.x, xv.x, nxl[0]); nxh[0] = __fmaf_ru(xv.x, xv.x, nxh[0]);
                 nxl[1] = __fmaf_rd(xv.y, xv.y, nxl[1]); nxh[1] = __fmaf_ru(xv.y, xv.y, nxh[1]);
                 nxl[2] = __fmaf_rd(xv.z, xv.z, nxl[2]); nxh[2] = __fmaf_ru(xv.z, xv.z, nxh[2]);
                 nxl[3] = __fmaf_rd(xv.w, xv.w, nxl[3]); nxh[3] = __fmaf_ru(xv.w, xv.w, nxh[3]);
-                const float c = S.cs[st][d][lane];
+                const float c = S.cs[xb][d][lane];
                 ncl = __fmaf_rd(c, c, ncl);
                 nch = __fmaf_ru(c, c, nch);
             }
@@ -3116,8 +3114,8 @@ k_final(const __grid_constant__ CUtensorMap tmx, const T* __restrict__ X, uint64
     }
 }
 
-template <typename T>
-constexpr size_t tma_smem_bytes() { return sizeof(TmaSmem<T>) + 1024; }
+template <typename T, int NS = 2>
+constexpr size_t tma_smem_bytes() { return sizeof(TmaSmem<T, NS>) + 1024; }
 
 // ===========================================================================
 // 4. Per-tile sequential sums (block_sum inner loop core.cpp:167-173).
