@@ -17,8 +17,9 @@ import paper_2204_07485_b200 as bm  # noqa: E402
 from paper_2204_07485_b200 import synthetic  # noqa: E402
 
 chunks = int(sys.argv[1]) if len(sys.argv) > 1 else 60
-w = synthetic.CONFIGS["c2"]
-d = bm.Dataset(synthetic.generate("c2"))
+KEY = os.environ.get("KLOG_CONFIG", "c2")
+w = synthetic.CONFIGS[KEY]
+d = bm.Dataset(synthetic.generate(KEY))
 cfg = bm.BigMeansConfig(k=w.k, chunk_size=w.s, max_chunks=chunks, seed=0)
 bm.big_means(d, cfg, want_labels=False)
 buf = np.zeros(540000, np.uint64)
