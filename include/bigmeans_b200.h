@@ -105,6 +105,9 @@ bm_status bm_dataset_shape(const bm_dataset* data, uint64_t* m, uint64_t* n);
 /* Device storage type: fp64 input whose every value is exactly representable
  * in fp32 is stored as fp32 (lossless; results unchanged). */
 bm_status bm_dataset_storage(const bm_dataset* data, bm_dtype* storage);
+/* io::min_max_normalize io.hpp:38 / io.cpp:245-264 on the device: per column
+ * (x - min) / (max - min), constant columns 0.0; a new dataset. */
+bm_status bm_dataset_min_max_normalize(const bm_dataset* data, bm_dataset** out);
 /* Exact-sum property (no reference counterpart; it changes no result): every
  * value is an integer multiple of 2^exponent and m * max|x| < 2^52 * 2^exponent,
  * so the ordered fp64 sums of update_centroids (core.cpp:206-229) are exact and

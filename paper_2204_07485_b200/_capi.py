@@ -66,6 +66,7 @@ PROTOS = {
     "bm_dataset_storage": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "bm_dataset_sum_mode": (C.c_int, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "bm_dataset_gather": (C.c_int, [vp, P_u64, u64, C.POINTER(vp)]),
+    "bm_dataset_min_max_normalize": (C.c_int, [vp, C.POINTER(vp)]),
     "bm_dataset_download": (C.c_int, [vp, P_dbl]),
     "bm_rng_create": (C.c_int, [u64, C.POINTER(vp)]),
     "bm_rng_destroy": (C.c_int, [vp]),

@@ -139,6 +139,12 @@ class Dataset:
         _check(self._lib.bm_dataset_sum_mode(self._h, C.byref(a), C.byref(e)))
         return bool(a.value), int(e.value)
 
+    def min_max_normalize(self) -> "Dataset":
+        """io::min_max_normalize (io.cpp:245-264) on the device: a new dataset."""
+        h = C.c_void_p()
+        _check(self._lib.bm_dataset_min_max_normalize(self._h, C.byref(h)))
+        return Dataset(None, device=self.device, _handle=h)
+
     def gather(self, rows) -> "Dataset":
         """New dataset holding the listed rows in the listed order (core.cpp:34-44)."""
         idx = np.ascontiguousarray(rows, dtype=np.uint64)

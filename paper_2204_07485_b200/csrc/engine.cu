@@ -2424,6 +2424,42 @@ bm_status bm_dataset_sum_mode(const bm_dataset* d, int32_t* exact, int32_t* expo
     });
 }
 
+bm_status bm_dataset_min_max_normalize(const bm_dataset* d, bm_dataset** out) {
+    return guarded([&] {
+        *out = nullptr;
+        DeviceGuard g(d->device);
+        cudaStream_t st = stream_of(d);
+        const int n = (int)d->n;
+        DevBuf<unsigned long long> lo(n), hi(n);
+        BM_CUDA(cudaMemsetAsync(lo.p, 0xFF, n * sizeof(unsigned long long), st));
+        BM_CUDA(cudaMemsetAsync(hi.p, 0, n * sizeof(unsigned long long), st));
+        DevBuf<double> tmp(d->m * d->n);
+        dispatch(d->dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int threads = std::max(1, 256 / n) * n;  // whole rows per CTA pass
+            if (n <= 256) {
+                dev::k_col_minmax<T><<<592, threads, 0, st>>>(static_cast<const T*>(d->X), d->m, n, d->ld, lo.p,
+                                                               hi.p);
+            } else {
+                for (int c0 = 0; c0 < n; c0 += 256) {  // column blocks of 256 (one row per thread group)
+                    const int nc = std::min(256, n - c0);
+                    dev::k_col_minmax<T><<<592, nc, 0, st>>>(static_cast<const T*>(d->X) + c0, d->m, nc, d->ld,
+                                                              lo.p + c0, hi.p + c0);
+                }
+            }
+            BM_LAUNCH();
+            dev::k_minmax_apply<T><<<1184, 256, 0, st>>>(static_cast<const T*>(d->X), d->m, n, d->ld, lo.p, hi.p,
+                                                         tmp.p);
+            BM_LAUNCH();
+        });
+        std::vector<double> host(d->m * d->n);  // the normalized values re-enter through the dataset checks
+        BM_CUDA(cudaMemcpyAsync(host.data(), tmp.p, host.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        const bm_status s = bm_dataset_create(host.data(), d->m, d->n, BM_F64, d->device, out);
+        if (s != BM_OK) throw StateError(bm_last_error());
+    });
+}
+
 bm_status bm_dataset_shape(const bm_dataset* d, uint64_t* m, uint64_t* n) {
     return guarded([&] {
         *m = d->m;

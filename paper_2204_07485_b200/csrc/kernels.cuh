@@ -3983,6 +3983,50 @@ k_kpar_reduce(const double* __restrict__ Cc, int n, const unsigned long long* __
 }
 
 // ===========================================================================
+// 8c. io::min_max_normalize (io.cpp:245-264) on the device: per-column min and
+// max (exact), then (x - lo) / (hi - lo), constant columns -> 0.0.
+// ===========================================================================
+__device__ __forceinline__ unsigned long long ordered_bits(double v) {  // total order of doubles as integers
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_ordered(unsigned long long o) {
+    return __longlong_as_double(static_cast<long long>((o >> 63) ? (o & 0x7FFFFFFFFFFFFFFFull) : ~o));
+}
+
+template <typename T>
+__global__ void k_col_minmax(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+                             unsigned long long* __restrict__ lo, unsigned long long* __restrict__ hi) {
+    // grid-stride over rows; each thread keeps one column's running min / max
+    const int d = threadIdx.x % n;  // blockDim.x is a multiple of n (host)
+    const int lanes = blockDim.x / n, li = threadIdx.x / n;
+    if (li >= lanes) return;
+    unsigned long long a = ~0ull, b = 0ull;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * lanes + li; i < rows;
+         i += static_cast<uint64_t>(gridDim.x) * lanes) {
+        const unsigned long long o = ordered_bits(to_f64(X[i * ld + d]));
+        a = o < a ? o : a;
+        b = o > b ? o : b;
+    }
+    atomicMin(&lo[d], a);
+    atomicMax(&hi[d], b);
+}
+
+template <typename T>
+__global__ void k_minmax_apply(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
+                               const unsigned long long* __restrict__ lo, const unsigned long long* __restrict__ hi,
+                               double* __restrict__ out) {  // out: rows x n, row-major (host layout)
+    const uint64_t total = rows * static_cast<uint64_t>(n);
+    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int d = static_cast<int>(e % n);
+        const double l = from_ordered(lo[d]), h = from_ordered(hi[d]);
+        const double range = __dsub_rn(h, l);
+        out[e] = range > 0.0 ? __ddiv_rn(__dsub_rn(to_f64(X[(e / n) * ld + d]), l), range) : 0.0;
+    }
+}
+
+// ===========================================================================
 // 9. Dataset helpers.
 // ===========================================================================
 // Exact-sum statistics (§5b) of one finite value: exponent of its lowest set

@@ -199,3 +199,21 @@ def test_lossless_fp32_storage():
     assert (d.values() == Xi).all()
     with pytest.raises(bm.ConfigError):
         bm.Dataset(np.array([[1.0, np.nan]]))
+
+
+@pytest.mark.parametrize("shape,dtype", [((5000, 7), np.float64), ((3000, 300), np.float32), ((777, 1), np.float64)])
+def test_min_max_normalize(shape, dtype):
+    """io::min_max_normalize (io.cpp:245-264): (x - lo) / (hi - lo) per column, constant
+    columns 0.0 — restated with numpy float64 (IEEE, no contraction)."""
+    r = np.random.default_rng(3)
+    X = (r.normal(size=shape) * r.uniform(0.1, 50, shape[1]) + r.normal(size=shape[1]) * 10).astype(dtype)
+    X[:, 0] = 2.5  # a constant column
+    if shape[1] > 2:
+        X[:, 2] = np.rint(X[:, 2])
+    Y = bm.Dataset(X).min_max_normalize().values()
+    Xd = X.astype(np.float64)
+    lo, hi = Xd.min(axis=0), Xd.max(axis=0)
+    rng_ = hi - lo
+    with np.errstate(invalid="ignore", divide="ignore"):
+        ref = np.where(rng_ > 0.0, (Xd - lo) / rng_, 0.0)
+    assert (bits(Y) == bits(ref)).all()
