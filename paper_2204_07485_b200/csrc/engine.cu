@@ -803,7 +803,7 @@ void launch_tile_sums(cudaStream_t st, const double* v, uint64_t count, uint64_t
                       double* tiles, const int* stop) {
     const uint64_t blocks = tiles_of(count) * narrays;
     if (blocks == 0) return;
-    dev::k_tile_sums<<<(unsigned)blocks, 256, 0, st>>>(v, count, stride, narrays, tiles, stop);
+    launch_pdl(dev::k_tile_sums, (unsigned)blocks, 256, 0, st, v, count, stride, narrays, tiles, stop);
     BM_LAUNCH();
     count_launch();
 }
@@ -1065,8 +1065,8 @@ void launch_dist_rows(cudaStream_t st, const Points& P, const uint32_t* cand, in
     const dim3 grid((unsigned)ceil_div(P.rows, 128), (unsigned)std::max(1, ncand));
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
-        dev::k_dist_rows<T><<<grid, 128, 0, st>>>(static_cast<const T*>(P.X), P.rows, P.n, P.ld, cand,
-                                                  ncand, d2, out, skip);
+        launch_pdl(dev::k_dist_rows<T>, grid, 128, 0, st, static_cast<const T*>(P.X), P.rows, P.n, P.ld, cand,
+                   ncand, d2, out, skip);
     });
     BM_LAUNCH();
     count_launch();
@@ -1124,23 +1124,23 @@ void kmeanspp_fill_device(cudaStream_t st, const Points& P, Workspace& w, std::v
         BM_CUDA(cudaMemsetAsync(w.pps.p, 0, sizeof(dev::PPState), st));
         const unsigned cgrid = (unsigned)std::min<uint64_t>(ceil_div(m, 256), 296);
         for (size_t q = first_slot; q < degenerate.size(); ++q) {
-            dev::k_pp_scan<<<(unsigned)ceil_div(m, dev::kPPThreads), dev::kPPThreads, 0, st>>>(
-                buf(d2i), m, w.pprefix.p, w.pptiles.p, w.pps.p);
+            launch_pdl(dev::k_pp_scan, (unsigned)ceil_div(m, dev::kPPThreads), dev::kPPThreads, 0, st,
+                       (const double*)buf(d2i), m, w.pprefix.p, w.pptiles.p, w.pps.p);
             BM_LAUNCH();
-            dev::k_pp_pick<<<1, dev::kPPThreads, 0, st>>>(m, w.ppmt.p, candidates, w.cand.p, w.pprefix.p,
-                                                          w.pptiles.p, w.pps.p);
+            launch_pdl(dev::k_pp_pick, 1, dev::kPPThreads, 0, st, m, w.ppmt.p, candidates, w.cand.p,
+                       (const long long*)w.pprefix.p, (const long long*)w.pptiles.p, w.pps.p);
             BM_LAUNCH();
             // (skipped after a fallback or a direct pick: the first two PPState fields)
             launch_dist_rows(st, P, w.cand.p, candidates, buf(d2i), buf(0), &w.pps.p->fallback);  // :186-189
             launch_tile_sums(st, buf(0), m, w.R, candidates, w.tile_buf.p, &w.pps.p->fallback);  // :190
             dispatch(P.dtype, [&](auto tag) {
                 using T = decltype(tag);
-                dev::k_pp_best<T><<<1, 128, 0, st>>>(w.tile_buf.p, ntiles, candidates, w.cand.p, w.pps.p,
-                                                     static_cast<const T*>(P.X), P.ld, P.n, w.C.p, w.mask.p,
-                                                     degenerate[q]);
+                launch_pdl(dev::k_pp_best<T>, 1, 128, 0, st, (const double*)w.tile_buf.p, ntiles, candidates,
+                           (const uint32_t*)w.cand.p, w.pps.p, static_cast<const T*>(P.X), P.ld, P.n, w.C.p,
+                           w.mask.p, degenerate[q]);
             });
             BM_LAUNCH();
-            dev::k_pp_take<<<cgrid, 256, 0, st>>>(w.d2pool.p, w.R, m, d2i, w.pps.p);
+            launch_pdl(dev::k_pp_take, cgrid, 256, 0, st, w.d2pool.p, w.R, m, d2i, (const dev::PPState*)w.pps.p);
             BM_LAUNCH();
             count_launch(3);
         }

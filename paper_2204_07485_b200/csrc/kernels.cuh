@@ -3124,6 +3124,7 @@ constexpr size_t tma_smem_bytes() { return sizeof(TmaSmem<T, NS>) + 1024; }
 // ===========================================================================
 __global__ void k_tile_sums(const double* __restrict__ v, uint64_t count, uint64_t stride,
                             int narrays, double* __restrict__ tiles, const int* __restrict__ stop_ptr) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
     // one CTA per (array, tile): coalesced staging, then a single-thread fold
     __shared__ __align__(16) double sm[kTile];
     if (stop_ptr && *stop_ptr) return;
@@ -3576,6 +3577,7 @@ template <typename T>
 __global__ void k_dist_rows(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld,
                             const uint32_t* __restrict__ cand, int ncand,
                             const double* __restrict__ d2, double* __restrict__ out, const int* skip) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= rows) return;
     if (skip && (skip[0] || skip[1])) return;  // device K-means++ step: fallback or direct pick
@@ -3636,6 +3638,7 @@ constexpr int kPPThreads = 1024;
 __global__ void __launch_bounds__(kPPThreads)
 k_pp_scan(const double* __restrict__ d2, uint64_t m, long long* __restrict__ prefix,
           long long* __restrict__ tile_tot, PPState* ps) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
     __shared__ long long wsum[kPPThreads / 32];
     if (ps->fallback) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -3679,6 +3682,7 @@ k_pp_scan(const double* __restrict__ d2, uint64_t m, long long* __restrict__ pre
 __global__ void __launch_bounds__(kPPThreads)
 k_pp_pick(uint64_t m, Mt64State* __restrict__ mt, int candidates, uint32_t* __restrict__ cand,
           const long long* __restrict__ prefix, const long long* __restrict__ tile_tot, PPState* ps) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
     __shared__ uint64_t xs[kMtN];
     __shared__ long long toff[kPPThreads + 1];
     __shared__ double us[8];
@@ -3749,6 +3753,7 @@ template <typename T>
 __global__ void k_pp_best(const double* __restrict__ tiles, uint64_t ntiles, int candidates,
                           const uint32_t* __restrict__ cand, PPState* ps, const T* __restrict__ X, uint64_t ld,
                           int n, double* __restrict__ C, uint8_t* __restrict__ mask, int slot) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
     __shared__ long long row_s;
     __shared__ __align__(16) double tl[4 * 1024];
     if (ps->fallback) return;
@@ -3786,6 +3791,7 @@ __global__ void k_pp_best(const double* __restrict__ tiles, uint64_t ntiles, int
 
 // dist2 := best_trial (:198)
 __global__ void k_pp_take(double* __restrict__ pool, uint64_t R, uint64_t m, int d2i, const PPState* ps) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
     if (ps->fallback || ps->direct || ps->best < 0) return;
     const double* src = pool + static_cast<uint64_t>(ps->best) * R;
     double* dst = pool + static_cast<uint64_t>(d2i) * R;
