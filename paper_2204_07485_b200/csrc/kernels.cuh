@@ -1668,7 +1668,9 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     const int tid = threadIdx.x;
     const int which = ctl.sum_which >= 0 ? ctl.sum_which : ctl.st->sum_sel;
     // this CTA's copy: [kSumCopies][kSMaxK][n] sums, then [kSumCopies][kSMaxK] counts
-    const int cp = static_cast<int>(blk % kSumCopies);
+    // (a begin spreads its atomics over the copies, which its control CTA then
+    // folds into copy 0; a round's few moves go to copy 0 directly)
+    const int cp = full ? static_cast<int>(blk % kSumCopies) : 0;
     long long* half = ctl.sums + static_cast<uint64_t>(which) * ctl.sum_half;
     long long* sg = half + static_cast<uint64_t>(cp) * kSMaxK * n;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n +
@@ -1775,6 +1777,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
             const long long c = (pc[tid + 1] - pc[tid]) - (mc[tid + 1] - mc[tid]);
             if (c != 0) atomicAdd(&cnt[tid], static_cast<unsigned long long>(c));
         }
+        __threadfence();  // this CTA's atomics before its arrival
         return;
     }
     // A begin: the partials of 8 CTAs are merged by the last of them (8x fewer
@@ -1807,6 +1810,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
         }
     }
     if (tid == 0) ctl.grp_ctr[g] = 0u;
+    __threadfence();  // this CTA's atomics before its arrival (the control CTA folds the copies)
 }
 
 // Exact-sum mode update (update_centroids core.cpp:183-244 via §5b): the
@@ -1825,7 +1829,7 @@ __device__ __noinline__ void centroids_from_sums(const long long* __restrict__ h
         long long c = 0;
         if (lane < k)
 #pragma unroll
-            for (int q = 0; q < kSumCopies; ++q) c += __ldcg(cnts + q * kSMaxK + lane);
+            c = __ldcg(cnts + lane);  // copy 0 (the begin's control CTA folded the others into it)
         const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
         if (lane < k) {
             tot[lane] = c;
@@ -1848,9 +1852,7 @@ __device__ __noinline__ void centroids_from_sums(const long long* __restrict__ h
         const int rk = rank[j];
         double sq = 0.0;
         for (int d = lane; d < n; d += 32) {
-            long long s = 0;
-#pragma unroll
-            for (int q = 0; q < kSumCopies; ++q) s += __ldcg(half + (static_cast<uint64_t>(q) * kSMaxK * n) + row + d);
+            const long long s = __ldcg(half + row + d);  // copy 0
             const double sum = __dmul_rn(static_cast<double>(s), unscale);  // exact (§5b)
             const double v = __dmul_rn(sum, inv);
             const double dv = __dsub_rn(v, C[row + d]);
@@ -1863,6 +1865,27 @@ __device__ __noinline__ void centroids_from_sums(const long long* __restrict__ h
         for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
         if (lane == 0) delta[j] = __double2float_ru(__dsqrt_ru(sq * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
     }
+}
+
+// A begin's control CTA: copies 1..7 of the half folded into copy 0 and zeroed
+// (CTA-wide; exact integer adds), so later readers touch one copy.
+__device__ __noinline__ void fold_sum_copies(long long* half, int k, int n) {
+    const uint64_t span = static_cast<uint64_t>(kSMaxK) * n;
+    long long* cnts = half + static_cast<uint64_t>(kSumCopies) * span;
+    const int kn = k * n;
+    for (int e = threadIdx.x; e < kn + k; e += blockDim.x) {
+        const bool is_cnt = e >= kn;
+        long long* base = is_cnt ? cnts + (e - kn) : half + e;
+        const uint64_t stride = is_cnt ? static_cast<uint64_t>(kSMaxK) : span;
+        long long v = __ldcg(base);
+#pragma unroll
+        for (int q = 1; q < kSumCopies; ++q) v += __ldcg(base + q * stride);
+        *base = v;
+#pragma unroll
+        for (int q = 1; q < kSumCopies; ++q) base[q * stride] = 0;
+    }
+    __threadfence();
+    __syncthreads();
 }
 
 // The fused form (LloydCtl::sum_fuse): the live half of this chunk buffer's sums.
@@ -2805,6 +2828,9 @@ fold:
         ktrace(5, hmode);
         if (ctl.host_st && (decision >= 0 || sst->incomplete)) status_to_host(sst, ctl.host_st);
         ktrace(30, hmode);
+        // a begin's sums: its copies folded into copy 0 (off the critical path for a speculative begin)
+        if (ctl.sums && ctl.mode == 1)
+            fold_sum_copies(ctl.sums + static_cast<uint64_t>(sst->sum_sel) * ctl.sum_half, kfull, n);
         // fused exact-sum update: the next round's centroids when the loop goes on
         if (ctl.sum_fuse && !sst->stop && !sst->state_error)
             centroids_fused(ctl, sst->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
