@@ -1906,6 +1906,29 @@ __device__ __forceinline__ T raw_at(const unsigned char* raw, int p, int d) {
     }
 }
 
+// One thread's share of a slab conversion: point p, dims 8h..8h+7 of the
+// swizzled TMA slab (f32: 64-byte rows, SWIZZLE_64B; f64: 128-byte rows,
+// SWIZZLE_128B) as 16-byte vector loads, into the fp32 [d][p] slab.
+template <typename T>
+__device__ __forceinline__ void convert_slab_part(const unsigned char* raw, float (*xs)[kABP], int p, int h) {
+    if constexpr (sizeof(T) == 4) {
+        const int sw = (p >> 1) & 3;
+        const float4 a = *reinterpret_cast<const float4*>(raw + p * 64 + (((2 * h) ^ sw) << 4));
+        const float4 b = *reinterpret_cast<const float4*>(raw + p * 64 + (((2 * h + 1) ^ sw) << 4));
+        float* o = &xs[8 * h][p];
+        o[0 * kABP] = a.x; o[1 * kABP] = a.y; o[2 * kABP] = a.z; o[3 * kABP] = a.w;
+        o[4 * kABP] = b.x; o[5 * kABP] = b.y; o[6 * kABP] = b.z; o[7 * kABP] = b.w;
+    } else {
+        const int sw = p & 7;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double2 v = *reinterpret_cast<const double2*>(raw + p * 128 + (((4 * h + c) ^ sw) << 4));
+            xs[8 * h + 2 * c][p] = static_cast<float>(v.x);
+            xs[8 * h + 2 * c + 1][p] = static_cast<float>(v.y);
+        }
+    }
+}
+
 // Exact fp64 distance of one stored row to one centroid row: the reference's
 // sequential chain (core.cpp:142-146) with vector loads (rows are 16-byte aligned
 // whenever the TMA path runs: TMA strides are multiples of 16 bytes).
@@ -2470,11 +2493,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         mbar_wait(&S.bar[st], (q / NS) & 1);
         if (sl < 6) ktrace(1 + sl, hmode);
         // raw (swizzled [p][d], storage type) -> fp32 [d][p], once per element
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int d = 8 * chalf + i;
-            S.xs[xb][d][cp_] = static_cast<float>(raw_at<T>(S.raw[st], cp_, d));
-        }
+        convert_slab_part<T>(S.raw[st], S.xs[xb], cp_, chalf);
         if (tid < kADC * kSMaxK / 4) {
             const float4 v = reinterpret_cast<const float4*>(&S.craw[st][0][0])[tid];
             reinterpret_cast<float4*>(&S.cs[xb][0][0])[tid] = v;
@@ -2941,11 +2960,7 @@ k_final(const __grid_constant__ CUtensorMap tmx, const T* __restrict__ X, uint64
             const int dl = min(kADC, n - d0);
             mbar_wait(&S.bar[st], static_cast<unsigned>((q / NS) & 1));
             float(*xsl)[kABP] = &S.xs[d0];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int d = 8 * chalf + i;
-                if (d0 + d < kFMaxD) xsl[d][cp_] = static_cast<float>(raw_at<T>(S.raw[st], cp_, d));
-            }
+            convert_slab_part<T>(S.raw[st], xsl, cp_, chalf);
             __syncthreads();  // slab converted; stage st is free
             if (tid == 0 && q + NS < total_q) issue(q + NS);
             if (comp) {
