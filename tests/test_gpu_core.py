@@ -165,7 +165,8 @@ def test_screen_adversarial_bitwise(port, case):
                                      ("BM_STORAGE", "native"), ("BM_SCREEN", "v4"),
                                      ("BM_HAMERLY", "0"), ("BM_FORCE_EXACT_CONTROL", "1"),
                                      ("BM_SPEC", "0"), ("BM_PDL", "0"), ("BM_PP", "host"),
-                                     ("BM_SUMS", "0"), ("BM_SUMS_FUSE", "0")])
+                                     ("BM_SUMS", "0"), ("BM_SUMS_FUSE", "0"), ("BM_SPEC_CTAS", "40"),
+                                     ("BM_FINAL", "tma")])
 def test_engine_modes_agree(var, alt):
     """Unscreened assignment (BM_ASSIGN_MODE=exact) and the host-driven chunk
     loop (BM_GRAPHS=0) give the same bits as the default path, in fresh processes."""
@@ -217,3 +218,26 @@ def test_min_max_normalize(shape, dtype):
     with np.errstate(invalid="ignore", divide="ignore"):
         ref = np.where(rng_ > 0.0, (Xd - lo) / rng_, 0.0)
     assert (bits(Y) == bits(ref)).all()
+
+
+@pytest.mark.parametrize("var,alt", [("BM_RING", "2"), ("BM_SPEC_CTAS", "24")])
+def test_engine_modes_agree_wide_rows(var, alt):
+    """Rows wider than 8 slabs (6-stage TMA ring) against the 2-stage ring, and
+    speculative begins looping over their blocks: same bits, fresh processes."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "import paper_2204_07485_b200 as bm;"
+        "X = np.random.default_rng(6).normal(size=(9000, 200)).astype(np.float32);"
+        "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=9, chunk_size=2500, max_chunks=5, seed=2));"
+        "import hashlib; print(repr(o.objective), o.counter.distance_evals, o.counter.iterations,"
+        " hashlib.sha1(o.centroids.values.tobytes()).hexdigest(), repr(t.records))")
+    env = dict(os.environ)
+    outs = []
+    for mode in (None, alt):
+        env.pop(var, None)
+        if mode is not None:
+            env[var] = mode
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                                   text=True, check=True).stdout)
+    assert outs[0] == outs[1] and outs[0]
