@@ -1663,7 +1663,7 @@ __device__ __forceinline__ long long sum_units(double x, double scale) {
 template <typename T, int NS>
 __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, const T* __restrict__ X, uint64_t ld,
                                         int n, uint64_t p0, int np, bool full, int kfull, unsigned char* scratch,
-                                        size_t scratch_bytes, unsigned blk) {
+                                        size_t scratch_bytes, unsigned blk, const float* pre) {
     __syncthreads();  // every point's (new, old) label recorded; the scratch area is free
     const int tid = threadIdx.x;
     const int which = ctl.sum_which >= 0 ? ctl.sum_which : ctl.st->sum_sel;
@@ -1713,7 +1713,9 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     // stage the moved rows (whole 16-byte vectors) with cp.async
     constexpr int kV = 16 / sizeof(T);
     const int vpr = static_cast<int>((n + kV - 1) / kV);
-    const bool staged = (ld % kV) == 0 && static_cast<size_t>(nm) * vpr * 16 <= scratch_bytes;
+    // pre: every row of the block already in shared memory (the full screen's
+    // staged fp32 rows, [p][ld]); else the moved rows are staged here
+    const bool staged = !pre && (ld % kV) == 0 && static_cast<size_t>(nm) * vpr * 16 <= scratch_bytes;
     T* xs = reinterpret_cast<T*>(scratch);
     if (staged) {
         for (int e = tid; e < np * vpr; e += blockDim.x) {
@@ -1754,7 +1756,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     const bool grouped = full && ctl.parts;
     const uint64_t slot_len = static_cast<uint64_t>(kSMaxK) * n + kSMaxK;
     long long* slot = grouped ? ctl.parts + blk * slot_len : nullptr;
-    const T* Xb = staged ? xs : X + p0 * ld;
+    const T* Xb = pre ? reinterpret_cast<const T*>(pre) : staged ? xs : X + p0 * ld;
     const uint64_t rs = staged ? static_cast<uint64_t>(vpr) * kV : ld;  // row stride of Xb
     for (int e = tid; e < kfull * n; e += blockDim.x) {
         const int j = e / n, d = e - j * n;
@@ -2155,6 +2157,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     for (unsigned blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const uint64_t p0 = static_cast<uint64_t>(blk) * kABP;
     const int np = p0 < rows ? static_cast<int>(min(static_cast<uint64_t>(kABP), rows - p0)) : 0;
+    const float* pre_rows = nullptr;  // the full screen's staged fp32 rows ([128][ld]), for the label sums
     if (np == 0) {  // fixup CTA of a round-1 launch: one tile of the pending chunk's final distances
         const GState* gst = ctl.gs;
         const int pend = gst->pending_fix;
@@ -2308,6 +2311,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                         *reinterpret_cast<const float4*>(&S.lbs[p][4 * ((c ^ p) & 7)]);
                 }
                 ktrace(15, hmode);
+                pre_rows = xr;  // the label sums read the moved rows from here
                 goto fold;
             }
             // many rechecks: the full screen below rewrites everything; its TMA
@@ -2552,6 +2556,22 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
     __syncthreads();
     ktrace(7, hmode);
+    // fp32 rows that fit the freed slab buffers: fetched now with cp.async,
+    // landing while the bounds are computed; the exact rechecks and the label
+    // sums then read them from shared memory
+    float* const xrow = reinterpret_cast<float*>(reuse);
+    const int ldr = static_cast<int>(ld);
+    const bool pre = sizeof(T) == 4 && static_cast<size_t>(kABP) * ld * 4 <=
+                                           static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse);
+    if (pre) {
+        pre_rows = xrow;
+        const int vpr = ldr / 4;
+        for (int e = tid; e < np * vpr; e += kSThreads) {
+            const int p = e / vpr, v = e - p * vpr;
+            cp_async_16(xrow + p * ldr + 4 * v, X + (p0 + p) * ld + 4 * v);
+        }
+        cp_async_commit();
+    }
     // certified bounds: upper bounds first, then each warp tests its lower
     // bounds against the point's minimum U and sets candidate bits.
     float Lk[4][kAK];
@@ -2644,7 +2664,13 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                 ++it;
             }
         }
-        if (NI > static_cast<uint32_t>(kSThreads)) {
+        if (pre) {  // the rows from shared memory (up to 2 items per thread)
+            cp_async_wait<0>();
+            __syncthreads();
+            for (uint32_t i = tid; i < NI; i += kSThreads)
+                item_d[i] = chain_smem_row(xrow + item_p[i] * ldr, Cact + static_cast<uint64_t>(item_j[i]) * ldc, n);
+            __syncthreads();
+        } else if (NI > static_cast<uint32_t>(kSThreads)) {
             tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, NI, item_p, item_j, item_d);
             qb += nslab;
         } else {  // one item per thread, rows straight from L2
@@ -2654,6 +2680,10 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                                              Cact + static_cast<uint64_t>(item_j[tid]) * ldc, n);
             __syncthreads();
         }
+    }
+    if (pre && overflow) {  // (the rows are still read by the label sums)
+        cp_async_wait<0>();
+        __syncthreads();
     }
     ktrace(9, hmode);
     if (tid < np) {
@@ -2692,7 +2722,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
     if (hmode >= 1 && lbk) {  // per (point, label) lower bounds in distance units, staged for coalesced rows
         __syncthreads();
-        float* lbt = reinterpret_cast<float*>(&S.raw[0][0]);  // [128][32], column j ^ (p & 31)
+        // [128][32], column j ^ (p & 31); the staged rows keep the slab buffers
+        float* lbt = pre ? reinterpret_cast<float*>(&S.lbs[0][0]) : reinterpret_cast<float*>(&S.raw[0][0]);
         if (comp) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -2720,7 +2751,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
 fold:
     ktrace(10, hmode);
     if (ctl.sums && np > 0) label_sums<T>(S, ctl, X, ld, n, p0, np, labels_old == nullptr, kfull, reuse,
-                                          static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse), blk);
+                                          static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse), blk,
+                                          pre_rows);
     ktrace(31, hmode);
     if (ctl.fast) {  // unordered CTA sum -> st->fsum; the last CTA runs the control
         __syncthreads();  // distances of this CTA written (some by other threads)
