@@ -1869,6 +1869,63 @@ __device__ __noinline__ void centroids_from_sums(const long long* __restrict__ h
     }
 }
 
+// The same for one label j per CTA (many CTAs in parallel: the begin that
+// finds the speculative one current): every CTA ranks the labels from the
+// counts; CTA 0 also writes the mask, the active list and their count.
+__device__ __noinline__ void centroid_of_label(const long long* __restrict__ half, int k, int n, double unscale,
+                                               double* __restrict__ C, uint8_t* __restrict__ mask,
+                                               double* __restrict__ Cact, int ldc, int* __restrict__ act_idx,
+                                               int* __restrict__ n_active, float* __restrict__ CT32,
+                                               float* __restrict__ delta, int j, double* red) {
+    const long long* cnts = half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    __shared__ long long cj;
+    __shared__ int rj;
+    if (warp == 0) {
+        const long long c = lane < k ? __ldcg(cnts + lane) : 0;
+        const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
+        const int r = __popc(live & ((1u << lane) - 1u));
+        if (lane == j) {
+            cj = c;
+            rj = c > 0 ? r : -1;
+        }
+        if (blockIdx.x == 0 && lane < k) {
+            mask[lane] = c > 0 ? 0 : 1;
+            if (c > 0) act_idx[r] = lane;
+            if (lane == 0) *n_active = __popc(live);
+        }
+    }
+    __syncthreads();
+    const long long c = cj;
+    const uint64_t row = static_cast<uint64_t>(j) * n;
+    if (c <= 0) {
+        for (int d = tid; d < n; d += blockDim.x) C[row + d] = 0.0;
+        return;
+    }
+    const double inv = __ddiv_rn(1.0, static_cast<double>(c));
+    const int rk = rj;
+    double sq = 0.0;
+    for (int d = tid; d < n; d += blockDim.x) {
+        const long long sv = __ldcg(half + row + d);  // copy 0
+        const double sum = __dmul_rn(static_cast<double>(sv), unscale);  // exact (§5b)
+        const double v = __dmul_rn(sum, inv);
+        const double dv = __dsub_rn(v, C[row + d]);
+        sq = __dadd_rn(sq, __dmul_rn(dv, dv));  // order-free: only bounds use it
+        C[row + d] = v;
+        Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
+        if (CT32) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        delta[j] = __double2float_ru(__dsqrt_ru(t * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+    }
+}
+
 // A begin's control CTA: copies 1..7 of the half folded into copy 0 and zeroed
 // (CTA-wide; exact integer adds), so later readers touch one copy.
 __device__ __noinline__ void fold_sum_copies(long long* half, int k, int n) {
@@ -2112,8 +2169,14 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                                    static_cast<long long>(*reinterpret_cast<const volatile long long*>(&ctl.gs->inc_version))) {
         // the speculative begin of this chunk is current; with the fused exact-sum
         // update CTA 0 turns its sums into round 1's centroids
-        if (ctl.sum_fuse && blockIdx.x == 0)
-            centroids_fused(ctl, ctl.st->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
+        if (ctl.sum_fuse) {  // a label per CTA (round 1's centroids)
+            const long long* half = ctl.sums + static_cast<uint64_t>(ctl.st->sum_sel) * ctl.sum_half;
+            for (int j = static_cast<int>(blockIdx.x); j < kfull; j += static_cast<int>(gridDim.x)) {
+                centroid_of_label(half, kfull, n, ctl.sum_unscale, ctl.cC, ctl.cmask, ctl.cCact, ctl.cldc, ctl.cact,
+                                  ctl.cn_active, ctl.cCT32, ctl.cdelta, j, reinterpret_cast<double*>(&S.red_u[0][0]));
+                __syncthreads();
+            }
+        }
         klog_exit(10 + hmode);
         return;
     }
