@@ -161,6 +161,7 @@ struct Workspace {
     bool sums_on = false;
     double sum_scale = 1.0, sum_unscale = 1.0;
     bool sums_fuse = false;  // the update runs in the control CTA of the previous launch (LloydCtl::sum_fuse)
+    bool sum_cluster = false;  // begins merge their label sums in 8-CTA clusters (LloydCtl::sum_cluster)
     bool sum_small = false;  // per-CTA sums of the value units below 2^31 (bm_dataset::sum_units_max < 2^23)
     uint64_t sum_half() const { return (uint64_t)dev::kSumCopies * dev::kSMaxK * (n + 1); }
     long long* sums_of(int buf) { return sums.p + (uint64_t)buf * 2 * sum_half(); }
@@ -580,6 +581,27 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     BM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
+// The same with an 8-CTA cluster dimension (the grid must be a multiple of 8).
+template <class... KArgs, class... Args>
+void launch_pdl_cluster8(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                         Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 8;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    BM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 int assign_threads(int k) {
     const int kg = std::min<int>(dev::kAMaxCG, (int)ceil_div(std::max(k, 1), dev::kAK));
     return dev::kAPG * kg;
@@ -757,6 +779,15 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                 // a speculative begin loops over its blocks with at most spec_ctas() CTAs
                 // (BM_SPEC_CTAS), leaving SM slots to the engine stream's rounds
                 const unsigned lgrid = fused_ctl && ctl->nblk ? std::min<unsigned>(grid, spec_ctas()) : grid;
+                if (fused_ctl && ctl->sum_cluster) {  // begins: 8-CTA clusters merge the label sums (padded grid)
+                    launch_pdl_cluster8(dev::k_assign_tma<T, NS>, (grid + 7) / 8 * 8, dev::kSThreads, shm, st,
+                        tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
+                        S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
+                        g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), *ctl,
+                        !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
+                        dstride);
+                    return;
+                }
                 launch_pdl(dev::k_assign_tma<T, NS>, lgrid, dev::kSThreads, shm, st,
                     tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
                     S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
@@ -941,12 +972,16 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
         c.has_acc = 1;
     }
     c.accept_run = g->accept ? 1 : 0;
-    if (g->begin_kind == 1) c.nblk = (unsigned)ceil_div(w.R, dev::kABP);  // capped in CTAs (launch_assign)
+    if (g->begin_kind == 1 && spec_ctas() != ~0u)  // capped in CTAs (launch_assign), looping over the blocks
+        c.nblk = (unsigned)ceil_div(w.R, dev::kABP);
     if (w.sums_on) {  // exact-sum mode: the begins fill a half, the rounds move points in the live one
         c.sums = w.sums_of(g->buf);
         c.sum_half = w.sum_half();
         c.sum_scale = w.sum_scale;
         c.sum_which = g->begin_kind == 1 ? 0 : g->begin_kind == 2 ? 1 : -1;
+        // begins of fp32 data whose partials fit a CTA's bound-row buffer: 8-CTA
+        // clusters with BM_SUM_CLUSTER=1 (default: the group-of-8 merge through global memory)
+        c.sum_cluster = g->begin_kind != 0 && w.sum_cluster && spec_ctas() == ~0u ? 1 : 0;
         if (g->begin_kind != 0) {
             c.parts = w.sum_parts.p + (uint64_t)g->buf * w.part_ctas() * w.part_len();
             c.grp_ctr = w.grp_ctr.p + (uint64_t)g->buf * ceil_div(w.part_ctas(), 8);
@@ -1589,7 +1624,8 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
                   (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
                   (void*)dc.chunk3.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n,
-                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse, w.sum_scale, (void*)w.sums.p);
+                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse + 8 * (int)w.sum_cluster, w.sum_scale,
+                  (void*)w.sums.p);
     if (w.graph_sig == sig && w.g_lloyd[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
@@ -1656,6 +1692,9 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         w.sum_small = d->sum_units_max < 0x1p23;  // 128 points per CTA: partial sums below 2^30
         static const bool fuse = !(std::getenv("BM_SUMS_FUSE") && std::string(std::getenv("BM_SUMS_FUSE")) == "0");
         w.sums_fuse = fuse;
+        // (measured slower on c2: 20.4 vs 18.6 ms, the 8-CTA clusters wait for co-resident slots)
+        static const bool clus = std::getenv("BM_SUM_CLUSTER") && std::string(std::getenv("BM_SUM_CLUSTER")) == "1";
+        w.sum_cluster = clus && d->dtype == BM_F32 && (uint64_t)k * n + k <= 2048;
         const uint64_t nb = dev::kStateBufs;
         if (w.sums.n < 2 * nb * w.sum_half()) w.sums.alloc(2 * nb * w.sum_half());
         if (w.sum_parts.n < nb * w.part_ctas() * w.part_len()) w.sum_parts.alloc(nb * w.part_ctas() * w.part_len());

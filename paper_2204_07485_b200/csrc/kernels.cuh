@@ -10,6 +10,7 @@
 // Citations are relative to /root/reference/proj.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -632,6 +633,7 @@ struct LloydCtl {
     int sum_fuse;
     double sum_unscale;
     unsigned nblk;          // point blocks when the CTAs loop over them (0: one block per CTA)
+    int sum_cluster;        // begins launched as 8-CTA clusters: partials merged through distributed shared memory
     double* cC;
     uint8_t* cmask;
     double* cCact;
@@ -1709,7 +1711,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     }
     __syncthreads();
     const int nm = flag[1];
-    if (nm == 0) return;  // nothing moved in this CTA
+    if (nm == 0 && !(full && ctl.sum_cluster)) return;  // nothing moved in this CTA
     // stage the moved rows (whole 16-byte vectors) with cp.async
     constexpr int kV = 16 / sizeof(T);
     const int vpr = static_cast<int>((n + kV - 1) / kV);
@@ -1753,7 +1755,9 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     if (staged) cp_async_wait<0>();
     __syncthreads();
     const double sc = ctl.sum_scale;
-    const bool grouped = full && ctl.parts;
+    const bool clustered = full && ctl.sum_cluster;  // (every CTA of the cluster gets here, np may be 0)
+    const bool grouped = full && ctl.parts && !clustered;
+    long long* cpart = reinterpret_cast<long long*>(&S.lbs[0][0]);  // clustered: this CTA's partials
     const uint64_t slot_len = static_cast<uint64_t>(kSMaxK) * n + kSMaxK;
     long long* slot = grouped ? ctl.parts + blk * slot_len : nullptr;
     const T* Xb = pre ? reinterpret_cast<const T*>(pre) : staged ? xs : X + p0 * ld;
@@ -1771,8 +1775,37 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
         for (; q < q1; ++q) s = __dadd_rn(s, to_f64(Xb[plist[q] * rs + d]));
         for (int r = mc[j]; r < mc[j + 1]; ++r) s = __dsub_rn(s, to_f64(Xb[mlist[r] * rs + d]));
         const long long v = sum_units(s, sc);
-        if (grouped) slot[e] = v;
+        if (clustered) cpart[e] = v;
+        else if (grouped) slot[e] = v;
         else if (v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&sg[e]), static_cast<unsigned long long>(v));
+    }
+    if (clustered) {
+        // The 8 CTAs of the cluster merge their partials through distributed
+        // shared memory: CTA r sums elements [r E/8, (r+1) E/8) of all eight and
+        // issues one atomic per nonzero element into copy (cluster % 8).
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        const int kn = kfull * n, E = kn + kfull;
+        if (tid < kfull) cpart[kn + tid] = pc[tid + 1] - pc[tid];
+        cl.sync();
+        const int r = static_cast<int>(cl.block_rank());
+        const int e0 = r * E / 8, e1 = (r + 1) * E / 8;
+        const int cidx = static_cast<int>((blockIdx.x / 8) % kSumCopies);
+        long long* csg = half + static_cast<uint64_t>(cidx) * kSMaxK * n;
+        unsigned long long* ccnt = reinterpret_cast<unsigned long long*>(
+            half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n + cidx * kSMaxK);
+        for (int e = e0 + tid; e < e1; e += blockDim.x) {
+            long long v = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v += *cl.map_shared_rank(cpart + e, q);
+            if (v != 0) {
+                if (e >= kn) atomicAdd(&ccnt[e - kn], static_cast<unsigned long long>(v));
+                else atomicAdd(reinterpret_cast<unsigned long long*>(&csg[e]), static_cast<unsigned long long>(v));
+            }
+        }
+        cl.sync();        // no CTA leaves (or reuses its shared memory) while others read it
+        __threadfence();  // this CTA's atomics before its arrival
+        return;
     }
     if (!grouped) {
         if (tid < kfull) {
@@ -2813,7 +2846,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     }
 fold:
     ktrace(10, hmode);
-    if (ctl.sums && np > 0) label_sums<T>(S, ctl, X, ld, n, p0, np, labels_old == nullptr, kfull, reuse,
+    if (ctl.sums && (np > 0 || ctl.sum_cluster)) label_sums<T>(S, ctl, X, ld, n, p0, np, labels_old == nullptr, kfull, reuse,
                                           static_cast<size_t>(reinterpret_cast<unsigned char*>(item_d) - reuse), blk,
                                           pre_rows);
     ktrace(31, hmode);

@@ -166,7 +166,7 @@ def test_screen_adversarial_bitwise(port, case):
                                      ("BM_HAMERLY", "0"), ("BM_FORCE_EXACT_CONTROL", "1"),
                                      ("BM_SPEC", "0"), ("BM_PDL", "0"), ("BM_PP", "host"),
                                      ("BM_SUMS", "0"), ("BM_SUMS_FUSE", "0"), ("BM_SPEC_CTAS", "40"),
-                                     ("BM_FINAL", "tma")])
+                                     ("BM_FINAL", "tma"), ("BM_SUM_CLUSTER", "1")])
 def test_engine_modes_agree(var, alt):
     """Unscreened assignment (BM_ASSIGN_MODE=exact) and the host-driven chunk
     loop (BM_GRAPHS=0) give the same bits as the default path, in fresh processes."""
