@@ -1796,7 +1796,13 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         auto exists = [&](uint64_t c) { return !cfg.has_max_chunks || c < cfg.max_chunks; };
         draw(0);
         launch_prep(0);
-        bool queued = false;     // chunk `chunk`'s Lloyd graph is already queued (guarded)
+        // Lloyd graphs queued from `chunk` on (each guarded by go: a chunk after
+        // one that needs a repair or more rounds does nothing and is relaunched)
+        uint64_t queued = 0;
+        static const uint64_t lloyd_depth = [] {  // BM_LLOYD_AHEAD: graphs queued beyond the current one
+            const char* e = std::getenv("BM_LLOYD_AHEAD");
+            return e ? (uint64_t)std::max(0, std::min(2, std::atoi(e))) : (uint64_t)2;
+        }();
         uint64_t ahead = 0;  // chunks after this one whose draws, prep and speculative begin are enqueued
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
@@ -1831,11 +1837,13 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 BM_CUDA(cudaMemsetAsync(&w.gs.p->go, 0x01, sizeof(int), st));
                 dev::k_bump_version<<<1, 1, 0, st>>>(w.gs.p);  // the start is no longer the incumbent's copy
                 BM_LAUNCH();
-                queued = false;
+                queued = 0;
                 ahead = 0;  // the draws, preps and begins made ahead are redone
             }
-            const bool next = exists(chunk + 1);
-            if (!queued) launch_lloyd(chunk);
+            if (queued == 0) {
+                launch_lloyd(chunk);
+                queued = 1;
+            }
             // chunks chunk+1 .. chunk+3: draws (the stream is past this chunk's
             // repair, if any), prep and speculative begin, each as soon as its
             // buffers' previous chunk (c-4) is done.  Beyond chunk+1 they assume
@@ -1849,14 +1857,18 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 if (spec) launch_spec(c2);
                 ++ahead;
             }
-            queued = next && speculate;
-            if (queued) launch_lloyd(chunk + 1);  // runs iff this chunk's accept needs no repair
+            // the next chunks' Lloyd graphs behind this one (each runs iff the chunk
+            // before it needed neither a repair nor more rounds)
+            while (speculate && queued < 1 + lloyd_depth && exists(chunk + queued)) {
+                launch_lloyd(chunk + queued);
+                ++queued;
+            }
             BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
             if (w.h_status.p[b].incomplete) {  // more rounds than the graph unrolls
                 BM_CUDA(cudaGraphLaunch(w.g_cont[i6], st));
                 BM_CUDA(cudaEventRecord(w.ev_lloyd[i6], st));
                 BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
-                queued = false;  // the queued next chunk found go == 0 and did nothing
+                queued = 1;  // the queued next chunks found go == 0 and did nothing
             }
             const dev::LloydStatus& ls = w.h_status.p[b];
             if (ls.state_error) throw StateError("assign_nearest: every centroid is degenerate");
@@ -1864,9 +1876,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             evals += ls.evals;  // lloyd accumulate (local_search.cpp:55-58)
             iterations += ls.iterations;
             inc_degenerate = ls.inc_degenerate;
+            static const bool iters_log = std::getenv("BM_ITERS") != nullptr;  // diagnostics: Lloyd rounds per chunk
+            if (iters_log) std::fprintf(stderr, "[iters] %llu %llu\n", (unsigned long long)chunk, ls.iterations);
             count_launch(3 + 3 * ls.iterations);
             out->chunks = chunk + 1;
             if (ahead) --ahead;
+            if (queued) --queued;
         }
         // the last chunk's record gets its exact objective
         dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.gs.p, accept_args(w), w.dists.p, w.R,

@@ -1862,9 +1862,7 @@ __device__ __noinline__ void centroids_from_sums(const long long* __restrict__ h
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (warp == 0) {
         long long c = 0;
-        if (lane < k)
-#pragma unroll
-            c = __ldcg(cnts + lane);  // copy 0 (the begin's control CTA folded the others into it)
+        if (lane < k) c = __ldcg(cnts + lane);  // copy 0 (the begin's control CTA folded the others into it)
         const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
         if (lane < k) {
             tot[lane] = c;
