@@ -263,3 +263,24 @@ def test_chunk_size_hint_known_answers(port):
         bm.choose_chunk_size_hint(d, 600, bm.ChunkHintConfig())
     with pytest.raises(bm.ConfigError):
         bm.choose_chunk_size_hint(d, 3, bm.ChunkHintConfig(runs_per_candidate=0))
+
+
+@pytest.mark.parametrize("integer", [False, True])
+def test_time_budget_vs_oracle(port, integer):
+    """Time-budget runs (big_means.cpp:74-77: no chunk count in advance, so no
+    speculation ahead): whatever number of chunks ran, the result is the
+    reference's for that chunk budget, bit for bit (ordered and exact-sum updates)."""
+    r = np.random.default_rng(91)
+    X = r.normal(size=(30000, 12)) * 8.0
+    if integer:
+        X = np.rint(X)
+    out, tr = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=9, chunk_size=2500, max_cpu_seconds=0.15, seed=4))
+    c = tr.chunks()
+    assert c >= 1
+    p = port.big_means(X, 9, 2500, c, seed=4)
+    got = [(r_.chunk_index, r_.candidate_objective, r_.incumbent_objective, r_.accepted,
+            r_.degenerate_repaired) for r_ in tr.records]
+    assert got == p.trace
+    assert out.objective == p.objective
+    assert (bits(out.centroids.values) == bits(p.centroids)).all()
+    assert (out.assignment == p.labels).all()
