@@ -2404,19 +2404,46 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
                 cudaStream_t s;
                 ~Tmp() { cudaFreeAsync(p, s); }
             } tmp_guard{tmp, d->stream};
-            BM_CUDA(cudaMemcpyAsync(tmp, values, m * n * sizeof(double), cudaMemcpyHostToDevice, d->stream));
-            dev::k_check_narrow<<<1184, 256, 0, d->stream>>>(tmp, m * n, flags.p, flags.p + 1, flags.p + 2, maxbits);
-            BM_LAUNCH();
-            BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, d->stream));
+            // Uploaded in row pieces; each piece is checked and narrowed (speculatively,
+            // one pass) on a second stream while the next piece is in flight.
+            const uint64_t ld32 = padded_ld(n, BM_F32);
+            float* x32 = nullptr;
+            BM_CUDA(cudaMallocAsync(&x32, m * ld32 * sizeof(float), d->stream));
+            cudaStream_t ks = nullptr;
+            BM_CUDA(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking));
+            struct KS {
+                cudaStream_t s;
+                ~KS() { cudaStreamDestroy(s); }
+            } ks_guard{ks};
+            constexpr int kPieces = 8;
+            const uint64_t per = ceil_div(m, (uint64_t)kPieces);
+            for (uint64_t r0 = 0; r0 < m; r0 += per) {
+                const uint64_t r1 = std::min(m, r0 + per);
+                BM_CUDA(cudaMemcpyAsync(tmp + r0 * n, static_cast<const double*>(values) + r0 * n,
+                                        (r1 - r0) * n * sizeof(double), cudaMemcpyHostToDevice, d->stream));
+                cudaEvent_t ev;
+                BM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                BM_CUDA(cudaEventRecord(ev, d->stream));
+                BM_CUDA(cudaStreamWaitEvent(ks, ev, 0));
+                BM_CUDA(cudaEventDestroy(ev));
+                dev::k_check_narrow_write<<<592, 256, 0, ks>>>(tmp, r0, r1, (int)n, flags.p, flags.p + 1, flags.p + 2,
+                                                               maxbits, x32, ld32);
+                BM_LAUNCH();
+            }
+            BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, ks));
+            BM_CUDA(cudaStreamSynchronize(ks));
             BM_CUDA(cudaStreamSynchronize(d->stream));
-            if (hf[0]) throw ConfigError("dataset contains a non-finite value");
+            if (hf[0]) {
+                cudaFreeAsync(x32, d->stream);
+                throw ConfigError("dataset contains a non-finite value");
+            }
             d->dtype = hf[1] ? BM_F64 : BM_F32;
             d->ld = padded_ld(n, d->dtype);
-            BM_CUDA(cudaMallocAsync(&d->X, m * d->ld * dtype_size(d->dtype), d->stream));
             if (d->dtype == BM_F32) {
-                dev::k_narrow<<<1184, 256, 0, d->stream>>>(tmp, m, (int)n, static_cast<float*>(d->X), d->ld);
-                BM_LAUNCH();
+                d->X = x32;
             } else {
+                BM_CUDA(cudaFreeAsync(x32, d->stream));
+                BM_CUDA(cudaMallocAsync(&d->X, m * d->ld * dtype_size(d->dtype), d->stream));
                 BM_CUDA(cudaMemcpy2DAsync(d->X, d->ld * sizeof(double), tmp, n * sizeof(double), n * sizeof(double),
                                           m, cudaMemcpyDeviceToDevice, d->stream));
             }

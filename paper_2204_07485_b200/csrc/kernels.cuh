@@ -4263,6 +4263,29 @@ __global__ void k_check_narrow(const double* __restrict__ v, uint64_t count, int
     exact_stats_flush(lowexp, maxbits, lowexp_out, maxbits_out);
 }
 
+// k_check_narrow + k_narrow in one pass over rows [r0, r1): the checks, and
+// the fp32 copy written speculatively (discarded when a value is not exact).
+__global__ void k_check_narrow_write(const double* __restrict__ v, uint64_t r0, uint64_t r1, int n, int* bad,
+                                     int* inexact, int* lowexp_out, unsigned long long* maxbits_out,
+                                     float* __restrict__ out, uint64_t ld) {
+    int lowexp = 0x7F7F7F7F;
+    unsigned long long maxbits = 0;
+    const uint64_t e0 = r0 * static_cast<uint64_t>(n), e1 = r1 * static_cast<uint64_t>(n);
+    for (uint64_t e = e0 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < e1;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double x = v[e];
+        const float f = static_cast<float>(x);
+        out[(e / n) * ld + (e % n)] = f;
+        if (!isfinite(x)) {
+            *bad = 1;
+            continue;
+        }
+        if (static_cast<double>(f) != x) *inexact = 1;
+        exact_stats(x, lowexp, maxbits);
+    }
+    exact_stats_flush(lowexp, maxbits, lowexp_out, maxbits_out);
+}
+
 __global__ void k_narrow(const double* __restrict__ in, uint64_t rows, int n, float* __restrict__ out, uint64_t ld) {
     const uint64_t total = rows * static_cast<uint64_t>(n);
     for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
