@@ -1978,6 +1978,76 @@ __device__ __noinline__ void fold_sum_copies(long long* half, int k, int n) {
     __syncthreads();
 }
 
+// The same, element-parallel (the control CTA of a round that goes on): every
+// thread's sums and old centroids loaded up front, the squared movements
+// through shared memory (dsq: k * n doubles), then a warp per label.
+__device__ __noinline__ void centroids_from_sums_ilp(const long long* __restrict__ half, int k, int n, double unscale,
+                                                     double* __restrict__ C, uint8_t* __restrict__ mask,
+                                                     double* __restrict__ Cact, int ldc, int* __restrict__ act_idx,
+                                                     int* __restrict__ n_active, float* __restrict__ CT32,
+                                                     float* __restrict__ delta, long long* tot, int* rank,
+                                                     double* dsq) {
+    const long long* cnts = half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n;
+    __shared__ double inv_s[kSMaxK];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nth = blockDim.x;
+    if (warp == 0) {
+        long long c = 0;
+        if (lane < k) c = __ldcg(cnts + lane);  // copy 0
+        const unsigned live = __ballot_sync(0xFFFFFFFFu, c > 0);
+        if (lane < k) {
+            tot[lane] = c;
+            const int r = __popc(live & ((1u << lane) - 1u));
+            rank[lane] = c > 0 ? r : -1;
+            mask[lane] = c > 0 ? 0 : 1;
+            if (c > 0) act_idx[r] = lane;
+            inv_s[lane] = c > 0 ? __ddiv_rn(1.0, static_cast<double>(c)) : 0.0;
+        }
+        if (lane == 0) *n_active = __popc(live);
+    }
+    __syncthreads();
+    const int kn = k * n;
+    constexpr int kU = 4;
+    for (int e0 = tid; e0 < kn; e0 += kU * nth) {
+        long long sv[kU];
+        double cv[kU];
+#pragma unroll
+        for (int r = 0; r < kU; ++r) {
+            const int e = e0 + r * nth;
+            if (e < kn) {
+                sv[r] = __ldcg(half + e);
+                cv[r] = C[e];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kU; ++r) {
+            const int e = e0 + r * nth;
+            if (e >= kn) continue;
+            const int j = e / n, d = e - j * n;
+            if (tot[j] <= 0) {
+                C[e] = 0.0;
+                dsq[e] = 0.0;
+                continue;
+            }
+            const double v = __dmul_rn(__dmul_rn(static_cast<double>(sv[r]), unscale), inv_s[j]);  // exact sum (§5b)
+            const double dv = __dsub_rn(v, cv[r]);
+            dsq[e] = __dmul_rn(dv, dv);
+            C[e] = v;
+            const int rk = rank[j];
+            Cact[static_cast<uint64_t>(rk) * ldc + d] = v;
+            if (CT32) CT32[static_cast<uint64_t>(d) * kSMaxK + rk] = __double2float_rn(v);
+        }
+    }
+    __syncthreads();
+    for (int j = warp; j < k; j += nth / 32) {
+        if (tot[j] <= 0) continue;
+        double sq = 0.0;
+        for (int d = lane; d < n; d += 32) sq = __dadd_rn(sq, dsq[j * n + d]);  // order-free: only bounds use it
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+        if (lane == 0) delta[j] = __double2float_ru(__dsqrt_ru(sq * (1.0 + 1e-12)) * (1.0 + 1e-12) + 1e-300);
+    }
+}
+
 // The fused form (LloydCtl::sum_fuse): the live half of this chunk buffer's sums.
 __device__ __forceinline__ void centroids_fused(const LloydCtl& c, int sum_sel, int k, int n, long long* tot,
                                                 int* rank) {
@@ -2977,8 +3047,16 @@ fold:
         if (ctl.sums && ctl.mode == 1)
             fold_sum_copies(ctl.sums + static_cast<uint64_t>(sst->sum_sel) * ctl.sum_half, kfull, n);
         // fused exact-sum update: the next round's centroids when the loop goes on
-        if (ctl.sum_fuse && !sst->stop && !sst->state_error)
-            centroids_fused(ctl, sst->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
+        if (ctl.sum_fuse && !sst->stop && !sst->state_error) {
+            __syncthreads();  // (the accept's staging area is free: the loop goes on)
+            if (16384 + static_cast<size_t>(kfull) * n * 8 <= reuse_bytes)
+                centroids_from_sums_ilp(ctl.sums + static_cast<uint64_t>(sst->sum_sel) * ctl.sum_half, kfull, n,
+                                        ctl.sum_unscale, ctl.cC, ctl.cmask, ctl.cCact, ctl.cldc, ctl.cact,
+                                        ctl.cn_active, ctl.cCT32, ctl.cdelta, reinterpret_cast<long long*>(&S.cand[0]),
+                                        &S.icount[0], reinterpret_cast<double*>(reuse + 16384));
+            else
+                centroids_fused(ctl, sst->sum_sel, kfull, n, reinterpret_cast<long long*>(&S.cand[0]), &S.icount[0]);
+        }
         if (tid == 0) klog_end(10 + hmode);
         return;
     }
