@@ -3939,15 +3939,20 @@ k_pp_pick(uint64_t m, Mt64State* __restrict__ mt, int candidates, uint32_t* __re
         if (tid == 0) ps->fallback = 1;
         return;
     }
-    if (tid == 0) {  // exclusive offsets of the tiles (<= 1024 exact integer adds)
+    // exclusive offsets of the tiles (<= 1024 exact integer adds): the totals
+    // staged in parallel, then one thread's running sum from shared memory
+    if (tid < ntiles) toff[tid + 1] = tile_tot[tid];
+    if (tid < kMtN) xs[tid] = mt->x[tid];
+    __syncthreads();
+    if (tid == 0) {
         long long r = 0;
         for (int t = 0; t < ntiles; ++t) {
+            const long long v = toff[t + 1];
             toff[t] = r;
-            r += tile_tot[t];
+            r += v;
         }
         toff[ntiles] = r;
     }
-    if (tid < kMtN) xs[tid] = mt->x[tid];
     __syncthreads();
     const long long total = toff[ntiles];
     if (total >= (1ll << 53)) {  // partial sums could round
