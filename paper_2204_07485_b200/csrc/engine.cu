@@ -984,7 +984,7 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
         c.sum_cluster = g->begin_kind != 0 && w.sum_cluster && spec_ctas() == ~0u ? 1 : 0;
         if (g->begin_kind != 0) {
             c.parts = w.sum_parts.p + (uint64_t)g->buf * w.part_ctas() * w.part_len();
-            c.grp_ctr = w.grp_ctr.p + (uint64_t)g->buf * ceil_div(w.part_ctas(), 8);
+            c.grp_ctr = w.grp_ctr.p + (uint64_t)g->buf * ceil_div(w.part_ctas(), (uint64_t)dev::kSumGroup);
             c.pts_rows = w.R;
         }
         c.sum_small = w.sum_small ? 1 : 0;
@@ -1698,8 +1698,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         const uint64_t nb = dev::kStateBufs;
         if (w.sums.n < 2 * nb * w.sum_half()) w.sums.alloc(2 * nb * w.sum_half());
         if (w.sum_parts.n < nb * w.part_ctas() * w.part_len()) w.sum_parts.alloc(nb * w.part_ctas() * w.part_len());
-        if (w.grp_ctr.n < nb * ceil_div(w.part_ctas(), 8)) {
-            w.grp_ctr.alloc(nb * ceil_div(w.part_ctas(), 8));
+        if (w.grp_ctr.n < nb * ceil_div(w.part_ctas(), (uint64_t)dev::kSumGroup)) {
+            w.grp_ctr.alloc(nb * ceil_div(w.part_ctas(), (uint64_t)dev::kSumGroup));
             BM_CUDA(cudaMemsetAsync(w.grp_ctr.p, 0, w.grp_ctr.n * sizeof(unsigned), st));
         }
     }

@@ -1656,7 +1656,11 @@ struct TmaSmem {
 // whose label changed, and k_centroids turns them into the next centroids
 // (sum * (1.0/count), core.cpp:237-239) — no ordered update pass at all.
 // ---------------------------------------------------------------------------
-constexpr int kSumCopies = 8;  // CTA b adds into copy b % 8 (spreads same-address atomics)
+constexpr int kSumCopies = 8;
+#ifndef BM_SUM_GROUP
+#define BM_SUM_GROUP 8
+#endif
+constexpr int kSumGroup = BM_SUM_GROUP;  // a begin's CTAs whose partial sums one of them merges  // CTA b adds into copy b % 8 (spreads same-address atomics)
 
 __device__ __forceinline__ long long sum_units(double x, double scale) {
     return __double2ll_rn(__dmul_rn(x, scale));  // exact: x * 2^-e is an integer below 2^53
@@ -1820,9 +1824,9 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     if (tid < kfull) slot[static_cast<uint64_t>(kSMaxK) * n + tid] = pc[tid + 1] - pc[tid];
     __threadfence();
     __syncthreads();
-    const int g = static_cast<int>(blk / 8);
+    const int g = static_cast<int>(blk / kSumGroup);
     const int pts_ctas = static_cast<int>((ctl.pts_rows + kABP - 1) / kABP);
-    const int members = min(8, pts_ctas - 8 * g);
+    const int members = min(kSumGroup, pts_ctas - kSumGroup * g);
     if (tid == 0) flag[1] = atomicAdd(&ctl.grp_ctr[g], 1u) == static_cast<unsigned>(members) - 1;
     __syncthreads();
     if (!flag[1]) return;
@@ -1830,14 +1834,14 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
     long long* gsg = half + static_cast<uint64_t>(g % kSumCopies) * kSMaxK * n;
     unsigned long long* gcnt = reinterpret_cast<unsigned long long*>(
         half + static_cast<uint64_t>(kSumCopies) * kSMaxK * n + (g % kSumCopies) * kSMaxK);
-    const long long* gbase = ctl.parts + static_cast<uint64_t>(8 * g) * slot_len;
+    const long long* gbase = ctl.parts + static_cast<uint64_t>(kSumGroup) * g * slot_len;
     const int kn = kfull * n;
     for (int e = tid; e < kn + kfull; e += blockDim.x) {
         const bool is_cnt = e >= kn;
         const uint64_t off = is_cnt ? static_cast<uint64_t>(kSMaxK) * n + (e - kn) : static_cast<uint64_t>(e);
         long long v = 0;
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+        for (int m = 0; m < kSumGroup; ++m)
             if (m < members) v += __ldcg(gbase + m * slot_len + off);
         if (v != 0) {
             if (is_cnt) atomicAdd(&gcnt[e - kn], static_cast<unsigned long long>(v));
