@@ -48,8 +48,9 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ref-chunks", type=int, default=20,
-                    help="chunks per reference-arm step (bounded CPU sample)")
+    ap.add_argument("--ref-chunks", type=int, default=0,
+                    help="chunks per reference-arm step (default 0: the config's full count, "
+                         "so both arms run the same workload)")
     return ap.parse_args()
 
 
@@ -110,8 +111,33 @@ def emit(line: dict):
 
 
 # ---------------------------------------------------------------------------
+def host_info() -> dict:
+    """CPU model and core count of this host (stated next to every CPU number)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cores": os.cpu_count() or 1, "cpu_model": model}
+
+
+def run_reference(R, w, X64, threads, chunks=None, final_assignment=True):
+    """One reference big_means (oracle/_ref = the unmodified reference sources)."""
+    R.set_worker_count(threads)
+    t0 = time.perf_counter()
+    o = R.big_means(X64, w.k, w.s, chunks or w.chunks, seed=w.seed,
+                    max_iterations=w.max_iterations, rel_tolerance=w.rel_tolerance,
+                    candidates_per_step=w.candidates, final_assignment=final_assignment)
+    return o, time.perf_counter() - t0
+
+
 def reference_arm(args, w, X, rank):
-    """--impl reference: the compiled reference (oracle/_ref) on host cores."""
+    """--impl reference: the compiled reference (oracle/_ref) on host cores,
+    same config, metric and unit as the B200 arm (full chunk count by default)."""
     if rank != 0:
         return
     from oracle.oracle import ref
@@ -119,40 +145,92 @@ def reference_arm(args, w, X, rank):
     if R is None:
         emit({"impl": "reference", "unavailable": "oracle/_ref/libbigmeans_ref.so not built"})
         return
-    cores = os.cpu_count() or 1
-    R.set_worker_count(cores)
-    Xd = np.ascontiguousarray(X, np.float64)
-    chunks = max(1, min(args.ref_chunks, w.chunks))
-
-    def step():
-        o = R.big_means(Xd, w.k, w.s, chunks, seed=w.seed, max_iterations=w.max_iterations,
-                        rel_tolerance=w.rel_tolerance, candidates_per_step=w.candidates)
-        return o.evals, o.chunks, o.cpu_init + o.cpu_full, o.cpu_init
+    hi = host_info()
+    cores = hi["cores"]
+    X64 = np.ascontiguousarray(X, np.float64)
+    chunks = args.ref_chunks or w.chunks
 
     for _ in range(args.warmup):
-        step()
+        run_reference(R, w, X64, cores, chunks)
     tot_e = tot_c = 0
+    loop = full = 0.0
     t0 = time.perf_counter()
-    loop = 0.0
     for _ in range(args.steps):
-        e, c, _, li = step()
-        tot_e += e
-        tot_c += c
-        loop += li
+        o, _ = run_reference(R, w, X64, cores, chunks)
+        tot_e += o.evals
+        tot_c += o.chunks
+        loop += o.cpu_init
+        full += o.cpu_full
     dt = time.perf_counter() - t0
     value = tot_e / dt
-    sample = f"{args.steps} steps x ({chunks} of {w.chunks} chunks + final pass over all {w.m} rows)"
+    sample = (f"{args.steps} steps x ({chunks} of {w.chunks} chunks + final pass over all {w.m} rows), "
+              f"{cores} threads on {hi['cpu_model']}")
     emit({"metric": METRIC, "value": value, "unit": "evals/s", "impl": "reference",
           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-          "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+          "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
           "config": {"workload": w.name, "m": w.m, "n": w.n, "k": w.k, "s": w.s,
                      "subproblems": chunks, "seed": w.seed},
-          "subproblems_per_s": tot_c / loop if loop > 0 else None,
-          "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores,
-                           "kind": "reference", "sample": sample},
+          "same_config": chunks == w.chunks,
+          # both arms: chunks / whole-step time; *_loop: chunks / chunk-loop time (cpu_init)
+          "subproblems_per_s": tot_c / dt,
+          "subproblems_per_s_loop": tot_c / loop if loop > 0 else None,
+          "ms_per_step_loop": loop / args.steps * 1e3, "ms_per_step_final": full / args.steps * 1e3,
+          "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
+                           "cpu_model": hi["cpu_model"], "sample": sample},
           "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                   "d2h_bytes_per_step": 0}})
+
+
+def parity_report(gpu_out, gpu_trace, ref_out) -> dict:
+    """Full-size comparison of one B200 big_means against the reference's."""
+    bits = lambda a: np.ascontiguousarray(a, np.float64).view(np.uint64)
+    got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+            r.degenerate_repaired) for r in gpu_trace.records]
+    c_g, c_r = gpu_out.centroids.values, ref_out.centroids
+    live = ~ref_out.mask.astype(bool)
+    rel = (np.abs(c_g[live] - c_r[live]) / np.maximum(np.abs(c_r[live]), 1e-300)).max() if live.any() else 0.0
+    return {
+        "objective_bitwise": gpu_out.objective == ref_out.objective,
+        "final_sse_rel_gap": abs(gpu_out.objective - ref_out.objective) / abs(ref_out.objective),
+        "centroids_bitwise": bool((bits(c_g) == bits(c_r)).all()),
+        "centroids_max_rel_diff": float(rel),
+        "mask_equal": bool((gpu_out.centroids.mask == ref_out.mask).all()),
+        "labels_equal": bool((gpu_out.assignment == ref_out.labels).all())
+        if ref_out.labels is not None else None,
+        "trace_equal": got == ref_out.trace,
+        "chunks": len(got),
+        "accepted": sum(1 for t in ref_out.trace if t[3]),
+        "n_d_equal": gpu_out.counter.distance_evals == ref_out.evals,
+        "iterations_equal": gpu_out.counter.iterations == ref_out.iterations,
+    }
+
+
+def cpu_baseline_leg(w, X, key, gpu_out, gpu_trace):
+    """The reference on this host's cores on the SAME full workload (same run),
+    its full-size parity with the B200 result, and a 1-thread run for c1."""
+    from oracle.oracle import ref
+    R = ref()
+    if R is None:
+        return {"value": None, "unit": "evals/s", "kind": "reference",
+                "sample": "oracle/_ref not built"}, None
+    hi = host_info()
+    X64 = np.ascontiguousarray(X, np.float64)
+    o, dt = run_reference(R, w, X64, hi["cores"])
+    cpu = {"value": o.evals / dt, "unit": "evals/s", "cores": hi["cores"], "kind": "reference",
+           "cpu_model": hi["cpu_model"],
+           "sample": f"one full {w.name} run ({w.chunks} chunks + final pass over {w.m} rows), "
+                     f"{dt:.2f} s",
+           "subproblems_per_s": o.chunks / dt, "subproblems_per_s_loop": o.chunks / o.cpu_init,
+           "cpu_init_s": o.cpu_init, "cpu_full_s": o.cpu_full,
+           "final_pass_evals_per_s": (w.m * int((~o.mask.astype(bool)).sum())) / o.cpu_full
+           if o.cpu_full > 0 else None}
+    if key == "c1":  # the 1-thread reference on the whole c1 run (BASELINE.md §3)
+        o1, dt1 = run_reference(R, w, X64, 1)
+        cpu["threads1"] = {"value": o1.evals / dt1, "unit": "evals/s", "cores": 1,
+                           "subproblems_per_s": o1.chunks / dt1, "seconds": dt1,
+                           "same_result": o1.objective == o.objective}
+    return cpu, parity_report(gpu_out, gpu_trace, o)
 
 
 # ---------------------------------------------------------------------------
@@ -248,13 +326,15 @@ def main():
                for nm in pres[0]["prof"]["phase_count"]}
 
     # ---- e2e through the public API with host buffers ----
+    # "e2e": the dataset in pinned host memory (the contract's form); "pageable":
+    # the same from an ordinary numpy array (what most callers hold).
     e2e = None
     if not args.no_e2e:
         Xp = torch.from_numpy(np.ascontiguousarray(X)).pin_memory().numpy()
 
-        def e2e_step():
+        def e2e_step(host):
             # (evals, D2H bytes) of one step: dataset upload, run, results to the host
-            with bm.Dataset(Xp, device=local) as dh:
+            with bm.Dataset(host, device=local) as dh:
                 if world == 1:
                     out, trace = bm.big_means(dh, cfg, want_labels=True)
                     return (out.counter.distance_evals,
@@ -263,28 +343,34 @@ def main():
                                                 multi.gpu_rows(dh), cfg.seed, device=dev)
                 return r.local_evals, r.centroids.nbytes
 
-        for _ in range(args.warmup):  # untimed: the first dataset grows the allocation pool
-            e2e_step()
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        ev_e2e, h2d, d2h = 0, 0, 0
-        for _ in range(args.steps):
-            ev, ob = e2e_step()
-            ev_e2e += ev
-            d2h += ob
-            h2d += Xp.nbytes
-        torch.cuda.synchronize()
-        barrier()
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt, ev_e2e], dtype=torch.float64, device=dev)
-            mx = t.clone()
-            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-            torch.distributed.all_reduce(t)
-            dt, ev_e2e = float(mx[0]), int(t[1])
-        e2e = {"value": ev_e2e / dt, "unit": "evals/s", "h2d_bytes_per_step": h2d // args.steps,
-               "d2h_bytes_per_step": d2h // args.steps}
+        def e2e_run(host):
+            for _ in range(args.warmup):  # untimed: the first dataset grows the allocation pool
+                e2e_step(host)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ev_e2e, h2d, d2h = 0, 0, 0
+            for _ in range(args.steps):
+                ev, ob = e2e_step(host)
+                ev_e2e += ev
+                d2h += ob
+                h2d += host.nbytes
+            torch.cuda.synchronize()
+            barrier()
+            dt = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([dt, ev_e2e], dtype=torch.float64, device=dev)
+                mx = t.clone()
+                torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+                torch.distributed.all_reduce(t)
+                dt, ev_e2e = float(mx[0]), int(t[1])
+            return {"value": ev_e2e / dt, "unit": "evals/s", "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": d2h // args.steps, "ms_per_step": dt / args.steps * 1e3}
+
+        e2e = e2e_run(Xp)
+        e2e["host_memory"] = "pinned"
+        pg = e2e_run(np.ascontiguousarray(X))
+        e2e["pageable"] = {"value": pg["value"], "ms_per_step": pg["ms_per_step"]}
 
     if rank != 0:
         return
@@ -309,29 +395,17 @@ def main():
                                "achieved_gbs": final_bytes / (final_avg_ms * 1e-3) / 1e9
                                if final_avg_ms > 0 else None}}
 
-    # ---- CPU baseline: compiled reference on this host, same config ----
+    # ---- CPU baseline + full-size parity: the reference on this host, same run ----
     cpu = None
-    gap = None
+    parity = None
     if world == 1 and not args.no_cpu:
         try:
-            from oracle.oracle import ref
-            R = ref()
-            if R is not None:
-                cores = os.cpu_count() or 1
-                R.set_worker_count(cores)
-                t0 = time.perf_counter()
-                o = R.big_means(np.ascontiguousarray(X, np.float64), w.k, w.s, w.chunks,
-                                seed=w.seed, max_iterations=w.max_iterations,
-                                rel_tolerance=w.rel_tolerance, candidates_per_step=w.candidates)
-                dt = time.perf_counter() - t0
-                cpu = {"value": o.evals / dt, "unit": "evals/s", "cores": cores,
-                       "kind": "reference",
-                       "sample": f"one full {w.name} run ({w.chunks} chunks + final pass), "
-                                 f"{dt:.1f} s, {o.chunks / o.cpu_init:.2f} subproblems/s"}
-                gap = abs(objective - o.objective) / o.objective
+            gout, gtrace = bm.big_means(data, cfg, want_labels=True)
+            cpu, parity = cpu_baseline_leg(w, X, args.config, gout, gtrace)
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"failed: {e}"}
+                   "sample": f"failed: {type(e).__name__}: {e}"}
+    gap = parity["final_sse_rel_gap"] if parity else None
 
     emit({"metric": METRIC, "value": evals / (ms * 1e-3), "unit": "evals/s", "n_gpus": world,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -343,7 +417,7 @@ def main():
                            "L2-resident within a step by design" % (X.nbytes / 1e9),
                      "parallelism": f"chains{world}"},
           "subproblems_per_s": chunks / (ms * 1e-3),
-          "final_sse_rel_gap": gap, "objective": objective,
+          "final_sse_rel_gap": gap, "parity_full_size": parity, "objective": objective,
           "gpu_launches": launches, "clocks": ck, "e2e": e2e, "roofline": roofline,
           "step_breakdown_ms": {nm: round(v, 3) for nm, v in phases.items()},
           "step_breakdown_launch_groups": phase_n,

@@ -190,6 +190,14 @@ typedef struct {
  * kmeans_parallel_init (:209-347), then lloyd.  out->labels may be NULL. */
 bm_status bm_kmeans(const bm_dataset* data, uint64_t k, const bm_init_config* init,
                     uint64_t max_iterations, double rel_tolerance, bm_outcome* out);
+/* The initialization stage of kmeans alone (local_search.cpp:66-83):
+ * forgy_init init.cpp:92-115, kmeanspp_fill from an all-degenerate start
+ * :123-201, kmeans_parallel_init :209-347, seeded by init->seed.  Writes the
+ * start centroids (k*n f64) and mask (k bytes); *evals = the init's distance
+ * evaluations.  kmeans == bm_init_centroids + bm_lloyd (the drop-in's
+ * local_search shim composes them exactly as local_search.cpp:62-94 does). */
+bm_status bm_init_centroids(const bm_dataset* data, uint64_t k, const bm_init_config* init,
+                            double* centroids, uint8_t* mask, uint64_t* evals);
 
 /* choose_chunk_size_hint big_means.hpp:72-73 / big_means.cpp:114-160 (ChunkHintConfig
  * :60-68): ladder NULL / empty = m/64 .. m; best mean objective of
@@ -205,6 +213,12 @@ bm_status bm_choose_chunk_size_hint(bm_dataset* data, uint64_t k, const uint64_t
  * at most trace_capacity records are written, out->chunks holds the count. */
 bm_status bm_big_means(bm_dataset* data, const bm_config* cfg, bm_outcome* out,
                        bm_chunk_record* trace, uint64_t trace_capacity);
+
+/* Every chunk record of the last bm_big_means call on this thread (the trace
+ * is never truncated here: *count is the full chunk count, at most `capacity`
+ * records are copied).  Lets a caller with a time budget size its trace from
+ * the result (BigMeansTrace big_means.hpp:36-40). */
+bm_status bm_last_trace(bm_chunk_record* out, uint64_t capacity, uint64_t* count);
 
 /* Multi-GPU pieces.  Row-sharded final pass: assign rows
  * [row_begin, row_end) (row_begin a multiple of 1024) against the centroids,

@@ -11,7 +11,6 @@
 // std::runtime_error (common.hpp:21-49), so callers (CLI exit codes,
 // bench failure accounting, acceptance gate) behave as before.
 #include <algorithm>
-#include <cstdlib>
 #include <limits>
 #include <numeric>
 #include <stdexcept>
@@ -19,35 +18,10 @@
 #include <vector>
 
 #include "bigmeans/big_means.hpp"
-#include "bigmeans_b200.h"
+#include "dropin_common.hpp"
 
 namespace bigmeans {
-
-namespace {
-
-void rethrow(bm_status st) {
-    if (st == BM_OK) return;
-    const std::string msg = bm_last_error();
-    if (st == BM_CONFIG_ERROR) throw ConfigError(msg);
-    if (st == BM_STATE_ERROR) throw StateError(msg);
-    throw std::runtime_error(msg);
-}
-
-int device_of_thread() {
-    const char* e = std::getenv("BIGMEANS_DEVICE");
-    return e ? std::atoi(e) : 0;
-}
-
-// Device copy of a (host, immutable) Dataset for the duration of one call.
-struct DeviceDataset {
-    bm_dataset* h = nullptr;
-    explicit DeviceDataset(const Dataset& d) {
-        rethrow(bm_dataset_create(d.values().data(), d.m(), d.n(), BM_F64, device_of_thread(), &h));
-    }
-    ~DeviceDataset() { bm_dataset_destroy(h); }
-};
-
-}  // namespace
+using namespace dropin;
 
 std::vector<std::size_t> sample_chunk(const Dataset& data, std::size_t s, Rng& rng) {
     const std::size_t m = data.m();
@@ -85,7 +59,7 @@ std::pair<ClusteringOutcome, BigMeansTrace> big_means(const Dataset& data, const
     c.final_assignment = cfg.final_assignment ? 1 : 0;
     if (data.m() < 1) throw ConfigError("big_means: empty dataset");
 
-    DeviceDataset dd(data);
+    const std::shared_ptr<Handle> dd = device_dataset(data);
     const std::size_t k = cfg.k, n = data.n();
     std::vector<double> centers(std::max<std::size_t>(k, 1) * n);
     std::vector<std::uint8_t> mask(std::max<std::size_t>(k, 1));
@@ -94,9 +68,12 @@ std::pair<ClusteringOutcome, BigMeansTrace> big_means(const Dataset& data, const
     o.centroids = centers.data();
     o.mask = mask.data();
     o.labels = cfg.final_assignment ? labels.data() : nullptr;
-    const uint64_t cap = cfg.max_chunks.value_or(1u << 20);
-    std::vector<bm_chunk_record> recs(static_cast<std::size_t>(std::min<uint64_t>(cap, 1u << 20)));
-    rethrow(bm_big_means(dd.h, &c, &o, recs.data(), recs.size()));
+    rethrow(bm_big_means(dd->h, &c, &o, nullptr, 0));
+    // the whole trace, sized from the chunk count (time budgets: unknown up front)
+    uint64_t nrec = 0;
+    rethrow(bm_last_trace(nullptr, 0, &nrec));
+    std::vector<bm_chunk_record> recs(nrec);
+    rethrow(bm_last_trace(recs.data(), nrec, &nrec));
 
     Centroids inc = Centroids::all_degenerate(k, n);
     for (std::size_t j = 0; j < k; ++j)
@@ -110,7 +87,7 @@ std::pair<ClusteringOutcome, BigMeansTrace> big_means(const Dataset& data, const
     out.counter.cpu_init = o.cpu_init;
     out.counter.cpu_full = o.cpu_full;
     BigMeansTrace trace;
-    for (uint64_t i = 0; i < o.chunks && i < recs.size(); ++i)
+    for (uint64_t i = 0; i < recs.size(); ++i)
         trace.records.push_back({recs[i].chunk_index, recs[i].candidate_objective,
                                  recs[i].incumbent_objective, recs[i].accepted != 0,
                                  static_cast<std::size_t>(recs[i].degenerate_repaired)});

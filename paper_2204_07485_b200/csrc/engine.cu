@@ -42,6 +42,7 @@ namespace bm {
 thread_local std::string g_last_error;
 thread_local bm_profile g_profile{};
 thread_local bool g_profiling = false;
+thread_local std::vector<bm_chunk_record> g_last_trace;  // every record of the last big_means call
 
 double seconds_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1672,7 +1673,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         if (!g_profiling && graphs_enabled() && dc.chunk2.n < bytes) dc.chunk2.alloc(bytes);
         if (!g_profiling && graphs_enabled() && dc.chunk3.n < bytes) dc.chunk3.alloc(bytes);
     }
-    const uint64_t want_rec = cfg.has_max_chunks ? cfg.max_chunks : 1024;
+    // one device record per chunk; a time budget starts small and grows (below)
+    const uint64_t want_rec = cfg.has_max_chunks && !cfg.has_max_cpu_seconds
+                                  ? cfg.max_chunks
+                                  : std::min<uint64_t>(cfg.has_max_chunks ? cfg.max_chunks : 1024, 1024);
     if (w.drec.n < want_rec) w.drec.alloc(want_rec);
     // incumbent all degenerate, f_opt = +inf (:63-64), chunk counter 0
     dev::k_run_init<<<1, 256, 0, st>>>(w.status.p, dev::kStateBufs, w.gs.p, w.fopt.p, w.Cinc.p, w.maskinc.p, w.C.p, w.mask.p, k, n,
@@ -2031,12 +2035,15 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     }
     out->distance_evals = evals;
     out->iterations = iterations;  // :97
-    for (uint64_t i = 0; i < out->chunks && trace && i < trace_cap; ++i) {
-        trace[i].chunk_index = records[i].chunk_index;
-        trace[i].candidate_objective = records[i].candidate_objective;
-        trace[i].incumbent_objective = records[i].incumbent_objective;
-        trace[i].accepted = records[i].accepted;
-        trace[i].degenerate_repaired = records[i].degenerate_repaired;
+    g_last_trace.resize(out->chunks);
+    for (uint64_t i = 0; i < out->chunks; ++i) {
+        bm_chunk_record& r = g_last_trace[i];
+        r.chunk_index = records[i].chunk_index;
+        r.candidate_objective = records[i].candidate_objective;
+        r.incumbent_objective = records[i].incumbent_objective;
+        r.accepted = records[i].accepted;
+        r.degenerate_repaired = records[i].degenerate_repaired;
+        if (trace && i < trace_cap) trace[i] = r;
     }
     if (g_profiling) g_prof.flush(g_profile);
 }
@@ -2299,18 +2306,13 @@ uint64_t choose_chunk_size_hint(bm_dataset* d, uint64_t k, std::vector<uint64_t>
 }
 
 // kmeans (local_search.cpp:62-94): init per method (init.seed), then lloyd.
-void kmeans(const bm_dataset* d, uint64_t k, const bm_init_config& init, uint64_t max_iterations,
-            double rel_tolerance, bm_outcome* out) {
+// The initialization stage of kmeans (local_search.cpp:66-83): w.C / w.mask
+// hold the start centroids afterwards; returns the init's distance evals.
+uint64_t init_stage(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t k, const bm_init_config& init) {
     if (k < 1) throw ConfigError("kmeans: k must be at least 1");
     if (d->m < k) throw ConfigError("kmeans: dataset has fewer points than clusters");
-    if (max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
-    if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
     if (init.method < 0 || init.method > 2) throw ConfigError("kmeans: unknown initialization method");
-    DeviceGuard g(d->device);
-    cudaStream_t st = stream_of(d);
-    Workspace& w = get_ws(d, d->m, (int)k, std::max(1, init.candidates_per_step), 0);
     Mt64 rng(init.seed);  // :71
-    const auto t_init = std::chrono::steady_clock::now();
     BM_CUDA(cudaMemsetAsync(w.C.p, 0, k * d->n * sizeof(double), st));
     BM_CUDA(cudaMemsetAsync(w.mask.p, 1, k, st));
     uint64_t init_evals = 0;
@@ -2324,8 +2326,24 @@ void kmeans(const bm_dataset* d, uint64_t k, const bm_init_config& init, uint64_
         kmeans_parallel_device(st, d, P, w, k, init, rng, init_evals);
     }
     BM_CUDA(cudaStreamSynchronize(st));
+    return init_evals;
+}
+
+void kmeans(const bm_dataset* d, uint64_t k, const bm_init_config& init, uint64_t max_iterations,
+            double rel_tolerance, bm_outcome* out) {
+    if (k < 1) throw ConfigError("kmeans: k must be at least 1");
+    if (d->m < k) throw ConfigError("kmeans: dataset has fewer points than clusters");
+    if (max_iterations < 1) throw ConfigError("lloyd: max_iterations must be at least 1");
+    if (rel_tolerance < 0.0) throw ConfigError("lloyd: rel_tolerance must be nonnegative");
+    if (init.method < 0 || init.method > 2) throw ConfigError("kmeans: unknown initialization method");
+    DeviceGuard g(d->device);
+    cudaStream_t st = stream_of(d);
+    Workspace& w = get_ws(d, d->m, (int)k, std::max(1, init.candidates_per_step), 0);
+    const auto t_init = std::chrono::steady_clock::now();
+    const uint64_t init_evals = init_stage(st, d, w, k, init);
     out->cpu_init = seconds_since(t_init);
     const auto t_search = std::chrono::steady_clock::now();
+    Points P = dataset_points(d);
     LloydResult r = lloyd_run(st, P, w, max_iterations, rel_tolerance);
     BM_CUDA(cudaMemcpyAsync(out->centroids, w.C.p, k * d->n * sizeof(double), cudaMemcpyDeviceToHost, st));
     BM_CUDA(cudaMemcpyAsync(out->mask, w.mask.p, k, cudaMemcpyDeviceToHost, st));
@@ -2813,6 +2831,20 @@ bm_status bm_kmeans(const bm_dataset* data, uint64_t k, const bm_init_config* in
     return guarded([&] { kmeans(data, k, *init, max_iterations, rel_tolerance, out); });
 }
 
+bm_status bm_init_centroids(const bm_dataset* dc, uint64_t k, const bm_init_config* init, double* centroids,
+                            uint8_t* mask, uint64_t* evals) {
+    return guarded([&] {
+        DeviceGuard g(dc->device);
+        cudaStream_t st = stream_of(dc);
+        Workspace& w = get_ws(dc, dc->m, (int)k, std::max(1, init->candidates_per_step), 0);
+        const uint64_t e = init_stage(st, dc, w, k, *init);
+        BM_CUDA(cudaMemcpyAsync(centroids, w.C.p, k * dc->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaMemcpyAsync(mask, w.mask.p, k, cudaMemcpyDeviceToHost, st));
+        BM_CUDA(cudaStreamSynchronize(st));
+        if (evals) *evals = e;
+    });
+}
+
 bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uint64_t seed,
                        uint64_t max_iterations, double rel_tolerance, bm_outcome* out) {
     return guarded([&] {
@@ -2853,6 +2885,15 @@ bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uin
 bm_status bm_big_means(bm_dataset* d, const bm_config* cfg, bm_outcome* out, bm_chunk_record* trace,
                        uint64_t trace_capacity) {
     return guarded([&] { big_means(d, *cfg, out, trace, trace_capacity); });
+}
+
+bm_status bm_last_trace(bm_chunk_record* out, uint64_t capacity, uint64_t* count) {
+    return guarded([&] {
+        if (count) *count = g_last_trace.size();
+        if (out)
+            std::copy(g_last_trace.begin(), g_last_trace.begin() + std::min<uint64_t>(capacity, g_last_trace.size()),
+                      out);
+    });
 }
 
 // Debug: per-CTA phase timestamps of the screened assignment (-DBM_KTRACE builds only).
