@@ -246,10 +246,22 @@ typedef struct bm_profile {
      * 4 gather, 5 k-means++ distances, 6 Lloyd control */
     double phase_ms[8];
     uint64_t phase_count[8];
+    /* persistent chunk kernel (one launch per chunk; device globaltimer stamps
+     * taken inside the timed run itself): summed launch durations, launches,
+     * assignment passes (first assignment + one per Lloyd round) and update
+     * passes over the chunk, rows per chunk */
+    double chunk_ms_total;
+    uint64_t chunk_launches;
+    uint64_t chunk_assign_passes;
+    uint64_t chunk_update_passes;
+    uint64_t chunk_rows;
 } bm_profile;
 bm_status bm_set_profiling(int enabled);
 /* Debug builds (-DBM_KTRACE): per-CTA phase timestamps of the screened assignment. */
 bm_status bm_debug_ktrace(uint64_t* out, uint64_t count);
+/* Debug (BM_CHUNK_DBG=1): phase stamps of the persistent chunk kernel,
+ * [chunk % 4][round 0..6, 7 = tail][16] globaltimer ns. */
+bm_status bm_debug_chunk_phases(uint64_t* out);
 bm_status bm_last_profile(bm_profile* out);
 
 #ifdef __cplusplus

@@ -51,7 +51,9 @@ class bm_profile(C.Structure):
     _fields_ = [("assign_ms_total", dbl), ("assign_launches", u64),
                 ("assign_rows_total", u64), ("kernel_launches", u64), ("final_ms", dbl),
                 ("final_rows", u64), ("screen_candidates", u64), ("screen_rows", u64),
-                ("phase_ms", dbl * 8), ("phase_count", u64 * 8)]
+                ("phase_ms", dbl * 8), ("phase_count", u64 * 8),
+                ("chunk_ms_total", dbl), ("chunk_launches", u64), ("chunk_assign_passes", u64),
+                ("chunk_update_passes", u64), ("chunk_rows", u64)]
 
 
 # name -> (restype, argtypes)
@@ -85,6 +87,8 @@ PROTOS = {
                            P_u64, P_u64]),
     "bm_kmeans_pp": (C.c_int, [vp, u64, i32, u64, u64, dbl, C.POINTER(bm_outcome)]),
     "bm_kmeans": (C.c_int, [vp, u64, C.POINTER(bm_init_config), u64, dbl, C.POINTER(bm_outcome)]),
+    "bm_init_centroids": (C.c_int, [vp, u64, C.POINTER(bm_init_config), P_dbl, C.POINTER(C.c_uint8), P_u64]),
+    "bm_last_trace": (C.c_int, [C.POINTER(bm_chunk_record), u64, P_u64]),
     "bm_choose_chunk_size_hint": (C.c_int, [vp, u64, P_u64, u64, u64, u64, u64, dbl, i32, u64, P_u64, P_dbl]),
     "bm_big_means": (C.c_int, [vp, C.POINTER(bm_config), C.POINTER(bm_outcome),
                                C.POINTER(bm_chunk_record), u64]),
@@ -92,6 +96,7 @@ PROTOS = {
     "bm_set_profiling": (C.c_int, [C.c_int]),
     "bm_debug_ktrace": (C.c_int, [P_u64, u64]),
     "bm_last_profile": (C.c_int, [C.POINTER(bm_profile)]),
+    "bm_debug_chunk_phases": (C.c_int, [P_u64]),
 }
 
 _lib = None

@@ -20,15 +20,16 @@ LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libbigmeans_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = [os.path.join(CSRC, "engine.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "common.cuh")] + [
-    os.path.join(ROOT, "include", "bigmeans_b200.h")]
+SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "chunk.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("kernels.cuh", "common.cuh", "device_common.cuh", "chunk.h",
+                                           "mt64.cuh", "tma.cuh")] + [os.path.join(ROOT, "include", "bigmeans_b200.h")]
+DEPS = SOURCES + HEADERS
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17", "-fmad=false",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fno-fast-math", "-Xcompiler", "-ffp-contract=off",
-    "-shared", "-I" + os.path.join(ROOT, "include"),
+    "-I" + os.path.join(ROOT, "include"),
 ]
 
 
@@ -40,11 +41,23 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit (in parallel) and link the shared library."""
     if not force and not needs_build():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(LIB_DIR, os.path.basename(src) + ".o")
+        cmd = [NVCC, *FLAGS, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd), cmd))
+        objs.append(obj)
+    for p, cmd in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SOURCES]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

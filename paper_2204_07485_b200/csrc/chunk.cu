@@ -1,0 +1,1053 @@
+// chunk.cu — persistent chunk kernel: one cooperative launch per Big-means
+// chunk (lloyd local_search.cpp:16-60 + accept big_means.cpp:89-94).
+//
+// Why: the multi-launch path (engine.cu) streams the chunk from L2 through a
+// TMA ring on every round and pays two launches and CTA-wide phase barriers
+// per round; on B200 that left the chunk-loop assignment at 0.05-0.15 of the
+// HBM roofline.  Here the chunk's rows are loaded into shared memory ONCE
+// (148 SMs x 227 KB holds a c2/c3 chunk) and every round reuses them; rounds
+// are separated by two grid barriers instead of kernel boundaries.
+//
+// Layout.  CTA g owns rows [g*B, g*B+B) of the chunk.  Real-valued data
+// ("ordered" mode): B = 1024, so CTA g IS reduction tile g and every
+// per-tile fold of the reference (update partials core.cpp:200-215, block_sum
+// core.cpp:165-173) is CTA-local and sequential in index order; partials are
+// merged in tile order (core.cpp:217-229).  Exact-sum data (every value an
+// integer multiple of 2^e, m*max|x| < 2^52*2^e: DESIGN §3.2b): all sums are
+// exact in fp64 whatever the order, so B is chosen to spread the chunk over
+// the SMs.
+//
+// One round (r >= 1):  [load centroids C from global -> compacted fp32/fp64
+// copies + norms]  assign (certified fp32 screen with the point rows in
+// registers, exact fp64 direct-form recheck of the candidates in ascending j,
+// strict <: reproduces assign_nearest core.cpp:129-155 bit for bit) ->
+// speculative update partials of the new labels (stable member lists, one
+// thread per (label, dim) folding the members in index order) -> grid
+// barrier A (fast distance sums and "changed" flags arrive with it) -> the
+// stop tests of local_search.cpp:39-50, decided identically by every CTA on
+// certified intervals of the unordered sums (exact block sums only when the
+// interval cannot decide) -> merge of the partials (one thread per (label,
+// dim), tile order, sum * (1.0/count): core.cpp:231-242) -> grid barrier B.
+// After the stop: exact block_sum of the final distances (tile folds, tile
+// order), the strict accept against f_opt, the record, the next start.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+#include <vector>
+
+#include "chunk.h"
+#include "common.cuh"
+
+namespace bm {
+namespace dev {
+namespace {
+
+constexpr int kCMaxT = 512;  // threads per CTA
+constexpr int kCKMax = 32;   // centroids (labels) per chunk kernel
+
+__device__ __forceinline__ float2 ffma2x(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+
+__device__ __forceinline__ unsigned long long u2(float2 a) { return *reinterpret_cast<const unsigned long long*>(&a); }
+__device__ __forceinline__ float2 f2(unsigned long long v) { return *reinterpret_cast<const float2*>(&v); }
+#define BM_F2OP2(name, ins)                                                    \
+    __device__ __forceinline__ float2 name(float2 a, float2 b) {              \
+        unsigned long long d;                                                  \
+        asm(ins " %0, %1, %2;" : "=l"(d) : "l"(u2(a)), "l"(u2(b)));            \
+        return f2(d);                                                          \
+    }
+BM_F2OP2(add2_rd, "add.rm.f32x2")
+BM_F2OP2(add2_ru, "add.rp.f32x2")
+BM_F2OP2(sub2_rd, "sub.rm.f32x2")
+BM_F2OP2(sub2_ru, "sub.rp.f32x2")
+BM_F2OP2(mul2_rd, "mul.rm.f32x2")
+BM_F2OP2(mul2_ru, "mul.rp.f32x2")
+BM_F2OP2(mul2_rn, "mul.rn.f32x2")
+BM_F2OP2(add2_rn, "add.rn.f32x2")
+#undef BM_F2OP2
+__device__ __forceinline__ float2 fma2_ru(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rp.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(u2(a)), "l"(u2(b)), "l"(u2(c)));
+    return f2(d);
+}
+__device__ __forceinline__ float2 ffma2s(float2 a, float b, float2 c) { return ffma2x(a, make_float2(b, b), c); }
+
+// Certified bounds of two (point, centroid) pairs at once (the screen's error
+// model, DESIGN §3.1 / chunk_screen_consts): dot = fp32 dot products, nx* / nc*
+// the fp32 norms (sum of squares rounded down / up, sqrt of the upper rounded
+// up; out-of-range rows carry (0, inf, inf), which yields L = 0 and a U that
+// never lowers the minimum).
+__device__ __forceinline__ void bounds2(float2 dot, float2 nxl, float2 nxh, float2 nxr, float2 ncl, float2 nch,
+                                        float2 ncr, const ScreenConsts& c, float2& L, float2& U) {
+    const float2 t2 = mul2_rn(dot, make_float2(2.f, 2.f));  // exact
+    const float2 Sn = add2_ru(nxr, ncr);
+    const float2 D = fma2_ru(mul2_ru(Sn, make_float2(c.K, c.K)), Sn, make_float2(c.dabs, c.dabs));
+    const float2 Al = add2_rd(nxl, ncl), Ah = add2_ru(nxh, nch);
+    const float2 Lr = mul2_rd(sub2_rd(sub2_rd(Al, t2), D), make_float2(c.lo64, c.lo64));
+    L = make_float2(fmaxf(Lr.x, 0.f), fmaxf(Lr.y, 0.f));
+    U = mul2_ru(add2_ru(sub2_ru(Ah, t2), D), make_float2(c.hi64, c.hi64));
+}
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid-wide barrier (all CTAs co-resident: cooperative launch).  Generation
+// counting: the arrival counter returns to 0 at every barrier, the generation
+// only grows, so the state carries over between launches.  The CTA's writes
+// are ordered before thread 0's release arrival by the CTA barrier (release is
+// cumulative); the waiters' acquire loads order everything after.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = ld_acquire(bar + 1);
+        unsigned arrived;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+        if (arrived == G - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+        } else {
+            while (ld_acquire(bar + 1) == gen) {
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Left fold from 0.0 of `len` doubles (global, L2; loads issued ahead of the adds).
+__device__ double fold_global(const double* v, int len) {
+    double a = 0.0;
+    int i = 0;
+    for (; i + 16 <= len; i += 16) {
+        double t[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) t[r] = __ldcg(v + i + r);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) a = __dadd_rn(a, t[r]);
+    }
+    for (; i < len; ++i) a = __dadd_rn(a, __ldcg(v + i));
+    return a;
+}
+
+// Direct-form squared distance (core.cpp:142-146): x row (storage T, shared
+// memory, 16-byte aligned), c row fp64 (shared, 16-byte aligned).
+template <typename T>
+__device__ __forceinline__ double exact_dist(const T* __restrict__ x, const double* __restrict__ c, int n) {
+    double s = 0.0;
+    int d = 0;
+    if constexpr (sizeof(T) == 4) {
+        for (; d + 4 <= n; d += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(x + d);
+            const double2 c0 = *reinterpret_cast<const double2*>(c + d);
+            const double2 c1 = *reinterpret_cast<const double2*>(c + d + 2);
+            s = dist_step(s, static_cast<double>(xv.x), c0.x);
+            s = dist_step(s, static_cast<double>(xv.y), c0.y);
+            s = dist_step(s, static_cast<double>(xv.z), c1.x);
+            s = dist_step(s, static_cast<double>(xv.w), c1.y);
+        }
+    } else {
+        for (; d + 2 <= n; d += 2) {
+            const double2 xv = *reinterpret_cast<const double2*>(x + d);
+            const double2 c0 = *reinterpret_cast<const double2*>(c + d);
+            s = dist_step(s, xv.x, c0.x);
+            s = dist_step(s, xv.y, c0.y);
+        }
+    }
+    for (; d < n; ++d) s = dist_step(s, to_f64(x[d]), c[d]);
+    return s;
+}
+
+// Left fold from 0.0 of `len` doubles in shared memory (16-byte aligned).
+__device__ __forceinline__ double fold_smem(const double* v, int len) {
+    double a = 0.0;
+    int i = 0;
+    for (; i + 8 <= len; i += 8) {
+        const double2 v0 = *reinterpret_cast<const double2*>(v + i);
+        const double2 v1 = *reinterpret_cast<const double2*>(v + i + 2);
+        const double2 v2 = *reinterpret_cast<const double2*>(v + i + 4);
+        const double2 v3 = *reinterpret_cast<const double2*>(v + i + 6);
+        a = __dadd_rn(a, v0.x);
+        a = __dadd_rn(a, v0.y);
+        a = __dadd_rn(a, v1.x);
+        a = __dadd_rn(a, v1.y);
+        a = __dadd_rn(a, v2.x);
+        a = __dadd_rn(a, v2.y);
+        a = __dadd_rn(a, v3.x);
+        a = __dadd_rn(a, v3.y);
+    }
+    for (; i < len; ++i) a = __dadd_rn(a, v[i]);
+    return a;
+}
+
+}  // namespace
+
+// Shared-memory carve-up (host and device agree).
+struct CLayout {
+    size_t xs, u, cf, cd, nrm, act, lab, dist, red, total;
+    int cdld;         // fp64 centroid row stride: even, an odd number of 16-byte units
+};
+
+__host__ __device__ inline int chunk_cdld(int n) {
+    int c = n + (n & 1);
+    if (((c / 2) & 1) == 0) c += 2;
+    return c;
+}
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, int nd, int n, unsigned G) {
+    CLayout L{};
+    size_t o = 0;
+    L.xs = o;
+    o = al16(o + (size_t)B * xld * es);
+    // region U (aliased): screen lower bounds Ls[k][B] | member lists for the
+    // update | staging of this CTA's merge pairs | staged distance / tile partials
+    const size_t ls = (size_t)k * B * 4;
+    const int nc = (B + 31) / 32;
+    const size_t sort = al16((size_t)B * 2) + al16((size_t)B) + al16((size_t)nc * k * 4) + al16((size_t)(2 * k + 2) * 4);
+    const size_t kn = (size_t)k * n, ppc = (kn + G - 1) / G;
+    const size_t merge = al16(ppc * G * 8) + al16((ppc / (size_t)n + 2) * G * 4);
+    const size_t tailf = (size_t)kTile * 8;  // exact-sum mode: a staged 1024-row tile of distances
+    size_t u = ls > sort ? ls : sort;
+    u = u > merge ? u : merge;
+    u = u > tailf ? u : tailf;
+    L.cdld = chunk_cdld(n);
+    L.u = o;
+    o = al16(o + u);
+    L.cf = o;
+    o = al16(o + (size_t)kCKMax * nd * 4);
+    L.cd = o;
+    o = al16(o + (size_t)kCKMax * chunk_cdld(n) * 8);
+    L.nrm = o;
+    o = al16(o + 3 * kCKMax * 4);
+    L.act = o;
+    o = al16(o + (kCKMax + 4) * 4);
+    L.lab = o;
+    o = al16(o + (size_t)B * 4);
+    L.dist = o;
+    o = al16(o + (size_t)B * 8);
+    L.red = o;
+    o = al16(o + 64 * 8);
+    L.total = o;
+    return L;
+}
+
+// Per-CTA control state, identical in every CTA (computed from the same
+// global values after each barrier).
+struct CCtl {
+    double f, f_lo, f_hi;
+    unsigned long long evals, iterations;
+    int stop, undecided, ka, state_error;
+    unsigned gdirty;  // labels whose membership changed in some tile this round
+};
+
+// Debug phase stamps (ChunkArgs::dbg, BM_CHUNK_DBG=1): CTA 0's globaltimer at
+// the phase boundaries of rounds 0..6 (row 7: the tail), chunk % 4.
+#define CDBG(row, ph)                                                                        \
+    do {                                                                                     \
+        if (a.dbg && cta == 0 && tid == 0 && (row) < 8)                                      \
+            a.dbg[((s_chunk & 3ull) * 8 + (row)) * 16 + (ph)] = gtimer();                    \
+    } while (0)
+
+template <typename T, int ND, int PPT>
+__global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ ChunkArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    if (!__ldcg(&a.gs->go)) return;  // a chunk queued behind one that needs a repair: nothing to do
+    const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+    const unsigned G = gridDim.x, cta = blockIdx.x;
+    const int B = a.B, n = a.n, k = a.k, xld = a.xld;
+    const uint64_t p0 = static_cast<uint64_t>(cta) * B;
+    const int np = static_cast<int>(min(static_cast<uint64_t>(B), a.rows - p0));
+    const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G);
+    const int cdld = L.cdld;
+    T* xs = reinterpret_cast<T*>(sm + L.xs);
+    float* Ls = reinterpret_cast<float*>(sm + L.u);
+    float* cf = reinterpret_cast<float*>(sm + L.cf);
+    double* cd = reinterpret_cast<double*>(sm + L.cd);
+    float* ncl = reinterpret_cast<float*>(sm + L.nrm);
+    float* nch = ncl + kCKMax;
+    float* ncr = nch + kCKMax;
+    int* act = reinterpret_cast<int*>(sm + L.act);
+    int* lab = reinterpret_cast<int*>(sm + L.lab);
+    double* dist = reinterpret_cast<double*>(sm + L.dist);
+    double* red = reinterpret_cast<double*>(sm + L.red);
+    __shared__ CCtl ctl;
+    __shared__ int s_any;
+    const float finf = __int_as_float(0x7F800000);
+    const double dinf = __longlong_as_double(0x7FF0000000000000LL);
+    __shared__ unsigned long long s_chunk;
+    if (cta == 0 && tid == 0) {
+        s_chunk = __ldcg(a.chunk_ctr);
+        if (a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = gtimer();
+    }
+    CDBG(7, 13);
+
+    // ---- the chunk's rows -> shared memory (once for all rounds) ----
+    {
+        const int vpr = static_cast<int>((static_cast<size_t>(n) * sizeof(T) + 15) / 16);  // 16-byte vectors per row
+        const unsigned char* src = static_cast<const unsigned char*>(a.X) + p0 * a.ld * sizeof(T);
+        for (int v = tid; v < np * vpr; v += NT) {
+            const int p = v / vpr, q = v - p * vpr;
+            cpa16(sm + L.xs + (static_cast<size_t>(p) * xld * sizeof(T)) + q * 16,
+                  src + static_cast<size_t>(p) * a.ld * sizeof(T) + q * 16);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        for (int e = tid; e < kCKMax * ND; e += NT) cf[e] = 0.f;  // padding rows / dims stay 0
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+    }
+    // this thread's points: p = tid + i*NT; fp32 rows in registers, norms (rd/ru)
+    // PPT == 2: xp[d] = (x_p0[d], x_p1[d]) (point pairs share every centroid
+    // load); PPT == 1: xp[h] = (x[2h], x[2h+1]) (dimension pairs).  Norms as
+    // (p0, p1) pairs (PPT == 1: both halves p0's).
+    constexpr int NX = PPT == 2 ? ND : ND / 2;
+    constexpr int JU = 8;  // centroids per screen pass (independent FMA chains)
+    float2 xp[NX];
+    float2 nxl2, nxh2, nxr2;
+    int mylab[PPT];
+    {
+        float lo[2] = {0.f, 0.f}, hi[2] = {0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+            const int p = tid + i * NT;
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                const float v = (p < np && d < n) ? static_cast<float>(xs[static_cast<size_t>(p) * xld + d]) : 0.f;
+                if constexpr (PPT == 2) {
+                    if (i == 0) xp[d].x = v;
+                    else xp[d].y = v;
+                } else {
+                    if (d & 1) xp[d >> 1].y = v;
+                    else xp[d >> 1].x = v;
+                }
+                lo[i] = __fmaf_rd(v, v, lo[i]);
+                hi[i] = __fmaf_ru(v, v, hi[i]);
+            }
+            mylab[i] = -1;
+        }
+        if (PPT == 1) {
+            lo[1] = lo[0];
+            hi[1] = hi[0];
+        }
+        // rows beyond the fp32 range guarantee of the bounds: (0, inf, inf)
+        const bool ok0 = hi[0] <= 1.0e36f, ok1 = hi[1] <= 1.0e36f;
+        nxl2 = make_float2(ok0 ? lo[0] : 0.f, ok1 ? lo[1] : 0.f);
+        nxh2 = make_float2(ok0 ? hi[0] : finf, ok1 ? hi[1] : finf);
+        nxr2 = make_float2(ok0 ? __fsqrt_ru(hi[0]) : finf, ok1 ? __fsqrt_ru(hi[1]) : finf);
+    }
+    if (tid == 0) {
+        ctl.evals = 0;
+        ctl.iterations = 0;
+        ctl.stop = 0;
+        ctl.state_error = 0;
+    }
+
+    const uint64_t ntiles = tiles_of(a.rows);
+    for (unsigned long long r = 0;; ++r) {
+        const int rr = r < 7 ? static_cast<int>(r) : 7;
+        CDBG(rr, 0);
+        const int slot = static_cast<int>(r & 1);
+        // ---- centroids: C (global) -> compacted fp64 / fp32 rows + norms ----
+        if (warp == 0) {
+            const bool live = lane < k && !__ldcg(a.mask + lane);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
+            if (live) act[__popc(bal & ((1u << lane) - 1u))] = lane;
+            if (lane == 0) act[kCKMax] = __popc(bal);
+        }
+        __syncthreads();
+        const int KA = act[kCKMax];
+        // compacted fp64 / fp32 copies (all threads: one L2 round trip), then
+        // the fp32 norms, a warp per row (warp sums rounded down / up: any
+        // order bounds the exact value)
+        for (int e = tid; e < KA * n; e += NT) {
+            const int rk = e / n, d = e - rk * n;
+            const double v = __ldcg(a.C + static_cast<size_t>(act[rk]) * n + d);
+            cd[rk * cdld + d] = v;
+            cf[rk * ND + d] = __double2float_rn(v);
+        }
+        __syncthreads();
+        for (int rk = warp; rk < KA; rk += NW) {
+            float lo = 0.f, hi = 0.f;
+            for (int d = lane; d < n; d += 32) {
+                const float f = cf[rk * ND + d];
+                lo = __fmaf_rd(f, f, lo);
+                hi = __fmaf_ru(f, f, hi);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = __fadd_rd(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+                hi = __fadd_ru(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+            }
+            if (lane == 0) {
+                const bool ok = hi <= 1.0e36f;  // beyond: (0, inf, inf), see bounds2
+                ncl[rk] = ok ? lo : 0.f;
+                nch[rk] = ok ? hi : finf;
+                ncr[rk] = ok ? __fsqrt_ru(hi) : finf;
+            }
+        }
+        __syncthreads();
+        if (KA == 0) {  // assign_nearest on all-degenerate centroids (core.cpp:115-118)
+            if (tid == 0) ctl.state_error = 1;
+            break;
+        }
+
+        CDBG(rr, 1);
+        // ---- assign: certified fp32 screen ----
+        // groups of JG centroids (8, then 4 / 2 / 1 for the rest: no padding
+        // work); per point the running minimum of the upper bounds and the
+        // running candidate mask {j : L_j <= running min at j} (a superset of
+        // the final candidates, filtered against the final minimum below)
+        float2 minU2 = make_float2(finf, finf);
+        unsigned rm[2] = {0u, 0u};
+        auto group = [&](auto jg_tag, int j0) {
+            constexpr int JG = decltype(jg_tag)::value;
+            float2 acc[JG];
+#pragma unroll
+            for (int u = 0; u < JG; ++u) acc[u] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d4 = 0; d4 < ND / 4; ++d4) {
+#pragma unroll
+                for (int u = 0; u < JG; ++u) {
+                    const float4 c = *reinterpret_cast<const float4*>(cf + (j0 + u) * ND + 4 * d4);
+                    if constexpr (PPT == 2) {
+                        acc[u] = ffma2s(xp[4 * d4], c.x, acc[u]);
+                        acc[u] = ffma2s(xp[4 * d4 + 1], c.y, acc[u]);
+                        acc[u] = ffma2s(xp[4 * d4 + 2], c.z, acc[u]);
+                        acc[u] = ffma2s(xp[4 * d4 + 3], c.w, acc[u]);
+                    } else {
+                        acc[u] = ffma2x(xp[2 * d4], make_float2(c.x, c.y), acc[u]);
+                        acc[u] = ffma2x(xp[2 * d4 + 1], make_float2(c.z, c.w), acc[u]);
+                    }
+                }
+            }
+            if constexpr (PPT == 2) {  // bounds of (p0, p1) x centroid j
+#pragma unroll
+                for (int u = 0; u < JG; ++u) {
+                    const int j = j0 + u;
+                    float2 Lb, Ub;
+                    bounds2(acc[u], nxl2, nxh2, nxr2, make_float2(ncl[j], ncl[j]), make_float2(nch[j], nch[j]),
+                            make_float2(ncr[j], ncr[j]), a.cst, Lb, Ub);
+                    Ls[j * B + tid] = Lb.x;
+                    Ls[j * B + tid + NT] = Lb.y;
+                    minU2 = make_float2(fminf(minU2.x, Ub.x), fminf(minU2.y, Ub.y));
+                    rm[0] |= (Lb.x <= minU2.x ? 1u : 0u) << j;
+                    rm[1] |= (Lb.y <= minU2.y ? 1u : 0u) << j;
+                }
+            } else {  // bounds of p x centroids (j, j+1)
+#pragma unroll
+                for (int u = 0; u < JG; u += 2) {
+                    const int j = j0 + u;
+                    const bool v1 = u + 1 < JG;
+                    const float2 dot = v1 ? add2_rn(make_float2(acc[u].x, acc[v1 ? u + 1 : u].x),
+                                                    make_float2(acc[u].y, acc[v1 ? u + 1 : u].y))
+                                          : make_float2(__fadd_rn(acc[u].x, acc[u].y), 0.f);
+                    const int j1 = v1 ? j + 1 : j;
+                    float2 Lb, Ub;
+                    bounds2(dot, nxl2, nxh2, nxr2, make_float2(ncl[j], ncl[j1]), make_float2(nch[j], nch[j1]),
+                            make_float2(ncr[j], ncr[j1]), a.cst, Lb, Ub);
+                    Ls[j * B + tid] = Lb.x;
+                    minU2.x = fminf(minU2.x, Ub.x);
+                    rm[0] |= (Lb.x <= minU2.x ? 1u : 0u) << j;
+                    if (v1) {
+                        Ls[j1 * B + tid] = Lb.y;
+                        minU2.x = fminf(minU2.x, Ub.y);
+                        rm[0] |= (Lb.y <= minU2.x ? 1u : 0u) << j1;
+                    }
+                }
+            }
+        };
+        {
+            int j0 = 0;
+            for (; j0 + 8 <= KA; j0 += 8) group(std::integral_constant<int, 8>{}, j0);
+            if (j0 + 4 <= KA) {
+                group(std::integral_constant<int, 4>{}, j0);
+                j0 += 4;
+            }
+            if (j0 + 2 <= KA) {
+                group(std::integral_constant<int, 2>{}, j0);
+                j0 += 2;
+            }
+            if (j0 < KA) group(std::integral_constant<int, 1>{}, j0);
+        }
+        const float minU[2] = {minU2.x, minU2.y};
+        CDBG(rr, 2);
+        // ---- exact fp64 recheck of the candidates: ascending j, strict < ----
+        // final candidates: the running ones whose L_j <= the final minimum;
+        // every thread rechecks its own points (lanes in lock step: one
+        // candidate per point is the common case)
+        unsigned cmask[PPT];
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+            const int p = tid + i * NT;
+            unsigned m = 0, r0 = p < np ? rm[i] : 0u;
+            while (r0) {
+                const int j = __ffs(r0) - 1;
+                r0 &= r0 - 1;
+                m |= (Ls[j * B + p] <= minU[i] ? 1u : 0u) << j;
+            }
+            cmask[i] = m;
+        }
+        CDBG(rr, 9);
+        CDBG(rr, 10);
+        CDBG(rr, 11);
+        unsigned chg = 0;  // labels this thread's points left or joined (r > 0)
+        double mysum = 0.0;
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+            const int p = tid + i * NT;
+            if (p >= np) continue;
+            double best = dinf;
+            int bj = -1;
+            {
+                unsigned m = cmask[i];
+                while (m) {
+                    const int j = __ffs(m) - 1;
+                    m &= m - 1;
+                    const double v = exact_dist(xs + static_cast<size_t>(p) * xld, cd + j * cdld, n);
+                    if (v < best) {
+                        best = v;
+                        bj = j;
+                    }
+                }
+            }
+            if (bj < 0) {  // no candidate (non-finite bounds): full exact scan
+                for (int j = 0; j < KA; ++j) {
+                    const double v = exact_dist(xs + static_cast<size_t>(p) * xld, cd + j * cdld, n);
+                    if (v < best) {
+                        best = v;
+                        bj = j;
+                    }
+                }
+                if (bj < 0) bj = 0;  // (NaN distances only; unreachable for finite data)
+            }
+            const int label = act[bj];
+            if (r > 0 && label != mylab[i]) chg |= (1u << label) | (1u << mylab[i]);
+            mylab[i] = label;
+            lab[p] = label;
+            dist[p] = best;
+            a.dists[static_cast<size_t>(slot) * a.rows + p0 + p] = best;
+            mysum += best;
+        }
+        __syncthreads();  // red / wsum reuse below
+        // CTA sum of the distances (unordered: certified interval below)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mysum += __shfl_down_sync(0xFFFFFFFFu, mysum, o);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) chg |= __shfl_xor_sync(0xFFFFFFFFu, chg, o);
+        if (lane == 0) {
+            red[warp] = mysum;
+            reinterpret_cast<unsigned*>(red + 32)[warp] = chg;
+        }
+        __syncthreads();
+        // labels whose membership changed in this tile (round 0: all of them);
+        // only their update partials are refolded, only they are re-merged
+        unsigned dirty = 0;
+        for (int w = 0; w < NW; ++w) dirty |= reinterpret_cast<const unsigned*>(red + 32)[w];
+        if (r == 0) dirty = k >= 32 ? 0xFFFFFFFFu : (1u << k) - 1u;
+        if (tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < NW; ++w) s += red[w];
+            atomicAdd(a.rsum + slot, s);
+            if (r > 0 && dirty) atomicOr(a.rchg + slot, static_cast<int>(dirty));
+        }
+
+        CDBG(rr, 3);
+        // ---- speculative update partials of the new labels (core.cpp:200-215) ----
+        if (dirty) {
+            const int nc = (np + 31) / 32;
+            unsigned char* up = sm + L.u;
+            uint16_t* members = reinterpret_cast<uint16_t*>(up);
+            unsigned char* rk = up + al16(static_cast<size_t>(B) * 2);
+            int* cnt = reinterpret_cast<int*>(rk + al16(static_cast<size_t>(B)));
+            int* ltot = cnt + al16(static_cast<size_t>(nc) * k * 4) / 4;
+            int* loff = ltot + k + 1;
+            for (int e = tid; e < nc * k; e += NT) cnt[e] = 0;
+            __syncthreads();
+            for (int c = warp; c < nc; c += NW) {
+                const int p = 32 * c + lane;
+                const int l = p < np ? lab[p] : -1;
+                const unsigned peers = __match_any_sync(0xFFFFFFFFu, l);
+                const int rnk = __popc(peers & ((1u << lane) - 1u));
+                if (p < np) {
+                    rk[p] = static_cast<unsigned char>(rnk);
+                    if (rnk == 0) cnt[c * k + l] = __popc(peers);
+                }
+            }
+            __syncthreads();
+            for (int j = warp; j < k; j += NW) {  // chunk-wise exclusive offsets per label
+                const int v = lane < nc ? cnt[lane * k + j] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (lane < nc) cnt[lane * k + j] = incl - v;
+                if (lane == 31) ltot[j] = incl;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const int v = lane < k ? ltot[lane] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (lane < k) loff[lane + 1] = incl;
+                if (lane == 0) loff[0] = 0;
+            }
+            __syncthreads();
+            for (int p = tid; p < np; p += NT) {
+                const int l = lab[p];
+                members[loff[l] + cnt[(p >> 5) * k + l] + rk[p]] = static_cast<uint16_t>(p);
+            }
+            __syncthreads();
+            CDBG(rr, 12);
+            // lane groups of LG lanes, one label per group, DPL dims per lane:
+            // row[d] += x[d] over the label's members in index order
+            // (core.cpp:206-214), member rows fetched 8 ahead of the adds
+            constexpr int LG = ND <= 64 ? 16 : 32;
+            constexpr int DPL = (ND + LG - 1) / LG;
+            const int NG = NT / LG, g = tid / LG, gl = tid - g * LG;
+            for (int j = g; j < k; j += NG) {
+                if (!((dirty >> j) & 1u)) continue;  // same members as last round: same partial
+                const int b = loff[j], e = loff[j + 1];
+                double acc[DPL];
+#pragma unroll
+                for (int t = 0; t < DPL; ++t) acc[t] = 0.0;
+                for (int i = b; i < e; i += 8) {
+                    const int cnt8 = min(8, e - i);
+                    int mr[8];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) mr[r] = r < cnt8 ? members[i + r] : 0;
+                    T xv[8][DPL];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+#pragma unroll
+                        for (int t = 0; t < DPL; ++t) {
+                            const int d = gl + LG * t;
+                            xv[r][t] = d < n ? xs[static_cast<size_t>(mr[r]) * xld + d] : T(0);
+                        }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (r < cnt8)
+#pragma unroll
+                            for (int t = 0; t < DPL; ++t) acc[t] = __dadd_rn(acc[t], to_f64(xv[r][t]));
+                }
+#pragma unroll
+                for (int t = 0; t < DPL; ++t) {
+                    const int d = gl + LG * t;
+                    if (d < n) a.part[(static_cast<size_t>(j) * n + d) * G + cta] = acc[t];
+                }
+                if (gl == 0) a.pcnt[static_cast<size_t>(j) * G + cta] = static_cast<unsigned>(e - b);
+            }
+        }
+        CDBG(rr, 4);
+        grid_sync(a.bar, G);  // ---------------- barrier A ----------------
+        CDBG(rr, 5);
+        // this CTA's merge pairs: their tile partials and counts staged now
+        // (speculatively: discarded when the loop stops), overlapping the control
+        const int kn = k * n;
+        const int ppc = (kn + static_cast<int>(G) - 1) / static_cast<int>(G);
+        const int q0 = static_cast<int>(cta) * ppc, q1 = min(kn, q0 + ppc);
+        double* stage = reinterpret_cast<double*>(sm + L.u);
+        unsigned* cstage = reinterpret_cast<unsigned*>(sm + L.u + al16(static_cast<size_t>(ppc) * G * 8));
+        const int mj0 = q0 / n;
+        if (q0 < q1) {
+            const int j1 = (q1 - 1) / n;
+            const size_t cnt_pairs = static_cast<size_t>(q1 - q0) * G;
+            const double* src = a.part + static_cast<size_t>(q0) * G;
+            for (size_t e = tid; e < cnt_pairs; e += NT) stage[e] = __ldcg(src + e);
+            for (size_t e = tid; e < static_cast<size_t>(j1 - mj0 + 1) * G; e += NT)
+                cstage[e] = __ldcg(a.pcnt + static_cast<size_t>(mj0) * G + e);
+        }
+
+        // ---- Lloyd control (local_search.cpp:26-51), every CTA identically ----
+        if (tid == 0) {
+            const double s = __ldcg(a.rsum + slot);
+            const int chg_all = __ldcg(a.rchg + slot);
+            ctl.gdirty = r == 0 ? 0xFFFFFFFFu : static_cast<unsigned>(chg_all);
+            double lo, hi;
+            sum_interval(s, a.rows, G, &lo, &hi);
+            ctl.evals += a.rows * static_cast<unsigned long long>(KA);
+            ctl.undecided = 0;
+            if (r == 0) {  // :26-28
+                ctl.f = s;
+                ctl.f_lo = lo;
+                ctl.f_hi = hi;
+                ctl.stop = 0;
+            } else {
+                ctl.iterations = r;  // :36
+                bool stop = chg_all == 0;  // :39-44
+                if (!stop) {
+                    if (ctl.f <= 0.0) {  // :45-47 (nonnegative terms: exact f is 0 iff the sum is)
+                        stop = true;
+                    } else if (a.rel_tolerance > 0.0) {  // :48-50 on intervals
+                        const double flo = fmax(ctl.f_lo, 0x1p-1074), fhi = ctl.f_hi;
+                        bool decided = !a.force_exact && isfinite(fhi) && isfinite(hi);
+                        if (decided) {
+                            const double a_lo = __dsub_rn(flo, hi), a_hi = __dsub_rn(fhi, lo);
+                            const double g0 = __ddiv_rn(a_lo, flo), g1 = __ddiv_rn(a_lo, fhi);
+                            const double g2 = __ddiv_rn(a_hi, flo), g3 = __ddiv_rn(a_hi, fhi);
+                            const double gmin = fmin(fmin(g0, g1), fmin(g2, g3));
+                            const double gmax = fmax(fmax(g0, g1), fmax(g2, g3));
+                            if (gmax < a.rel_tolerance) stop = true;
+                            else if (!(gmin >= a.rel_tolerance)) decided = false;
+                        }
+                        if (!decided) ctl.undecided = 1;
+                    }
+                }
+                ctl.stop = stop ? 1 : 0;
+                if (!stop && !ctl.undecided) {  // :51
+                    ctl.f = s;
+                    ctl.f_lo = lo;
+                    ctl.f_hi = hi;
+                }
+            }
+        }
+        __syncthreads();
+        if (ctl.undecided) {  // exact block sums of both assignments (grid-uniform branch)
+            for (uint64_t t = static_cast<uint64_t>(cta) * NT + tid; t < 2 * ntiles; t += static_cast<uint64_t>(G) * NT) {
+                const int which = t < ntiles ? 0 : 1;  // 0: previous assignment, 1: this one
+                const uint64_t tt = t - which * ntiles;
+                const int sl = which ? slot : slot ^ 1;
+                const uint64_t tb = tt * kTile;
+                const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), a.rows - tb));
+                a.tiles[t] = fold_global(a.dists + static_cast<size_t>(sl) * a.rows + tb, len);
+            }
+            grid_sync(a.bar, G);
+            if (tid == 0) {
+                double f = 0.0, fn = 0.0;
+                for (uint64_t t = 0; t < ntiles; ++t) f = __dadd_rn(f, __ldcg(a.tiles + t));
+                for (uint64_t t = 0; t < ntiles; ++t) fn = __dadd_rn(fn, __ldcg(a.tiles + ntiles + t));
+                const bool stop = __ddiv_rn(__dsub_rn(f, fn), f) < a.rel_tolerance;
+                ctl.stop = stop ? 1 : 0;
+                if (!stop) {
+                    const double s = __ldcg(a.rsum + slot);
+                    double lo, hi;
+                    sum_interval(s, a.rows, G, &lo, &hi);
+                    ctl.f = s;
+                    ctl.f_lo = lo;
+                    ctl.f_hi = hi;
+                }
+            }
+            __syncthreads();
+        }
+        if (r >= 1 && r >= a.max_iterations) {  // :32 loop bound
+            if (tid == 0) ctl.stop = 1;
+            __syncthreads();
+        }
+        if (ctl.stop) break;
+        // the other round slot: nobody reads it again before the next barrier B
+        if (cta == 0 && tid == 0) {
+            a.rsum[slot ^ 1] = 0.0;
+            a.rchg[slot ^ 1] = 0;
+        }
+
+        CDBG(rr, 6);
+        // ---- merge (core.cpp:217-242): this CTA's (label, dim) pairs, tile order ----
+        if (q0 < q1) {
+            const unsigned gdirty = ctl.gdirty;
+            for (int q = q0 + tid; q < q1; q += NT) {
+                const int j = q / n, d = q - j * n;
+                if (!((gdirty >> j) & 1u)) continue;  // no tile changed this label: C, mask unchanged
+                const double* sv = stage + static_cast<size_t>(q - q0) * G;
+                const unsigned* cv = cstage + static_cast<size_t>(j - mj0) * G;
+                double tot = 0.0;
+                unsigned c = 0;
+                unsigned g = 0;
+                for (; g + 8 <= G; g += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int r8 = 0; r8 < 8; ++r8) {
+                        v[r8] = sv[g + r8];
+                        c += cv[g + r8];
+                    }
+#pragma unroll
+                    for (int r8 = 0; r8 < 8; ++r8) tot = __dadd_rn(tot, v[r8]);
+                }
+                for (; g < G; ++g) {
+                    tot = __dadd_rn(tot, sv[g]);
+                    c += cv[g];
+                }
+                double v = 0.0;
+                if (c) v = __dmul_rn(tot, __ddiv_rn(1.0, static_cast<double>(c)));  // :237-239
+                a.C[q] = v;
+                if (d == 0) a.mask[j] = c == 0 ? 1 : 0;
+            }
+        }
+        CDBG(rr, 7);
+        grid_sync(a.bar, G);  // ---------------- barrier B ----------------
+        CDBG(rr, 8);
+    }
+
+    // ---- after the stop: exact objective (block_sum), accept, record ----
+    CDBG(7, 9);
+    const int fslot = static_cast<int>(ctl.iterations & 1);
+    if (!ctl.state_error) {
+        // block_sum inner folds (core.cpp:167-173) of the final distances, one
+        // thread per 1024-row tile from shared memory: ordered mode folds its
+        // own tile (dist[]); exact-sum mode stages tile `cta` from global first
+        if (a.ordered) {
+            if (tid == 0) a.tiles[cta] = fold_smem(dist, np);
+        } else if (cta < ntiles) {
+            double* stage = reinterpret_cast<double*>(sm + L.u);
+            const uint64_t tb = static_cast<uint64_t>(cta) * kTile;
+            const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), a.rows - tb));
+            const double* src = a.dists + static_cast<size_t>(fslot) * a.rows + tb;
+            for (int i = tid; i < len; i += NT) stage[i] = __ldcg(src + i);
+            __syncthreads();
+            if (tid == 0) a.tiles[cta] = fold_smem(stage, len);
+        }
+    }
+    CDBG(7, 10);
+    grid_sync(a.bar, G);
+    CDBG(7, 11);
+    if (cta != 0) return;
+    __shared__ int s_acc;
+    __shared__ unsigned char s_mk[kCKMax];
+    __shared__ double s_fc;
+    {  // the tile partials -> shared memory (coalesced), folded in tile order by thread 0
+        double* tstage = reinterpret_cast<double*>(sm + L.u);
+        for (uint64_t t = tid; t < ntiles; t += NT) tstage[t] = __ldcg(a.tiles + t);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const double fo = __ldcg(&a.gs->fopt_exact);
+        const double fc = fold_smem(reinterpret_cast<const double*>(sm + L.u), static_cast<int>(ntiles));
+        const int accepted = !ctl.state_error && fc < fo;  // :89 strict
+        s_acc = accepted;
+        s_fc = fc;
+        const unsigned long long chunk = __ldcg(a.chunk_ctr);
+        Record* rec = a.rec_base + chunk;
+        rec->chunk_index = chunk;
+        rec->candidate_objective = fc;
+        rec->incumbent_objective = accepted ? fc : fo;
+        rec->accepted = static_cast<unsigned long long>(accepted);
+        rec->degenerate_repaired = static_cast<unsigned long long>(__ldcg(&a.gs->inc_degenerate));
+        if (accepted) {
+            *a.f_opt = fc;
+            a.gs->fopt_exact = fc;
+        }
+        *a.chunk_ctr = chunk + 1;
+        a.rsum[0] = 0.0;  // every CTA read the round slots before the last barrier
+        a.rsum[1] = 0.0;
+        a.rchg[0] = 0;
+        a.rchg[1] = 0;
+    }
+    __syncthreads();
+    const int accepted = s_acc;
+    // incumbent := trained (accepted); next start (:82) := incumbent
+    for (int j = tid; j < k; j += NT) {
+        const uint8_t mv = accepted ? __ldcg(a.mask + j) : __ldcg(a.maskinc + j);
+        s_mk[j] = mv;
+        if (accepted) a.maskinc[j] = mv;
+        else a.mask[j] = mv;
+    }
+    for (int e = tid; e < k * n; e += NT) {
+        if (accepted) a.Cinc[e] = __ldcg(a.C + e);
+        else a.C[e] = __ldcg(a.Cinc + e);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int dcount = 0;
+        for (int j = 0; j < k; ++j) dcount += s_mk[j] ? 1 : 0;
+        a.gs->inc_degenerate = dcount;
+        a.gs->go = dcount == 0;
+        a.gs->n_active = k - dcount;
+        if (accepted) a.gs->n_active_inc = k - dcount;
+        a.gs->pending_fix = -1;
+        LloydStatus* st = a.st;
+        st->f = ctl.f;
+        st->objective = s_fc;
+        st->evals = ctl.evals;
+        st->iterations = ctl.iterations;
+        st->parity = fslot;
+        st->stop = 1;
+        st->changed = 0;
+        st->state_error = ctl.state_error;
+        st->inc_degenerate = dcount;
+        st->bad_label = 0;
+        st->incomplete = 0;
+        if (a.host_st) {
+            volatile LloydStatus* h = a.host_st;
+            h->objective = s_fc;
+            h->evals = ctl.evals;
+            h->iterations = ctl.iterations;
+            h->stop = 1;
+            h->state_error = ctl.state_error;
+            h->inc_degenerate = dcount;
+            h->bad_label = 0;
+            h->incomplete = 0;
+        }
+        if (a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk + 1] = gtimer();
+        CDBG(7, 12);
+    }
+    (void)s_any;
+}
+
+}  // namespace dev
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+namespace {
+
+float f_ru32(double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) < x) f = std::nextafter(f, INFINITY);
+    return f;
+}
+float f_rd32(double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) > x) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+
+template <typename T, int ND, int PPT>
+void* kernel_ptr() {
+    return reinterpret_cast<void*>(&dev::k_chunk<T, ND, PPT>);
+}
+
+// (ND, PPT) instances: ND = padded width (multiple of 8, or 4 below 8).
+struct Inst {
+    int nd, ppt;
+    void* f32;
+    void* f64;
+};
+
+const std::vector<Inst>& instances() {
+    static const std::vector<Inst> v = {
+        {8, 2, kernel_ptr<float, 8, 2>(), kernel_ptr<double, 8, 2>()},
+        {16, 2, kernel_ptr<float, 16, 2>(), kernel_ptr<double, 16, 2>()},
+        {24, 2, kernel_ptr<float, 24, 2>(), kernel_ptr<double, 24, 2>()},
+        {32, 2, kernel_ptr<float, 32, 2>(), kernel_ptr<double, 32, 2>()},
+        {40, 1, kernel_ptr<float, 40, 1>(), kernel_ptr<double, 40, 1>()},
+        {56, 1, kernel_ptr<float, 56, 1>(), kernel_ptr<double, 56, 1>()},
+        {72, 1, kernel_ptr<float, 72, 1>(), kernel_ptr<double, 72, 1>()},
+        {88, 1, kernel_ptr<float, 88, 1>(), kernel_ptr<double, 88, 1>()},
+    };
+    return v;
+}
+
+std::mutex g_attr_mu;
+
+}  // namespace
+
+dev::ScreenConsts chunk_screen_consts(int n) {
+    // dot products: two interleaved fp32 FMA chains over the dimension pairs,
+    // added at the end -> |err| <= gamma_{ceil(n/2)+1} sum|x_d c_d|; taken as
+    // gamma_{n+2} (covers any n); the rest as in engine.cu's screen_consts.
+    const double u = std::ldexp(1.0, -24);
+    auto gam = [&](double m) { return m * u / (1.0 - m * u); };
+    const double gb = gam(n + 2);
+    const double up = u * (1.0 + 4 * u) / (1.0 - u);
+    const double K = gb / 2.0 + 2.0 * up + up * up;
+    const double u64 = std::ldexp(1.0, -53);
+    const double g64 = (n + 3) * u64 / (1.0 - (n + 3) * u64);
+    dev::ScreenConsts c;
+    c.K = f_ru32(K * (1.0 + 1e-6));
+    c.dabs = std::ldexp(1.0f, -40);
+    c.lo64 = f_rd32((1.0 - g64) * (1.0 - 4 * u64));
+    c.hi64 = f_ru32((1.0 + g64) * (1.0 + 4 * u64));
+    return c;
+}
+
+ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums) {
+    ChunkPlan p;
+    if (k < 1 || k > dev::kCKMax || n < 1 || s < 1 || s > (1ull << 31)) return p;
+    const Inst* in = nullptr;
+    for (const Inst& i : instances())
+        if (n <= i.nd) {
+            in = &i;
+            break;
+        }
+    if (!in) return p;
+    int sms = 148, smem_optin = 227 * 1024;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const int es = storage == BM_F64 ? 8 : 4;
+    // shared-memory row: whole 16-byte units, an odd number of them (conflict-free row reads)
+    int units = (n * es + 15) / 16;
+    if ((units & 1) == 0) ++units;
+    const int xld = units * 16 / es;
+    int B, threads;
+    if (!exact_sums) {  // ordered: one reduction tile per CTA
+        if (in->ppt != 2) return p;
+        B = kTile;
+        threads = kTile / 2;
+    } else {  // exact sums: spread over the SMs
+        const uint64_t per = (s + sms - 1) / sms;
+        threads = static_cast<int>(std::min<uint64_t>(dev::kCMaxT, ((per + in->ppt - 1) / in->ppt + 31) / 32 * 32));
+        threads = std::max(threads, 32);
+        B = threads * in->ppt;
+    }
+    const unsigned grid = static_cast<unsigned>((s + B - 1) / B);
+    if (grid > static_cast<unsigned>(sms)) return p;  // one CTA per SM, all co-resident
+    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid);
+    if (L.total + 2048 > static_cast<size_t>(smem_optin)) return p;
+    p.ok = true;
+    p.B = B;
+    p.threads = threads;
+    p.ppt = in->ppt;
+    p.nd = in->nd;
+    p.xld = xld;
+    p.ordered = exact_sums ? 0 : 1;
+    p.grid = grid;
+    p.smem = L.total;
+    return p;
+}
+
+void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a0) {
+    void* fn = nullptr;
+    for (const Inst& i : instances())
+        if (i.nd == p.nd && i.ppt == p.ppt) fn = storage == BM_F64 ? i.f64 : i.f32;
+    if (!fn) throw CudaError("chunk kernel: no instance");
+    {
+        // the attribute is per device: set it on the current one (idempotent)
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        BM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
+    }
+    dev::ChunkArgs a = a0;
+    a.B = p.B;
+    a.xld = p.xld;
+    a.ordered = p.ordered;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(p.threads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* args[] = {&a};
+    BM_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+}
+
+}  // namespace bm

@@ -1,0 +1,73 @@
+// chunk.h — the persistent chunk kernel (chunk.cu): one cooperative launch
+// runs a whole Big-means chunk on the device — lloyd (local_search.cpp:16-60:
+// the first assignment, every update/assign round, the stop tests) and the
+// accept (big_means.cpp:89-94) with its record — with the chunk's rows held
+// in shared memory across all rounds.  Host-visible plan + launch entry.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "bigmeans_b200.h"
+#include "device_common.cuh"
+
+namespace bm {
+namespace dev {
+
+// Everything one chunk launch reads and writes (pointers into the Workspace).
+struct ChunkArgs {
+    const void* X;            // the gathered chunk: rows x ld, storage T
+    uint64_t rows;            // s
+    int n;
+    uint64_t ld;              // global row stride (elements)
+    int k;
+    int B;                    // points per CTA (ordered mode: 1024 = one reduction tile)
+    int xld;                  // shared-memory row stride (elements)
+    int ordered;              // 1: real-valued data, CTA = 1024-tile, tile-order merge; 0: exact sums
+    double* C;                // working centroids k x n (the start; then every update)
+    uint8_t* mask;            // their degenerate mask
+    double* part;             // update partials [k*n][G] (CTA g's fold of label j, dim d)
+    unsigned* pcnt;           // member counts [k][G]
+    double* dists;            // [2][rows]: the distances of the last two assignments
+    double* tiles;            // [2][ntiles]: exact 1024-tile partials (tolerance fallback, accept)
+    unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
+    double* rsum;             // [2] per-round fast distance sums (slot = round & 1)
+    int* rchg;                // [2] per-round "a label changed" flags
+    ScreenConsts cst;
+    unsigned long long max_iterations;
+    double rel_tolerance;
+    int force_exact;          // test hook: every interval decision takes the exact path
+    // accept (big_means.cpp:89-94) and chain state
+    double* f_opt;
+    double* Cinc;
+    uint8_t* maskinc;
+    Record* rec_base;
+    unsigned long long* chunk_ctr;
+    GState* gs;
+    LloydStatus* st;          // this chunk buffer's status
+    LloydStatus* host_st;     // mapped host copy of it
+    unsigned long long* timing;  // optional [2 * timing_cap]: per chunk, globaltimer at CTA 0's start and the accept's end
+    unsigned long long timing_cap;
+    unsigned long long* dbg;  // optional [4][8][16] phase stamps (BM_CHUNK_DBG)
+};
+
+}  // namespace dev
+
+// Launch geometry for one (s, n, k, storage) — ok == false: use the
+// multi-launch path (engine.cu).
+struct ChunkPlan {
+    bool ok = false;
+    int B = 0, threads = 0, ppt = 0, nd = 0, xld = 0, ordered = 0;
+    unsigned grid = 0;
+    size_t smem = 0;
+};
+
+ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums);
+// Enqueue one chunk (cooperative launch, capturable into a graph).
+void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a);
+// The certified-screen constants of the chunk kernel's dot-product order.
+dev::ScreenConsts chunk_screen_consts(int n);
+
+}  // namespace bm

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "bigmeans_b200.h"
+#include "chunk.h"
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
@@ -184,6 +185,26 @@ struct Workspace {
     DevBuf<uint8_t> maskinc;
     DevBuf<dev::Record> drec;              // per-chunk records (big_means trace)
     DevBuf<unsigned long long> chunk_ctr;  // device-side chunk index
+    // persistent chunk kernel (chunk.cu): update partials, tile partials, grid
+    // barrier, per-round sums / flags, per-chunk timing stamps
+    DevBuf<double> cpart, ctiles, crsum;
+    DevBuf<unsigned> cpcnt, cbar;
+    DevBuf<int> crchg;
+    DevBuf<unsigned long long> ctiming;
+    void ensure_chunk(const ChunkPlan& p) {
+        const uint64_t kn = (uint64_t)k * n;
+        if (cpart.n < kn * p.grid) cpart.alloc(kn * p.grid);
+        if (cpcnt.n < (uint64_t)k * p.grid) cpcnt.alloc((uint64_t)k * p.grid);
+        if (ctiles.n < 2 * tiles) ctiles.alloc(2 * tiles);
+        if (!cbar.n) {
+            cbar.alloc(2);
+            BM_CUDA(cudaMemset(cbar.p, 0, 2 * sizeof(unsigned)));
+            crsum.alloc(2);
+            BM_CUDA(cudaMemset(crsum.p, 0, 2 * sizeof(double)));
+            crchg.alloc(2);
+            BM_CUDA(cudaMemset(crchg.p, 0, 2 * sizeof(int)));
+        }
+    }
     // CUDA graphs of one chunk (sample resolution + gather, and the Lloyd loop)
     std::string graph_sig;
     // graph mode: chunk c uses graphs [c % 4]: data and state buffer c % 4, draw buffer c % 2
@@ -1429,6 +1450,29 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
 // big_means (big_means.cpp:58-112)
 // ---------------------------------------------------------------------------
 // ---- CUDA graphs of one steady-state chunk --------------------------------
+// BM_CHUNK_DBG=1: the chunk kernel stamps its phases (bm_debug_chunk_phases).
+unsigned long long* chunk_dbg_buffer() {
+    static unsigned long long* p = [] {
+        unsigned long long* q = nullptr;
+        if (std::getenv("BM_CHUNK_DBG")) {
+            BM_CUDA(cudaMalloc(&q, 4 * 8 * 16 * sizeof(unsigned long long)));
+            BM_CUDA(cudaMemset(q, 0, 4 * 8 * 16 * sizeof(unsigned long long)));
+        }
+        return q;
+    }();
+    return p;
+}
+
+// BM_PERSIST=0: the multi-launch chunk graphs instead of the persistent chunk
+// kernel (A/B checks; the kernel also needs a plan that fits, chunk_plan).
+bool persist_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_PERSIST");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
 bool graphs_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("BM_GRAPHS");
@@ -1618,16 +1662,17 @@ cudaGraphExec_t capture_spec(cudaStream_t st, Workspace& w, const Points& P, int
 }
 
 void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, SamplerWs& sw, Workspace& w,
-                   const Points& P, uint64_t max_it, double tol) {
+                   const Points& P, uint64_t max_it, double tol, bool persist = false) {
     char sig[512];
     // the dataset enters only through shape: its base is read from sw.xslot
     std::snprintf(sig, sizeof(sig), "%llu/%llu/%d/%p/%p/%p/%p/%p/%p/%llu/%a/%llu/%d/%a/%p",
                   (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
                   (void*)dc.chunk3.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n,
-                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse + 8 * (int)w.sum_cluster, w.sum_scale,
-                  (void*)w.sums.p);
-    if (w.graph_sig == sig && w.g_lloyd[0]) return;
+                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse + 8 * (int)w.sum_cluster +
+                      16 * (int)persist,
+                  w.sum_scale, (void*)w.sums.p);
+    if (w.graph_sig == sig && w.g_prep[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
     void* bufs[dev::kStateBufs] = {dc.chunk.p, dc.chunk1.p, dc.chunk2.p, dc.chunk3.p};
@@ -1637,6 +1682,7 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
         Points Pb = P;
         Pb.X = bufs[i];
         w.g_prep[i] = capture_prep(st, d, sw, i % 2, bufs[i]);
+        if (persist) continue;  // the chunk is one persistent kernel launch (launch_chunk)
         w.g_lloyd[i] = capture_lloyd(st, w, Pb, max_it, tol, b);
         if (fast) {
             w.g_cont[i] = capture_cont(st, w, Pb, max_it, tol, b);
@@ -1687,8 +1733,17 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         BM_CUDA(cudaMemcpyAsync(sw->xslot.p, &d->X, sizeof(void*), cudaMemcpyHostToDevice, st));
     }
     const bool use_graphs = !identity && !g_profiling && graphs_enabled();
+    // persistent chunk kernel (chunk.cu): one cooperative launch per chunk
+    ChunkPlan cplan;
+    if (use_graphs && persist_enabled() && !w.hist_cap)
+        cplan = chunk_plan(d->device, s, n, k, d->dtype, d->exact_sums && exact_sums_enabled());
+    const bool persist = cplan.ok;
+    if (persist) {
+        w.ensure_chunk(cplan);
+        if (w.ctiming.n < 2 * w.drec.n) w.ctiming.alloc(2 * w.drec.n);
+    }
     // exact-sum mode for the graph chunks (kernels.cuh §5b)
-    w.sums_on = use_graphs && d->exact_sums && exact_sums_enabled() && screen_enabled(k) && tma_screen() &&
+    w.sums_on = use_graphs && !persist && d->exact_sums && exact_sums_enabled() && screen_enabled(k) && tma_screen() &&
                 s < (1ull << 31) && !w.hist_cap;
     if (w.sums_on) {
         w.sum_scale = std::ldexp(1.0, -d->sum_exp);
@@ -1707,8 +1762,9 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaMemsetAsync(w.grp_ctr.p, 0, w.grp_ctr.n * sizeof(unsigned), st));
         }
     }
-    if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
+    if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance, persist);
     uint64_t evals = 0, iterations = 0;
+    uint64_t chunk_assign_passes = 0, chunk_update_passes = 0;
     int inc_degenerate = k;
     std::vector<uint8_t> hmask(k);
 
@@ -1766,7 +1822,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         };
         // BM_SPEC=0: no speculative begins (every chunk graph runs its own)
         static const bool spec_on = !(std::getenv("BM_SPEC") && std::string(std::getenv("BM_SPEC")) == "0");
-        const bool spec = spec_on && w.g_spec[0] != nullptr;
+        const bool spec = spec_on && !persist && w.g_spec[0] != nullptr;
         if (spec && !dc.sstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.sstream, cudaStreamNonBlocking));
         auto launch_spec = [&](uint64_t c) {  // chunk c's first assignment, overlapping chunks c-2 and c-1
             const int i = (int)(c % dev::kStateBufs);
@@ -1786,7 +1842,42 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i], 0));
             if (spec) BM_CUDA(cudaStreamWaitEvent(st, w.ev_spec[i], 0));
             cudaEvent_t e0 = tl_ev(st);
-            BM_CUDA(cudaGraphLaunch(w.g_lloyd[i], st));
+            if (persist) {
+                dev::ChunkArgs a{};
+                a.X = bufP[i].X;
+                a.rows = s;
+                a.n = n;
+                a.ld = d->ld;
+                a.k = k;
+                a.C = w.C.p;
+                a.mask = w.mask.p;
+                a.part = w.cpart.p;
+                a.pcnt = w.cpcnt.p;
+                a.dists = w.dists.p + 3 * (uint64_t)i * w.R;
+                a.tiles = w.ctiles.p;
+                a.bar = w.cbar.p;
+                a.rsum = w.crsum.p;
+                a.rchg = w.crchg.p;
+                a.cst = chunk_screen_consts(n);
+                a.max_iterations = cfg.max_iterations;
+                a.rel_tolerance = cfg.rel_tolerance;
+                a.force_exact = force_exact_control() ? 1 : 0;
+                a.f_opt = w.fopt.p;
+                a.Cinc = w.Cinc.p;
+                a.maskinc = w.maskinc.p;
+                a.rec_base = w.drec.p;
+                a.chunk_ctr = w.chunk_ctr.p;
+                a.gs = w.gs.p;
+                a.st = w.status.p + i;
+                a.host_st = w.h_status.p + i;
+                a.timing = w.ctiming.p;
+                a.timing_cap = w.ctiming.n / 2;
+                a.dbg = chunk_dbg_buffer();
+                launch_chunk(st, cplan, d->dtype, a);
+                count_launch();
+            } else {
+                BM_CUDA(cudaGraphLaunch(w.g_lloyd[i], st));
+            }
             if (timeline) tl.push_back({1, e0, tl_ev(st)});
             BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
         };
@@ -1822,7 +1913,15 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 BM_CUDA(cudaStreamSynchronize(st));
                 std::swap(w.drec.p, bigger.p);
                 std::swap(w.drec.n, bigger.n);
-                ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance);
+                if (persist && w.ctiming.n < 2 * w.drec.n) {
+                    DevBuf<unsigned long long> t2(2 * w.drec.n);
+                    BM_CUDA(cudaMemcpyAsync(t2.p, w.ctiming.p, w.ctiming.n * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToDevice, st));
+                    BM_CUDA(cudaStreamSynchronize(st));
+                    std::swap(w.ctiming.p, t2.p);
+                    std::swap(w.ctiming.n, t2.n);
+                }
+                ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance, persist);
             }
             const int b = (int)(chunk % dev::kStateBufs), i6 = b;
             if (inc_degenerate > 0) {  // kmeanspp_fill (:84) after this chunk's sample draws
@@ -1879,10 +1978,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             if (ls.bad_label) throw ConfigError("update_centroids: label out of range");
             evals += ls.evals;  // lloyd accumulate (local_search.cpp:55-58)
             iterations += ls.iterations;
+            chunk_assign_passes += ls.iterations + 1;
+            chunk_update_passes += ls.iterations;
             inc_degenerate = ls.inc_degenerate;
             static const bool iters_log = std::getenv("BM_ITERS") != nullptr;  // diagnostics: Lloyd rounds per chunk
             if (iters_log) std::fprintf(stderr, "[iters] %llu %llu\n", (unsigned long long)chunk, ls.iterations);
-            count_launch(3 + 3 * ls.iterations);
+            if (!persist) count_launch(3 + 3 * ls.iterations);
             out->chunks = chunk + 1;
             if (ahead) --ahead;
             if (queued) --queued;
@@ -2035,6 +2136,18 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     }
     out->distance_evals = evals;
     out->iterations = iterations;  // :97
+    if (persist && out->chunks) {  // device time of the chunk kernels (globaltimer stamps, timed run)
+        const uint64_t nc = std::min<uint64_t>(out->chunks, w.ctiming.n / 2);
+        std::vector<unsigned long long> tm(2 * nc);
+        BM_CUDA(cudaMemcpy(tm.data(), w.ctiming.p, tm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        double ns = 0.0;
+        for (uint64_t c = 0; c < nc; ++c) ns += (double)(tm[2 * c + 1] - tm[2 * c]);
+        g_profile.chunk_ms_total = ns * 1e-6;
+        g_profile.chunk_launches = nc;
+        g_profile.chunk_assign_passes = chunk_assign_passes;
+        g_profile.chunk_update_passes = chunk_update_passes;
+        g_profile.chunk_rows = s;
+    }
     g_last_trace.resize(out->chunks);
     for (uint64_t i = 0; i < out->chunks; ++i) {
         bm_chunk_record& r = g_last_trace[i];
@@ -2893,6 +3006,15 @@ bm_status bm_last_trace(bm_chunk_record* out, uint64_t capacity, uint64_t* count
         if (out)
             std::copy(g_last_trace.begin(), g_last_trace.begin() + std::min<uint64_t>(capacity, g_last_trace.size()),
                       out);
+    });
+}
+
+// Debug: the chunk kernel's phase stamps ([4][8][16] globaltimer values; BM_CHUNK_DBG=1).
+bm_status bm_debug_chunk_phases(uint64_t* out) {
+    return guarded([&] {
+        unsigned long long* p = chunk_dbg_buffer();
+        if (!p) throw ConfigError("set BM_CHUNK_DBG=1");
+        BM_CUDA(cudaMemcpy(out, p, 4 * 8 * 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }
 

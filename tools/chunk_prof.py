@@ -1,0 +1,49 @@
+"""Per-chunk kernel time of the persistent chunk kernel (globaltimer stamps)
+and the graph timeline, for one config: python tools/chunk_prof.py c2 [chunks]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2204_07485_b200 as bm  # noqa: E402
+from paper_2204_07485_b200 import synthetic  # noqa: E402
+
+key = sys.argv[1]
+w = synthetic.CONFIGS[key]
+chunks = int(sys.argv[2]) if len(sys.argv) > 2 else w.chunks
+X = synthetic.generate(key)
+d = bm.Dataset(X)
+cfg = bm.BigMeansConfig(k=w.k, chunk_size=w.s, max_chunks=chunks, seed=w.seed)
+for rep in range(3):
+    out, tr = bm.big_means(d, cfg, want_labels=False)
+    p = bm.last_profile()
+    n = max(p["chunk_launches"], 1)
+    print(f"{key} rep{rep}: cpu_init {out.counter.cpu_init*1e3:.2f} ms, final {out.counter.cpu_full*1e3:.2f} ms, "
+          f"chunk kernels {p['chunk_launches']} avg {p['chunk_ms_total']/n*1e3:.1f} us, "
+          f"assign passes/chunk {p['chunk_assign_passes']/n:.2f}, iters {out.counter.iterations}", flush=True)
+
+if os.environ.get("BM_CHUNK_DBG"):
+    import ctypes as C
+    import numpy as np
+    from paper_2204_07485_b200 import _capi
+    buf = np.zeros(4 * 8 * 16, np.uint64)
+    _capi.load().bm_debug_chunk_phases(buf.ctypes.data_as(C.POINTER(C.c_uint64)))
+    buf = buf.reshape(4, 8, 16).astype(np.int64)
+    names = ["start", "cent", "screen", "recheck", "fold", "barA", "ctl", "merge", "barB"]
+    for c in range(4):
+        t0 = buf[c, 0, 0]
+        if t0 == 0:
+            continue
+        print(f"chunk%4={c}")
+        for r in range(7):
+            row = buf[c, r]
+            if row[0] == 0:
+                continue
+            segs = [f"{names[i]}->{names[i+1]} {(row[i+1]-row[i])/1e3:.1f}" for i in range(8) if row[i + 1] >= row[i] > 0]
+            if row[9] and row[11]:
+                segs.append(f"[cand {(row[9]-row[2])/1e3:.1f} exact {(row[11]-row[9])/1e3:.1f}]")
+            if row[12] > row[3] > 0:
+                segs.append(f"[sort {(row[12]-row[3])/1e3:.1f} fold {(row[4]-row[12])/1e3:.1f}]")
+            print(f"  r{r} @{(row[0]-t0)/1e3:.1f}us: " + " | ".join(segs))
+        tail = buf[c, 7]
+        print(f"  rows->smem {(buf[c,0,0]-tail[13])/1e3:.1f} us")
+        print(f"  tail: loop-end @{(tail[9]-t0)/1e3:.1f} fold {(tail[10]-tail[9])/1e3:.1f} bar {(tail[11]-tail[10])/1e3:.1f} accept {(tail[12]-tail[11])/1e3:.1f}")
