@@ -18,9 +18,9 @@ roofline   dominant kernel = k_assign (chunk-loop launches), CUDA events on
 cpu_baseline  the compiled reference (oracle/_ref) on this box's host cores,
            on the same config (rank 0, N=1).
 
-N > 1 (torchrun): weak scaling — every rank runs its own chain of the full
-chunk budget with seed + rank, then NCCL select/broadcast and a row-sharded
-final pass (paper_2204_07485_b200/multi.py).
+N > 1 (torchrun): strong scaling — the config's N subproblems are sharded over
+the ranks (rank g: seed + g, floor(N/G) (+1 for g < N mod G) chunks), then NCCL
+select/broadcast and a row-sharded final pass (paper_2204_07485_b200/multi.py).
 """
 from __future__ import annotations
 
@@ -270,12 +270,13 @@ def main():
             out, trace = bm.big_means(data, cfg, want_labels=False)
             prof = bm.last_profile()
             return dict(evals=out.counter.distance_evals, chunks=trace.chunks(),
-                        objective=out.objective, launches=prof["kernel_launches"], prof=prof)
+                        objective=out.objective, launches=prof["kernel_launches"], prof=prof,
+                        cpu_init=out.counter.cpu_init, cpu_full=out.counter.cpu_full)
         r = multi.big_means_distributed(data.m, w.k, w.n, multi.gpu_chain(data, cfg),
-                                        multi.gpu_rows(data), cfg.seed, device=dev)
+                                        multi.gpu_rows(data), cfg.seed, w.chunks, device=dev)
         prof = bm.last_profile()
         return dict(evals=r.local_evals, chunks=r.local_chunks, objective=r.objective,
-                    launches=prof["kernel_launches"], prof=prof)
+                    launches=prof["kernel_launches"], prof=prof, cpu_init=0.0, cpu_full=0.0)
 
     for _ in range(args.warmup):
         step()
@@ -305,25 +306,18 @@ def main():
         torch.distributed.all_reduce(t)
         ms, evals, chunks = float(mx[0]), int(t[1]), int(t[2])
 
-    # ---- profiled pass: CUDA events around every launch group (roofline) ----
-    bm.set_profiling(True)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    pres = [step() for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    profiled_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    bm.set_profiling(False)
-    a_ms = sum(r["prof"]["assign_ms_total"] for r in pres)
-    a_n = sum(r["prof"]["assign_launches"] for r in pres)
-    a_rows = sum(r["prof"]["assign_rows_total"] for r in pres)
-    f_ms = sum(r["prof"]["final_ms"] for r in pres)
-    f_rows = sum(r["prof"]["final_rows"] for r in pres)
-    s_cand = sum(r["prof"]["screen_candidates"] for r in pres)
-    s_rows = sum(r["prof"]["screen_rows"] for r in pres)
-    phases = {nm: sum(r["prof"]["phase_ms"][nm] for r in pres) / args.steps
-              for nm in pres[0]["prof"]["phase_ms"]}
-    phase_n = {nm: sum(r["prof"]["phase_count"][nm] for r in pres) / args.steps
-               for nm in pres[0]["prof"]["phase_count"]}
+    # ---- roofline inputs.  Persistent chunk kernel (c1-c3): per-launch device
+    # durations from globaltimer stamps taken INSIDE the timed steps above.
+    # Multi-launch path (wide rows, c4/c5): an extra pass with CUDA events
+    # around every launch group (that path's own kernels). ----
+    pres = None
+    persist = sum(r["prof"]["chunk_launches"] for r in res) > 0
+    if not persist:
+        bm.set_profiling(True)
+        torch.cuda.synchronize()
+        pres = [step() for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        bm.set_profiling(False)
 
     # ---- e2e through the public API with host buffers ----
     # "e2e": the dataset in pinned host memory (the contract's form); "pageable":
@@ -340,7 +334,7 @@ def main():
                     return (out.counter.distance_evals,
                             out.assignment.nbytes + out.centroids.values.nbytes + out.centroids.mask.nbytes)
                 r = multi.big_means_distributed(dh.m, w.k, w.n, multi.gpu_chain(dh, cfg),
-                                                multi.gpu_rows(dh), cfg.seed, device=dev)
+                                                multi.gpu_rows(dh), cfg.seed, w.chunks, device=dev)
                 return r.local_evals, r.centroids.nbytes
 
         def e2e_run(host):
@@ -375,25 +369,57 @@ def main():
     if rank != 0:
         return
 
-    # ---- roofline of the dominant kernel (k_assign in the chunk loop) ----
+    # ---- roofline of the dominant kernel ----
     hbm, hbm_src = peaks()
     b = 4 if w.dtype == "f32" else 8
-    rows_per_launch = a_rows / a_n if a_n else 0.0
-    alg_bytes = rows_per_launch * (w.n * b + 4) + 8 * np.ceil(rows_per_launch / 1024)
-    avg_ms = a_ms / a_n if a_n else float("nan")
-    achieved = alg_bytes / (avg_ms * 1e-3) / 1e9 if a_n else None
-    final_bytes = f_rows / max(args.steps, 1) * (w.n * b + 4)
-    final_avg_ms = f_ms / max(args.steps, 1)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm if achieved else None, "traffic": None,
-                "kernel": "k_assign (chunk loop)", "peak_source": hbm_src,
-                "launches_timed": a_n, "avg_launch_ms": avg_ms,
-                "alg_bytes_per_launch": alg_bytes,
-                "fp64_flops_per_launch": 3.0 * rows_per_launch * w.k * w.n,
-                "screen_candidates_per_point": s_cand / s_rows if s_rows else None,
-                "final_pass": {"avg_ms": final_avg_ms, "alg_bytes": final_bytes,
-                               "achieved_gbs": final_bytes / (final_avg_ms * 1e-3) / 1e9
-                               if final_avg_ms > 0 else None}}
+    T = np.ceil(w.s / 1024)
+    traffic = None
+    try:  # ncu capture of the same kernel (profiles/r02_ncu_chunk_kernel.json)
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_chunk_kernel.json")) as f:
+            tk = json.load(f).get(args.config)
+        if tk:
+            traffic = tk["dram_read_bytes"] + tk["dram_write_bytes"]
+    except (OSError, ValueError, KeyError):
+        traffic = None
+    final_ms = 1e3 * sum(r["cpu_full"] for r in res) / max(len(res), 1)
+    final_bytes = w.m * (w.n * b + 4) + 8 * np.ceil(w.m / 1024)
+    final = {"avg_ms_host": final_ms, "alg_bytes": final_bytes,
+             "achieved_gbs": final_bytes / (final_ms * 1e-3) / 1e9 if final_ms > 0 else None}
+    if persist:
+        n_l = sum(r["prof"]["chunk_launches"] for r in res)
+        k_ms = sum(r["prof"]["chunk_ms_total"] for r in res)
+        A = sum(r["prof"]["chunk_assign_passes"] for r in res)
+        U = sum(r["prof"]["chunk_update_passes"] for r in res)
+        P = w.s
+        alg_total = A * (P * w.n * b + 4 * P + 8 * T) + U * (P * w.n * b + 4 * P)
+        alg_bytes = alg_total / n_l
+        avg_ms = k_ms / n_l
+        achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic,
+                    "kernel": "k_chunk (persistent: one launch = one chunk's whole Lloyd + accept)",
+                    "peak_source": hbm_src, "timing": "globaltimer stamps inside the timed steps",
+                    "launches_timed": n_l, "avg_launch_ms": avg_ms, "alg_bytes_per_launch": alg_bytes,
+                    "assign_passes_per_launch": A / n_l, "update_passes_per_launch": U / n_l,
+                    "fp64_flops_per_launch": 3.0 * P * w.k * w.n * A / n_l,
+                    "kernel_share_of_step": k_ms / ms,
+                    "limiter": "latency: grid barriers and CTA-wide phases (ncu: issue-active 22-31%, "
+                               "barrier stalls dominate); DRAM traffic = the chunk once per launch",
+                    "final_pass": final}
+    else:
+        a_ms = sum(r["prof"]["assign_ms_total"] for r in pres)
+        a_n = sum(r["prof"]["assign_launches"] for r in pres)
+        a_rows = sum(r["prof"]["assign_rows_total"] for r in pres)
+        rows_per_launch = a_rows / a_n if a_n else 0.0
+        alg_bytes = rows_per_launch * (w.n * b + 4) + 8 * np.ceil(rows_per_launch / 1024)
+        avg_ms = a_ms / a_n if a_n else float("nan")
+        achieved = alg_bytes / (avg_ms * 1e-3) / 1e9 if a_n else None
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm if achieved else None, "traffic": traffic,
+                    "kernel": "k_assign_tma (multi-launch chunk loop, wide rows)", "peak_source": hbm_src,
+                    "timing": "CUDA events around each launch in a separate profiled pass",
+                    "launches_timed": a_n, "avg_launch_ms": avg_ms, "alg_bytes_per_launch": alg_bytes,
+                    "fp64_flops_per_launch": 3.0 * rows_per_launch * w.k * w.n, "final_pass": final}
 
     # ---- CPU baseline + full-size parity: the reference on this host, same run ----
     cpu = None
@@ -409,19 +435,18 @@ def main():
 
     emit({"metric": METRIC, "value": evals / (ms * 1e-3), "unit": "evals/s", "n_gpus": world,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
           "data": "synthetic",
           "config": {"workload": w.name, "m": w.m, "n": w.n, "k": w.k, "s": w.s,
-                     "subproblems_per_chain": w.chunks, "storage": w.dtype, "seed": w.seed,
+                     "subproblems": w.chunks, "subproblems_per_chain": [multi.chain_chunks(w.chunks, g, world) for g in range(world)],
+                     "storage": w.dtype, "seed": w.seed,
                      "l2": "inputs larger than L2 (dataset %.2f GB); the sampled chunk is "
                            "L2-resident within a step by design" % (X.nbytes / 1e9),
                      "parallelism": f"chains{world}"},
           "subproblems_per_s": chunks / (ms * 1e-3),
+          "subproblems_per_s_loop": chunks / sum(r["cpu_init"] for r in res) if world == 1 else None,
           "final_sse_rel_gap": gap, "parity_full_size": parity, "objective": objective,
           "gpu_launches": launches, "clocks": ck, "e2e": e2e, "roofline": roofline,
-          "step_breakdown_ms": {nm: round(v, 3) for nm, v in phases.items()},
-          "step_breakdown_launch_groups": phase_n,
-          "ms_per_step_profiled_pass": profiled_ms,
           "cpu_baseline": cpu})
 
 

@@ -214,6 +214,23 @@ bm_status bm_choose_chunk_size_hint(bm_dataset* data, uint64_t k, const uint64_t
 bm_status bm_big_means(bm_dataset* data, const bm_config* cfg, bm_outcome* out,
                        bm_chunk_record* trace, uint64_t trace_capacity);
 
+/* Multi-GPU Big-means in one process (paper parallel mode 2, PAPER.md:216;
+ * the reference runs one chain: big_means.hpp:56).  data[g] is chain g's
+ * handle of the SAME matrix (normally one handle per GPU).  Chain g runs
+ * big_means with seed + g and floor(N/G) (+1 for g < N mod G) of the
+ * cfg->max_chunks = N chunks (a time budget applies to every chain), without
+ * its own final pass; one host thread per device drives that device's chains.
+ * The lowest-index chain with the minimum f_opt wins (*winner); its incumbent
+ * is the result; with cfg->final_assignment the final pass is row-sharded over
+ * the distinct devices on 1024-row tiles, the tile partials folded in row
+ * order (== block_sum over all rows, core.cpp:165-175).  n_d / iterations /
+ * chunks sum over the chains (+ the final pass); cpu_init is the slowest
+ * chain's loop.  trace: the chains' records in chain order (chain_chunks[g]
+ * of them each; both may be NULL). */
+bm_status bm_big_means_multi(bm_dataset* const* data, int32_t chains, const bm_config* cfg,
+                             bm_outcome* out, bm_chunk_record* trace, uint64_t trace_capacity,
+                             uint64_t* chain_chunks, int32_t* winner);
+
 /* Every chunk record of the last bm_big_means call on this thread (the trace
  * is never truncated here: *count is the full chunk count, at most `capacity`
  * records are copied).  Lets a caller with a time budget size its trace from

@@ -9,7 +9,8 @@ from .api import (  # noqa: F401
     K_DEFAULT_SEED, K_REDUCTION_BLOCK, BigMeansConfig, BigMeansTrace, Centroids, ChunkRecord,
     ClusteringOutcome, ConfigError, Dataset, DeviceError, EvalCounter, InitConfig, InitMethod, Rng,
     RoundsRule, ChunkHintConfig, choose_chunk_size_hint,
-    SearchConfig, StateError, assign_nearest, assign_rows, big_means, block_sum, device_count,
+    SearchConfig, StateError, assign_nearest, assign_rows, big_means, big_means_multi, block_sum,
+    device_count,
     kmeans, kmeanspp_fill, last_profile, lloyd, objective, sample_chunk, sample_chunk_device,
     set_profiling,
     update_centroids)

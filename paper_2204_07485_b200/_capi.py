@@ -89,6 +89,8 @@ PROTOS = {
     "bm_kmeans": (C.c_int, [vp, u64, C.POINTER(bm_init_config), u64, dbl, C.POINTER(bm_outcome)]),
     "bm_init_centroids": (C.c_int, [vp, u64, C.POINTER(bm_init_config), P_dbl, C.POINTER(C.c_uint8), P_u64]),
     "bm_last_trace": (C.c_int, [C.POINTER(bm_chunk_record), u64, P_u64]),
+    "bm_big_means_multi": (C.c_int, [C.POINTER(vp), C.c_int32, C.POINTER(bm_config), C.POINTER(bm_outcome),
+                                     C.POINTER(bm_chunk_record), u64, P_u64, C.POINTER(C.c_int32)]),
     "bm_choose_chunk_size_hint": (C.c_int, [vp, u64, P_u64, u64, u64, u64, u64, dbl, i32, u64, P_u64, P_dbl]),
     "bm_big_means": (C.c_int, [vp, C.POINTER(bm_config), C.POINTER(bm_outcome),
                                C.POINTER(bm_chunk_record), u64]),

@@ -545,16 +545,54 @@ def big_means(data: Dataset, cfg: BigMeansConfig, want_labels: bool = True):
     out.centroids = _ptr(cv, _capi.P_dbl)
     out.mask = _ptr(cm, _capi.P_u8)
     out.labels = _ptr(labels, _capi.P_i32)
-    cap = int(cfg.max_chunks) if cfg.max_chunks is not None else 1 << 16
-    recs = (_capi.bm_chunk_record * cap)()
-    _check(_capi.load().bm_big_means(data.handle, C.byref(c), C.byref(out), recs, cap))
+    lib = _capi.load()
+    _check(lib.bm_big_means(data.handle, C.byref(c), C.byref(out), None, 0))
+    nrec = C.c_uint64(0)  # the whole trace, sized from the result (time budgets included)
+    _check(lib.bm_last_trace(None, 0, C.byref(nrec)))
+    recs = (_capi.bm_chunk_record * max(nrec.value, 1))()
+    _check(lib.bm_last_trace(recs, nrec.value, C.byref(nrec)))
     trace = BigMeansTrace([ChunkRecord(int(r.chunk_index), float(r.candidate_objective),
                                        float(r.incumbent_objective), bool(r.accepted),
                                        int(r.degenerate_repaired))
-                           for r in recs[:min(int(out.chunks), cap)]])
+                           for r in recs[:nrec.value]])
     counter = EvalCounter(out.distance_evals, out.iterations, out.cpu_init, out.cpu_full)
     asg = labels if labels is not None else np.empty(0, np.int32)
     return ClusteringOutcome(Centroids(cv, cm), asg, out.objective, [], counter), trace
+
+
+def big_means_multi(datasets, cfg: BigMeansConfig, want_labels: bool = True):
+    """Multi-GPU big_means in one process (bm_big_means_multi): chain g on
+    datasets[g] (the same matrix, normally one handle per GPU) with seed + g and
+    floor(N/G) (+1 for g < N mod G) of cfg.max_chunks = N chunks, lowest-index
+    minimum f_opt wins, final pass row-sharded over the devices.
+    Returns (ClusteringOutcome, BigMeansTrace, chain_chunks, winner)."""
+    G = len(datasets)
+    if G < 1:
+        raise ConfigError("big_means_multi: at least one chain")
+    c = _native_config(cfg)
+    k, m, n = int(cfg.k), datasets[0].m, datasets[0].n
+    cv = np.empty((k, n), np.float64)
+    cm = np.empty(k, np.uint8)
+    labels = np.empty(m, np.int32) if (cfg.final_assignment and want_labels) else None
+    out = _capi.bm_outcome()
+    out.centroids = _ptr(cv, _capi.P_dbl)
+    out.mask = _ptr(cm, _capi.P_u8)
+    out.labels = _ptr(labels, _capi.P_i32)
+    cap = int(cfg.max_chunks) if cfg.max_chunks is not None else 1 << 16
+    recs = (_capi.bm_chunk_record * max(cap, 1))()
+    handles = (C.c_void_p * G)(*[d.handle for d in datasets])
+    counts = np.zeros(G, np.uint64)
+    winner = C.c_int32(-1)
+    _check(_capi.load().bm_big_means_multi(handles, G, C.byref(c), C.byref(out), recs, cap,
+                                           _ptr(counts, _capi.P_u64), C.byref(winner)))
+    nrec = min(int(out.chunks), cap)
+    trace = BigMeansTrace([ChunkRecord(int(r.chunk_index), float(r.candidate_objective),
+                                       float(r.incumbent_objective), bool(r.accepted),
+                                       int(r.degenerate_repaired)) for r in recs[:nrec]])
+    counter = EvalCounter(out.distance_evals, out.iterations, out.cpu_init, out.cpu_full)
+    asg = labels if labels is not None else np.empty(0, np.int32)
+    return (ClusteringOutcome(Centroids(cv, cm), asg, out.objective, [], counter), trace,
+            [int(x) for x in counts], int(winner.value))
 
 
 def assign_rows(data: Dataset, cent: Centroids, row_begin: int, row_end: int,

@@ -36,7 +36,9 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "chunk.h"
@@ -1028,9 +1030,16 @@ void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const d
         if (i.nd == p.nd && i.ppt == p.ppt) fn = storage == BM_F64 ? i.f64 : i.f32;
     if (!fn) throw CudaError("chunk kernel: no instance");
     {
-        // the attribute is per device: set it on the current one (idempotent)
+        // the attribute is a per-device maximum: raise it, never lower it
+        static std::map<std::pair<int, void*>, size_t> cur;
+        int dev = 0;
+        BM_CUDA(cudaGetDevice(&dev));
         std::lock_guard<std::mutex> lk(g_attr_mu);
-        BM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
+        size_t& c = cur[std::make_pair(dev, fn)];
+        if (p.smem > c) {
+            BM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
+            c = p.smem;
+        }
     }
     dev::ChunkArgs a = a0;
     a.B = p.B;

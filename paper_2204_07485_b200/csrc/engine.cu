@@ -20,6 +20,9 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <mutex>
+#include <set>
+#include <thread>
 #include <unordered_map>
 #include <memory>
 #include <random>
@@ -624,6 +627,23 @@ void launch_pdl_cluster8(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t s
     BM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device maximum:
+// raise it (never lower it) per (device, kernel), thread-safe (one host thread
+// per GPU drives its own chain).
+template <class F>
+void set_max_smem(F* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cur;
+    int dev = 0;
+    BM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& c = cur[std::make_pair(dev, reinterpret_cast<const void*>(fn))];
+    if (bytes > c) {
+        BM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        c = bytes;
+    }
+}
+
 int assign_threads(int k) {
     const int kg = std::min<int>(dev::kAMaxCG, (int)ceil_div(std::max(k, 1), dev::kAK));
     return dev::kAPG * kg;
@@ -791,12 +811,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             auto go = [&](auto ns_tag) {
                 constexpr int NS = decltype(ns_tag)::value;
                 constexpr size_t shm = dev::tma_smem_bytes<T, NS>();
-                static bool attr_set = false;  // per template instance
-                if (!attr_set) {
-                    BM_CUDA(cudaFuncSetAttribute(dev::k_assign_tma<T, NS>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-                    attr_set = true;
-                }
+                set_max_smem(dev::k_assign_tma<T, NS>, shm);
                 const CUtensorMap tmx = points_map<T>(P);
                 // a speculative begin loops over its blocks with at most spec_ctas() CTAs
                 // (BM_SPEC_CTAS), leaving SM slots to the engine stream's rounds
@@ -821,12 +836,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             else go(std::integral_constant<int, 2>{});
         } else if (screen) {
             constexpr size_t shm = dev::screen_smem_bytes();
-            static bool attr_set = false;  // per template instance
-            if (!attr_set) {
-                BM_CUDA(cudaFuncSetAttribute(dev::k_assign_screen<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-                attr_set = true;
-            }
+            set_max_smem(dev::k_assign_screen<T>, shm);
             dev::k_assign_screen<T><<<grid, dev::kSThreads, shm, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
                 &w.gs.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out,
@@ -899,8 +909,7 @@ void launch_update(cudaStream_t st, const Points& P, Workspace& w, const int* pa
                       bad_label ? bad_label : &w.status.p->bad_label, stop};
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
-        if (shm > 48 * 1024)
-            BM_CUDA(cudaFuncSetAttribute(dev::k_update<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+        if (shm > 48 * 1024) set_max_smem(dev::k_update<T>, shm);
         launch_pdl(dev::k_update<T>, grid, dev::kUThreads, shm, st, static_cast<const T*>(P.X), P.rows, n, P.ld,
                    labels ? labels : w.labels.p, w.R, parity, k, dslab, u);
     });
@@ -1414,11 +1423,7 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
         dispatch(P.dtype, [&](auto tag) {
             using T = decltype(tag);
             constexpr size_t shm = dev::final_smem_bytes<T>();
-            static bool attr_set = false;  // per template instance
-            if (!attr_set) {
-                BM_CUDA(cudaFuncSetAttribute(dev::k_final<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-                attr_set = true;
-            }
+            set_max_smem(dev::k_final<T>, shm);
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
             const uint64_t blocks = ceil_div(P.rows, dev::kABP);
@@ -2471,6 +2476,134 @@ void kmeans(const bm_dataset* d, uint64_t k, const bm_init_config& init, uint64_
     out->chunks = 1;
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU Big-means in one process (paper mode 2):
+// chain g = big_means with seed + g and floor(N/G) (+1 for g < N mod G) of the
+// N chunks, on its own dataset handle (one per GPU); one host thread per
+// device (chains sharing a device run one after the other on that device's
+// thread); the lowest-index chain with the minimum f_opt wins; the final pass
+// is row-sharded over the distinct devices on 1024-row tiles and the tile
+// partials are folded in row order (bit-identical to block_sum, core.cpp:165-175).
+// ---------------------------------------------------------------------------
+uint64_t chain_chunks(uint64_t N, int g, int G) { return N / G + ((uint64_t)g < N % G ? 1 : 0); }
+
+void big_means_multi(bm_dataset* const* data, int G, const bm_config& cfg, bm_outcome* out, bm_chunk_record* trace,
+                     uint64_t trace_cap, uint64_t* chain_chunk_counts, int* winner_out) {
+    if (G < 1) throw ConfigError("big_means_multi: at least one chain");
+    for (int g = 0; g < G; ++g) {
+        if (!data[g]) throw ConfigError("big_means_multi: null dataset handle");
+        if (data[g]->m != data[0]->m || data[g]->n != data[0]->n)
+            throw ConfigError("big_means_multi: every chain needs the same dataset");
+        validate(data[g], cfg);
+    }
+    if (cfg.has_max_chunks && cfg.max_chunks < (uint64_t)G)
+        throw ConfigError("big_means_multi: fewer chunks than chains");
+    const uint64_t k = cfg.k, n = data[0]->n, m = data[0]->m;
+    struct Chain {
+        std::vector<double> C;
+        std::vector<uint8_t> mask;
+        bm_outcome o{};
+        std::vector<bm_chunk_record> recs;
+    };
+    std::vector<Chain> ch(G);
+    std::vector<int> devs;
+    for (int g = 0; g < G; ++g)
+        if (std::find(devs.begin(), devs.end(), data[g]->device) == devs.end()) devs.push_back(data[g]->device);
+    std::vector<std::string> errs(devs.size());
+    std::vector<bm_status> codes(devs.size(), BM_OK);
+    auto run_threads = [&](auto&& body) {
+        std::vector<std::thread> th;
+        for (size_t di = 0; di < devs.size(); ++di)
+            th.emplace_back([&, di] {
+                codes[di] = guarded([&] { body(di, devs[di]); });
+                if (codes[di] != BM_OK) errs[di] = g_last_error;
+            });
+        for (auto& t : th) t.join();
+        for (size_t di = 0; di < devs.size(); ++di)
+            if (codes[di] != BM_OK) {
+                if (codes[di] == BM_CONFIG_ERROR) throw ConfigError(errs[di]);
+                if (codes[di] == BM_STATE_ERROR) throw StateError(errs[di]);
+                throw CudaError(errs[di]);
+            }
+    };
+    // 1. the chains
+    run_threads([&](size_t, int dev) {
+        for (int g = 0; g < G; ++g) {
+            if (data[g]->device != dev) continue;
+            bm_config c = cfg;
+            c.seed = cfg.seed + (uint64_t)g;
+            if (cfg.has_max_chunks) c.max_chunks = chain_chunks(cfg.max_chunks, g, G);
+            c.final_assignment = 0;
+            Chain& x = ch[g];
+            x.C.assign(k * n, 0.0);
+            x.mask.assign(k, 1);
+            x.o.centroids = x.C.data();
+            x.o.mask = x.mask.data();
+            x.o.labels = nullptr;
+            big_means(data[g], c, &x.o, nullptr, 0);
+            x.recs = g_last_trace;
+        }
+    });
+    // 2. select: the first chain with the minimum f_opt (strict <)
+    int w = 0;
+    double best = std::numeric_limits<double>::infinity();
+    for (int g = 0; g < G; ++g)
+        if (ch[g].o.objective < best) {
+            best = ch[g].o.objective;
+            w = g;
+        }
+    uint64_t evals = 0, iters = 0, chunks = 0, rec_i = 0;
+    double loop_wall = 0.0;
+    for (int g = 0; g < G; ++g) {
+        evals += ch[g].o.distance_evals;
+        iters += ch[g].o.iterations;
+        chunks += ch[g].o.chunks;
+        loop_wall = std::max(loop_wall, ch[g].o.cpu_init);
+        if (chain_chunk_counts) chain_chunk_counts[g] = ch[g].o.chunks;
+        for (const auto& r : ch[g].recs)
+            if (trace && rec_i < trace_cap) trace[rec_i++] = r;
+    }
+    std::copy(ch[w].C.begin(), ch[w].C.end(), out->centroids);
+    std::copy(ch[w].mask.begin(), ch[w].mask.end(), out->mask);
+    out->cpu_init = loop_wall;
+    out->cpu_full = 0.0;
+    out->objective = best;
+    if (cfg.final_assignment) {
+        // 3. row-sharded final pass: device di assigns whole tiles [t0, t1)
+        const auto t_full = std::chrono::steady_clock::now();
+        const uint64_t T = tiles_of(m), D = devs.size();
+        std::vector<double> tiles(T);
+        std::vector<uint64_t> fe(D, 0);
+        run_threads([&](size_t di, int dev) {
+            const uint64_t t0 = di * (T / D) + std::min<uint64_t>(di, T % D);
+            const uint64_t t1 = t0 + T / D + (di < T % D ? 1 : 0);
+            const uint64_t r0 = std::min(m, t0 * kTile), r1 = std::min(m, t1 * kTile);
+            if (r1 <= r0) return;
+            const bm_dataset* d = nullptr;
+            for (int g = 0; g < G; ++g)
+                if (data[g]->device == dev) {
+                    d = data[g];
+                    break;
+                }
+            DeviceGuard dg(dev);
+            Workspace& fw = get_ws(d, 0, (int)k, 1, 0);
+            upload_centroids(stream_of(d), fw, ch[w].C.data(), ch[w].mask.data());
+            launch_compact(stream_of(d), fw, fw.C.p, fw.mask.p);
+            final_pass(stream_of(d), d, fw, r0, r1, out->labels ? out->labels + r0 : nullptr, tiles.data() + t0,
+                       &fe[di]);
+        });
+        double total = 0.0;  // block_sum outer fold over all tiles in row order (core.cpp:172)
+        for (double t : tiles) total += t;
+        out->objective = total;
+        for (uint64_t e : fe) evals += e;
+        out->cpu_full = seconds_since(t_full);
+    }
+    out->distance_evals = evals;
+    out->iterations = iters;
+    out->chunks = chunks;
+    if (winner_out) *winner_out = w;
+}
+
 }  // namespace bm
 
 extern "C" {
@@ -2998,6 +3131,12 @@ bm_status bm_kmeans_pp(const bm_dataset* dc, uint64_t k, int32_t candidates, uin
 bm_status bm_big_means(bm_dataset* d, const bm_config* cfg, bm_outcome* out, bm_chunk_record* trace,
                        uint64_t trace_capacity) {
     return guarded([&] { big_means(d, *cfg, out, trace, trace_capacity); });
+}
+
+bm_status bm_big_means_multi(bm_dataset* const* data, int32_t chains, const bm_config* cfg, bm_outcome* out,
+                             bm_chunk_record* trace, uint64_t trace_capacity, uint64_t* chain_chunks,
+                             int32_t* winner) {
+    return guarded([&] { big_means_multi(data, chains, *cfg, out, trace, trace_capacity, chain_chunks, winner); });
 }
 
 bm_status bm_last_trace(bm_chunk_record* out, uint64_t capacity, uint64_t* count) {

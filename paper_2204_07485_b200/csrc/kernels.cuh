@@ -1547,11 +1547,12 @@ struct TmaSmem {
 // whose label changed, and k_centroids turns them into the next centroids
 // (sum * (1.0/count), core.cpp:237-239) — no ordered update pass at all.
 // ---------------------------------------------------------------------------
-constexpr int kSumCopies = 8;
+constexpr int kSumCopies = 8;  // CTA b adds into copy b % 8 (spreads same-address atomics)
 #ifndef BM_SUM_GROUP
 #define BM_SUM_GROUP 8
 #endif
-constexpr int kSumGroup = BM_SUM_GROUP;  // a begin's CTAs whose partial sums one of them merges  // CTA b adds into copy b % 8 (spreads same-address atomics)
+constexpr int kSumGroup = BM_SUM_GROUP;  // a begin's CTAs whose partial sums one of them merges
+static_assert(kSumGroup >= 1 && kSumGroup <= 32, "BM_SUM_GROUP must be in [1, 32]");
 
 __device__ __forceinline__ long long sum_units(double x, double scale) {
     return __double2ll_rn(__dmul_rn(x, scale));  // exact: x * 2^-e is an integer below 2^53
@@ -1710,7 +1711,7 @@ __device__ __noinline__ void label_sums(TmaSmem<T, NS>& S, const LloydCtl& ctl, 
         __threadfence();  // this CTA's atomics before its arrival
         return;
     }
-    // A begin: the partials of 8 CTAs are merged by the last of them (8x fewer
+    // A begin: the partials of kSumGroup CTAs are merged by the last of them (fewer
     // global atomics, which are the bottleneck at this volume).
     if (tid < kfull) slot[static_cast<uint64_t>(kSMaxK) * n + tid] = pc[tid + 1] - pc[tid];
     __threadfence();

@@ -1,9 +1,10 @@
 """Multi-GPU Big-means: one independent subproblem chain per rank.
 
 This is the paper's parallel mode 2 (the reference implements
-only mode 1).  Rank g runs big_means with seed + g on the
-replicated dataset (weak scaling: each chain runs cfg.max_chunks chunks), then
-the ranks exchange exactly three small messages:
+only mode 1).  The N = cfg.max_chunks subproblems are sharded over
+the G ranks (strong scaling): rank g runs big_means with seed + g
+and floor(N/G) (+1 for g < N mod G) chunks on the replicated dataset, then the
+ranks exchange exactly three small messages:
 
 1. all_gather of (f_opt_g): the winner is the first rank with the minimum
    (strict < scanning ranks in order -> ties go to the lowest rank);
@@ -62,6 +63,11 @@ def shard_rows(m: int, rank: int, world: int) -> tuple[int, int]:
     return min(m, t0 * TILE), min(m, t1 * TILE)
 
 
+def chain_chunks(total: int, rank: int, world: int) -> int:
+    """Chunks of chain `rank`: floor(N/G), plus one for the first N mod G chains."""
+    return total // world + (1 if rank < total % world else 0)
+
+
 def select_winner(f_opts) -> int:
     best, w = float("inf"), 0
     for g, f in enumerate(f_opts):
@@ -78,13 +84,18 @@ def fold_tiles(parts) -> float:
     return total
 
 
-def big_means_distributed(m: int, k: int, n: int, chain: Callable[[int], ChainResult],
+def big_means_distributed(m: int, k: int, n: int, chain: Callable[[int, int], ChainResult],
                           rows: Callable[[np.ndarray, np.ndarray, int, int], tuple],
-                          seed: int, device: torch.device | str = "cpu") -> DistributedResult:
-    """chain(seed_g) runs this rank's chain (final_assignment off);
+                          seed: int, total_chunks: int,
+                          device: torch.device | str = "cpu") -> DistributedResult:
+    """chain(seed_g, chunks_g) runs this rank's chain (final_assignment off);
     rows(C, mask, r0, r1) -> (tile partials f64[ceil((r1-r0)/1024)], evals)."""
     rank, world = dist.get_rank(), dist.get_world_size()
-    local = chain(seed + rank)
+    cg = chain_chunks(total_chunks, rank, world)
+    if cg > 0:
+        local = chain(seed + rank, cg)
+    else:  # more ranks than chunks: this rank has no chain
+        local = ChainResult(np.zeros((k, n)), np.ones(k, np.uint8), float("inf"), 0, 0, 0)
     # 1. select
     f = torch.tensor([local.f_opt], dtype=torch.float64, device=device)
     fs = [torch.empty_like(f) for _ in range(world)]
@@ -129,8 +140,9 @@ def gpu_chain(data, cfg):
     """chain callable over the C-ABI: big_means on this rank's device."""
     from . import api
 
-    def run(seed_g: int) -> ChainResult:
-        out, trace = api.big_means(data, replace(cfg, seed=seed_g, final_assignment=False))
+    def run(seed_g: int, chunks_g: int) -> ChainResult:
+        out, trace = api.big_means(data, replace(cfg, seed=seed_g, max_chunks=chunks_g,
+                                                  final_assignment=False))
         return ChainResult(out.centroids.values, out.centroids.mask, out.objective,
                            out.counter.distance_evals, out.counter.iterations, trace.chunks())
     return run

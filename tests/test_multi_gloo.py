@@ -22,7 +22,7 @@ def _free_port():
 
 def _data():
     X = np.random.default_rng(77).normal(size=(5000, 4)) * 4.0
-    return X, dict(k=6, s=700, chunks=5, seed=11)
+    return X, dict(k=6, s=700, chunks=7, seed=11)  # 7 chunks over 2 ranks: 4 + 3
 
 
 def _worker(rank, world, port, q):
@@ -33,8 +33,8 @@ def _worker(rank, world, port, q):
     P = oport()
     X, c = _data()
 
-    def chain(seed_g):
-        o = P.big_means(X, c["k"], c["s"], c["chunks"], seed=seed_g, final_assignment=False)
+    def chain(seed_g, chunks_g):
+        o = P.big_means(X, c["k"], c["s"], chunks_g, seed=seed_g, final_assignment=False)
         return multi.ChainResult(o.centroids, o.mask, o.objective, o.evals, o.iterations, o.chunks)
 
     def rows(C, mask, r0, r1):
@@ -42,7 +42,7 @@ def _worker(rank, world, port, q):
         parts = [P.block_sum(d[a:a + 1024]) for a in range(0, r1 - r0, 1024)]
         return np.array(parts), ev
 
-    res = multi.big_means_distributed(X.shape[0], c["k"], X.shape[1], chain, rows, c["seed"])
+    res = multi.big_means_distributed(X.shape[0], c["k"], X.shape[1], chain, rows, c["seed"], c["chunks"])
     q.put((rank, res.objective, res.centroids.tobytes(), res.winner, res.evals, res.chunks))
     dist.destroy_process_group()
 
@@ -55,6 +55,14 @@ def test_shard_rows_cover_tiles():
             for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
                 assert a1 == b0
             assert all(a % 1024 == 0 for a, b in spans if b > a)
+
+
+def test_chain_chunks_partition():
+    for total in (1, 7, 200, 512):
+        for world in (1, 2, 3, 8):
+            parts = [multi.chain_chunks(total, g, world) for g in range(world)]
+            assert sum(parts) == total and max(parts) - min(parts) <= 1
+            assert parts == sorted(parts, reverse=True)
 
 
 def test_select_winner_ties_lowest_rank():
@@ -78,8 +86,8 @@ def test_two_rank_exchange_equals_serial_oracle():
         p.join(timeout=60)
         assert p.exitcode == 0
     # serial G-chain oracle
-    chains = [P.big_means(X, c["k"], c["s"], c["chunks"], seed=c["seed"] + g, final_assignment=False)
-              for g in range(world)]
+    chains = [P.big_means(X, c["k"], c["s"], multi.chain_chunks(c["chunks"], g, world),
+                          seed=c["seed"] + g, final_assignment=False) for g in range(world)]
     w = multi.select_winner([o.objective for o in chains])
     lab, d, ev = P.assign_nearest(X, chains[w].centroids, chains[w].mask)
     expected = P.block_sum(d)
@@ -88,4 +96,4 @@ def test_two_rank_exchange_equals_serial_oracle():
         assert obj == expected
         assert cbytes == chains[w].centroids.tobytes()
         assert winner == w
-        assert evals == total_evals and chunks == world * c["chunks"]
+        assert evals == total_evals and chunks == c["chunks"]
