@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libbigmeans_b200.so")
+# BM_LIB_PATH: an alternative build of the same library (A/B diagnostics only)
+LIB_PATH = os.environ.get("BM_LIB_PATH") or os.path.join(HERE, "_lib", "libbigmeans_b200.so")
 
 u64 = C.c_uint64
 i32 = C.c_int32

@@ -105,6 +105,12 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -180,6 +186,25 @@ __device__ __forceinline__ double exact_dist(const T* __restrict__ x, const doub
     }
     for (; d < n; ++d) s = dist_step(s, to_f64(x[d]), c[d]);
     return s;
+}
+
+// Global -> shared copies with U loads in flight per thread (a plain
+// load-then-store loop would wait one L2 round trip per element).
+template <int U, class Load, class Store>
+__device__ __forceinline__ void batched_copy(int count, int tid, int NT, Load ld, Store st) {
+    for (int e0 = tid; e0 < count; e0 += U * NT) {
+        decltype(ld(0)) v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * NT;
+            if (e < count) v[u] = ld(e);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * NT;
+            if (e < count) st(e, v[u]);
+        }
+    }
 }
 
 // Left fold from 0.0 of `len` doubles in shared memory (16-byte aligned).
@@ -264,6 +289,9 @@ struct CCtl {
     unsigned long long evals, iterations;
     int stop, undecided, ka, state_error;
     unsigned gdirty;  // labels whose membership changed in some tile this round
+    double s_last, lo_last, hi_last;  // fast sum (and its interval) of the last assignment
+    double fo;                        // exact f_opt before the accept
+    int decision;                     // accept: 1 / 0, -1: the interval cannot decide (exact fold)
 };
 
 // Debug phase stamps (ChunkArgs::dbg, BM_CHUNK_DBG=1): CTA 0's globaltimer at
@@ -301,9 +329,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     const float finf = __int_as_float(0x7F800000);
     const double dinf = __longlong_as_double(0x7FF0000000000000LL);
     __shared__ unsigned long long s_chunk;
-    if (cta == 0 && tid == 0) {
-        s_chunk = __ldcg(a.chunk_ctr);
-        if (a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = gtimer();
+    if (tid == 0) {
+        s_chunk = __ldcg(a.chunk_ctr);  // every CTA: stable until CTA 0's accept (after a grid barrier)
+        if (cta == 0 && a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = gtimer();
     }
     CDBG(7, 13);
 
@@ -326,30 +354,63 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     // load); PPT == 1: xp[h] = (x[2h], x[2h+1]) (dimension pairs).  Norms as
     // (p0, p1) pairs (PPT == 1: both halves p0's).
     constexpr int NX = PPT == 2 ? ND : ND / 2;
-    constexpr int JU = 8;  // centroids per screen pass (independent FMA chains)
-    float2 xp[NX];
-    float2 nxl2, nxh2, nxr2;
-    int mylab[PPT];
-    {
-        float lo[2] = {0.f, 0.f}, hi[2] = {0.f, 0.f};
+    // this thread's rows, fp32, into registers (16-byte loads of the shared
+    // rows; dimensions >= n read as 0).  Reloaded for every screen so that the
+    // registers are free in the other phases.
+    auto load_xp = [&](float2 (&xp)[NX]) {
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const int p = tid + i * NT;
+            const T* row = xs + static_cast<size_t>(p < np ? p : 0) * xld;
 #pragma unroll
-            for (int d = 0; d < ND; ++d) {
-                const float v = (p < np && d < n) ? static_cast<float>(xs[static_cast<size_t>(p) * xld + d]) : 0.f;
-                if constexpr (PPT == 2) {
-                    if (i == 0) xp[d].x = v;
-                    else xp[d].y = v;
+            for (int q = 0; q < ND / 4; ++q) {
+                float v[4];
+                if constexpr (sizeof(T) == 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(row + 4 * q);
+                    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
                 } else {
-                    if (d & 1) xp[d >> 1].y = v;
-                    else xp[d >> 1].x = v;
+                    const double2 t0 = *reinterpret_cast<const double2*>(row + 4 * q);
+                    const double2 t1 = *reinterpret_cast<const double2*>(row + 4 * q + 2);
+                    v[0] = static_cast<float>(t0.x); v[1] = static_cast<float>(t0.y);
+                    v[2] = static_cast<float>(t1.x); v[3] = static_cast<float>(t1.y);
                 }
-                lo[i] = __fmaf_rd(v, v, lo[i]);
-                hi[i] = __fmaf_ru(v, v, hi[i]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int d = 4 * q + u;
+                    const float x = (p < np && d < n) ? v[u] : 0.f;
+                    if constexpr (PPT == 2) {
+                        if (i == 0) xp[d].x = x;
+                        else xp[d].y = x;
+                    } else {
+                        if (d & 1) xp[d >> 1].y = x;
+                        else xp[d >> 1].x = x;
+                    }
+                }
             }
-            mylab[i] = -1;
         }
+    };
+    float2 nxl2, nxh2, nxr2;
+    int mylab[PPT];
+    {
+        float2 xp[NX];
+        load_xp(xp);
+        float lo[2] = {0.f, 0.f}, hi[2] = {0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < NX; ++h) {
+            if constexpr (PPT == 2) {
+                lo[0] = __fmaf_rd(xp[h].x, xp[h].x, lo[0]);
+                hi[0] = __fmaf_ru(xp[h].x, xp[h].x, hi[0]);
+                lo[1] = __fmaf_rd(xp[h].y, xp[h].y, lo[1]);
+                hi[1] = __fmaf_ru(xp[h].y, xp[h].y, hi[1]);
+            } else {
+                lo[0] = __fmaf_rd(xp[h].x, xp[h].x, lo[0]);
+                hi[0] = __fmaf_ru(xp[h].x, xp[h].x, hi[0]);
+                lo[0] = __fmaf_rd(xp[h].y, xp[h].y, lo[0]);
+                hi[0] = __fmaf_ru(xp[h].y, xp[h].y, hi[0]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) mylab[i] = -1;
         if (PPT == 1) {
             lo[1] = lo[0];
             hi[1] = hi[0];
@@ -384,12 +445,17 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         // compacted fp64 / fp32 copies (all threads: one L2 round trip), then
         // the fp32 norms, a warp per row (warp sums rounded down / up: any
         // order bounds the exact value)
-        for (int e = tid; e < KA * n; e += NT) {
-            const int rk = e / n, d = e - rk * n;
-            const double v = __ldcg(a.C + static_cast<size_t>(act[rk]) * n + d);
-            cd[rk * cdld + d] = v;
-            cf[rk * ND + d] = __double2float_rn(v);
-        }
+        batched_copy<4>(
+            KA * n, tid, NT,
+            [&](int e) {
+                const int rk = e / n;
+                return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+            },
+            [&](int e, double v) {
+                const int rk = e / n, d = e - rk * n;
+                cd[rk * cdld + d] = v;
+                cf[rk * ND + d] = __double2float_rn(v);
+            });
         __syncthreads();
         for (int rk = warp; rk < KA; rk += NW) {
             float lo = 0.f, hi = 0.f;
@@ -422,6 +488,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         // work); per point the running minimum of the upper bounds and the
         // running candidate mask {j : L_j <= running min at j} (a superset of
         // the final candidates, filtered against the final minimum below)
+        float2 xp[NX];
+        load_xp(xp);
         float2 minU2 = make_float2(finf, finf);
         unsigned rm[2] = {0u, 0u};
         auto group = [&](auto jg_tag, int j0) {
@@ -663,9 +731,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
 #pragma unroll
                 for (int t = 0; t < DPL; ++t) {
                     const int d = gl + LG * t;
-                    if (d < n) a.part[(static_cast<size_t>(j) * n + d) * G + cta] = acc[t];
+                    if (d < n) a.part[static_cast<size_t>(cta) * k * n + static_cast<size_t>(j) * n + d] = acc[t];
                 }
-                if (gl == 0) a.pcnt[static_cast<size_t>(j) * G + cta] = static_cast<unsigned>(e - b);
+                if (gl == 0) a.pcnt[static_cast<size_t>(cta) * k + j] = static_cast<unsigned>(e - b);
             }
         }
         CDBG(rr, 4);
@@ -679,13 +747,28 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         double* stage = reinterpret_cast<double*>(sm + L.u);
         unsigned* cstage = reinterpret_cast<unsigned*>(sm + L.u + al16(static_cast<size_t>(ppc) * G * 8));
         const int mj0 = q0 / n;
-        if (q0 < q1) {
-            const int j1 = (q1 - 1) / n;
-            const size_t cnt_pairs = static_cast<size_t>(q1 - q0) * G;
-            const double* src = a.part + static_cast<size_t>(q0) * G;
-            for (size_t e = tid; e < cnt_pairs; e += NT) stage[e] = __ldcg(src + e);
-            for (size_t e = tid; e < static_cast<size_t>(j1 - mj0 + 1) * G; e += NT)
-                cstage[e] = __ldcg(a.pcnt + static_cast<size_t>(mj0) * G + e);
+        if (q0 < q1) {  // part[g][q] -> stage[q - q0][g], pcnt[g][j] -> cstage[j - mj0][g]
+            const int nq = q1 - q0, nj = (q1 - 1) / n - mj0 + 1;
+            batched_copy<4>(
+                nq * static_cast<int>(G), tid, NT,
+                [&](int e) {
+                    const int g = e / nq;
+                    return __ldcg(a.part + static_cast<size_t>(g) * kn + q0 + (e - g * nq));
+                },
+                [&](int e, double v) {
+                    const int g = e / nq;
+                    stage[static_cast<size_t>(e - g * nq) * G + g] = v;
+                });
+            batched_copy<2>(
+                nj * static_cast<int>(G), tid, NT,
+                [&](int e) {
+                    const int g = e / nj;
+                    return __ldcg(a.pcnt + static_cast<size_t>(g) * k + mj0 + (e - g * nj));
+                },
+                [&](int e, unsigned v) {
+                    const int g = e / nj;
+                    cstage[static_cast<size_t>(e - g * nj) * G + g] = v;
+                });
         }
 
         // ---- Lloyd control (local_search.cpp:26-51), every CTA identically ----
@@ -695,6 +778,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             ctl.gdirty = r == 0 ? 0xFFFFFFFFu : static_cast<unsigned>(chg_all);
             double lo, hi;
             sum_interval(s, a.rows, G, &lo, &hi);
+            ctl.s_last = s;
+            ctl.lo_last = lo;
+            ctl.hi_last = hi;
             ctl.evals += a.rows * static_cast<unsigned long long>(KA);
             ctl.undecided = 0;
             if (r == 0) {  // :26-28
@@ -807,10 +893,28 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         CDBG(rr, 8);
     }
 
-    // ---- after the stop: exact objective (block_sum), accept, record ----
+    // ---- after the stop: accept (big_means.cpp:89-94), record ----
+    // f_opt is exact once every earlier chunk's deferred objective is folded
+    // (their k_chunk_fix ran on the side stream during this chunk); the
+    // decision fc < f_opt is taken on the certified interval of the final fast
+    // sum, identically in every CTA; only an undecidable interval folds the
+    // exact block_sum here.  Otherwise k_chunk_fix folds it after this kernel.
     CDBG(7, 9);
     const int fslot = static_cast<int>(ctl.iterations & 1);
-    if (!ctl.state_error) {
+    if (tid == 0) {
+        if (a.fix_seq)
+            while (ld_acquire64(a.fix_seq) < s_chunk) {
+            }
+        const double fo = __ldcg(&a.gs->fopt_exact);
+        ctl.fo = fo;
+        if (ctl.state_error) ctl.decision = 0;
+        else if (!a.force_exact && ctl.hi_last < fo) ctl.decision = 1;
+        else if (!a.force_exact && !(ctl.lo_last < fo)) ctl.decision = 0;
+        else ctl.decision = -1;
+    }
+    __syncthreads();
+    __shared__ double s_fc;
+    if (ctl.decision < 0 || !a.fix_seq) {  // grid-uniform: the exact objective now
         // block_sum inner folds (core.cpp:167-173) of the final distances, one
         // thread per 1024-row tile from shared memory: ordered mode folds its
         // own tile (dist[]); exact-sum mode stages tile `cta` from global first
@@ -821,42 +925,59 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             const uint64_t tb = static_cast<uint64_t>(cta) * kTile;
             const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), a.rows - tb));
             const double* src = a.dists + static_cast<size_t>(fslot) * a.rows + tb;
-            for (int i = tid; i < len; i += NT) stage[i] = __ldcg(src + i);
+            batched_copy<8>(len, tid, NT, [&](int i) { return __ldcg(src + i); },
+                            [&](int i, double v) { stage[i] = v; });
             __syncthreads();
             if (tid == 0) a.tiles[cta] = fold_smem(stage, len);
         }
+        CDBG(7, 10);
+        grid_sync(a.bar, G);
+        CDBG(7, 11);
+        if (cta != 0) return;
+        double* tstage = reinterpret_cast<double*>(sm + L.u);
+        batched_copy<4>(static_cast<int>(ntiles), tid, NT, [&](int t) { return __ldcg(a.tiles + t); },
+                        [&](int t, double v) { tstage[t] = v; });
+        __syncthreads();
+        if (tid == 0) {
+            const double fc = fold_smem(tstage, static_cast<int>(ntiles));  // block_sum outer fold
+            s_fc = fc;
+            ctl.decision = !ctl.state_error && fc < ctl.fo ? 1 : 0;  // :89 strict
+        }
+        __syncthreads();
+    } else {
+        if (cta != 0) return;
+        if (tid == 0) s_fc = __longlong_as_double(0x7FF8000000000000LL);  // folded by k_chunk_fix
     }
-    CDBG(7, 10);
-    grid_sync(a.bar, G);
-    CDBG(7, 11);
-    if (cta != 0) return;
     __shared__ int s_acc;
     __shared__ unsigned char s_mk[kCKMax];
-    __shared__ double s_fc;
-    {  // the tile partials -> shared memory (coalesced), folded in tile order by thread 0
-        double* tstage = reinterpret_cast<double*>(sm + L.u);
-        for (uint64_t t = tid; t < ntiles; t += NT) tstage[t] = __ldcg(a.tiles + t);
-        __syncthreads();
-    }
     if (tid == 0) {
-        const double fo = __ldcg(&a.gs->fopt_exact);
-        const double fc = fold_smem(reinterpret_cast<const double*>(sm + L.u), static_cast<int>(ntiles));
-        const int accepted = !ctl.state_error && fc < fo;  // :89 strict
+        const int accepted = ctl.decision;
+        const bool exact = !(s_fc != s_fc);  // s_fc is not NaN
         s_acc = accepted;
-        s_fc = fc;
-        const unsigned long long chunk = __ldcg(a.chunk_ctr);
+        const unsigned long long chunk = s_chunk;
         Record* rec = a.rec_base + chunk;
         rec->chunk_index = chunk;
-        rec->candidate_objective = fc;
-        rec->incumbent_objective = accepted ? fc : fo;
         rec->accepted = static_cast<unsigned long long>(accepted);
         rec->degenerate_repaired = static_cast<unsigned long long>(__ldcg(&a.gs->inc_degenerate));
-        if (accepted) {
-            *a.f_opt = fc;
-            a.gs->fopt_exact = fc;
+        if (exact) {
+            rec->candidate_objective = s_fc;
+            rec->incumbent_objective = accepted ? s_fc : ctl.fo;
+            if (accepted) {
+                *a.f_opt = s_fc;
+                a.gs->fopt_exact = s_fc;
+            }
+        }
+        if (a.job) {
+            FixJob* jb = a.job;
+            jb->chunk = chunk;
+            jb->fo = ctl.fo;
+            jb->slot = fslot;
+            jb->accepted = accepted;
+            jb->have_exact = exact ? 1 : 0;
+            jb->valid = 1;
         }
         *a.chunk_ctr = chunk + 1;
-        a.rsum[0] = 0.0;  // every CTA read the round slots before the last barrier
+        a.rsum[0] = 0.0;  // every CTA read the round slots before its last barrier
         a.rsum[1] = 0.0;
         a.rchg[0] = 0;
         a.rchg[1] = 0;
@@ -910,6 +1031,62 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         CDBG(7, 12);
     }
     (void)s_any;
+}
+
+// The deferred exact objective (block_sum core.cpp:165-175) of the chunk the
+// preceding k_chunk accepted or rejected: CTA t folds tile t of its final
+// distances in index order; the last CTA folds the tile partials in tile
+// order and completes the record (big_means.cpp:94) and, for an accepted
+// chunk, f_opt (:89-93); then publishes fix_seq = chunk + 1.
+__global__ void __launch_bounds__(256) k_chunk_fix(const __grid_constant__ FixArgs f) {
+    __shared__ __align__(16) double stage[kTile];
+    __shared__ int last;
+    FixJob jb;  // written by the previous kernel on the other stream: read through L2
+    jb.valid = __ldcg(&f.job->valid);
+    if (!jb.valid) return;
+    jb.chunk = __ldcg(&f.job->chunk);
+    jb.fo = __ldcg(&f.job->fo);
+    jb.slot = __ldcg(&f.job->slot);
+    jb.accepted = __ldcg(&f.job->accepted);
+    jb.have_exact = __ldcg(&f.job->have_exact);  // its chunk kernel found go == 0 (relaunched after the repair)
+    const int tid = threadIdx.x;
+    const uint64_t t = blockIdx.x, ntiles = gridDim.x;
+    if (!jb.have_exact) {
+        const uint64_t tb = t * kTile;
+        const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), f.rows - tb));
+        const double* src = f.dists + static_cast<size_t>(jb.slot) * f.rows + tb;
+        batched_copy<4>(len, tid, blockDim.x, [&](int i) { return __ldcg(src + i); },
+                        [&](int i, double v) { stage[i] = v; });
+        __syncthreads();
+        if (tid == 0) f.tiles[t] = fold_smem(stage, len);
+    }
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(f.counter, 1u) == ntiles - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (!jb.have_exact) {
+        batched_copy<4>(static_cast<int>(ntiles), tid, blockDim.x, [&](int i) { return __ldcg(f.tiles + i); },
+                        [&](int i, double v) { stage[i] = v; });
+        __syncthreads();
+    }
+    if (tid == 0) {
+        *f.counter = 0u;
+        if (!jb.have_exact) {
+            const double fc = fold_smem(stage, static_cast<int>(ntiles));
+            Record* rec = f.rec_base + jb.chunk;
+            rec->candidate_objective = fc;
+            rec->incumbent_objective = jb.accepted ? fc : jb.fo;
+            if (jb.accepted) {
+                *f.f_opt = fc;
+                f.gs->fopt_exact = fc;
+            }
+        }
+        f.job->valid = 0;
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(f.fix_seq), "l"(jb.chunk + 1) : "memory");
+    }
 }
 
 }  // namespace dev
@@ -1012,6 +1189,9 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
     if (grid > static_cast<unsigned>(sms)) return p;  // one CTA per SM, all co-resident
     const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid);
     if (L.total + 2048 > static_cast<size_t>(smem_optin)) return p;
+    // the previous chunk's k_chunk_fix must find room next to this kernel's
+    // CTAs (the accept waits for it): a free SM, or room on every SM
+    if (grid >= static_cast<unsigned>(sms) && (threads > 384 || L.total > 216 * 1024)) return p;
     p.ok = true;
     p.B = B;
     p.threads = threads;
@@ -1022,6 +1202,12 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
     p.grid = grid;
     p.smem = L.total;
     return p;
+}
+
+void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f) {
+    const unsigned tiles = static_cast<unsigned>(tiles_of(f.rows));
+    dev::k_chunk_fix<<<tiles, 256, 0, st>>>(f);
+    BM_CUDA(cudaGetLastError());
 }
 
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a0) {

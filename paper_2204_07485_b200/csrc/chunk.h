@@ -16,6 +16,18 @@
 namespace bm {
 namespace dev {
 
+// The deferred exact objective of one chunk (k_chunk -> k_chunk_fix, per
+// chunk buffer): block_sum of its final distances (core.cpp:165-175) is folded
+// by a small kernel on a side stream while the next chunk runs.
+struct FixJob {
+    unsigned long long chunk;
+    double fo;        // exact f_opt before this chunk's accept
+    int slot;         // distance slot of the final assignment
+    int accepted;
+    int have_exact;   // the accept needed the exact objective: record / f_opt already final
+    int valid;
+};
+
 // Everything one chunk launch reads and writes (pointers into the Workspace).
 struct ChunkArgs {
     const void* X;            // the gathered chunk: rows x ld, storage T
@@ -28,8 +40,8 @@ struct ChunkArgs {
     int ordered;              // 1: real-valued data, CTA = 1024-tile, tile-order merge; 0: exact sums
     double* C;                // working centroids k x n (the start; then every update)
     uint8_t* mask;            // their degenerate mask
-    double* part;             // update partials [k*n][G] (CTA g's fold of label j, dim d)
-    unsigned* pcnt;           // member counts [k][G]
+    double* part;             // update partials [G][k*n] (CTA g's fold of label j, dim d)
+    unsigned* pcnt;           // member counts [G][k]
     double* dists;            // [2][rows]: the distances of the last two assignments
     double* tiles;            // [2][ntiles]: exact 1024-tile partials (tolerance fallback, accept)
     unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
@@ -51,6 +63,21 @@ struct ChunkArgs {
     unsigned long long* timing;  // optional [2 * timing_cap]: per chunk, globaltimer at CTA 0's start and the accept's end
     unsigned long long timing_cap;
     unsigned long long* dbg;  // optional [4][8][16] phase stamps (BM_CHUNK_DBG)
+    FixJob* job;              // this chunk buffer's deferred exact objective
+    unsigned long long* fix_seq;  // chunks whose exact objective is final (k_chunk_fix)
+};
+
+// k_chunk_fix: grid = tiles of the chunk, one CTA per 1024-row tile.
+struct FixArgs {
+    FixJob* job;
+    const double* dists;      // the chunk buffer's [2][rows] distances
+    uint64_t rows;
+    double* tiles;            // [ntiles]
+    unsigned* counter;
+    Record* rec_base;
+    double* f_opt;
+    GState* gs;
+    unsigned long long* fix_seq;
 };
 
 }  // namespace dev
@@ -67,6 +94,8 @@ struct ChunkPlan {
 ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums);
 // Enqueue one chunk (cooperative launch, capturable into a graph).
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a);
+// Enqueue the deferred exact objective of the chunk just launched (side stream).
+void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f);
 // The certified-screen constants of the chunk kernel's dot-product order.
 dev::ScreenConsts chunk_screen_consts(int n);
 

@@ -194,7 +194,24 @@ struct Workspace {
     DevBuf<unsigned> cpcnt, cbar;
     DevBuf<int> crchg;
     DevBuf<unsigned long long> ctiming;
+    DevBuf<dev::FixJob> cjob;              // [kStateBufs] deferred exact objectives
+    DevBuf<unsigned long long> cfix_seq;   // chunks whose exact objective is final
+    DevBuf<double> cfix_tiles;
+    DevBuf<unsigned> cfix_ctr;
+    cudaStream_t fix_stream = nullptr;
+    cudaEvent_t ev_chunk[dev::kStateBufs] = {};
     void ensure_chunk(const ChunkPlan& p) {
+        if (!cjob.n) {
+            cjob.alloc(dev::kStateBufs);
+            BM_CUDA(cudaMemset(cjob.p, 0, dev::kStateBufs * sizeof(dev::FixJob)));
+            cfix_seq.alloc(1);
+            BM_CUDA(cudaMemset(cfix_seq.p, 0, sizeof(unsigned long long)));
+            cfix_ctr.alloc(1);
+            BM_CUDA(cudaMemset(cfix_ctr.p, 0, sizeof(unsigned)));
+            BM_CUDA(cudaStreamCreateWithFlags(&fix_stream, cudaStreamNonBlocking));
+            for (auto& e : ev_chunk) BM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        if (cfix_tiles.n < tiles) cfix_tiles.alloc(std::max<uint64_t>(tiles, 1));
         const uint64_t kn = (uint64_t)k * n;
         if (cpart.n < kn * p.grid) cpart.alloc(kn * p.grid);
         if (cpcnt.n < (uint64_t)k * p.grid) cpcnt.alloc((uint64_t)k * p.grid);
@@ -230,6 +247,9 @@ struct Workspace {
     }
     ~Workspace() {
         drop_graphs();
+        if (fix_stream) cudaStreamDestroy(fix_stream);
+        for (auto e : ev_chunk)
+            if (e) cudaEventDestroy(e);
         for (auto q : {cap1, cap2})
             if (q) cudaStreamDestroy(q);
         for (auto* v : {&ev_lloyd, &ev_prep, &ev_spec})
@@ -1746,6 +1766,9 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     if (persist) {
         w.ensure_chunk(cplan);
         if (w.ctiming.n < 2 * w.drec.n) w.ctiming.alloc(2 * w.drec.n);
+        // (every fix of the previous run finished: its fix stream was synchronized)
+        BM_CUDA(cudaMemsetAsync(w.cfix_seq.p, 0, sizeof(unsigned long long), st));
+        BM_CUDA(cudaMemsetAsync(w.cjob.p, 0, dev::kStateBufs * sizeof(dev::FixJob), st));
     }
     // exact-sum mode for the graph chunks (kernels.cuh §5b)
     w.sums_on = use_graphs && !persist && d->exact_sums && exact_sums_enabled() && screen_enabled(k) && tma_screen() &&
@@ -1878,8 +1901,27 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 a.timing = w.ctiming.p;
                 a.timing_cap = w.ctiming.n / 2;
                 a.dbg = chunk_dbg_buffer();
+                static const bool defer = !(std::getenv("BM_CHUNK_FIX") && std::string(std::getenv("BM_CHUNK_FIX")) == "0");
+                a.job = defer ? w.cjob.p + i : nullptr;
+                a.fix_seq = defer ? w.cfix_seq.p : nullptr;
                 launch_chunk(st, cplan, d->dtype, a);
-                count_launch();
+                // its exact objective, folded on the side stream during the next chunk
+                if (defer) {
+                BM_CUDA(cudaEventRecord(w.ev_chunk[i], st));
+                BM_CUDA(cudaStreamWaitEvent(w.fix_stream, w.ev_chunk[i], 0));
+                dev::FixArgs fa{};
+                fa.job = w.cjob.p + i;
+                fa.dists = a.dists;
+                fa.rows = s;
+                fa.tiles = w.cfix_tiles.p;
+                fa.counter = w.cfix_ctr.p;
+                fa.rec_base = w.drec.p;
+                fa.f_opt = w.fopt.p;
+                fa.gs = w.gs.p;
+                fa.fix_seq = w.cfix_seq.p;
+                launch_chunk_fix(w.fix_stream, fa);
+                }
+                count_launch(defer ? 2 : 1);
             } else {
                 BM_CUDA(cudaGraphLaunch(w.g_lloyd[i], st));
             }
@@ -1994,9 +2036,13 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             if (queued) --queued;
         }
         // the last chunk's record gets its exact objective
-        dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.gs.p, accept_args(w), w.dists.p, w.R,
-                                                                   w.fix_tiles.p, w.tiles_done.p);
-        BM_LAUNCH();
+        if (persist) {
+            BM_CUDA(cudaStreamSynchronize(w.fix_stream));
+        } else {
+            dev::k_fix_final<<<(unsigned)tiles_of(w.R), 256, 0, st>>>(w.gs.p, accept_args(w), w.dists.p, w.R,
+                                                                       w.fix_tiles.p, w.tiles_done.p);
+            BM_LAUNCH();
+        }
         BM_CUDA(cudaStreamSynchronize(st));
         BM_CUDA(cudaStreamSynchronize(pst));
         if (dc.sstream) BM_CUDA(cudaStreamSynchronize(dc.sstream));

@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_big_means.py tests/test_gpu_multi.py -x -q > gpurun_out/pt_bm.log 2>&1; echo "rc=$?" >> gpurun_out/pt_bm.log
+for c in c2 c3 c1; do
+  BM_CHUNK_DBG=1 timeout 300 python tools/chunk_prof.py $c 20 > gpurun_out/dbg_$c.log 2>&1
+done
+for c in c2 c3; do
+  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/bh_$c.json 2> gpurun_out/bh_$c.err
+done
