@@ -188,6 +188,72 @@ __device__ __forceinline__ double exact_dist(const T* __restrict__ x, const doub
     return s;
 }
 
+// ---- tcgen05 / TMEM / mbarrier helpers (tensor-core screen, fp32 rows) ----
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
+// 1024 B apart (SBO), LBO unused (encoded 1), version 1 (sm_100).
+__device__ __forceinline__ unsigned long long umma_desc_sw128(unsigned saddr) {
+    return static_cast<unsigned long long>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+// Instruction descriptor: D fp32, A / B tf32, both K-major, N = 32, M = 128.
+constexpr unsigned kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// Issued by a whole warp with warp-uniform operands; one elected lane issues
+// (operands stay in uniform registers: no per-MMA broadcast loop).
+__device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db, int accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate));
+}
+// (whole warp; the same elected lane as the MMAs: it tracks that lane's MMAs)
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ float tf32_rna(float x) {
+    unsigned r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+// 32 consecutive TMEM columns of this thread's lane (row) -> registers.
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
+    unsigned r[32];
+    // the load and its wait in ONE asm statement: the outputs must not be read
+    // (moved or spilled by the compiler) before tcgen05.wait::ld completes
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // Global -> shared copies with U loads in flight per thread (a plain
 // load-then-store loop would wait one L2 round trip per element).
 template <int U, class Load, class Store>
@@ -233,7 +299,7 @@ __device__ __forceinline__ double fold_smem(const double* v, int len) {
 
 // Shared-memory carve-up (host and device agree).
 struct CLayout {
-    size_t xs, u, cf, cd, nrm, act, lab, dist, red, total;
+    size_t xs, cb, u, cf, cd, nrm, act, lab, dist, red, total;
     int cdld;         // fp64 centroid row stride: even, an odd number of 16-byte units
 };
 
@@ -245,14 +311,29 @@ __host__ __device__ inline int chunk_cdld(int n) {
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, int nd, int n, unsigned G) {
+// Tensor-core layout of the fp32 rows (tc): UMMA K-major, 128-byte swizzle.
+// K-atoms of 32 dims; atom `ka` holds Mpad rows x 128 B (rows 8-grouped into
+// 1024 B core-matrix groups, 16-byte chunks XOR-swizzled by row & 7).
+__host__ __device__ inline int tc_mpad(int B) { return (B + 127) / 128 * 128; }
+__host__ __device__ inline int tc_katoms(int nd) { return (nd + 31) / 32; }
+
+__host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, int nd, int n, unsigned G,
+                                                bool tc = false) {
     CLayout L{};
     size_t o = 0;
     L.xs = o;
-    o = al16(o + (size_t)B * xld * es);
-    // region U (aliased): screen lower bounds Ls[k][B] | member lists for the
-    // update | staging of this CTA's merge pairs | staged distance / tile partials
-    const size_t ls = (size_t)k * B * 4;
+    if (tc) {  // rows (A operand) + centroid hi / lo parts (B operands), 1024-aligned
+        o += (size_t)tc_katoms(nd) * tc_mpad(B) * 128;
+        L.cb = o;
+        o += (size_t)2 * tc_katoms(nd) * kCKMax * 128;
+    } else {
+        o = al16(o + (size_t)B * xld * es);
+        L.cb = o;
+    }
+    // region U (aliased): screen lower bounds Ls[k][B] (FFMA screen) | member
+    // lists for the update | staging of this CTA's merge pairs | staged
+    // distance / tile partials
+    const size_t ls = tc ? 0 : (size_t)k * B * 4;
     const int nc = (B + 31) / 32;
     const size_t sort = al16((size_t)B * 2) + al16((size_t)B) + al16((size_t)nc * k * 4) + al16((size_t)(2 * k + 2) * 4);
     const size_t kn = (size_t)k * n, ppc = (kn + G - 1) / G;
@@ -265,7 +346,7 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
     L.u = o;
     o = al16(o + u);
     L.cf = o;
-    o = al16(o + (size_t)kCKMax * nd * 4);
+    if (!tc) o = al16(o + (size_t)kCKMax * nd * 4);
     L.cd = o;
     o = al16(o + (size_t)kCKMax * chunk_cdld(n) * 8);
     L.nrm = o;
@@ -278,7 +359,7 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
     o = al16(o + (size_t)B * 8);
     L.red = o;
     o = al16(o + 64 * 8);
-    L.total = o;
+    L.total = o + (tc ? 1024 : 0);  // tc: slack to align the base to 1024 B
     return L;
 }
 
@@ -304,15 +385,22 @@ struct CCtl {
 
 template <typename T, int ND, int PPT>
 __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ ChunkArgs a) {
-    extern __shared__ __align__(16) unsigned char sm[];
+    // fp32 rows: tensor-core screen (tcgen05.mma kind::tf32, TMEM accumulators);
+    // fp64 rows: packed-FFMA screen with the rows in registers
+    constexpr bool TC = sizeof(T) == 4;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
     if (!__ldcg(&a.gs->go)) return;  // a chunk queued behind one that needs a repair: nothing to do
     const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
     const unsigned G = gridDim.x, cta = blockIdx.x;
     const int B = a.B, n = a.n, k = a.k, xld = a.xld;
     const uint64_t p0 = static_cast<uint64_t>(cta) * B;
     const int np = static_cast<int>(min(static_cast<uint64_t>(B), a.rows - p0));
-    const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G);
+    const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G, TC);
+    // tc: operand tiles need a 1024-byte aligned base (128-byte swizzle atoms)
+    unsigned char* sm = TC ? sm_raw + ((1024u - (smem_addr(sm_raw) & 1023u)) & 1023u) : sm_raw;
     const int cdld = L.cdld;
+    const int MP = tc_mpad(B), NKA = tc_katoms(ND);
+    const size_t ASZ = static_cast<size_t>(MP) * 128;  // bytes of one K-atom of the rows
     T* xs = reinterpret_cast<T*>(sm + L.xs);
     float* Ls = reinterpret_cast<float*>(sm + L.u);
     float* cf = reinterpret_cast<float*>(sm + L.cf);
@@ -326,6 +414,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     double* red = reinterpret_cast<double*>(sm + L.red);
     __shared__ CCtl ctl;
     __shared__ int s_any;
+    __shared__ unsigned s_tmem;
+    __shared__ __align__(8) unsigned long long s_mbar;
     const float finf = __int_as_float(0x7F800000);
     const double dinf = __longlong_as_double(0x7FF0000000000000LL);
     __shared__ unsigned long long s_chunk;
@@ -334,43 +424,136 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         if (cta == 0 && a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = gtimer();
     }
     CDBG(7, 13);
+    // 16-byte chunk q of row p (fp32: dims 4q..4q+3; fp64: 2q, 2q+1):
+    // tc rows in the swizzled K-major layout, else row-major with stride xld
+    auto xchunk = [&](int p, int q) -> unsigned char* {
+        if constexpr (TC) {
+            const int ka = q >> 3, c = q & 7;  // (p >> 3) * 1024 + (p & 7) * 128 == p * 128
+            return sm + L.xs + static_cast<size_t>(ka) * ASZ + static_cast<size_t>(p) * 128 + ((c ^ (p & 7)) << 4);
+        } else {
+            return sm + L.xs + static_cast<size_t>(p) * xld * sizeof(T) + static_cast<size_t>(q) * 16;
+        }
+    };
+    constexpr int EPC = 16 / static_cast<int>(sizeof(T));  // elements per 16-byte chunk
+    auto xat = [&](int p, int d) -> T { return reinterpret_cast<const T*>(xchunk(p, d / EPC))[d % EPC]; };
+    // direct-form squared distance of row p to compacted fp64 row j (core.cpp:142-146)
+    auto exact = [&](int p, int j) -> double {
+        const double* c = cd + j * cdld;
+        double s = 0.0;
+        int d = 0;
+        if constexpr (TC) {
+            const unsigned char* rowb = sm + L.xs + static_cast<size_t>(p) * 128;
+            const int sw = p & 7;
+            for (; d + 4 <= n; d += 4) {
+                const int q = d >> 2;
+                const float4 xv = *reinterpret_cast<const float4*>(rowb + static_cast<size_t>(q >> 3) * ASZ +
+                                                                    (((q & 7) ^ sw) << 4));
+                const double2 c0 = *reinterpret_cast<const double2*>(c + d);
+                const double2 c1 = *reinterpret_cast<const double2*>(c + d + 2);
+                s = dist_step(s, static_cast<double>(xv.x), c0.x);
+                s = dist_step(s, static_cast<double>(xv.y), c0.y);
+                s = dist_step(s, static_cast<double>(xv.z), c1.x);
+                s = dist_step(s, static_cast<double>(xv.w), c1.y);
+            }
+            for (; d < n; ++d) s = dist_step(s, static_cast<double>(xat(p, d)), c[d]);
+            return s;
+        } else {
+            return exact_dist(xs + static_cast<size_t>(p) * xld, c, n);
+        }
+    };
 
     // ---- the chunk's rows -> shared memory (once for all rounds) ----
+    int xinexact = 0;  // tc: some row value is not exactly a tf32 (looser screen bound)
     {
         const int vpr = static_cast<int>((static_cast<size_t>(n) * sizeof(T) + 15) / 16);  // 16-byte vectors per row
         const unsigned char* src = static_cast<const unsigned char*>(a.X) + p0 * a.ld * sizeof(T);
         for (int v = tid; v < np * vpr; v += NT) {
             const int p = v / vpr, q = v - p * vpr;
-            cpa16(sm + L.xs + (static_cast<size_t>(p) * xld * sizeof(T)) + q * 16,
-                  src + static_cast<size_t>(p) * a.ld * sizeof(T) + q * 16);
+            cpa16(xchunk(p, q), src + static_cast<size_t>(p) * a.ld * sizeof(T) + q * 16);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
-        for (int e = tid; e < kCKMax * ND; e += NT) cf[e] = 0.f;  // padding rows / dims stay 0
+        if constexpr (!TC) {
+            for (int e = tid; e < kCKMax * ND; e += NT) cf[e] = 0.f;  // padding rows / dims stay 0
+        }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
+        if constexpr (TC) {
+            // zero the padding the MMA reads (dims n..ND-1, rows np..MP-1), check tf32 exactness,
+            // make the rows visible to the tensor core (async proxy); TMEM for the accumulators
+            // every 16-byte chunk of every K-atom row (the tensor core reads whole
+            // atoms): zeros past n and in rows np..MP-1; tf32 exactness of the
+            // data (a warp per row, a lane per chunk); the B operands start at 0
+            constexpr int QC = (ND + 31) / 32 * 8;
+            static_assert(QC <= 32, "a lane per 16-byte chunk");
+            const int vq = n >> 2;  // chunks holding 4 data values
+            const int zq = (n + 3) >> 2;  // first chunk holding no data value
+            // rows < np: the data chunks (exactness check, the partial chunk's
+            // tail zeroed) and chunks zq..QC-1; rows np..MP-1: every chunk
+            const int per_row = QC - vq;  // chunks of a row touched below (data chunks are read for the check)
+            for (int e = tid; e < np * QC; e += NT) {
+                const int p = e / QC, q = e - p * QC;
+                float4* x = reinterpret_cast<float4*>(xchunk(p, q));
+                if (q >= zq) {
+                    *x = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+                    float4 v = *x;
+                    if (q == vq) {  // the partial chunk: dims n..4q+3 -> 0
+                        if ((n & 3) < 2) v.y = 0.f;
+                        if ((n & 3) < 3) v.z = 0.f;
+                        v.w = 0.f;
+                        *x = v;
+                    }
+                    xinexact |= ((__float_as_uint(v.x) | __float_as_uint(v.y) | __float_as_uint(v.z) |
+                                  __float_as_uint(v.w)) & 0x1FFFu) != 0u;
+                }
+            }
+            (void)per_row;
+            for (int e = np * QC + tid; e < MP * QC; e += NT)
+                *reinterpret_cast<float4*>(xchunk(e / QC, e % QC)) = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int e = tid; e < NKA * kCKMax * 8 * 2; e += NT)
+                reinterpret_cast<float4*>(sm + L.cb)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+            xinexact = __syncthreads_or(xinexact);
+            fence_proxy_async_smem();
+            if (warp == 0) {
+                const unsigned cols = MP / 128 * 32 <= 32 ? 32 : MP / 128 * 32 <= 64 ? 64 : MP / 128 * 32 <= 128 ? 128 : 256;
+                asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
+                             "r"(cols)
+                             : "memory");
+                asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+            }
+            if (tid == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_mbar)) : "memory");
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+        }
     }
+    const ScreenConsts cst = TC && xinexact ? a.cst_loose : a.cst;
+    unsigned mma_phase = 0;
+    int prevKA = 0;  // tc: B operand rows holding values (the rest are 0)
     // this thread's points: p = tid + i*NT; fp32 rows in registers, norms (rd/ru)
     // PPT == 2: xp[d] = (x_p0[d], x_p1[d]) (point pairs share every centroid
     // load); PPT == 1: xp[h] = (x[2h], x[2h+1]) (dimension pairs).  Norms as
     // (p0, p1) pairs (PPT == 1: both halves p0's).
     constexpr int NX = PPT == 2 ? ND : ND / 2;
-    // this thread's rows, fp32, into registers (16-byte loads of the shared
-    // rows; dimensions >= n read as 0).  Reloaded for every screen so that the
-    // registers are free in the other phases.
+    // this thread's rows, fp32, into registers (dimensions >= n read as 0).
+    // Reloaded for every screen so that the registers are free in the other phases.
     auto load_xp = [&](float2 (&xp)[NX]) {
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const int p = tid + i * NT;
-            const T* row = xs + static_cast<size_t>(p < np ? p : 0) * xld;
+            const int pp = p < np ? p : 0;
 #pragma unroll
             for (int q = 0; q < ND / 4; ++q) {
                 float v[4];
                 if constexpr (sizeof(T) == 4) {
-                    const float4 t = *reinterpret_cast<const float4*>(row + 4 * q);
+                    const float4 t = *reinterpret_cast<const float4*>(xchunk(pp, q));
                     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
                 } else {
-                    const double2 t0 = *reinterpret_cast<const double2*>(row + 4 * q);
-                    const double2 t1 = *reinterpret_cast<const double2*>(row + 4 * q + 2);
+                    const double2 t0 = *reinterpret_cast<const double2*>(xchunk(pp, 2 * q));
+                    const double2 t1 = *reinterpret_cast<const double2*>(xchunk(pp, 2 * q + 1));
                     v[0] = static_cast<float>(t0.x); v[1] = static_cast<float>(t0.y);
                     v[2] = static_cast<float>(t1.x); v[3] = static_cast<float>(t1.y);
                 }
@@ -392,25 +575,35 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     float2 nxl2, nxh2, nxr2;
     int mylab[PPT];
     {
-        float2 xp[NX];
-        load_xp(xp);
         float lo[2] = {0.f, 0.f}, hi[2] = {0.f, 0.f};
 #pragma unroll
-        for (int h = 0; h < NX; ++h) {
-            if constexpr (PPT == 2) {
-                lo[0] = __fmaf_rd(xp[h].x, xp[h].x, lo[0]);
-                hi[0] = __fmaf_ru(xp[h].x, xp[h].x, hi[0]);
-                lo[1] = __fmaf_rd(xp[h].y, xp[h].y, lo[1]);
-                hi[1] = __fmaf_ru(xp[h].y, xp[h].y, hi[1]);
-            } else {
-                lo[0] = __fmaf_rd(xp[h].x, xp[h].x, lo[0]);
-                hi[0] = __fmaf_ru(xp[h].x, xp[h].x, hi[0]);
-                lo[0] = __fmaf_rd(xp[h].y, xp[h].y, lo[0]);
-                hi[0] = __fmaf_ru(xp[h].y, xp[h].y, hi[0]);
+        for (int i = 0; i < PPT; ++i) {
+            const int p = tid + i * NT;
+            if (p < np) {
+                if constexpr (TC) {  // 16-byte chunks of the swizzled row (padding dims are 0)
+                    const unsigned char* rowb = sm + L.xs + static_cast<size_t>(p) * 128;
+                    for (int q = 0; q < (n + 3) / 4; ++q) {
+                        const float4 v = *reinterpret_cast<const float4*>(rowb + static_cast<size_t>(q >> 3) * ASZ +
+                                                                         (((q & 7) ^ (p & 7)) << 4));
+                        lo[i] = __fmaf_rd(v.x, v.x, lo[i]);
+                        hi[i] = __fmaf_ru(v.x, v.x, hi[i]);
+                        lo[i] = __fmaf_rd(v.y, v.y, lo[i]);
+                        hi[i] = __fmaf_ru(v.y, v.y, hi[i]);
+                        lo[i] = __fmaf_rd(v.z, v.z, lo[i]);
+                        hi[i] = __fmaf_ru(v.z, v.z, hi[i]);
+                        lo[i] = __fmaf_rd(v.w, v.w, lo[i]);
+                        hi[i] = __fmaf_ru(v.w, v.w, hi[i]);
+                    }
+                } else {
+                    for (int d = 0; d < n; ++d) {
+                        const float x = static_cast<float>(xat(p, d));
+                        lo[i] = __fmaf_rd(x, x, lo[i]);
+                        hi[i] = __fmaf_ru(x, x, hi[i]);
+                    }
+                }
             }
+            mylab[i] = -1;
         }
-#pragma unroll
-        for (int i = 0; i < PPT; ++i) mylab[i] = -1;
         if (PPT == 1) {
             lo[1] = lo[0];
             hi[1] = hi[0];
@@ -445,22 +638,57 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         // compacted fp64 / fp32 copies (all threads: one L2 round trip), then
         // the fp32 norms, a warp per row (warp sums rounded down / up: any
         // order bounds the exact value)
-        batched_copy<4>(
-            KA * n, tid, NT,
-            [&](int e) {
-                const int rk = e / n;
-                return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
-            },
-            [&](int e, double v) {
+        if constexpr (TC) {
+            // the B operands: fl32(c) = hi + lo, hi = tf32(c) (round to nearest),
+            // lo = fl32(c) - hi (exact), rows = compacted active centroids; the
+            // rest stays 0 (zeroed at the start; rows that became inactive are
+            // cleared here)
+            unsigned char* cbhi = sm + L.cb;
+            unsigned char* cblo = cbhi + static_cast<size_t>(NKA) * kCKMax * 128;
+            auto boff = [&](int rk, int d) -> size_t {
+                return static_cast<size_t>(d >> 5) * (kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
+                       (d & 3) * 4;
+            };
+            batched_copy<4>(
+                KA * n, tid, NT,
+                [&](int e) {
+                    const int rk = e / n;
+                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+                },
+                [&](int e, double v) {
+                    const int rk = e / n, d = e - rk * n;
+                    cd[rk * cdld + d] = v;
+                    const float f = __double2float_rn(v), hi = tf32_rna(f);
+                    const size_t off = boff(rk, d);
+                    *reinterpret_cast<float*>(cbhi + off) = hi;
+                    *reinterpret_cast<float*>(cblo + off) = f - hi;
+                });
+            for (int e = KA * n + tid; e < prevKA * n; e += NT) {
                 const int rk = e / n, d = e - rk * n;
-                cd[rk * cdld + d] = v;
-                cf[rk * ND + d] = __double2float_rn(v);
-            });
+                const size_t off = boff(rk, d);
+                *reinterpret_cast<float*>(cbhi + off) = 0.f;
+                *reinterpret_cast<float*>(cblo + off) = 0.f;
+            }
+            prevKA = KA;
+            fence_proxy_async_smem();
+        } else {
+            batched_copy<4>(
+                KA * n, tid, NT,
+                [&](int e) {
+                    const int rk = e / n;
+                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+                },
+                [&](int e, double v) {
+                    const int rk = e / n, d = e - rk * n;
+                    cd[rk * cdld + d] = v;
+                    cf[rk * ND + d] = __double2float_rn(v);
+                });
+        }
         __syncthreads();
         for (int rk = warp; rk < KA; rk += NW) {
             float lo = 0.f, hi = 0.f;
             for (int d = lane; d < n; d += 32) {
-                const float f = cf[rk * ND + d];
+                const float f = TC ? __double2float_rn(cd[rk * cdld + d]) : cf[rk * ND + d];
                 lo = __fmaf_rd(f, f, lo);
                 hi = __fmaf_ru(f, f, hi);
             }
@@ -476,6 +704,32 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 ncr[rk] = ok ? __fsqrt_ru(hi) : finf;
             }
         }
+        CDBG(rr, 15);
+        if constexpr (TC) {
+            // warp 0 issues the tile MMAs (one elected lane): D[tile] = rows . (hi + lo)^T over K
+            if (warp == 0) {
+                tc_fence_after();
+                // descriptors advance through their 14-bit start-address field
+                // (units of 16 B); k-steps outer, tiles inner: consecutive MMAs
+                // feed different accumulators
+                const unsigned long long da0 = umma_desc_sw128(smem_addr(sm + L.xs));
+                const unsigned long long dbh = umma_desc_sw128(smem_addr(sm + L.cb));
+                const unsigned long long dbl = dbh + ((static_cast<unsigned long long>(NKA) * kCKMax * 128) >> 4);
+                const int ntl = MP / 128;
+                constexpr int KSTEPS = (ND + 31) / 32 * 4;  // whole K-atoms (zero-padded)
+                for (int ks = 0; ks < KSTEPS; ++ks) {
+                    const unsigned long long ko = ((ks & 3) * 32) >> 4;
+                    const unsigned long long bo = ((static_cast<unsigned long long>(ks >> 2) * kCKMax * 128) >> 4) + ko;
+                    const unsigned long long ao = ((static_cast<unsigned long long>(ks >> 2) * ASZ) >> 4) + ko;
+                    for (int t = 0; t < ntl; ++t) {
+                        const unsigned long long da = da0 + ao + static_cast<unsigned long long>(t) * (16384 >> 4);
+                        umma_tf32(s_tmem + 32u * t, da, dbh + bo, ks > 0);
+                        umma_tf32(s_tmem + 32u * t, da, dbl + bo, 1);
+                    }
+                }
+                umma_commit(&s_mbar);
+            }
+        }
         __syncthreads();
         if (KA == 0) {  // assign_nearest on all-degenerate centroids (core.cpp:115-118)
             if (tid == 0) ctl.state_error = 1;
@@ -483,7 +737,79 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
 
         CDBG(rr, 1);
-        // ---- assign: certified fp32 screen ----
+        // ---- assign: certified screen, then the candidate masks ----
+        unsigned cmask[PPT];
+        if constexpr (TC) {
+            // dot products of this thread's points with the 32 centroid slots
+            // from TMEM (tile = point / 128; this warp's lane quarter); packed
+            // bounds (two points, or two centroids); candidates j with L_j <= min U
+            mbar_wait_parity(&s_mbar, mma_phase);
+            mma_phase ^= 1u;
+            tc_fence_after();
+            // one point at a time: 32 dot products in registers, bounds of
+            // centroid pairs (j, j+1), then the candidates j with L_j <= min U
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                const int p = tid + i * NT;
+                float Lv[32];
+                tmem_ld32(s_tmem + (static_cast<unsigned>(32 * (warp & 3)) << 16) + 32u * static_cast<unsigned>(p >> 7),
+                          Lv);
+#ifdef BM_CHUNK_MMA_DIAG
+                if (a.dbg_mma && cta == 0 && p < np) {  // diagnostics: observed MMA error / (||x|| ||c||)
+                    float worst = 0.f;
+                    for (int j = 0; j < KA; ++j) {
+                        double ex = 0.0;
+                        for (int d = 0; d < n; ++d)
+                            ex += static_cast<double>(xat(p, d)) * static_cast<double>(__double2float_rn(cd[j * cdld + d]));
+                        const double den = sqrt(static_cast<double>(i ? nxh2.y : nxh2.x)) * sqrt(static_cast<double>(nch[j]));
+                        if (den > 0) worst = fmaxf(worst, static_cast<float>(fabs(static_cast<double>(Lv[j]) - ex) / den));
+                        if (a.dbg && !(fabs(static_cast<double>(Lv[j]) - ex) <= 1e-2 * den + 1e-30)) {
+                            if (r == 0) atomicAdd(&a.dbg[(0 * 8 + 5) * 16 + (p >> 7)], 1ull);
+                            if (r == 0) atomicAdd(&a.dbg[(0 * 8 + 5) * 16 + 8 + (p & 7)], 1ull);
+                            unsigned long long* slot = &a.dbg[((s_chunk & 3ull) * 8 + 6) * 16];
+                            if (atomicCAS(slot, 0ull, 1ull) == 0ull) {
+                                slot[1] = static_cast<unsigned long long>(p);
+                                slot[2] = static_cast<unsigned long long>(j);
+                                slot[3] = static_cast<unsigned long long>(r);
+                                slot[4] = __double_as_longlong(static_cast<double>(Lv[j]));
+                                slot[5] = __double_as_longlong(ex);
+                                slot[6] = static_cast<unsigned long long>(KA);
+                                slot[7] = static_cast<unsigned long long>(np);
+                            }
+                        }
+                    }
+                    if (a.dbg)
+                        atomicMax(reinterpret_cast<unsigned*>(&a.dbg[((s_chunk & 3ull) * 8 + 7) * 16 + 14]),
+                                  __float_as_uint(worst));
+                }
+#endif
+                const float2 nl = make_float2(i ? nxl2.y : nxl2.x, i ? nxl2.y : nxl2.x);
+                const float2 nh = make_float2(i ? nxh2.y : nxh2.x, i ? nxh2.y : nxh2.x);
+                const float2 nr = make_float2(i ? nxr2.y : nxr2.x, i ? nxr2.y : nxr2.x);
+                float mu = finf;
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    if (j >= KA) break;
+                    const bool v1 = j + 1 < KA;
+                    const int j1 = v1 ? j + 1 : j;
+                    float2 Lb, Ub;
+                    bounds2(make_float2(Lv[j], Lv[j + 1]), nl, nh, nr, make_float2(ncl[j], ncl[j1]),
+                            make_float2(nch[j], nch[j1]), make_float2(ncr[j], ncr[j1]), cst, Lb, Ub);
+                    Lv[j] = Lb.x;
+                    Lv[j + 1] = Lb.y;
+                    mu = fminf(mu, Ub.x);
+                    if (v1) mu = fminf(mu, Ub.y);
+                }
+                unsigned m = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < KA) m |= (Lv[j] <= mu ? 1u : 0u) << j;
+                cmask[i] = p < np ? m : 0u;
+            }
+            tc_fence_before();  // TMEM reads done before the next round's MMAs (behind CTA barriers)
+            CDBG(rr, 2);
+        } else {
+        // certified fp32 screen (packed FFMA)
         // groups of JG centroids (8, then 4 / 2 / 1 for the rest: no padding
         // work); per point the running minimum of the upper bounds and the
         // running candidate mask {j : L_j <= running min at j} (a superset of
@@ -519,7 +845,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                     const int j = j0 + u;
                     float2 Lb, Ub;
                     bounds2(acc[u], nxl2, nxh2, nxr2, make_float2(ncl[j], ncl[j]), make_float2(nch[j], nch[j]),
-                            make_float2(ncr[j], ncr[j]), a.cst, Lb, Ub);
+                            make_float2(ncr[j], ncr[j]), cst, Lb, Ub);
                     Ls[j * B + tid] = Lb.x;
                     Ls[j * B + tid + NT] = Lb.y;
                     minU2 = make_float2(fminf(minU2.x, Ub.x), fminf(minU2.y, Ub.y));
@@ -537,7 +863,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                     const int j1 = v1 ? j + 1 : j;
                     float2 Lb, Ub;
                     bounds2(dot, nxl2, nxh2, nxr2, make_float2(ncl[j], ncl[j1]), make_float2(nch[j], nch[j1]),
-                            make_float2(ncr[j], ncr[j1]), a.cst, Lb, Ub);
+                            make_float2(ncr[j], ncr[j1]), cst, Lb, Ub);
                     Ls[j * B + tid] = Lb.x;
                     minU2.x = fminf(minU2.x, Ub.x);
                     rm[0] |= (Lb.x <= minU2.x ? 1u : 0u) << j;
@@ -568,7 +894,6 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         // final candidates: the running ones whose L_j <= the final minimum;
         // every thread rechecks its own points (lanes in lock step: one
         // candidate per point is the common case)
-        unsigned cmask[PPT];
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const int p = tid + i * NT;
@@ -579,6 +904,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 m |= (Ls[j * B + p] <= minU[i] ? 1u : 0u) << j;
             }
             cmask[i] = m;
+        }
         }
         CDBG(rr, 9);
         CDBG(rr, 10);
@@ -596,7 +922,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 while (m) {
                     const int j = __ffs(m) - 1;
                     m &= m - 1;
-                    const double v = exact_dist(xs + static_cast<size_t>(p) * xld, cd + j * cdld, n);
+                    const double v = exact(p, j);
                     if (v < best) {
                         best = v;
                         bj = j;
@@ -605,7 +931,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             }
             if (bj < 0) {  // no candidate (non-finite bounds): full exact scan
                 for (int j = 0; j < KA; ++j) {
-                    const double v = exact_dist(xs + static_cast<size_t>(p) * xld, cd + j * cdld, n);
+                    const double v = exact(p, j);
                     if (v < best) {
                         best = v;
                         bj = j;
@@ -703,6 +1029,23 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             constexpr int LG = ND <= 64 ? 16 : 32;
             constexpr int DPL = (ND + LG - 1) / LG;
             const int NG = NT / LG, g = tid / LG, gl = tid - g * LG;
+            // per dimension of this lane: byte offset within a member row, and
+            // (tc) its 16-byte chunk index within the swizzle atom (lanes past n
+            // read a valid dimension and are never stored)
+            unsigned doff[DPL];
+            int dq[DPL];
+#pragma unroll
+            for (int t = 0; t < DPL; ++t) {
+                const int d = gl + LG * t < n ? gl + LG * t : 0;
+                if constexpr (TC) {
+                    doff[t] = static_cast<unsigned>(L.xs + static_cast<size_t>(d >> 5) * ASZ) + (d & 3) * 4;
+                    dq[t] = (d >> 2) & 7;
+                } else {
+                    doff[t] = static_cast<unsigned>(L.xs) + d * static_cast<unsigned>(sizeof(T));
+                    dq[t] = 0;
+                }
+            }
+            const unsigned rstride = TC ? 128u : static_cast<unsigned>(xld * sizeof(T));
             for (int j = g; j < k; j += NG) {
                 if (!((dirty >> j) & 1u)) continue;  // same members as last round: same partial
                 const int b = loff[j], e = loff[j + 1];
@@ -711,17 +1054,21 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 for (int t = 0; t < DPL; ++t) acc[t] = 0.0;
                 for (int i = b; i < e; i += 8) {
                     const int cnt8 = min(8, e - i);
-                    int mr[8];
+                    unsigned mrow[8];
+                    int msw[8];
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) mr[r] = r < cnt8 ? members[i + r] : 0;
+                    for (int r = 0; r < 8; ++r) {
+                        const int m = members[min(i + r, e - 1)];
+                        mrow[r] = static_cast<unsigned>(m) * rstride;
+                        msw[r] = m & 7;
+                    }
                     T xv[8][DPL];
 #pragma unroll
                     for (int r = 0; r < 8; ++r)
 #pragma unroll
-                        for (int t = 0; t < DPL; ++t) {
-                            const int d = gl + LG * t;
-                            xv[r][t] = d < n ? xs[static_cast<size_t>(mr[r]) * xld + d] : T(0);
-                        }
+                        for (int t = 0; t < DPL; ++t)
+                            xv[r][t] = *reinterpret_cast<const T*>(sm + (doff[t] + mrow[r] +
+                                                                          (TC ? static_cast<unsigned>((dq[t] ^ msw[r]) << 4) : 0u)));
 #pragma unroll
                     for (int r = 0; r < 8; ++r)
                         if (r < cnt8)
@@ -893,6 +1240,15 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         CDBG(rr, 8);
     }
 
+    if constexpr (TC) {  // the accumulators are no longer needed
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) {
+            tc_fence_after();
+            const unsigned cols = MP / 128 * 32 <= 32 ? 32 : MP / 128 * 32 <= 64 ? 64 : MP / 128 * 32 <= 128 ? 128 : 256;
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(cols) : "memory");
+        }
+    }
     // ---- after the stop: accept (big_means.cpp:89-94), record ----
     // f_opt is exact once every earlier chunk's deferred objective is folded
     // (their k_chunk_fix ran on the side stream during this chunk); the
@@ -1137,13 +1493,22 @@ std::mutex g_attr_mu;
 
 }  // namespace
 
-dev::ScreenConsts chunk_screen_consts(int n) {
-    // dot products: two interleaved fp32 FMA chains over the dimension pairs,
-    // added at the end -> |err| <= gamma_{ceil(n/2)+1} sum|x_d c_d|; taken as
-    // gamma_{n+2} (covers any n); the rest as in engine.cu's screen_consts.
+dev::ScreenConsts chunk_screen_consts(int n, bool tc, bool rows_tf32_exact) {
+    // |computed dot - x^.c^| <= gb ||x^|| ||c^||  (x^, c^: the fp32 rows / centroids):
+    //  * packed-FFMA screen: two interleaved fp32 FMA chains added at the end,
+    //    gamma_{ceil(n/2)+1}, taken as gamma_{n+2};
+    //  * tensor core (tcgen05 kind::tf32, fp32 accumulate): c^ = hi + lo with
+    //    hi = tf32(c^), lo exact; the MMA reads lo (and x^, unless every row
+    //    value is exactly a tf32) truncated to tf32 (< 2^-10 relative), products
+    //    are exact, and each of the <= 2n accumulations loses < 2^-23 of the
+    //    running magnitude (<= sum |x^_d c^_d|): gb = e_x + 2^-21 + 2n 2^-23,
+    //    doubled as a safety margin.
+    // The rest as in engine.cu's screen_consts.
     const double u = std::ldexp(1.0, -24);
     auto gam = [&](double m) { return m * u / (1.0 - m * u); };
-    const double gb = gam(n + 2);
+    const double gb = tc ? 2.0 * ((rows_tf32_exact ? 0.0 : std::ldexp(1.0, -10)) + std::ldexp(1.0, -21) +
+                                  2.0 * n * std::ldexp(1.0, -23))
+                         : gam(n + 2);
     const double up = u * (1.0 + 4 * u) / (1.0 - u);
     const double K = gb / 2.0 + 2.0 * up + up * up;
     const double u64 = std::ldexp(1.0, -53);
@@ -1183,11 +1548,14 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
         const uint64_t per = (s + sms - 1) / sms;
         threads = static_cast<int>(std::min<uint64_t>(dev::kCMaxT, ((per + in->ppt - 1) / in->ppt + 31) / 32 * 32));
         threads = std::max(threads, 32);
+        // tensor-core screen with two points per thread: thread t's second point
+        // (t + threads) must sit in the same TMEM lane quarter as its first
+        if (storage == BM_F32 && in->ppt == 2) threads = (threads + 127) / 128 * 128;
         B = threads * in->ppt;
     }
     const unsigned grid = static_cast<unsigned>((s + B - 1) / B);
     if (grid > static_cast<unsigned>(sms)) return p;  // one CTA per SM, all co-resident
-    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid);
+    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid, storage == BM_F32);
     if (L.total + 2048 > static_cast<size_t>(smem_optin)) return p;
     // the previous chunk's k_chunk_fix must find room next to this kernel's
     // CTAs (the accept waits for it): a free SM, or room on every SM

@@ -47,7 +47,8 @@ struct ChunkArgs {
     unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
     double* rsum;             // [2] per-round fast distance sums (slot = round & 1)
     int* rchg;                // [2] per-round "a label changed" flags
-    ScreenConsts cst;
+    ScreenConsts cst;         // screen bounds: packed-FFMA (fp64 rows) / tensor core, rows exact in tf32
+    ScreenConsts cst_loose;   // tensor core, rows not exact in tf32 (truncated by the MMA)
     unsigned long long max_iterations;
     double rel_tolerance;
     int force_exact;          // test hook: every interval decision takes the exact path
@@ -63,6 +64,7 @@ struct ChunkArgs {
     unsigned long long* timing;  // optional [2 * timing_cap]: per chunk, globaltimer at CTA 0's start and the accept's end
     unsigned long long timing_cap;
     unsigned long long* dbg;  // optional [4][8][16] phase stamps (BM_CHUNK_DBG)
+    int dbg_mma;              // diagnostics (BM_CHUNK_DBG=2): max observed MMA dot error into dbg
     FixJob* job;              // this chunk buffer's deferred exact objective
     unsigned long long* fix_seq;  // chunks whose exact objective is final (k_chunk_fix)
 };
@@ -96,7 +98,9 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a);
 // Enqueue the deferred exact objective of the chunk just launched (side stream).
 void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f);
-// The certified-screen constants of the chunk kernel's dot-product order.
-dev::ScreenConsts chunk_screen_consts(int n);
+// The certified-screen constants of the chunk kernel's dot products: the
+// packed-FFMA screen (tc = false) or the tensor-core screen (tc = true, with
+// rows exactly representable in tf32 or not).
+dev::ScreenConsts chunk_screen_consts(int n, bool tc = false, bool rows_tf32_exact = true);
 
 }  // namespace bm

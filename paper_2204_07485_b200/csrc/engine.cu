@@ -1886,7 +1886,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 a.bar = w.cbar.p;
                 a.rsum = w.crsum.p;
                 a.rchg = w.crchg.p;
-                a.cst = chunk_screen_consts(n);
+                a.cst = chunk_screen_consts(n, d->dtype == BM_F32, true);
+                a.cst_loose = chunk_screen_consts(n, d->dtype == BM_F32, false);
                 a.max_iterations = cfg.max_iterations;
                 a.rel_tolerance = cfg.rel_tolerance;
                 a.force_exact = force_exact_control() ? 1 : 0;
@@ -1901,6 +1902,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 a.timing = w.ctiming.p;
                 a.timing_cap = w.ctiming.n / 2;
                 a.dbg = chunk_dbg_buffer();
+                a.dbg_mma = a.dbg && std::string(std::getenv("BM_CHUNK_DBG")) == "2";
                 static const bool defer = !(std::getenv("BM_CHUNK_FIX") && std::string(std::getenv("BM_CHUNK_FIX")) == "0");
                 a.job = defer ? w.cjob.p + i : nullptr;
                 a.fix_seq = defer ? w.cfix_seq.p : nullptr;

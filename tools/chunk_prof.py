@@ -41,9 +41,12 @@ if os.environ.get("BM_CHUNK_DBG"):
             segs = [f"{names[i]}->{names[i+1]} {(row[i+1]-row[i])/1e3:.1f}" for i in range(8) if row[i + 1] >= row[i] > 0]
             if row[9] and row[11]:
                 segs.append(f"[cand {(row[9]-row[2])/1e3:.1f} exact {(row[11]-row[9])/1e3:.1f}]")
+            if row[15] > row[0] > 0:
+                segs.append(f"[cent-load {(row[15]-row[0])/1e3:.1f}]")
             if row[12] > row[3] > 0:
                 segs.append(f"[sort {(row[12]-row[3])/1e3:.1f} fold {(row[4]-row[12])/1e3:.1f}]")
             print(f"  r{r} @{(row[0]-t0)/1e3:.1f}us: " + " | ".join(segs))
         tail = buf[c, 7]
-        print(f"  rows->smem {(buf[c,0,0]-tail[13])/1e3:.1f} us")
+        print(f"  rows->smem {(buf[c,0,0]-tail[13])/1e3:.1f} us; max MMA dot error / (|x||c|) "
+              f"{np.array([tail[14] & 0xFFFFFFFF], np.uint32).view(np.float32)[0]:.3g}")
         print(f"  tail: loop-end @{(tail[9]-t0)/1e3:.1f} fold {(tail[10]-tail[9])/1e3:.1f} bar {(tail[11]-tail[10])/1e3:.1f} accept {(tail[12]-tail[11])/1e3:.1f}")
