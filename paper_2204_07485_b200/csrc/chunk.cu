@@ -383,11 +383,12 @@ struct CCtl {
             a.dbg[((s_chunk & 3ull) * 8 + (row)) * 16 + (ph)] = gtimer();                    \
     } while (0)
 
-template <typename T, int ND, int PPT>
+template <typename T, int ND, int PPT, bool TC>
 __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ ChunkArgs a) {
-    // fp32 rows: tensor-core screen (tcgen05.mma kind::tf32, TMEM accumulators);
-    // fp64 rows: packed-FFMA screen with the rows in registers
-    constexpr bool TC = sizeof(T) == 4;
+    // TC (fp32 rows): tensor-core screen (tcgen05.mma kind::tf32, TMEM
+    // accumulators) over rows in the swizzled K-major layout; otherwise the
+    // packed-FFMA screen with the rows in registers (row-major shared rows)
+    static_assert(!TC || sizeof(T) == 4, "the tensor-core screen reads fp32 rows");
     extern __shared__ __align__(16) unsigned char sm_raw[];
     if (!__ldcg(&a.gs->go)) return;  // a chunk queued behind one that needs a repair: nothing to do
     const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
@@ -1463,31 +1464,30 @@ float f_rd32(double x) {
     return f;
 }
 
-template <typename T, int ND, int PPT>
+template <typename T, int ND, int PPT, bool TC>
 void* kernel_ptr() {
-    return reinterpret_cast<void*>(&dev::k_chunk<T, ND, PPT>);
+    return reinterpret_cast<void*>(&dev::k_chunk<T, ND, PPT, TC>);
 }
 
-// (ND, PPT) instances: ND = padded width (multiple of 8, or 4 below 8).
+// (ND, PPT) instances: ND = padded width (multiple of 8); fp32 with the
+// tensor-core screen (tc) or the packed-FFMA screen, fp64 with the latter.
 struct Inst {
     int nd, ppt;
+    void* f32tc;
     void* f32;
     void* f64;
 };
 
+#define BM_CHUNK_INST(ND, PPT)                                                                              \
+    {ND, PPT, kernel_ptr<float, ND, PPT, true>(), kernel_ptr<float, ND, PPT, false>(), kernel_ptr<double, ND, PPT, false>()}
 const std::vector<Inst>& instances() {
     static const std::vector<Inst> v = {
-        {8, 2, kernel_ptr<float, 8, 2>(), kernel_ptr<double, 8, 2>()},
-        {16, 2, kernel_ptr<float, 16, 2>(), kernel_ptr<double, 16, 2>()},
-        {24, 2, kernel_ptr<float, 24, 2>(), kernel_ptr<double, 24, 2>()},
-        {32, 2, kernel_ptr<float, 32, 2>(), kernel_ptr<double, 32, 2>()},
-        {40, 1, kernel_ptr<float, 40, 1>(), kernel_ptr<double, 40, 1>()},
-        {56, 1, kernel_ptr<float, 56, 1>(), kernel_ptr<double, 56, 1>()},
-        {72, 1, kernel_ptr<float, 72, 1>(), kernel_ptr<double, 72, 1>()},
-        {88, 1, kernel_ptr<float, 88, 1>(), kernel_ptr<double, 88, 1>()},
+        BM_CHUNK_INST(8, 2),  BM_CHUNK_INST(16, 2), BM_CHUNK_INST(24, 2), BM_CHUNK_INST(32, 2),
+        BM_CHUNK_INST(40, 1), BM_CHUNK_INST(56, 1), BM_CHUNK_INST(72, 1), BM_CHUNK_INST(88, 1),
     };
     return v;
 }
+#undef BM_CHUNK_INST
 
 std::mutex g_attr_mu;
 
@@ -1521,7 +1521,8 @@ dev::ScreenConsts chunk_screen_consts(int n, bool tc, bool rows_tf32_exact) {
     return c;
 }
 
-ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums) {
+ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc) {
+    tc = tc && storage == BM_F32;
     ChunkPlan p;
     if (k < 1 || k > dev::kCKMax || n < 1 || s < 1 || s > (1ull << 31)) return p;
     const Inst* in = nullptr;
@@ -1550,17 +1551,18 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
         threads = std::max(threads, 32);
         // tensor-core screen with two points per thread: thread t's second point
         // (t + threads) must sit in the same TMEM lane quarter as its first
-        if (storage == BM_F32 && in->ppt == 2) threads = (threads + 127) / 128 * 128;
+        if (tc && in->ppt == 2) threads = (threads + 127) / 128 * 128;
         B = threads * in->ppt;
     }
     const unsigned grid = static_cast<unsigned>((s + B - 1) / B);
     if (grid > static_cast<unsigned>(sms)) return p;  // one CTA per SM, all co-resident
-    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid, storage == BM_F32);
+    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid, tc);
     if (L.total + 2048 > static_cast<size_t>(smem_optin)) return p;
     // the previous chunk's k_chunk_fix must find room next to this kernel's
     // CTAs (the accept waits for it): a free SM, or room on every SM
     if (grid >= static_cast<unsigned>(sms) && (threads > 384 || L.total > 216 * 1024)) return p;
     p.ok = true;
+    p.tc = tc;
     p.B = B;
     p.threads = threads;
     p.ppt = in->ppt;
@@ -1581,7 +1583,7 @@ void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f) {
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a0) {
     void* fn = nullptr;
     for (const Inst& i : instances())
-        if (i.nd == p.nd && i.ppt == p.ppt) fn = storage == BM_F64 ? i.f64 : i.f32;
+        if (i.nd == p.nd && i.ppt == p.ppt) fn = storage == BM_F64 ? i.f64 : p.tc ? i.f32tc : i.f32;
     if (!fn) throw CudaError("chunk kernel: no instance");
     {
         // the attribute is a per-device maximum: raise it, never lower it

@@ -88,12 +88,13 @@ struct FixArgs {
 // multi-launch path (engine.cu).
 struct ChunkPlan {
     bool ok = false;
+    bool tc = false;  // tensor-core screen (fp32 rows, swizzled layout)
     int B = 0, threads = 0, ppt = 0, nd = 0, xld = 0, ordered = 0;
     unsigned grid = 0;
     size_t smem = 0;
 };
 
-ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums);
+ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc);
 // Enqueue one chunk (cooperative launch, capturable into a graph).
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a);
 // Enqueue the deferred exact objective of the chunk just launched (side stream).

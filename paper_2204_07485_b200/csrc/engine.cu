@@ -425,6 +425,9 @@ struct bm_dataset {
     bool exact_sums = false;
     int sum_exp = 0;
     double sum_units_max = 0.0;  // max|x| / 2^sum_exp
+    // fp32 storage whose every value is exactly a tf32 (11 significant bits):
+    // the chunk kernel's tensor-core screen has a tight certified bound
+    bool tf32_exact = false;
     cudaStream_t stream = nullptr;  // upload / download only
     ~bm_dataset() {  // X comes from the stream-ordered pool
         if (X) {
@@ -1488,6 +1491,15 @@ unsigned long long* chunk_dbg_buffer() {
     return p;
 }
 
+// The chunk kernel's screen for fp32 rows: tensor core (tcgen05) when the rows
+// are exact in tf32 (tight bound), else packed FFMA (BM_TC=1 / 0 force it).
+bool tc_screen_enabled(bool tf32_exact) {
+    const char* e = std::getenv("BM_TC");
+    if (e && std::string(e) == "1") return true;
+    if (e && std::string(e) == "0") return false;
+    return tf32_exact;
+}
+
 // BM_PERSIST=0: the multi-launch chunk graphs instead of the persistent chunk
 // kernel (A/B checks; the kernel also needs a plan that fits, chunk_plan).
 bool persist_enabled() {
@@ -1761,7 +1773,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     // persistent chunk kernel (chunk.cu): one cooperative launch per chunk
     ChunkPlan cplan;
     if (use_graphs && persist_enabled() && !w.hist_cap)
-        cplan = chunk_plan(d->device, s, n, k, d->dtype, d->exact_sums && exact_sums_enabled());
+        cplan = chunk_plan(d->device, s, n, k, d->dtype, d->exact_sums && exact_sums_enabled(),
+                           d->dtype == BM_F32 && tc_screen_enabled(d->tf32_exact));
     const bool persist = cplan.ok;
     if (persist) {
         w.ensure_chunk(cplan);
@@ -1886,8 +1899,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 a.bar = w.cbar.p;
                 a.rsum = w.crsum.p;
                 a.rchg = w.crchg.p;
-                a.cst = chunk_screen_consts(n, d->dtype == BM_F32, true);
-                a.cst_loose = chunk_screen_consts(n, d->dtype == BM_F32, false);
+                a.cst = chunk_screen_consts(n, cplan.tc, true);
+                a.cst_loose = chunk_screen_consts(n, cplan.tc, false);
                 a.max_iterations = cfg.max_iterations;
                 a.rel_tolerance = cfg.rel_tolerance;
                 a.force_exact = force_exact_control() ? 1 : 0;
@@ -2739,7 +2752,7 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
                 BM_CUDA(cudaStreamWaitEvent(ks, ev, 0));
                 BM_CUDA(cudaEventDestroy(ev));
                 dev::k_check_narrow_write<<<592, 256, 0, ks>>>(tmp, r0, r1, (int)n, flags.p, flags.p + 1, flags.p + 2,
-                                                               maxbits, x32, ld32);
+                                                               maxbits, x32, ld32, flags.p + 3);
                 BM_LAUNCH();
             }
             BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, ks));
@@ -2774,13 +2787,14 @@ bm_status bm_dataset_create(const void* values, uint64_t m, uint64_t n, bm_dtype
             dispatch(dtype, [&](auto tag) {
                 using T = decltype(tag);
                 dev::k_check_finite<T><<<1184, 256, 0, d->stream>>>(static_cast<const T*>(d->X), m, (int)n, d->ld,
-                                                                    flags.p, flags.p + 2, maxbits);
+                                                                    flags.p, flags.p + 2, maxbits, flags.p + 3);
             });
             BM_LAUNCH();
             BM_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, d->stream));
             BM_CUDA(cudaStreamSynchronize(d->stream));
             if (hf[0]) throw ConfigError("dataset contains a non-finite value");
         }
+        d->tf32_exact = d->dtype == BM_F32 && hf[3] == 0;
         {  // exact-sum test (kernels.cuh §5b): every value k * 2^e, m * max|x| < 2^52 * 2^e
             unsigned long long mb = 0;
             std::memcpy(&mb, hf + 4, sizeof(mb));
@@ -2874,6 +2888,7 @@ bm_status bm_dataset_gather(const bm_dataset* d, const uint64_t* rows, uint64_t 
         o->dtype = d->dtype;
         o->ld = d->ld;
         o->exact_sums = d->exact_sums;  // a subset of the rows keeps the exact-sum property
+        o->tf32_exact = d->tf32_exact;
         o->sum_exp = d->sum_exp;
         o->sum_units_max = d->sum_units_max;
         BM_CUDA(cudaStreamCreateWithFlags(&o->stream, cudaStreamNonBlocking));

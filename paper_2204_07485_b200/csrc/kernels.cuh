@@ -4209,15 +4209,18 @@ __device__ __forceinline__ void exact_stats_flush(int lowexp, unsigned long long
 
 template <typename T>
 __global__ void k_check_finite(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld, int* bad, int* lowexp_out,
-                               unsigned long long* maxbits_out) {
+                               unsigned long long* maxbits_out, int* not_tf32) {
     const uint64_t total = rows * static_cast<uint64_t>(n);
     int lowexp = 0x7F7F7F7F;
     unsigned long long maxbits = 0;
     for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const double v = to_f64(X[(e / n) * ld + (e % n)]);
+        const T x = X[(e / n) * ld + (e % n)];
+        const double v = to_f64(x);
         if (!isfinite(v)) *bad = 1;
         else exact_stats(v, lowexp, maxbits);
+        // fp32 values with more than tf32's 11 significant bits (tensor-core screen bound)
+        if (sizeof(T) != 4 || (__float_as_uint(static_cast<float>(x)) & 0x1FFFu) != 0u) *not_tf32 = 1;
     }
     exact_stats_flush(lowexp, maxbits, lowexp_out, maxbits_out);
 }
@@ -4246,7 +4249,7 @@ __global__ void k_check_narrow(const double* __restrict__ v, uint64_t count, int
 // the fp32 copy written speculatively (discarded when a value is not exact).
 __global__ void k_check_narrow_write(const double* __restrict__ v, uint64_t r0, uint64_t r1, int n, int* bad,
                                      int* inexact, int* lowexp_out, unsigned long long* maxbits_out,
-                                     float* __restrict__ out, uint64_t ld) {
+                                     float* __restrict__ out, uint64_t ld, int* not_tf32) {
     int lowexp = 0x7F7F7F7F;
     unsigned long long maxbits = 0;
     const uint64_t e0 = r0 * static_cast<uint64_t>(n), e1 = r1 * static_cast<uint64_t>(n);
@@ -4260,6 +4263,7 @@ __global__ void k_check_narrow_write(const double* __restrict__ v, uint64_t r0, 
             continue;
         }
         if (static_cast<double>(f) != x) *inexact = 1;
+        if ((__float_as_uint(f) & 0x1FFFu) != 0u) *not_tf32 = 1;
         exact_stats(x, lowexp, maxbits);
     }
     exact_stats_flush(lowexp, maxbits, lowexp_out, maxbits_out);

@@ -284,3 +284,26 @@ def test_time_budget_vs_oracle(port, integer):
     assert out.objective == p.objective
     assert (bits(out.centroids.values) == bits(p.centroids)).all()
     assert (out.assignment == p.labels).all()
+
+
+@pytest.mark.parametrize("screen", ["tc", "ffma"])
+@pytest.mark.parametrize("n", [3, 6, 13, 16, 24, 28, 37, 68, 80])
+def test_chunk_kernel_screens_vs_oracle(port, monkeypatch, screen, n):
+    """The persistent chunk kernel's two screens for fp32 rows — tensor core
+    (tcgen05 kind::tf32, swizzled rows; forced with BM_TC=1 even for data that
+    is not exact in tf32, i.e. the loose certified bound) and packed FFMA
+    (BM_TC=0) — on every row-width instance, bitwise against the oracle."""
+    monkeypatch.setenv("BM_TC", "1" if screen == "tc" else "0")
+    rng = np.random.default_rng(1000 + n)
+    m, k, s = 9000, 11, 2100
+    X = (rng.normal(size=(m, n)) * 5.0 + rng.integers(0, 3, (m, 1)) * 4.0).astype(np.float32)
+    for integer in (False, True):
+        Xi = np.rint(X) if integer else X  # integer rows: exact-sum mode (B spread over the SMs)
+        out, trace = bm.big_means(bm.Dataset(Xi), cfg(k, s, 5, seed=n))
+        p = port.big_means(np.asarray(Xi, np.float64), k, s, 5, seed=n)
+        got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+                r.degenerate_repaired) for r in trace.records]
+        assert got == p.trace
+        assert out.objective == p.objective
+        assert (bits(out.centroids.values) == bits(p.centroids)).all()
+        assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
