@@ -36,8 +36,16 @@ typedef enum bm_status {
     BM_CONFIG_ERROR = 1,   /* ConfigError  common.hpp:21-24 */
     BM_STATE_ERROR = 2,    /* StateError   common.hpp:46-49 */
     BM_CUDA_ERROR = 3,     /* device failure (runtime_error) */
-    BM_INTERNAL_ERROR = 4  /* anything else (runtime_error) */
+    BM_INTERNAL_ERROR = 4, /* anything else (runtime_error) */
+    BM_PARSE_ERROR = 5     /* ParseError   common.hpp:28-42 (bm_last_parse_location) */
 } bm_status;
+
+/* io::Format io.hpp:14. */
+typedef enum bm_format {
+    BM_FORMAT_CSV = 0,
+    BM_FORMAT_WHITESPACE = 1,
+    BM_FORMAT_TSPLIB = 2
+} bm_format;
 
 typedef enum bm_dtype {
     BM_F64 = 0, /* reference storage type (core.hpp:34) */
@@ -236,6 +244,25 @@ bm_status bm_big_means_multi(bm_dataset* const* data, int32_t chains, const bm_c
  * records are copied).  Lets a caller with a time budget size its trace from
  * the result (BigMeansTrace big_means.hpp:36-40). */
 bm_status bm_last_trace(bm_chunk_record* out, uint64_t capacity, uint64_t* count);
+
+/* Dataset ingestion: io::load io.hpp:31-37 / io.cpp:224-243 (DatasetSpec
+ * io.hpp:18-25: path, format, has_header, columns, normalize).  Parses the file
+ * on the host (delimited formats in parallel over line ranges; threads <= 0:
+ * all cores), with the reference's cell rules, ragged-row check, errors and
+ * 1-based line / column (BM_PARSE_ERROR; bm_last_parse_location), the Dataset
+ * finiteness check (BM_CONFIG_ERROR) and the column selection (columns NULL:
+ * all; an empty selection is BM_CONFIG_ERROR), then uploads it and, with
+ * normalize, min-max normalises it on the device (io.cpp:245-264). */
+bm_status bm_dataset_load(const char* path, int32_t format, int32_t has_header, int32_t normalize,
+                          const uint64_t* columns, uint64_t ncolumns, int32_t threads, int device,
+                          bm_dataset** out);
+/* The host part of bm_dataset_load alone (no device): *values (malloc'd,
+ * release with bm_free_values) holds m x n row-major f64. */
+bm_status bm_parse_file(const char* path, int32_t format, int32_t has_header, const uint64_t* columns,
+                        uint64_t ncolumns, int32_t threads, double** values, uint64_t* m, uint64_t* n);
+void bm_free_values(double* values);
+/* 1-based line and column of the last BM_PARSE_ERROR on this thread. */
+bm_status bm_last_parse_location(uint64_t* line, uint64_t* column);
 
 /* Multi-GPU pieces.  Row-sharded final pass: assign rows
  * [row_begin, row_end) (row_begin a multiple of 1024) against the centroids,

@@ -353,6 +353,31 @@ class Oracle:
         if self.kind == "ref":
             self.lib.ref_set_worker_count(C.c_uint(n))
 
+    def io_load(self, path, format="csv", has_header=False, normalize=False, columns=None):
+        """The reference's io::load (io.cpp:224-243), "ref" back end only.
+        Returns ("ok", values m x n) or (kind, message, line, column) for an error
+        (kind: "config" / "state" / "parse" / "other")."""
+        if self.kind != "ref":
+            raise OracleError(1, "io_load needs the compiled reference")
+        lib = self.lib
+        lib.ref_io_load.restype = C.c_int
+        lib.ref_io_last_error.restype = C.c_char_p
+        fmt = {"csv": 0, "whitespace": 1, "tsplib": 2}[format]
+        cols = None if columns is None else np.ascontiguousarray(columns, np.uint64)
+        out = C.POINTER(C.c_double)()
+        m, n, el, ec = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        rc = lib.ref_io_load(str(path).encode(), fmt, int(has_header), int(normalize),
+                             None if cols is None else cols.ctypes.data_as(C.POINTER(C.c_uint64)),
+                             C.c_uint64(0 if cols is None else cols.size), int(cols is not None),
+                             C.byref(out), C.byref(m), C.byref(n), C.byref(el), C.byref(ec))
+        if rc != 0:
+            kind = {1: "config", 2: "state", 5: "parse"}.get(rc, "other")
+            return (kind, lib.ref_io_last_error().decode(), el.value, ec.value)
+        size = m.value * n.value
+        vals = np.ctypeslib.as_array(out, shape=(size,)).copy() if size else np.empty(0)
+        lib.ref_io_free(out)
+        return ("ok", vals.reshape(m.value, n.value))
+
 
 def port() -> Oracle:
     return Oracle("port")

@@ -10,7 +10,7 @@ from .api import (  # noqa: F401
     ClusteringOutcome, ConfigError, Dataset, DeviceError, EvalCounter, InitConfig, InitMethod, Rng,
     RoundsRule, ChunkHintConfig, choose_chunk_size_hint,
     SearchConfig, StateError, assign_nearest, assign_rows, big_means, big_means_multi, block_sum,
-    device_count,
+    device_count, load, parse_file, ParseError,
     kmeans, kmeanspp_fill, last_profile, lloyd, objective, sample_chunk, sample_chunk_device,
     set_profiling,
     update_centroids)

@@ -21,7 +21,8 @@ P_u8 = C.POINTER(C.c_uint8)
 P_i32 = C.POINTER(C.c_int32)
 P_u64 = C.POINTER(C.c_uint64)
 
-BM_OK, BM_CONFIG_ERROR, BM_STATE_ERROR, BM_CUDA_ERROR, BM_INTERNAL_ERROR = range(5)
+BM_OK, BM_CONFIG_ERROR, BM_STATE_ERROR, BM_CUDA_ERROR, BM_INTERNAL_ERROR, BM_PARSE_ERROR = range(6)
+BM_FORMAT_CSV, BM_FORMAT_WHITESPACE, BM_FORMAT_TSPLIB = range(3)
 BM_F64, BM_F32 = 0, 1
 
 
@@ -90,6 +91,12 @@ PROTOS = {
     "bm_kmeans": (C.c_int, [vp, u64, C.POINTER(bm_init_config), u64, dbl, C.POINTER(bm_outcome)]),
     "bm_init_centroids": (C.c_int, [vp, u64, C.POINTER(bm_init_config), P_dbl, C.POINTER(C.c_uint8), P_u64]),
     "bm_last_trace": (C.c_int, [C.POINTER(bm_chunk_record), u64, P_u64]),
+    "bm_dataset_load": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, P_u64, u64, C.c_int32, C.c_int,
+                                  C.POINTER(vp)]),
+    "bm_parse_file": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, P_u64, u64, C.c_int32, C.POINTER(P_dbl), P_u64,
+                                P_u64]),
+    "bm_free_values": (None, [P_dbl]),
+    "bm_last_parse_location": (C.c_int, [P_u64, P_u64]),
     "bm_big_means_multi": (C.c_int, [C.POINTER(vp), C.c_int32, C.POINTER(bm_config), C.POINTER(bm_outcome),
                                      C.POINTER(bm_chunk_record), u64, P_u64, C.POINTER(C.c_int32)]),
     "bm_choose_chunk_size_hint": (C.c_int, [vp, u64, P_u64, u64, u64, u64, u64, dbl, i32, u64, P_u64, P_dbl]),

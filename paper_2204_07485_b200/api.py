@@ -54,14 +54,29 @@ class DeviceError(RuntimeError):
     """CUDA failure or internal error."""
 
 
+class ParseError(RuntimeError):
+    """Failure while reading external input, with its 1-based line and column
+    (common.hpp:28-42)."""
+
+    def __init__(self, what: str, line: int, column: int):
+        super().__init__(what)
+        self.line = line
+        self.column = column
+
+
 def _check(rc: int) -> None:
     if rc == _capi.BM_OK:
         return
-    msg = _capi.load().bm_last_error().decode()
+    lib = _capi.load()
+    msg = lib.bm_last_error().decode()
     if rc == _capi.BM_CONFIG_ERROR:
         raise ConfigError(msg)
     if rc == _capi.BM_STATE_ERROR:
         raise StateError(msg)
+    if rc == _capi.BM_PARSE_ERROR:
+        line, col = C.c_uint64(), C.c_uint64()
+        lib.bm_last_parse_location(C.byref(line), C.byref(col))
+        raise ParseError(msg, line.value, col.value)
     raise DeviceError(msg)
 
 
@@ -558,6 +573,46 @@ def big_means(data: Dataset, cfg: BigMeansConfig, want_labels: bool = True):
     counter = EvalCounter(out.distance_evals, out.iterations, out.cpu_init, out.cpu_full)
     asg = labels if labels is not None else np.empty(0, np.int32)
     return ClusteringOutcome(Centroids(cv, cm), asg, out.objective, [], counter), trace
+
+
+_FORMATS = {"csv": 0, "whitespace": 1, "tsplib": 2}  # io::parse_format io.cpp:198-209
+
+
+def _format_id(fmt: str) -> int:
+    if fmt not in _FORMATS:
+        raise ConfigError(f"unknown dataset format '{fmt}'")
+    return _FORMATS[fmt]
+
+
+def parse_file(path: str, format: str = "csv", has_header: bool = False, columns=None,
+               threads: int = 0) -> np.ndarray:
+    """The host half of io::load (io.cpp:224-243): the parsed (and column-selected)
+    m x n float64 matrix, parsed natively in parallel; the reference's errors."""
+    lib = _capi.load()
+    cols = None if columns is None else np.ascontiguousarray(columns, np.uint64)
+    out = _capi.P_dbl()
+    m, n = C.c_uint64(), C.c_uint64()
+    _check(lib.bm_parse_file(str(path).encode(), _format_id(format), int(has_header), _ptr(cols, _capi.P_u64),
+                             0 if cols is None else cols.size, threads, C.byref(out), C.byref(m), C.byref(n)))
+    try:
+        arr = np.ctypeslib.as_array(out, shape=(m.value * n.value,)).copy() if m.value * n.value else np.empty(0)
+    finally:
+        lib.bm_free_values(out)
+    return arr.reshape(m.value, n.value)
+
+
+def load(path: str, format: str = "csv", has_header: bool = False, normalize: bool = False, columns=None,
+         device: int = 0, threads: int = 0) -> Dataset:
+    """io::load (io.hpp:31-37, DatasetSpec io.hpp:18-25) straight to a device
+    Dataset: native parallel parse, upload, and the min-max normalisation
+    (io.cpp:245-264) on the device."""
+    lib = _capi.load()
+    cols = None if columns is None else np.ascontiguousarray(columns, np.uint64)
+    h = C.c_void_p()
+    _check(lib.bm_dataset_load(str(path).encode(), _format_id(format), int(has_header), int(normalize),
+                               _ptr(cols, _capi.P_u64), 0 if cols is None else cols.size, threads, device,
+                               C.byref(h)))
+    return Dataset(None, device=device, _handle=h)
 
 
 def big_means_multi(datasets, cfg: BigMeansConfig, want_labels: bool = True):

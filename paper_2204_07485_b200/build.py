@@ -20,7 +20,7 @@ LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libbigmeans_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "chunk.cu")]
+SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "chunk.cu"), os.path.join(CSRC, "io.cpp")]
 HEADERS = [os.path.join(CSRC, f) for f in ("kernels.cuh", "common.cuh", "device_common.cuh", "chunk.h",
                                            "mt64.cuh", "tma.cuh")] + [os.path.join(ROOT, "include", "bigmeans_b200.h")]
 DEPS = SOURCES + HEADERS
