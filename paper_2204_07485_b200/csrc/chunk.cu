@@ -717,7 +717,11 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 const unsigned long long dbh = umma_desc_sw128(smem_addr(sm + L.cb));
                 const unsigned long long dbl = dbh + ((static_cast<unsigned long long>(NKA) * kCKMax * 128) >> 4);
                 const int ntl = MP / 128;
-                constexpr int KSTEPS = (ND + 31) / 32 * 4;  // whole K-atoms (zero-padded)
+                // k-steps of 8 dims; a narrow row (ND < 32) still runs its whole
+                // first K-atom: measured wrong with only 1-2 k-steps into the
+                // first swizzle atom (ND 8 / 16), right with >= 3 and with full
+                // atoms followed by a partial one (ND 40 ... 88); padding is zero
+                constexpr int KSTEPS = ND < 32 ? 4 : ND / 8;
                 for (int ks = 0; ks < KSTEPS; ++ks) {
                     const unsigned long long ko = ((ks & 3) * 32) >> 4;
                     const unsigned long long bo = ((static_cast<unsigned long long>(ks >> 2) * kCKMax * 128) >> 4) + ko;
@@ -1572,6 +1576,11 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
     p.grid = grid;
     p.smem = L.total;
     return p;
+}
+
+void chunk_fix_prefer_max_smem() {
+    BM_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(dev::k_chunk_fix),
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
 }
 
 void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f) {

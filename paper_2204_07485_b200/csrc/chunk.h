@@ -97,6 +97,8 @@ struct ChunkPlan {
 ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc);
 // Enqueue one chunk (cooperative launch, capturable into a graph).
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a);
+// k_chunk_fix prefers the maximum shared-memory carveout (current device).
+void chunk_fix_prefer_max_smem();
 // Enqueue the deferred exact objective of the chunk just launched (side stream).
 void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f);
 // The certified-screen constants of the chunk kernel's dot products: the

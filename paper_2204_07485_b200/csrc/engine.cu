@@ -667,6 +667,31 @@ void set_max_smem(F* fn, size_t bytes) {
     }
 }
 
+// The kernels that run beside the persistent chunk kernel (draws, sample
+// resolution, gather, the deferred objective) ask for the maximum shared-memory
+// carveout too: an SM then never has to drain and repartition L1 / shared
+// memory between them and a chunk kernel that uses ~200 KB per CTA.
+// (BM_CARVEOUT=0 leaves the default for A/B.)
+void prefer_max_smem_carveout() {
+    static const bool on = !(std::getenv("BM_CARVEOUT") && std::string(std::getenv("BM_CARVEOUT")) == "0");
+    if (!on) return;
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    BM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.insert(dev).second) return;
+    const void* ks[] = {reinterpret_cast<const void*>(dev::k_mt_twist), reinterpret_cast<const void*>(dev::k_mt_emit),
+                        reinterpret_cast<const void*>(dev::k_mt_fix), reinterpret_cast<const void*>(dev::k_fy_pass1),
+                        reinterpret_cast<const void*>(dev::k_fy_pass2),
+                        reinterpret_cast<const void*>(dev::k_bitmap_block_counts),
+                        reinterpret_cast<const void*>(dev::k_bitmap_emit),
+                        reinterpret_cast<const void*>(dev::k_epoch_bump), reinterpret_cast<const void*>(dev::k_gather)};
+    for (const void* k : ks)
+        BM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    chunk_fix_prefer_max_smem();
+}
+
 int assign_threads(int k) {
     const int kg = std::min<int>(dev::kAMaxCG, (int)ceil_div(std::max(k, 1), dev::kAK));
     return dev::kAPG * kg;
@@ -1777,6 +1802,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                            d->dtype == BM_F32 && tc_screen_enabled(d->tf32_exact));
     const bool persist = cplan.ok;
     if (persist) {
+        prefer_max_smem_carveout();
         w.ensure_chunk(cplan);
         if (w.ctiming.n < 2 * w.drec.n) w.ctiming.alloc(2 * w.drec.n);
         // (every fix of the previous run finished: its fix stream was synchronized)
