@@ -9,6 +9,7 @@ explicit __d*_rn intrinsics; this is belt and braces).
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -21,8 +22,8 @@ LIB = os.path.join(LIB_DIR, "libbigmeans_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "chunk.cu"), os.path.join(CSRC, "io.cpp")]
-HEADERS = [os.path.join(CSRC, f) for f in ("kernels.cuh", "common.cuh", "device_common.cuh", "chunk.h",
-                                           "mt64.cuh", "tma.cuh")] + [os.path.join(ROOT, "include", "bigmeans_b200.h")]
+HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [
+    os.path.join(ROOT, "include", "bigmeans_b200.h")]
 DEPS = SOURCES + HEADERS
 
 FLAGS = [

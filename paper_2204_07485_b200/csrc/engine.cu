@@ -166,7 +166,6 @@ struct Workspace {
     bool sums_on = false;
     double sum_scale = 1.0, sum_unscale = 1.0;
     bool sums_fuse = false;  // the update runs in the control CTA of the previous launch (LloydCtl::sum_fuse)
-    bool sum_cluster = false;  // begins merge their label sums in 8-CTA clusters (LloydCtl::sum_cluster)
     bool sum_small = false;  // per-CTA sums of the value units below 2^31 (bm_dataset::sum_units_max < 2^23)
     uint64_t sum_half() const { return (uint64_t)dev::kSumCopies * dev::kSMaxK * (n + 1); }
     long long* sums_of(int buf) { return sums.p + (uint64_t)buf * 2 * sum_half(); }
@@ -487,7 +486,7 @@ DeviceCache& cache_of(int device) {
     // The engine stream (the chunk chain's critical path) gets a priority above
     // the speculative begins and chunk preps (default priority), the draw
     // stream stays highest.  BM_PRIO=0: default priority (A/B diagnostics).
-    static const bool prio = !(std::getenv("BM_PRIO") && std::string(std::getenv("BM_PRIO")) == "0");
+    const bool prio = true;
     int lo = 0, hi = 0;
     BM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     BM_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio && hi < lo ? hi + 1 : lo));
@@ -629,27 +628,6 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     BM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
-// The same with an 8-CTA cluster dimension (the grid must be a multiple of 8).
-template <class... KArgs, class... Args>
-void launch_pdl_cluster8(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                         Args&&... args) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = 8;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    BM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
-}
-
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device maximum:
 // raise it (never lower it) per (device, kernel), thread-safe (one host thread
 // per GPU drives its own chain).
@@ -754,37 +732,6 @@ bool narrow_storage() {
     return on;
 }
 
-// BM_SCREEN=v4 selects the LDG-staged screen (A/B checks); default: TMA (v5).
-// BM_SPEC_CTAS: cap on the CTAs of a speculative begin, which then loop over its
-// blocks (default 0: one CTA per block; capping measured slower on c2).
-unsigned spec_ctas() {
-    static const unsigned v = [] {
-        const char* e = std::getenv("BM_SPEC_CTAS");
-        const long x = e ? std::atol(e) : 0;
-        return x > 0 ? (unsigned)x : ~0u;
-    }();
-    return v;
-}
-
-// BM_FINAL=tma: the final pass through k_assign_tma (one 128-point block per
-// CTA) instead of the streaming k_final.
-bool final_streaming() {
-    static const bool on = [] {
-        const char* e = std::getenv("BM_FINAL");
-        return !(e && std::string(e) == "tma");
-    }();
-    return on;
-}
-
-// BM_RING=2: the 2-stage TMA ring for wide rows too (A/B of the 6-stage ring).
-bool wide_ring() {
-    static const bool on = [] {
-        const char* e = std::getenv("BM_RING");
-        return !(e && std::string(e) == "2");
-    }();
-    return on;
-}
-
 // BM_SUMS=0 disables the exact-sum update (kernels.cuh §5b) for A/B checks.
 bool exact_sums_enabled() {
     static const bool on = [] {
@@ -794,13 +741,6 @@ bool exact_sums_enabled() {
     return on;
 }
 
-bool tma_screen() {
-    static const bool on = [] {
-        const char* e = std::getenv("BM_SCREEN");
-        return !(e && std::string(e) == "v4");
-    }();
-    return on;
-}
 
 // BM_HAMERLY=0 disables the bound-based Lloyd-round fast path (A/B checks).
 bool hamerly_enabled() {
@@ -851,7 +791,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
     const bool screen = screen_enabled(k);
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
-        if (screen && tma_screen() && P.rows < (1ull << 31)) {
+        if (screen && P.rows < (1ull << 31)) {
             fused_ctl = ctl && (tile_out || ctl->fast);
             // NS-stage TMA slab ring: 2 stages (3 CTAs per SM) for rows of up to
             // 8 slabs, 6 stages (2 CTAs per SM) for wide rows, whose CTAs stream
@@ -861,18 +801,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                 constexpr size_t shm = dev::tma_smem_bytes<T, NS>();
                 set_max_smem(dev::k_assign_tma<T, NS>, shm);
                 const CUtensorMap tmx = points_map<T>(P);
-                // a speculative begin loops over its blocks with at most spec_ctas() CTAs
-                // (BM_SPEC_CTAS), leaving SM slots to the engine stream's rounds
-                const unsigned lgrid = fused_ctl && ctl->nblk ? std::min<unsigned>(grid, spec_ctas()) : grid;
-                if (fused_ctl && ctl->sum_cluster) {  // begins: 8-CTA clusters merge the label sums (padded grid)
-                    launch_pdl_cluster8(dev::k_assign_tma<T, NS>, (grid + 7) / 8 * 8, dev::kSThreads, shm, st,
-                        tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
-                        S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
-                        g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), *ctl,
-                        !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
-                        dstride);
-                    return;
-                }
+                const unsigned lgrid = grid;
                 launch_pdl(dev::k_assign_tma<T, NS>, lgrid, dev::kSThreads, shm, st,
                     tmx, *S.tmc, static_cast<const T*>(P.X), P.rows, P.n, P.ld, S.Cact, w.ldc, S.act,
                     S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
@@ -880,15 +809,8 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                     !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
                     dstride);
             };
-            if (P.n > 8 * dev::kADC && wide_ring()) go(std::integral_constant<int, 6>{});
+            if (P.n > 8 * dev::kADC) go(std::integral_constant<int, 6>{});
             else go(std::integral_constant<int, 2>{});
-        } else if (screen) {
-            constexpr size_t shm = dev::screen_smem_bytes();
-            set_max_smem(dev::k_assign_screen<T>, shm);
-            dev::k_assign_screen<T><<<grid, dev::kSThreads, shm, st>>>(
-                static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p,
-                &w.gs.p->n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out,
-                tile_ctr, g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n));
         } else {
             dev::k_assign<T><<<grid, assign_threads(k), 0, st>>>(
                 static_cast<const T*>(P.X), P.rows, P.n, P.ld, w.Cact.p, w.ldc, w.act.p, &w.gs.p->n_active,
@@ -1051,16 +973,11 @@ void apply_graph(dev::LloydCtl& c, Workspace& w, const GraphRound* g) {
         c.has_acc = 1;
     }
     c.accept_run = g->accept ? 1 : 0;
-    if (g->begin_kind == 1 && spec_ctas() != ~0u)  // capped in CTAs (launch_assign), looping over the blocks
-        c.nblk = (unsigned)ceil_div(w.R, dev::kABP);
     if (w.sums_on) {  // exact-sum mode: the begins fill a half, the rounds move points in the live one
         c.sums = w.sums_of(g->buf);
         c.sum_half = w.sum_half();
         c.sum_scale = w.sum_scale;
         c.sum_which = g->begin_kind == 1 ? 0 : g->begin_kind == 2 ? 1 : -1;
-        // begins of fp32 data whose partials fit a CTA's bound-row buffer: 8-CTA
-        // clusters with BM_SUM_CLUSTER=1 (default: the group-of-8 merge through global memory)
-        c.sum_cluster = g->begin_kind != 0 && w.sum_cluster && spec_ctas() == ~0u ? 1 : 0;
         if (g->begin_kind != 0) {
             c.parts = w.sum_parts.p + (uint64_t)g->buf * w.part_ctas() * w.part_len();
             c.grp_ctr = w.grp_ctr.p + (uint64_t)g->buf * ceil_div(w.part_ctas(), (uint64_t)dev::kSumGroup);
@@ -1425,10 +1342,7 @@ void enqueue_gather(cudaStream_t st, const bm_dataset* d, const uint32_t* idx, u
                     const void* const* xslot = nullptr) {
     PhaseScope ps(PH_GATHER, s);
     const uint64_t row_vecs = d->ld * dtype_size(d->dtype) / 16;
-    static const unsigned cap = [] {  // 4 CTAs per SM (148 SMs); BM_GATHER_CTAS overrides (A/B)
-        const char* e = std::getenv("BM_GATHER_CTAS");
-        return e ? (unsigned)std::max(1, std::atoi(e)) : 592u;
-    }();
+    constexpr unsigned cap = 592u;  // 4 CTAs per SM (148 SMs)
     const unsigned grid = (unsigned)std::min<uint64_t>(cap, ceil_div((uint64_t)s * row_vecs, 4 * 256));
     dev::k_gather<<<grid, 256, 0, st>>>(static_cast<const uint4*>(d->X),
                                         reinterpret_cast<const uint4* const*>(xslot), (uint32_t)row_vecs, idx, s,
@@ -1465,7 +1379,7 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
     P.X = static_cast<const uint8_t*>(d->X) + r0 * d->ld * dtype_size(d->dtype);
     P.rows = r1 - r0;
     c.ensure_final(P.rows);
-    if (final_streaming() && screen_enabled(w.k) && P.n <= dev::kFMaxD && tma_screen() && P.rows < (1ull << 31)) {
+    if (screen_enabled(w.k) && P.n <= dev::kFMaxD && P.rows < (1ull << 31)) {
         // streaming form (k_final): persistent CTAs, one continuous TMA ring; then the tile partials
         PhaseScope ps(PH_FINAL, P.rows);
         dispatch(P.dtype, [&](auto tag) {
@@ -1617,7 +1531,7 @@ cudaGraphExec_t capture_lloyd(cudaStream_t st, Workspace& w, const Points& P, ui
     if (!w.cap2) BM_CUDA(cudaStreamCreateWithFlags(&w.cap2, cudaStreamNonBlocking));
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     // fast-sum control whenever the TMA screen (which implements it) runs
-    const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
+    const bool fast = screen_enabled(w.k) && P.rows < (1ull << 31) && !w.hist_cap;
     if (fast) {
         // begin unless the speculative begin (capture_spec) is current ->
         // round 1 (+ fixup CTAs: the previous chunk's exact objective for its
@@ -1731,14 +1645,14 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
                   (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
                   (void*)dc.chunk3.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n,
-                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse + 8 * (int)w.sum_cluster +
+                  (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse +
                       16 * (int)persist,
                   w.sum_scale, (void*)w.sums.p);
     if (w.graph_sig == sig && w.g_prep[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
     void* bufs[dev::kStateBufs] = {dc.chunk.p, dc.chunk1.p, dc.chunk2.p, dc.chunk3.p};
-    const bool fast = screen_enabled(w.k) && tma_screen() && P.rows < (1ull << 31) && !w.hist_cap;
+    const bool fast = screen_enabled(w.k) && P.rows < (1ull << 31) && !w.hist_cap;
     for (int i = 0; i < dev::kStateBufs; ++i) {  // data and state buffer i, draw buffer i % 2
         const int b = i;
         Points Pb = P;
@@ -1810,7 +1724,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         BM_CUDA(cudaMemsetAsync(w.cjob.p, 0, dev::kStateBufs * sizeof(dev::FixJob), st));
     }
     // exact-sum mode for the graph chunks (kernels.cuh §5b)
-    w.sums_on = use_graphs && !persist && d->exact_sums && exact_sums_enabled() && screen_enabled(k) && tma_screen() &&
+    w.sums_on = use_graphs && !persist && d->exact_sums && exact_sums_enabled() && screen_enabled(k) &&
                 s < (1ull << 31) && !w.hist_cap;
     if (w.sums_on) {
         w.sum_scale = std::ldexp(1.0, -d->sum_exp);
@@ -1818,9 +1732,6 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         w.sum_small = d->sum_units_max < 0x1p23;  // 128 points per CTA: partial sums below 2^30
         static const bool fuse = !(std::getenv("BM_SUMS_FUSE") && std::string(std::getenv("BM_SUMS_FUSE")) == "0");
         w.sums_fuse = fuse;
-        // (measured slower on c2: 20.4 vs 18.6 ms, the 8-CTA clusters wait for co-resident slots)
-        static const bool clus = std::getenv("BM_SUM_CLUSTER") && std::string(std::getenv("BM_SUM_CLUSTER")) == "1";
-        w.sum_cluster = clus && d->dtype == BM_F32 && (uint64_t)k * n + k <= 2048;
         const uint64_t nb = dev::kStateBufs;
         if (w.sums.n < 2 * nb * w.sum_half()) w.sums.alloc(2 * nb * w.sum_half());
         if (w.sum_parts.n < nb * w.part_ctas() * w.part_len()) w.sum_parts.alloc(nb * w.part_ctas() * w.part_len());
@@ -1856,9 +1767,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
             BM_CUDA(cudaEventRecord(w.ev_spec[i], st));
         }
-        // BM_PIPE=0: preps on the Lloyd stream (no overlap; timeline diagnostics)
-        static const bool pipe = !(std::getenv("BM_PIPE") && std::string(std::getenv("BM_PIPE")) == "0");
-        const cudaStream_t pst = pipe ? dc.pstream : st;
+        const cudaStream_t pst = dc.pstream;
         Points bufP[dev::kStateBufs] = {chunkP, chunkP, chunkP, chunkP};
         bufP[1].X = dc.chunk1.p;
         bufP[2].X = dc.chunk2.p;
@@ -1982,10 +1891,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         // Lloyd graphs queued from `chunk` on (each guarded by go: a chunk after
         // one that needs a repair or more rounds does nothing and is relaunched)
         uint64_t queued = 0;
-        static const uint64_t lloyd_depth = [] {  // BM_LLOYD_AHEAD: graphs queued beyond the current one
-            const char* e = std::getenv("BM_LLOYD_AHEAD");
-            return e ? (uint64_t)std::max(0, std::min(2, std::atoi(e))) : (uint64_t)2;
-        }();
+        constexpr uint64_t lloyd_depth = 2;  // graphs queued beyond the current one
         uint64_t ahead = 0;  // chunks after this one whose draws, prep and speculative begin are enqueued
         for (uint64_t chunk = 0;; ++chunk) {
             if (cfg.has_max_chunks && chunk >= cfg.max_chunks) break;  // :71-73
@@ -2069,8 +1975,6 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             chunk_assign_passes += ls.iterations + 1;
             chunk_update_passes += ls.iterations;
             inc_degenerate = ls.inc_degenerate;
-            static const bool iters_log = std::getenv("BM_ITERS") != nullptr;  // diagnostics: Lloyd rounds per chunk
-            if (iters_log) std::fprintf(stderr, "[iters] %llu %llu\n", (unsigned long long)chunk, ls.iterations);
             if (!persist) count_launch(3 + 3 * ls.iterations);
             out->chunks = chunk + 1;
             if (ahead) --ahead;

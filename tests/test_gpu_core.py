@@ -161,32 +161,56 @@ def test_screen_adversarial_bitwise(port, case):
     assert bm.objective(bm.Dataset(X), bm.Centroids(C, mask)) == port.block_sum(d2)
 
 
-@pytest.mark.parametrize("var,alt", [("BM_ASSIGN_MODE", "exact"), ("BM_GRAPHS", "0"),
-                                     ("BM_STORAGE", "native"), ("BM_SCREEN", "v4"),
-                                     ("BM_HAMERLY", "0"), ("BM_FORCE_EXACT_CONTROL", "1"),
-                                     ("BM_SPEC", "0"), ("BM_PDL", "0"), ("BM_PP", "host"),
-                                     ("BM_SUMS", "0"), ("BM_SUMS_FUSE", "0"), ("BM_SPEC_CTAS", "40"),
-                                     ("BM_FINAL", "tma"), ("BM_SUM_CLUSTER", "1")])
-def test_engine_modes_agree(var, alt):
-    """Unscreened assignment (BM_ASSIGN_MODE=exact) and the host-driven chunk
-    loop (BM_GRAPHS=0) give the same bits as the default path, in fresh processes."""
+_MODE_CODE = (
+    "import numpy as np, sys; sys.path.insert(0, '.');"
+    "import paper_2204_07485_b200 as bm;"
+    "X = {X};"
+    "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k={k}, chunk_size={s}, max_chunks=6, seed=3));"
+    "import hashlib; print(repr(o.objective), o.counter.distance_evals, o.counter.iterations,"
+    " hashlib.sha1(o.centroids.values.tobytes()).hexdigest(), repr(t.records))")
+
+
+def _modes_agree(base, var, alt, X="np.rint(np.random.default_rng(5).normal(size=(20000, 16)) * 4)", k=10, s=3000):
     import subprocess, sys, os
-    code = (
-        "import numpy as np, sys; sys.path.insert(0, '.');"
-        "import paper_2204_07485_b200 as bm;"
-        "X = np.rint(np.random.default_rng(5).normal(size=(20000, 16)) * 4);"
-        "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=10, chunk_size=3000, max_chunks=6, seed=3));"
-        "import hashlib; print(repr(o.objective), o.counter.distance_evals, o.counter.iterations,"
-        " hashlib.sha1(o.centroids.values.tobytes()).hexdigest(), repr(t.records))")
-    env = dict(os.environ)
+    code = _MODE_CODE.format(X=X, k=k, s=s)
     outs = []
     for mode in (None, alt):
+        env = dict(os.environ)
+        env.update(base)
         env.pop(var, None)
         if mode is not None:
             env[var] = mode
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                                    text=True, check=True).stdout)
     assert outs[0] == outs[1] and outs[0]
+
+
+# The persistent chunk kernel (default) against the multi-launch chunk graphs
+# and the host-driven loop, the screens against each other, and the
+# deferred-objective / carveout switches: same bits, fresh processes.
+@pytest.mark.parametrize("var,alt", [("BM_PERSIST", "0"), ("BM_GRAPHS", "0"), ("BM_STORAGE", "native"),
+                                     ("BM_FORCE_EXACT_CONTROL", "1"), ("BM_TC", "0"), ("BM_CHUNK_FIX", "0"),
+                                     ("BM_CARVEOUT", "0"), ("BM_PP", "host")])
+def test_engine_modes_agree(var, alt):
+    _modes_agree({}, var, alt)
+
+
+@pytest.mark.parametrize("data", ["int", "real"])
+def test_tc_screen_forced_agrees(data):
+    """Real-valued fp32 rows are not exact in tf32: the default packed-FFMA
+    screen against the tensor-core screen forced on (its loose bound)."""
+    X = ("np.random.default_rng(5).normal(size=(20000, 16)).astype(np.float32)" if data == "real"
+         else "np.rint(np.random.default_rng(5).normal(size=(20000, 16)) * 4)")
+    _modes_agree({}, "BM_TC", "1", X=X)
+
+
+# Switches of the multi-launch chunk graphs (still the path for rows wider
+# than the chunk kernel's instances): each against that path's default.
+@pytest.mark.parametrize("var,alt", [("BM_ASSIGN_MODE", "exact"), ("BM_HAMERLY", "0"), ("BM_SPEC", "0"),
+                                     ("BM_PDL", "0"), ("BM_SUMS", "0"), ("BM_SUMS_FUSE", "0"),
+                                     ("BM_FORCE_EXACT_CONTROL", "1")])
+def test_multi_launch_modes_agree(var, alt):
+    _modes_agree({"BM_PERSIST": "0"}, var, alt)
 
 
 def test_lossless_fp32_storage():
@@ -220,24 +244,10 @@ def test_min_max_normalize(shape, dtype):
     assert (bits(Y) == bits(ref)).all()
 
 
-@pytest.mark.parametrize("var,alt", [("BM_RING", "2"), ("BM_SPEC_CTAS", "24")])
+@pytest.mark.parametrize("var,alt", [("BM_SPEC", "0"), ("BM_HAMERLY", "0")])
 def test_engine_modes_agree_wide_rows(var, alt):
-    """Rows wider than 8 slabs (6-stage TMA ring) against the 2-stage ring, and
-    speculative begins looping over their blocks: same bits, fresh processes."""
-    import subprocess, sys, os
-    code = (
-        "import numpy as np, sys; sys.path.insert(0, '.');"
-        "import paper_2204_07485_b200 as bm;"
-        "X = np.random.default_rng(6).normal(size=(9000, 200)).astype(np.float32);"
-        "o, t = bm.big_means(bm.Dataset(X), bm.BigMeansConfig(k=9, chunk_size=2500, max_chunks=5, seed=2));"
-        "import hashlib; print(repr(o.objective), o.counter.distance_evals, o.counter.iterations,"
-        " hashlib.sha1(o.centroids.values.tobytes()).hexdigest(), repr(t.records))")
-    env = dict(os.environ)
-    outs = []
-    for mode in (None, alt):
-        env.pop(var, None)
-        if mode is not None:
-            env[var] = mode
-        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
-                                   text=True, check=True).stdout)
-    assert outs[0] == outs[1] and outs[0]
+    """Rows wider than the chunk kernel's instances (multi-launch path, 6-stage
+    TMA ring): speculative begins and the bound fast path off, same bits."""
+    _modes_agree({}, var, alt, X="np.random.default_rng(6).normal(size=(9000, 200)).astype(np.float32)", k=9, s=2500)
+
+
