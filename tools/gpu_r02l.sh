@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-2 re-entry check of the current tree: GPU tests, smoke, every config at
+# full size with the reference on the host (parity_full_size + cpu_baseline),
+# the c2 reference arm, the c2 launch list and one ncu --set full per config of
+# the persistent chunk kernel.
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+lscpu > gpurun_out/lscpu.txt 2>&1
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+for c in c1 c2 c3 c4 c5; do
+  timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_c2_ref.json 2> gpurun_out/bench_c2_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+  --log-file gpurun_out/launches_c2.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
+CONFIGS="c1 c2 c3" bash tools/gpu_ncu_chunk.sh
