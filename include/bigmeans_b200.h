@@ -293,12 +293,15 @@ typedef struct bm_profile {
     /* persistent chunk kernel (one launch per chunk; device globaltimer stamps
      * taken inside the timed run itself): summed launch durations, launches,
      * assignment passes (first assignment + one per Lloyd round) and update
-     * passes over the chunk, rows per chunk */
+     * passes over the chunk, rows per chunk, gaps between launches */
     double chunk_ms_total;
     uint64_t chunk_launches;
     uint64_t chunk_assign_passes;
     uint64_t chunk_update_passes;
     uint64_t chunk_rows;
+    /* summed idle time between consecutive chunk kernels (one's end stamp to
+     * the next one's start stamp) */
+    double chunk_gap_ms_total;
 } bm_profile;
 bm_status bm_set_profiling(int enabled);
 /* Debug builds (-DBM_KTRACE): per-CTA phase timestamps of the screened assignment. */

@@ -55,7 +55,7 @@ class bm_profile(C.Structure):
                 ("final_rows", u64), ("screen_candidates", u64), ("screen_rows", u64),
                 ("phase_ms", dbl * 8), ("phase_count", u64 * 8),
                 ("chunk_ms_total", dbl), ("chunk_launches", u64), ("chunk_assign_passes", u64),
-                ("chunk_update_passes", u64), ("chunk_rows", u64)]
+                ("chunk_update_passes", u64), ("chunk_rows", u64), ("chunk_gap_ms_total", dbl)]
 
 
 # name -> (restype, argtypes)

@@ -43,6 +43,7 @@
 
 #include "chunk.h"
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace bm {
 namespace dev {
@@ -98,11 +99,6 @@ __device__ __forceinline__ void bounds2(float2 dot, float2 nxl, float2 nxh, floa
     const float2 Lr = mul2_rd(sub2_rd(sub2_rd(Al, t2), D), make_float2(c.lo64, c.lo64));
     L = make_float2(fmaxf(Lr.x, 0.f), fmaxf(Lr.y, 0.f));
     U = mul2_ru(add2_ru(sub2_ru(Ah, t2), D), make_float2(c.hi64, c.hi64));
-}
-
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
@@ -194,30 +190,35 @@ __device__ __forceinline__ unsigned smem_addr(const void* p) {
 }
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
 // 1024 B apart (SBO), LBO unused (encoded 1), version 1 (sm_100).
-__device__ __forceinline__ unsigned long long umma_desc_sw128(unsigned saddr) {
-    return static_cast<unsigned long long>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
-           (2ull << 61);
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
+// 1024 B apart (SBO), LBO unused (encoded 1), version 1 (sm_100), from the
+// start address in 16-byte units.  The two 32-bit halves are joined in PTX:
+// ptxas (CUDA 12.9) was seen to drop the constant high half of a 64-bit
+// descriptor built as (const | addr) + offset (SBO = 0, no swizzle: garbage
+// MMA results for some code shapes), so no 64-bit arithmetic touches it.
+__device__ __forceinline__ unsigned long long umma_desc_sw128_units(unsigned start_units) {
+    unsigned long long d;
+    asm volatile("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"((start_units & 0x3FFFu) | (1u << 16)),
+                 "r"(64u | (1u << 14) | (2u << 29)));
+    return d;
 }
 // Instruction descriptor: D fp32, A / B tf32, both K-major, N = 32, M = 128.
 constexpr unsigned kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-// Issued by a whole warp with warp-uniform operands; one elected lane issues
-// (operands stay in uniform registers: no per-MMA broadcast loop).
+// Issued by ONE thread (the same thread for every MMA of a round and for
+// their commit: tcgen05.commit tracks only the executing thread's MMAs — with
+// a per-call elect.sync a different lane could commit and the barrier would
+// complete before the MMAs did).
 __device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db, int accumulate) {
     asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
+        "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate));
-}
-// (whole warp; the same elected lane as the MMAs: it tracks that lane's MMAs)
-__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
-            smem_addr(bar))
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate)
         : "memory");
+}
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
 }
 __device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
     asm volatile(
@@ -311,6 +312,13 @@ __host__ __device__ inline int chunk_cdld(int n) {
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Rows per TMA box of the row-major (non tensor-core) layout: the CTA's B rows
+// in the fewest boxes of <= 256 rows, all of one size.
+__host__ __device__ inline int chunk_box_rows(int B) {
+    const int nb = (B + 255) / 256;
+    return ((B + nb - 1) / nb + 7) / 8 * 8;  // a multiple of 8 rows: 128-byte aligned boxes
+}
+
 // Tensor-core layout of the fp32 rows (tc): UMMA K-major, 128-byte swizzle.
 // K-atoms of 32 dims; atom `ka` holds Mpad rows x 128 B (rows 8-grouped into
 // 1024 B core-matrix groups, 16-byte chunks XOR-swizzled by row & 7).
@@ -326,8 +334,8 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
         o += (size_t)tc_katoms(nd) * tc_mpad(B) * 128;
         L.cb = o;
         o += (size_t)2 * tc_katoms(nd) * kCKMax * 128;
-    } else {
-        o = al16(o + (size_t)B * xld * es);
+    } else {  // whole TMA boxes of chunk_box_rows(B) rows
+        o = al16(o + (size_t)chunk_box_rows(B) * ((B + chunk_box_rows(B) - 1) / chunk_box_rows(B)) * xld * es);
         L.cb = o;
     }
     // region U (aliased): screen lower bounds Ls[k][B] (FFMA screen) | member
@@ -359,7 +367,7 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
     o = al16(o + (size_t)B * 8);
     L.red = o;
     o = al16(o + 64 * 8);
-    L.total = o + (tc ? 1024 : 0);  // tc: slack to align the base to 1024 B
+    L.total = o + (tc ? 1024 : 128);  // slack to align the base (tc: 1024 B for the swizzle atoms; TMA boxes: 128 B)
     return L;
 }
 
@@ -398,7 +406,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     const int np = static_cast<int>(min(static_cast<uint64_t>(B), a.rows - p0));
     const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G, TC);
     // tc: operand tiles need a 1024-byte aligned base (128-byte swizzle atoms)
-    unsigned char* sm = TC ? sm_raw + ((1024u - (smem_addr(sm_raw) & 1023u)) & 1023u) : sm_raw;
+    unsigned char* sm = TC ? sm_raw + ((1024u - (smem_addr(sm_raw) & 1023u)) & 1023u)
+                           : sm_raw + ((128u - (smem_addr(sm_raw) & 127u)) & 127u);
     const int cdld = L.cdld;
     const int MP = tc_mpad(B), NKA = tc_katoms(ND);
     const size_t ASZ = static_cast<size_t>(MP) * 128;  // bytes of one K-atom of the rows
@@ -417,6 +426,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     __shared__ int s_any;
     __shared__ unsigned s_tmem;
     __shared__ __align__(8) unsigned long long s_mbar;
+    __shared__ __align__(8) uint64_t s_xbar;  // the rows' TMA boxes
     const float finf = __int_as_float(0x7F800000);
     const double dinf = __longlong_as_double(0x7FF0000000000000LL);
     __shared__ unsigned long long s_chunk;
@@ -463,56 +473,169 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
     };
 
+    int prevKA = 0;  // tc: B operand rows holding values (the rest are 0)
+    // C (global) -> compacted active rows: fp64 (exact recheck) and the screen's
+    // fp32 / tf32 hi+lo copies, then their certified fp32 norms
+    auto load_centroids = [&](int rr) {
+        // the active list from the mask, then the active rows with every load
+        // of a thread in flight at once (U = 4)
+        if (warp == 0) {
+            const bool live = lane < k && !__ldcg(a.mask + lane);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
+            if (live) act[__popc(bal & ((1u << lane) - 1u))] = lane;
+            if (lane == 0) act[kCKMax] = __popc(bal);
+        }
+        __syncthreads();
+        const int KA = act[kCKMax];
+        if constexpr (TC) {
+            unsigned char* cbhi = sm + L.cb;
+            unsigned char* cblo = cbhi + static_cast<size_t>(NKA) * kCKMax * 128;
+            auto boff = [&](int rk, int d) -> size_t {
+                return static_cast<size_t>(d >> 5) * (kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
+                       (d & 3) * 4;
+            };
+            batched_copy<4>(
+                KA * n, tid, NT,
+                [&](int e) {
+                    const int rk = e / n;
+                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+                },
+                [&](int e, double v) {
+                    const int rk = e / n, d = e - rk * n;
+                    cd[rk * cdld + d] = v;
+                    const float f = __double2float_rn(v), hi = tf32_rna(f);
+                    const size_t off = boff(rk, d);
+                    *reinterpret_cast<float*>(cbhi + off) = hi;
+                    *reinterpret_cast<float*>(cblo + off) = f - hi;
+                });
+            for (int e = KA * n + tid; e < prevKA * n; e += NT) {
+                const int rk = e / n, d = e - rk * n;
+                const size_t off = boff(rk, d);
+                *reinterpret_cast<float*>(cbhi + off) = 0.f;
+                *reinterpret_cast<float*>(cblo + off) = 0.f;
+            }
+            prevKA = KA;
+            fence_proxy_async_smem();
+        } else {
+            batched_copy<4>(
+                KA * n, tid, NT,
+                [&](int e) {
+                    const int rk = e / n;
+                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+                },
+                [&](int e, double v) {
+                    const int rk = e / n, d = e - rk * n;
+                    cd[rk * cdld + d] = v;
+                    cf[rk * ND + d] = __double2float_rn(v);
+                });
+        }
+        __syncthreads();
+        for (int rk = warp; rk < KA; rk += NW) {
+            float lo = 0.f, hi = 0.f;
+            for (int d = lane; d < n; d += 32) {
+                const float f = TC ? __double2float_rn(cd[rk * cdld + d]) : cf[rk * ND + d];
+                lo = __fmaf_rd(f, f, lo);
+                hi = __fmaf_ru(f, f, hi);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = __fadd_rd(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+                hi = __fadd_ru(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+            }
+            if (lane == 0) {
+                const bool ok = hi <= 1.0e36f;  // beyond: (0, inf, inf), see bounds2
+                ncl[rk] = ok ? lo : 0.f;
+                nch[rk] = ok ? hi : finf;
+                ncr[rk] = ok ? __fsqrt_ru(hi) : finf;
+            }
+        }
+        CDBG(rr, 15);
+    };
     // ---- the chunk's rows -> shared memory (once for all rounds) ----
     int xinexact = 0;  // tc: some row value is not exactly a tf32 (looser screen bound)
     {
-        const int vpr = static_cast<int>((static_cast<size_t>(n) * sizeof(T) + 15) / 16);  // 16-byte vectors per row
-        const unsigned char* src = static_cast<const unsigned char*>(a.X) + p0 * a.ld * sizeof(T);
-        for (int v = tid; v < np * vpr; v += NT) {
-            const int p = v / vpr, q = v - p * vpr;
-            cpa16(xchunk(p, q), src + static_cast<size_t>(p) * a.ld * sizeof(T) + q * 16);
+        // TMA boxes of the chunk's rows, completion on s_xbar (one thread issues)
+        if (tid == 0) {
+            mbar_init(&s_xbar, 1);
+            fence_mbar_init();
+            tma_prefetch_map(&a.xmap);
+            if constexpr (TC) {
+                const int ntl = MP / 128;
+                mbar_expect_tx(&s_xbar, static_cast<unsigned>(ntl * NKA * 16384));
+                for (int t = 0; t < ntl; ++t)
+                    for (int ka = 0; ka < NKA; ++ka)
+                        tma_load_2d(sm + L.xs + static_cast<size_t>(ka) * ASZ + static_cast<size_t>(t) * 16384, &a.xmap,
+                                    &s_xbar, ka * 32, static_cast<int>(p0) + 128 * t);
+            } else {
+                const int RB = chunk_box_rows(B), nb = (B + RB - 1) / RB;
+                mbar_expect_tx(&s_xbar, static_cast<unsigned>(nb * RB * xld * sizeof(T)));
+                for (int i = 0; i < nb; ++i)
+                    tma_load_2d(sm + L.xs + static_cast<size_t>(i) * RB * xld * sizeof(T), &a.xmap, &s_xbar, 0,
+                                static_cast<int>(p0) + RB * i);
+            }
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        // while the rows are in flight: the round-0 centroids (start of the chunk)
         if constexpr (!TC) {
             for (int e = tid; e < kCKMax * ND; e += NT) cf[e] = 0.f;  // padding rows / dims stay 0
+        } else {
+            for (int e = tid; e < NKA * kCKMax * 8 * 2; e += NT)  // the B operands start at 0
+                reinterpret_cast<float4*>(sm + L.cb)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
-        if constexpr (TC) {
-            // zero the padding the MMA reads (dims n..ND-1, rows np..MP-1), check tf32 exactness,
-            // make the rows visible to the tensor core (async proxy); TMEM for the accumulators
-            // every 16-byte chunk of every K-atom row (the tensor core reads whole
-            // atoms): zeros past n and in rows np..MP-1; tf32 exactness of the
-            // data (a warp per row, a lane per chunk); the B operands start at 0
-            constexpr int QC = (ND + 31) / 32 * 8;
-            static_assert(QC <= 32, "a lane per 16-byte chunk");
-            const int vq = n >> 2;  // chunks holding 4 data values
-            const int zq = (n + 3) >> 2;  // first chunk holding no data value
-            // rows < np: the data chunks (exactness check, the partial chunk's
-            // tail zeroed) and chunks zq..QC-1; rows np..MP-1: every chunk
-            const int per_row = QC - vq;  // chunks of a row touched below (data chunks are read for the check)
-            for (int e = tid; e < np * QC; e += NT) {
-                const int p = e / QC, q = e - p * QC;
-                float4* x = reinterpret_cast<float4*>(xchunk(p, q));
-                if (q >= zq) {
-                    *x = make_float4(0.f, 0.f, 0.f, 0.f);
-                } else {
-                    float4 v = *x;
-                    if (q == vq) {  // the partial chunk: dims n..4q+3 -> 0
-                        if ((n & 3) < 2) v.y = 0.f;
-                        if ((n & 3) < 3) v.z = 0.f;
-                        v.w = 0.f;
-                        *x = v;
+        load_centroids(0);
+        mbar_wait(&s_xbar, 0);
+        CDBG(0, 13);
+#ifdef BM_CHUNK_MMA_DIAG
+        if (a.dbg_mma && a.dbg && TC) {  // diagnostics: the landed rows against global memory
+            unsigned bad = 0;
+            for (int e = tid; e < np * 32 * NKA; e += NT) {
+                const int pp = e / (32 * NKA), d = e % (32 * NKA);
+                const T want = d < n ? static_cast<const T*>(a.X)[(p0 + pp) * a.ld + d] : T(0);
+                const T got = reinterpret_cast<const T*>(xchunk(pp, d / EPC))[d % EPC];
+                if (!(got == want)) {
+                    ++bad;
+                    unsigned long long* sl = &a.dbg[(1 * 8 + 7) * 16];
+                    if (cta == 0 && atomicCAS(sl, 0ull, 1ull) == 0ull) {
+                        sl[1] = pp;
+                        sl[2] = d;
+                        sl[3] = __double_as_longlong(static_cast<double>(got));
+                        sl[4] = __double_as_longlong(static_cast<double>(want));
                     }
+                }
+            }
+            if (bad) atomicAdd(&a.dbg[(2 * 8 + 7) * 16 + 15], static_cast<unsigned long long>(bad));
+            // the B operands (hi / lo parts of the compacted fp32 centroids, zero elsewhere)
+            unsigned bbad = 0;
+            const int KA0 = act[kCKMax];
+            for (int e = tid; e < 2 * 32 * 32 * NKA; e += NT) {
+                const int part = e / (32 * 32 * NKA), rem = e % (32 * 32 * NKA), rk = rem / (32 * NKA), d = rem % (32 * NKA);
+                float want = 0.f;
+                if (rk < KA0 && d < n) {
+                    const float f = __double2float_rn(cd[rk * cdld + d]), hi = tf32_rna(f);
+                    want = part ? f - hi : hi;
+                }
+                const size_t off = static_cast<size_t>(d >> 5) * (kCKMax * 128) + rk * 128 +
+                                   ((((d >> 2) & 7) ^ (rk & 7)) << 4) + (d & 3) * 4 +
+                                   (part ? static_cast<size_t>(NKA) * kCKMax * 128 : 0);
+                const float got = *reinterpret_cast<const float*>(sm + L.cb + off);
+                if (!(got == want)) ++bbad;
+            }
+            if (bbad) atomicAdd(&a.dbg[(3 * 8 + 7) * 16 + 15], static_cast<unsigned long long>(bbad));
+        }
+#endif
+        if constexpr (TC) {
+            // the MMA reads whole atoms: TMA zero-filled dims n..ND-1 and rows past
+            // the chunk (rows np..MP-1 of an inner CTA hold the next CTA's rows:
+            // finite, and their dot products are never read).  tf32 exactness of
+            // this CTA's values unless the dataset is known to be exact
+            if (!a.rows_tf32_exact) {
+                const int zq = (n + 3) >> 2;  // 16-byte chunks holding data values
+                for (int e = tid; e < np * zq; e += NT) {
+                    const float4 v = *reinterpret_cast<const float4*>(xchunk(e / zq, e % zq));
                     xinexact |= ((__float_as_uint(v.x) | __float_as_uint(v.y) | __float_as_uint(v.z) |
                                   __float_as_uint(v.w)) & 0x1FFFu) != 0u;
                 }
             }
-            (void)per_row;
-            for (int e = np * QC + tid; e < MP * QC; e += NT)
-                *reinterpret_cast<float4*>(xchunk(e / QC, e % QC)) = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int e = tid; e < NKA * kCKMax * 8 * 2; e += NT)
-                reinterpret_cast<float4*>(sm + L.cb)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
             xinexact = __syncthreads_or(xinexact);
             fence_proxy_async_smem();
             if (warp == 0) {
@@ -533,7 +656,6 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     }
     const ScreenConsts cst = TC && xinexact ? a.cst_loose : a.cst;
     unsigned mma_phase = 0;
-    int prevKA = 0;  // tc: B operand rows holding values (the rest are 0)
     // this thread's points: p = tid + i*NT; fp32 rows in registers, norms (rd/ru)
     // PPT == 2: xp[d] = (x_p0[d], x_p1[d]) (point pairs share every centroid
     // load); PPT == 1: xp[h] = (x[2h], x[2h+1]) (dimension pairs).  Norms as
@@ -628,108 +750,32 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         CDBG(rr, 0);
         const int slot = static_cast<int>(r & 1);
         // ---- centroids: C (global) -> compacted fp64 / fp32 rows + norms ----
-        if (warp == 0) {
-            const bool live = lane < k && !__ldcg(a.mask + lane);
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
-            if (live) act[__popc(bal & ((1u << lane) - 1u))] = lane;
-            if (lane == 0) act[kCKMax] = __popc(bal);
-        }
-        __syncthreads();
+        // (round 0: loaded while the rows were in flight)
+        if (r > 0) load_centroids(rr);
         const int KA = act[kCKMax];
-        // compacted fp64 / fp32 copies (all threads: one L2 round trip), then
-        // the fp32 norms, a warp per row (warp sums rounded down / up: any
-        // order bounds the exact value)
         if constexpr (TC) {
-            // the B operands: fl32(c) = hi + lo, hi = tf32(c) (round to nearest),
-            // lo = fl32(c) - hi (exact), rows = compacted active centroids; the
-            // rest stays 0 (zeroed at the start; rows that became inactive are
-            // cleared here)
-            unsigned char* cbhi = sm + L.cb;
-            unsigned char* cblo = cbhi + static_cast<size_t>(NKA) * kCKMax * 128;
-            auto boff = [&](int rk, int d) -> size_t {
-                return static_cast<size_t>(d >> 5) * (kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
-                       (d & 3) * 4;
-            };
-            batched_copy<4>(
-                KA * n, tid, NT,
-                [&](int e) {
-                    const int rk = e / n;
-                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
-                },
-                [&](int e, double v) {
-                    const int rk = e / n, d = e - rk * n;
-                    cd[rk * cdld + d] = v;
-                    const float f = __double2float_rn(v), hi = tf32_rna(f);
-                    const size_t off = boff(rk, d);
-                    *reinterpret_cast<float*>(cbhi + off) = hi;
-                    *reinterpret_cast<float*>(cblo + off) = f - hi;
-                });
-            for (int e = KA * n + tid; e < prevKA * n; e += NT) {
-                const int rk = e / n, d = e - rk * n;
-                const size_t off = boff(rk, d);
-                *reinterpret_cast<float*>(cbhi + off) = 0.f;
-                *reinterpret_cast<float*>(cblo + off) = 0.f;
-            }
-            prevKA = KA;
-            fence_proxy_async_smem();
-        } else {
-            batched_copy<4>(
-                KA * n, tid, NT,
-                [&](int e) {
-                    const int rk = e / n;
-                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
-                },
-                [&](int e, double v) {
-                    const int rk = e / n, d = e - rk * n;
-                    cd[rk * cdld + d] = v;
-                    cf[rk * ND + d] = __double2float_rn(v);
-                });
-        }
-        __syncthreads();
-        for (int rk = warp; rk < KA; rk += NW) {
-            float lo = 0.f, hi = 0.f;
-            for (int d = lane; d < n; d += 32) {
-                const float f = TC ? __double2float_rn(cd[rk * cdld + d]) : cf[rk * ND + d];
-                lo = __fmaf_rd(f, f, lo);
-                hi = __fmaf_ru(f, f, hi);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                lo = __fadd_rd(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
-                hi = __fadd_ru(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
-            }
-            if (lane == 0) {
-                const bool ok = hi <= 1.0e36f;  // beyond: (0, inf, inf), see bounds2
-                ncl[rk] = ok ? lo : 0.f;
-                nch[rk] = ok ? hi : finf;
-                ncr[rk] = ok ? __fsqrt_ru(hi) : finf;
-            }
-        }
-        CDBG(rr, 15);
-        if constexpr (TC) {
-            // warp 0 issues the tile MMAs (one elected lane): D[tile] = rows . (hi + lo)^T over K
-            if (warp == 0) {
+            // thread 0 issues the tile MMAs and their commit: D[tile] = rows . (hi + lo)^T over K
+            if (tid == 0) {
                 tc_fence_after();
-                // descriptors advance through their 14-bit start-address field
-                // (units of 16 B); k-steps outer, tiles inner: consecutive MMAs
-                // feed different accumulators
-                const unsigned long long da0 = umma_desc_sw128(smem_addr(sm + L.xs));
-                const unsigned long long dbh = umma_desc_sw128(smem_addr(sm + L.cb));
-                const unsigned long long dbl = dbh + ((static_cast<unsigned long long>(NKA) * kCKMax * 128) >> 4);
+                // descriptors from their 14-bit start-address field (units of
+                // 16 B); k-steps outer, tiles inner: consecutive MMAs feed
+                // different accumulators
+                const unsigned ua0 = smem_addr(sm + L.xs) >> 4;  // start addresses, 16-byte units
+                const unsigned ubh = smem_addr(sm + L.cb) >> 4;
+                const unsigned ubl = ubh + ((NKA * kCKMax * 128) >> 4);
                 const int ntl = MP / 128;
-                // k-steps of 8 dims; a narrow row (ND < 32) still runs its whole
-                // first K-atom: measured wrong with only 1-2 k-steps into the
-                // first swizzle atom (ND 8 / 16), right with >= 3 and with full
-                // atoms followed by a partial one (ND 40 ... 88); padding is zero
-                constexpr int KSTEPS = ND < 32 ? 4 : ND / 8;
+                // k-steps of 8 dims (dims n..ND-1 are zero in both operands)
+                constexpr int KSTEPS = ND / 8;
                 for (int ks = 0; ks < KSTEPS; ++ks) {
-                    const unsigned long long ko = ((ks & 3) * 32) >> 4;
-                    const unsigned long long bo = ((static_cast<unsigned long long>(ks >> 2) * kCKMax * 128) >> 4) + ko;
-                    const unsigned long long ao = ((static_cast<unsigned long long>(ks >> 2) * ASZ) >> 4) + ko;
+                    const unsigned ko = ((ks & 3) * 32) >> 4;
+                    const unsigned bo = (((ks >> 2) * kCKMax * 128) >> 4) + ko;
+                    const unsigned ao = static_cast<unsigned>((static_cast<size_t>(ks >> 2) * ASZ) >> 4) + ko;
+                    const unsigned long long dbh = umma_desc_sw128_units(ubh + bo);
+                    const unsigned long long dbl = umma_desc_sw128_units(ubl + bo);
                     for (int t = 0; t < ntl; ++t) {
-                        const unsigned long long da = da0 + ao + static_cast<unsigned long long>(t) * (16384 >> 4);
-                        umma_tf32(s_tmem + 32u * t, da, dbh + bo, ks > 0);
-                        umma_tf32(s_tmem + 32u * t, da, dbl + bo, 1);
+                        const unsigned long long da = umma_desc_sw128_units(ua0 + ao + static_cast<unsigned>(t) * (16384 >> 4));
+                        umma_tf32(s_tmem + 32u * t, da, dbh, ks > 0);
+                        umma_tf32(s_tmem + 32u * t, da, dbl, 1);
                     }
                 }
                 umma_commit(&s_mbar);
@@ -769,6 +815,17 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                         const double den = sqrt(static_cast<double>(i ? nxh2.y : nxh2.x)) * sqrt(static_cast<double>(nch[j]));
                         if (den > 0) worst = fmaxf(worst, static_cast<float>(fabs(static_cast<double>(Lv[j]) - ex) / den));
                         if (a.dbg && !(fabs(static_cast<double>(Lv[j]) - ex) <= 1e-2 * den + 1e-30)) {
+                            // theories: the row the MMA result belongs to
+                            auto dotq = [&](int q) {
+                                double e2 = 0.0;
+                                for (int d = 0; d < n; ++d)
+                                    e2 += static_cast<double>(xat(q, d)) * static_cast<double>(__double2float_rn(cd[j * cdld + d]));
+                                return e2;
+                            };
+                            const int qa = (p & ~127) + (p & 31), qb = (p & ~127) + (p & 7);
+                            const bool ma = fabs(dotq(qa) - Lv[j]) <= 1e-3 * (fabs(Lv[j]) + 1.0);
+                            const bool mb = fabs(dotq(qb) - Lv[j]) <= 1e-3 * (fabs(Lv[j]) + 1.0);
+                            atomicAdd(&a.dbg[(1 * 8 + 5) * 16 + (ma ? 1 : 0) + (mb ? 2 : 0)], 1ull);
                             if (r == 0) atomicAdd(&a.dbg[(0 * 8 + 5) * 16 + (p >> 7)], 1ull);
                             if (r == 0) atomicAdd(&a.dbg[(0 * 8 + 5) * 16 + 8 + (p & 7)], 1ull);
                             unsigned long long* slot = &a.dbg[((s_chunk & 3ull) * 8 + 6) * 16];
@@ -780,6 +837,30 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                                 slot[5] = __double_as_longlong(ex);
                                 slot[6] = static_cast<unsigned long long>(KA);
                                 slot[7] = static_cast<unsigned long long>(np);
+                                // which row's dot product did the MMA return? (first match)
+                                slot[8] = 0xFFFFFFFFull;
+                                for (int q = 0; q < np; ++q) {
+                                    double ex2 = 0.0;
+                                    for (int d = 0; d < n; ++d)
+                                        ex2 += static_cast<double>(xat(q, d)) * static_cast<double>(__double2float_rn(cd[j * cdld + d]));
+                                    if (fabs(ex2 - static_cast<double>(Lv[j])) <= 1e-3 * (fabs(ex2) + 1.0)) {
+                                        slot[8] = static_cast<unsigned long long>(q);
+                                        break;
+                                    }
+                                }
+                                // and with which centroid of the same row?
+                                slot[9] = 0xFFFFFFFFull;
+                                for (int jj = 0; jj < KA; ++jj) {
+                                    double ex2 = 0.0;
+                                    for (int d = 0; d < n; ++d)
+                                        ex2 += static_cast<double>(xat(p, d)) * static_cast<double>(__double2float_rn(cd[jj * cdld + d]));
+                                    if (fabs(ex2 - static_cast<double>(Lv[j])) <= 1e-3 * (fabs(ex2) + 1.0)) {
+                                        slot[9] = static_cast<unsigned long long>(jj);
+                                        break;
+                                    }
+                                }
+                                slot[10] = static_cast<unsigned long long>(__float_as_uint(Lv[(j + 1) & 31]));
+                                slot[11] = static_cast<unsigned long long>(__float_as_uint(Lv[(j + 2) & 31]));
                             }
                         }
                     }
@@ -1576,6 +1657,23 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
     p.grid = grid;
     p.smem = L.total;
     return p;
+}
+
+CUtensorMap chunk_rows_map(const ChunkPlan& p, bm_dtype storage, const void* X, uint64_t rows, int n, uint64_t ld) {
+    CUtensorMap m{};
+    auto enc = tmap_encoder();
+    if (!enc) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    const size_t es = storage == BM_F64 ? 8 : 4;
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+    const cuuint32_t box[2] = {p.tc ? 32u : (cuuint32_t)p.xld, p.tc ? 128u : (cuuint32_t)dev::chunk_box_rows(p.B)};
+    const cuuint32_t estr[2] = {1, 1};
+    const auto dt = es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const auto sw = p.tc ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    if (enc(&m, dt, 2, const_cast<void*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled(chunk rows) failed");
+    return m;
 }
 
 void chunk_fix_prefer_max_smem() {

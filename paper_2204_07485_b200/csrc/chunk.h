@@ -5,6 +5,7 @@
 // in shared memory across all rounds.  Host-visible plan + launch entry.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -30,6 +31,12 @@ struct FixJob {
 
 // Everything one chunk launch reads and writes (pointers into the Workspace).
 struct ChunkArgs {
+    // tensor map of the gathered chunk (2-D [rows][n], stride ld): the rows
+    // land in shared memory by TMA — tensor-core screen: 32-dim x 128-row
+    // boxes in the UMMA K-major 128-byte-swizzle layout; otherwise xld-wide x
+    // chunk_box_rows(B)-row boxes, row-major (dims n..xld-1 and rows past the
+    // chunk zero-filled)
+    CUtensorMap xmap;
     const void* X;            // the gathered chunk: rows x ld, storage T
     uint64_t rows;            // s
     int n;
@@ -38,6 +45,7 @@ struct ChunkArgs {
     int B;                    // points per CTA (ordered mode: 1024 = one reduction tile)
     int xld;                  // shared-memory row stride (elements)
     int ordered;              // 1: real-valued data, CTA = 1024-tile, tile-order merge; 0: exact sums
+    int rows_tf32_exact;      // every dataset value is exactly a tf32 (no per-CTA check needed)
     double* C;                // working centroids k x n (the start; then every update)
     uint8_t* mask;            // their degenerate mask
     double* part;             // update partials [G][k*n] (CTA g's fold of label j, dim d)
@@ -95,6 +103,8 @@ struct ChunkPlan {
 };
 
 ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc);
+// The row tensor map of one gathered chunk buffer for a plan.
+CUtensorMap chunk_rows_map(const ChunkPlan& p, bm_dtype storage, const void* X, uint64_t rows, int n, uint64_t ld);
 // Enqueue one chunk (cooperative launch, capturable into a graph).
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a);
 // k_chunk_fix prefers the maximum shared-memory carveout (current device).

@@ -193,6 +193,14 @@ struct Workspace {
     DevBuf<unsigned> cpcnt, cbar;
     DevBuf<int> crchg;
     DevBuf<unsigned long long> ctiming;
+    struct ChunkMap {  // tensor map of chunk buffer i's rows for the current plan
+        const void* X = nullptr;
+        uint64_t rows = 0, ld = 0;
+        int B = 0, xld = 0, n = 0;
+        bool tc = false;
+        bm_dtype dtype = BM_F64;
+        CUtensorMap map{};
+    } cmaps[dev::kStateBufs];
     DevBuf<dev::FixJob> cjob;              // [kStateBufs] deferred exact objectives
     DevBuf<unsigned long long> cfix_seq;   // chunks whose exact objective is final
     DevBuf<double> cfix_tiles;
@@ -1820,6 +1828,23 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             cudaEvent_t e0 = tl_ev(st);
             if (persist) {
                 dev::ChunkArgs a{};
+                {  // the rows' tensor map of this chunk buffer (re-encoded when the buffer or plan changes)
+                    auto& cm = w.cmaps[i];
+                    if (cm.X != bufP[i].X || cm.rows != s || cm.B != cplan.B || cm.tc != cplan.tc || cm.xld != cplan.xld ||
+                        cm.n != n || cm.ld != d->ld || cm.dtype != d->dtype) {
+                        cm.map = chunk_rows_map(cplan, d->dtype, bufP[i].X, s, n, d->ld);
+                        cm.X = bufP[i].X;
+                        cm.rows = s;
+                        cm.B = cplan.B;
+                        cm.tc = cplan.tc;
+                        cm.xld = cplan.xld;
+                        cm.n = n;
+                        cm.ld = d->ld;
+                        cm.dtype = d->dtype;
+                    }
+                    a.xmap = cm.map;
+                }
+                a.rows_tf32_exact = d->tf32_exact ? 1 : 0;
                 a.X = bufP[i].X;
                 a.rows = s;
                 a.n = n;
@@ -2137,8 +2162,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         std::vector<unsigned long long> tm(2 * nc);
         BM_CUDA(cudaMemcpy(tm.data(), w.ctiming.p, tm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         double ns = 0.0;
+        double gap = 0.0;
         for (uint64_t c = 0; c < nc; ++c) ns += (double)(tm[2 * c + 1] - tm[2 * c]);
+        for (uint64_t c = 1; c < nc; ++c)
+            if (tm[2 * c] > tm[2 * c - 1]) gap += (double)(tm[2 * c] - tm[2 * c - 1]);
         g_profile.chunk_ms_total = ns * 1e-6;
+        g_profile.chunk_gap_ms_total = gap * 1e-6;
         g_profile.chunk_launches = nc;
         g_profile.chunk_assign_passes = chunk_assign_passes;
         g_profile.chunk_update_passes = chunk_update_passes;

@@ -18,7 +18,7 @@ for rep in range(3):
     p = bm.last_profile()
     n = max(p["chunk_launches"], 1)
     print(f"{key} rep{rep}: cpu_init {out.counter.cpu_init*1e3:.2f} ms, final {out.counter.cpu_full*1e3:.2f} ms, "
-          f"chunk kernels {p['chunk_launches']} avg {p['chunk_ms_total']/n*1e3:.1f} us, "
+          f"chunk kernels {p['chunk_launches']} avg {p['chunk_ms_total']/n*1e3:.1f} us, gap avg {p['chunk_gap_ms_total']/max(n-1,1)*1e3:.1f} us, "
           f"assign passes/chunk {p['chunk_assign_passes']/n:.2f}, iters {out.counter.iterations}", flush=True)
 
 if os.environ.get("BM_CHUNK_DBG"):
@@ -47,6 +47,6 @@ if os.environ.get("BM_CHUNK_DBG"):
                 segs.append(f"[sort {(row[12]-row[3])/1e3:.1f} fold {(row[4]-row[12])/1e3:.1f}]")
             print(f"  r{r} @{(row[0]-t0)/1e3:.1f}us: " + " | ".join(segs))
         tail = buf[c, 7]
-        print(f"  rows->smem {(buf[c,0,0]-tail[13])/1e3:.1f} us; max MMA dot error / (|x||c|) "
+        print(f"  prologue {(buf[c,0,0]-tail[13])/1e3:.1f} us (rows landed at {(buf[c,0,13]-tail[13])/1e3:.1f}); max MMA dot error / (|x||c|) "
               f"{np.array([tail[14] & 0xFFFFFFFF], np.uint32).view(np.float32)[0]:.3g}")
         print(f"  tail: loop-end @{(tail[9]-t0)/1e3:.1f} fold {(tail[10]-tail[9])/1e3:.1f} bar {(tail[11]-tail[10])/1e3:.1f} accept {(tail[12]-tail[11])/1e3:.1f}")
