@@ -309,6 +309,9 @@ bm_status bm_debug_ktrace(uint64_t* out, uint64_t count);
 /* Debug (BM_CHUNK_DBG=1): phase stamps of the persistent chunk kernel,
  * [chunk % 4][round 0..6, 7 = tail][16] globaltimer ns. */
 bm_status bm_debug_chunk_phases(uint64_t* out);
+/* Debug builds (-DBM_WIDE_DBG, BM_WIDE_DBG=1): k_wide_screen CTA (0,0)'s per-atom
+ * globaltimer stamps [4][64]: TMA issued, data landed, MMAs issued, stage retired. */
+bm_status bm_debug_wide_stamps(uint64_t* out);
 bm_status bm_last_profile(bm_profile* out);
 
 #ifdef __cplusplus

@@ -107,6 +107,7 @@ PROTOS = {
     "bm_debug_ktrace": (C.c_int, [P_u64, u64]),
     "bm_last_profile": (C.c_int, [C.POINTER(bm_profile)]),
     "bm_debug_chunk_phases": (C.c_int, [P_u64]),
+    "bm_debug_wide_stamps": (C.c_int, [P_u64]),
 }
 
 _lib = None

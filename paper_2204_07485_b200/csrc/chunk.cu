@@ -44,6 +44,7 @@
 #include "chunk.h"
 #include "common.cuh"
 #include "tma.cuh"
+#include "umma.cuh"
 
 namespace bm {
 namespace dev {
@@ -184,76 +185,20 @@ __device__ __forceinline__ double exact_dist(const T* __restrict__ x, const doub
     return s;
 }
 
-// ---- tcgen05 / TMEM / mbarrier helpers (tensor-core screen, fp32 rows) ----
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+// ---- tcgen05 / TMEM helpers (umma.cuh) under the names used below ----
+using umma::smem_addr;
+using umma::mbar_wait_parity;
+using umma::tf32_rna;
+using umma::tmem_ld32;
+__device__ __forceinline__ unsigned long long umma_desc_sw128_units(unsigned u) { return umma::desc_sw128(u); }
+constexpr unsigned kTcIdesc = umma::idesc_tf32<32>();
+__device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db, int acc) {
+    umma::mma_tf32(tmem_d, da, db, kTcIdesc, acc);
 }
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
-// 1024 B apart (SBO), LBO unused (encoded 1), version 1 (sm_100).
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
-// 1024 B apart (SBO), LBO unused (encoded 1), version 1 (sm_100), from the
-// start address in 16-byte units.  The two 32-bit halves are joined in PTX:
-// ptxas (CUDA 12.9) was seen to drop the constant high half of a 64-bit
-// descriptor built as (const | addr) + offset (SBO = 0, no swizzle: garbage
-// MMA results for some code shapes), so no 64-bit arithmetic touches it.
-__device__ __forceinline__ unsigned long long umma_desc_sw128_units(unsigned start_units) {
-    unsigned long long d;
-    asm volatile("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"((start_units & 0x3FFFu) | (1u << 16)),
-                 "r"(64u | (1u << 14) | (2u << 29)));
-    return d;
-}
-// Instruction descriptor: D fp32, A / B tf32, both K-major, N = 32, M = 128.
-constexpr unsigned kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-// Issued by ONE thread (the same thread for every MMA of a round and for
-// their commit: tcgen05.commit tracks only the executing thread's MMAs — with
-// a per-call elect.sync a different lane could commit and the barrier would
-// complete before the MMAs did).
-__device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db, int accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(kTcIdesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ float tf32_rna(float x) {
-    unsigned r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-// 32 consecutive TMEM columns of this thread's lane (row) -> registers.
-__device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
-    unsigned r[32];
-    // the load and its wait in ONE asm statement: the outputs must not be read
-    // (moved or spilled by the compiler) before tcgen05.wait::ld completes
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
-        "tcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr)
-        : "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) { umma::commit(bar); }
+__device__ __forceinline__ void tc_fence_before() { umma::fence_before(); }
+__device__ __forceinline__ void tc_fence_after() { umma::fence_after(); }
+__device__ __forceinline__ void fence_proxy_async_smem() { umma::fence_proxy_async_smem(); }
 
 // Global -> shared copies with U loads in flight per thread (a plain
 // load-then-store loop would wait one L2 round trip per element).

@@ -32,6 +32,7 @@
 
 #include "bigmeans_b200.h"
 #include "chunk.h"
+#include "wide.h"
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
@@ -109,6 +110,7 @@ struct Points {
     uint64_t rows;
     int n;
     uint64_t ld;
+    bool tf32_exact = false;  // every value exactly a tf32 (wide rows: tensor-core pre-screen)
 };
 
 template <class F>
@@ -193,6 +195,21 @@ struct Workspace {
     DevBuf<unsigned> cpcnt, cbar;
     DevBuf<int> crchg;
     DevBuf<unsigned long long> ctiming;
+    // wide rows (wide.cu): split-K partial dot products / norms per pool slot
+    // (0..3: graph chunk buffers, 4: other calls, 5: the final pass), allocated
+    // before any graph capture (ensure_wide)
+    struct WideSlot {
+        DevBuf<float> dot, nx, nc, bops;
+        DevBuf<double> best;
+        DevBuf<int> bj;
+        const void* X = nullptr;
+        uint64_t rows = 0, ld = 0;
+        int n = 0;
+        CUtensorMap map{}, map32{};  // the rows: 128-row boxes (screen), 32-row boxes (recheck)
+        const double* C = nullptr;   // the centroid map's source
+        int ck = 0, cn = 0, cld = 0, cnp = 0;
+        CUtensorMap cmap{};
+    } wide[6];
     struct ChunkMap {  // tensor map of chunk buffer i's rows for the current plan
         const void* X = nullptr;
         uint64_t rows = 0, ld = 0;
@@ -510,7 +527,7 @@ cudaStream_t stream_of(const bm_dataset* d) { return cache_of(d->device).stream;
 namespace bm {
 namespace {
 
-Points dataset_points(const bm_dataset* d) { return Points{d->X, d->dtype, d->m, (int)d->n, d->ld}; }
+Points dataset_points(const bm_dataset* d) { return Points{d->X, d->dtype, d->m, (int)d->n, d->ld, d->tf32_exact}; }
 
 Workspace& get_ws(const bm_dataset* d, uint64_t rows, int k, int ncand, uint64_t hist) {
     DeviceCache& c = cache_of(d->device);
@@ -781,6 +798,55 @@ struct AssignSrc {
     float* lbk;
 };
 
+// Diagnostics (library built with -DBM_WIDE_DBG, BM_WIDE_DBG=1): k_wide_screen
+// CTA (0,0)'s per-atom stamps [4][64] (TMA issue, data landed, MMAs issued, retired).
+unsigned long long* wide_dbg_buffer() {
+    static unsigned long long* p = nullptr;
+    if (!p && std::getenv("BM_WIDE_DBG")) {
+        BM_CUDA(cudaMalloc(&p, 4 * 64 * sizeof(unsigned long long)));
+        BM_CUDA(cudaMemset(p, 0, 4 * 64 * sizeof(unsigned long long)));
+    }
+    return p;
+}
+
+// BM_WIDE=0: wide rows keep k_assign_tma's own slab screen (A/B checks).
+bool wide_enabled() {
+    const char* e = std::getenv("BM_WIDE");
+    return !(e && std::string(e) == "0");
+}
+
+// The tensor-core pre-screen applies to fp32 rows exact in tf32 that are too
+// wide for the persistent chunk kernel (wide.cu).
+bool use_wide(const Points& P, int k) {
+    return wide_enabled() && P.dtype == BM_F32 && P.tf32_exact && P.n > 88 && k >= 1 && k <= 32 &&
+           P.rows < (1ull << 31);
+}
+
+int current_device() {
+    int d = 0;
+    BM_CUDA(cudaGetDevice(&d));
+    return d;
+}
+
+// Pool slot sized for `rows` (never during a capture: graphs are captured after ensure_wide).
+void ensure_wide_slot(Workspace::WideSlot& ws, const WidePlan& wp) {
+    if (ws.dot.n < wp.dot_floats()) ws.dot.alloc(wp.dot_floats());
+    if (ws.nx.n < wp.nx_floats()) ws.nx.alloc(wp.nx_floats());
+    if (ws.nc.n < wp.nc_floats()) ws.nc.alloc(wp.nc_floats());
+    if (ws.bops.n < wp.bops_floats()) ws.bops.alloc(wp.bops_floats());
+    const size_t rows = static_cast<size_t>(wp.tiles) * 128;
+    if (ws.best.n < rows) ws.best.alloc(rows);
+    if (ws.bj.n < rows) ws.bj.alloc(rows);
+}
+
+void ensure_wide(Workspace& w, const Points& P, int k) {
+    if (!use_wide(P, k)) return;
+    const WidePlan wp = wide_plan(current_device(), P.rows, P.n, k);
+    if (!wp.ok) return;
+    for (int i = 0; i < 5; ++i) ensure_wide_slot(w.wide[i], wp);
+    (void)wide_dbg_buffer();  // (diagnostics: allocated before any capture)
+}
+
 // assign_nearest over P with the compacted centroids of ws (Cact/act/n_active).
 // With tile_out the per-1024-row tile partials of the distances are produced
 // too (fused into the screened kernel; a separate fold after the exact one).
@@ -788,7 +854,8 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                    uint64_t pair_stride, const int* parity, double* dists, int* changed,
                    const int* stop, bool final_pass = false, double* tile_out = nullptr,
                    unsigned* tile_ctr = nullptr, const dev::LloydCtl* ctl = nullptr, int hmode = 0,
-                   uint64_t dstride = 0, unsigned extra_ctas = 0, const AssignSrc* src = nullptr) {
+                   uint64_t dstride = 0, unsigned extra_ctas = 0, const AssignSrc* src = nullptr,
+                   int wide_slot = 4) {
     const dev::LloydCtl noctl{};
     const AssignSrc def{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, w.lbk.p};
     const AssignSrc& S = src ? *src : def;
@@ -804,6 +871,80 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
             // NS-stage TMA slab ring: 2 stages (3 CTAs per SM) for rows of up to
             // 8 slabs, 6 stages (2 CTAs per SM) for wide rows, whose CTAs stream
             // tens to hundreds of slabs each
+            // wide fp32 rows exact in tf32: the dot products from the tensor-core
+            // pre-screen (split-K over the dims, wide.cu); hmode 0 (no bound rows)
+            dev::PreDots pd{};
+            if (use_wide(P, k)) {
+                const WidePlan wp = wide_plan(current_device(), P.rows, P.n, k);
+                if (wp.ok) {
+                    Workspace::WideSlot& ws = w.wide[final_pass ? 5 : wide_slot];
+                    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                    BM_CUDA(cudaStreamIsCapturing(st, &cs));
+                    if (cs == cudaStreamCaptureStatusNone) ensure_wide_slot(ws, wp);
+                    else if (ws.dot.n < wp.dot_floats() || ws.nx.n < wp.nx_floats() || ws.nc.n < wp.nc_floats() ||
+                             ws.bops.n < wp.bops_floats() || ws.best.n < P.rows)
+                        throw CudaError("wide pre-screen buffers not allocated before the graph capture");
+                    if (ws.X != P.X || ws.rows != P.rows || ws.n != P.n || ws.ld != P.ld) {
+                        ws.map = wide_rows_map(P.X, P.rows, P.n, P.ld);
+                        ws.map32 = wide_rows_map(P.X, P.rows, P.n, P.ld, 32);
+                        ws.X = P.X;
+                        ws.rows = P.rows;
+                        ws.n = P.n;
+                        ws.ld = P.ld;
+                    }
+                    dev::WideArgs wa{};
+                    wa.xmap = ws.map;
+                    wa.Cact = S.Cact;
+                    wa.ldc = w.ldc;
+                    wa.n_active = S.n_active;
+                    wa.rows = P.rows;
+                    wa.n = P.n;
+                    wa.na = wp.na;
+                    wa.bpa = wp.bpa;
+                    wa.natoms = wp.natoms;
+                    wa.dot = ws.dot.p;
+                    wa.nx = ws.nx.p;
+                    wa.nc = ws.nc.p;
+                    wa.bops = ws.bops.p;
+                    wa.stop = stop;
+                    wa.go = ctl ? ctl->go : nullptr;
+                    wa.dbg = wide_dbg_buffer();
+                    launch_wide_screen(st, wp, wa, pdl_enabled());
+                    if (ws.C != S.Cact || ws.ck != k || ws.cn != P.n || ws.cld != w.ldc || ws.cnp != wp.np) {
+                        ws.cmap = wide_cent_map(S.Cact, k, P.n, w.ldc, wp.np);
+                        ws.C = S.Cact;
+                        ws.ck = k;
+                        ws.cn = P.n;
+                        ws.cld = w.ldc;
+                        ws.cnp = wp.np;
+                    }
+                    dev::RecheckArgs ra{};
+                    ra.xmap = ws.map32;
+                    ra.cmap = ws.cmap;
+                    ra.X = static_cast<const float*>(P.X);
+                    ra.ld = P.ld;
+                    ra.rows = P.rows;
+                    ra.n = P.n;
+                    ra.Cact = S.Cact;
+                    ra.ldc = w.ldc;
+                    ra.n_active = S.n_active;
+                    ra.dot = ws.dot.p;
+                    ra.nx = ws.nx.p;
+                    ra.nc = ws.nc.p;
+                    ra.ks = wp.ks;
+                    ra.natoms = wp.natoms;
+                    ra.np = wp.np;
+                    ra.cst = wide_screen_consts(wp, P.n);
+                    ra.best = ws.best.p;
+                    ra.bj = ws.bj.p;
+                    ra.stop = stop;
+                    ra.go = wa.go;
+                    launch_wide_recheck(st, wp, ra, pdl_enabled());
+                    count_launch(3);
+                    pd = dev::PreDots{ws.best.p, ws.bj.p};
+                    hmode = 0;
+                }
+            }
             auto go = [&](auto ns_tag) {
                 constexpr int NS = decltype(ns_tag)::value;
                 constexpr size_t shm = dev::tma_smem_bytes<T, NS>();
@@ -815,7 +956,7 @@ void launch_assign(cudaStream_t st, const Points& P, Workspace& w, int k, int32_
                     S.n_active, labels_pair, pair_stride, parity, dists, changed, stop, tile_out, tile_ctr,
                     g_profiling ? g_prof.d_cand : nullptr, screen_consts(P.n), fused_ctl ? *ctl : noctl,
                     !hamerly_enabled() || (hmode == 2 && w.drift_slabs == 0) ? 0 : hmode, S.lbk, w.delta.p, k,
-                    dstride);
+                    dstride, pd);
             };
             if (P.n > 8 * dev::kADC) go(std::integral_constant<int, 6>{});
             else go(std::integral_constant<int, 2>{});
@@ -1027,7 +1168,7 @@ void lloyd_enqueue_begin(cudaStream_t st, const Points& P, Workspace& w, bool do
     AssignSrc src{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, gr_lbk(w, g)};
     if (g && g->begin_kind == 1) src = AssignSrc{w.CactI.p, w.actI.p, &w.gs.p->n_active_inc, &w.tm_ctI, gr_lbk(w, g)};
     launch_assign(st, P, w, w.k, gr_labels(w, g) + slot * w.R, 0, nullptr, gr_dists(w, g) + slot * w.R, nullptr,
-                  nullptr, false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1, 0, 0u, &src);
+                  nullptr, false, fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 1, 0, 0u, &src, g ? g->buf : 4);
 }
 
 // update (:33) + assign (:34-35) + step (:36-51), the step fused into the assignment.
@@ -1045,7 +1186,7 @@ void lloyd_enqueue_round(cudaStream_t st, const Points& P, Workspace& w, uint64_
     AssignSrc src{w.Cact.p, w.act.p, &w.gs.p->n_active, &w.tm_ct, gr_lbk(w, g)};
     launch_assign(st, P, w, w.k, gr_labels(w, g), w.R, parity, gr_dists(w, g), &sts->changed, stop, false,
                   fast ? nullptr : w.tile_buf.p, w.tile_ctr.p, &ctl, 2, fast ? w.R : 0,
-                  g && g->fix ? (unsigned)tiles_of(w.R) : 0u, &src);
+                  g && g->fix ? (unsigned)tiles_of(w.R) : 0u, &src, g ? g->buf : 4);
 }
 
 // Runs the loop to completion; `between` is called once after the first
@@ -1649,13 +1790,13 @@ void ensure_graphs(cudaStream_t st, const bm_dataset* d, DeviceCache& dc, Sample
                    const Points& P, uint64_t max_it, double tol, bool persist = false) {
     char sig[512];
     // the dataset enters only through shape: its base is read from sw.xslot
-    std::snprintf(sig, sizeof(sig), "%llu/%llu/%d/%p/%p/%p/%p/%p/%p/%llu/%a/%llu/%d/%a/%p",
+    std::snprintf(sig, sizeof(sig), "%llu/%llu/%d/%p/%p/%p/%p/%p/%p/%llu/%a/%llu/%d/%a/%p/%p",
                   (unsigned long long)d->m, (unsigned long long)d->ld, (int)d->dtype, (void*)dc.chunk.p, (void*)dc.chunk1.p,
                   (void*)dc.chunk3.p, (void*)&sw,
                   (void*)w.drec.p, (void*)sw.mt.p, (unsigned long long)max_it, tol, (unsigned long long)w.drec.n,
                   (int)w.sums_on + 2 * (int)w.sum_small + 4 * (int)w.sums_fuse +
-                      16 * (int)persist,
-                  w.sum_scale, (void*)w.sums.p);
+                      16 * (int)persist + 32 * (int)use_wide(P, w.k),
+                  w.sum_scale, (void*)w.sums.p, (void*)w.wide[0].dot.p);
     if (w.graph_sig == sig && w.g_prep[0]) return;
     w.drop_graphs();
     const uint64_t saved = g_profile.kernel_launches;
@@ -1692,7 +1833,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     Workspace& w = get_ws(d, s, k, cfg.candidates_per_step, 0);
     const bool identity = s == m;  // sample_chunk(s == m): whole range, no draws (:46-48)
     SamplerWs* sw = identity ? nullptr : &get_sws(d, s);
-    Points chunkP{nullptr, d->dtype, s, n, d->ld};
+    Points chunkP{nullptr, d->dtype, s, n, d->ld, d->tf32_exact};
     if (identity) {
         chunkP = dataset_points(d);
     } else {
@@ -1748,6 +1889,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaMemsetAsync(w.grp_ctr.p, 0, w.grp_ctr.n * sizeof(unsigned), st));
         }
     }
+    if (!persist) ensure_wide(w, chunkP, k);  // before any capture
     if (use_graphs) ensure_graphs(st, d, dc, *sw, w, chunkP, cfg.max_iterations, cfg.rel_tolerance, persist);
     uint64_t evals = 0, iterations = 0;
     uint64_t chunk_assign_passes = 0, chunk_update_passes = 0;
@@ -3167,6 +3309,16 @@ bm_status bm_last_trace(bm_chunk_record* out, uint64_t capacity, uint64_t* count
         if (out)
             std::copy(g_last_trace.begin(), g_last_trace.begin() + std::min<uint64_t>(capacity, g_last_trace.size()),
                       out);
+    });
+}
+
+// Debug: k_wide_screen's per-atom stamps (BM_WIDE_DBG=1, -DBM_WIDE_DBG build).
+extern "C" bm_status bm_debug_wide_stamps(uint64_t* out) {
+    return bm::guarded([&] {
+        unsigned long long* p = bm::wide_dbg_buffer();
+        if (!p) throw bm::ConfigError("set BM_WIDE_DBG=1");
+        BM_CUDA(cudaDeviceSynchronize());
+        BM_CUDA(cudaMemcpy(out, p, 4 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     });
 }
 

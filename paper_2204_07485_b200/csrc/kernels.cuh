@@ -19,6 +19,7 @@
 #include "device_common.cuh"
 #include "mt64.cuh"
 #include "tma.cuh"
+#include "wide.h"
 
 namespace bm {
 namespace dev {

@@ -696,8 +696,18 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T, NS>& S, const CUtensorMap*
                                            int qb, const double* __restrict__ Cact, int ldc, int KA, uint32_t ni,
                                            const short* item_p, const signed char* item_j, double* item_d) {
     constexpr int kCS = 18;  // centroid slab row stride (doubles): 16-byte rows, spread banks
+    // slabs in flight: the 6-stage ring (wide rows) keeps 4 ahead, its centroid
+    // pieces in 5 buffers over the (now free) screen staging from craw on;
+    // the 2-stage ring keeps 2 ahead in 2 buffers over xs
+    constexpr int DEPTH = NS >= 6 ? 4 : 2;
+    constexpr int NCB = DEPTH + 1 > 2 ? DEPTH + 1 : 2;
+    using SmemT = TmaSmem<T, NS>;
+    static_assert(NS < 6 || offsetof(SmemT, craw) + NCB * kSMaxK * kCS * sizeof(double) <=
+                                offsetof(SmemT, red_u) - kItemCap * (sizeof(double) + 3),
+                  "tma_chains centroid ring overlaps the item list");
     const int tid = threadIdx.x;
-    double(*c64)[kSMaxK][kCS] = reinterpret_cast<double(*)[kSMaxK][kCS]>(&S.xs[0][0][0]);
+    double(*c64)[kSMaxK][kCS] = reinterpret_cast<double(*)[kSMaxK][kCS]>(
+        NS >= 6 ? reinterpret_cast<void*>(&S.craw[0][0][0]) : reinterpret_cast<void*>(&S.xs[0][0][0]));
     __syncthreads();  // item list complete; the ring and the staging area are free
     double acc[2] = {0.0, 0.0};
     int ip[2] = {-1, -1}, ij[2] = {0, 0};
@@ -710,7 +720,7 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T, NS>& S, const CUtensorMap*
         }
     }
     auto issue = [&](int sl) {
-        const int st = (qb + sl) % NS, cb = (qb + sl) & 1;
+        const int st = (qb + sl) % NS, cb = sl % NCB;
         if (tid == 0) {
             mbar_expect_tx(&S.bar[st], TmaSmem<T, NS>::kRawBytes);
             tma_load_2d(S.raw[st], tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
@@ -721,12 +731,13 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T, NS>& S, const CUtensorMap*
         }
         cp_async_commit();
     };
-    issue(0);
-    if (nslab > 1) issue(1);
+    for (int i = 0; i < DEPTH; ++i) {
+        if (i < nslab) issue(i);
+        else cp_async_commit();  // (empty groups keep the wait count uniform)
+    }
     for (int sl = 0; sl < nslab; ++sl) {
-        const int q = qb + sl, st = q % NS, cb = q & 1;
-        if (sl + 1 < nslab) cp_async_wait<1>();
-        else cp_async_wait<0>();
+        const int q = qb + sl, st = q % NS, cb = sl % NCB;
+        cp_async_wait<DEPTH - 1>();  // slab sl's centroid pieces (DEPTH groups are in flight)
         mbar_wait(&S.bar[st], (q / NS) & 1);
         if (qb == 0 && sl < 5) ktrace(16 + 2 * sl, 2);
         __syncthreads();  // everyone's centroid pieces landed
@@ -763,8 +774,10 @@ __device__ __forceinline__ void tma_chains(TmaSmem<T, NS>& S, const CUtensorMap*
         }
         __syncthreads();  // stage st consumed
         if (qb == 0 && sl < 5) ktrace(17 + 2 * sl, 2);
-        if (sl + 2 < nslab) issue(sl + 2);
+        if (sl + DEPTH < nslab) issue(sl + DEPTH);
+        else cp_async_commit();
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int r = 0; r < 2; ++r)
         if (ip[r] >= 0) item_d[tid + r * kSThreads] = acc[r];
@@ -788,8 +801,12 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
              double* __restrict__ tile_out, unsigned* __restrict__ tile_counter,
              unsigned long long* __restrict__ cand_counter, ScreenConsts cst, const __grid_constant__ LloydCtl ctl,
              int hmode, float* __restrict__ lbk, const float* __restrict__ delta, int kfull,
-             uint64_t dstride) {
+             uint64_t dstride, const PreDots pdots) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // pdots.best: wide rows pre-screened and rechecked by k_wide_screen /
+    // k_wide_recheck (wide.cu) — each point's exact minimum comes precomputed;
+    // no slab screen and no recheck here (hmode is 0)
+    const bool pm = pdots.best != nullptr;
     // TMA destinations with 128-byte swizzle need 1024-byte alignment
     unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     TmaSmem<T, NS>& S = *reinterpret_cast<TmaSmem<T, NS>*>(smem_al);
@@ -1137,7 +1154,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
                     ++it;
                 }
             }
-            if (NI > static_cast<uint32_t>(kSThreads)) {
+            if (NI > static_cast<uint32_t>(kSThreads) || (NI > 0 && n > 256)) {  // (wide rows: streamed)
                 tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, NI, item_p, item_j, item_d);
                 qb += nslab;
             } else if (NI > 0) {  // few rechecks: one thread per item, rows straight from L2
@@ -1191,7 +1208,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         tma_load_2d(S.raw[st], &tmx, &S.bar[st], sl * kADC, static_cast<int>(p0));
         tma_load_2d(&S.craw[st][0][0], &tmc, &S.bar[st], 0, sl * kADC);
     };
-    if (tid == 0)
+    if (tid == 0 && !pm)
         for (int i = 0; i < NS && i < nslab; ++i) issue(i);
 
     float2 tot[2][kAK];
@@ -1203,7 +1220,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     float ncl = 0.f, nch = 0.f;
     const int cp_ = tid & (kABP - 1), chalf = tid >> 7;  // conversion: point, 8-dim half
 
-    for (int sl = 0; sl < nslab; ++sl) {
+    for (int sl = 0; sl < (pm ? 0 : nslab); ++sl) {
         const int q = qb + sl, st = q % NS, xb = q & 1, dl = min(kADC, n - sl * kADC);
         mbar_wait(&S.bar[st], (q / NS) & 1);
         if (sl < 6) ktrace(1 + sl, hmode);
@@ -1253,8 +1270,8 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             }
         }
     }
-    qb += nslab;  // (the screen's slabs; a streamed recheck takes them again below)
-    if (normw) {
+    if (!pm) qb += nslab;  // (the screen's slabs; a streamed recheck takes them again below)
+    if (normw && !pm) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             S.nx_lo[4 * lane + q] = nxl[q];
@@ -1287,7 +1304,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
     // bounds against the point's minimum U and sets candidate bits.
     float Lk[4][kAK];
     if (tid < kABP) S.cand[tid] = 0u;
-    if (comp) {
+    if (comp && !pm) {
         float un[4] = {finf, finf, finf, finf};
 #pragma unroll
         for (int u = 0; u < kAK; ++u) {
@@ -1316,7 +1333,7 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         for (int q = 0; q < 4; ++q) S.red_u[warp][4 * lane + q] = un[q];
     }
     __syncthreads();
-    if (comp) {
+    if (comp && !pm) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int p = 4 * lane + q;
@@ -1381,7 +1398,9 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
             for (uint32_t i = tid; i < NI; i += kSThreads)
                 item_d[i] = chain_smem_row(xrow + item_p[i] * ldr, Cact + static_cast<uint64_t>(item_j[i]) * ldc, n);
             __syncthreads();
-        } else if (NI > static_cast<uint32_t>(kSThreads)) {
+        } else if (NI > 0 && (NI > static_cast<uint32_t>(kSThreads) || n > 256)) {
+            // streamed through the TMA ring (wide rows: a chain straight from L2
+            // would wait one L2 round trip per 16 dims)
             tma_chains<T>(S, &tmx, p0, n, nslab, qb, Cact, ldc, KA, NI, item_p, item_j, item_d);
             qb += nslab;
         } else {  // one item per thread, rows straight from L2
@@ -1402,7 +1421,10 @@ k_assign_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CU
         const uint64_t gp = p0 + p;
         double best = __longlong_as_double(0x7FF0000000000000LL);
         int bj = -1;
-        if (!overflow) {  // ascending j, strict < (core.cpp:147)
+        if (pm) {  // k_wide_recheck's minimum
+            best = pdots.best[gp];
+            bj = pdots.bj[gp];
+        } else if (!overflow) {  // ascending j, strict < (core.cpp:147)
             const uint32_t b1 = p + 1 < np ? static_cast<uint32_t>(S.icount[p + 1]) : NI;
             for (uint32_t i = S.icount[p]; i < b1; ++i) {
                 if (item_d[i] < best) {

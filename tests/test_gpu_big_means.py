@@ -307,3 +307,29 @@ def test_chunk_kernel_screens_vs_oracle(port, monkeypatch, screen, n):
         assert out.objective == p.objective
         assert (bits(out.centroids.values) == bits(p.centroids)).all()
         assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
+
+
+@pytest.mark.parametrize("n,k,m,s", [(89, 7, 3000, 700), (100, 3, 2000, 520), (300, 17, 2600, 900),
+                                     (777, 32, 1500, 600), (2500, 10, 900, 400), (5003, 5, 600, 300),
+                                     (5000, 10, 4500, 4000)])  # the last: c5's split shape (2 atoms per block)
+def test_wide_rows_tensor_core_prescreen_vs_oracle(port, monkeypatch, n, k, m, s):
+    """Wide fp32 rows exact in tf32 (n > 88, the c5 regime): the split-K
+    tensor-core pre-screen (wide.cu, tcgen05 kind::tf32 with one TMEM block
+    per 32-dim atom) feeding k_assign_tma's recheck — bitwise against the
+    oracle, with the pre-screen on and off (BM_WIDE=0); ragged tiles and atoms,
+    N = 16 and 32 centroid slots, 1..many splits."""
+    rng = np.random.default_rng(n + 7 * k)
+    grp = rng.integers(0, 3, (m, 1))
+    X = np.where(rng.random((m, n)) < 0.85, 0.0, rng.integers(1, 1000, (m, n)) * (grp + 1.0)).astype(np.float64)
+    chunks = 2 if s >= 4000 else 4
+    p = port.big_means(X, k, s, chunks, seed=n)
+    for wide in ("1", "0"):
+        monkeypatch.setenv("BM_WIDE", wide)
+        out, trace = bm.big_means(bm.Dataset(X), cfg(k, s, chunks, seed=n))
+        got = [(r.chunk_index, r.candidate_objective, r.incumbent_objective, r.accepted,
+                r.degenerate_repaired) for r in trace.records]
+        assert got == p.trace, wide
+        assert out.objective == p.objective
+        assert (bits(out.centroids.values) == bits(p.centroids)).all()
+        assert (out.assignment == p.labels).all()
+        assert (out.counter.distance_evals, out.counter.iterations) == (p.evals, p.iterations)
