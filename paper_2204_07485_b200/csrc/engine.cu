@@ -1873,8 +1873,10 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         BM_CUDA(cudaMemsetAsync(w.cjob.p, 0, dev::kStateBufs * sizeof(dev::FixJob), st));
     }
     // exact-sum mode for the graph chunks (kernels.cuh §5b)
+    // (wide rows keep the ordered update: integer label sums over thousands of
+    // dims cost more than k_update — c5: 128 vs 85 ms per step)
     w.sums_on = use_graphs && !persist && d->exact_sums && exact_sums_enabled() && screen_enabled(k) &&
-                s < (1ull << 31) && !w.hist_cap;
+                s < (1ull << 31) && !w.hist_cap && n <= 256;
     if (w.sums_on) {
         w.sum_scale = std::ldexp(1.0, -d->sum_exp);
         w.sum_unscale = std::ldexp(1.0, d->sum_exp);
