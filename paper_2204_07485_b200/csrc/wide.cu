@@ -254,8 +254,12 @@ __host__ __device__ inline size_t wide_recheck_smem_bytes(int rs, int npr) {
     return 1024 + static_cast<size_t>(rs) * wide_recheck_stage_bytes(npr);
 }
 
+// 160 threads: warps 0-3 compute (the bounds of 32 points, then up to 4
+// chains each per streaming round), warp 4's lane 0 streams the dims: step g
+// (round g / nsteps, dims 32 (g % nsteps) ..) into stage g % kRS by TMA; a
+// stage is refilled once its 128 readers have arrived (no block barrier per step).
 template <int kRS, int NPR>
-__global__ void __launch_bounds__(kRT) k_wide_recheck(const __grid_constant__ RecheckArgs a) {
+__global__ void __launch_bounds__(kRT + 32) k_wide_recheck(const __grid_constant__ RecheckArgs a) {
     extern __shared__ __align__(16) unsigned char rsm[];
     __shared__ float ncl[32], nch[32], ncr[32];
     __shared__ unsigned cand[kRP];
@@ -263,41 +267,42 @@ __global__ void __launch_bounds__(kRT) k_wide_recheck(const __grid_constant__ Re
     __shared__ short item_p[kRP * 32];
     __shared__ signed char item_j[kRP * 32];
     __shared__ double item_d[kRP * 32];
+    __shared__ __align__(8) unsigned long long s_full[kRS], s_empty[kRS];
     pdl_wait();
     if ((a.stop && *a.stop) || (a.go && !*a.go)) return;
     const int tid = threadIdx.x;
+    const bool producer = tid == kRT;
     const uint64_t q0 = static_cast<uint64_t>(blockIdx.x) * kRP;
     const int np = static_cast<int>(min(static_cast<uint64_t>(kRP), a.rows - q0));
     const int KA = *a.n_active;
     const float finf = __int_as_float(0x7F800000);
-    __shared__ __align__(8) unsigned long long s_full[kRS];
     // stage: [x box: 32 rows x 128 B][centroid box dims 0-15: NPR rows x 128 B][dims 16-31], 128-byte swizzle
     unsigned char* stg = rsm + ((1024u - (umma::smem_addr(rsm) & 1023u)) & 1023u);
     constexpr unsigned kStage = static_cast<unsigned>(kRP * 128 + 2 * NPR * 128);
     const int nsteps = (a.n + kRD - 1) / kRD;
     if (tid == 0) {
-        for (int i = 0; i < kRS; ++i) mbar_init(reinterpret_cast<uint64_t*>(&s_full[i]), 1);
+        for (int i = 0; i < kRS; ++i) {
+            mbar_init(reinterpret_cast<uint64_t*>(&s_full[i]), 1);
+            mbar_init(reinterpret_cast<uint64_t*>(&s_empty[i]), kRT);
+        }
         fence_mbar_init();
-        tma_prefetch_map(&a.xmap);
-        tma_prefetch_map(&a.cmap);
     }
     __syncthreads();
-    // step t (dims [32 t, 32 t + 32)) into stage t % kRS by TMA (one thread; dims past n,
-    // rows past the chunk / past k zero-filled)
-    auto issue = [&](int t) {
-        if (tid == 0 && t < nsteps) {
-            const int st = t % kRS, d0 = t * kRD;
-            unsigned char* b = stg + static_cast<size_t>(st) * kStage;
-            uint64_t* bar = reinterpret_cast<uint64_t*>(&s_full[st]);
-            mbar_expect_tx(bar, kStage);
-            tma_load_2d(b, &a.xmap, bar, d0, static_cast<int>(q0));
-            tma_load_2d(b + kRP * 128, &a.cmap, bar, d0, 0);
-            tma_load_2d(b + kRP * 128 + NPR * 128, &a.cmap, bar, d0 + 16, 0);
-        }
+    auto issue = [&](int g) {  // global step g (producer only)
+        const int st = g % kRS, d0 = (g % nsteps) * kRD;
+        unsigned char* b = stg + static_cast<size_t>(st) * kStage;
+        uint64_t* bar = reinterpret_cast<uint64_t*>(&s_full[st]);
+        mbar_expect_tx(bar, kStage);
+        tma_load_2d(b, &a.xmap, bar, d0, static_cast<int>(q0));
+        tma_load_2d(b + kRP * 128, &a.cmap, bar, d0, 0);
+        tma_load_2d(b + kRP * 128 + NPR * 128, &a.cmap, bar, d0 + 16, 0);
     };
-    // the first stages are in flight while the candidates are found
-    for (int t = 0; t < kRS - 1; ++t) issue(t);
-    // centroid norms: the KS partials added (rounded down / up)
+    if (producer) {  // the first stages are in flight while the candidates are found
+        tma_prefetch_map(&a.xmap);
+        tma_prefetch_map(&a.cmap);
+        for (int g = 0; g < kRS && g < nsteps; ++g) issue(g);
+    }
+    // centroid norms: the atoms' partial norms added (rounded down / up)
     if (tid < KA) {
         float lo = 0.f, hi = 0.f;
         for (int q = 0; q < a.natoms; ++q) {  // the atoms' partial norms (k_wide_prep)
@@ -370,81 +375,80 @@ __global__ void __launch_bounds__(kRT) k_wide_recheck(const __grid_constant__ Re
     }
     __syncthreads();
     const int NI = icount[kRP];
-    // exact fp64 chains (direct form, core.cpp:142-146) of up to 4 items per
-    // thread per streaming round; the dims arrive stage by stage
-    for (int i0 = 0; i0 < NI; i0 += kRItems) {
-        if (i0 > 0) {  // another round over the dims (more than 16 candidates per point on average)
-            __syncthreads();
-            for (int t = 0; t < kRS - 1; ++t) issue(t);
+    const int rounds = (NI + kRItems - 1) / kRItems, total = rounds * nsteps;
+    if (producer) {
+        for (int g = min(kRS, nsteps); g < total; ++g) {  // (the prologue issued steps < min(kRS, nsteps))
+            if (g >= kRS) umma::mbar_wait_parity(&s_empty[g % kRS], ((g / kRS) - 1) & 1);
+            issue(g);
         }
-        const int phase0 = i0 / kRItems;  // rounds so far: each consumed every stage's phases nsteps times
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        int ip[4], ij[4];
-        // item slot of this thread: consecutive items on consecutive warps (a
-        // few items per point: every warp / SM sub-partition gets some chains)
+    } else if (tid < kRT) {
+        // exact fp64 chains (direct form, core.cpp:142-146) of up to 4 items per
+        // thread per round; consecutive items on consecutive warps
         const int slot = (tid & 3) * 32 + (tid >> 2);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int i = i0 + slot + r * kRT;
-            ip[r] = i < NI ? item_p[i] : -1;
-            ij[r] = i < NI ? item_j[i] : 0;
-        }
-        for (int t = 0; t < nsteps; ++t) {
-            const int st = t % kRS, d0 = t * kRD, dl = min(kRD, a.n - d0);
-            // phase parity of stage st at step t of this round
-            const int use = phase0 * ((nsteps + kRS - 1 - st) / kRS) + t / kRS;
-            mbar_wait(reinterpret_cast<uint64_t*>(&s_full[st]), use & 1);
-            const unsigned char* b = stg + static_cast<size_t>(st) * kStage;
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int i0 = rd * kRItems;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            int ip[4], ij[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                if (ip[r] < 0) continue;
-                const int pr = ip[r], jr = ij[r];
-                const unsigned char* xrow = b + pr * 128;
-                const unsigned char* c0row = b + kRP * 128 + jr * 128;
-                const unsigned char* c1row = c0row + NPR * 128;
-                auto xq = [&](int c) { return *reinterpret_cast<const float4*>(xrow + ((c ^ (pr & 7)) << 4)); };
-                auto cq = [&](int d) {  // dims d, d+1 (d even)
-                    const unsigned char* row = d < 16 ? c0row : c1row;
-                    return *reinterpret_cast<const double2*>(row + ((((d & 15) >> 1) ^ (jr & 7)) << 4));
-                };
-                double s_ = acc[r];
-                if (dl == kRD) {
-                    // the 32 squared differences first (independent: loads, conversions,
-                    // subtractions and products overlap), then the dependent left fold
-                    // in dim order (core.cpp:144-145: the same operations, same order)
-                    double q[kRD];
-#pragma unroll
-                    for (int c = 0; c < kRD / 4; ++c) {
-                        const float4 xv = xq(c);
-                        const double2 c0 = cq(4 * c);
-                        const double2 c1 = cq(4 * c + 2);
-                        const double d0 = __dsub_rn(static_cast<double>(xv.x), c0.x);
-                        const double d1 = __dsub_rn(static_cast<double>(xv.y), c0.y);
-                        const double d2 = __dsub_rn(static_cast<double>(xv.z), c1.x);
-                        const double d3 = __dsub_rn(static_cast<double>(xv.w), c1.y);
-                        q[4 * c] = __dmul_rn(d0, d0);
-                        q[4 * c + 1] = __dmul_rn(d1, d1);
-                        q[4 * c + 2] = __dmul_rn(d2, d2);
-                        q[4 * c + 3] = __dmul_rn(d3, d3);
-                    }
-#pragma unroll
-                    for (int i = 0; i < kRD; ++i) s_ = __dadd_rn(s_, q[i]);
-                } else {
-                    for (int d = 0; d < dl; ++d) {
-                        const float xv = reinterpret_cast<const float*>(xrow + (((d >> 2) ^ (pr & 7)) << 4))[d & 3];
-                        const double cv = (d & 1) ? cq(d & ~1).y : cq(d & ~1).x;
-                        s_ = dist_step(s_, static_cast<double>(xv), cv);
-                    }
-                }
-                acc[r] = s_;
+                const int i = i0 + slot + r * kRT;
+                ip[r] = i < NI ? item_p[i] : -1;
+                ij[r] = i < NI ? item_j[i] : 0;
             }
-            __syncthreads();  // stage (t - 1) % kRS consumed by every thread: refill it with step t + kRS - 1
-            issue(t + kRS - 1);
-        }
+            for (int t = 0; t < nsteps; ++t) {
+                const int g = rd * nsteps + t, st = g % kRS, d0 = t * kRD, dl = min(kRD, a.n - d0);
+                mbar_wait(reinterpret_cast<uint64_t*>(&s_full[st]), (g / kRS) & 1);
+                const unsigned char* b = stg + static_cast<size_t>(st) * kStage;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int i = i0 + slot + r * kRT;
-            if (i < NI) item_d[i] = acc[r];
+                for (int r = 0; r < 4; ++r) {
+                    if (ip[r] < 0) continue;
+                    const int pr = ip[r], jr = ij[r];
+                    const unsigned char* xrow = b + pr * 128;
+                    const unsigned char* c0row = b + kRP * 128 + jr * 128;
+                    const unsigned char* c1row = c0row + NPR * 128;
+                    auto xq = [&](int c) { return *reinterpret_cast<const float4*>(xrow + ((c ^ (pr & 7)) << 4)); };
+                    auto cq = [&](int d) {  // dims d, d+1 (d even)
+                        const unsigned char* row = d < 16 ? c0row : c1row;
+                        return *reinterpret_cast<const double2*>(row + ((((d & 15) >> 1) ^ (jr & 7)) << 4));
+                    };
+                    double s_ = acc[r];
+                    if (dl == kRD) {
+                        // the 32 squared differences first (independent: loads, conversions,
+                        // subtractions and products overlap), then the dependent left fold
+                        // in dim order (core.cpp:144-145: the same operations, same order)
+                        double q[kRD];
+#pragma unroll
+                        for (int c = 0; c < kRD / 4; ++c) {
+                            const float4 xv = xq(c);
+                            const double2 c0 = cq(4 * c);
+                            const double2 c1 = cq(4 * c + 2);
+                            const double e0 = __dsub_rn(static_cast<double>(xv.x), c0.x);
+                            const double e1 = __dsub_rn(static_cast<double>(xv.y), c0.y);
+                            const double e2 = __dsub_rn(static_cast<double>(xv.z), c1.x);
+                            const double e3 = __dsub_rn(static_cast<double>(xv.w), c1.y);
+                            q[4 * c] = __dmul_rn(e0, e0);
+                            q[4 * c + 1] = __dmul_rn(e1, e1);
+                            q[4 * c + 2] = __dmul_rn(e2, e2);
+                            q[4 * c + 3] = __dmul_rn(e3, e3);
+                        }
+#pragma unroll
+                        for (int i = 0; i < kRD; ++i) s_ = __dadd_rn(s_, q[i]);
+                    } else {
+                        for (int d = 0; d < dl; ++d) {
+                            const float xv = reinterpret_cast<const float*>(xrow + (((d >> 2) ^ (pr & 7)) << 4))[d & 3];
+                            const double cv = (d & 1) ? cq(d & ~1).y : cq(d & ~1).x;
+                            s_ = dist_step(s_, static_cast<double>(xv), cv);
+                        }
+                    }
+                    acc[r] = s_;
+                }
+                mbar_arrive(&s_empty[st]);  // this thread is done with the stage
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int i = i0 + slot + r * kRT;
+                if (i < NI) item_d[i] = acc[r];
+            }
         }
     }
     __syncthreads();
@@ -624,7 +628,7 @@ void launch_wide_recheck(cudaStream_t st, const WidePlan& p, const dev::RecheckA
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.recheck_ctas(a.rows));
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(160);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
