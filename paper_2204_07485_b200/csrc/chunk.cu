@@ -191,7 +191,7 @@ using umma::mbar_wait_parity;
 using umma::tf32_rna;
 using umma::tmem_ld32;
 __device__ __forceinline__ unsigned long long umma_desc_sw128_units(unsigned u) { return umma::desc_sw128(u); }
-constexpr unsigned kTcIdesc = umma::idesc_tf32<32>();
+constexpr unsigned kTcIdesc = umma::idesc_tf32<64>();  // N = 64: 32 hi slots, then 32 lo slots
 __device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db, int acc) {
     umma::mma_tf32(tmem_d, da, db, kTcIdesc, acc);
 }
@@ -433,10 +433,11 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         __syncthreads();
         const int KA = act[kCKMax];
         if constexpr (TC) {
+            // B operand of K-atom ka: 64 rows = [hi of slots 0..31][lo of slots 0..31] (one N = 64 MMA per k-step)
             unsigned char* cbhi = sm + L.cb;
-            unsigned char* cblo = cbhi + static_cast<size_t>(NKA) * kCKMax * 128;
+            unsigned char* cblo = cbhi + kCKMax * 128;
             auto boff = [&](int rk, int d) -> size_t {
-                return static_cast<size_t>(d >> 5) * (kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
+                return static_cast<size_t>(d >> 5) * (2 * kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
                        (d & 3) * 4;
             };
             batched_copy<4>(
@@ -559,9 +560,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                     const float f = __double2float_rn(cd[rk * cdld + d]), hi = tf32_rna(f);
                     want = part ? f - hi : hi;
                 }
-                const size_t off = static_cast<size_t>(d >> 5) * (kCKMax * 128) + rk * 128 +
-                                   ((((d >> 2) & 7) ^ (rk & 7)) << 4) + (d & 3) * 4 +
-                                   (part ? static_cast<size_t>(NKA) * kCKMax * 128 : 0);
+                const size_t off = static_cast<size_t>(d >> 5) * (2 * kCKMax * 128) + rk * 128 +
+                                   ((((d >> 2) & 7) ^ (rk & 7)) << 4) + (d & 3) * 4 + (part ? kCKMax * 128 : 0);
                 const float got = *reinterpret_cast<const float*>(sm + L.cb + off);
                 if (!(got == want)) ++bbad;
             }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             xinexact = __syncthreads_or(xinexact);
             fence_proxy_async_smem();
             if (warp == 0) {
-                const unsigned cols = MP / 128 * 32 <= 32 ? 32 : MP / 128 * 32 <= 64 ? 64 : MP / 128 * 32 <= 128 ? 128 : 256;
+                const unsigned cols = umma::tmem_cols(static_cast<unsigned>(MP / 128) * 64);
                 asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
                              "r"(cols)
                              : "memory");
@@ -706,21 +706,19 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 // 16 B); k-steps outer, tiles inner: consecutive MMAs feed
                 // different accumulators
                 const unsigned ua0 = smem_addr(sm + L.xs) >> 4;  // start addresses, 16-byte units
-                const unsigned ubh = smem_addr(sm + L.cb) >> 4;
-                const unsigned ubl = ubh + ((NKA * kCKMax * 128) >> 4);
+                const unsigned ub0 = smem_addr(sm + L.cb) >> 4;
                 const int ntl = MP / 128;
-                // k-steps of 8 dims (dims n..ND-1 are zero in both operands)
+                // k-steps of 8 dims (dims n..ND-1 are zero in both operands);
+                // D[tile] (64 columns) = rows . [hi | lo]^T
                 constexpr int KSTEPS = ND / 8;
                 for (int ks = 0; ks < KSTEPS; ++ks) {
                     const unsigned ko = ((ks & 3) * 32) >> 4;
-                    const unsigned bo = (((ks >> 2) * kCKMax * 128) >> 4) + ko;
+                    const unsigned bo = (((ks >> 2) * 2 * kCKMax * 128) >> 4) + ko;
                     const unsigned ao = static_cast<unsigned>((static_cast<size_t>(ks >> 2) * ASZ) >> 4) + ko;
-                    const unsigned long long dbh = umma_desc_sw128_units(ubh + bo);
-                    const unsigned long long dbl = umma_desc_sw128_units(ubl + bo);
+                    const unsigned long long db = umma_desc_sw128_units(ub0 + bo);
                     for (int t = 0; t < ntl; ++t) {
                         const unsigned long long da = umma_desc_sw128_units(ua0 + ao + static_cast<unsigned>(t) * (16384 >> 4));
-                        umma_tf32(s_tmem + 32u * t, da, dbh, ks > 0);
-                        umma_tf32(s_tmem + 32u * t, da, dbl, 1);
+                        umma_tf32(s_tmem + 64u * t, da, db, ks > 0);
                     }
                 }
                 umma_commit(&s_mbar);
@@ -748,8 +746,14 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             for (int i = 0; i < PPT; ++i) {
                 const int p = tid + i * NT;
                 float Lv[32];
-                tmem_ld32(s_tmem + (static_cast<unsigned>(32 * (warp & 3)) << 16) + 32u * static_cast<unsigned>(p >> 7),
-                          Lv);
+                {  // the dot products with hi and with lo, added (fp32, round to nearest)
+                    const unsigned ta = s_tmem + (static_cast<unsigned>(32 * (warp & 3)) << 16) + 64u * static_cast<unsigned>(p >> 7);
+                    float Lw[32];
+                    tmem_ld32(ta, Lv);
+                    tmem_ld32(ta + 32u, Lw);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) Lv[j] = __fadd_rn(Lv[j], Lw[j]);
+                }
 #ifdef BM_CHUNK_MMA_DIAG
                 if (a.dbg_mma && cta == 0 && p < np) {  // diagnostics: observed MMA error / (||x|| ||c||)
                     float worst = 0.f;
@@ -1276,7 +1280,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         __syncthreads();
         if (warp == 0) {
             tc_fence_after();
-            const unsigned cols = MP / 128 * 32 <= 32 ? 32 : MP / 128 * 32 <= 64 ? 64 : MP / 128 * 32 <= 128 ? 128 : 256;
+            const unsigned cols = umma::tmem_cols(static_cast<unsigned>(MP / 128) * 64);
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(cols) : "memory");
         }
     }
@@ -1536,8 +1540,9 @@ dev::ScreenConsts chunk_screen_consts(int n, bool tc, bool rows_tf32_exact) {
     // The rest as in engine.cu's screen_consts.
     const double u = std::ldexp(1.0, -24);
     auto gam = [&](double m) { return m * u / (1.0 - m * u); };
+    // (tensor core: + 2^-24 for the fp32 sum of the hi and lo dot products, read from separate columns)
     const double gb = tc ? 2.0 * ((rows_tf32_exact ? 0.0 : std::ldexp(1.0, -10)) + std::ldexp(1.0, -21) +
-                                  2.0 * n * std::ldexp(1.0, -23))
+                                  2.0 * n * std::ldexp(1.0, -23) + std::ldexp(1.0, -24))
                          : gam(n + 2);
     const double up = u * (1.0 + 4 * u) / (1.0 - u);
     const double K = gb / 2.0 + 2.0 * up + up * up;
