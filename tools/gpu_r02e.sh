@@ -1,6 +1,16 @@
 #!/bin/bash
+# Round-2 final check of the current tree: GPU tests, smoke, every config at
+# full size with the reference on the host (parity_full_size + cpu_baseline),
+# the c2 reference arm, the c2 launch list, ncu --set full of the chunk kernel
+# (c1-c3) and of the wide-row kernels (c5).
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_big_means.py -x -q > gpurun_out/pt_bm.log 2>&1; echo "rc=$?" >> gpurun_out/pt_bm.log
-for c in c2 c3 c1; do
-  BM_CHUNK_DBG=1 timeout 300 python tools/chunk_prof.py $c 20 > gpurun_out/dbg_$c.log 2>&1
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+for c in c1 c2 c3 c4 c5; do
+  timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_c2_ref.json 2> gpurun_out/bench_c2_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+  --log-file gpurun_out/launches_c2.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1
