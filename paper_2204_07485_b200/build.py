@@ -22,7 +22,7 @@ LIB = os.path.join(LIB_DIR, "libbigmeans_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "chunk.cu"), os.path.join(CSRC, "wide.cu"),
-           os.path.join(CSRC, "io.cpp")]
+           os.path.join(CSRC, "finaltc.cu"), os.path.join(CSRC, "io.cpp")]
 HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [
     os.path.join(ROOT, "include", "bigmeans_b200.h")]
 DEPS = SOURCES + HEADERS

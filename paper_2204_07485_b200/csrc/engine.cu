@@ -33,6 +33,7 @@
 #include "bigmeans_b200.h"
 #include "chunk.h"
 #include "wide.h"
+#include "finaltc.h"
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
@@ -1528,7 +1529,25 @@ void final_pass(cudaStream_t st, const bm_dataset* d, Workspace& w, uint64_t r0,
     P.X = static_cast<const uint8_t*>(d->X) + r0 * d->ld * dtype_size(d->dtype);
     P.rows = r1 - r0;
     c.ensure_final(P.rows);
-    if (screen_enabled(w.k) && P.n <= dev::kFMaxD && P.rows < (1ull << 31)) {
+    static const bool final_tc = !(std::getenv("BM_FINAL_TC") && std::string(std::getenv("BM_FINAL_TC")) == "0");
+    if (final_tc && P.dtype == BM_F32 && P.tf32_exact && final_tc_supported(P.n, w.k) && P.rows < (1ull << 31)) {
+        // fp32 rows exact in tf32: the tensor-core final pass (finaltc.cu); then the tile partials
+        PhaseScope ps(PH_FINAL, P.rows);
+        dev::FinalTcArgs fa{};
+        fa.xmap = final_tc_map(P.X, P.rows, P.n, P.ld);
+        fa.rows = P.rows;
+        fa.n = P.n;
+        fa.Cact = w.Cact.p;
+        fa.ldc = w.ldc;
+        fa.act = w.act.p;
+        fa.n_active = &w.gs.p->n_active;
+        fa.cst = chunk_screen_consts(P.n, true, true);
+        fa.labels = c.flabels.p;
+        fa.dists = c.fdists.p;
+        launch_final_tc(st, d->device, fa, pdl_enabled());
+        count_launch();
+        launch_tile_sums(st, c.fdists.p, P.rows, 0, 1, c.ftiles.p, nullptr);
+    } else if (screen_enabled(w.k) && P.n <= dev::kFMaxD && P.rows < (1ull << 31)) {
         // streaming form (k_final): persistent CTAs, one continuous TMA ring; then the tile partials
         PhaseScope ps(PH_FINAL, P.rows);
         dispatch(P.dtype, [&](auto tag) {
