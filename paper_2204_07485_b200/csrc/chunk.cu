@@ -36,7 +36,9 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
+#include <string>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -245,7 +247,7 @@ __device__ __forceinline__ double fold_smem(const double* v, int len) {
 
 // Shared-memory carve-up (host and device agree).
 struct CLayout {
-    size_t xs, cb, u, cf, cd, nrm, act, lab, dist, red, total;
+    size_t xs, cb, u, cf, cd, ssum, scnt, nrm, act, lab, dist, red, total;
     int cdld;         // fp64 centroid row stride: even, an odd number of 16-byte units
 };
 
@@ -271,7 +273,7 @@ __host__ __device__ inline int tc_mpad(int B) { return (B + 127) / 128 * 128; }
 __host__ __device__ inline int tc_katoms(int nd) { return (nd + 31) / 32; }
 
 __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, int nd, int n, unsigned G,
-                                                bool tc = false) {
+                                                bool tc = false, bool redm = false) {
     CLayout L{};
     size_t o = 0;
     L.xs = o;
@@ -290,8 +292,10 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
     const int nc = (B + 31) / 32;
     const size_t sort = al16((size_t)B * 2) + al16((size_t)B) + al16((size_t)nc * k * 4) + al16((size_t)(2 * k + 2) * 4);
     const size_t kn = (size_t)k * n, ppc = (kn + G - 1) / G;
-    const size_t merge = al16(ppc * G * 8) + al16((ppc / (size_t)n + 2) * G * 4);
-    const size_t tailf = (size_t)kTile * 8;  // exact-sum mode: a staged 1024-row tile of distances
+    // (red mode: no merge staging — every CTA keeps the label sums, below)
+    const size_t merge = redm ? 0 : al16(ppc * G * 8) + al16((ppc / (size_t)n + 2) * G * 4);
+    // exact-sum mode: a staged 1024-row tile of distances (red mode: in the rows' region when it is large enough)
+    const size_t tailf = redm && L.cb - L.xs >= (size_t)kTile * 8 ? 0 : (size_t)kTile * 8;
     size_t u = ls > sort ? ls : sort;
     u = u > merge ? u : merge;
     u = u > tailf ? u : tailf;
@@ -301,7 +305,11 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
     L.cf = o;
     if (!tc) o = al16(o + (size_t)kCKMax * nd * 4);
     L.cd = o;
-    o = al16(o + (size_t)kCKMax * chunk_cdld(n) * 8);
+    o = al16(o + (size_t)k * chunk_cdld(n) * 8);
+    L.ssum = o;  // red mode: running label sums [k][cdld] (fp64) and member counts
+    if (redm) o = al16(o + (size_t)k * chunk_cdld(n) * 8);
+    L.scnt = o;  // [kCKMax] 1.0 / count (fp64), then [kCKMax] counts
+    if (redm) o = al16(o + (size_t)kCKMax * 12);
     L.nrm = o;
     o = al16(o + 3 * kCKMax * 4);
     L.act = o;
@@ -349,7 +357,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     const int B = a.B, n = a.n, k = a.k, xld = a.xld;
     const uint64_t p0 = static_cast<uint64_t>(cta) * B;
     const int np = static_cast<int>(min(static_cast<uint64_t>(B), a.rows - p0));
-    const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G, TC);
+    const bool RED = a.red != 0;  // exact-sum data: RED deltas, one grid barrier per round
+    const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G, TC, RED);
     // tc: operand tiles need a 1024-byte aligned base (128-byte swizzle atoms)
     unsigned char* sm = TC ? sm_raw + ((1024u - (smem_addr(sm_raw) & 1023u)) & 1023u)
                            : sm_raw + ((128u - (smem_addr(sm_raw) & 127u)) & 127u);
@@ -367,6 +376,10 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     int* lab = reinterpret_cast<int*>(sm + L.lab);
     double* dist = reinterpret_cast<double*>(sm + L.dist);
     double* red = reinterpret_cast<double*>(sm + L.red);
+    double* ssum = reinterpret_cast<double*>(sm + L.ssum);  // red mode
+    double* sinv = reinterpret_cast<double*>(sm + L.scnt);
+    int* scnt = reinterpret_cast<int*>(sm + L.scnt + kCKMax * 8);
+    const int kn = k * n;
     __shared__ CCtl ctl;
     __shared__ int s_any;
     __shared__ unsigned s_tmem;
@@ -418,19 +431,63 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
     };
 
+    // Tensor-core screen: one thread issues the tile MMAs and their commit:
+    // D[tile] = rows . (hi + lo)^T over K
+    auto issue_mma = [&]() {
+        tc_fence_after();
+        // descriptors from their 14-bit start-address field (units of
+        // 16 B); k-steps outer, tiles inner: consecutive MMAs feed
+        // different accumulators
+        const unsigned ua0 = smem_addr(sm + L.xs) >> 4;  // start addresses, 16-byte units
+        const unsigned ub0 = smem_addr(sm + L.cb) >> 4;
+        const int ntl = MP / 128;
+        // k-steps of 8 dims (dims n..ND-1 are zero in both operands);
+        // D[tile] (64 columns) = rows . [hi | lo]^T
+        constexpr int KSTEPS = ND / 8;
+        for (int ks = 0; ks < KSTEPS; ++ks) {
+            const unsigned ko = ((ks & 3) * 32) >> 4;
+            const unsigned bo = (((ks >> 2) * 2 * kCKMax * 128) >> 4) + ko;
+            const unsigned ao = static_cast<unsigned>((static_cast<size_t>(ks >> 2) * ASZ) >> 4) + ko;
+            const unsigned long long db = umma_desc_sw128_units(ub0 + bo);
+            for (int t = 0; t < ntl; ++t) {
+                const unsigned long long da = umma_desc_sw128_units(ua0 + ao + static_cast<unsigned>(t) * (16384 >> 4));
+                umma_tf32(s_tmem + 64u * t, da, db, ks > 0);
+            }
+        }
+        umma_commit(&s_mbar);
+    };
     int prevKA = 0;  // tc: B operand rows holding values (the rest are 0)
     // C (global) -> compacted active rows: fp64 (exact recheck) and the screen's
     // fp32 / tf32 hi+lo copies, then their certified fp32 norms
-    auto load_centroids = [&](int rr) {
+    auto load_centroids = [&](int rr, unsigned long long r) {
+        const bool own = RED && r > 0;  // centroids from this CTA's label sums (core.cpp:231-242)
+        if (own) {
+            // label sums += the deltas of the previous assignment (exact sums: any order)
+            const double* dsrc = a.dsum + static_cast<size_t>((r - 1) % 3) * kn;
+            batched_copy<4>(kn, tid, NT, [&](int e) { return __ldcg(dsrc + e); },
+                            [&](int e, double v) {
+                                const int j = e / n;
+                                double* sp = ssum + j * cdld + (e - j * n);
+                                *sp = __dadd_rn(*sp, v);
+                            });
+            if (tid < k) {
+                const int c = scnt[tid] + __ldcg(a.dcnt + ((r - 1) % 3) * k + tid);
+                scnt[tid] = c;
+                sinv[tid] = c > 0 ? __ddiv_rn(1.0, static_cast<double>(c)) : 0.0;  // :237-239
+            }
+            __syncthreads();
+        }
+        CDBG(rr, 10);
         // the active list from the mask, then the active rows with every load
         // of a thread in flight at once (U = 4)
         if (warp == 0) {
-            const bool live = lane < k && !__ldcg(a.mask + lane);
+            const bool live = lane < k && (own ? scnt[lane] > 0 : !__ldcg(a.mask + lane));
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
             if (live) act[__popc(bal & ((1u << lane) - 1u))] = lane;
             if (lane == 0) act[kCKMax] = __popc(bal);
         }
         __syncthreads();
+        CDBG(rr, 11);
         const int KA = act[kCKMax];
         if constexpr (TC) {
             // B operand of K-atom ka: 64 rows = [hi of slots 0..31][lo of slots 0..31] (one N = 64 MMA per k-step)
@@ -443,8 +500,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             batched_copy<4>(
                 KA * n, tid, NT,
                 [&](int e) {
-                    const int rk = e / n;
-                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+                    const int rk = e / n, j = act[rk];
+                    if (own) return __dmul_rn(ssum[j * cdld + (e - rk * n)], sinv[j]);
+                    return __ldcg(a.C + static_cast<size_t>(j) * n + (e - rk * n));
                 },
                 [&](int e, double v) {
                     const int rk = e / n, d = e - rk * n;
@@ -466,8 +524,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             batched_copy<4>(
                 KA * n, tid, NT,
                 [&](int e) {
-                    const int rk = e / n;
-                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
+                    const int rk = e / n, j = act[rk];
+                    if (own) return __dmul_rn(ssum[j * cdld + (e - rk * n)], sinv[j]);
+                    return __ldcg(a.C + static_cast<size_t>(j) * n + (e - rk * n));
                 },
                 [&](int e, double v) {
                     const int rk = e / n, d = e - rk * n;
@@ -476,7 +535,15 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 });
         }
         __syncthreads();
-        for (int rk = warp; rk < KA; rk += NW) {
+        if (rr > 0) CDBG(rr, 13);
+        // tensor core, rounds >= 1 (round 0 waits for the rows): the last warp
+        // issues the MMAs while the other warps take the norms
+        const bool split = TC && r > 0 && NW > 1;
+        if constexpr (TC) {
+            if (r > 0 && tid == (NW > 1 ? (NW - 1) * 32 : 0)) issue_mma();
+        }
+        const int NWN = split ? NW - 1 : NW;
+        for (int rk = warp; rk < KA && warp < NWN; rk += NWN) {
             float lo = 0.f, hi = 0.f;
             for (int d = lane; d < n; d += 32) {
                 const float f = TC ? __double2float_rn(cd[rk * cdld + d]) : cf[rk * ND + d];
@@ -527,8 +594,12 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             for (int e = tid; e < NKA * kCKMax * 8 * 2; e += NT)  // the B operands start at 0
                 reinterpret_cast<float4*>(sm + L.cb)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        if (RED) {
+            for (int e = tid; e < k * cdld; e += NT) ssum[e] = 0.0;
+            if (tid < kCKMax) scnt[tid] = 0;
+        }
         __syncthreads();
-        load_centroids(0);
+        load_centroids(0, 0);
         mbar_wait(&s_xbar, 0);
         CDBG(0, 13);
 #ifdef BM_CHUNK_MMA_DIAG
@@ -690,39 +761,19 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     }
 
     const uint64_t ntiles = tiles_of(a.rows);
+    bool part_valid = true;  // red mode: part[cta] holds this CTA's label partials of the last assignment
     for (unsigned long long r = 0;; ++r) {
         const int rr = r < 7 ? static_cast<int>(r) : 7;
         CDBG(rr, 0);
-        const int slot = static_cast<int>(r & 1);
+        const int slot = static_cast<int>(r & 1);                   // distance slot
+        const int rslot = RED ? static_cast<int>(r % 3) : slot;     // round sums / changed flags
         // ---- centroids: C (global) -> compacted fp64 / fp32 rows + norms ----
         // (round 0: loaded while the rows were in flight)
-        if (r > 0) load_centroids(rr);
+        if (r > 0) load_centroids(rr, r);
         const int KA = act[kCKMax];
         if constexpr (TC) {
-            // thread 0 issues the tile MMAs and their commit: D[tile] = rows . (hi + lo)^T over K
-            if (tid == 0) {
-                tc_fence_after();
-                // descriptors from their 14-bit start-address field (units of
-                // 16 B); k-steps outer, tiles inner: consecutive MMAs feed
-                // different accumulators
-                const unsigned ua0 = smem_addr(sm + L.xs) >> 4;  // start addresses, 16-byte units
-                const unsigned ub0 = smem_addr(sm + L.cb) >> 4;
-                const int ntl = MP / 128;
-                // k-steps of 8 dims (dims n..ND-1 are zero in both operands);
-                // D[tile] (64 columns) = rows . [hi | lo]^T
-                constexpr int KSTEPS = ND / 8;
-                for (int ks = 0; ks < KSTEPS; ++ks) {
-                    const unsigned ko = ((ks & 3) * 32) >> 4;
-                    const unsigned bo = (((ks >> 2) * 2 * kCKMax * 128) >> 4) + ko;
-                    const unsigned ao = static_cast<unsigned>((static_cast<size_t>(ks >> 2) * ASZ) >> 4) + ko;
-                    const unsigned long long db = umma_desc_sw128_units(ub0 + bo);
-                    for (int t = 0; t < ntl; ++t) {
-                        const unsigned long long da = umma_desc_sw128_units(ua0 + ao + static_cast<unsigned>(t) * (16384 >> 4));
-                        umma_tf32(s_tmem + 64u * t, da, db, ks > 0);
-                    }
-                }
-                umma_commit(&s_mbar);
-            }
+            // round 0: the rows have landed by now (later rounds: issued inside load_centroids)
+            if (r == 0 && tid == 0) issue_mma();
         }
         __syncthreads();
         if (KA == 0) {  // assign_nearest on all-degenerate centroids (core.cpp:115-118)
@@ -942,13 +993,13 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
         }
         CDBG(rr, 9);
-        CDBG(rr, 10);
-        CDBG(rr, 11);
         unsigned chg = 0;  // labels this thread's points left or joined (r > 0)
+        int oldlab[PPT];   // red mode: the label a moved point left (-1: not moved)
         double mysum = 0.0;
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const int p = tid + i * NT;
+            oldlab[i] = -1;
             if (p >= np) continue;
             double best = dinf;
             int bj = -1;
@@ -975,22 +1026,33 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 if (bj < 0) bj = 0;  // (NaN distances only; unreachable for finite data)
             }
             const int label = act[bj];
-            if (r > 0 && label != mylab[i]) chg |= (1u << label) | (1u << mylab[i]);
+            if (r > 0 && label != mylab[i]) {
+                chg |= (1u << label) | (1u << mylab[i]);
+                oldlab[i] = mylab[i];
+            }
             mylab[i] = label;
             lab[p] = label;
             dist[p] = best;
             a.dists[static_cast<size_t>(slot) * a.rows + p0 + p] = best;
             mysum += best;
         }
+        int nmoved = 0;
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) nmoved += oldlab[i] >= 0 ? 1 : 0;
         __syncthreads();  // red / wsum reuse below
         // CTA sum of the distances (unordered: certified interval below)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mysum += __shfl_down_sync(0xFFFFFFFFu, mysum, o);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) chg |= __shfl_xor_sync(0xFFFFFFFFu, chg, o);
+        if (RED) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nmoved += __shfl_xor_sync(0xFFFFFFFFu, nmoved, o);
+        }
         if (lane == 0) {
             red[warp] = mysum;
             reinterpret_cast<unsigned*>(red + 32)[warp] = chg;
+            reinterpret_cast<int*>(red + 32)[32 + warp] = nmoved;
         }
         __syncthreads();
         // labels whose membership changed in this tile (round 0: all of them);
@@ -1001,13 +1063,25 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         if (tid == 0) {
             double s = 0.0;
             for (int w = 0; w < NW; ++w) s += red[w];
-            atomicAdd(a.rsum + slot, s);
-            if (r > 0 && dirty) atomicOr(a.rchg + slot, static_cast<int>(dirty));
+            atomicAdd(a.rsum + rslot, s);
+            if (r > 0 && dirty) atomicOr(a.rchg + rslot, static_cast<int>(dirty));
+        }
+        // red mode: the deltas of this assignment's label sums go to dsum[r % 3]
+        // — refolded labels (new partial - old partial) while this CTA's
+        // partials are current and many points moved, else per moved point
+        double* dcur = a.dsum + static_cast<size_t>(r % 3) * kn;
+        int* ccur = a.dcnt + (r % 3) * k;
+        bool refold = true;
+        if (RED && r > 0) {
+            int mv = 0;
+            for (int w = 0; w < NW; ++w) mv += reinterpret_cast<const int*>(red + 32)[32 + w];
+            refold = part_valid && mv * 8 > np;
+            if (!refold) part_valid = false;
         }
 
         CDBG(rr, 3);
         // ---- speculative update partials of the new labels (core.cpp:200-215) ----
-        if (dirty) {
+        if (dirty && refold) {
             const int nc = (np + 31) / 32;
             unsigned char* up = sm + L.u;
             uint16_t* members = reinterpret_cast<uint16_t*>(up);
@@ -1113,23 +1187,66 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
 #pragma unroll
                 for (int t = 0; t < DPL; ++t) {
                     const int d = gl + LG * t;
-                    if (d < n) a.part[static_cast<size_t>(cta) * k * n + static_cast<size_t>(j) * n + d] = acc[t];
+                    if (d < n) {
+                        double* pp = a.part + static_cast<size_t>(cta) * k * n + static_cast<size_t>(j) * n + d;
+                        if (RED) {  // this thread wrote *pp in the earlier rounds
+                            const double dl = r > 0 ? __dsub_rn(acc[t], __ldcg(pp)) : acc[t];
+                            if (dl != 0.0) atomicAdd(dcur + j * n + d, dl);
+                        }
+                        *pp = acc[t];
+                    }
                 }
-                if (gl == 0) a.pcnt[static_cast<size_t>(cta) * k + j] = static_cast<unsigned>(e - b);
+                if (gl == 0) {
+                    unsigned* pc = a.pcnt + static_cast<size_t>(cta) * k + j;
+                    if (RED) {
+                        const int dc = (e - b) - (r > 0 ? static_cast<int>(__ldcg(pc)) : 0);
+                        if (dc) atomicAdd(ccur + j, dc);
+                    }
+                    *pc = static_cast<unsigned>(e - b);
+                }
             }
+            CDBG(rr, 14);
+        }
+        if (RED && !refold) {  // per moved point: + its row to the new label's sums, - to the old one's
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                unsigned bal = __ballot_sync(0xFFFFFFFFu, oldlab[i] >= 0);
+                while (bal) {
+                    const int src = __ffs(bal) - 1;
+                    bal &= bal - 1;
+                    const int pm = __shfl_sync(0xFFFFFFFFu, tid + i * NT, src);
+                    const int ln = __shfl_sync(0xFFFFFFFFu, mylab[i], src);
+                    const int lo = __shfl_sync(0xFFFFFFFFu, oldlab[i], src);
+                    for (int d = lane; d < n; d += 32) {
+                        const double x = to_f64(xat(pm, d));
+                        if (x != 0.0) {
+                            atomicAdd(dcur + ln * n + d, x);
+                            atomicAdd(dcur + lo * n + d, -x);
+                        }
+                    }
+                    if (lane == 0) {
+                        atomicAdd(ccur + ln, 1);
+                        atomicAdd(ccur + lo, -1);
+                    }
+                }
+            }
+        }
+        const int ppc = (kn + static_cast<int>(G) - 1) / static_cast<int>(G);
+        const int q0 = static_cast<int>(cta) * ppc, q1 = min(kn, q0 + ppc);
+        if (RED) {  // this CTA's share of the next round's delta buffer (last read a round ago)
+            double* dnx = a.dsum + static_cast<size_t>((r + 1) % 3) * kn;
+            for (int q = q0 + tid; q < q1; q += NT) dnx[q] = 0.0;
+            if (cta == 0 && tid < k) a.dcnt[((r + 1) % 3) * k + tid] = 0;
         }
         CDBG(rr, 4);
         grid_sync(a.bar, G);  // ---------------- barrier A ----------------
         CDBG(rr, 5);
         // this CTA's merge pairs: their tile partials and counts staged now
         // (speculatively: discarded when the loop stops), overlapping the control
-        const int kn = k * n;
-        const int ppc = (kn + static_cast<int>(G) - 1) / static_cast<int>(G);
-        const int q0 = static_cast<int>(cta) * ppc, q1 = min(kn, q0 + ppc);
         double* stage = reinterpret_cast<double*>(sm + L.u);
         unsigned* cstage = reinterpret_cast<unsigned*>(sm + L.u + al16(static_cast<size_t>(ppc) * G * 8));
         const int mj0 = q0 / n;
-        if (q0 < q1) {  // part[g][q] -> stage[q - q0][g], pcnt[g][j] -> cstage[j - mj0][g]
+        if (!RED && q0 < q1) {  // part[g][q] -> stage[q - q0][g], pcnt[g][j] -> cstage[j - mj0][g]
             const int nq = q1 - q0, nj = (q1 - 1) / n - mj0 + 1;
             batched_copy<4>(
                 nq * static_cast<int>(G), tid, NT,
@@ -1155,8 +1272,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
 
         // ---- Lloyd control (local_search.cpp:26-51), every CTA identically ----
         if (tid == 0) {
-            const double s = __ldcg(a.rsum + slot);
-            const int chg_all = __ldcg(a.rchg + slot);
+            const double s = __ldcg(a.rsum + rslot);
+            const int chg_all = __ldcg(a.rchg + rslot);
             ctl.gdirty = r == 0 ? 0xFFFFFFFFu : static_cast<unsigned>(chg_all);
             double lo, hi;
             sum_interval(s, a.rows, G, &lo, &hi);
@@ -1217,7 +1334,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
                 const bool stop = __ddiv_rn(__dsub_rn(f, fn), f) < a.rel_tolerance;
                 ctl.stop = stop ? 1 : 0;
                 if (!stop) {
-                    const double s = __ldcg(a.rsum + slot);
+                    const double s = __ldcg(a.rsum + rslot);
                     double lo, hi;
                     sum_interval(s, a.rows, G, &lo, &hi);
                     ctl.f = s;
@@ -1232,11 +1349,14 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             __syncthreads();
         }
         if (ctl.stop) break;
-        // the other round slot: nobody reads it again before the next barrier B
+        // a round slot nobody reads again before it is next added to (two
+        // barriers per round: the other one; red mode: the one before this)
         if (cta == 0 && tid == 0) {
-            a.rsum[slot ^ 1] = 0.0;
-            a.rchg[slot ^ 1] = 0;
+            const int zs = RED ? static_cast<int>((r + 2) % 3) : slot ^ 1;
+            a.rsum[zs] = 0.0;
+            a.rchg[zs] = 0;
         }
+        if (RED) continue;  // the next round forms its centroids from the label sums
 
         CDBG(rr, 6);
         // ---- merge (core.cpp:217-242): this CTA's (label, dim) pairs, tile order ----
@@ -1275,6 +1395,15 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         CDBG(rr, 8);
     }
 
+    // every control read of this CTA is done: CTA 0 resets the round slots
+    // once all CTAs are here (bar[2])
+    if (tid == 0 && cta != 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 2) : "memory");
+    if (RED) {  // nobody reads a delta buffer after the last barrier: dsum[0] / dcnt[0] zero for the next launch
+        const int ppc = (kn + static_cast<int>(G) - 1) / static_cast<int>(G);
+        const int q0 = static_cast<int>(cta) * ppc, q1 = min(kn, q0 + ppc);
+        for (int q = q0 + tid; q < q1; q += NT) a.dsum[q] = 0.0;
+        if (cta == 0 && tid < k) a.dcnt[tid] = 0;
+    }
     if constexpr (TC) {  // the accumulators are no longer needed
         tc_fence_before();
         __syncthreads();
@@ -1312,7 +1441,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         if (a.ordered) {
             if (tid == 0) a.tiles[cta] = fold_smem(dist, np);
         } else if (cta < ntiles) {
-            double* stage = reinterpret_cast<double*>(sm + L.u);
+            // (red mode: the rows are no longer needed, their region stages the tile)
+            double* stage = reinterpret_cast<double*>(sm + (RED && L.cb - L.xs >= kTile * 8 ? L.xs : L.u));
             const uint64_t tb = static_cast<uint64_t>(cta) * kTile;
             const int len = static_cast<int>(min(static_cast<uint64_t>(kTile), a.rows - tb));
             const double* src = a.dists + static_cast<size_t>(fslot) * a.rows + tb;
@@ -1368,23 +1498,40 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             jb->valid = 1;
         }
         *a.chunk_ctr = chunk + 1;
-        a.rsum[0] = 0.0;  // every CTA read the round slots before its last barrier
-        a.rsum[1] = 0.0;
-        a.rchg[0] = 0;
-        a.rchg[1] = 0;
+        while (ld_acquire(a.bar + 2) < G - 1) {  // every CTA has read the round slots
+        }
+        a.bar[2] = 0;
+        for (int z = 0; z < 3; ++z) {
+            a.rsum[z] = 0.0;
+            a.rchg[z] = 0;
+        }
     }
     __syncthreads();
     const int accepted = s_acc;
     // incumbent := trained (accepted); next start (:82) := incumbent
+    // (red mode: the trained centroids are this CTA's label sums / counts — C
+    // and mask in global memory still hold the start)
+    const bool own = RED && ctl.iterations >= 1;
     for (int j = tid; j < k; j += NT) {
-        const uint8_t mv = accepted ? __ldcg(a.mask + j) : __ldcg(a.maskinc + j);
+        const uint8_t mv = !accepted ? __ldcg(a.maskinc + j) : own ? (scnt[j] > 0 ? 0 : 1) : __ldcg(a.mask + j);
         s_mk[j] = mv;
         if (accepted) a.maskinc[j] = mv;
-        else a.mask[j] = mv;
+        if (!accepted || own) a.mask[j] = mv;
     }
     for (int e = tid; e < k * n; e += NT) {
-        if (accepted) a.Cinc[e] = __ldcg(a.C + e);
-        else a.C[e] = __ldcg(a.Cinc + e);
+        if (accepted) {
+            double v;
+            if (own) {
+                const int j = e / n;
+                v = scnt[j] > 0 ? __dmul_rn(ssum[j * cdld + (e - j * n)], sinv[j]) : 0.0;  // core.cpp:231-242
+                a.C[e] = v;
+            } else {
+                v = __ldcg(a.C + e);
+            }
+            a.Cinc[e] = v;
+        } else {
+            a.C[e] = __ldcg(a.Cinc + e);
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -1556,7 +1703,7 @@ dev::ScreenConsts chunk_screen_consts(int n, bool tc, bool rows_tf32_exact) {
     return c;
 }
 
-ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc) {
+ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc, bool red) {
     tc = tc && storage == BM_F32;
     ChunkPlan p;
     if (k < 1 || k > dev::kCKMax || n < 1 || s < 1 || s > (1ull << 31)) return p;
@@ -1591,7 +1738,8 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
     }
     const unsigned grid = static_cast<unsigned>((s + B - 1) / B);
     if (grid > static_cast<unsigned>(sms)) return p;  // one CTA per SM, all co-resident
-    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid, tc);
+    red = red && exact_sums;
+    const dev::CLayout L = dev::chunk_layout(B, xld, es, k, in->nd, n, grid, tc, red);
     if (L.total + 2048 > static_cast<size_t>(smem_optin)) return p;
     // the previous chunk's k_chunk_fix must find room next to this kernel's
     // CTAs (the accept waits for it): a free SM, or room on every SM
@@ -1604,6 +1752,7 @@ ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, boo
     p.nd = in->nd;
     p.xld = xld;
     p.ordered = exact_sums ? 0 : 1;
+    p.red = red ? 1 : 0;
     p.grid = grid;
     p.smem = L.total;
     return p;
@@ -1658,6 +1807,7 @@ void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const d
     a.B = p.B;
     a.xld = p.xld;
     a.ordered = p.ordered;
+    a.red = p.red;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
     cfg.blockDim = dim3(p.threads);
@@ -1667,7 +1817,8 @@ void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const d
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    static const bool coop = !(std::getenv("BM_CHUNK_COOP") && std::string(std::getenv("BM_CHUNK_COOP")) == "0");
+    cfg.numAttrs = coop ? 1 : 0;
     void* args[] = {&a};
     BM_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
 }

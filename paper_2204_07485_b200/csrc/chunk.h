@@ -52,9 +52,16 @@ struct ChunkArgs {
     unsigned* pcnt;           // member counts [G][k]
     double* dists;            // [2][rows]: the distances of the last two assignments
     double* tiles;            // [2][ntiles]: exact 1024-tile partials (tolerance fallback, accept)
-    unsigned* bar;            // grid barrier: [0] arrivals, [1] generation
-    double* rsum;             // [2] per-round fast distance sums (slot = round & 1)
-    int* rchg;                // [2] per-round "a label changed" flags
+    unsigned* bar;            // grid barrier: [0] arrivals, [1] generation; [2] CTAs past their last control read
+    double* rsum;             // [3] per-round fast distance sums (slot = round & 1; red mode: round % 3)
+    int* rchg;                // [3] per-round "a label changed" flags
+    // red mode (exact-sum data, one grid barrier per round): label-sum deltas
+    // of round r's assignment, added by RED into dsum[r % 3] / dcnt[r % 3];
+    // every CTA keeps the running sums in shared memory and forms the
+    // centroids itself (any order of exact sums gives the reference's bits)
+    int red;
+    double* dsum;             // [3][k*n], all zero between launches
+    int* dcnt;                // [3][k]
     ScreenConsts cst;         // screen bounds: packed-FFMA (fp64 rows) / tensor core, rows exact in tf32
     ScreenConsts cst_loose;   // tensor core, rows not exact in tf32 (truncated by the MMA)
     unsigned long long max_iterations;
@@ -98,11 +105,12 @@ struct ChunkPlan {
     bool ok = false;
     bool tc = false;  // tensor-core screen (fp32 rows, swizzled layout)
     int B = 0, threads = 0, ppt = 0, nd = 0, xld = 0, ordered = 0;
+    int red = 0;      // exact sums by RED deltas, one grid barrier per round
     unsigned grid = 0;
     size_t smem = 0;
 };
 
-ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc);
+ChunkPlan chunk_plan(int device, uint64_t s, int n, int k, bm_dtype storage, bool exact_sums, bool tc, bool red = true);
 // The row tensor map of one gathered chunk buffer for a plan.
 CUtensorMap chunk_rows_map(const ChunkPlan& p, bm_dtype storage, const void* X, uint64_t rows, int n, uint64_t ld);
 // Enqueue one chunk (cooperative launch, capturable into a graph).

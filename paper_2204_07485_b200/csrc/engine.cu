@@ -192,7 +192,8 @@ struct Workspace {
     DevBuf<unsigned long long> chunk_ctr;  // device-side chunk index
     // persistent chunk kernel (chunk.cu): update partials, tile partials, grid
     // barrier, per-round sums / flags, per-chunk timing stamps
-    DevBuf<double> cpart, ctiles, crsum;
+    DevBuf<double> cpart, ctiles, crsum, cdsum;
+    DevBuf<int> cdcnt;
     DevBuf<unsigned> cpcnt, cbar;
     DevBuf<int> crchg;
     DevBuf<unsigned long long> ctiming;
@@ -242,12 +243,18 @@ struct Workspace {
         if (cpcnt.n < (uint64_t)k * p.grid) cpcnt.alloc((uint64_t)k * p.grid);
         if (ctiles.n < 2 * tiles) ctiles.alloc(2 * tiles);
         if (!cbar.n) {
-            cbar.alloc(2);
-            BM_CUDA(cudaMemset(cbar.p, 0, 2 * sizeof(unsigned)));
-            crsum.alloc(2);
-            BM_CUDA(cudaMemset(crsum.p, 0, 2 * sizeof(double)));
-            crchg.alloc(2);
-            BM_CUDA(cudaMemset(crchg.p, 0, 2 * sizeof(int)));
+            cbar.alloc(4);
+            BM_CUDA(cudaMemset(cbar.p, 0, 4 * sizeof(unsigned)));
+            crsum.alloc(3);
+            BM_CUDA(cudaMemset(crsum.p, 0, 3 * sizeof(double)));
+            crchg.alloc(3);
+            BM_CUDA(cudaMemset(crchg.p, 0, 3 * sizeof(int)));
+        }
+        if (cdsum.n < 3 * kn) {  // red mode: label-sum deltas, all zero between launches
+            cdsum.alloc(3 * kn);
+            BM_CUDA(cudaMemset(cdsum.p, 0, 3 * kn * sizeof(double)));
+            cdcnt.alloc(3 * (uint64_t)k);
+            BM_CUDA(cudaMemset(cdcnt.p, 0, 3 * (uint64_t)k * sizeof(int)));
         }
     }
     // CUDA graphs of one chunk (sample resolution + gather, and the Lloyd loop)
@@ -373,6 +380,35 @@ struct SamplerWs {
     DevBuf<uint32_t> js, js2, bitmap, blockcnt, idx;  // js2: second target buffer (pipelined draws)
     DevBuf<unsigned long long> hkeys, hvals, LT;      // epoch-tagged resolution tables
     DevBuf<uint32_t> exclbits;                        // values < s leaving the first s positions
+    // Resolution tables (set 0 = the members above; set 1 = a second copy):
+    // the graph pipeline resolves odd chunks (target buffer 1) in set 1 on a
+    // second prep stream, so that two chunks' preps overlap.  Each set sees
+    // increasing epochs (the draws into its target buffer).
+    struct Tabs {
+        uint32_t *bitmap, *blockcnt, *idx, *exclbits;
+        unsigned long long *hkeys, *hvals, *LT;
+    };
+    DevBuf<uint32_t> bitmap1, blockcnt1, idx1, exclbits1;
+    DevBuf<unsigned long long> hkeys1, hvals1, LT1;
+    Tabs tabs(int set) {
+        if (set && !idx1.n) {  // allocated on first use (graph pipeline only)
+            const size_t h = (size_t)hmask + 1;
+            hkeys1.alloc(h);
+            hvals1.alloc(h);
+            BM_CUDA(cudaMemset(hkeys1.p, 0, h * sizeof(unsigned long long)));
+            BM_CUDA(cudaMemset(hvals1.p, 0, h * sizeof(unsigned long long)));
+            bitmap1.alloc(nwords);
+            BM_CUDA(cudaMemset(bitmap1.p, 0, nwords * sizeof(uint32_t)));
+            blockcnt1.alloc(std::max<uint32_t>(nblocks, 1));
+            idx1.alloc(s);
+            LT1.alloc(s);
+            BM_CUDA(cudaMemset(LT1.p, 0, s * sizeof(unsigned long long)));
+            exclbits1.alloc(ceil_div(s, 32));
+            BM_CUDA(cudaMemset(exclbits1.p, 0, ceil_div(s, 32) * sizeof(uint32_t)));
+        }
+        if (set) return Tabs{bitmap1.p, blockcnt1.p, idx1.p, exclbits1.p, hkeys1.p, hvals1.p, LT1.p};
+        return Tabs{bitmap.p, blockcnt.p, idx.p, exclbits.p, hkeys.p, hvals.p, LT.p};
+    }
     DevBuf<uint32_t> epoch;                           // [0] counter, [1+b] epoch of target buffer b
     cudaStream_t rng_stream = nullptr;                      // device draws of the next chunk
     cudaEvent_t drawn[2] = {nullptr, nullptr}, resolved[2] = {nullptr, nullptr};
@@ -478,7 +514,8 @@ struct DeviceCache {
     std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<SamplerWs>> sws;
     DevBuf<uint8_t> chunk;        // gathered chunk, s * ld * elem
     DevBuf<uint8_t> chunk1, chunk2, chunk3;  // graph mode: chunks c+1..c+3 are gathered while chunk c runs
-    cudaStream_t pstream = nullptr;  // graph mode: prep (resolution + gather) of the next chunk
+    cudaStream_t pstream = nullptr;  // graph mode: prep (resolution + gather) of the coming even chunks
+    cudaStream_t pstream2 = nullptr; // ... and of the odd chunks (their own resolution tables)
     cudaStream_t sstream = nullptr;  // graph mode: speculative begin of the next chunk
     DevBuf<int32_t> flabels;      // final pass
     DevBuf<double> fdists, ftiles;
@@ -488,6 +525,7 @@ struct DeviceCache {
         sws.clear();
         if (stream) cudaStreamDestroy(stream);
         if (pstream) cudaStreamDestroy(pstream);
+        if (pstream2) cudaStreamDestroy(pstream2);
         if (sstream) cudaStreamDestroy(sstream);
     }
     void ensure_final(uint64_t rows) {
@@ -1459,20 +1497,18 @@ void get_stream(cudaStream_t st, SamplerWs& sw, Mt64& rng, int slot = 0) {
 }
 
 // Fisher-Yates resolution of the targets in buffer b (epoch-tagged tables, no
-// clearing between chunks); result in sw.idx.
-void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw, int b = 0) {
+// clearing between chunks); result in the table set's idx (set 0: sw.idx).
+void enqueue_resolve_device(cudaStream_t st, SamplerWs& sw, int b = 0, int set = 0) {
     PhaseScope ps(PH_SAMPLE, sw.s);
     const uint32_t s = (uint32_t)sw.s;
     const uint32_t* js = sw.jsbuf(b);
     const uint32_t* ep = sw.epoch_slot(b);
     const unsigned g = (unsigned)ceil_div(s, 256);
-    dev::k_fy_pass1<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask);
-    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, ep, s, sw.LT.p, sw.hkeys.p, sw.hvals.p, sw.hmask, sw.exclbits.p,
-                                       sw.bitmap.p);
-    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.exclbits.p, s,
-                                                                         sw.nwords, sw.blockcnt.p);
-    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(sw.bitmap.p, sw.exclbits.p, s, sw.nwords,
-                                                                 sw.blockcnt.p, sw.idx.p);
+    const SamplerWs::Tabs t = sw.tabs(set);
+    dev::k_fy_pass1<<<g, 256, 0, st>>>(js, ep, s, t.LT, t.hkeys, t.hvals, sw.hmask);
+    dev::k_fy_pass2<<<g, 256, 0, st>>>(js, ep, s, t.LT, t.hkeys, t.hvals, sw.hmask, t.exclbits, t.bitmap);
+    dev::k_bitmap_block_counts<<<sw.nblocks, dev::kScanThreads, 0, st>>>(t.bitmap, t.exclbits, s, sw.nwords, t.blockcnt);
+    dev::k_bitmap_emit<<<sw.nblocks, dev::kScanThreads, 0, st>>>(t.bitmap, t.exclbits, s, sw.nwords, t.blockcnt, t.idx);
     BM_LAUNCH();
     count_launch(4);
 }
@@ -1617,6 +1653,16 @@ bool persist_enabled() {
     return on;
 }
 
+// BM_CHUNK_RED=0: exact-sum chunks keep the two-barrier rounds (tile partials
+// merged by their owners) instead of RED deltas with one barrier per round.
+bool chunk_red_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("BM_CHUNK_RED");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
 bool graphs_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("BM_GRAPHS");
@@ -1659,10 +1705,11 @@ void enqueue_accept(cudaStream_t st, Workspace& w) {
 // prep[b]: Fisher-Yates resolution of target buffer b, gather (:79-80), start := incumbent (:82)
 cudaGraphExec_t capture_prep(cudaStream_t st, const bm_dataset* d, SamplerWs& sw, int b, void* chunk) {
     cudaGraph_t g = nullptr;
+    const SamplerWs::Tabs t = sw.tabs(b);  // before the capture: set 1 is allocated on first use
     BM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    enqueue_resolve_device(st, sw, b);
+    enqueue_resolve_device(st, sw, b, b);  // target buffer b in table set b: odd and even chunks' preps overlap
     BM_CUDA(cudaEventRecordWithFlags(sw.resolved[b], st, cudaEventRecordExternal));
-    enqueue_gather(st, d, sw.idx.p, (uint32_t)sw.s, chunk, sw.xslot.p);
+    enqueue_gather(st, d, t.idx, (uint32_t)sw.s, chunk, sw.xslot.p);
     BM_CUDA(cudaStreamEndCapture(st, &g));
     cudaGraphExec_t e = nullptr;
     BM_CUDA(cudaGraphInstantiate(&e, g, 0));
@@ -1881,7 +1928,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
     ChunkPlan cplan;
     if (use_graphs && persist_enabled() && !w.hist_cap)
         cplan = chunk_plan(d->device, s, n, k, d->dtype, d->exact_sums && exact_sums_enabled(),
-                           d->dtype == BM_F32 && tc_screen_enabled(d->tf32_exact));
+                           d->dtype == BM_F32 && tc_screen_enabled(d->tf32_exact), chunk_red_enabled());
     const bool persist = cplan.ok;
     if (persist) {
         prefer_max_smem_carveout();
@@ -1890,6 +1937,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         // (every fix of the previous run finished: its fix stream was synchronized)
         BM_CUDA(cudaMemsetAsync(w.cfix_seq.p, 0, sizeof(unsigned long long), st));
         BM_CUDA(cudaMemsetAsync(w.cjob.p, 0, dev::kStateBufs * sizeof(dev::FixJob), st));
+        BM_CUDA(cudaMemsetAsync(w.cdsum.p, 0, w.cdsum.n * sizeof(double), st));
+        BM_CUDA(cudaMemsetAsync(w.cdcnt.p, 0, w.cdcnt.n * sizeof(int), st));
     }
     // exact-sum mode for the graph chunks (kernels.cuh §5b)
     // (wide rows keep the ordered update: integer label sums over thousands of
@@ -1931,6 +1980,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         // RNG order (big_means.hpp:21-23) is kept: draws made ahead of a repair
         // are discarded and redone after it.
         if (!dc.pstream) BM_CUDA(cudaStreamCreateWithFlags(&dc.pstream, cudaStreamNonBlocking));
+        if (!dc.pstream2) BM_CUDA(cudaStreamCreateWithFlags(&dc.pstream2, cudaStreamNonBlocking));
         for (int i = 0; i < dev::kStateBufs; ++i) {
             if (!w.ev_lloyd[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_lloyd[i], cudaEventDisableTiming));
             if (!w.ev_prep[i]) BM_CUDA(cudaEventCreateWithFlags(&w.ev_prep[i], cudaEventDisableTiming));
@@ -1938,7 +1988,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
             BM_CUDA(cudaEventRecord(w.ev_spec[i], st));
         }
-        const cudaStream_t pst = dc.pstream;
+        const cudaStream_t pst = dc.pstream, pst2 = dc.pstream2;
         Points bufP[dev::kStateBufs] = {chunkP, chunkP, chunkP, chunkP};
         bufP[1].X = dc.chunk1.p;
         bufP[2].X = dc.chunk2.p;
@@ -1959,12 +2009,13 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         // chunk c's prep (its draws are enqueued on rng_stream: drawn[c % 2])
         auto launch_prep = [&](uint64_t c) {
             const int i = (int)(c % dev::kStateBufs);
-            BM_CUDA(cudaStreamWaitEvent(pst, sw->drawn[c & 1], 0));
-            BM_CUDA(cudaStreamWaitEvent(pst, w.ev_lloyd[i], 0));  // the data buffer's previous chunk (c-4)
-            cudaEvent_t e0 = tl_ev(pst);
-            BM_CUDA(cudaGraphLaunch(w.g_prep[i], pst));
-            if (timeline) tl.push_back({0, e0, tl_ev(pst)});
-            BM_CUDA(cudaEventRecord(w.ev_prep[i], pst));
+            const cudaStream_t ps = (c & 1) ? pst2 : pst;  // same parity: same target buffer and table set, in order
+            BM_CUDA(cudaStreamWaitEvent(ps, sw->drawn[c & 1], 0));
+            BM_CUDA(cudaStreamWaitEvent(ps, w.ev_lloyd[i], 0));  // the data buffer's previous chunk (c-4)
+            cudaEvent_t e0 = tl_ev(ps);
+            BM_CUDA(cudaGraphLaunch(w.g_prep[i], ps));
+            if (timeline) tl.push_back({0, e0, tl_ev(ps)});
+            BM_CUDA(cudaEventRecord(w.ev_prep[i], ps));
             count_launch(6);
         };
         // BM_SPEC=0: no speculative begins (every chunk graph runs its own)
@@ -2022,6 +2073,8 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 a.bar = w.cbar.p;
                 a.rsum = w.crsum.p;
                 a.rchg = w.crchg.p;
+                a.dsum = w.cdsum.p;
+                a.dcnt = w.cdcnt.p;
                 a.cst = chunk_screen_consts(n, cplan.tc, true);
                 a.cst_loose = chunk_screen_consts(n, cplan.tc, false);
                 a.max_iterations = cfg.max_iterations;
@@ -2088,6 +2141,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             if (chunk >= w.drec.n) {  // time-budget runs: grow the record buffer (graphs re-captured)
                 BM_CUDA(cudaStreamSynchronize(st));
                 BM_CUDA(cudaStreamSynchronize(pst));
+                BM_CUDA(cudaStreamSynchronize(pst2));
                 if (dc.sstream) BM_CUDA(cudaStreamSynchronize(dc.sstream));
                 DevBuf<dev::Record> bigger(w.drec.n * 2);
                 BM_CUDA(cudaMemcpyAsync(bigger.p, w.drec.p, w.drec.n * sizeof(dev::Record),
@@ -2178,6 +2232,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
         }
         BM_CUDA(cudaStreamSynchronize(st));
         BM_CUDA(cudaStreamSynchronize(pst));
+        BM_CUDA(cudaStreamSynchronize(pst2));
         if (dc.sstream) BM_CUDA(cudaStreamSynchronize(dc.sstream));
         if (timeline && tl.size() > 2) {
             double dur[3] = {0, 0, 0}, gap = 0;

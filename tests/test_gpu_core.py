@@ -190,7 +190,7 @@ def _modes_agree(base, var, alt, X="np.rint(np.random.default_rng(5).normal(size
 # deferred-objective / carveout switches: same bits, fresh processes.
 @pytest.mark.parametrize("var,alt", [("BM_PERSIST", "0"), ("BM_GRAPHS", "0"), ("BM_STORAGE", "native"),
                                      ("BM_FORCE_EXACT_CONTROL", "1"), ("BM_TC", "0"), ("BM_CHUNK_FIX", "0"),
-                                     ("BM_CARVEOUT", "0"), ("BM_PP", "host")])
+                                     ("BM_CARVEOUT", "0"), ("BM_PP", "host"), ("BM_CHUNK_RED", "0")])
 def test_engine_modes_agree(var, alt):
     _modes_agree({}, var, alt)
 

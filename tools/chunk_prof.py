@@ -13,11 +13,14 @@ chunks = int(sys.argv[2]) if len(sys.argv) > 2 else w.chunks
 X = synthetic.generate(key)
 d = bm.Dataset(X)
 cfg = bm.BigMeansConfig(k=w.k, chunk_size=w.s, max_chunks=chunks, seed=w.seed)
+import time
 for rep in range(3):
+    t0 = time.perf_counter()
     out, tr = bm.big_means(d, cfg, want_labels=False)
+    wall = time.perf_counter() - t0
     p = bm.last_profile()
     n = max(p["chunk_launches"], 1)
-    print(f"{key} rep{rep}: cpu_init {out.counter.cpu_init*1e3:.2f} ms, final {out.counter.cpu_full*1e3:.2f} ms, "
+    print(f"{key} rep{rep}: wall {wall*1e3:.2f} ms, cpu_init {out.counter.cpu_init*1e3:.2f} ms, final {out.counter.cpu_full*1e3:.2f} ms, "
           f"chunk kernels {p['chunk_launches']} avg {p['chunk_ms_total']/n*1e3:.1f} us, gap avg {p['chunk_gap_ms_total']/max(n-1,1)*1e3:.1f} us, "
           f"assign passes/chunk {p['chunk_assign_passes']/n:.2f}, iters {out.counter.iterations}", flush=True)
 
@@ -39,8 +42,12 @@ if os.environ.get("BM_CHUNK_DBG"):
             if row[0] == 0:
                 continue
             segs = [f"{names[i]}->{names[i+1]} {(row[i+1]-row[i])/1e3:.1f}" for i in range(8) if row[i + 1] >= row[i] > 0]
-            if row[9] and row[11]:
-                segs.append(f"[cand {(row[9]-row[2])/1e3:.1f} exact {(row[11]-row[9])/1e3:.1f}]")
+            if row[10] and row[11] and row[15]:  # inside load_centroids
+                segs.append(f"[cent: sums {(row[10]-row[0])/1e3:.1f} active {(row[11]-row[10])/1e3:.1f} "
+                            + (f"copy {(row[13]-row[11])/1e3:.1f} norms {(row[15]-row[13])/1e3:.1f}]" if row[13] > row[11]
+                               else f"copy+norms {(row[15]-row[11])/1e3:.1f}]"))
+            if row[14] > row[12] > 0:
+                segs.append(f"[fold loops {(row[14]-row[12])/1e3:.1f} rest {(row[4]-row[14])/1e3:.1f}]")
             if row[15] > row[0] > 0:
                 segs.append(f"[cent-load {(row[15]-row[0])/1e3:.1f}]")
             if row[12] > row[3] > 0:
