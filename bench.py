@@ -278,12 +278,15 @@ def main():
         return dict(evals=r.local_evals, chunks=r.local_chunks, objective=r.objective,
                     launches=prof["kernel_launches"], prof=prof, cpu_init=0.0, cpu_full=0.0)
 
+    # the clock sampler starts before the warm-up steps: nvidia-smi's own start-up
+    # (NVML init under the driver's locks) would otherwise land in the timed
+    # region and slow its launches; it keeps sampling through the timed steps
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
 
     # ---- timed region (device-resident inputs, no event brackets inside) ----
-    clocks = Clocks(local)
-    clocks.start()
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)

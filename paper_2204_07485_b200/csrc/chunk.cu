@@ -308,8 +308,8 @@ __host__ __device__ inline CLayout chunk_layout(int B, int xld, int es, int k, i
     o = al16(o + (size_t)k * chunk_cdld(n) * 8);
     L.ssum = o;  // red mode: running label sums [k][cdld] (fp64) and member counts
     if (redm) o = al16(o + (size_t)k * chunk_cdld(n) * 8);
-    L.scnt = o;  // [kCKMax] 1.0 / count (fp64), then [kCKMax] counts
-    if (redm) o = al16(o + (size_t)kCKMax * 12);
+    L.scnt = o;  // [kCKMax] 1.0 / count (fp64), then [2][kCKMax] counts (by round parity)
+    if (redm) o = al16(o + (size_t)kCKMax * 16);
     L.nrm = o;
     o = al16(o + 3 * kCKMax * 4);
     L.act = o;
@@ -344,8 +344,9 @@ struct CCtl {
             a.dbg[((s_chunk & 3ull) * 8 + (row)) * 16 + (ph)] = gtimer();                    \
     } while (0)
 
-template <typename T, int ND, int PPT, bool TC>
+template <typename T, int ND, int PPT, bool TC, bool RED>
 __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ ChunkArgs a) {
+    // RED: exact-sum data, label-sum deltas by RED and one grid barrier per round (ChunkArgs::red)
     // TC (fp32 rows): tensor-core screen (tcgen05.mma kind::tf32, TMEM
     // accumulators) over rows in the swizzled K-major layout; otherwise the
     // packed-FFMA screen with the rows in registers (row-major shared rows)
@@ -357,7 +358,6 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     const int B = a.B, n = a.n, k = a.k, xld = a.xld;
     const uint64_t p0 = static_cast<uint64_t>(cta) * B;
     const int np = static_cast<int>(min(static_cast<uint64_t>(B), a.rows - p0));
-    const bool RED = a.red != 0;  // exact-sum data: RED deltas, one grid barrier per round
     const CLayout L = chunk_layout(B, xld, (int)sizeof(T), k, ND, n, G, TC, RED);
     // tc: operand tiles need a 1024-byte aligned base (128-byte swizzle atoms)
     unsigned char* sm = TC ? sm_raw + ((1024u - (smem_addr(sm_raw) & 1023u)) & 1023u)
@@ -388,6 +388,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     const float finf = __int_as_float(0x7F800000);
     const double dinf = __longlong_as_double(0x7FF0000000000000LL);
     __shared__ unsigned long long s_chunk;
+    // (no repair before this chunk: its start is the incumbent's copy — red mode leaves C / mask untouched)
+    const bool start_is_inc = __ldcg(&a.gs->inc_degenerate) == 0;
     if (tid == 0) {
         s_chunk = __ldcg(a.chunk_ctr);  // every CTA: stable until CTA 0's accept (after a grid barrier)
         if (cta == 0 && a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = gtimer();
@@ -461,58 +463,101 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     // fp32 / tf32 hi+lo copies, then their certified fp32 norms
     auto load_centroids = [&](int rr, unsigned long long r) {
         const bool own = RED && r > 0;  // centroids from this CTA's label sums (core.cpp:231-242)
+        // B operand of K-atom ka: 64 rows = [hi of slots 0..31][lo of slots 0..31] (one N = 64 MMA per k-step)
+        unsigned char* cbhi = sm + L.cb;
+        unsigned char* cblo = cbhi + kCKMax * 128;
+        auto boff = [&](int rk, int d) -> size_t {
+            return static_cast<size_t>(d >> 5) * (2 * kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
+                   (d & 3) * 4;
+        };
+        // compacted row rk, dim d := v (fp64 for the recheck, the screen's fp32 / tf32 hi + lo copy)
+        auto put = [&](int rk, int d, double v) {
+            cd[rk * cdld + d] = v;
+            const float f = __double2float_rn(v);
+            if constexpr (TC) {
+                const float hi = tf32_rna(f);
+                const size_t off = boff(rk, d);
+                *reinterpret_cast<float*>(cbhi + off) = hi;
+                *reinterpret_cast<float*>(cblo + off) = f - hi;
+            } else {
+                cf[rk * ND + d] = f;
+            }
+        };
+        int KA;
         if (own) {
-            // label sums += the deltas of the previous assignment (exact sums: any order)
-            const double* dsrc = a.dsum + static_cast<size_t>((r - 1) % 3) * kn;
-            batched_copy<4>(kn, tid, NT, [&](int e) { return __ldcg(dsrc + e); },
-                            [&](int e, double v) {
-                                const int j = e / n;
-                                double* sp = ssum + j * cdld + (e - j * n);
-                                *sp = __dadd_rn(*sp, v);
-                            });
-            if (tid < k) {
-                const int c = scnt[tid] + __ldcg(a.dcnt + ((r - 1) % 3) * k + tid);
-                scnt[tid] = c;
-                sinv[tid] = c > 0 ? __ddiv_rn(1.0, static_cast<double>(c)) : 0.0;  // :237-239
+            // One pass, no CTA barrier inside: every warp takes the member
+            // counts (previous counts + the deltas), their reciprocals
+            // (:237-239) and the active mask; every thread adds the deltas of
+            // the previous assignment to its elements of the label sums (exact
+            // sums: any order) and writes the centroid sum * (1.0 / count) into
+            // the compacted row of its label.
+            const int pr = static_cast<int>((r - 1) % 3);
+            int cj = 0;
+            double inv = 0.0;
+            if (lane < k) {
+                cj = scnt[((r - 1) & 1) * kCKMax + lane] + __ldcg(a.dcnt + pr * k + lane);
+                inv = cj > 0 ? __ddiv_rn(1.0, static_cast<double>(cj)) : 0.0;
+            }
+            const unsigned live = __ballot_sync(0xFFFFFFFFu, lane < k && cj > 0);
+            KA = __popc(live);
+            if (warp == 0) {  // (scnt is double-buffered by round parity: the other warps read the previous counts)
+                if (lane < k) {
+                    scnt[(r & 1) * kCKMax + lane] = cj;
+                    sinv[lane] = inv;
+                    if (cj > 0) act[__popc(live & ((1u << lane) - 1u))] = lane;
+                }
+                if (lane == 0) act[kCKMax] = KA;
+            }
+            const double* dsrc = a.dsum + static_cast<size_t>(pr) * kn;
+            for (int e0 = 0; e0 < kn; e0 += 4 * NT) {  // (warp-uniform trip count: shuffles inside)
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * NT + tid;
+                    v[u] = e < kn ? __ldcg(dsrc + e) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * NT + tid;
+                    const bool ok = e < kn;
+                    const int j = ok ? e / n : 0, d = ok ? e - j * n : 0;
+                    const double invj = __shfl_sync(0xFFFFFFFFu, inv, j);
+                    if (ok) {
+                        double* sp = ssum + j * cdld + d;
+                        const double S = __dadd_rn(*sp, v[u]);
+                        *sp = S;
+                        if ((live >> j) & 1u) put(__popc(live & ((1u << j) - 1u)), d, __dmul_rn(S, invj));
+                    }
+                }
+            }
+            CDBG(rr, 10);
+            CDBG(rr, 11);
+        } else {
+            CDBG(rr, 10);
+            // the active list from the mask, then the active rows with every load
+            // of a thread in flight at once (U = 4)
+            if (warp == 0) {
+                const bool live = lane < k && !__ldcg(a.mask + lane);
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
+                if (live) act[__popc(bal & ((1u << lane) - 1u))] = lane;
+                if (lane == 0) act[kCKMax] = __popc(bal);
             }
             __syncthreads();
-        }
-        CDBG(rr, 10);
-        // the active list from the mask, then the active rows with every load
-        // of a thread in flight at once (U = 4)
-        if (warp == 0) {
-            const bool live = lane < k && (own ? scnt[lane] > 0 : !__ldcg(a.mask + lane));
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, live);
-            if (live) act[__popc(bal & ((1u << lane) - 1u))] = lane;
-            if (lane == 0) act[kCKMax] = __popc(bal);
-        }
-        __syncthreads();
-        CDBG(rr, 11);
-        const int KA = act[kCKMax];
-        if constexpr (TC) {
-            // B operand of K-atom ka: 64 rows = [hi of slots 0..31][lo of slots 0..31] (one N = 64 MMA per k-step)
-            unsigned char* cbhi = sm + L.cb;
-            unsigned char* cblo = cbhi + kCKMax * 128;
-            auto boff = [&](int rk, int d) -> size_t {
-                return static_cast<size_t>(d >> 5) * (2 * kCKMax * 128) + rk * 128 + ((((d >> 2) & 7) ^ (rk & 7)) << 4) +
-                       (d & 3) * 4;
-            };
+            CDBG(rr, 11);
+            KA = act[kCKMax];
             batched_copy<4>(
                 KA * n, tid, NT,
                 [&](int e) {
-                    const int rk = e / n, j = act[rk];
-                    if (own) return __dmul_rn(ssum[j * cdld + (e - rk * n)], sinv[j]);
-                    return __ldcg(a.C + static_cast<size_t>(j) * n + (e - rk * n));
+                    const int rk = e / n;
+                    return __ldcg(a.C + static_cast<size_t>(act[rk]) * n + (e - rk * n));
                 },
                 [&](int e, double v) {
-                    const int rk = e / n, d = e - rk * n;
-                    cd[rk * cdld + d] = v;
-                    const float f = __double2float_rn(v), hi = tf32_rna(f);
-                    const size_t off = boff(rk, d);
-                    *reinterpret_cast<float*>(cbhi + off) = hi;
-                    *reinterpret_cast<float*>(cblo + off) = f - hi;
+                    const int rk = e / n;
+                    put(rk, e - rk * n, v);
                 });
-            for (int e = KA * n + tid; e < prevKA * n; e += NT) {
+        }
+        if constexpr (TC) {
+            for (int e = KA * n + tid; e < prevKA * n; e += NT) {  // rows that held values last round
                 const int rk = e / n, d = e - rk * n;
                 const size_t off = boff(rk, d);
                 *reinterpret_cast<float*>(cbhi + off) = 0.f;
@@ -520,19 +565,6 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             }
             prevKA = KA;
             fence_proxy_async_smem();
-        } else {
-            batched_copy<4>(
-                KA * n, tid, NT,
-                [&](int e) {
-                    const int rk = e / n, j = act[rk];
-                    if (own) return __dmul_rn(ssum[j * cdld + (e - rk * n)], sinv[j]);
-                    return __ldcg(a.C + static_cast<size_t>(j) * n + (e - rk * n));
-                },
-                [&](int e, double v) {
-                    const int rk = e / n, d = e - rk * n;
-                    cd[rk * cdld + d] = v;
-                    cf[rk * ND + d] = __double2float_rn(v);
-                });
         }
         __syncthreads();
         if (rr > 0) CDBG(rr, 13);
@@ -596,9 +628,24 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
         if (RED) {
             for (int e = tid; e < k * cdld; e += NT) ssum[e] = 0.0;
-            if (tid < kCKMax) scnt[tid] = 0;
+            for (int e = tid; e < 2 * kCKMax; e += NT) scnt[e] = 0;
+        }
+        if constexpr (TC) {  // the accumulators (TMEM) and the MMA-completion barrier, while the rows are in flight
+            if (warp == 0) {
+                const unsigned cols = umma::tmem_cols(static_cast<unsigned>(MP / 128) * 64);
+                asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
+                             "r"(cols)
+                             : "memory");
+                asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+            }
+            if (tid == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_mbar)) : "memory");
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            tc_fence_before();
         }
         __syncthreads();
+        if constexpr (TC) tc_fence_after();
         load_centroids(0, 0);
         mbar_wait(&s_xbar, 0);
         CDBG(0, 13);
@@ -654,20 +701,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             }
             xinexact = __syncthreads_or(xinexact);
             fence_proxy_async_smem();
-            if (warp == 0) {
-                const unsigned cols = umma::tmem_cols(static_cast<unsigned>(MP / 128) * 64);
-                asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
-                             "r"(cols)
-                             : "memory");
-                asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-            }
-            if (tid == 0) {
-                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_mbar)) : "memory");
-                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            }
-            tc_fence_before();
-            __syncthreads();
-            tc_fence_after();
+            // round 0's MMAs go out now (their operands are in place); the
+            // rows' norms below are taken while they run
+            if (tid == 0) issue_mma();
         }
     }
     const ScreenConsts cst = TC && xinexact ? a.cst_loose : a.cst;
@@ -771,10 +807,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         // (round 0: loaded while the rows were in flight)
         if (r > 0) load_centroids(rr, r);
         const int KA = act[kCKMax];
-        if constexpr (TC) {
-            // round 0: the rows have landed by now (later rounds: issued inside load_centroids)
-            if (r == 0 && tid == 0) issue_mma();
-        }
+        // (tensor core: the round's MMAs were issued in the prologue / inside load_centroids)
         __syncthreads();
         if (KA == 0) {  // assign_nearest on all-degenerate centroids (core.cpp:115-118)
             if (tid == 0) ctl.state_error = 1;
@@ -1028,7 +1061,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             const int label = act[bj];
             if (r > 0 && label != mylab[i]) {
                 chg |= (1u << label) | (1u << mylab[i]);
-                oldlab[i] = mylab[i];
+                if constexpr (RED) oldlab[i] = mylab[i];
             }
             mylab[i] = label;
             lab[p] = label;
@@ -1037,8 +1070,10 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             mysum += best;
         }
         int nmoved = 0;
+        if constexpr (RED) {
 #pragma unroll
-        for (int i = 0; i < PPT; ++i) nmoved += oldlab[i] >= 0 ? 1 : 0;
+            for (int i = 0; i < PPT; ++i) nmoved += oldlab[i] >= 0 ? 1 : 0;
+        }
         __syncthreads();  // red / wsum reuse below
         // CTA sum of the distances (unordered: certified interval below)
 #pragma unroll
@@ -1052,7 +1087,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         if (lane == 0) {
             red[warp] = mysum;
             reinterpret_cast<unsigned*>(red + 32)[warp] = chg;
-            reinterpret_cast<int*>(red + 32)[32 + warp] = nmoved;
+            if constexpr (RED) reinterpret_cast<int*>(red + 32)[32 + warp] = nmoved;
         }
         __syncthreads();
         // labels whose membership changed in this tile (round 0: all of them);
@@ -1132,6 +1167,24 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             }
             __syncthreads();
             CDBG(rr, 12);
+            // this CTA's partial of (label j, dim d) / member count of label j: stored, and in
+            // red mode its change added to the round's delta buffer
+            auto emit_part = [&](int j, int d, double accv) {
+                double* pp = a.part + static_cast<size_t>(cta) * k * n + static_cast<size_t>(j) * n + d;
+                if (RED) {  // this thread wrote *pp in the earlier rounds
+                    const double dl = r > 0 ? __dsub_rn(accv, __ldcg(pp)) : accv;
+                    if (dl != 0.0) atomicAdd(dcur + j * n + d, dl);
+                }
+                *pp = accv;
+            };
+            auto emit_cnt = [&](int j, int members_j) {
+                unsigned* pc = a.pcnt + static_cast<size_t>(cta) * k + j;
+                if (RED) {
+                    const int dc = members_j - (r > 0 ? static_cast<int>(__ldcg(pc)) : 0);
+                    if (dc) atomicAdd(ccur + j, dc);
+                }
+                *pc = static_cast<unsigned>(members_j);
+            };
             // lane groups of LG lanes, one label per group, DPL dims per lane:
             // row[d] += x[d] over the label's members in index order
             // (core.cpp:206-214), member rows fetched 8 ahead of the adds
@@ -1187,23 +1240,9 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
 #pragma unroll
                 for (int t = 0; t < DPL; ++t) {
                     const int d = gl + LG * t;
-                    if (d < n) {
-                        double* pp = a.part + static_cast<size_t>(cta) * k * n + static_cast<size_t>(j) * n + d;
-                        if (RED) {  // this thread wrote *pp in the earlier rounds
-                            const double dl = r > 0 ? __dsub_rn(acc[t], __ldcg(pp)) : acc[t];
-                            if (dl != 0.0) atomicAdd(dcur + j * n + d, dl);
-                        }
-                        *pp = acc[t];
-                    }
+                    if (d < n) emit_part(j, d, acc[t]);
                 }
-                if (gl == 0) {
-                    unsigned* pc = a.pcnt + static_cast<size_t>(cta) * k + j;
-                    if (RED) {
-                        const int dc = (e - b) - (r > 0 ? static_cast<int>(__ldcg(pc)) : 0);
-                        if (dc) atomicAdd(ccur + j, dc);
-                    }
-                    *pc = static_cast<unsigned>(e - b);
-                }
+                if (gl == 0) emit_cnt(j, e - b);
             }
             CDBG(rr, 14);
         }
@@ -1356,7 +1395,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             a.rsum[zs] = 0.0;
             a.rchg[zs] = 0;
         }
-        if (RED) continue;  // the next round forms its centroids from the label sums
+        // (red mode: the next round forms its centroids from the label sums)
+        if constexpr (!RED) {
 
         CDBG(rr, 6);
         // ---- merge (core.cpp:217-242): this CTA's (label, dim) pairs, tile order ----
@@ -1393,6 +1433,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         CDBG(rr, 7);
         grid_sync(a.bar, G);  // ---------------- barrier B ----------------
         CDBG(rr, 8);
+        }
     }
 
     // every control read of this CTA is done: CTA 0 resets the round slots
@@ -1512,18 +1553,20 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     // (red mode: the trained centroids are this CTA's label sums / counts — C
     // and mask in global memory still hold the start)
     const bool own = RED && ctl.iterations >= 1;
+    const bool keep = RED && !accepted && start_is_inc;  // C, mask still hold the incumbent
+    const int* fcnt = scnt + (ctl.iterations & 1) * kCKMax;  // the counts behind the trained centroids
     for (int j = tid; j < k; j += NT) {
-        const uint8_t mv = !accepted ? __ldcg(a.maskinc + j) : own ? (scnt[j] > 0 ? 0 : 1) : __ldcg(a.mask + j);
+        const uint8_t mv = !accepted ? __ldcg(a.maskinc + j) : own ? (fcnt[j] > 0 ? 0 : 1) : __ldcg(a.mask + j);
         s_mk[j] = mv;
         if (accepted) a.maskinc[j] = mv;
-        if (!accepted || own) a.mask[j] = mv;
+        if ((!accepted || own) && !keep) a.mask[j] = mv;
     }
-    for (int e = tid; e < k * n; e += NT) {
+    for (int e = tid; e < k * n && !keep; e += NT) {
         if (accepted) {
             double v;
             if (own) {
                 const int j = e / n;
-                v = scnt[j] > 0 ? __dmul_rn(ssum[j * cdld + (e - j * n)], sinv[j]) : 0.0;  // core.cpp:231-242
+                v = fcnt[j] > 0 ? __dmul_rn(ssum[j * cdld + (e - j * n)], sinv[j]) : 0.0;  // core.cpp:231-242
                 a.C[e] = v;
             } else {
                 v = __ldcg(a.C + e);
@@ -1645,22 +1688,25 @@ float f_rd32(double x) {
     return f;
 }
 
-template <typename T, int ND, int PPT, bool TC>
+template <typename T, int ND, int PPT, bool TC, bool RED>
 void* kernel_ptr() {
-    return reinterpret_cast<void*>(&dev::k_chunk<T, ND, PPT, TC>);
+    return reinterpret_cast<void*>(&dev::k_chunk<T, ND, PPT, TC, RED>);
 }
 
 // (ND, PPT) instances: ND = padded width (multiple of 8); fp32 with the
 // tensor-core screen (tc) or the packed-FFMA screen, fp64 with the latter.
 struct Inst {
     int nd, ppt;
-    void* f32tc;
-    void* f32;
-    void* f64;
+    void* f32tc[2];  // [red]
+    void* f32[2];
+    void* f64[2];
 };
 
-#define BM_CHUNK_INST(ND, PPT)                                                                              \
-    {ND, PPT, kernel_ptr<float, ND, PPT, true>(), kernel_ptr<float, ND, PPT, false>(), kernel_ptr<double, ND, PPT, false>()}
+#define BM_CHUNK_INST(ND, PPT)                                                                      \
+    {ND, PPT,                                                                                       \
+     {kernel_ptr<float, ND, PPT, true, false>(), kernel_ptr<float, ND, PPT, true, true>()},        \
+     {kernel_ptr<float, ND, PPT, false, false>(), kernel_ptr<float, ND, PPT, false, true>()},      \
+     {kernel_ptr<double, ND, PPT, false, false>(), kernel_ptr<double, ND, PPT, false, true>()}}
 const std::vector<Inst>& instances() {
     static const std::vector<Inst> v = {
         BM_CHUNK_INST(8, 2),  BM_CHUNK_INST(16, 2), BM_CHUNK_INST(24, 2), BM_CHUNK_INST(32, 2),
@@ -1789,7 +1835,8 @@ void launch_chunk_fix(cudaStream_t st, const dev::FixArgs& f) {
 void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const dev::ChunkArgs& a0) {
     void* fn = nullptr;
     for (const Inst& i : instances())
-        if (i.nd == p.nd && i.ppt == p.ppt) fn = storage == BM_F64 ? i.f64 : p.tc ? i.f32tc : i.f32;
+        if (i.nd == p.nd && i.ppt == p.ppt)
+            fn = storage == BM_F64 ? i.f64[p.red ? 1 : 0] : p.tc ? i.f32tc[p.red ? 1 : 0] : i.f32[p.red ? 1 : 0];
     if (!fn) throw CudaError("chunk kernel: no instance");
     {
         // the attribute is a per-device maximum: raise it, never lower it

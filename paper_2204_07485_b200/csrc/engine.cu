@@ -1663,6 +1663,13 @@ bool chunk_red_enabled() {
     return on;
 }
 
+// BM_CHUNK_FIX=0: the chunk kernel folds its exact objective itself instead of
+// leaving it to k_chunk_fix on the side stream.
+bool chunk_fix_deferred() {
+    static const bool on = !(std::getenv("BM_CHUNK_FIX") && std::string(std::getenv("BM_CHUNK_FIX")) == "0");
+    return on;
+}
+
 bool graphs_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("BM_GRAPHS");
@@ -1988,7 +1995,9 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
             BM_CUDA(cudaEventRecord(w.ev_spec[i], st));
         }
-        const cudaStream_t pst = dc.pstream, pst2 = dc.pstream2;
+        // BM_PREP_STREAMS=1: every prep on one stream (A/B)
+        static const bool one_prep = std::getenv("BM_PREP_STREAMS") && std::string(std::getenv("BM_PREP_STREAMS")) == "1";
+        const cudaStream_t pst = dc.pstream, pst2 = one_prep ? dc.pstream : dc.pstream2;
         Points bufP[dev::kStateBufs] = {chunkP, chunkP, chunkP, chunkP};
         bufP[1].X = dc.chunk1.p;
         bufP[2].X = dc.chunk2.p;
@@ -2037,7 +2046,12 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
             if (w.sums_on && (c == 0 || !spec))  // no speculative begin zeroed this buffer's sums
                 BM_CUDA(cudaMemsetAsync(w.sums_of((int)(c % dev::kStateBufs)), 0, 2 * w.sum_half() * sizeof(long long),
                                         st));
-            BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i], 0));
+            // (the prep runs chunks ahead: when it has already finished, no wait is enqueued
+            // between the chunk kernels)
+            if (cudaEventQuery(w.ev_prep[i]) != cudaSuccess) {
+                (void)cudaGetLastError();
+                BM_CUDA(cudaStreamWaitEvent(st, w.ev_prep[i], 0));
+            }
             if (spec) BM_CUDA(cudaStreamWaitEvent(st, w.ev_spec[i], 0));
             cudaEvent_t e0 = tl_ev(st);
             if (persist) {
@@ -2092,14 +2106,15 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 a.timing_cap = w.ctiming.n / 2;
                 a.dbg = chunk_dbg_buffer();
                 a.dbg_mma = a.dbg && std::string(std::getenv("BM_CHUNK_DBG")) == "2";
-                static const bool defer = !(std::getenv("BM_CHUNK_FIX") && std::string(std::getenv("BM_CHUNK_FIX")) == "0");
+                const bool defer = chunk_fix_deferred();
                 a.job = defer ? w.cjob.p + i : nullptr;
                 a.fix_seq = defer ? w.cfix_seq.p : nullptr;
                 launch_chunk(st, cplan, d->dtype, a);
                 // its exact objective, folded on the side stream during the next chunk
                 if (defer) {
-                BM_CUDA(cudaEventRecord(w.ev_chunk[i], st));
-                BM_CUDA(cudaStreamWaitEvent(w.fix_stream, w.ev_chunk[i], 0));
+                // (one event per chunk kernel: the fix stream and the buffer's next prep both wait on ev_lloyd)
+                BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
+                BM_CUDA(cudaStreamWaitEvent(w.fix_stream, w.ev_lloyd[i], 0));
                 dev::FixArgs fa{};
                 fa.job = w.cjob.p + i;
                 fa.dists = a.dists;
@@ -2117,7 +2132,7 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 BM_CUDA(cudaGraphLaunch(w.g_lloyd[i], st));
             }
             if (timeline) tl.push_back({1, e0, tl_ev(st)});
-            BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
+            if (!(persist && chunk_fix_deferred())) BM_CUDA(cudaEventRecord(w.ev_lloyd[i], st));
         };
         auto draw = [&](uint64_t c) {  // chunk c's sample draws into target buffer c % 2
             if (c >= 2) BM_CUDA(cudaStreamWaitEvent(sw->rng_stream, sw->resolved[c & 1], 0));  // read by chunk c-2

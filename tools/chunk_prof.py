@@ -56,4 +56,7 @@ if os.environ.get("BM_CHUNK_DBG"):
         tail = buf[c, 7]
         print(f"  prologue {(buf[c,0,0]-tail[13])/1e3:.1f} us (rows landed at {(buf[c,0,13]-tail[13])/1e3:.1f}); max MMA dot error / (|x||c|) "
               f"{np.array([tail[14] & 0xFFFFFFFF], np.uint32).view(np.float32)[0]:.3g}")
-        print(f"  tail: loop-end @{(tail[9]-t0)/1e3:.1f} fold {(tail[10]-tail[9])/1e3:.1f} bar {(tail[11]-tail[10])/1e3:.1f} accept {(tail[12]-tail[11])/1e3:.1f}")
+        if tail[10] and tail[11]:
+            print(f"  tail: loop-end @{(tail[9]-t0)/1e3:.1f} fold {(tail[10]-tail[9])/1e3:.1f} bar {(tail[11]-tail[10])/1e3:.1f} accept {(tail[12]-tail[11])/1e3:.1f}")
+        else:
+            print(f"  tail: loop-end @{(tail[9]-t0)/1e3:.1f}, accept + record + next start {(tail[12]-tail[9])/1e3:.1f} (exact objective deferred)")
