@@ -138,6 +138,19 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G) {
     __syncthreads();
 }
 
+// One lane of the (converged) calling warp.
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xFFFFFFFF;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -352,7 +365,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     // packed-FFMA screen with the rows in registers (row-major shared rows)
     static_assert(!TC || sizeof(T) == 4, "the tensor-core screen reads fp32 rows");
     extern __shared__ __align__(16) unsigned char sm_raw[];
-    if (!__ldcg(&a.gs->go)) return;  // a chunk queued behind one that needs a repair: nothing to do
+    const unsigned long long t_entry = gtimer();
     const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
     const unsigned G = gridDim.x, cta = blockIdx.x;
     const int B = a.B, n = a.n, k = a.k, xld = a.xld;
@@ -389,12 +402,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     const double dinf = __longlong_as_double(0x7FF0000000000000LL);
     __shared__ unsigned long long s_chunk;
     // (no repair before this chunk: its start is the incumbent's copy — red mode leaves C / mask untouched)
-    const bool start_is_inc = __ldcg(&a.gs->inc_degenerate) == 0;
-    if (tid == 0) {
-        s_chunk = __ldcg(a.chunk_ctr);  // every CTA: stable until CTA 0's accept (after a grid barrier)
-        if (cta == 0 && a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = gtimer();
-    }
-    CDBG(7, 13);
+    bool start_is_inc = false;
     // 16-byte chunk q of row p (fp32: dims 4q..4q+3; fp64: 2q, 2q+1):
     // tc rows in the swizzled K-major layout, else row-major with stride xld
     auto xchunk = [&](int p, int q) -> unsigned char* {
@@ -433,10 +441,12 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
     };
 
-    // Tensor-core screen: one thread issues the tile MMAs and their commit:
-    // D[tile] = rows . (hi + lo)^T over K
+    // Tensor-core screen: a whole (converged) warp calls this, its elected lane
+    // issues the tile MMAs and their commit: D[tile] = rows . (hi + lo)^T over K
+    // (inside a one-thread branch the compiler wraps every MMA in an election loop)
     auto issue_mma = [&]() {
         tc_fence_after();
+        if (!elect_one()) return;
         // descriptors from their 14-bit start-address field (units of
         // 16 B); k-steps outer, tiles inner: consecutive MMAs feed
         // different accumulators
@@ -572,7 +582,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         // issues the MMAs while the other warps take the norms
         const bool split = TC && r > 0 && NW > 1;
         if constexpr (TC) {
-            if (r > 0 && tid == (NW > 1 ? (NW - 1) * 32 : 0)) issue_mma();
+            if (r > 0 && warp == (NW > 1 ? NW - 1 : 0)) issue_mma();
         }
         const int NWN = split ? NW - 1 : NW;
         for (int rk = warp; rk < KA && warp < NWN; rk += NWN) {
@@ -646,6 +656,32 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
         __syncthreads();
         if constexpr (TC) tc_fence_after();
+        // ---- Everything above is independent of the previous chunk kernel (under a
+        // programmatic dependent launch it overlaps that kernel's accept); from here
+        // on its results are read.  The three values its accept left, one L2 round trip:
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        const int go_ = __ldcg(&a.gs->go);
+        const int incdeg_ = __ldcg(&a.gs->inc_degenerate);
+        const unsigned long long chunk_ = __ldcg(a.chunk_ctr);
+        if (!go_) {  // a chunk queued behind one that needs a repair: nothing to do
+            mbar_wait(&s_xbar, 0);  // (no exit with the rows' copies in flight)
+            if constexpr (TC) {
+                tc_fence_before();
+                __syncthreads();
+                if (warp == 0) {
+                    tc_fence_after();
+                    const unsigned cols = umma::tmem_cols(static_cast<unsigned>(MP / 128) * 64);
+                    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(cols) : "memory");
+                }
+            }
+            return;
+        }
+        start_is_inc = incdeg_ == 0;
+        if (tid == 0) {
+            s_chunk = chunk_;  // every CTA: stable until CTA 0's accept (after a grid barrier)
+            if (cta == 0 && a.timing && s_chunk < a.timing_cap) a.timing[2 * s_chunk] = t_entry;
+        }
+        CDBG(7, 13);
         load_centroids(0, 0);
         mbar_wait(&s_xbar, 0);
         CDBG(0, 13);
@@ -703,7 +739,7 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
             fence_proxy_async_smem();
             // round 0's MMAs go out now (their operands are in place); the
             // rows' norms below are taken while they run
-            if (tid == 0) issue_mma();
+            if (warp == 0) issue_mma();
         }
     }
     const ScreenConsts cst = TC && xinexact ? a.cst_loose : a.cst;
@@ -1436,6 +1472,8 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
         }
     }
 
+    // (a dependent launch of the next chunk kernel may start its prologue on the SMs that free up)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // every control read of this CTA is done: CTA 0 resets the round slots
     // once all CTAs are here (bar[2])
     if (tid == 0 && cta != 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 2) : "memory");
@@ -1864,8 +1902,15 @@ void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const d
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     cfg.attrs = at;
-    static const bool coop = !(std::getenv("BM_CHUNK_COOP") && std::string(std::getenv("BM_CHUNK_COOP")) == "0");
-    cfg.numAttrs = coop ? 1 : 0;
+    // BM_CHUNK_PDL=1: plain launch with programmatic stream serialization (the next
+    // chunk kernel's prologue overlaps this one's accept); BM_CHUNK_COOP=0: plain launch
+    static const bool pdl = std::getenv("BM_CHUNK_PDL") && std::string(std::getenv("BM_CHUNK_PDL")) == "1";
+    static const bool coop = !pdl && !(std::getenv("BM_CHUNK_COOP") && std::string(std::getenv("BM_CHUNK_COOP")) == "0");
+    if (pdl) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+    }
+    cfg.numAttrs = coop || pdl ? 1 : 0;
     void* args[] = {&a};
     BM_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
 }

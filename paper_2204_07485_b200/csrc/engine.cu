@@ -2217,7 +2217,21 @@ void big_means(const bm_dataset* d, const bm_config& cfg, bm_outcome* out, bm_ch
                 launch_lloyd(chunk + queued);
                 ++queued;
             }
-            BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
+            {
+                // BM_HOSTPROF=1: how long the host waits for the device per chunk (0: the loop is host-bound)
+                static const bool hostprof = std::getenv("BM_HOSTPROF") != nullptr;
+                const auto tw = std::chrono::steady_clock::now();
+                BM_CUDA(cudaEventSynchronize(w.ev_lloyd[i6]));
+                if (hostprof) {
+                    static double waited = 0.0;
+                    static uint64_t nwait = 0;
+                    waited += seconds_since(tw);
+                    if (++nwait % 200 == 0) {
+                        std::fprintf(stderr, "[hostprof] %.1f us waiting on the device per chunk (last 200)\n", waited / 200 * 1e6);
+                        waited = 0.0;
+                    }
+                }
+            }
             if (w.h_status.p[b].incomplete) {  // more rounds than the graph unrolls
                 BM_CUDA(cudaGraphLaunch(w.g_cont[i6], st));
                 BM_CUDA(cudaEventRecord(w.ev_lloyd[i6], st));
