@@ -1284,8 +1284,13 @@ void launch_dist_rows(cudaStream_t st, const Points& P, const uint32_t* cand, in
     const dim3 grid((unsigned)ceil_div(P.rows, 128), (unsigned)std::max(1, ncand));
     dispatch(P.dtype, [&](auto tag) {
         using T = decltype(tag);
-        launch_pdl(dev::k_dist_rows<T>, grid, 128, 0, st, static_cast<const T*>(P.X), P.rows, P.n, P.ld, cand,
-                   ncand, d2, out, skip);
+        static const bool narrow = !(std::getenv("BM_DIST_NARROW") && std::string(std::getenv("BM_DIST_NARROW")) == "0");
+        if (narrow && P.n <= dev::kDistRowsN && ncand >= 1 && ncand <= 4)  // narrow rows: every candidate in one thread
+            launch_pdl(dev::k_dist_rows_narrow<T>, dim3(grid.x), 128, 0, st, static_cast<const T*>(P.X), P.rows, P.n,
+                       P.ld, cand, ncand, d2, out, skip);
+        else
+            launch_pdl(dev::k_dist_rows<T>, grid, 128, 0, st, static_cast<const T*>(P.X), P.rows, P.n, P.ld, cand,
+                       ncand, d2, out, skip);
     });
     BM_LAUNCH();
     count_launch();

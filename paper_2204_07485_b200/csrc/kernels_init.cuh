@@ -33,6 +33,53 @@ __global__ void k_dist_rows(const T* __restrict__ X, uint64_t rows, int n, uint6
     }
 }
 
+// The same for narrow rows (n <= kDistRowsN) and up to 4 candidates: one thread
+// per row takes every candidate at once — the row is read once in 16-byte
+// vectors and converted once, the candidate rows sit in shared memory as fp64
+// (one conversion each), the chains of the candidates run side by side.  Every
+// (row, candidate) chain is the same ascending-d fold as above.
+constexpr int kDistRowsN = 128;
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_dist_rows_narrow(const T* __restrict__ X, uint64_t rows, int n, uint64_t ld, const uint32_t* __restrict__ cand,
+                   int ncand, const double* __restrict__ d2, double* __restrict__ out, const int* skip) {
+    pdl_wait();  // (programmatic dependent launch: the previous kernel's writes)
+    if (skip && (skip[0] || skip[1])) return;  // device K-means++ step: fallback or direct pick
+    __shared__ __align__(16) double rs[4][kDistRowsN];
+    for (int e = threadIdx.x; e < ncand * n; e += blockDim.x) {
+        const int c = e / n, d = e - c * n;
+        rs[c][d] = to_f64(X[static_cast<uint64_t>(cand[c]) * ld + d]);
+    }
+    __syncthreads();
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    constexpr int EPC = 16 / static_cast<int>(sizeof(T));  // elements per 16-byte vector (ld is a multiple)
+    const T* x = X + i * ld;
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int d0 = 0; d0 < n; d0 += EPC) {
+        T v[EPC];
+        *reinterpret_cast<uint4*>(v) = *reinterpret_cast<const uint4*>(x + d0);
+#pragma unroll
+        for (int u = 0; u < EPC; ++u) {
+            const int d = d0 + u;
+            if (d < n) {
+                const double xd = to_f64(v[u]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (c < ncand) sum[c] = dist_step(sum[c], xd, rs[c][d]);
+            }
+        }
+    }
+    const double o = d2 ? d2[i] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        if (c < ncand) {
+            double v = sum[c];
+            if (d2 && o < v) v = o;
+            out[static_cast<uint64_t>(c) * rows + i] = v;
+        }
+}
+
 // ---------------------------------------------------------------------------
 // Device K-means++ step (init.cpp:171-199) for integer D^2 weights.
 // prefix_sums (init.cpp:81-88) is a sequential fp64 fold; when every weight is
