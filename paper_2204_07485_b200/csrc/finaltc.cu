@@ -45,7 +45,7 @@ __host__ __device__ inline size_t ft_smem_bytes(int nka, int n) {
 }
 
 template <int NKA>
-__global__ void __launch_bounds__(kFT + 64, 1) k_final_tc(const __grid_constant__ FinalTcArgs a) {
+__global__ void __launch_bounds__(2 * kFT + 64, 1) k_final_tc(const __grid_constant__ FinalTcArgs a) {
     extern __shared__ __align__(16) unsigned char fsm_raw[];
     __shared__ __align__(8) unsigned long long s_full[kFS], s_empty[kFS], s_done[2], s_free[2];
     __shared__ unsigned s_tmem;
@@ -54,6 +54,10 @@ __global__ void __launch_bounds__(kFT + 64, 1) k_final_tc(const __grid_constant_
     pdl_wait();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool producer = tid == kFT, mma_thread = tid == kFT + 32;  // warps 4 and 5
+    // two epilogue groups (warps 0-3 and 6-9): group g takes this CTA's tiles li = g, g + 2, ...
+    // (accumulator li & 1 = g), so one tile's exact recheck runs beside the next tile's
+    const int eg = warp < 4 ? 0 : warp >= 6 ? 1 : -1;
+    const int row = 32 * (warp & 3) + lane;  // this thread's tile row = its TMEM lane (lane quarter warp % 4)
     const int n = a.n, cdld = ft_cdld(n);
     const uint64_t ntiles = (a.rows + 127) / 128;
     const uint64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // tiles of this CTA
@@ -151,19 +155,19 @@ __global__ void __launch_bounds__(kFT + 64, 1) k_final_tc(const __grid_constant_
         }
     } else if (mma_thread) {
         for (uint64_t li = 0; li < my; ++li) issue(li);
-    } else if (tid < kFT) {
+    } else if (eg >= 0) {
         const float finf = __int_as_float(0x7F800000);
         const double dinf = __longlong_as_double(0x7FF0000000000000LL);
-        for (uint64_t li = 0; li < my; ++li) {
+        for (uint64_t li = static_cast<uint64_t>(eg); li < my; li += 2) {
             const int s = static_cast<int>(li % kFS), acc = static_cast<int>(li & 1);
             const uint64_t tile = blockIdx.x + li * gridDim.x;
-            const uint64_t gp = tile * 128 + tid;
+            const uint64_t gp = tile * 128 + row;
             umma::mbar_wait_parity(&s_done[acc], static_cast<unsigned>((li / 2) & 1));
             __syncwarp();  // (tcgen05.ld is warp-aligned)
             umma::fence_after();
             float Lv[32];
             {
-                const unsigned ta = tbase + (static_cast<unsigned>(32 * warp) << 16) + 64u * acc;
+                const unsigned ta = tbase + (static_cast<unsigned>(32 * (warp & 3)) << 16) + 64u * acc;
                 float Lw[32];
                 umma::tmem_ld32(ta, Lv);
                 umma::tmem_ld32(ta + 32u, Lw);
@@ -172,8 +176,8 @@ __global__ void __launch_bounds__(kFT + 64, 1) k_final_tc(const __grid_constant_
             }
             umma::fence_before();
             mbar_arrive_ft(&s_free[acc]);  // this thread's TMEM reads of the accumulator are done
-            const unsigned char* rowb = stg + static_cast<size_t>(s) * kTile + static_cast<size_t>(tid) * 128;
-            const int sw = tid & 7;
+            const unsigned char* rowb = stg + static_cast<size_t>(s) * kTile + static_cast<size_t>(row) * 128;
+            const int sw = row & 7;
             if (gp < a.rows) {
                 // this row's squared norm (rounded down / up), from the staged row
                 float xl = 0.f, xh = 0.f;
@@ -280,7 +284,7 @@ void launch_final_tc(cudaStream_t st, int device, const dev::FinalTcArgs& a, boo
     const uint64_t ntiles = (a.rows + 127) / 128;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(ntiles < static_cast<uint64_t>(sms) ? ntiles : sms));
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(2 * 128 + 64);  // two epilogue groups + the producer and MMA warps
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
