@@ -366,7 +366,10 @@ __global__ void __launch_bounds__(kCMaxT, 1) k_chunk(const __grid_constant__ Chu
     static_assert(!TC || sizeof(T) == 4, "the tensor-core screen reads fp32 rows");
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const unsigned long long t_entry = gtimer();
-    const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+    // (a.threads < blockDim.x: the launch is padded with warps that leave at once — their
+    // registers stay allocated, so no side kernel's CTA fits beside this one; BM_CHUNK_OWN_SM=1)
+    if (static_cast<int>(threadIdx.x) >= a.threads) return;
+    const int tid = threadIdx.x, NT = a.threads, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
     const unsigned G = gridDim.x, cta = blockIdx.x;
     const int B = a.B, n = a.n, k = a.k, xld = a.xld;
     const uint64_t p0 = static_cast<uint64_t>(cta) * B;
@@ -1918,7 +1921,9 @@ void launch_chunk(cudaStream_t st, const ChunkPlan& p, bm_dtype storage, const d
     a.red = p.red;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3(p.threads);
+    static const bool own_sm = std::getenv("BM_CHUNK_OWN_SM") && std::string(std::getenv("BM_CHUNK_OWN_SM")) == "1";
+    a.threads = p.threads;
+    cfg.blockDim = dim3(own_sm ? dev::kCMaxT : p.threads);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];

@@ -42,6 +42,7 @@ struct ChunkArgs {
     int n;
     uint64_t ld;              // global row stride (elements)
     int k;
+    int threads;              // working threads per CTA (the launch may be padded beyond them)
     int B;                    // points per CTA (ordered mode: 1024 = one reduction tile)
     int xld;                  // shared-memory row stride (elements)
     int ordered;              // 1: real-valued data, CTA = 1024-tile, tile-order merge; 0: exact sums
